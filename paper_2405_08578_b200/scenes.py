@@ -1,0 +1,116 @@
+"""Seeded synthetic scenes for the five BASELINE configurations.
+
+Benchmark/test infrastructure, not part of the hot path.  The reference
+ships no generator for the BASELINE "blurred noise + filled shapes" scenes
+(its own ``synthetic.make_texture`` at
+reference ``pkg/src/peakstitch/synthetic.py:21-36`` is a different texture),
+so the parameters below are pinned here and every generated array is
+identified by the SHA-256 of its bytes (``scene_digest``).
+
+Parameters:
+  1. white noise U[0, 255) float64 from ``default_rng(seed)``;
+  2. separable Gaussian blur, sigma 3, radius 12, mirror ("reflect") borders;
+  3. min-max stretch to [0, 255];
+  4. ``round(200 * H * W / 2048**2)`` filled shapes painted in order, each a
+     rectangle or a disk with probability 1/2: rectangle sides U[8, 256]*s,
+     disk radius U[4, 128]*s, s = sqrt(H*W)/2048, centre uniform over the
+     image, integer intensity U{0..255};
+  5. rint, clip to [0, 255], uint8.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+
+import numpy as np
+
+SIGMA = 3.0
+RADIUS = 12
+SHAPES_AT_2048 = 200
+
+
+def _gauss_taps() -> np.ndarray:
+    x = np.arange(-RADIUS, RADIUS + 1, dtype=np.float64)
+    k = np.exp(-(x * x) / (2.0 * SIGMA * SIGMA))
+    return k / k.sum()
+
+
+def _blur_axis(a: np.ndarray, axis: int) -> np.ndarray:
+    # scipy's C correlate1d (half-sample mirror borders); pinned by the digests
+    # in tests/golden/scene_digests.json
+    from scipy.ndimage import correlate1d
+
+    return correlate1d(a, _gauss_taps(), axis=axis, mode="reflect")
+
+
+def scene(h: int, w: int, seed: int = 0) -> np.ndarray:
+    """(h, w) uint8 noise+shapes scene, deterministic in (h, w, seed)."""
+    rng = np.random.default_rng(seed)
+    f = rng.uniform(0.0, 255.0, size=(h, w))
+    f = _blur_axis(_blur_axis(f, 0), 1)
+    lo, hi = float(f.min()), float(f.max())
+    f = (f - lo) * (255.0 / (hi - lo))
+    s = math.sqrt(h * w) / 2048.0
+    n_shapes = int(round(SHAPES_AT_2048 * h * w / 2048.0**2))
+    for _ in range(n_shapes):
+        kind = rng.integers(0, 2)
+        cy = rng.uniform(0, h)
+        cx = rng.uniform(0, w)
+        val = float(rng.integers(0, 256))
+        if kind == 0:
+            sh = rng.uniform(8, 256) * s
+            sw = rng.uniform(8, 256) * s
+            r0, r1 = int(max(0, round(cy - sh / 2))), int(min(h, round(cy + sh / 2)))
+            c0, c1 = int(max(0, round(cx - sw / 2))), int(min(w, round(cx + sw / 2)))
+            f[r0:r1, c0:c1] = val
+        else:
+            rad = rng.uniform(4, 128) * s
+            r0, r1 = int(max(0, math.floor(cy - rad))), int(min(h, math.ceil(cy + rad) + 1))
+            c0, c1 = int(max(0, math.floor(cx - rad))), int(min(w, math.ceil(cx + rad) + 1))
+            if r1 <= r0 or c1 <= c0:
+                continue
+            yy = np.arange(r0, r1, dtype=np.float64)[:, None] - cy
+            xx = np.arange(c0, c1, dtype=np.float64)[None, :] - cx
+            m = yy * yy + xx * xx <= rad * rad
+            f[r0:r1, c0:c1][m] = val
+    return np.clip(np.rint(f), 0, 255).astype(np.uint8)
+
+
+def scene_digest(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+# ---- per-config inputs -----------------------------
+
+def config1_pair(seed: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """C1: two 768x1024 crops of scene(2048, 2048), 40% overlap, integer shift."""
+    s = scene(2048, 2048, seed)
+    return s[640:1408, 0:1024].copy(), s[640:1408, 614:1638].copy()
+
+
+def _scene_job(args):
+    return scene(*args)
+
+
+def config2_batch(n: int = 64, h: int = 1600, w: int = 2688, seed0: int = 0,
+                  workers: int = 0) -> np.ndarray:
+    """C2: n independent scenes, image k seeded with seed0 + k; (n, h, w) uint8."""
+    out = np.empty((n, h, w), dtype=np.uint8)
+    jobs = [(h, w, seed0 + k) for k in range(n)]
+    if workers > 1 and n > 1:
+        import multiprocessing as mp
+
+        with mp.get_context("fork").Pool(workers) as pool:
+            for k, img in enumerate(pool.imap(_scene_job, jobs)):
+                out[k] = img
+    else:
+        for k, job in enumerate(jobs):
+            out[k] = scene(*job)
+    return out
+
+
+def config4_pair(seed: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """C4: two 8192x8192 crops of scene(8192, 12288) with 50% overlap."""
+    s = scene(8192, 12288, seed)
+    return s[:, 0:8192].copy(), s[:, 4096:12288].copy()

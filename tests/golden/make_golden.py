@@ -1,0 +1,338 @@
+"""Generate the golden fixtures by running the REAL reference package.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+The reference (pure Python, numpy) is imported read-only from
+``/root/reference/pkg/src``.  Its outputs on seeded inputs are written to
+``tests/golden/*.npz``; ``tests/test_oracle_golden.py`` pins the oracle to
+them and the GPU parity tests compare the CUDA path with them.  Nothing at
+test / bench time on the GPU box reads /root/reference.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.dont_write_bytecode = True
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+from peakstitch import descriptor as R_desc  # noqa: E402
+from peakstitch import detector as R_det  # noqa: E402
+from peakstitch import imaging as R_img  # noqa: E402
+from peakstitch import matcher as R_match  # noqa: E402
+from peakstitch import registration as R_reg  # noqa: E402
+from peakstitch.errors import RegistrationError  # noqa: E402
+
+from paper_2405_08578_b200 import scenes  # noqa: E402
+
+POL = {"max": 0, "min": 1}
+
+
+def kp_arrays(feats):
+    return dict(
+        row=np.array([f.row for f in feats], np.int64),
+        col=np.array([f.col for f in feats], np.int64),
+        scale=np.array([f.scale for f in feats], np.int64),
+        pol=np.array([POL[f.polarity] for f in feats], np.int8),
+        window=np.array([f.window_index for f in feats], np.int64),
+        value=np.array([f.value for f in feats], np.float64),
+    )
+
+
+def save(name, **arrays):
+    np.savez_compressed(os.path.join(HERE, name), **arrays)
+
+
+# --------------------------------------------------------------------------
+# detector cases: (label, pixels, alpha, scales, dedupe)
+# --------------------------------------------------------------------------
+
+def detector_cases():
+    rng = np.random.default_rng(20240514)
+    cases = []
+    # uint8 tie-heavy content with the pipeline's default alpha
+    for k, (nr, nc) in enumerate([(64, 64), (70, 83), (96, 64), (130, 150), (33, 41)]):
+        px = rng.integers(0, 4, size=(nr, nc)).astype(np.float64) * 60.0
+        for scales in [(8, 16, 32), (8, 9, 33) if min(nr, nc) >= 33 else (8, 9), (16, 32), (32,)]:
+            if max(scales) > min(nr, nc):
+                continue
+            for dd in (True, False):
+                cases.append((f"tie{k}_{'_'.join(map(str, scales))}_{int(dd)}", px, None, scales, dd))
+    # float uniform (reference tests' style, alpha 1e-5 / 1e-6)
+    for k, (nr, nc) in enumerate([(64, 64), (48, 80), (50, 83), (400, 602)]):
+        px = rng.uniform(0, 255, size=(nr, nc))
+        scales = (16, 32) if nr < 400 else (32, 40)
+        cases.append((f"flt{k}", px, 1e-5, scales, True))
+    # noise+shapes scene crops, uint8, default alpha; includes (32, 40) and (8,9,128)
+    s = scenes.scene(512, 512, 7).astype(np.float64)
+    cases.append(("scene_32_40", s[:300, :400], None, (32, 40), True))
+    cases.append(("scene_8_9_128", s[:256, :256], None, (8, 9, 128), True))
+    cases.append(("scene_16_64_raw", s[:200, :333], None, (16, 32, 64), False))
+    cases.append(("constant", np.full((64, 64), 7.0), 1e-5, (32,), True))
+    return cases
+
+
+def make_detector():
+    out = {}
+    meta = []
+    for label, px, alpha, scales, dd in detector_cases():
+        nr, nc = px.shape
+        a = R_img.default_alpha(nr, nc) if alpha is None else alpha
+        rimg = R_img.apply_linear_ramp(R_img.IntensityImage(px, label), a)
+        feats = R_det.detect_features(rimg, R_det.ScaleSet(tuple(scales)), dedupe=dd)
+        arr = kp_arrays(feats)
+        out[f"{label}__pixels"] = px.astype(np.uint8) if np.all(px == np.rint(px)) and px.max() < 256 else px
+        for k, v in arr.items():
+            out[f"{label}__{k}"] = v
+        meta.append(dict(label=label, alpha=a, scales=list(scales), dedupe=dd, shape=[nr, nc]))
+    out["meta"] = np.array(json.dumps(meta))
+    save("detector.npz", **out)
+    print("detector cases", len(meta))
+
+
+# --------------------------------------------------------------------------
+# descriptor cases
+# --------------------------------------------------------------------------
+
+def make_descriptor():
+    rng = np.random.default_rng(303)
+    recs = dict(img_id=[], row=[], col=[], scale=[], beta0=[], d=[], l_max=[], orient=[], desc=[])
+    images = []
+    # (a) reference-test style random float images with no ramp
+    for t in range(24):
+        nr, nc = int(rng.integers(40, 90)), int(rng.integers(40, 90))
+        images.append((rng.uniform(0, 255, size=(nr, nc)), None))
+    # (b) ramped uint8 scene crops (flat regions + ramp)
+    s = scenes.scene(512, 512, 11)
+    for t in range(4):
+        r0, c0 = int(rng.integers(0, 200)), int(rng.integers(0, 200))
+        crop = s[r0:r0 + 200, c0:c0 + 260].astype(np.float64)
+        images.append((crop, R_img.default_alpha(*crop.shape)))
+    img_store = {}
+    for iid, (px, alpha) in enumerate(images):
+        if alpha is None:
+            rimg = R_img.RampedImage(px, 1e-9, "t")
+            img_store[f"img{iid}"] = px
+        else:
+            rimg = R_img.apply_linear_ramp(R_img.IntensityImage(px, "t"), alpha)
+            img_store[f"img{iid}"] = px.astype(np.uint8)
+            img_store[f"alpha{iid}"] = np.float64(alpha)
+        nr, nc = px.shape
+        n_kp = 6 if alpha is None else 40
+        for _ in range(n_kp):
+            row, col = int(rng.integers(0, nr)), int(rng.integers(0, nc))
+            if alpha is None:
+                cfg = R_desc.DescriptorConfig(beta0=0.0625, d=4, l_max=64,
+                                              orientation_normalize=bool(rng.integers(0, 2)))
+                scale = int(rng.choice([16, 32, 64]))
+            else:
+                cfg = R_desc.DescriptorConfig(beta0=0.0625, d=4, l_max=128, orientation_normalize=True)
+                scale = int(rng.choice([8, 16, 32, 64, 128]))
+            fp = R_det.FeaturePoint(row, col, scale, "max", 0, 0.0)
+            v = R_desc.compute_descriptor(rimg, fp, cfg).values
+            for k, val in (("img_id", iid), ("row", row), ("col", col), ("scale", scale),
+                           ("beta0", cfg.beta0), ("d", cfg.d), ("l_max", cfg.l_max),
+                           ("orient", cfg.orientation_normalize), ("desc", v)):
+                recs[k].append(val)
+    out = {k: np.array(v) for k, v in recs.items()}
+    out.update(img_store)
+    save("descriptor.npz", **out)
+    print("descriptor cases", len(recs["row"]))
+
+
+# --------------------------------------------------------------------------
+# matcher cases
+# --------------------------------------------------------------------------
+
+def described(desc):
+    feats = [R_det.FeaturePoint(i, 0, 16, "max", 0, 0.0) for i in range(len(desc))]
+    return R_desc.DescribedFeatures("m", feats, np.asarray(desc, np.float64))
+
+
+def make_matcher():
+    rng = np.random.default_rng(77)
+    out = {}
+    cases = []
+    # random unit-ish descriptors with planted near-copies and exact clusters
+    for k, (n1, n2) in enumerate([(40, 55), (300, 280), (700, 650), (1, 1), (0, 5)]):
+        A = rng.random((n1, 128)).astype(np.float32).astype(np.float64)
+        A /= np.linalg.norm(A, axis=1, keepdims=True) + 1e-30
+        A = A.astype(np.float32).astype(np.float64)
+        B = rng.random((n2, 128)).astype(np.float32).astype(np.float64)
+        if n1 and n2:
+            m = min(n1, n2) // 2
+            B[:m] = (A[:m] + rng.normal(0, 0.01, (m, 128))).astype(np.float32)
+            if n1 > 10 and n2 > 10:
+                B[m:m + 4] = A[0]  # exact duplicates of one row -> column ties
+                A[5] = A[6]  # identical rows -> row ties
+        cases.append((f"rand{k}", A, B))
+    # real descriptors from the reference (saturated clusters, F6)
+    s = scenes.scene(512, 512, 5).astype(np.float64)
+    a, b = s[100:356, 0:300], s[100:356, 180:480]
+    cfg = R_desc.DescriptorConfig(beta0=0.0625, d=4, l_max=64)
+    sets = []
+    for px in (a, b):
+        r = R_img.apply_linear_ramp(R_img.IntensityImage(px, "x"), R_img.default_alpha(*px.shape))
+        f = R_det.detect_features(r, R_det.ScaleSet((16, 32, 64)))
+        sets.append(R_desc.describe_features(r, f, cfg).descriptors.astype(np.float32).astype(np.float64))
+    cases.append(("scene", sets[0], sets[1]))
+    meta = []
+    for label, A, B in cases:
+        out[f"{label}__A"] = A.astype(np.float32)
+        out[f"{label}__B"] = B.astype(np.float32)
+        for strat, ds in (("nearest_neighbor", 0.35), ("nearest_neighbor", 1.2), ("threshold_all", 0.35)):
+            if strat == "threshold_all" and len(A) * len(B) > 100000:
+                ds = 0.25
+            pairs = R_match.match_features(described(A), described(B), R_match.MatcherConfig(ds, strat))
+            tag = f"{label}__{strat}__{ds}"
+            out[f"{tag}__ref1"] = np.array([p.ref1 for p in pairs], np.int64)
+            out[f"{tag}__ref2"] = np.array([p.ref2 for p in pairs], np.int64)
+            out[f"{tag}__delta"] = np.array([p.delta for p in pairs], np.float64)
+            meta.append(dict(label=label, strategy=strat, delta_s=ds, tag=tag, n=len(pairs)))
+    out["meta"] = np.array(json.dumps(meta))
+    save("matcher.npz", **out)
+    print("matcher cases", len(meta))
+
+
+# --------------------------------------------------------------------------
+# RANSAC / rigid estimation cases, plus the scalar-call sample stream
+# --------------------------------------------------------------------------
+
+def pairs_from_xy(src, dst):
+    return [R_match.MatchPair((float(sy), float(sx)), (float(dy), float(dx)), 0.0, i, i)
+            for i, ((sx, sy), (dx, dy)) in enumerate(zip(src, dst))]
+
+
+def make_ransac():
+    rng = np.random.default_rng(99)
+    out = {}
+    meta = []
+    cases = []
+    for k in range(10):
+        th = float(rng.uniform(-0.4, 0.4)) if k % 3 else 0.0
+        truth = R_reg.RigidTransform(th, float(rng.uniform(-60, 60)), float(rng.uniform(-60, 60)))
+        n_in, n_out = int(rng.integers(8, 300)), int(rng.integers(0, 200))
+        src_in = rng.integers(0, 800, size=(n_in, 2)).astype(np.float64)  # integer pixel coords
+        dst_in = truth.transform_points(src_in)
+        if k % 2:
+            dst_in = np.rint(dst_in)
+        src = np.vstack([src_in, rng.integers(0, 800, size=(n_out, 2))]).astype(np.float64)
+        dst = np.vstack([dst_in, rng.integers(0, 800, size=(n_out, 2))]).astype(np.float64)
+        perm = rng.permutation(len(src))
+        cases.append((f"syn{k}", src[perm], dst[perm], dict(iterations=int(rng.choice([200, 1000, 2000])),
+                                                           inlier_tol=3.0, min_inliers=8, seed=int(k * 7 + 1))))
+    # pure noise -> RegistrationError
+    cases.append(("noise", rng.uniform(0, 400, (30, 2)), rng.uniform(0, 400, (30, 2)),
+                  dict(iterations=500, inlier_tol=1.0, min_inliers=8, seed=2)))
+    # too few pairs
+    cases.append(("few", np.arange(10.0).reshape(5, 2), np.arange(10.0).reshape(5, 2) + 1,
+                  dict(iterations=100, inlier_tol=3.0, min_inliers=8, seed=0)))
+    # degenerate-heavy: many coincident source points
+    src = np.repeat(np.array([[5.0, 5.0], [100.0, 40.0]]), 20, axis=0)
+    cases.append(("degenerate", src, src + np.array([3.0, -2.0]),
+                  dict(iterations=300, inlier_tol=3.0, min_inliers=8, seed=4)))
+    for label, src, dst, cfgd in cases:
+        cfg = R_reg.RansacConfig(**cfgd)
+        try:
+            res = R_reg.ransac_rigid(pairs_from_xy(src, dst), cfg)
+            ok = True
+            model = np.array([res.transform.theta, res.transform.t_x, res.transform.t_y])
+            inl = np.array(res.inliers, np.int64)
+            rms, cons = res.residual_rms, res.consensus_size
+        except RegistrationError:
+            ok, model, inl, rms, cons = False, np.zeros(3), np.zeros(0, np.int64), 0.0, 0
+        out[f"{label}__src"], out[f"{label}__dst"] = src, dst
+        out[f"{label}__model"], out[f"{label}__inliers"] = model, inl
+        out[f"{label}__rms"], out[f"{label}__consensus"], out[f"{label}__ok"] = rms, cons, ok
+        meta.append(dict(label=label, **cfgd))
+    # estimate_rigid KATs on random point sets (refit path: column means, pairwise sums)
+    est = []
+    for k in range(20):
+        m = int(rng.integers(2, 400))
+        s_ = rng.integers(0, 1000, size=(m, 2)).astype(np.float64)
+        d_ = s_ @ np.array([[0.9, -0.3], [0.3, 0.9]]) + rng.normal(0, 2, (m, 2))
+        t = R_reg.estimate_rigid(s_, d_)
+        out[f"est{k}__src"], out[f"est{k}__dst"] = s_, d_
+        out[f"est{k}__model"] = np.array([t.theta, t.t_x, t.t_y])
+        est.append(k)
+    # scalar-call sample streams (registration.py:164, 170-173)
+    streams = []
+    for seed in (0, 1, 11, 99, 12345, 2**40 + 3):
+        for n in (2, 3, 17, 1242, 50000):
+            r = np.random.default_rng(seed)
+            v = []
+            for _ in range(300):
+                i = int(r.integers(0, n))
+                j = int(r.integers(0, n - 1))
+                if j >= i:
+                    j += 1
+                v.append((i, j))
+            out[f"stream_{seed}_{n}"] = np.array(v, np.int64)
+            streams.append([seed, n])
+    out["meta"] = np.array(json.dumps(dict(cases=meta, est=est, streams=streams)))
+    save("ransac.npz", **out)
+    print("ransac cases", len(meta))
+
+
+# --------------------------------------------------------------------------
+# end-to-end small pair through the whole reference chain
+# --------------------------------------------------------------------------
+
+def make_e2e():
+    s = scenes.scene(640, 640, 3)
+    a, b = s[100:484, 0:400], s[100:484, 180:580]  # 384x400 crops, integer shift
+    out = dict(a=a, b=b)
+    cfg = R_desc.DescriptorConfig(beta0=0.0625, d=4, l_max=64)
+    described_sets = []
+    for tag, px in (("a", a), ("b", b)):
+        pxf = px.astype(np.float64)
+        r = R_img.apply_linear_ramp(R_img.IntensityImage(pxf, tag), R_img.default_alpha(*px.shape))
+        feats = R_det.detect_features(r, R_det.ScaleSet((16, 32, 64)))
+        ds = R_desc.describe_features(r, feats, cfg)
+        for k, v in kp_arrays(feats).items():
+            out[f"{tag}__{k}"] = v
+        out[f"{tag}__desc"] = ds.descriptors
+        described_sets.append(ds)
+    # P3 convention: match on the fp32-rounded descriptors
+    d32 = [R_desc.DescribedFeatures(x.image_id, x.features, x.descriptors.astype(np.float32).astype(np.float64))
+           for x in described_sets]
+    pairs = R_match.match_features(d32[0], d32[1], R_match.MatcherConfig())
+    out["m__ref1"] = np.array([p.ref1 for p in pairs], np.int64)
+    out["m__ref2"] = np.array([p.ref2 for p in pairs], np.int64)
+    out["m__delta"] = np.array([p.delta for p in pairs])
+    res = R_reg.ransac_rigid(pairs, R_reg.RansacConfig(iterations=1000, inlier_tol=3.0, min_inliers=8, seed=0))
+    out["r__model"] = np.array([res.transform.theta, res.transform.t_x, res.transform.t_y])
+    out["r__inliers"] = np.array(res.inliers, np.int64)
+    out["r__rms"], out["r__consensus"] = res.residual_rms, res.consensus_size
+    save("e2e.npz", **out)
+    print("e2e matches", len(pairs), "inliers", len(res.inliers))
+
+
+def make_scene_digests():
+    d = {}
+    for (h, w, seed) in [(64, 96, 0), (256, 256, 1), (512, 512, 7), (1600, 2688, 0), (2048, 2048, 0)]:
+        d[f"{h}x{w}_seed{seed}"] = scenes.scene_digest(scenes.scene(h, w, seed))
+    with open(os.path.join(HERE, "scene_digests.json"), "w") as f:
+        json.dump(d, f, indent=1)
+
+
+if __name__ == "__main__":
+    t = time.time()
+    what = sys.argv[1:] or ["detector", "descriptor", "matcher", "ransac", "e2e", "digests"]
+    for w in what:
+        {"detector": make_detector, "descriptor": make_descriptor, "matcher": make_matcher,
+         "ransac": make_ransac, "e2e": make_e2e, "digests": make_scene_digests}[w]()
+    env = dict(numpy=np.__version__, python=sys.version.split()[0])
+    with open(os.path.join(HERE, "ENV.json"), "w") as f:
+        json.dump(env, f)
+    print("done in %.1fs" % (time.time() - t))

@@ -1,0 +1,130 @@
+"""Pin the CPU oracle (oracle/lpsift_oracle.py) to the reference's own outputs.
+
+The fixtures in tests/golden/ were produced by running the real reference
+package (tests/golden/make_golden.py).  The oracle must reproduce them
+bit-exactly (keypoints, matches, inlier sets, sample streams) and to 1e-12
+for descriptors (same numpy kernels, same summation orders).
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from oracle import lpsift_oracle as O
+
+KP_FIELDS = ("row", "col", "scale", "pol", "window", "value")
+
+
+def detector_meta(golden):
+    g = golden("detector.npz")
+    return g, json.loads(str(g["meta"]))
+
+
+def test_oracle_detector_matches_reference(golden):
+    g, meta = detector_meta(golden)
+    for m in meta:
+        lab = m["label"]
+        px = g[f"{lab}__pixels"].astype(np.float64)
+        P = O.ramp(px, m["alpha"])
+        kp = O.detect(P, m["scales"], m["dedupe"])
+        for f in KP_FIELDS:
+            assert np.array_equal(kp[f], g[f"{lab}__{f}"]), (lab, f)
+
+
+def test_oracle_descriptor_matches_reference(golden):
+    g = golden("descriptor.npz")
+    worst = 0.0
+    for i in range(len(g["row"])):
+        iid = int(g["img_id"][i])
+        px = g[f"img{iid}"].astype(np.float64)
+        if f"alpha{iid}" in g.files:
+            P = O.ramp(px, float(g[f"alpha{iid}"]))
+        else:
+            P = px
+        v = O.describe_one(P, int(g["row"][i]), int(g["col"][i]), int(g["scale"][i]),
+                           float(g["beta0"][i]), int(g["d"][i]), int(g["l_max"][i]), bool(g["orient"][i]))
+        worst = max(worst, float(np.max(np.abs(v - g["desc"][i]))))
+    assert worst <= 1e-12, worst
+
+
+def test_oracle_matcher_matches_reference(golden):
+    g = golden("matcher.npz")
+    meta = json.loads(str(g["meta"]))
+    for m in meta:
+        A = g[f"{m['label']}__A"].astype(np.float64)
+        B = g[f"{m['label']}__B"].astype(np.float64)
+        r1, r2, dl = O.match(A, B, m["delta_s"], m["strategy"])
+        assert np.array_equal(r1, g[f"{m['tag']}__ref1"]), m["tag"]
+        assert np.array_equal(r2, g[f"{m['tag']}__ref2"]), m["tag"]
+        assert np.array_equal(dl, g[f"{m['tag']}__delta"]), m["tag"]
+
+
+def test_oracle_sample_stream_matches_scalar_calls(golden):
+    g = golden("ransac.npz")
+    meta = json.loads(str(g["meta"]))
+    for seed, n in meta["streams"]:
+        want = g[f"stream_{seed}_{n}"]
+        got = O.sample_stream(seed, n, len(want))
+        assert np.array_equal(got, want), (seed, n)
+
+
+def test_oracle_estimate_rigid_matches_reference(golden):
+    g = golden("ransac.npz")
+    meta = json.loads(str(g["meta"]))
+    for k in meta["est"]:
+        got = O.fit_rigid(g[f"est{k}__src"], g[f"est{k}__dst"])
+        assert np.array_equal(np.array(got), g[f"est{k}__model"]), k
+
+
+def test_oracle_ransac_matches_reference(golden):
+    g = golden("ransac.npz")
+    meta = json.loads(str(g["meta"]))
+    for m in meta["cases"]:
+        lab = m["label"]
+        src, dst = g[f"{lab}__src"], g[f"{lab}__dst"]
+        ok = bool(g[f"{lab}__ok"])
+        if not ok:
+            with pytest.raises(O.NoConsensus):
+                O.ransac(src, dst, m["iterations"], m["inlier_tol"], m["min_inliers"], m["seed"])
+            continue
+        r = O.ransac(src, dst, m["iterations"], m["inlier_tol"], m["min_inliers"], m["seed"])
+        assert np.array_equal(r["inliers"], g[f"{lab}__inliers"]), lab
+        assert r["consensus"] == int(g[f"{lab}__consensus"]), lab
+        assert np.array_equal(np.array(r["model"]), g[f"{lab}__model"]), lab
+        assert r["rms"] == float(g[f"{lab}__rms"]), lab
+
+
+def test_oracle_end_to_end_small_pair(golden):
+    g = golden("e2e.npz")
+    kps, descs = [], []
+    for tag in ("a", "b"):
+        px = g[tag].astype(np.float64)
+        P = O.ramp(px, O.default_alpha(*px.shape))
+        kp = O.detect(P, (16, 32, 64))
+        for f in KP_FIELDS:
+            assert np.array_equal(kp[f], g[f"{tag}__{f}"]), (tag, f)
+        d = O.describe(P, kp, 0.0625, 4, 64, True)
+        assert np.max(np.abs(d - g[f"{tag}__desc"])) <= 1e-12
+        kps.append(kp)
+        descs.append(g[f"{tag}__desc"].astype(np.float32).astype(np.float64))
+    r1, r2, dl = O.match(descs[0], descs[1])
+    assert np.array_equal(r1, g["m__ref1"]) and np.array_equal(r2, g["m__ref2"])
+    assert np.array_equal(dl, g["m__delta"])
+    src, dst = O.pair_points(r1, r2, kps[0], kps[1])
+    r = O.ransac(src, dst, 1000, 3.0, 8, 0)
+    assert np.array_equal(r["inliers"], g["r__inliers"])
+    assert np.array_equal(np.array(r["model"]), g["r__model"])
+
+
+def test_scene_digests_pinned():
+    import os
+
+    from paper_2405_08578_b200 import scenes
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "scene_digests.json")) as f:
+        want = json.load(f)
+    for key in ("64x96_seed0", "256x256_seed1", "512x512_seed7"):
+        hw, seed = key.split("_seed")
+        h, w = map(int, hw.split("x"))
+        assert scenes.scene_digest(scenes.scene(h, w, int(seed))) == want[key], key
