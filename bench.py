@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 LP-SIFT hot path -- BASELINE.json configs[1] (C2).
+
+Workload (BASELINE.json configs[1]): 64 seeded 2688x1600
+uint8 noise+shapes scenes, LP-SIFT scales L in {8,16,32,64,128}, multiscale
+extremum detection + float32 128-d descriptors (no matching).  One step =
+detect + describe of the whole 64-image batch; metric Mpixel/s.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+* ``value``: device-resident inputs, CUDA events around exactly K steps,
+  barrier + synchronize on both sides, max over ranks.  Images are sharded
+  over ranks (strong scaling: 64 images in total, no collective on the data
+  path).  The 275 MB input batch is larger than the 126 MB L2, so no flush.
+* ``e2e``: the same metric through the public host API
+  (``pipeline.BatchPreparer``): pinned host images in, host keypoints and
+  float32 descriptors out, H2D/D2H inside the timed region.
+* ``roofline``: the dominant kernel (describe) against measured HBM
+  bandwidth, plus the detect kernel, from CUDA events inside the timed run.
+* ``cpu_baseline``: the oracle port (oracle/lpsift_oracle.py, numpy, the
+  reference's algorithm) on this host's cores, bounded sample, rank 0, N=1.
+* ``--impl reference``: times that CPU port as the reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+N_IMAGES, NR, NC = 64, 1600, 2688
+SCALES = (8, 16, 32, 64, 128)
+WORKLOAD = ("C2: 64 seeded 2688x1600 uint8 noise+shapes scenes; LP-SIFT L in {8..128}; "
+            "detect + float32 128-d describe")
+CPU_SAMPLE_KP = 6000  # keypoints described per CPU-baseline worker per step
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--images", type=int, default=N_IMAGES)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run N steps untimed and exit")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port, bounded sample
+# ---------------------------------------------------------------------------
+
+def _cpu_job(args):
+    seed, n_kp = args
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle import lpsift_oracle as O
+    from paper_2405_08578_b200 import scenes
+
+    img = scenes.scene(NR, NC, seed)
+    t0 = time.perf_counter()
+    P = O.ramp(img.astype(np.float64), O.default_alpha(NR, NC))
+    kp = O.detect(P, SCALES)
+    t1 = time.perf_counter()
+    O.describe(P, kp[:n_kp], 0.0625, 4, 128, True)
+    t2 = time.perf_counter()
+    # extrapolated seconds for the whole image: detect + describe of all keypoints
+    return (t1 - t0) + (t2 - t1) * len(kp) / n_kp
+
+
+def cpu_baseline(steps=1, warmup=0, n_kp=CPU_SAMPLE_KP):
+    """Mpx/s of the oracle port with one process per host core."""
+    import multiprocessing as mp
+
+    P = os.cpu_count() or 1
+    vals = []
+    with mp.get_context("fork").Pool(P) as pool:
+        for s in range(warmup + steps):
+            t0 = time.perf_counter()
+            secs = pool.map(_cpu_job, [(k, n_kp) for k in range(P)])
+            wall = time.perf_counter() - t0
+            if s >= warmup:
+                # P images processed concurrently; per-image time extrapolated
+                vals.append(P * NR * NC / 1e6 / max(secs))
+            _ = wall
+    return dict(value=float(statistics.median(vals)), unit="Mpixel/s", cores=P, kind="port",
+                sample=(f"{P} processes x 1 image each: full detect + describe of the first {n_kp} of "
+                        f"134400 keypoints, describe time extrapolated x{134400 / n_kp:.1f}; oracle port "
+                        f"(numpy) of the reference algorithm"))
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, uuid):
+        self.uuid, self.proc, self.lines = uuid, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.uuid, f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_08578_b200 import _lib, device, scenes
+    from paper_2405_08578_b200.pipeline import BatchPreparer, PipelineConfig, alloc_host_features
+    from paper_2405_08578_b200.records import DescriptorConfig, default_alpha
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    mine = [k for k in range(args.images) if k % world == rank]
+    n = len(mine)
+    # seeds follow the global image index so any N covers the same 64 images
+    host = np.empty((n, NR, NC), dtype=np.uint8)
+    import multiprocessing as mp
+
+    with mp.get_context("fork").Pool(min(16, os.cpu_count() or 1)) as pool:
+        for i, img in enumerate(pool.imap(scenes._scene_job, [(NR, NC, k) for k in mine])):
+            host[i] = img
+    alpha = default_alpha(NR, NC)
+    cfg = DescriptorConfig(0.0625, 4, 128, True)
+    imgs = torch.from_numpy(host).to(dev)
+    dimg = device.DeviceImages(imgs, "u8", alpha)
+    stream = torch.cuda.current_stream()
+    kp = device.detect(dimg, SCALES, meta=False)
+    K = kp.cap
+    desc = torch.empty((n, K, 128), dtype=torch.float32, device=dev)
+
+    def step(evs=None):
+        if evs:
+            evs[0].record(stream)
+        k = device.detect(dimg, SCALES, meta=False)
+        if evs:
+            evs[1].record(stream)
+        device.describe_into(dimg, k, cfg, desc, scale_set=k.scale_set)
+        if evs:
+            evs[2].record(stream)
+        return k
+
+    if args.profile_steps:
+        for _ in range(args.profile_steps):
+            step()
+        torch.cuda.synchronize()
+        return None
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    uuid = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid).replace("GPU-", "")
+    sampler = ClockSampler(uuid)
+    sampler.start()
+    time.sleep(0.3)
+    per = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    launches0 = _lib.kernel_launches()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for s in range(args.steps):
+        step(per[s])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    launches = _lib.kernel_launches() - launches0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms_total = t_start.elapsed_time(t_end)
+    det_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in per)
+    des_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in per)
+    if world > 1:
+        t = torch.tensor([ms_total, det_ms, des_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total, det_ms, des_ms = t.tolist()
+    ms_step = ms_total / args.steps
+    total_px = args.images * NR * NC
+    value = total_px / 1e6 / (ms_step / 1e3)
+
+    # ---- roofline (per launch on this rank's shard) ----
+    peak, peak_kind = measured_peaks()
+    n_kp = K * n
+    bytes_detect = n * NR * NC + n_kp * 16  # image read + (row, col, value) out
+    bytes_desc = n * NR * NC + n_kp * (16 + 128 * 4)  # image + keypoints in, fp32 rows out
+    traffic = None
+    tp = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tj = json.load(f)
+        tr = tj.get("describe_kernel")
+        if tr and int(tr.get("images", -1)) == n:
+            traffic = tr["dram_bytes_per_launch"]
+    ach_des = bytes_desc / (des_ms / 1e3) / 1e9
+    ach_det = bytes_detect / (det_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": "describe_kernel", "achieved": round(ach_des, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(ach_des / peak, 4), "traffic": traffic,
+            "peak_source": peak_kind, "kernel_ms": round(des_ms, 4),
+            "algorithmic_bytes_per_launch": bytes_desc,
+            "note": "describe is float64-pipe bound; bytes = 1 B/px + 16 B/kp in + 512 B/kp out"}
+    kernels = {"detect_u8_w8": {"ms": round(det_ms, 4), "GB/s": round(ach_det, 1),
+                                "frac_hbm": round(ach_det / peak, 4), "bytes_per_launch": bytes_detect},
+               "describe_kernel": {"ms": round(des_ms, 4), "GB/s": round(ach_des, 1),
+                                   "keypoints_per_s": round(n_kp / (des_ms / 1e3), 1)}}
+
+    # ---- e2e through the public host API ----
+    e2e = None
+    if not args.no_e2e:
+        pcfg = PipelineConfig(window_min=8, window_max=128)
+        hin = torch.from_numpy(host).pin_memory()
+        hout = alloc_host_features(n, NR, NC, pcfg)
+        prep = BatchPreparer(NR, NC, pcfg, chunk=8)
+        prep.run(hin, hout)
+        torch.cuda.synchronize()
+        e_steps = max(1, min(args.steps, 3))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            prep.run(hin, hout)
+        torch.cuda.synchronize()
+        e_ms = (time.perf_counter() - t0) * 1e3 / e_steps
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = t.item()
+        d2h = n * (K * (4 + 4 + 8 + 128 * 4) + 4)
+        e2e = {"value": round(total_px / 1e6 / (e_ms / 1e3), 2), "unit": "Mpixel/s", "ms_per_step": round(e_ms, 3),
+               "h2d_bytes_per_step": n * NR * NC * world, "d2h_bytes_per_step": d2h * world,
+               "api": "paper_2405_08578_b200.pipeline.BatchPreparer.run (pinned host in/out, 3-stream pipeline)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(steps=1, warmup=0)
+
+    if rank == 0:
+        out = {
+            "metric": "Mpixel/s LP-SIFT detect+describe", "value": round(value, 2), "unit": "Mpixel/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8/f64",
+            "data": "synthetic (seeded noise+shapes generator, paper_2405_08578_b200/scenes.py)",
+            "config": {"workload": WORKLOAD, "images": args.images, "image_hw": [NR, NC], "scales": list(SCALES),
+                       "keypoints_per_image": K, "descriptor": "float32 128-d", "l2": "inputs larger than L2",
+                       "parallelism": f"images sharded over {world} rank(s)"},
+            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": clocks,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return None
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cb = cpu_baseline(steps=max(args.steps, 1), warmup=max(args.warmup, 0) and 1)
+    out = {"metric": "Mpixel/s LP-SIFT detect+describe", "value": round(cb["value"], 4), "unit": "Mpixel/s",
+           "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded noise+shapes generator)",
+           "config": {"workload": WORKLOAD, "images": args.images, "image_hw": [NR, NC], "scales": list(SCALES)},
+           "cpu_baseline": cb,
+           "e2e": {"value": round(cb["value"], 4), "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,173 @@
+/*
+ * peakstitch_b200 -- C-ABI of the B200 (sm_100a) LP-SIFT hot path:
+ *   detect -> describe -> match -> RANSAC-score
+ *
+ * This is the drop-in boundary for the reference package `peakstitch`
+ * (/root/reference/pkg/src/peakstitch).  The reference has no FFI of its own;
+ * its boundary is four Python entry points, each replaced here by one C entry
+ * point (the Python mirror in paper_2405_08578_b200/ keeps their names,
+ * signatures and exceptions):
+ *
+ *   ps_detect        <- detect_features(img, scales, dedupe)   detector.py:154-172
+ *   ps_describe      <- describe_features(img, features, cfg)  descriptor.py:259-269
+ *                       (and compute_descriptor, descriptor.py:219-256)
+ *   ps_match         <- match_features(set1, set2, cfg)        matcher.py:57-95
+ *   ps_ransac_rigid  <- ransac_rigid(pairs, cfg)               registration.py:149-203
+ *   ps_estimate_rigid<- estimate_rigid(src, dst)               registration.py:107-131
+ *
+ * (line numbers are those of the reference files as shipped.)
+ *
+ * Conventions
+ *  - Every function returns an int status (enum ps_status).  Status codes map
+ *    one-to-one onto the reference's exceptions (errors.py:4-17).  No C++
+ *    exception and no abort() crosses this boundary.
+ *  - All array arguments are DEVICE pointers unless the parameter name says
+ *    `host_`.  Buffers are caller-owned; scratch is a caller-provided device
+ *    workspace whose size the matching *_plan call reports.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    Work is enqueued asynchronously; results are valid once the stream is
+ *    synchronised.  Outcomes that depend on data (e.g. "no consensus") are
+ *    reported through device-side info words, not the return status.
+ *  - No hidden global mutable state other than the launch counter and the
+ *    thread-local last-error message; all calls are re-entrant.
+ */
+#ifndef PEAKSTITCH_B200_H
+#define PEAKSTITCH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define PS_API __attribute__((visibility("default")))
+#else
+#define PS_API
+#endif
+
+enum ps_status {
+  PS_OK = 0,
+  PS_ERR_CONFIG = 1,       /* peakstitch.errors.ConfigError           */
+  PS_ERR_VALUE = 2,        /* ValueError (geometry / region checks)    */
+  PS_ERR_DEGENERATE = 3,   /* peakstitch.errors.DegenerateSampleError */
+  PS_ERR_REGISTRATION = 4, /* peakstitch.errors.RegistrationError     */
+  PS_ERR_CUDA = 5,         /* CUDA runtime error                       */
+  PS_ERR_ARGUMENT = 6,     /* bad pointer / size / unsupported layout  */
+  PS_ERR_CAPACITY = 7      /* output capacity too small                */
+};
+
+enum ps_pixel_type {
+  PS_PIXELS_U8 = 0,  /* raw 8-bit intensities; the linear ramp of
+                        apply_linear_ramp (imaging.py:130-149) is fused:
+                        P[r,c] = fl(I[r,c] + fl((r*nc+c+1) * alpha))        */
+  PS_PIXELS_F64 = 1, /* an already-ramped float64 raster (RampedImage.pixels) */
+  PS_PIXELS_F64_RAW = 2 /* float64 intensities (IntensityImage.pixels); ramp
+                           fused as for PS_PIXELS_U8                          */
+};
+
+enum ps_match_strategy {
+  PS_MATCH_NEAREST = 0,      /* "nearest_neighbor": mutual NN + dist < delta_s */
+  PS_MATCH_THRESHOLD_ALL = 1 /* "threshold_all": every dist < delta_s         */
+};
+
+/* A batch of B equally sized images in device memory. */
+typedef struct ps_image_batch {
+  const void* data;     /* device pointer to image 0, pixel (0,0)            */
+  int32_t pixel_type;   /* enum ps_pixel_type                                */
+  int32_t batch;        /* B >= 1                                            */
+  int32_t nr, nc;       /* rows, columns                                     */
+  int64_t row_pitch;    /* elements between consecutive rows  (>= nc)        */
+  int64_t image_stride; /* elements between consecutive images              */
+  double alpha;         /* ramp coefficient (PS_PIXELS_U8 only)              */
+} ps_image_batch;
+
+/* Keypoints of a batch, image b occupying slots [b*cap, b*cap + count[b]).
+ * Field meaning follows FeaturePoint (detector.py:71-80); polarity 0 = "max",
+ * 1 = "min".  scale / polarity / window may be NULL on output (not written)
+ * and `scale` may be NULL on input to ps_describe (then every keypoint has
+ * scale `default_scale`). */
+typedef struct ps_keypoints {
+  int32_t* row;
+  int32_t* col;
+  double* value;
+  int32_t* scale;
+  int8_t* polarity;
+  int32_t* window;
+  int32_t* count; /* device [B] */
+  int64_t cap;    /* slots per image */
+} ps_keypoints;
+
+PS_API int ps_abi_version(void);
+PS_API const char* ps_last_error(void);      /* thread-local message of the last failure */
+PS_API uint64_t ps_kernel_launches(void);    /* kernels launched by this library so far   */
+PS_API int ps_device_sync(void* stream);     /* cudaStreamSynchronize + error check       */
+
+/* ---- detect: detector.py:154-172 --------------------------------------- */
+/* Validates the scale set (ScaleSet rules, detector.py:188-217) against the
+ * image and reports the per-image output capacity and workspace size. */
+PS_API int ps_detect_plan(int32_t batch, int32_t nr, int32_t nc, const int32_t* host_scales,
+                   int32_t n_scales, int32_t dedupe, int64_t* cap_out,
+                   size_t* workspace_bytes_out);
+PS_API int ps_detect(const ps_image_batch* img, const int32_t* host_scales, int32_t n_scales,
+              int32_t dedupe, ps_keypoints* out, void* workspace, size_t workspace_bytes,
+              void* stream);
+
+/* ---- describe: descriptor.py:219-269 ------------------------------------ */
+/* host_scale_set lists every scale that may occur in kp->scale (the ScaleSet);
+ * region sizes are derived on the host per scale (descriptor.py:82-95, 118-131).
+ * Keypoints must lie inside the image and carry a scale of the set (slots
+ * that do not are skipped, unwritten).  Output row k of out_desc32 / out_desc64 ([B*cap, 8*d*d], row-major) is the
+ * descriptor of keypoint slot k; slots >= count are not written.  Either
+ * output pointer may be NULL. */
+PS_API int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, int32_t default_scale,
+                const int32_t* host_scale_set, int32_t n_scale_set, double beta0, int32_t d,
+                int32_t l_max, int32_t orientation_normalize, float* out_desc32,
+                double* out_desc64, void* stream);
+
+/* ---- match: matcher.py:57-95 -------------------------------------------- */
+PS_API int ps_match_plan(int64_t n1, int64_t n2, int32_t dim, int32_t strategy, int64_t cap,
+                  size_t* workspace_bytes_out);
+/* desc1 [n1, dim], desc2 [n2, dim] row-major, float32 (desc_is_f64 = 0; the
+ * values are upcast to float64 exactly) or float64 (desc_is_f64 = 1).  All
+ * distance arithmetic is the reference's float64 arithmetic.
+ * Writes up to `cap` pairs sorted by (delta, ref1, ref2) and the total pair
+ * count to *out_count (device int64); if the total exceeds cap only the
+ * first `cap` are valid and the caller retries with a larger cap. */
+PS_API int ps_match(const void* desc1, int64_t n1, const void* desc2, int64_t n2, int32_t dim,
+             int32_t desc_is_f64, double delta_s, int32_t strategy, int32_t* out_ref1, int32_t* out_ref2,
+             double* out_delta, int64_t* out_count, int64_t cap, void* workspace,
+             size_t workspace_bytes, void* stream);
+
+/* Gather (x, y) = (col, row) float64 point pairs of matches
+ * (registration.py:143-146) from two keypoint arrays. */
+PS_API int ps_pair_points(const int32_t* ref1, const int32_t* ref2, const int64_t* count,
+                   const int32_t* row1, const int32_t* col1, const int32_t* row2,
+                   const int32_t* col2, double* src_xy, double* dst_xy, int64_t cap,
+                   void* stream);
+
+/* ---- RANSAC: registration.py:107-203 ------------------------------------ */
+/* samples: device int32 [iterations, 2], the reference's index stream
+ * (registration.py:164, 170-173), generated on the host from the seed.
+ * out_model: device double[3] = (theta, t_x, t_y) of the refit, theta in
+ * (-pi, pi].  out_mask: device uint8[n] final inlier mask.
+ * out_info: device int64[4] = (status, consensus_size, n_inliers, best_iter)
+ * with status PS_OK or PS_ERR_REGISTRATION.  out_rms: device double[1]. */
+PS_API int ps_ransac_plan(int64_t n, int32_t iterations, size_t* workspace_bytes_out);
+PS_API int ps_ransac_rigid(const double* src_xy, const double* dst_xy, int64_t n,
+                    const int32_t* samples, int32_t iterations, double inlier_tol,
+                    int32_t min_inliers, double* out_model, uint8_t* out_mask,
+                    int64_t* out_info, double* out_rms, void* workspace,
+                    size_t workspace_bytes, void* stream);
+/* Least-squares rigid fit of dst ~ H(src) over all n points; out_info[0] is
+ * PS_OK or PS_ERR_DEGENERATE. */
+PS_API int ps_estimate_rigid(const double* src_xy, const double* dst_xy, int64_t n,
+                      double* out_model, int64_t* out_info, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PEAKSTITCH_B200_H */

@@ -1,0 +1,113 @@
+"""ctypes binding of the C-ABI library ``libpeakstitch_b200.so``.
+
+The library is built in-tree (``__graft_entry__.build()`` / ``make -C
+paper_2405_08578_b200/csrc``).  There is no fallback: if the shared object
+is missing or does not load, every hot-path entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import ConfigError, DegenerateSampleError, RegistrationError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpeakstitch_b200.so")
+
+PS_OK, PS_ERR_CONFIG, PS_ERR_VALUE, PS_ERR_DEGENERATE, PS_ERR_REGISTRATION = 0, 1, 2, 3, 4
+PS_ERR_CUDA, PS_ERR_ARGUMENT, PS_ERR_CAPACITY = 5, 6, 7
+PS_PIXELS_U8, PS_PIXELS_F64, PS_PIXELS_F64_RAW = 0, 1, 2
+PS_MATCH_NEAREST, PS_MATCH_THRESHOLD_ALL = 0, 1
+
+
+class ImageBatch(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("pixel_type", C.c_int32), ("batch", C.c_int32),
+                ("nr", C.c_int32), ("nc", C.c_int32), ("row_pitch", C.c_int64),
+                ("image_stride", C.c_int64), ("alpha", C.c_double)]
+
+
+class KeypointsC(C.Structure):
+    _fields_ = [("row", C.c_void_p), ("col", C.c_void_p), ("value", C.c_void_p),
+                ("scale", C.c_void_p), ("polarity", C.c_void_p), ("window", C.c_void_p),
+                ("count", C.c_void_p), ("cap", C.c_int64)]
+
+
+# exported symbol -> (restype, argtypes); mirrors include/peakstitch_b200.h
+SIGNATURES = {
+    "ps_abi_version": (C.c_int, []),
+    "ps_last_error": (C.c_char_p, []),
+    "ps_kernel_launches": (C.c_uint64, []),
+    "ps_device_sync": (C.c_int, [C.c_void_p]),
+    "ps_detect_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32,
+                                 C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_size_t)]),
+    "ps_detect": (C.c_int, [C.POINTER(ImageBatch), C.POINTER(C.c_int32), C.c_int32, C.c_int32,
+                            C.POINTER(KeypointsC), C.c_void_p, C.c_size_t, C.c_void_p]),
+    "ps_describe": (C.c_int, [C.POINTER(ImageBatch), C.POINTER(KeypointsC), C.c_int32,
+                              C.POINTER(C.c_int32), C.c_int32, C.c_double, C.c_int32, C.c_int32,
+                              C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ps_match_plan": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int64,
+                                C.POINTER(C.c_size_t)]),
+    "ps_match": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_double,
+                           C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                           C.c_void_p, C.c_size_t, C.c_void_p]),
+    "ps_pair_points": (C.c_int, [C.c_void_p] * 9 + [C.c_int64, C.c_void_p]),
+    "ps_ransac_plan": (C.c_int, [C.c_int64, C.c_int32, C.POINTER(C.c_size_t)]),
+    "ps_ransac_rigid": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32,
+                                  C.c_double, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "ps_estimate_rigid": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                    C.c_void_p]),
+}
+
+_lib = None
+
+
+def lib():
+    """The loaded library (raises if it is missing: there is no CPU path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} not built; run `make -C paper_2405_08578_b200/csrc` "
+                "(or __graft_entry__.build()).  peakstitch_b200 has no CPU fallback."
+            )
+        handle = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        if handle.ps_abi_version() != 1:
+            raise ImportError("libpeakstitch_b200 ABI version mismatch")
+        _lib = handle
+    return _lib
+
+
+def last_error() -> str:
+    return lib().ps_last_error().decode("utf-8", "replace")
+
+
+def check(status: int, what: str = "") -> None:
+    """Map a ps_status onto the reference's exception taxonomy (errors.py:4-17)."""
+    if status == PS_OK:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if status == PS_ERR_CONFIG:
+        raise ConfigError(msg)
+    if status == PS_ERR_VALUE:
+        raise ValueError(msg)
+    if status == PS_ERR_DEGENERATE:
+        raise DegenerateSampleError(msg)
+    if status == PS_ERR_REGISTRATION:
+        raise RegistrationError(msg)
+    if status == PS_ERR_ARGUMENT:
+        raise ValueError(msg)
+    raise RuntimeError(f"peakstitch_b200 CUDA failure ({status}): {msg}")
+
+
+def kernel_launches() -> int:
+    return int(lib().ps_kernel_launches())
+
+
+def int32_array(values):
+    arr = (C.c_int32 * len(values))(*[int(v) for v in values])
+    return arr

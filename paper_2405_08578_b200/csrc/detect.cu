@@ -1,0 +1,503 @@
+// K1 -- multiscale window-extremum detector (reference detector.py:154-172).
+//
+// Semantics reproduced:
+//  * windows of side L tile the image row-major, trailing ones shrunk
+//    (detector.py:87-103); window_index = (row0/L)*ceil(nc/L) + col0/L;
+//  * per window the FIRST argmax / argmin of the ramped float64 raster
+//    (detector.py:114-119).  For 8-bit input with a valid ramp (alpha >= 2^-40
+//    and alpha*nr*nc <= 0.5) the ramp makes every pixel distinct and the rule
+//    is the integer key (v, k): max -> largest v then HIGHEST flat index,
+//    min -> smallest v then LOWEST flat index.  Otherwise the float64 values
+//    P[r,c] are recomputed bit-exactly and compared with first-occurrence ties;
+//  * dedupe keeps the first (smallest-scale) feature per (row, col, polarity)
+//    (detector.py:139-151) and the output is ordered (scale, window, polarity).
+//    A scale L whose every window is a union of windows of a smaller scale L'
+//    (L % L' == 0) can only contribute duplicates, so with dedupe it is not
+//    evaluated at all; for the usual doubling scale sets only L_min remains.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "ps_common.cuh"
+
+namespace ps {
+namespace {
+
+constexpr int kMaxScales = 16;
+
+struct ScalePlan {
+  int n;                    // evaluated scales (ascending)
+  int L[kMaxScales];        // window side
+  int wc[kMaxScales];       // windows per row
+  int nwin[kMaxScales];     // windows per image
+  int64_t raw_off[kMaxScales + 1];  // raw feature offset of scale i (2 per window)
+};
+
+struct KpOut {
+  int32_t* row;
+  int32_t* col;
+  double* value;
+  int32_t* scale;
+  int8_t* pol;
+  int32_t* window;
+  int64_t cap;
+};
+
+// ---- comparison helpers -----------------------------------------------------
+
+struct BestF64 {
+  double v;
+  int32_t k;
+};
+// max: larger value wins, equal value -> lower flat index (first occurrence)
+__device__ __forceinline__ bool better_max(double v, int32_t k, double bv, int32_t bk) {
+  return v > bv || (v == bv && k < bk);
+}
+__device__ __forceinline__ bool better_min(double v, int32_t k, double bv, int32_t bk) {
+  return v < bv || (v == bv && k < bk);
+}
+
+// ---- generic kernel: one warp per window -----------------------------------
+// MODE 0: u8 integer key (valid ramp); MODE 1: float64 compare on P[r,c].
+template <int MODE, class Img>
+__global__ void __launch_bounds__(256) window_extrema_warp(
+    Img img, int64_t img_stride, int B, int L, int wc, int nwin, int32_t* __restrict__ tmax,
+    int32_t* __restrict__ tmin, KpOut out, int32_t scale_tag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int nr = img.nr, nc = img.nc;
+  for (int64_t g = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); g < (int64_t)B * nwin;
+       g += warps) {
+    const int b = (int)(g / nwin);
+    const int w = (int)(g % nwin);
+    Img im = img;
+    im.p = img.p + (int64_t)b * img_stride;
+    const int r0 = (w / wc) * L, c0 = (w % wc) * L;
+    const int h = min(L, nr - r0), wd = min(L, nc - c0);
+    int32_t kmax, kmin;
+    if (MODE == 0) {
+      uint64_t best_hi = 0, best_lo = ~0ull;
+      for (int r = 0; r < h; ++r) {
+        const int64_t rowbase = (int64_t)(r0 + r) * nc;
+        for (int c = lane; c < wd; c += 32) {
+          const uint8_t* pp = reinterpret_cast<const uint8_t*>(im.p);
+          uint64_t v = pp[(int64_t)(r0 + r) * im.pitch + c0 + c];
+          uint64_t key = (v << 32) | (uint64_t)(rowbase + c0 + c);
+          best_hi = key > best_hi ? key : best_hi;
+          best_lo = key < best_lo ? key : best_lo;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        uint64_t a = __shfl_xor_sync(0xffffffffu, best_hi, o);
+        uint64_t c = __shfl_xor_sync(0xffffffffu, best_lo, o);
+        best_hi = a > best_hi ? a : best_hi;
+        best_lo = c < best_lo ? c : best_lo;
+      }
+      kmax = (int32_t)(best_hi & 0xffffffffu);
+      kmin = (int32_t)(best_lo & 0xffffffffu);
+    } else {
+      double vh = 0, vl = 0;
+      int32_t kh = INT32_MAX, kl = INT32_MAX;
+      bool any = false;
+      for (int r = 0; r < h; ++r) {
+        for (int c = lane; c < wd; c += 32) {
+          const double v = im.at(r0 + r, c0 + c);
+          const int32_t k = (r0 + r) * nc + c0 + c;
+          if (!any) {
+            vh = vl = v;
+            kh = kl = k;
+            any = true;
+          } else {
+            if (better_max(v, k, vh, kh)) { vh = v; kh = k; }
+            if (better_min(v, k, vl, kl)) { vl = v; kl = k; }
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        double v2 = __shfl_xor_sync(0xffffffffu, vh, o);
+        int32_t k2 = __shfl_xor_sync(0xffffffffu, kh, o);
+        double v3 = __shfl_xor_sync(0xffffffffu, vl, o);
+        int32_t k3 = __shfl_xor_sync(0xffffffffu, kl, o);
+        if (k2 != INT32_MAX && (kh == INT32_MAX || better_max(v2, k2, vh, kh))) { vh = v2; kh = k2; }
+        if (k3 != INT32_MAX && (kl == INT32_MAX || better_min(v3, k3, vl, kl))) { vl = v3; kl = k3; }
+      }
+      kmax = kh;
+      kmin = kl;
+    }
+    if (lane == 0) {
+      if (tmax) {
+        tmax[(int64_t)b * nwin + w] = kmax;
+        tmin[(int64_t)b * nwin + w] = kmin;
+      }
+      if (out.row) {  // direct emission: slot 2w (max), 2w+1 (min)
+        const int64_t s = (int64_t)b * out.cap + 2 * (int64_t)w;
+        const int32_t ks[2] = {kmax, kmin};
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int rr = ks[q] / nc, cc = ks[q] % nc;
+          out.row[s + q] = rr;
+          out.col[s + q] = cc;
+          out.value[s + q] = im.at(rr, cc);
+          if (out.scale) out.scale[s + q] = scale_tag;
+          if (out.pol) out.pol[s + q] = (int8_t)q;
+          if (out.window) out.window[s + q] = w;
+        }
+      }
+    }
+  }
+}
+
+// ---- fast path: u8, L = 8, valid ramp, 16-byte aligned rows ---------------
+// One thread owns two horizontally adjacent 8x8 windows (a 16-byte column
+// strip over 8 rows, eight 16-byte loads; a warp reads 8 rows x 512 B).
+// Keys are 16-bit (v << 8 | 8*lr + lc) packed two per register with PRMT and
+// reduced with the 3-input packed-u16 max/min (VIMNMX3).
+__device__ __forceinline__ void keys_of_word(uint32_t word, uint32_t idxbytes, uint32_t& k01,
+                                             uint32_t& k23) {
+  k01 = __byte_perm(word, idxbytes, 0x1504);  // [idx0, v0, idx1, v1]
+  k23 = __byte_perm(word, idxbytes, 0x3726);  // [idx2, v2, idx3, v3]
+}
+
+__device__ __forceinline__ void emit_pair(const KpOut& out, int64_t slot, int32_t kmax, int32_t kmin,
+                                          int nc, const RampU8& im, int32_t scale_tag, int w) {
+  const int r0 = kmax / nc, c0 = kmax % nc, r1 = kmin / nc, c1 = kmin % nc;
+  *reinterpret_cast<int2*>(out.row + slot) = make_int2(r0, r1);
+  *reinterpret_cast<int2*>(out.col + slot) = make_int2(c0, c1);
+  *reinterpret_cast<double2*>(out.value + slot) = make_double2(im.at(r0, c0), im.at(r1, c1));
+  if (out.scale) { out.scale[slot] = scale_tag; out.scale[slot + 1] = scale_tag; }
+  if (out.pol) { out.pol[slot] = 0; out.pol[slot + 1] = 1; }
+  if (out.window) { out.window[slot] = w; out.window[slot + 1] = w; }
+}
+
+__global__ void __launch_bounds__(256) detect_u8_w8(RampU8 img, int64_t img_stride, int B, int wr_n,
+                                                    int wc_n, int pairs_per_row, KpOut out,
+                                                    int32_t* __restrict__ tmax, int32_t* __restrict__ tmin) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per_img = (int64_t)wr_n * pairs_per_row;
+  if (t >= (int64_t)B * per_img) return;
+  const int b = (int)(t / per_img);
+  const int rem = (int)(t % per_img);
+  const int wr = rem / pairs_per_row, q = rem % pairs_per_row;
+  const int nr = img.nr, nc = img.nc;
+  RampU8 im = img;
+  im.p = img.p + (int64_t)b * img_stride;
+  const int r0 = wr * 8, cbase = q * 16;
+  const int w0 = wr * wc_n + 2 * q;
+  const bool second = (2 * q + 1) < wc_n;
+  int32_t kmax[2], kmin[2];
+  if (r0 + 8 <= nr && cbase + 16 <= nc) {
+    uint32_t mx[2] = {0u, 0u}, mn[2] = {0xffffffffu, 0xffffffffu};
+    const uint8_t* base = im.p + (int64_t)r0 * im.pitch + cbase;
+    uint4 rows[8];
+#pragma unroll
+    for (int lr = 0; lr < 8; ++lr) rows[lr] = __ldg(reinterpret_cast<const uint4*>(base + lr * im.pitch));
+#pragma unroll
+    for (int lr = 0; lr < 8; ++lr) {
+      const uint32_t ib = (uint32_t)(lr * 8) * 0x01010101u;
+      uint32_t a0, a1, a2, a3, b0, b1, b2, b3;
+      keys_of_word(rows[lr].x, ib + 0x03020100u, a0, a1);
+      keys_of_word(rows[lr].y, ib + 0x07060504u, a2, a3);
+      keys_of_word(rows[lr].z, ib + 0x03020100u, b0, b1);
+      keys_of_word(rows[lr].w, ib + 0x07060504u, b2, b3);
+      mx[0] = __vimax3_u16x2(mx[0], __vimax3_u16x2(a0, a1, a2), a3);
+      mn[0] = __vimin3_u16x2(mn[0], __vimin3_u16x2(a0, a1, a2), a3);
+      mx[1] = __vimax3_u16x2(mx[1], __vimax3_u16x2(b0, b1, b2), b3);
+      mn[1] = __vimin3_u16x2(mn[1], __vimin3_u16x2(b0, b1, b2), b3);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t hi = max(mx[h] & 0xffffu, mx[h] >> 16);
+      const uint32_t lo = min(mn[h] & 0xffffu, mn[h] >> 16);
+      const int cw = cbase + 8 * h;
+      kmax[h] = (r0 + (int)((hi & 0xff) >> 3)) * nc + cw + (int)(hi & 7);
+      kmin[h] = (r0 + (int)((lo & 0xff) >> 3)) * nc + cw + (int)(lo & 7);
+    }
+  } else {
+    // edge strip: scalar keys over the clipped windows (same order)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t hi = 0, lo = 0xffffffffu;
+      const int cw = cbase + 8 * h;
+      for (int lr = 0; lr < 8 && r0 + lr < nr; ++lr)
+        for (int lc = 0; lc < 8 && cw + lc < nc; ++lc) {
+          const uint32_t key = ((uint32_t)im.p[(int64_t)(r0 + lr) * im.pitch + cw + lc] << 8) | (lr * 8 + lc);
+          hi = max(hi, key);
+          lo = min(lo, key);
+        }
+      kmax[h] = (r0 + (int)((hi & 0xff) >> 3)) * nc + cw + (int)(hi & 7);
+      kmin[h] = (r0 + (int)((lo & 0xff) >> 3)) * nc + cw + (int)(lo & 7);
+    }
+  }
+  const int64_t nwin = (int64_t)wr_n * wc_n;
+  if (out.row) {
+    emit_pair(out, (int64_t)b * out.cap + 2 * (int64_t)w0, kmax[0], kmin[0], nc, im, 8, w0);
+    if (second) emit_pair(out, (int64_t)b * out.cap + 2 * (int64_t)(w0 + 1), kmax[1], kmin[1], nc, im, 8, w0 + 1);
+  }
+  if (tmax) {
+    tmax[b * nwin + w0] = kmax[0];
+    tmin[b * nwin + w0] = kmin[0];
+    if (second) {
+      tmax[b * nwin + w0 + 1] = kmax[1];
+      tmin[b * nwin + w0 + 1] = kmin[1];
+    }
+  }
+}
+
+// ---- general emission (several scales and/or dedupe) ------------------------
+struct Tables {
+  int32_t* tmax[kMaxScales];
+  int32_t* tmin[kMaxScales];
+};
+
+__global__ void dedupe_flags(ScalePlan sp, Tables tb, int B, int nc, int dedupe, int32_t* __restrict__ flags) {
+  const int64_t raw = sp.raw_off[sp.n];
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < (int64_t)B * raw;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(g / raw);
+    const int64_t f = g % raw;
+    int si = 0;
+    while (f >= sp.raw_off[si + 1]) ++si;
+    const int64_t loc = f - sp.raw_off[si];
+    const int w = (int)(loc >> 1), pol = (int)(loc & 1);
+    int keep = 1;
+    if (dedupe) {
+      const int32_t k = pol ? tb.tmin[si][(int64_t)b * sp.nwin[si] + w] : tb.tmax[si][(int64_t)b * sp.nwin[si] + w];
+      const int r = k / nc, c = k % nc;
+      for (int sj = 0; sj < si; ++sj) {
+        const int wj = (r / sp.L[sj]) * sp.wc[sj] + c / sp.L[sj];
+        const int32_t kj = pol ? tb.tmin[sj][(int64_t)b * sp.nwin[sj] + wj] : tb.tmax[sj][(int64_t)b * sp.nwin[sj] + wj];
+        if (kj == k) { keep = 0; break; }
+      }
+    }
+    flags[g] = keep;
+  }
+}
+
+template <class Img>
+__global__ void scatter_kept(ScalePlan sp, Tables tb, Img img, int64_t img_stride, int B,
+                             const int32_t* __restrict__ flags, const int32_t* __restrict__ pos, KpOut out,
+                             int32_t* __restrict__ counts) {
+  const int64_t raw = sp.raw_off[sp.n];
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < (int64_t)B * raw;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(g / raw);
+    const int64_t f = g % raw;
+    const int64_t base = pos[(int64_t)b * raw];
+    if (f == raw - 1) counts[b] = (int32_t)(pos[g] + flags[g] - base);
+    if (!flags[g]) continue;
+    int si = 0;
+    while (f >= sp.raw_off[si + 1]) ++si;
+    const int64_t loc = f - sp.raw_off[si];
+    const int w = (int)(loc >> 1), pol = (int)(loc & 1);
+    const int32_t k = pol ? tb.tmin[si][(int64_t)b * sp.nwin[si] + w] : tb.tmax[si][(int64_t)b * sp.nwin[si] + w];
+    Img im = img;
+    im.p = img.p + (int64_t)b * img_stride;
+    const int r = k / img.nc, c = k % img.nc;
+    const int64_t s = (int64_t)b * out.cap + (pos[g] - base);
+    out.row[s] = r;
+    out.col[s] = c;
+    out.value[s] = im.at(r, c);
+    if (out.scale) out.scale[s] = sp.L[si];
+    if (out.pol) out.pol[s] = (int8_t)pol;
+    if (out.window) out.window[s] = w;
+  }
+}
+
+__global__ void fill_counts(int32_t* counts, int B, int32_t v) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < B) counts[i] = v;
+}
+
+// ---- host planning -----------------------------------------------------------
+
+int validate_scales(int nr, int nc, const int32_t* s, int n) {
+  // ScaleSet.__post_init__ / validate_for (detector.py:188-217)
+  PS_REQUIRE(n >= 1, PS_ERR_CONFIG, "scale set must contain at least one size");
+  PS_REQUIRE(n <= kMaxScales, PS_ERR_ARGUMENT, "at most %d scales supported", kMaxScales);
+  for (int i = 0; i < n; ++i) PS_REQUIRE(s[i] >= 8, PS_ERR_CONFIG, "window sizes must be integers >= 8");
+  for (int i = 1; i < n; ++i) PS_REQUIRE(s[i] > s[i - 1], PS_ERR_CONFIG, "window sizes must be strictly increasing");
+  PS_REQUIRE(s[n - 1] <= std::min(nr, nc), PS_ERR_CONFIG, "largest window %d exceeds image side %d", s[n - 1],
+             std::min(nr, nc));
+  PS_REQUIRE((int64_t)nr * nc < (int64_t)INT32_MAX, PS_ERR_ARGUMENT, "image too large (nr*nc >= 2^31)");
+  return PS_OK;
+}
+
+ScalePlan make_plan(int nr, int nc, const int32_t* s, int n, int dedupe) {
+  ScalePlan sp{};
+  sp.n = 0;
+  for (int i = 0; i < n; ++i) {
+    bool shadowed = false;
+    if (dedupe)
+      for (int j = 0; j < i; ++j)
+        if (s[i] % s[j] == 0) shadowed = true;
+    if (shadowed) continue;
+    const int L = s[i];
+    sp.L[sp.n] = L;
+    sp.wc[sp.n] = (nc + L - 1) / L;
+    sp.nwin[sp.n] = ((nr + L - 1) / L) * sp.wc[sp.n];
+    sp.n++;
+  }
+  sp.raw_off[0] = 0;
+  for (int i = 0; i < sp.n; ++i) sp.raw_off[i + 1] = sp.raw_off[i] + 2 * (int64_t)sp.nwin[i];
+  return sp;
+}
+
+bool key_rule_valid(int nr, int nc, double alpha) {
+  return alpha >= 9.094947017729282e-13 /* 2^-40 */ && alpha * (double)nr * (double)nc <= 0.5;
+}
+
+size_t scan_temp_bytes(int64_t n) {
+  size_t t = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, t, (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+  return t;
+}
+
+size_t workspace_need(int B, const ScalePlan& sp, bool direct) {
+  if (direct) return 0;
+  Arena a{nullptr, 0, 0};
+  for (int i = 0; i < sp.n; ++i) {
+    a.take<int32_t>((size_t)B * sp.nwin[i]);
+    a.take<int32_t>((size_t)B * sp.nwin[i]);
+  }
+  const int64_t raw = (int64_t)B * sp.raw_off[sp.n];
+  a.take<int32_t>(raw);
+  a.take<int32_t>(raw);
+  a.take<char>(scan_temp_bytes(raw));
+  return a.used + 256;
+}
+
+int grid_for(int64_t work, int per_block) {
+  int64_t g = (work + per_block - 1) / per_block;
+  if (g > 148 * 64) g = 148 * 64;
+  return (int)std::max<int64_t>(g, 1);
+}
+
+template <class Img>
+int launch_key(const Img&, const ps_image_batch*, int, int, int, int, bool, const KpOut&, int32_t*, int32_t*,
+               cudaStream_t) {
+  set_error("integer-key detection requires 8-bit pixels");
+  return PS_ERR_ARGUMENT;
+}
+
+// u8 pixels with a valid ramp: integer-key kernels (L == 8 vectorised path).
+int launch_key(const RampU8& img, const ps_image_batch* ib, int B, int L, int wc, int nwin, bool aligned,
+               const KpOut& ko, int32_t* tmax, int32_t* tmin, cudaStream_t st) {
+  if (L == 8 && aligned) {
+    const int wr_n = (img.nr + 7) / 8, wc_n = (img.nc + 7) / 8, ppr = (wc_n + 1) / 2;
+    const int64_t th = (int64_t)B * wr_n * ppr;
+    detect_u8_w8<<<(unsigned)((th + 255) / 256), 256, 0, st>>>(img, ib->image_stride, B, wr_n, wc_n, ppr, ko, tmax,
+                                                                tmin);
+    PS_LAUNCHED("detect_u8_w8");
+  } else {
+    window_extrema_warp<0><<<grid_for((int64_t)B * nwin, 8), 256, 0, st>>>(img, ib->image_stride, B, L, wc, nwin,
+                                                                             tmax, tmin, ko, L);
+    PS_LAUNCHED("window_extrema_warp<key>");
+  }
+  return PS_OK;
+}
+
+template <class Img>
+int run_detect(const ps_image_batch* ib, Img img, bool u8, const int32_t* s, int n, int dedupe, ps_keypoints* out,
+               void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int B = ib->batch, nr = ib->nr, nc = ib->nc;
+  ScalePlan sp = make_plan(nr, nc, s, n, dedupe);
+  const bool keymode = u8 && key_rule_valid(nr, nc, ib->alpha);
+  const bool direct = sp.n == 1;  // one evaluated scale: no cross-scale dedupe needed
+  PS_REQUIRE(out->cap >= sp.raw_off[sp.n], PS_ERR_CAPACITY, "keypoint capacity %lld < %lld",
+             (long long)out->cap, (long long)sp.raw_off[sp.n]);
+  KpOut ko{out->row, out->col, out->value, out->scale, out->polarity, out->window, out->cap};
+  if (direct) {
+    const int L = sp.L[0];
+    const bool aligned = (((uintptr_t)ib->data) % 16 == 0) && ib->row_pitch % 16 == 0 && ib->image_stride % 16 == 0;
+    if (keymode) {
+      int rc = launch_key(img, ib, B, L, sp.wc[0], sp.nwin[0], aligned, ko, nullptr, nullptr, st);
+      if (rc) return rc;
+    } else {
+      window_extrema_warp<1><<<grid_for((int64_t)B * sp.nwin[0], 8), 256, 0, st>>>(
+          img, ib->image_stride, B, L, sp.wc[0], sp.nwin[0], nullptr, nullptr, ko, L);
+      PS_LAUNCHED("window_extrema_warp<f64>");
+    }
+    fill_counts<<<(B + 255) / 256, 256, 0, st>>>(out->count, B, (int32_t)sp.raw_off[1]);
+    PS_LAUNCHED("fill_counts");
+    return PS_OK;
+  }
+  const size_t need = workspace_need(B, sp, false);
+  PS_REQUIRE(ws != nullptr && ws_bytes >= need, PS_ERR_ARGUMENT, "detect workspace %zu < %zu", ws_bytes, need);
+  Arena a{(char*)ws, ws_bytes, 0};
+  Tables tb{};
+  for (int i = 0; i < sp.n; ++i) {
+    tb.tmax[i] = a.take<int32_t>((size_t)B * sp.nwin[i]);
+    tb.tmin[i] = a.take<int32_t>((size_t)B * sp.nwin[i]);
+  }
+  const int64_t raw = (int64_t)B * sp.raw_off[sp.n];
+  int32_t* flags = a.take<int32_t>(raw);
+  int32_t* pos = a.take<int32_t>(raw);
+  size_t tb_bytes = scan_temp_bytes(raw);
+  void* tmp = a.take<char>(tb_bytes);
+  KpOut none{};
+  for (int i = 0; i < sp.n; ++i) {
+    const int L = sp.L[i];
+    const bool aligned = (((uintptr_t)ib->data) % 16 == 0) && ib->row_pitch % 16 == 0 && ib->image_stride % 16 == 0;
+    if (keymode) {
+      int rc = launch_key(img, ib, B, L, sp.wc[i], sp.nwin[i], aligned, none, tb.tmax[i], tb.tmin[i], st);
+      if (rc) return rc;
+    } else {
+      window_extrema_warp<1><<<grid_for((int64_t)B * sp.nwin[i], 8), 256, 0, st>>>(
+          img, ib->image_stride, B, L, sp.wc[i], sp.nwin[i], tb.tmax[i], tb.tmin[i], none, L);
+      PS_LAUNCHED("window_extrema_warp<f64>");
+    }
+  }
+  dedupe_flags<<<grid_for(raw, 256), 256, 0, st>>>(sp, tb, B, nc, dedupe, flags);
+  PS_LAUNCHED("dedupe_flags");
+  cub::DeviceScan::ExclusiveSum(tmp, tb_bytes, flags, pos, (int)raw, st);
+  PS_LAUNCHED("cub_exclusive_scan");
+  scatter_kept<<<grid_for(raw, 256), 256, 0, st>>>(sp, tb, img, ib->image_stride, B, flags, pos, ko, out->count);
+  PS_LAUNCHED("scatter_kept");
+  return PS_OK;
+}
+
+}  // namespace
+}  // namespace ps
+
+using namespace ps;
+
+extern "C" int ps_detect_plan(int32_t batch, int32_t nr, int32_t nc, const int32_t* host_scales, int32_t n_scales,
+                              int32_t dedupe, int64_t* cap_out, size_t* workspace_bytes_out) {
+  PS_REQUIRE(batch >= 1 && nr >= 1 && nc >= 1 && host_scales, PS_ERR_ARGUMENT, "bad detect plan arguments");
+  int st = validate_scales(nr, nc, host_scales, n_scales);
+  if (st) return st;
+  ScalePlan sp = make_plan(nr, nc, host_scales, n_scales, dedupe);
+  if (cap_out) *cap_out = sp.raw_off[sp.n];
+  if (workspace_bytes_out) *workspace_bytes_out = workspace_need(batch, sp, sp.n == 1);
+  return PS_OK;
+}
+
+extern "C" int ps_detect(const ps_image_batch* img, const int32_t* host_scales, int32_t n_scales, int32_t dedupe,
+                         ps_keypoints* out, void* workspace, size_t workspace_bytes, void* stream) {
+  PS_REQUIRE(img && out && host_scales && img->data && out->row && out->col && out->value && out->count,
+             PS_ERR_ARGUMENT, "null argument to ps_detect");
+  PS_REQUIRE(img->batch >= 1 && img->nr >= 1 && img->nc >= 1 && img->row_pitch >= img->nc &&
+                 (img->batch == 1 || img->image_stride >= img->row_pitch * img->nr),
+             PS_ERR_ARGUMENT, "bad image geometry");
+  int st = validate_scales(img->nr, img->nc, host_scales, n_scales);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (img->pixel_type == PS_PIXELS_U8) {
+    PS_REQUIRE(img->alpha > 0 && img->alpha * img->nr * img->nc <= 0.05 * 255.0, PS_ERR_CONFIG,
+               "alpha=%g outside the ramp limits (imaging.py:138-145)", img->alpha);
+    RampU8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
+    return run_detect(img, im, true, host_scales, n_scales, dedupe, out, workspace, workspace_bytes, s);
+  }
+  if (img->pixel_type == PS_PIXELS_F64_RAW) {
+    PS_REQUIRE(img->alpha > 0 && img->alpha * img->nr * img->nc <= 0.05 * 255.0, PS_ERR_CONFIG,
+               "alpha=%g outside the ramp limits (imaging.py:138-145)", img->alpha);
+    RampF64Raw im{(const double*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
+    return run_detect(img, im, false, host_scales, n_scales, dedupe, out, workspace, workspace_bytes, s);
+  }
+  PS_REQUIRE(img->pixel_type == PS_PIXELS_F64, PS_ERR_ARGUMENT, "unknown pixel type %d", img->pixel_type);
+  RampF64 im{(const double*)img->data, img->row_pitch, img->nr, img->nc};
+  return run_detect(img, im, false, host_scales, n_scales, dedupe, out, workspace, workspace_bytes, s);
+}

@@ -1,0 +1,356 @@
+"""Tensor-in / tensor-out API of the B200 hot path (torch CUDA tensors).
+
+Every function here is a thin call into the C-ABI library (``_lib``); torch
+is only used for device memory, streams and small host<->device copies.
+There is no CPU path: on a machine without CUDA these functions raise.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ConfigError, RegistrationError
+from .records import default_alpha
+
+
+def _require_cuda(t: torch.Tensor, what: str) -> None:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor (peakstitch_b200 has no CPU path)")
+
+
+def _stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+# ---------------------------------------------------------------------------
+# images
+# ---------------------------------------------------------------------------
+
+@dataclass
+class DeviceImages:
+    """A batch of same-sized rasters on the GPU.
+
+    kind "u8"     : raw 8-bit intensities, ramp fused with ``alpha``;
+    kind "f64raw" : float64 intensities, ramp fused with ``alpha``;
+    kind "f64"    : already-ramped float64 raster (alpha informational).
+    """
+
+    data: torch.Tensor  # [B, nr, nc]
+    kind: str
+    alpha: float
+
+    @property
+    def batch(self) -> int:
+        return int(self.data.shape[0])
+
+    @property
+    def nr(self) -> int:
+        return int(self.data.shape[1])
+
+    @property
+    def nc(self) -> int:
+        return int(self.data.shape[2])
+
+    def c_struct(self) -> _lib.ImageBatch:
+        d = self.data
+        if d.dim() != 3 or d.stride(2) != 1:
+            raise ValueError("images must be [B, nr, nc] with unit column stride")
+        ptype = {"u8": _lib.PS_PIXELS_U8, "f64": _lib.PS_PIXELS_F64, "f64raw": _lib.PS_PIXELS_F64_RAW}[self.kind]
+        return _lib.ImageBatch(d.data_ptr(), ptype, d.shape[0], d.shape[1], d.shape[2], d.stride(1),
+                               d.stride(0) if d.shape[0] > 1 else d.stride(1) * d.shape[1], float(self.alpha))
+
+
+def as_device_images(images, alpha=None, *, ramped=False, device=None) -> DeviceImages:
+    """Wrap a [B, nr, nc] / [nr, nc] uint8 or float64 tensor (uploads if on CPU)."""
+    if isinstance(images, DeviceImages):
+        return images
+    t = images if isinstance(images, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(images))
+    if t.dim() == 2:
+        t = t.unsqueeze(0)
+    if not t.is_cuda:
+        t = t.to(device or "cuda", non_blocking=False)
+    if t.dtype == torch.uint8:
+        kind = "u8"
+    elif t.dtype == torch.float64:
+        kind = "f64" if ramped else "f64raw"
+    else:
+        t, kind = t.to(torch.float64), ("f64" if ramped else "f64raw")
+    if t.stride(2) != 1:
+        t = t.contiguous()
+    if alpha is None:
+        alpha = default_alpha(t.shape[1], t.shape[2])
+    return DeviceImages(t, kind, float(alpha))
+
+
+# ---------------------------------------------------------------------------
+# keypoints
+# ---------------------------------------------------------------------------
+
+@dataclass
+class Keypoints:
+    """Per-image keypoint slots [B, cap]; image b's valid slots are [0, count[b])."""
+
+    row: torch.Tensor
+    col: torch.Tensor
+    value: torch.Tensor
+    count: torch.Tensor
+    scale: torch.Tensor | None = None
+    polarity: torch.Tensor | None = None
+    window: torch.Tensor | None = None
+    default_scale: int = 0
+    scale_set: tuple = ()
+
+    @property
+    def cap(self) -> int:
+        return int(self.row.shape[1])
+
+    @property
+    def batch(self) -> int:
+        return int(self.row.shape[0])
+
+    def c_struct(self) -> _lib.KeypointsC:
+        def p(t):
+            return None if t is None else t.data_ptr()
+
+        return _lib.KeypointsC(p(self.row), p(self.col), p(self.value), p(self.scale), p(self.polarity),
+                               p(self.window), p(self.count), self.cap)
+
+    def image(self, b: int) -> dict:
+        """Host copy of image b's keypoints (numpy arrays)."""
+        n = int(self.count[b].item())
+        out = dict(row=self.row[b, :n].cpu().numpy(), col=self.col[b, :n].cpu().numpy(),
+                   value=self.value[b, :n].cpu().numpy())
+        for k in ("scale", "polarity", "window"):
+            t = getattr(self, k)
+            if t is not None:
+                out[k] = t[b, :n].cpu().numpy()
+        return out
+
+
+def detect(images, scales, *, alpha=None, dedupe=True, ramped=False, meta=True, stream=None) -> Keypoints:
+    """Multiscale window extrema of every image (detector.py:154-172).
+
+    ``meta=False`` skips writing scale/polarity/window (they are implied by
+    the slot for single-evaluated-scale plans: slot 2w -> window w max,
+    2w+1 -> min, scale = scales[0]).
+    """
+    im = as_device_images(images, alpha, ramped=ramped)
+    sizes = [int(s) for s in (scales.sizes if hasattr(scales, "sizes") else scales)]
+    L = _lib.lib()
+    arr = _lib.int32_array(sizes)
+    cap, wsb = C.c_int64(), C.c_size_t()
+    _lib.check(L.ps_detect_plan(im.batch, im.nr, im.nc, arr, len(sizes), int(bool(dedupe)), C.byref(cap),
+                                C.byref(wsb)), "detect")
+    dev = im.data.device
+    B, K = im.batch, cap.value
+    kp = Keypoints(
+        row=torch.empty((B, K), dtype=torch.int32, device=dev),
+        col=torch.empty((B, K), dtype=torch.int32, device=dev),
+        value=torch.empty((B, K), dtype=torch.float64, device=dev),
+        count=torch.empty((B,), dtype=torch.int32, device=dev),
+        scale=torch.empty((B, K), dtype=torch.int32, device=dev) if meta else None,
+        polarity=torch.empty((B, K), dtype=torch.int8, device=dev) if meta else None,
+        window=torch.empty((B, K), dtype=torch.int32, device=dev) if meta else None,
+        default_scale=sizes[0],
+        scale_set=tuple(sizes),
+    )
+    ws = _workspace(wsb.value, dev)
+    ib, kc = im.c_struct(), kp.c_struct()
+    _lib.check(L.ps_detect(C.byref(ib), arr, len(sizes), int(bool(dedupe)), C.byref(kc), C.c_void_p(ws.data_ptr()),
+                           wsb.value, C.c_void_p(_stream_ptr(stream))), "detect")
+    kp._ws = ws  # keep the workspace alive until the stream has consumed it
+    return kp
+
+
+def describe(images, kp: Keypoints, cfg, *, alpha=None, ramped=False, scale_set=None, out64=False,
+             out32=True, stream=None):
+    """Descriptors of every keypoint slot (descriptor.py:219-269).
+
+    Returns float32 [B, cap, D] (and float64 if ``out64``); slots >= count
+    are left unwritten (zero-initialised here).
+    """
+    im = as_device_images(images, alpha, ramped=ramped)
+    D = cfg.d * cfg.d * 8
+    if scale_set is None:
+        scale_set = kp.scale_set or (kp.default_scale,)
+    sset = [int(s) for s in (scale_set.sizes if hasattr(scale_set, "sizes") else scale_set)]
+    dev = im.data.device
+    d32 = torch.zeros((kp.batch, kp.cap, D), dtype=torch.float32, device=dev) if out32 else None
+    d64 = torch.zeros((kp.batch, kp.cap, D), dtype=torch.float64, device=dev) if out64 else None
+    L = _lib.lib()
+    ib, kc = im.c_struct(), kp.c_struct()
+    _lib.check(L.ps_describe(C.byref(ib), C.byref(kc), int(kp.default_scale), _lib.int32_array(sset), len(sset),
+                             float(cfg.beta0), int(cfg.d), int(cfg.l_max), int(bool(cfg.orientation_normalize)),
+                             _ptr(d32), _ptr(d64), C.c_void_p(_stream_ptr(stream))), "describe")
+    if out64 and out32:
+        return d32, d64
+    return d64 if out64 else d32
+
+
+def describe_into(images, kp: Keypoints, cfg, out32: torch.Tensor, *, scale_set=None, stream=None) -> None:
+    """As ``describe`` into a preallocated float32 [B, cap, D] buffer (no allocation)."""
+    im = images if isinstance(images, DeviceImages) else as_device_images(images)
+    sset = [int(s) for s in (scale_set or kp.scale_set or (kp.default_scale,))]
+    ib, kc = im.c_struct(), kp.c_struct()
+    _lib.check(_lib.lib().ps_describe(C.byref(ib), C.byref(kc), int(kp.default_scale), _lib.int32_array(sset),
+                                      len(sset), float(cfg.beta0), int(cfg.d), int(cfg.l_max),
+                                      int(bool(cfg.orientation_normalize)), _ptr(out32), None,
+                                      C.c_void_p(_stream_ptr(stream))), "describe")
+
+
+# ---------------------------------------------------------------------------
+# matching
+# ---------------------------------------------------------------------------
+
+STRATEGIES = {"nearest_neighbor": _lib.PS_MATCH_NEAREST, "threshold_all": _lib.PS_MATCH_THRESHOLD_ALL}
+
+
+def match(desc1: torch.Tensor, desc2: torch.Tensor, delta_s: float = 0.35, strategy: str = "nearest_neighbor",
+          cap: int | None = None, stream=None):
+    """Matches sorted by (delta, ref1, ref2) (matcher.py:57-95).
+
+    Returns device tensors (ref1 int32 [M], ref2 int32 [M], delta float64 [M]).
+    """
+    if strategy not in STRATEGIES:
+        raise ConfigError(f"unknown match strategy {strategy!r}")
+    if delta_s <= 0:
+        raise ConfigError(f"delta_s must be positive, got {delta_s}")
+    # float64 inputs are matched exactly as given; anything else as float32
+    dt = torch.float64 if (desc1.dtype == torch.float64 or desc2.dtype == torch.float64) else torch.float32
+    d1 = desc1.to(dt).contiguous()
+    d2 = desc2.to(dt).contiguous()
+    _require_cuda(d1, "desc1")
+    n1, n2 = int(d1.shape[0]), int(d2.shape[0])
+    dim = int(d1.shape[1]) if d1.dim() == 2 else 128
+    dev = d1.device
+    if n1 == 0 or n2 == 0:
+        e = torch.zeros(0, dtype=torch.int32, device=dev)
+        return e, e.clone(), torch.zeros(0, dtype=torch.float64, device=dev)
+    strat = STRATEGIES[strategy]
+    if cap is None:
+        cap = min(n1, n2) if strat == _lib.PS_MATCH_NEAREST else max(4 * (n1 + n2), 1024)
+    L = _lib.lib()
+    while True:
+        wsb = C.c_size_t()
+        _lib.check(L.ps_match_plan(n1, n2, dim, strat, cap, C.byref(wsb)), "match")
+        ws = _workspace(wsb.value, dev)
+        r1 = torch.empty(cap, dtype=torch.int32, device=dev)
+        r2 = torch.empty(cap, dtype=torch.int32, device=dev)
+        dl = torch.empty(cap, dtype=torch.float64, device=dev)
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        _lib.check(L.ps_match(_ptr(d1), n1, _ptr(d2), n2, dim, int(dt == torch.float64), float(delta_s), strat, _ptr(r1), _ptr(r2), _ptr(dl),
+                              _ptr(cnt), cap, _ptr(ws), wsb.value, C.c_void_p(_stream_ptr(stream))), "match")
+        m = int(cnt.item())
+        if m <= cap:
+            return r1[:m], r2[:m], dl[:m]
+        cap = m  # threshold_all overflow: retry with the exact size
+
+
+def pair_points(r1, r2, kp1_row, kp1_col, kp2_row, kp2_col, stream=None):
+    """(x, y) = (col, row) float64 coordinates of matched pairs (registration.py:143-146)."""
+    n = int(r1.shape[0])
+    dev = r1.device
+    src = torch.empty((n, 2), dtype=torch.float64, device=dev)
+    dst = torch.empty((n, 2), dtype=torch.float64, device=dev)
+    if n:
+        cnt = torch.tensor([n], dtype=torch.int64, device=dev)
+        _lib.check(_lib.lib().ps_pair_points(_ptr(r1), _ptr(r2), _ptr(cnt), _ptr(kp1_row), _ptr(kp1_col),
+                                             _ptr(kp2_row), _ptr(kp2_col), _ptr(src), _ptr(dst), n,
+                                             C.c_void_p(_stream_ptr(stream))), "pair_points")
+    return src, dst
+
+
+# ---------------------------------------------------------------------------
+# registration
+# ---------------------------------------------------------------------------
+
+def sample_stream(seed: int, n: int, iterations: int) -> np.ndarray:
+    """The reference's RANSAC index stream (registration.py:164, 170-173).
+
+    numpy's PCG64 ``Generator`` is the reference's own RNG; one vector draw
+    with highs [n, n-1, n, n-1, ...] equals its alternating scalar calls.
+    Host-side by design (seeded sampling is part of the interface).
+    """
+    rng = np.random.default_rng(seed)
+    highs = np.tile(np.array([n, n - 1], dtype=np.int64), iterations)
+    v = rng.integers(0, highs).reshape(iterations, 2)
+    v[:, 1] += v[:, 1] >= v[:, 0]
+    return v.astype(np.int32)
+
+
+@dataclass
+class RansacOutcome:
+    ok: bool
+    status: int
+    theta: float
+    t_x: float
+    t_y: float
+    inliers: np.ndarray
+    consensus: int
+    rms: float
+    best_iteration: int
+
+
+def ransac(src: torch.Tensor, dst: torch.Tensor, iterations=2000, inlier_tol=3.0, min_inliers=8, seed=0,
+           stream=None) -> RansacOutcome:
+    """2-point rigid RANSAC on device (registration.py:149-203)."""
+    if iterations < 1 or inlier_tol <= 0 or min_inliers < 2:
+        raise ConfigError("invalid RANSAC parameters")
+    n = int(src.shape[0])
+    if n < min_inliers:
+        raise RegistrationError(f"only {n} candidate pairs, need at least {min_inliers}")
+    _require_cuda(src, "src")
+    dev = src.device
+    src = src.to(torch.float64).contiguous()
+    dst = dst.to(torch.float64).contiguous()
+    samples = torch.from_numpy(sample_stream(seed, n, iterations)).to(dev, non_blocking=True)
+    L = _lib.lib()
+    wsb = C.c_size_t()
+    _lib.check(L.ps_ransac_plan(n, iterations, C.byref(wsb)), "ransac")
+    ws = _workspace(wsb.value, dev)
+    model = torch.empty(3, dtype=torch.float64, device=dev)
+    mask = torch.empty(n, dtype=torch.uint8, device=dev)
+    info = torch.empty(4, dtype=torch.int64, device=dev)
+    rms = torch.empty(1, dtype=torch.float64, device=dev)
+    _lib.check(L.ps_ransac_rigid(_ptr(src), _ptr(dst), n, _ptr(samples), iterations, float(inlier_tol),
+                                 int(min_inliers), _ptr(model), _ptr(mask), _ptr(info), _ptr(rms), _ptr(ws),
+                                 wsb.value, C.c_void_p(_stream_ptr(stream))), "ransac")
+    info_h = info.cpu().numpy()
+    model_h = model.cpu().numpy()
+    inl = torch.nonzero(mask).flatten().cpu().numpy().astype(np.int64)
+    st = int(info_h[0])
+    return RansacOutcome(ok=st == _lib.PS_OK, status=st, theta=float(model_h[0]), t_x=float(model_h[1]),
+                         t_y=float(model_h[2]), inliers=inl, consensus=int(info_h[1]), rms=float(rms.item()),
+                         best_iteration=int(info_h[3]))
+
+
+def estimate(src: torch.Tensor, dst: torch.Tensor, stream=None):
+    """Least-squares rigid fit (registration.py:107-131) -> (theta, t_x, t_y, status)."""
+    _require_cuda(src, "src")
+    dev = src.device
+    src = src.to(torch.float64).contiguous()
+    dst = dst.to(torch.float64).contiguous()
+    model = torch.empty(3, dtype=torch.float64, device=dev)
+    info = torch.empty(1, dtype=torch.int64, device=dev)
+    _lib.check(_lib.lib().ps_estimate_rigid(_ptr(src), _ptr(dst), int(src.shape[0]), _ptr(model), _ptr(info),
+                                            C.c_void_p(_stream_ptr(stream))), "estimate_rigid")
+    m = model.cpu().numpy()
+    return float(m[0]), float(m[1]), float(m[2]), int(info.item())
+
+
+def kernel_launches() -> int:
+    return _lib.kernel_launches()

@@ -1,0 +1,84 @@
+"""Host-side logic of the package (no GPU): value types, config validation,
+region sizes and the RANSAC sample stream, checked against the oracle and
+the reference fixtures."""
+
+import json
+import math
+
+import numpy as np
+import pytest
+
+from oracle import lpsift_oracle as O
+from paper_2405_08578_b200 import records as R
+from paper_2405_08578_b200.device import sample_stream
+from paper_2405_08578_b200.errors import ConfigError
+from paper_2405_08578_b200.pipeline import PipelineConfig, pair_seed
+
+
+def test_scale_set_rules():
+    assert R.ScaleSet.from_range(32, 40).sizes == (32, 40)
+    assert R.ScaleSet.from_range(8, 64).sizes == (8, 16, 32, 64)
+    assert R.ScaleSet.from_range(32, 32).sizes == (32,)
+    for bad in [(16, 16), (32, 16), (4,), ()]:
+        with pytest.raises(ConfigError):
+            R.ScaleSet(bad)
+    with pytest.raises(ConfigError):
+        R.ScaleSet.from_range(64, 32)
+    R.ScaleSet((8, 9, 128))
+
+
+def test_partition_windows_geometry():
+    w = R.partition_windows(70, 64, 32)
+    assert [x.height for x in w] == [32, 32, 32, 32, 6, 6]
+    assert len(R.partition_windows(50, 83, 16)) == R.window_count(50, 83, 16)
+
+
+def test_region_size_matches_oracle():
+    for beta0, d, lmax in [(0.0625, 4, 128), (0.25, 4, 128), (0.24, 4, 64), (0.0625, 4, 64), (0.1, 3, 40)]:
+        cfg = R.DescriptorConfig(beta0, d, lmax)
+        for s in range(8, lmax + 1):
+            assert R.region_size(s, cfg) == O.region_side(s, beta0, d, lmax)
+    assert R.region_size(128, R.DescriptorConfig()) == 32
+    assert R.region_size(32, R.DescriptorConfig()) == 16
+
+
+def test_sample_stream_matches_reference_scalar_calls(golden):
+    g = golden("ransac.npz")
+    for seed, n in json.loads(str(g["meta"]))["streams"]:
+        want = g[f"stream_{seed}_{n}"]
+        assert np.array_equal(sample_stream(seed, n, len(want)).astype(np.int64), want)
+
+
+def test_rigid_transform_algebra():
+    t = R.RigidTransform(math.pi / 2, 5, -3)
+    assert R.apply_transform(t, (1, 0)) == pytest.approx((5, -2), abs=1e-12)
+    assert R.RigidTransform(-math.pi, 0, 0).theta == pytest.approx(math.pi)
+    rng = np.random.default_rng(0)
+    for _ in range(10):
+        a = R.RigidTransform(rng.uniform(-3, 3), rng.uniform(-9, 9), rng.uniform(-9, 9))
+        assert np.allclose(a.compose(a.inverse()).matrix, np.eye(3), atol=1e-9)
+
+
+def test_pipeline_config_validation():
+    PipelineConfig(window_min=16, window_max=64)
+    PipelineConfig(window_min=8, window_max=128)  # beta0 sits exactly at the bound (C2)
+    with pytest.raises(ConfigError):
+        PipelineConfig(window_min=4, window_max=16)  # config 4 literal
+    with pytest.raises(ConfigError):
+        PipelineConfig(beta0=0.5)
+    with pytest.raises(ConfigError):
+        PipelineConfig(match_strategy="ratio")
+
+
+def test_pair_seed_is_seedsequence():
+    assert pair_seed(0, 1, 2) == int(np.random.SeedSequence([0, 1, 2]).generate_state(1)[0])
+
+
+def test_apply_linear_ramp_validation_and_lazy_view():
+    img = R.IntensityImage(np.full((4, 5), 10.0))
+    r = R.apply_linear_ramp(img, 1e-3)
+    assert np.array_equal(np.asarray(r.pixels), O.ramp(np.full((4, 5), 10.0), 1e-3))
+    with pytest.raises(ConfigError):
+        R.apply_linear_ramp(img, 0.0)
+    with pytest.raises(ConfigError):
+        R.apply_linear_ramp(img, 1.0)
