@@ -82,6 +82,15 @@ struct RampF64 {
   }
 };
 
+// round-to-nearest add that nvcc may not contract (host: plain IEEE add)
+__host__ __device__ __forceinline__ double dadd(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dadd_rn(a, b);
+#else
+  return a + b;
+#endif
+}
+
 struct RampF64Raw {
   const double* p;
   int64_t pitch;
@@ -93,37 +102,60 @@ struct RampF64Raw {
   }
 };
 
+// Leaf of the pairwise sum: n <= 128 elements.
+template <class Next>
+__host__ __device__ inline double np_pairwise_leaf(Next& next, int64_t n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; ++i) res = dadd(res, next());
+    return res;
+  }
+  double r[8];
+  for (int t = 0; t < 8; ++t) r[t] = next();
+  int64_t i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int t = 0; t < 8; ++t) r[t] = dadd(r[t], next());
+  double res = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])), dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
+  for (; i < n; ++i) res = dadd(res, next());
+  return res;
+}
+
 // numpy's float64 pairwise summation (add.reduce over a contiguous axis):
 // n < 8 sequential from 0.0; n <= 128 eight interleaved accumulators then
 // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus the tail; else split at
-// n/2 rounded down to a multiple of 8.  Elements are pulled in index order
-// from `next()`, so the evaluation can stream a filtered sequence.
+// n/2 rounded down to a multiple of 8 and add the halves.  Elements are
+// pulled in index order from `next()`, so a filtered sequence can be
+// streamed.  Iterative (explicit stack): no device recursion.
 template <class Next>
-__device__ double np_pairwise_stream(Next& next, int64_t n) {
-  if (n < 8) {
-    double res = 0.0;
-    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, next());
-    return res;
-  }
-  if (n <= 128) {
-    double r[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) r[t] = next();
-    int64_t i = 8;
-    for (; i < n - (n % 8); i += 8) {
-#pragma unroll
-      for (int t = 0; t < 8; ++t) r[t] = __dadd_rn(r[t], next());
+__host__ __device__ inline double np_pairwise_stream(Next& next, int64_t n) {
+  int64_t right[64];
+  double left[64];
+  bool has_left[64];
+  int sp = 0;
+  int64_t len = n;
+  double result = 0.0;
+  for (;;) {
+    while (len > 128) {  // descend into the left half
+      int64_t n2 = len / 2;
+      n2 -= n2 % 8;
+      right[sp] = len - n2;
+      has_left[sp] = false;
+      ++sp;
+      len = n2;
     }
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, next());
-    return res;
+    result = np_pairwise_leaf(next, len);
+    for (;;) {  // ascend
+      if (sp == 0) return result;
+      if (!has_left[sp - 1]) {
+        left[sp - 1] = result;
+        has_left[sp - 1] = true;
+        len = right[sp - 1];
+        break;  // now sum the right half
+      }
+      result = dadd(left[sp - 1], result);
+      --sp;
+    }
   }
-  int64_t n2 = n / 2;
-  n2 -= n2 % 8;
-  double a = np_pairwise_stream(next, n2);
-  double b = np_pairwise_stream(next, n - n2);
-  return __dadd_rn(a, b);
 }
 
 // numpy float mod (npy_divmod): fmod, then + b when the signs differ; a zero
