@@ -10,6 +10,7 @@
 // atan2 / hypot are CUDA's float64 versions (numpy's own differ from libm by
 // ~1 ulp), hence the 1e-4 relative parity bar of contract P2.
 #include <cmath>
+#include <cstring>
 #include <vector>
 
 #include "ps_common.cuh"
@@ -18,38 +19,56 @@ namespace ps {
 namespace {
 
 constexpr int kMaxDescScales = 16;
-constexpr int kWarps = 4;
+constexpr int kWarps = 8;
 
 struct DescParams {
   int n_scales;
   int scale[kMaxDescScales];
-  int w[kMaxDescScales];  // region side after region_size + _fit_region cap
+  int w[kMaxDescScales];       // region side after region_size + _fit_region cap
+  double fx[kMaxDescScales];   // fixed-point scale 2^e of the histogram accumulators
+  int lb[kMaxDescScales];      // bits per accumulator limb (3 limbs per bin)
   int d, D, orient;
   double k36, k8, two_pi;  // PEAK_BINS / TWO_PI, ORIENTATION_BINS / TWO_PI, TWO_PI
   double theta[36], cos_t[36], sin_t[36];  // theta0_k and cos/sin(-theta0_k)
 };
 
-// Add `mag` to hist[bin] for the 32 samples of a chunk, per bin in lane
-// (= raster) order.  Lanes with the same bin form a group; its lowest lane
-// folds the members' magnitudes in sequentially.
-__device__ __forceinline__ void ordered_add(double* hist, double* stage, int bin, double mag, bool on) {
-  const int lane = threadIdx.x & 31;
-  on = on && mag != 0.0;  // +0.0 leaves a non-negative sum bit-identical
-  stage[lane] = mag;
-  const unsigned peers = __match_any_sync(0xffffffffu, on ? bin : (0x40000000 | lane));
-  __syncwarp();
-  if (on && (__ffs(peers) - 1) == lane) {
-    double h = hist[bin];
-    unsigned m = peers;
-    while (m) {
-      const int j = __ffs(m) - 1;
-      m &= m - 1;
-      h = __dadd_rn(h, stage[j]);
-    }
-    hist[bin] = h;
+// numpy mod(x, 2*pi) for -4*pi < x < 2*pi (descriptor.py:138, 215): fmod is
+// x + 2*pi exactly below -2*pi (Sterbenz), then + 2*pi when negative, and a
+// zero result is +0.0 -- identical to npy_divmod on this range.
+__device__ __forceinline__ double mod_two_pi(double x, double two_pi) {
+  if (x <= -two_pi) x = __dadd_rn(x, two_pi);
+  if (x < 0.0) {
+    x = __dadd_rn(x, two_pi);
+  } else if (x == 0.0) {
+    x = 0.0;
   }
-  __syncwarp();
+  return x;
 }
+
+// Histogram accumulation is exact fixed point: q = rint(mag * 2^e) split into
+// three limbs of `lb` bits, each summed with a native 32-bit shared atomic
+// (limb sums cannot overflow: nsamp * 2^lb < 2^32).  Integer sums are
+// order-independent, so the histograms are bit-reproducible (F6) without
+// serial chains; the scale keeps the quantum ~1e-15 of the largest sum.
+struct FxHist {
+  unsigned* h;  // [3][nbins]
+  int nbins, lb;
+  __device__ __forceinline__ void add(int bin, double mag, double fx) const {
+    if (mag == 0.0) return;
+    const unsigned long long q = __double2ull_rn(__dmul_rn(mag, fx));
+    const unsigned m = (1u << lb) - 1u;
+    atomicAdd(h + bin, (unsigned)(q & m));
+    atomicAdd(h + nbins + bin, (unsigned)((q >> lb) & m));
+    atomicAdd(h + 2 * nbins + bin, (unsigned)(q >> (2 * lb)));
+  }
+  __device__ __forceinline__ unsigned long long get(int bin) const {
+    return (unsigned long long)h[bin] + ((unsigned long long)h[nbins + bin] << lb) +
+           ((unsigned long long)h[2 * nbins + bin] << (2 * lb));
+  }
+  __device__ __forceinline__ void zero(int lane) const {
+    for (int q = lane; q < 3 * nbins; q += 32) h[q] = 0u;
+  }
+};
 
 template <class Img>
 __device__ __forceinline__ void axis_sample(const Img& im, int r, int c, double& a, double& b) {
@@ -58,172 +77,204 @@ __device__ __forceinline__ void axis_sample(const Img& im, int r, int c, double&
   b = __dsub_rn(im.at(r, c + 1), im.at(r, c - 1));
 }
 
-template <class Img>
-__global__ void __launch_bounds__(kWarps * 32) describe_kernel(Img img, int64_t img_stride, int B,
-                                                               const int32_t* __restrict__ kp_row,
-                                                               const int32_t* __restrict__ kp_col,
-                                                               const int32_t* __restrict__ kp_scale,
-                                                               int32_t default_scale,
-                                                               const int32_t* __restrict__ counts, int64_t cap,
-                                                               DescParams prm, float* __restrict__ out32,
-                                                               double* __restrict__ out64) {
-  extern __shared__ double smem[];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int D = prm.D;
-  double* hist = smem + wid * (D + 36 + 32);
-  double* hist36 = hist + D;
-  double* stage = hist36 + 36;
-  const int nr = img.nr, nc = img.nc;
+// One keypoint, one warp.  W / DD > 0 fix the region side / grid at compile
+// time (the common w in {8, 16, 32}, d = 4); 0 means runtime values.
+template <int W, int DD, class Img>
+__device__ __forceinline__ void describe_keypoint(const Img& im, int row, int col, int w_rt, int d_rt, double fx,
+                                                  int lb, const DescParams& prm, unsigned* hbase,
+                                                  float* __restrict__ o32, double* __restrict__ o64) {
+  const int lane = threadIdx.x & 31;
+  const int w = W > 0 ? W : w_rt;
+  const int d = DD > 0 ? DD : d_rt;
+  const int D = d * d * 8;
+  const int ws = w / d, nsamp = w * w;
+  const int nr = im.nr, nc = im.nc;
   const double two_pi = prm.two_pi;
+  // _fit_region (descriptor.py:129-130)
+  const int r0 = min(max(row - w / 2, 1), nr - 1 - w);
+  const int c0 = min(max(col - w / 2, 1), nc - 1 - w);
+  const FxHist h128{hbase, D, lb};
+  const FxHist h36{hbase + 3 * D, 36, lb};
+  h128.zero(lane);
+  h36.zero(lane);
+  __syncwarp();
+  if (prm.orient) {
+    // --- dominant orientation: 36-bin histogram of the axis region (:142-146)
+#pragma unroll 4
+    for (int s = lane; s < nsamp; s += 32) {
+      double a, b;
+      axis_sample(im, r0 + s / w, c0 + s % w, a, b);
+      const double ori = mod_two_pi(atan2(b, a), two_pi);
+      h36.add(min((int)__dmul_rn(ori, prm.k36), 35), hypot(a, b), fx);
+    }
+    __syncwarp();
+    // first argmax over the 36 bins
+    unsigned long long hv = h36.get(lane);
+    int hk = lane;
+    if (lane < 4 && h36.get(lane + 32) > hv) { hv = h36.get(lane + 32); hk = lane + 32; }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long v2 = __shfl_xor_sync(0xffffffffu, hv, o);
+      const int k2 = __shfl_xor_sync(0xffffffffu, hk, o);
+      if (v2 > hv || (v2 == hv && k2 < hk)) { hv = v2; hk = k2; }
+    }
+    const double theta0 = prm.theta[hk], ct = prm.cos_t[hk], st = prm.sin_t[hk];
+    // --- rotated grid centred on the (clamped) feature pixel (:237-240, 164-216)
+    const double half = (double)(w - 1) / 2.0;
+    const double cy = fmin(fmax((double)row, 1.0 + half), __dsub_rn((double)nr - 2.0, half));
+    const double cx = fmin(fmax((double)col, 1.0 + half), __dsub_rn((double)nc - 2.0, half));
+    // positions are coordinate-wise monotone in (u, v) -> extremes at the corners
+    double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
+#pragma unroll
+    for (int cv = 0; cv < 2; ++cv)
+#pragma unroll
+      for (int cu = 0; cu < 2; ++cu) {
+        const double u = __dsub_rn((double)(cu * (w - 1)), half);
+        const double v = __dsub_rn((double)(cv * (w - 1)), half);
+        const double x = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, u)), __dmul_rn(st, v));
+        const double y = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, u)), __dmul_rn(ct, v));
+        xmin = fmin(xmin, x); xmax = fmax(xmax, x);
+        ymin = fmin(ymin, y); ymax = fmax(ymax, y);
+      }
+    const int pr0 = max((int)floor(ymin), 1), pr1 = min((int)ceil(ymax), nr - 2);
+    const int pc0 = max((int)floor(xmin), 1), pc1 = min((int)ceil(xmax), nc - 2);
+    const int xcap = max(pc1 - pc0 - 1, 0), ycap = max(pr1 - pr0 - 1, 0);
+    const double xhi = (double)(nc - 2), yhi = (double)(nr - 2);
+#pragma unroll 2
+    for (int s = lane; s < nsamp; s += 32) {
+      const int iv = s / w, iu = s % w;
+      const double u = __dsub_rn((double)iu, half), v = __dsub_rn((double)iv, half);
+      const double x = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, u)), __dmul_rn(st, v));
+      const double y = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, u)), __dmul_rn(ct, v));
+      const bool inside = x >= 1.0 && x <= xhi && y >= 1.0 && y <= yhi;
+      const double lx = __dsub_rn(fmin(fmax(x, (double)pc0), (double)pc1), (double)pc0);
+      const double ly = __dsub_rn(fmin(fmax(y, (double)pr0), (double)pr1), (double)pr0);
+      const int x0 = min((int)floor(lx), xcap), y0 = min((int)floor(ly), ycap);
+      const double fxx = __dsub_rn(lx, (double)x0), fyy = __dsub_rn(ly, (double)y0);
+      const int x1 = min(x0 + 1, pc1 - pc0), y1 = min(y0 + 1, pr1 - pr0);
+      const int gy0 = pr0 + y0, gy1 = pr0 + y1, gx0 = pc0 + x0, gx1 = pc0 + x1;
+      double a00, b00, a01, b01, a10, b10, a11, b11;
+      axis_sample(im, gy0, gx0, a00, b00);
+      axis_sample(im, gy0, gx1, a01, b01);
+      axis_sample(im, gy1, gx0, a10, b10);
+      axis_sample(im, gy1, gx1, a11, b11);
+      const double sy = __dsub_rn(1.0, fyy), sx = __dsub_rn(1.0, fxx);
+      // left-to-right: f00*(1-fy)*(1-fx) + f01*(1-fy)*fx + f10*fy*(1-fx) + f11*fy*fx
+      const double as = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(a00, sy), sx), __dmul_rn(__dmul_rn(a01, sy), fxx)),
+                                            __dmul_rn(__dmul_rn(a10, fyy), sx)),
+                                  __dmul_rn(__dmul_rn(a11, fyy), fxx));
+      const double bs = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(b00, sy), sx), __dmul_rn(__dmul_rn(b01, sy), fxx)),
+                                            __dmul_rn(__dmul_rn(b10, fyy), sx)),
+                                  __dmul_rn(__dmul_rn(b11, fyy), fxx));
+      if (inside) {  // mag = hypot(as, bs) * valid: invalid samples add +0.0
+        const double ori = mod_two_pi(__dsub_rn(atan2(bs, as), theta0), two_pi);
+        const int ob = min((int)__dmul_rn(ori, prm.k8), 7);
+        h128.add(((iv / ws) * d + iu / ws) * 8 + ob, hypot(as, bs), fx);
+      }
+    }
+  } else {
+#pragma unroll 4
+    for (int s = lane; s < nsamp; s += 32) {
+      const int iv = s / w, iu = s % w;
+      double a, b;
+      axis_sample(im, r0 + iv, c0 + iu, a, b);
+      const double ori = mod_two_pi(atan2(b, a), two_pi);
+      const int ob = min((int)__dmul_rn(ori, prm.k8), 7);
+      h128.add(((iv / ws) * d + iu / ws) * 8 + ob, hypot(a, b), fx);
+    }
+  }
+  __syncwarp();
+  // --- L2 normalise, clamp at 0.2, renormalise (descriptor.py:250-255)
+  const double inv_fx = 1.0 / fx;  // exact: fx is a power of two
+  constexpr int kPer = DD > 0 ? (DD * DD * 8 + 31) / 32 : 16;
+  double vals[kPer];
+  double ss = 0.0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int q = lane + 32 * j;
+    vals[j] = q < D ? __dmul_rn((double)h128.get(q), inv_fx) : 0.0;
+    ss = __dadd_rn(ss, __dmul_rn(vals[j], vals[j]));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+  const double n1 = __dsqrt_rn(ss);
+  double n2 = 0.0;
+  if (n1 > 0.0) {
+    double ss2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      vals[j] = fmin(__ddiv_rn(vals[j], n1), 0.2);
+      ss2 = __dadd_rn(ss2, __dmul_rn(vals[j], vals[j]));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss2 = __dadd_rn(ss2, __shfl_xor_sync(0xffffffffu, ss2, o));
+    n2 = __dsqrt_rn(ss2);
+  }
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int q = lane + 32 * j;
+    if (q < D) {
+      const double v = n1 > 0.0 ? __ddiv_rn(vals[j], n2) : 0.0;
+      if (o32) o32[q] = __double2float_rn(v);
+      if (o64) o64[q] = v;
+    }
+  }
+  __syncwarp();
+}
+
+template <class Img>
+__global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64_t img_stride, int B,
+                                                                  const int32_t* __restrict__ kp_row,
+                                                                  const int32_t* __restrict__ kp_col,
+                                                                  const int32_t* __restrict__ kp_scale,
+                                                                  int32_t default_scale,
+                                                                  const int32_t* __restrict__ counts, int64_t cap,
+                                                                  DescParams prm, float* __restrict__ out32,
+                                                                  double* __restrict__ out64) {
+  extern __shared__ unsigned hsm[];
+  const int wid = threadIdx.x >> 5;
+  const int D = prm.D;
+  unsigned* hw = hsm + wid * 3 * (D + 36);
   const int64_t total = (int64_t)B * cap;
   for (int64_t g = (int64_t)blockIdx.x * kWarps + wid; g < total; g += (int64_t)gridDim.x * kWarps) {
     const int b = (int)(g / cap);
-    const int64_t i = g % cap;
+    const int64_t i = g - (int64_t)b * cap;
     if (counts && i >= counts[b]) continue;
     Img im = img;
     im.p = img.p + (int64_t)b * img_stride;
     const int row = kp_row[g], col = kp_col[g];
     const int scale = kp_scale ? kp_scale[g] : default_scale;
     int w = -1;
+    double fx = 0.0;
+    int lb = 0;
     for (int s = 0; s < prm.n_scales; ++s)
-      if (prm.scale[s] == scale) w = prm.w[s];
-    if (w < 0 || row < 0 || row >= nr || col < 0 || col >= nc) continue;  // validated by the caller
-    const int d = prm.d, ws = w / d, nsamp = w * w;
-    // _fit_region (descriptor.py:129-130)
-    const int r0 = min(max(row - w / 2, 1), nr - 1 - w);
-    const int c0 = min(max(col - w / 2, 1), nc - 1 - w);
-    for (int q = lane; q < D; q += 32) hist[q] = 0.0;
-    if (prm.orient) {
-      // --- dominant orientation: 36-bin histogram over the axis region (:142-146)
-      for (int q = lane; q < 36; q += 32) hist36[q] = 0.0;
-      __syncwarp();
-      for (int base = 0; base < nsamp; base += 32) {
-        const int s = base + lane;
-        const bool on = s < nsamp;
-        double mag = 0.0;
-        int bin = 0;
-        if (on) {
-          double a, bb;
-          axis_sample(im, r0 + s / w, c0 + s % w, a, bb);
-          mag = hypot(a, bb);
-          const double ori = np_mod_pos(atan2(bb, a), two_pi);
-          bin = min((int)__dmul_rn(ori, prm.k36), 35);
-        }
-        ordered_add(hist36, stage, bin, mag, on);
-      }
-      // first argmax over 36 bins
-      double hv = hist36[lane];
-      int hk = lane;
-      if (lane < 4 && hist36[lane + 32] > hv) { hv = hist36[lane + 32]; hk = lane + 32; }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double v2 = __shfl_xor_sync(0xffffffffu, hv, o);
-        const int k2 = __shfl_xor_sync(0xffffffffu, hk, o);
-        if (v2 > hv || (v2 == hv && k2 < hk)) { hv = v2; hk = k2; }
-      }
-      const double theta0 = prm.theta[hk], ct = prm.cos_t[hk], st = prm.sin_t[hk];
-      // --- rotated grid centred on the (clamped) feature pixel (:237-240, 164-216)
-      const double half = (double)(w - 1) / 2.0;
-      const double cy = fmin(fmax((double)row, 1.0 + half), __dsub_rn((double)nr - 2.0, half));
-      const double cx = fmin(fmax((double)col, 1.0 + half), __dsub_rn((double)nc - 2.0, half));
-      // sample positions are coordinate-wise monotone in (u, v), so the grid's
-      // extreme x / y lie at its corners
-      double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
-#pragma unroll
-      for (int cv = 0; cv < 2; ++cv)
-#pragma unroll
-        for (int cu = 0; cu < 2; ++cu) {
-          const double u = __dsub_rn((double)(cu * (w - 1)), half);
-          const double v = __dsub_rn((double)(cv * (w - 1)), half);
-          const double x = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, u)), __dmul_rn(st, v));
-          const double y = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, u)), __dmul_rn(ct, v));
-          xmin = fmin(xmin, x); xmax = fmax(xmax, x);
-          ymin = fmin(ymin, y); ymax = fmax(ymax, y);
-        }
-      const int pr0 = max((int)floor(ymin), 1), pr1 = min((int)ceil(ymax), nr - 2);
-      const int pc0 = max((int)floor(xmin), 1), pc1 = min((int)ceil(xmax), nc - 2);
-      const int xcap = max(pc1 - pc0 - 1, 0), ycap = max(pr1 - pr0 - 1, 0);
-      for (int base = 0; base < nsamp; base += 32) {
-        const int s = base + lane;
-        const bool on = s < nsamp;
-        double mag = 0.0;
-        int cell = 0;
-        if (on) {
-          const int iv = s / w, iu = s % w;
-          const double u = __dsub_rn((double)iu, half), v = __dsub_rn((double)iv, half);
-          const double x = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, u)), __dmul_rn(st, v));
-          const double y = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, u)), __dmul_rn(ct, v));
-          const bool inside = x >= 1.0 && x <= (double)(nc - 2) && y >= 1.0 && y <= (double)(nr - 2);
-          const double lx = __dsub_rn(fmin(fmax(x, (double)pc0), (double)pc1), (double)pc0);
-          const double ly = __dsub_rn(fmin(fmax(y, (double)pr0), (double)pr1), (double)pr0);
-          const int x0 = min((int)floor(lx), xcap), y0 = min((int)floor(ly), ycap);
-          const double fx = __dsub_rn(lx, (double)x0), fy = __dsub_rn(ly, (double)y0);
-          const int x1 = min(x0 + 1, pc1 - pc0), y1 = min(y0 + 1, pr1 - pr0);
-          const int gy0 = pr0 + y0, gy1 = pr0 + y1, gx0 = pc0 + x0, gx1 = pc0 + x1;
-          double a00, b00, a01, b01, a10, b10, a11, b11;
-          axis_sample(im, gy0, gx0, a00, b00);
-          axis_sample(im, gy0, gx1, a01, b01);
-          axis_sample(im, gy1, gx0, a10, b10);
-          axis_sample(im, gy1, gx1, a11, b11);
-          const double sy = __dsub_rn(1.0, fy), sx = __dsub_rn(1.0, fx);
-          // left-to-right: f00*(1-fy)*(1-fx) + f01*(1-fy)*fx + f10*fy*(1-fx) + f11*fy*fx
-          const double as = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(a00, sy), sx), __dmul_rn(__dmul_rn(a01, sy), fx)),
-                                                __dmul_rn(__dmul_rn(a10, fy), sx)),
-                                      __dmul_rn(__dmul_rn(a11, fy), fx));
-          const double bs = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(b00, sy), sx), __dmul_rn(__dmul_rn(b01, sy), fx)),
-                                                __dmul_rn(__dmul_rn(b10, fy), sx)),
-                                      __dmul_rn(__dmul_rn(b11, fy), fx));
-          mag = __dmul_rn(hypot(as, bs), inside ? 1.0 : 0.0);
-          const double ori = np_mod_pos(__dsub_rn(atan2(bs, as), theta0), two_pi);
-          const int ob = min((int)__dmul_rn(ori, prm.k8), 7);
-          cell = ((iv / ws) * d + iu / ws) * 8 + ob;
-        }
-        ordered_add(hist, stage, cell, mag, on);
-      }
+      if (prm.scale[s] == scale) { w = prm.w[s]; fx = prm.fx[s]; lb = prm.lb[s]; }
+    if (w < 0 || row < 0 || row >= im.nr || col < 0 || col >= im.nc) continue;  // validated by the caller
+    float* o32 = out32 ? out32 + g * D : nullptr;
+    double* o64 = out64 ? out64 + g * D : nullptr;
+    if (prm.d == 4 && w == 8) {
+      describe_keypoint<8, 4>(im, row, col, w, 4, fx, lb, prm, hw, o32, o64);
+    } else if (prm.d == 4 && w == 16) {
+      describe_keypoint<16, 4>(im, row, col, w, 4, fx, lb, prm, hw, o32, o64);
+    } else if (prm.d == 4 && w == 32) {
+      describe_keypoint<32, 4>(im, row, col, w, 4, fx, lb, prm, hw, o32, o64);
     } else {
-      __syncwarp();
-      for (int base = 0; base < nsamp; base += 32) {
-        const int s = base + lane;
-        const bool on = s < nsamp;
-        double mag = 0.0;
-        int cell = 0;
-        if (on) {
-          const int iv = s / w, iu = s % w;
-          double a, bb;
-          axis_sample(im, r0 + iv, c0 + iu, a, bb);
-          mag = hypot(a, bb);
-          const double ori = np_mod_pos(atan2(bb, a), two_pi);
-          const int ob = min((int)__dmul_rn(ori, prm.k8), 7);
-          cell = ((iv / ws) * d + iu / ws) * 8 + ob;
-        }
-        ordered_add(hist, stage, cell, mag, on);
-      }
+      describe_keypoint<0, 0>(im, row, col, w, prm.d, fx, lb, prm, hw, o32, o64);
     }
-    // --- L2 normalise, clamp at 0.2, renormalise (descriptor.py:250-255)
-    double ss = 0.0;
-    for (int q = lane; q < D; q += 32) ss = __dadd_rn(ss, __dmul_rn(hist[q], hist[q]));
-#pragma unroll
-    for (int o = 16; o; o >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
-    const double n1 = __dsqrt_rn(ss);
-    double scale1 = 0.0;
-    if (n1 > 0.0) {
-      double ss2 = 0.0;
-      for (int q = lane; q < D; q += 32) {
-        const double v = fmin(__ddiv_rn(hist[q], n1), 0.2);
-        hist[q] = v;
-        ss2 = __dadd_rn(ss2, __dmul_rn(v, v));
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) ss2 = __dadd_rn(ss2, __shfl_xor_sync(0xffffffffu, ss2, o));
-      scale1 = __dsqrt_rn(ss2);
-    }
-    for (int q = lane; q < D; q += 32) {
-      const double v = n1 > 0.0 ? __ddiv_rn(hist[q], scale1) : 0.0;
-      if (out32) out32[g * D + q] = __double2float_rn(v);
-      if (out64) out64[g * D + q] = v;
-    }
-    __syncwarp();
   }
+}
+
+__global__ void max_abs_kernel(const double* __restrict__ p, int B, int nr, int nc, int64_t pitch, int64_t stride,
+                               unsigned long long* __restrict__ out) {
+  double m = 0.0;
+  const int64_t total = (int64_t)B * nr * nc;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = t / ((int64_t)nr * nc), rem = t % ((int64_t)nr * nc);
+    const double v = fabs(p[b * stride + (rem / nc) * pitch + rem % nc]);
+    m = v > m ? v : m;  // NaN ignored
+  }
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
 // region_size + _fit_region width on the host, with the host libm exactly as
@@ -259,12 +310,42 @@ extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, in
   PS_REQUIRE(n_scale_set >= 1 && n_scale_set <= kMaxDescScales, PS_ERR_ARGUMENT, "1..%d scales supported",
              kMaxDescScales);
   PS_REQUIRE(img->nr >= 3 && img->nc >= 3, PS_ERR_VALUE, "image too small");
+  PS_REQUIRE((int64_t)img->nr * img->nc < (int64_t)INT32_MAX, PS_ERR_ARGUMENT, "image too large (nr*nc >= 2^31)");
+  cudaStream_t s = (cudaStream_t)stream;
+  // bound on |P| for the fixed-point histogram scale
+  double pmax = 255.0 + 0.05 * 255.0;
+  if (img->pixel_type != PS_PIXELS_U8) {
+    unsigned long long* dmax = nullptr;
+    cudaMallocAsync(&dmax, sizeof(unsigned long long), s);
+    cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), s);
+    max_abs_kernel<<<148 * 4, 256, 0, s>>>((const double*)img->data, img->batch, img->nr, img->nc, img->row_pitch,
+                                           img->batch > 1 ? img->image_stride : 0, dmax);
+    PS_LAUNCHED("max_abs_kernel");
+    unsigned long long hbits = 0;
+    cudaMemcpyAsync(&hbits, dmax, sizeof(hbits), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(dmax, s);
+    cudaStreamSynchronize(s);
+    int st = check_cuda("max_abs");
+    if (st) return st;
+    double m;
+    memcpy(&m, &hbits, sizeof(m));
+    pmax = m + (img->pixel_type == PS_PIXELS_F64_RAW ? 0.05 * 255.0 : 0.0);
+    PS_REQUIRE(std::isfinite(pmax), PS_ERR_VALUE, "pixel values must be finite");
+    if (pmax < 1e-300) pmax = 1e-300;
+  }
   DescParams prm{};
   prm.n_scales = n_scale_set;
-  for (int s = 0; s < n_scale_set; ++s) {
-    prm.scale[s] = host_scale_set[s];
-    int st = region_width(host_scale_set[s], beta0, d, l_max, img->nr, img->nc, &prm.w[s]);
+  for (int si = 0; si < n_scale_set; ++si) {
+    prm.scale[si] = host_scale_set[si];
+    int st = region_width(host_scale_set[si], beta0, d, l_max, img->nr, img->nc, &prm.w[si]);
     if (st) return st;
+    // limb width: nsamp * 2^lb < 2^32; scale: every bin sum (<= nsamp *
+    // 2*sqrt(2)*pmax) stays below 2^(3*lb), i.e. fits the three limbs
+    const double nsamp = (double)prm.w[si] * prm.w[si];
+    const int lb = std::min(21, 32 - (int)std::ceil(std::log2(nsamp + 1.0)));
+    PS_REQUIRE(lb >= 8, PS_ERR_ARGUMENT, "descriptor region %d too large", prm.w[si]);
+    prm.lb[si] = lb;
+    prm.fx[si] = std::ldexp(1.0, (int)std::floor(3.0 * lb - std::log2(nsamp * 2.9 * pmax)));
   }
   const double two_pi = 2.0 * M_PI;  // descriptor.py:31
   prm.d = d;
@@ -281,10 +362,9 @@ extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, in
   }
   const int64_t total = (int64_t)img->batch * kp->cap;
   if (total == 0) return PS_OK;
-  cudaStream_t s = (cudaStream_t)stream;
-  const size_t shmem = (size_t)kWarps * (prm.D + 36 + 32) * sizeof(double);
+  const size_t shmem = (size_t)kWarps * 3 * (prm.D + 36) * sizeof(unsigned);
   int64_t blocks = (total + kWarps - 1) / kWarps;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > 148 * 8) blocks = 148 * 8;
   if (img->pixel_type == PS_PIXELS_U8) {
     RampU8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
     describe_kernel<<<(unsigned)blocks, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,

@@ -62,14 +62,21 @@ struct Arena {
 // (reference imaging.py:146-149): fl(I + fl(k * alpha)), k = r*nc + c + 1.
 // Explicit _rn intrinsics keep nvcc from contracting into an FMA.
 // ---------------------------------------------------------------------------
+// exact int -> double for 0 <= x < 2^32 on the FP64 pipe (no I2F):
+// the bits 0x43300000:x are 2^52 + x, and subtracting 2^52 is exact.
+__device__ __forceinline__ double u32_to_f64(unsigned x) {
+  return __dsub_rn(__hiloint2double(0x43300000, (int)x), 4503599627370496.0);
+}
+
+// (callers guarantee nr * nc < 2^31, so the flat index fits in 32 bits)
 struct RampU8 {
   const uint8_t* p;
   int64_t pitch;
   int32_t nr, nc;
   double alpha;
   __device__ __forceinline__ double at(int r, int c) const {
-    double k = (double)((int64_t)r * nc + c + 1);
-    return __dadd_rn((double)p[(int64_t)r * pitch + c], __dmul_rn(k, alpha));
+    const double k = u32_to_f64((unsigned)(r * nc + c + 1));
+    return __dadd_rn(u32_to_f64(p[(int64_t)r * pitch + c]), __dmul_rn(k, alpha));
   }
 };
 
@@ -97,7 +104,7 @@ struct RampF64Raw {
   int32_t nr, nc;
   double alpha;
   __device__ __forceinline__ double at(int r, int c) const {
-    double k = (double)((int64_t)r * nc + c + 1);
+    const double k = u32_to_f64((unsigned)(r * nc + c + 1));
     return __dadd_rn(p[(int64_t)r * pitch + c], __dmul_rn(k, alpha));
   }
 };
