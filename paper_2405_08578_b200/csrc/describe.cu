@@ -79,10 +79,24 @@ __device__ __forceinline__ void axis_sample(const Img& im, int r, int c, double&
 
 // One keypoint, one warp.  W / DD > 0 fix the region side / grid at compile
 // time (the common w in {8, 16, 32}, d = 4); 0 means runtime values.
+// Staging capacity (doubles per warp) for compile-time W: the P box of the
+// rotated patch plus its two gradient fields.  The rotated grid spans at most
+// (W-1)*sqrt(2) in x and y, so pr1 - pr0 <= ceil((W-1)*sqrt(2)) + 1.
+template <int W>
+struct Stage {
+  static constexpr int kSpan = W > 0 ? (int)((W - 1) * 1.41422) + 3 : 0;  // >= pr1 - pr0 + 1
+  static constexpr int kP = (kSpan + 2) * (kSpan + 2);
+  static constexpr int kF = kSpan * kSpan;
+  static constexpr int kTotal = W > 0 ? kP + 2 * kF : 0;
+};
+constexpr int kStageW = 8;  // region side served from shared memory
+constexpr int kStageDoubles = Stage<kStageW>::kTotal;
+
 template <int W, int DD, class Img>
 __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int col, int w_rt, int d_rt, double fx,
-                                                  int lb, const DescParams& prm, unsigned* hbase,
+                                                  int lb, const DescParams& prm, unsigned* hbase, double* stage,
                                                   float* __restrict__ o32, double* __restrict__ o64) {
+  constexpr bool kStaged = W == kStageW;
   const int lane = threadIdx.x & 31;
   const int w = W > 0 ? W : w_rt;
   const int d = DD > 0 ? DD : d_rt;
@@ -98,12 +112,27 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
   h128.zero(lane);
   h36.zero(lane);
   __syncwarp();
+  if (kStaged) {  // P over rows r0-1..r0+w, cols c0-1..c0+w
+    constexpr int E = W + 2;
+#pragma unroll
+    for (int e = lane; e < E * E; e += 32) stage[e] = im.at(r0 - 1 + e / E, c0 - 1 + e % E);
+    __syncwarp();
+  }
+  auto axis_ab = [&](int iv, int iu, double& a, double& b) {
+    if (kStaged) {
+      constexpr int E = W + 2;
+      a = __dsub_rn(stage[(iv + 2) * E + iu + 1], stage[iv * E + iu + 1]);
+      b = __dsub_rn(stage[(iv + 1) * E + iu + 2], stage[(iv + 1) * E + iu]);
+    } else {
+      axis_sample(im, r0 + iv, c0 + iu, a, b);
+    }
+  };
   if (prm.orient) {
     // --- dominant orientation: 36-bin histogram of the axis region (:142-146)
 #pragma unroll 4
     for (int s = lane; s < nsamp; s += 32) {
       double a, b;
-      axis_sample(im, r0 + s / w, c0 + s % w, a, b);
+      axis_ab(s / w, s % w, a, b);
       const double ori = mod_two_pi(atan2(b, a), two_pi);
       h36.add(min((int)__dmul_rn(ori, prm.k36), 35), hypot(a, b), fx);
     }
@@ -140,6 +169,21 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
     const int pc0 = max((int)floor(xmin), 1), pc1 = min((int)ceil(xmax), nc - 2);
     const int xcap = max(pc1 - pc0 - 1, 0), ycap = max(pr1 - pr0 - 1, 0);
     const double xhi = (double)(nc - 2), yhi = (double)(nr - 2);
+    const int FR = pr1 - pr0 + 1, FC = pc1 - pc0 + 1;  // field patch (descriptor.py:192-193)
+    double* fa = stage + Stage<W>::kP;
+    double* fb = fa + Stage<W>::kF;
+    if (kStaged) {
+      __syncwarp();
+      const int PC = FC + 2, PR = FR + 2;
+      for (int e = lane; e < PR * PC; e += 32) stage[e] = im.at(pr0 - 1 + e / PC, pc0 - 1 + e % PC);
+      __syncwarp();
+      for (int e = lane; e < FR * FC; e += 32) {
+        const int y = e / FC, x = e % FC;
+        fa[e] = __dsub_rn(stage[(y + 2) * PC + x + 1], stage[y * PC + x + 1]);
+        fb[e] = __dsub_rn(stage[(y + 1) * PC + x + 2], stage[(y + 1) * PC + x]);
+      }
+      __syncwarp();
+    }
 #pragma unroll 2
     for (int s = lane; s < nsamp; s += 32) {
       const int iv = s / w, iu = s % w;
@@ -152,12 +196,19 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
       const int x0 = min((int)floor(lx), xcap), y0 = min((int)floor(ly), ycap);
       const double fxx = __dsub_rn(lx, (double)x0), fyy = __dsub_rn(ly, (double)y0);
       const int x1 = min(x0 + 1, pc1 - pc0), y1 = min(y0 + 1, pr1 - pr0);
-      const int gy0 = pr0 + y0, gy1 = pr0 + y1, gx0 = pc0 + x0, gx1 = pc0 + x1;
       double a00, b00, a01, b01, a10, b10, a11, b11;
-      axis_sample(im, gy0, gx0, a00, b00);
-      axis_sample(im, gy0, gx1, a01, b01);
-      axis_sample(im, gy1, gx0, a10, b10);
-      axis_sample(im, gy1, gx1, a11, b11);
+      if (kStaged) {
+        a00 = fa[y0 * FC + x0]; b00 = fb[y0 * FC + x0];
+        a01 = fa[y0 * FC + x1]; b01 = fb[y0 * FC + x1];
+        a10 = fa[y1 * FC + x0]; b10 = fb[y1 * FC + x0];
+        a11 = fa[y1 * FC + x1]; b11 = fb[y1 * FC + x1];
+      } else {
+        const int gy0 = pr0 + y0, gy1 = pr0 + y1, gx0 = pc0 + x0, gx1 = pc0 + x1;
+        axis_sample(im, gy0, gx0, a00, b00);
+        axis_sample(im, gy0, gx1, a01, b01);
+        axis_sample(im, gy1, gx0, a10, b10);
+        axis_sample(im, gy1, gx1, a11, b11);
+      }
       const double sy = __dsub_rn(1.0, fyy), sx = __dsub_rn(1.0, fxx);
       // left-to-right: f00*(1-fy)*(1-fx) + f01*(1-fy)*fx + f10*fy*(1-fx) + f11*fy*fx
       const double as = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(a00, sy), sx), __dmul_rn(__dmul_rn(a01, sy), fxx)),
@@ -177,7 +228,7 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
     for (int s = lane; s < nsamp; s += 32) {
       const int iv = s / w, iu = s % w;
       double a, b;
-      axis_sample(im, r0 + iv, c0 + iu, a, b);
+      axis_ab(iv, iu, a, b);
       const double ori = mod_two_pi(atan2(b, a), two_pi);
       const int ob = min((int)__dmul_rn(ori, prm.k8), 7);
       h128.add(((iv / ws) * d + iu / ws) * 8 + ob, hypot(a, b), fx);
@@ -200,21 +251,22 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
   const double n1 = __dsqrt_rn(ss);
   double n2 = 0.0;
   if (n1 > 0.0) {
+    const double r1 = __drcp_rn(n1);
     double ss2 = 0.0;
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
-      vals[j] = fmin(__ddiv_rn(vals[j], n1), 0.2);
+      vals[j] = fmin(__dmul_rn(vals[j], r1), 0.2);
       ss2 = __dadd_rn(ss2, __dmul_rn(vals[j], vals[j]));
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) ss2 = __dadd_rn(ss2, __shfl_xor_sync(0xffffffffu, ss2, o));
-    n2 = __dsqrt_rn(ss2);
+    n2 = __drcp_rn(__dsqrt_rn(ss2));
   }
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
     const int q = lane + 32 * j;
     if (q < D) {
-      const double v = n1 > 0.0 ? __ddiv_rn(vals[j], n2) : 0.0;
+      const double v = n1 > 0.0 ? __dmul_rn(vals[j], n2) : 0.0;
       if (o32) o32[q] = __double2float_rn(v);
       if (o64) o64[q] = v;
     }
@@ -231,10 +283,11 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
                                                                   const int32_t* __restrict__ counts, int64_t cap,
                                                                   DescParams prm, float* __restrict__ out32,
                                                                   double* __restrict__ out64) {
-  extern __shared__ unsigned hsm[];
+  extern __shared__ double dsm[];
   const int wid = threadIdx.x >> 5;
   const int D = prm.D;
-  unsigned* hw = hsm + wid * 3 * (D + 36);
+  double* stage = dsm + wid * kStageDoubles;
+  unsigned* hw = reinterpret_cast<unsigned*>(dsm + kWarps * kStageDoubles) + wid * 3 * (D + 36);
   const int64_t total = (int64_t)B * cap;
   for (int64_t g = (int64_t)blockIdx.x * kWarps + wid; g < total; g += (int64_t)gridDim.x * kWarps) {
     const int b = (int)(g / cap);
@@ -253,13 +306,13 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
     float* o32 = out32 ? out32 + g * D : nullptr;
     double* o64 = out64 ? out64 + g * D : nullptr;
     if (prm.d == 4 && w == 8) {
-      describe_keypoint<8, 4>(im, row, col, w, 4, fx, lb, prm, hw, o32, o64);
+      describe_keypoint<8, 4>(im, row, col, w, 4, fx, lb, prm, hw, stage, o32, o64);
     } else if (prm.d == 4 && w == 16) {
-      describe_keypoint<16, 4>(im, row, col, w, 4, fx, lb, prm, hw, o32, o64);
+      describe_keypoint<16, 4>(im, row, col, w, 4, fx, lb, prm, hw, stage, o32, o64);
     } else if (prm.d == 4 && w == 32) {
-      describe_keypoint<32, 4>(im, row, col, w, 4, fx, lb, prm, hw, o32, o64);
+      describe_keypoint<32, 4>(im, row, col, w, 4, fx, lb, prm, hw, stage, o32, o64);
     } else {
-      describe_keypoint<0, 0>(im, row, col, w, prm.d, fx, lb, prm, hw, o32, o64);
+      describe_keypoint<0, 0>(im, row, col, w, prm.d, fx, lb, prm, hw, stage, o32, o64);
     }
   }
 }
@@ -362,9 +415,12 @@ extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, in
   }
   const int64_t total = (int64_t)img->batch * kp->cap;
   if (total == 0) return PS_OK;
-  const size_t shmem = (size_t)kWarps * 3 * (prm.D + 36) * sizeof(unsigned);
+  const size_t shmem = (size_t)kWarps * (kStageDoubles * sizeof(double) + 3 * (prm.D + 36) * sizeof(unsigned));
   int64_t blocks = (total + kWarps - 1) / kWarps;
   if (blocks > 148 * 8) blocks = 148 * 8;
+  cudaFuncSetAttribute(describe_kernel<RampU8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
+  cudaFuncSetAttribute(describe_kernel<RampF64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
+  cudaFuncSetAttribute(describe_kernel<RampF64Raw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
   if (img->pixel_type == PS_PIXELS_U8) {
     RampU8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
     describe_kernel<<<(unsigned)blocks, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,
