@@ -11,6 +11,7 @@
 // ~1 ulp), hence the 1e-4 relative parity bar of contract P2.
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "ps_common.cuh"
@@ -30,6 +31,8 @@ struct DescParams {
   int d, D, orient;
   double k36, k8, two_pi;  // PEAK_BINS / TWO_PI, ORIENTATION_BINS / TWO_PI, TWO_PI
   double theta[36], cos_t[36], sin_t[36];  // theta0_k and cos/sin(-theta0_k)
+  double cb36[37], sb36[37];                // cos/sin of the 36-bin edges m*2pi/36
+  double c8[9], s8[9];                      // cos/sin of m*pi/4 (8-bin edges relative to theta0)
 };
 
 // numpy mod(x, 2*pi) for -4*pi < x < 2*pi (descriptor.py:138, 215): fmod is
@@ -61,6 +64,14 @@ struct FxHist {
     atomicAdd(h + nbins + bin, (unsigned)((q >> lb) & m));
     atomicAdd(h + 2 * nbins + bin, (unsigned)(q >> (2 * lb)));
   }
+  __device__ __forceinline__ void add_f(int bin, float mag, float fx) const {
+    if (mag == 0.0f) return;
+    const unsigned long long q = __float2ull_rn(mag * fx);
+    const unsigned m = (1u << lb) - 1u;
+    atomicAdd(h + bin, (unsigned)(q & m));
+    atomicAdd(h + nbins + bin, (unsigned)((q >> lb) & m));
+    atomicAdd(h + 2 * nbins + bin, (unsigned)(q >> (2 * lb)));
+  }
   __device__ __forceinline__ unsigned long long get(int bin) const {
     return (unsigned long long)h[bin] + ((unsigned long long)h[nbins + bin] << lb) +
            ((unsigned long long)h[2 * nbins + bin] << (2 * lb));
@@ -85,18 +96,60 @@ __device__ __forceinline__ void axis_sample(const Img& im, int r, int c, double&
 template <int W>
 struct Stage {
   static constexpr int kSpan = W > 0 ? (int)((W - 1) * 1.41422) + 3 : 0;  // >= pr1 - pr0 + 1
-  static constexpr int kP = (kSpan + 2) * (kSpan + 2);
-  static constexpr int kF = kSpan * kSpan;
+  static constexpr int kStride = kSpan + 2 > 16 ? kSpan + 2 : 16;           // row stride (>= kSpan + 2)
+  static constexpr int kP = (kSpan + 2) * kStride;
+  static constexpr int kF = kSpan * kStride;
   static constexpr int kTotal = W > 0 ? kP + 2 * kF : 0;
+  static_assert(W <= 0 || W + 2 <= kStride, "stage stride too small");
 };
 constexpr int kStageW = 8;  // region side served from shared memory
 constexpr int kStageDoubles = Stage<kStageW>::kTotal;
 
-template <int W, int DD, class Img>
+// ---- float32 screening of the discrete decisions -------------------------------
+// On 8-bit rasters the gradients (exact float64 differences of the ramped
+// raster) are bounded and well scaled, so the orientation bin of a sample is
+// first taken from float32 atan2 and accepted only when the float32 bin
+// coordinate lies at least kBinMargin from a bin edge (its error is < 2e-5
+// bins: f32 rounding of the inputs, atan2f, the theta0 shift, the scaling);
+// otherwise the float64 path decides.  Magnitudes enter the histograms in
+// float32 (relative error < 3e-7, inside contract P2's 1e-4), and the argmax
+// of the 36-bin histogram is accepted only when the top bin leads the next by
+// more than the accumulated error, else that histogram is rebuilt in float64.
+constexpr float kBinMargin = 1e-4f;
+
+__device__ __forceinline__ bool certified_bin(float x, int nbins, int& bin) {
+  const float f = floorf(x);
+  const float fr = x - f;
+  bin = min(max((int)f, 0), nbins - 1);
+  return fr > kBinMargin && fr < 1.0f - kBinMargin && x > 0.0f && x < (float)nbins;
+}
+
+// Bin of a float64 gradient (a, b) whose float32 bin coordinate fell within
+// kBinMargin of edge m (angle of the edge: cos ce, sin se).  The exact angle
+// lies more than 1e-12 rad from the edge unless |b ce - a se| is tiny, and
+// then the reference's float64 atan2 / mod / trunc cannot straddle the edge,
+// so the side of the edge decides the bin; -1 asks for the full float64 path.
+__device__ __forceinline__ int side_bin(double a, double b, double ce, double se, int m, int nbins) {
+  const double sd = __dsub_rn(__dmul_rn(b, ce), __dmul_rn(a, se));
+  const double thr = 1e-12 * (fabs(a) + fabs(b));
+  if (sd > thr) return m == nbins ? 0 : m;
+  if (sd < -thr) return m == 0 ? nbins - 1 : m - 1;
+  return -1;
+}
+
+__device__ __forceinline__ float wrap_two_pi_f(float x) {
+  const float tp = 6.283185307179586f;
+  if (x < 0.0f) x += tp;
+  if (x < 0.0f) x += tp;
+  return x;
+}
+
+template <int W, int DD, bool FAST, class Img>
 __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int col, int w_rt, int d_rt, double fx,
                                                   int lb, const DescParams& prm, unsigned* hbase, double* stage,
                                                   float* __restrict__ o32, double* __restrict__ o64) {
   constexpr bool kStaged = W == kStageW;
+  constexpr int SP = Stage<W>::kStride;
   const int lane = threadIdx.x & 31;
   const int w = W > 0 ? W : w_rt;
   const int d = DD > 0 ? DD : d_rt;
@@ -104,6 +157,7 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
   const int ws = w / d, nsamp = w * w;
   const int nr = im.nr, nc = im.nc;
   const double two_pi = prm.two_pi;
+  const float fxf = (float)fx;  // a power of two, exact in float32
   // _fit_region (descriptor.py:129-130)
   const int r0 = min(max(row - w / 2, 1), nr - 1 - w);
   const int c0 = min(max(col - w / 2, 1), nc - 1 - w);
@@ -111,33 +165,67 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
   const FxHist h36{hbase + 3 * D, 36, lb};
   h128.zero(lane);
   h36.zero(lane);
-  __syncwarp();
+  const int sx_ = lane & 15, sy_ = lane >> 4;  // staging: 2 rows x 16 columns per step
   if (kStaged) {  // P over rows r0-1..r0+w, cols c0-1..c0+w
     constexpr int E = W + 2;
 #pragma unroll
-    for (int e = lane; e < E * E; e += 32) stage[e] = im.at(r0 - 1 + e / E, c0 - 1 + e % E);
-    __syncwarp();
+    for (int y = sy_; y < E; y += 2)
+      if (sx_ < E) stage[y * SP + sx_] = im.at(r0 - 1 + y, c0 - 1 + sx_);
   }
+  __syncwarp();
   auto axis_ab = [&](int iv, int iu, double& a, double& b) {
     if (kStaged) {
-      constexpr int E = W + 2;
-      a = __dsub_rn(stage[(iv + 2) * E + iu + 1], stage[iv * E + iu + 1]);
-      b = __dsub_rn(stage[(iv + 1) * E + iu + 2], stage[(iv + 1) * E + iu]);
+      a = __dsub_rn(stage[(iv + 2) * SP + iu + 1], stage[iv * SP + iu + 1]);
+      b = __dsub_rn(stage[(iv + 1) * SP + iu + 2], stage[(iv + 1) * SP + iu]);
     } else {
       axis_sample(im, r0 + iv, c0 + iu, a, b);
     }
   };
+  // bin of a float64 gradient (reference arithmetic), optionally shifted by -theta0
+  auto bin64 = [&](double a, double b, double shift, double k, int nbins) {
+    const double ori = mod_two_pi(__dsub_rn(atan2(b, a), shift), two_pi);
+    return min((int)__dmul_rn(ori, k), nbins - 1);
+  };
+  // 36-bin orientation of an axis sample: float32 screen, edge side test, float64
+  auto bin36 = [&](double a, double b, float af, float bf) {
+    const float x = wrap_two_pi_f(atan2f(bf, af)) * 5.729577951308232f;
+    int bin;
+    if (certified_bin(x, 36, bin)) return bin;
+    const int m = min(max(__float2int_rn(x), 0), 36);
+    bin = side_bin(a, b, prm.cb36[m], prm.sb36[m], m, 36);
+    return bin >= 0 ? bin : bin64(a, b, 0.0, prm.k36, 36);
+  };
   if (prm.orient) {
     // --- dominant orientation: 36-bin histogram of the axis region (:142-146)
+    bool exact = !FAST;
+    for (;;) {
 #pragma unroll 4
-    for (int s = lane; s < nsamp; s += 32) {
-      double a, b;
-      axis_ab(s / w, s % w, a, b);
-      const double ori = mod_two_pi(atan2(b, a), two_pi);
-      h36.add(min((int)__dmul_rn(ori, prm.k36), 35), hypot(a, b), fx);
+      for (int s = lane; s < nsamp; s += 32) {
+        double a, b;
+        axis_ab(s / w, s % w, a, b);
+        if (exact) {
+          h36.add(bin64(a, b, 0.0, prm.k36, 36), hypot(a, b), fx);
+        } else {
+          const float af = (float)a, bf = (float)b;
+          h36.add_f(bin36(a, b, af, bf), __fsqrt_rn(__fmaf_rn(af, af, bf * bf)), fxf);
+        }
+      }
+      __syncwarp();
+      if (exact) break;
+      // float32 magnitudes: accept the argmax only with a clear lead.  Keys are
+      // the float32 bin sums with the low 6 mantissa bits replaced by 63 - bin.
+      const float f1 = (float)h36.get(lane), f2 = lane < 4 ? (float)h36.get(lane + 32) : 0.0f;
+      const unsigned k1 = (__float_as_uint(f1) & ~63u) | (63u - lane);
+      const unsigned k2 = lane < 4 ? ((__float_as_uint(f2) & ~63u) | (31u - lane)) : 0u;
+      const unsigned top = __reduce_max_sync(0xffffffffu, max(k1, k2));
+      const unsigned sec = __reduce_max_sync(0xffffffffu, max(k1 == top ? 0u : k1, k2 == top ? 0u : k2));
+      const float tv = __uint_as_float(top & ~63u), sv = __uint_as_float(sec & ~63u);
+      if (sv < tv * 0.99994f) break;  // lead > 6e-5 relative: float64 sums agree
+      exact = true;  // near-tie: rebuild this histogram in float64 (warp-uniform)
+      h36.zero(lane);
+      __syncwarp();
     }
-    __syncwarp();
-    // first argmax over the 36 bins
+    // first argmax over the 36 bins (exact integer sums)
     unsigned long long hv = h36.get(lane);
     int hk = lane;
     if (lane < 4 && h36.get(lane + 32) > hv) { hv = h36.get(lane + 32); hk = lane + 32; }
@@ -148,6 +236,7 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
       if (v2 > hv || (v2 == hv && k2 < hk)) { hv = v2; hk = k2; }
     }
     const double theta0 = prm.theta[hk], ct = prm.cos_t[hk], st = prm.sin_t[hk];
+    const float theta0f = (float)theta0;
     // --- rotated grid centred on the (clamped) feature pixel (:237-240, 164-216)
     const double half = (double)(w - 1) / 2.0;
     const double cy = fmin(fmax((double)row, 1.0 + half), __dsub_rn((double)nr - 2.0, half));
@@ -175,15 +264,18 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
     if (kStaged) {
       __syncwarp();
       const int PC = FC + 2, PR = FR + 2;
-      for (int e = lane; e < PR * PC; e += 32) stage[e] = im.at(pr0 - 1 + e / PC, pc0 - 1 + e % PC);
+      for (int y = sy_; y < PR; y += 2)
+        if (sx_ < PC) stage[y * SP + sx_] = im.at(pr0 - 1 + y, pc0 - 1 + sx_);
       __syncwarp();
-      for (int e = lane; e < FR * FC; e += 32) {
-        const int y = e / FC, x = e % FC;
-        fa[e] = __dsub_rn(stage[(y + 2) * PC + x + 1], stage[y * PC + x + 1]);
-        fb[e] = __dsub_rn(stage[(y + 1) * PC + x + 2], stage[(y + 1) * PC + x]);
-      }
+      for (int y = sy_; y < FR; y += 2)
+        if (sx_ < FC) {
+          fa[y * SP + sx_] = __dsub_rn(stage[(y + 2) * SP + sx_ + 1], stage[y * SP + sx_ + 1]);
+          fb[y * SP + sx_] = __dsub_rn(stage[(y + 1) * SP + sx_ + 2], stage[(y + 1) * SP + sx_]);
+        }
       __syncwarp();
     }
+    // 8-bin edges m*pi/4 + theta0 as (cos, sin) for the side test
+    const double c0t = ct, s0t = -st;  // cos(theta0), sin(theta0)
 #pragma unroll 2
     for (int s = lane; s < nsamp; s += 32) {
       const int iv = s / w, iu = s % w;
@@ -191,6 +283,7 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
       const double x = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, u)), __dmul_rn(st, v));
       const double y = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, u)), __dmul_rn(ct, v));
       const bool inside = x >= 1.0 && x <= xhi && y >= 1.0 && y <= yhi;
+      if (!inside) continue;  // mag = hypot * valid = +0.0 adds nothing
       const double lx = __dsub_rn(fmin(fmax(x, (double)pc0), (double)pc1), (double)pc0);
       const double ly = __dsub_rn(fmin(fmax(y, (double)pr0), (double)pr1), (double)pr0);
       const int x0 = min((int)floor(lx), xcap), y0 = min((int)floor(ly), ycap);
@@ -198,10 +291,10 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
       const int x1 = min(x0 + 1, pc1 - pc0), y1 = min(y0 + 1, pr1 - pr0);
       double a00, b00, a01, b01, a10, b10, a11, b11;
       if (kStaged) {
-        a00 = fa[y0 * FC + x0]; b00 = fb[y0 * FC + x0];
-        a01 = fa[y0 * FC + x1]; b01 = fb[y0 * FC + x1];
-        a10 = fa[y1 * FC + x0]; b10 = fb[y1 * FC + x0];
-        a11 = fa[y1 * FC + x1]; b11 = fb[y1 * FC + x1];
+        a00 = fa[y0 * SP + x0]; b00 = fb[y0 * SP + x0];
+        a01 = fa[y0 * SP + x1]; b01 = fb[y0 * SP + x1];
+        a10 = fa[y1 * SP + x0]; b10 = fb[y1 * SP + x0];
+        a11 = fa[y1 * SP + x1]; b11 = fb[y1 * SP + x1];
       } else {
         const int gy0 = pr0 + y0, gy1 = pr0 + y1, gx0 = pc0 + x0, gx1 = pc0 + x1;
         axis_sample(im, gy0, gx0, a00, b00);
@@ -217,10 +310,21 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
       const double bs = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(b00, sy), sx), __dmul_rn(__dmul_rn(b01, sy), fxx)),
                                             __dmul_rn(__dmul_rn(b10, fyy), sx)),
                                   __dmul_rn(__dmul_rn(b11, fyy), fxx));
-      if (inside) {  // mag = hypot(as, bs) * valid: invalid samples add +0.0
-        const double ori = mod_two_pi(__dsub_rn(atan2(bs, as), theta0), two_pi);
-        const int ob = min((int)__dmul_rn(ori, prm.k8), 7);
-        h128.add(((iv / ws) * d + iu / ws) * 8 + ob, hypot(as, bs), fx);
+      const int cell = ((iv / ws) * d + iu / ws) * 8;
+      if (FAST) {
+        const float af = (float)as, bf = (float)bs;
+        const float xb = wrap_two_pi_f(atan2f(bf, af) - theta0f) * 1.2732395447351628f;
+        int ob;
+        if (!certified_bin(xb, 8, ob)) {
+          const int m = min(max(__float2int_rn(xb), 0), 8);
+          const double ce = __dsub_rn(__dmul_rn(c0t, prm.c8[m]), __dmul_rn(s0t, prm.s8[m]));
+          const double se = __dadd_rn(__dmul_rn(s0t, prm.c8[m]), __dmul_rn(c0t, prm.s8[m]));
+          ob = side_bin(as, bs, ce, se, m, 8);
+          if (ob < 0) ob = bin64(as, bs, theta0, prm.k8, 8);
+        }
+        h128.add_f(cell + ob, __fsqrt_rn(__fmaf_rn(af, af, bf * bf)), fxf);
+      } else {
+        h128.add(cell + bin64(as, bs, theta0, prm.k8, 8), hypot(as, bs), fx);
       }
     }
   } else {
@@ -229,9 +333,20 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
       const int iv = s / w, iu = s % w;
       double a, b;
       axis_ab(iv, iu, a, b);
-      const double ori = mod_two_pi(atan2(b, a), two_pi);
-      const int ob = min((int)__dmul_rn(ori, prm.k8), 7);
-      h128.add(((iv / ws) * d + iu / ws) * 8 + ob, hypot(a, b), fx);
+      const int cell = ((iv / ws) * d + iu / ws) * 8;
+      if (FAST) {
+        const float af = (float)a, bf = (float)b;
+        const float xb = wrap_two_pi_f(atan2f(bf, af)) * 1.2732395447351628f;
+        int ob;
+        if (!certified_bin(xb, 8, ob)) {
+          const int m = min(max(__float2int_rn(xb), 0), 8);
+          ob = side_bin(a, b, prm.c8[m], prm.s8[m], m, 8);
+          if (ob < 0) ob = bin64(a, b, 0.0, prm.k8, 8);
+        }
+        h128.add_f(cell + ob, __fsqrt_rn(__fmaf_rn(af, af, bf * bf)), fxf);
+      } else {
+        h128.add(cell + bin64(a, b, 0.0, prm.k8, 8), hypot(a, b), fx);
+      }
     }
   }
   __syncwarp();
@@ -305,14 +420,15 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
     if (w < 0 || row < 0 || row >= im.nr || col < 0 || col >= im.nc) continue;  // validated by the caller
     float* o32 = out32 ? out32 + g * D : nullptr;
     double* o64 = out64 ? out64 + g * D : nullptr;
+    constexpr bool kFast = std::is_same<Img, RampU8>::value;
     if (prm.d == 4 && w == 8) {
-      describe_keypoint<8, 4>(im, row, col, w, 4, fx, lb, prm, hw, stage, o32, o64);
+      describe_keypoint<8, 4, kFast>(im, row, col, w, 4, fx, lb, prm, hw, stage, o32, o64);
     } else if (prm.d == 4 && w == 16) {
-      describe_keypoint<16, 4>(im, row, col, w, 4, fx, lb, prm, hw, stage, o32, o64);
+      describe_keypoint<16, 4, kFast>(im, row, col, w, 4, fx, lb, prm, hw, stage, o32, o64);
     } else if (prm.d == 4 && w == 32) {
-      describe_keypoint<32, 4>(im, row, col, w, 4, fx, lb, prm, hw, stage, o32, o64);
+      describe_keypoint<32, 4, kFast>(im, row, col, w, 4, fx, lb, prm, hw, stage, o32, o64);
     } else {
-      describe_keypoint<0, 0>(im, row, col, w, prm.d, fx, lb, prm, hw, stage, o32, o64);
+      describe_keypoint<0, 0, kFast>(im, row, col, w, prm.d, fx, lb, prm, hw, stage, o32, o64);
     }
   }
 }
@@ -363,7 +479,8 @@ extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, in
   PS_REQUIRE(n_scale_set >= 1 && n_scale_set <= kMaxDescScales, PS_ERR_ARGUMENT, "1..%d scales supported",
              kMaxDescScales);
   PS_REQUIRE(img->nr >= 3 && img->nc >= 3, PS_ERR_VALUE, "image too small");
-  PS_REQUIRE((int64_t)img->nr * img->nc < (int64_t)INT32_MAX, PS_ERR_ARGUMENT, "image too large (nr*nc >= 2^31)");
+  PS_REQUIRE((int64_t)img->nr * img->nc < (int64_t)INT32_MAX && (int64_t)img->nr * img->row_pitch < (int64_t)INT32_MAX,
+             PS_ERR_ARGUMENT, "image too large (nr*pitch >= 2^31)");
   cudaStream_t s = (cudaStream_t)stream;
   // bound on |P| for the fixed-point histogram scale
   double pmax = 255.0 + 0.05 * 255.0;
@@ -407,6 +524,14 @@ extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, in
   prm.k36 = 36 / two_pi;
   prm.k8 = 8 / two_pi;
   prm.two_pi = two_pi;
+  for (int m = 0; m <= 36; ++m) {
+    prm.cb36[m] = std::cos(m * (two_pi / 36));
+    prm.sb36[m] = std::sin(m * (two_pi / 36));
+  }
+  for (int m = 0; m <= 8; ++m) {
+    prm.c8[m] = std::cos(m * (two_pi / 8));
+    prm.s8[m] = std::sin(m * (two_pi / 8));
+  }
   for (int k = 0; k < 36; ++k) {  // descriptor.py:146 and :180 (host libm, as Python's math)
     const double th = ((double)k + 0.5) * (two_pi / 36);
     prm.theta[k] = th;

@@ -479,6 +479,8 @@ extern "C" int ps_detect(const ps_image_batch* img, const int32_t* host_scales, 
                          ps_keypoints* out, void* workspace, size_t workspace_bytes, void* stream) {
   PS_REQUIRE(img && out && host_scales && img->data && out->row && out->col && out->value && out->count,
              PS_ERR_ARGUMENT, "null argument to ps_detect");
+  PS_REQUIRE((int64_t)img->nr * img->row_pitch < (int64_t)INT32_MAX, PS_ERR_ARGUMENT,
+             "image too large (nr*pitch >= 2^31)");
   PS_REQUIRE(img->batch >= 1 && img->nr >= 1 && img->nc >= 1 && img->row_pitch >= img->nc &&
                  (img->batch == 1 || img->image_stride >= img->row_pitch * img->nr),
              PS_ERR_ARGUMENT, "bad image geometry");

@@ -68,7 +68,7 @@ __device__ __forceinline__ double u32_to_f64(unsigned x) {
   return __dsub_rn(__hiloint2double(0x43300000, (int)x), 4503599627370496.0);
 }
 
-// (callers guarantee nr * nc < 2^31, so the flat index fits in 32 bits)
+// (callers guarantee nr * nc < 2^31 and nr * pitch < 2^31: 32-bit offsets)
 struct RampU8 {
   const uint8_t* p;
   int64_t pitch;
@@ -76,7 +76,7 @@ struct RampU8 {
   double alpha;
   __device__ __forceinline__ double at(int r, int c) const {
     const double k = u32_to_f64((unsigned)(r * nc + c + 1));
-    return __dadd_rn(u32_to_f64(p[(int64_t)r * pitch + c]), __dmul_rn(k, alpha));
+    return __dadd_rn(u32_to_f64(p[r * (int)pitch + c]), __dmul_rn(k, alpha));
   }
 };
 
