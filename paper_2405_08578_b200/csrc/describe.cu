@@ -137,6 +137,12 @@ __device__ __forceinline__ int side_bin(double a, double b, double ce, double se
   return -1;
 }
 
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __device__ __forceinline__ float wrap_two_pi_f(float x) {
   const float tp = 6.283185307179586f;
   if (x < 0.0f) x += tp;
@@ -198,6 +204,7 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
   if (prm.orient) {
     // --- dominant orientation: 36-bin histogram of the axis region (:142-146)
     bool exact = !FAST;
+    int hk = -1;
     for (;;) {
 #pragma unroll 4
       for (int s = lane; s < nsamp; s += 32) {
@@ -220,20 +227,24 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
       const unsigned top = __reduce_max_sync(0xffffffffu, max(k1, k2));
       const unsigned sec = __reduce_max_sync(0xffffffffu, max(k1 == top ? 0u : k1, k2 == top ? 0u : k2));
       const float tv = __uint_as_float(top & ~63u), sv = __uint_as_float(sec & ~63u);
-      if (sv < tv * 0.99994f) break;  // lead > 6e-5 relative: float64 sums agree
+      if (sv < tv * 0.99994f) {  // lead > 6e-5 relative: float64 sums agree
+        hk = 63 - (int)(top & 63u);
+        break;
+      }
       exact = true;  // near-tie: rebuild this histogram in float64 (warp-uniform)
       h36.zero(lane);
       __syncwarp();
     }
-    // first argmax over the 36 bins (exact integer sums)
-    unsigned long long hv = h36.get(lane);
-    int hk = lane;
-    if (lane < 4 && h36.get(lane + 32) > hv) { hv = h36.get(lane + 32); hk = lane + 32; }
+    if (hk < 0) {  // first argmax over the 36 bins (exact integer sums)
+      unsigned long long hv = h36.get(lane);
+      hk = lane;
+      if (lane < 4 && h36.get(lane + 32) > hv) { hv = h36.get(lane + 32); hk = lane + 32; }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const unsigned long long v2 = __shfl_xor_sync(0xffffffffu, hv, o);
-      const int k2 = __shfl_xor_sync(0xffffffffu, hk, o);
-      if (v2 > hv || (v2 == hv && k2 < hk)) { hv = v2; hk = k2; }
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long v2 = __shfl_xor_sync(0xffffffffu, hv, o);
+        const int k2 = __shfl_xor_sync(0xffffffffu, hk, o);
+        if (v2 > hv || (v2 == hv && k2 < hk)) { hv = v2; hk = k2; }
+      }
     }
     const double theta0 = prm.theta[hk], ct = prm.cos_t[hk], st = prm.sin_t[hk];
     const float theta0f = (float)theta0;
@@ -241,19 +252,12 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
     const double half = (double)(w - 1) / 2.0;
     const double cy = fmin(fmax((double)row, 1.0 + half), __dsub_rn((double)nr - 2.0, half));
     const double cx = fmin(fmax((double)col, 1.0 + half), __dsub_rn((double)nc - 2.0, half));
-    // positions are coordinate-wise monotone in (u, v) -> extremes at the corners
-    double xmin = 1e300, xmax = -1e300, ymin = 1e300, ymax = -1e300;
-#pragma unroll
-    for (int cv = 0; cv < 2; ++cv)
-#pragma unroll
-      for (int cu = 0; cu < 2; ++cu) {
-        const double u = __dsub_rn((double)(cu * (w - 1)), half);
-        const double v = __dsub_rn((double)(cv * (w - 1)), half);
-        const double x = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, u)), __dmul_rn(st, v));
-        const double y = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, u)), __dmul_rn(ct, v));
-        xmin = fmin(xmin, x); xmax = fmax(xmax, x);
-        ymin = fmin(ymin, y); ymax = fmax(ymax, y);
-      }
+    // Rounded positions are coordinate-wise monotone in u and in v, so each
+    // extreme of x / y over the grid sits at the corner picked by the signs.
+    const double xmin = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, ct >= 0.0 ? -half : half)), __dmul_rn(st, st >= 0.0 ? half : -half));
+    const double xmax = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, ct >= 0.0 ? half : -half)), __dmul_rn(st, st >= 0.0 ? -half : half));
+    const double ymin = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, st >= 0.0 ? -half : half)), __dmul_rn(ct, ct >= 0.0 ? -half : half));
+    const double ymax = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, st >= 0.0 ? half : -half)), __dmul_rn(ct, ct >= 0.0 ? half : -half));
     const int pr0 = max((int)floor(ymin), 1), pr1 = min((int)ceil(ymax), nr - 2);
     const int pc0 = max((int)floor(xmin), 1), pc1 = min((int)ceil(xmax), nc - 2);
     const int xcap = max(pc1 - pc0 - 1, 0), ycap = max(pr1 - pr0 - 1, 0);
@@ -351,8 +355,40 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
   }
   __syncwarp();
   // --- L2 normalise, clamp at 0.2, renormalise (descriptor.py:250-255)
-  const double inv_fx = 1.0 / fx;  // exact: fx is a power of two
   constexpr int kPer = DD > 0 ? (DD * DD * 8 + 31) / 32 : 16;
+  if (FAST && o64 == nullptr) {
+    // float32 output only: float32 arithmetic (relative error ~1e-6, P2 bar 1e-4)
+    const float inv_fx = 1.0f / fxf;
+    float vals[kPer];
+    float ss = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int q = lane + 32 * j;
+      vals[j] = q < D ? (float)h128.get(q) * inv_fx : 0.0f;
+      ss = __fmaf_rn(vals[j], vals[j], ss);
+    }
+    ss = warp_sum_f(ss);
+    if (ss > 0.0f) {
+      const float r1 = rsqrtf(ss);
+      float ss2 = 0.0f;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        vals[j] = fminf(vals[j] * r1, 0.2f);
+        ss2 = __fmaf_rn(vals[j], vals[j], ss2);
+      }
+      const float r2 = rsqrtf(warp_sum_f(ss2));
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) vals[j] *= r2;
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int q = lane + 32 * j;
+      if (q < D) o32[q] = vals[j];
+    }
+    __syncwarp();
+    return;
+  }
+  const double inv_fx = 1.0 / fx;  // exact: fx is a power of two
   double vals[kPer];
   double ss = 0.0;
 #pragma unroll
@@ -404,8 +440,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
   double* stage = dsm + wid * kStageDoubles;
   unsigned* hw = reinterpret_cast<unsigned*>(dsm + kWarps * kStageDoubles) + wid * 3 * (D + 36);
   const int64_t total = (int64_t)B * cap;
+  const bool small = total < (1ll << 31);
   for (int64_t g = (int64_t)blockIdx.x * kWarps + wid; g < total; g += (int64_t)gridDim.x * kWarps) {
-    const int b = (int)(g / cap);
+    const int b = small ? (int)((unsigned)g / (unsigned)cap) : (int)(g / cap);
     const int64_t i = g - (int64_t)b * cap;
     if (counts && i >= counts[b]) continue;
     Img im = img;
@@ -415,8 +452,12 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
     int w = -1;
     double fx = 0.0;
     int lb = 0;
-    for (int s = 0; s < prm.n_scales; ++s)
-      if (prm.scale[s] == scale) { w = prm.w[s]; fx = prm.fx[s]; lb = prm.lb[s]; }
+    if (prm.n_scales == 1) {
+      if (prm.scale[0] == scale) { w = prm.w[0]; fx = prm.fx[0]; lb = prm.lb[0]; }
+    } else {
+      for (int s = 0; s < prm.n_scales; ++s)
+        if (prm.scale[s] == scale) { w = prm.w[s]; fx = prm.fx[s]; lb = prm.lb[s]; }
+    }
     if (w < 0 || row < 0 || row >= im.nr || col < 0 || col >= im.nc) continue;  // validated by the caller
     float* o32 = out32 ? out32 + g * D : nullptr;
     double* o64 = out64 ? out64 + g * D : nullptr;

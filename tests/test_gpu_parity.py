@@ -151,6 +151,7 @@ def test_descriptor_full_c2_image_sampled_against_oracle():
     t = torch.from_numpy(img).cuda()
     kp = device.detect(t, (8, 16, 32, 64, 128), alpha=alpha, meta=False)
     d32, d64 = device.describe(t, kp, cfg, out64=True)
+    d32_only = device.describe(t, kp, cfg)  # float32-only output path (float32 normalisation)
     assert int(kp.count[0]) == 134400
     P = O.ramp(img.astype(np.float64), alpha)
     h = kp.image(0)
@@ -161,6 +162,8 @@ def test_descriptor_full_c2_image_sampled_against_oracle():
         want = O.describe_one(P, int(h["row"][k]), int(h["col"][k]), 8, 0.0625, 4, 128, True)
         got = d64[0, k].cpu().numpy()
         worst = max(worst, float(np.max(np.abs(got - want)) / max(np.linalg.norm(want), 1e-300)))
+        g32 = d32_only[0, k].double().cpu().numpy()
+        worst = max(worst, float(np.max(np.abs(g32 - want)) / max(np.linalg.norm(want), 1e-300)))
         assert np.array_equal(d32[0, k].cpu().numpy(), got.astype(np.float32))
     assert worst <= P2_TOL, worst
 
