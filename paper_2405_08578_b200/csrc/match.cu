@@ -11,10 +11,23 @@
 // Accepted pairs are sorted by (delta, ref1, ref2) with stable radix sorts.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include "ps_common.cuh"
+
+template <class T>
+int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double delta_s, unsigned long long* keys_pair,
+                       unsigned long long* keys_delta, unsigned long long* counter, void* ws, size_t ws_bytes,
+                       cudaStream_t st);
+size_t ps_tc_nearest_ws(int64_t n1, int64_t n2);
 
 namespace ps {
 namespace {
+
+// tensor-core path: 128-d nearest_neighbor problems large enough to pay off
+bool use_tc(int64_t n1, int64_t n2, int dim, int strategy) {
+  return strategy == PS_MATCH_NEAREST && dim == 128 && n1 * n2 >= (int64_t)1 << 20 && getenv("PS_MATCH_EXACT") == nullptr;
+}
 
 constexpr int TILE = 32;     // rows x cols per tile
 constexpr int SPAD = 129;    // padded smem row stride (doubles) for D <= 128
@@ -235,6 +248,8 @@ struct MatchWs {
   unsigned long long *kp, *kd, *kp2, *kd2, *counter;
   void* tmp;
   size_t tmp_bytes;
+  void* extra;  // tensor-core path workspace
+  size_t extra_bytes;
 };
 
 size_t sort_temp_bytes(int64_t n) {
@@ -244,7 +259,7 @@ size_t sort_temp_bytes(int64_t n) {
   return t;
 }
 
-MatchWs carve(void* base, int64_t n1, int64_t n2, int64_t cand, size_t* used) {
+MatchWs carve(void* base, int64_t n1, int64_t n2, int64_t cand, size_t* used, size_t extra = 0) {
   Arena a{(char*)base, 0, 0};
   MatchWs w{};
   w.nn12 = a.take<int32_t>(n1);
@@ -258,6 +273,8 @@ MatchWs carve(void* base, int64_t n1, int64_t n2, int64_t cand, size_t* used) {
   w.counter = a.take<unsigned long long>(1);
   w.tmp_bytes = sort_temp_bytes(cand > 0 ? cand : 1);
   w.tmp = a.take<char>(w.tmp_bytes);
+  w.extra = extra ? a.take<char>(extra) : nullptr;
+  w.extra_bytes = extra;
   *used = a.used + 256;
   return w;
 }
@@ -305,7 +322,8 @@ extern "C" int ps_match_plan(int64_t n1, int64_t n2, int32_t dim, int32_t strate
   PS_REQUIRE(strategy == PS_MATCH_NEAREST || strategy == PS_MATCH_THRESHOLD_ALL, PS_ERR_CONFIG,
              "unknown match strategy %d", strategy);
   size_t used = 0;
-  carve(nullptr, n1, n2, candidate_cap(n1, n2, strategy, cap), &used);
+  carve(nullptr, n1, n2, candidate_cap(n1, n2, strategy, cap), &used,
+        use_tc(n1, n2, dim, strategy) ? ps_tc_nearest_ws(n1, n2) : 0);
   if (workspace_bytes_out) *workspace_bytes_out = used;
   return PS_OK;
 }
@@ -328,15 +346,25 @@ extern "C" int ps_match(const void* desc1, int64_t n1, const void* desc2, int64_
   }
   PS_REQUIRE(desc1 && desc2, PS_ERR_ARGUMENT, "null descriptors");
   const int64_t cand = candidate_cap(n1, n2, strategy, cap);
+  const bool tc = use_tc(n1, n2, dim, strategy);
+  const size_t extra = tc ? ps_tc_nearest_ws(n1, n2) : 0;
   size_t used = 0;
-  carve(nullptr, n1, n2, cand, &used);
+  carve(nullptr, n1, n2, cand, &used, extra);
   PS_REQUIRE(workspace && workspace_bytes >= used, PS_ERR_ARGUMENT, "match workspace %zu < %zu", workspace_bytes,
              used);
-  MatchWs w = carve(workspace, n1, n2, cand, &used);
+  MatchWs w = carve(workspace, n1, n2, cand, &used, extra);
   cudaMemsetAsync(w.counter, 0, sizeof(unsigned long long), st);
-  int rc = desc_is_f64
-               ? launch_match((const double*)desc1, n1, (const double*)desc2, n2, dim, delta_s, strategy, w, cand, st)
-               : launch_match((const float*)desc1, n1, (const float*)desc2, n2, dim, delta_s, strategy, w, cand, st);
+  int rc;
+  if (tc) {
+    rc = desc_is_f64 ? ps_tc_nearest_impl((const double*)desc1, n1, (const double*)desc2, n2, delta_s, w.kp, w.kd,
+                                          w.counter, w.extra, w.extra_bytes, st)
+                     : ps_tc_nearest_impl((const float*)desc1, n1, (const float*)desc2, n2, delta_s, w.kp, w.kd,
+                                          w.counter, w.extra, w.extra_bytes, st);
+  } else {
+    rc = desc_is_f64
+             ? launch_match((const double*)desc1, n1, (const double*)desc2, n2, dim, delta_s, strategy, w, cand, st)
+             : launch_match((const float*)desc1, n1, (const float*)desc2, n2, dim, delta_s, strategy, w, cand, st);
+  }
   if (rc) return rc;
   // Sort by (delta, ref1, ref2): two stable radix passes, pair key first,
   // then delta bits (non-negative doubles order like their bit patterns).

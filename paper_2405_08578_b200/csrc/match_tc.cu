@@ -1,0 +1,604 @@
+// K3 (tensor cores) -- mutual-nearest-neighbour matching of 128-d descriptors
+// on tcgen05 with an exact float64 certification (reference matcher.py:48-95).
+//
+// Design (SURVEY.md §7 hard part 1, contract P3):
+//  1. Bit-identical descriptor rows are grouped on each side; the lowest index
+//     represents its group.  Distances to identical rows are bitwise equal, so
+//     np.argmin's first-occurrence winner among them is the representative.
+//  2. Pass 1 (rows): one CTA owns 128 rows of X (fp16, K-major SW128 image in
+//     shared memory for the whole pass) and streams every 256-row tile of Y
+//     through a 3-stage bulk-copy pipeline; one thread issues 8 tcgen05.mma
+//     (M=128, N=256, K=16) per tile into a double-buffered TMEM accumulator;
+//     four epilogue warps read it with tcgen05.ld (thread = row) and keep
+//     v = |y|^2 - 2 x.y with a fused running minimum; only when a tile holds a
+//     value below the row's current 4th best is it rescanned into a top-4 list.
+//     The distance matrix never leaves TMEM.
+//  3. Certification: |v - (d^2 - |x|^2)| <= E_i, a rigorous bound from the
+//     fp16 rounding residual norms and fp32 accumulation, so the true first
+//     argmin is among the candidates with v <= v_min + 2 E_i; those are
+//     recomputed with the reference's exact float64 arithmetic.  Rows whose
+//     candidate set may exceed the top-4 are rescanned exactly in float64.
+//  4. Pass 2 repeats 2-3 for the columns that can be matched (nn12 of rows
+//     with d < delta_s) against all rows, giving the column argmin nn21.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include <cuda_fp16.h>
+
+#include "ps_common.cuh"
+#include "tc_primitives.cuh"
+
+namespace ps {
+namespace tc {
+
+constexpr int BM = 128;   // X rows per CTA (= TMEM lanes)
+constexpr int BN = 256;   // Y rows per tile (= MMA N, TMEM columns)
+constexpr int KD = 128;   // descriptor length
+constexpr int TOPK = 4;
+constexpr int STAGES = 3;
+constexpr uint32_t A_BYTES = BM * KD * 2;  // 32 KB
+constexpr uint32_t B_BYTES = BN * KD * 2;  // 64 KB
+constexpr int kThreads = 192;              // warp 0 TMA, warp 1 MMA/TMEM, warps 2-5 epilogue
+constexpr size_t kSmemBytes = 1024 + A_BYTES + STAGES * (size_t)B_BYTES + 256;
+
+// ---- operand preparation ----------------------------------------------------------
+// Row u of the output (u < count) is source row idx[u] (or u); rows >= count are
+// zero.  Writes the fp16 K-major SW128 tile image, |x|^2 as float (+inf for
+// padding when pad_inf), and float64 |x|, |x - x_h|, |x_h|; folds their maxima
+// into maxes[0..2] (non-negative float bits).
+template <class T>
+__global__ void prep_tiles(const T* __restrict__ src, const int32_t* __restrict__ idx,
+                           const int32_t* __restrict__ count_p, int64_t count_const, int64_t n_pad, int R,
+                           uint8_t* __restrict__ tiles, float* __restrict__ norm2, double* __restrict__ info,
+                           unsigned* __restrict__ maxes, int pad_inf) {
+  const int lane = threadIdx.x & 31;
+  const int64_t count = count_p ? (int64_t)*count_p : count_const;
+  for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < n_pad;
+       u += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const bool live = u < count;
+    const int64_t s = live ? (idx ? (int64_t)idx[u] : u) : 0;
+    double x[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) x[e] = live ? (double)src[s * KD + lane * 4 + e] : 0.0;
+    __half h[4];
+    double sx = 0.0, sr = 0.0, sh = 0.0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      h[e] = __double2half(x[e]);
+      const double hv = (double)__half2float(h[e]);
+      const double rv = x[e] - hv;
+      sx += x[e] * x[e];
+      sr += rv * rv;
+      sh += hv * hv;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      sx += __shfl_xor_sync(0xffffffffu, sx, o);
+      sr += __shfl_xor_sync(0xffffffffu, sr, o);
+      sh += __shfl_xor_sync(0xffffffffu, sh, o);
+    }
+    const int64_t tile = u / R;
+    const int r = (int)(u % R);
+    uint8_t* base = tiles + tile * (int64_t)R * KD * 2;
+    const uint32_t off = sw128_offset(R, r, lane * 4);
+    __half2 p0 = __halves2half2(h[0], h[1]), p1 = __halves2half2(h[2], h[3]);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&p0);
+    pk.y = *reinterpret_cast<uint32_t*>(&p1);
+    *reinterpret_cast<uint2*>(base + off) = pk;
+    if (lane == 0) {
+      norm2[u] = live ? (float)sx : (pad_inf ? INFINITY : 0.0f);
+      info[3 * u + 0] = sqrt(sx);
+      info[3 * u + 1] = sqrt(sr);
+      info[3 * u + 2] = sqrt(sh);
+      if (live && maxes) {
+        atomicMax(maxes + 0, __float_as_uint((float)(sqrt(sx) * (1.0 + 1e-6))));
+        atomicMax(maxes + 1, __float_as_uint((float)(sqrt(sr) * (1.0 + 1e-6))));
+        atomicMax(maxes + 2, __float_as_uint((float)(sqrt(sh) * (1.0 + 1e-6))));
+      }
+    }
+  }
+}
+
+// ---- the tcgen05 row-minimum kernel --------------------------------------------------
+__device__ __forceinline__ void topk_insert(float v, int j, float (&tv)[TOPK], int (&tj)[TOPK]) {
+  // sorted ascending; caller guarantees v < tv[TOPK-1]
+#pragma unroll
+  for (int q = TOPK - 1; q > 0; --q) {
+    const bool shift = v < tv[q - 1];
+    const float nv = shift ? tv[q - 1] : v;
+    const int nj = shift ? tj[q - 1] : j;
+    if (v < tv[q]) { tv[q] = nv; tj[q] = nj; }
+  }
+  if (v < tv[0]) { tv[0] = v; tj[0] = j; }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Yt,
+                                                          const float* __restrict__ yn,
+                                                          const int32_t* __restrict__ cnt_x,
+                                                          const int32_t* __restrict__ cnt_y, float* __restrict__ topv,
+                                                          int32_t* __restrict__ topj) {
+  extern __shared__ uint8_t smem_raw[];
+  const int nx = *cnt_x, ny = *cnt_y;
+  const int rb = blockIdx.x;
+  if (rb * BM >= nx || ny <= 0) return;  // uniform for the whole CTA
+  const int n_tiles = (ny + BN - 1) / BN;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* a_full = bars;
+  uint64_t* b_full = bars + 1;
+  uint64_t* b_empty = b_full + STAGES;
+  uint64_t* acc_full = b_empty + STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    mbar_init(a_full, 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(b_full + s, 1);
+      mbar_init(b_empty + s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(acc_full + s, 1);
+      mbar_init(acc_empty + s, 4 * 32);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- bulk-copy producer
+      mbar_arrive_expect_tx(a_full, A_BYTES);
+      bulk_g2s(sA, Xt + (size_t)rb * A_BYTES, A_BYTES, a_full);
+      for (int t = 0; t < n_tiles; ++t) {
+        const int s = t % STAGES;
+        mbar_wait(b_empty + s, ((t / STAGES) & 1) ^ 1);
+        mbar_arrive_expect_tx(b_full + s, B_BYTES);
+        bulk_g2s(sB + s * B_BYTES, Yt + (size_t)t * B_BYTES, B_BYTES, b_full + s);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      const uint32_t idesc = idesc_f16_f32(BM, BN);
+      const uint32_t a0 = smem_u32(sA);
+      mbar_wait(a_full, 0);
+      for (int t = 0; t < n_tiles; ++t) {
+        const int s = t % STAGES, ab = t & 1;
+        mbar_wait(acc_empty + ab, ((t >> 1) & 1) ^ 1);
+        mbar_wait(b_full + s, (t / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t b0 = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+        for (int k = 0; k < KD / 16; ++k) {
+          const uint32_t koff = (uint32_t)((k & 3) * 32);  // 16 fp16 = 32 B within the atom
+          const uint64_t ad = sdesc_k_sw128(a0 + (k >> 2) * (BM * 128) + koff);
+          const uint64_t bd = sdesc_k_sw128(b0 + (k >> 2) * (BN * 128) + koff);
+          mma_f16(tmem + ab * BN, ad, bd, idesc, k > 0 ? 1u : 0u);
+        }
+        mma_commit(b_empty + s);
+        mma_commit(acc_full + ab);
+      }
+    }
+  } else {  // ---- epilogue: thread = row
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    float tv[TOPK];
+    int tj[TOPK];
+#pragma unroll
+    for (int q = 0; q < TOPK; ++q) { tv[q] = INFINITY; tj[q] = -1; }
+    for (int t = 0; t < n_tiles; ++t) {
+      const int ab = t & 1;
+      mbar_wait(acc_full + ab, (t >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + ab * BN;
+      const float* ynt = yn + (size_t)t * BN;
+      float m = INFINITY;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 64) {
+        uint32_t r[64];
+        tmem_ld64(tbase + c0, r);
+        tmem_ld_wait();
+        const float4* y4 = reinterpret_cast<const float4*>(ynt + c0);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const float4 y = __ldg(y4 + q);
+          m = fminf(m, fmaf(-2.0f, __uint_as_float(r[4 * q + 0]), y.x));
+          m = fminf(m, fmaf(-2.0f, __uint_as_float(r[4 * q + 1]), y.y));
+          m = fminf(m, fmaf(-2.0f, __uint_as_float(r[4 * q + 2]), y.z));
+          m = fminf(m, fmaf(-2.0f, __uint_as_float(r[4 * q + 3]), y.w));
+        }
+      }
+      const bool mine = m < tv[TOPK - 1];
+      if (__any_sync(0xffffffffu, mine)) {  // rescan (tcgen05.ld must stay warp-converged)
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 64) {
+          uint32_t r[64];
+          tmem_ld64(tbase + c0, r);
+          tmem_ld_wait();
+          if (mine) {
+#pragma unroll
+            for (int c = 0; c < 64; ++c) {
+              const float v = fmaf(-2.0f, __uint_as_float(r[c]), __ldg(ynt + c0 + c));
+              if (v < tv[TOPK - 1]) topk_insert(v, t * BN + c0 + c, tv, tj);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(acc_empty + ab);
+    }
+    const int64_t g = (int64_t)rb * BM + row;
+    if (g < nx) {
+#pragma unroll
+      for (int q = 0; q < TOPK; ++q) {
+        topv[g * TOPK + q] = tv[q];
+        topj[g * TOPK + q] = tj[q];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// ---- certification + exact float64 recheck ------------------------------------------
+// Reference distance between float-typed rows a and b (numpy pairwise order).
+template <class T>
+__device__ __forceinline__ double exact_dist(const T* __restrict__ a, const T* __restrict__ b) {
+  double r[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) r[t] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < KD; k += 8) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const double e = __dsub_rn((double)b[k + t], (double)a[k + t]);
+      r[t] = __dadd_rn(r[t], __dmul_rn(e, e));
+    }
+  }
+  return __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                              __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7]))));
+}
+
+// One thread per X' row u.  x_orig[u] / y_orig[j'] map tile rows to original
+// indices (ties break on original indices).  Writes nn[x_orig[u]] and d[...];
+// rows whose candidates may not fit the top-4 are appended to `overflow`.
+template <class T>
+__global__ void certify_exact(const float* __restrict__ topv, const int32_t* __restrict__ topj,
+                              const int32_t* __restrict__ cnt_x, const int32_t* __restrict__ x_orig,
+                              const int32_t* __restrict__ y_orig, const double* __restrict__ xinfo,
+                              const unsigned* __restrict__ ymax, const T* __restrict__ X, const T* __restrict__ Y,
+                              int32_t* __restrict__ nn, double* __restrict__ dist, int32_t* __restrict__ overflow,
+                              int32_t* __restrict__ n_overflow) {
+  const int nx = *cnt_x;
+  const double Nmax = __uint_as_float(ymax[0]), Rmax = __uint_as_float(ymax[1]), Hmax = __uint_as_float(ymax[2]);
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < nx; u += gridDim.x * blockDim.x) {
+    const int xi = x_orig ? x_orig[u] : u;
+    const double rx = xinfo[3 * u + 1], hx = xinfo[3 * u + 2];
+    // |v - (d^2 - |x|^2)| <= 2(|x - x_h||y| + |x_h||y - y_h|) + 2 g |x_h||y_h| + rounding of v
+    const double gamma = 128.0 * 2.384185791015625e-07;  // 128 * 2^-22 (fp32 accumulation)
+    const double E = 1.01 * (2.0 * (rx * Nmax + hx * Rmax) + 2.0 * gamma * hx * Hmax +
+                             4.8e-7 * (1.0 + Nmax * Nmax) + 4.8e-7 * 2.0 * hx * Hmax);
+    float tv[TOPK];
+    int tj[TOPK];
+#pragma unroll
+    for (int q = 0; q < TOPK; ++q) {
+      tv[q] = topv[(int64_t)u * TOPK + q];
+      tj[q] = topj[(int64_t)u * TOPK + q];
+    }
+    const double lim = (double)tv[0] + 2.0 * E;
+    if ((double)tv[TOPK - 1] <= lim) {  // candidates may extend past the top-4
+      const int slot = atomicAdd(n_overflow, 1);
+      overflow[slot] = u;
+      continue;
+    }
+    double bd = INFINITY;
+    int bj = INT32_MAX;
+#pragma unroll
+    for (int q = 0; q < TOPK; ++q) {
+      if (tj[q] < 0 || (double)tv[q] > lim) continue;
+      const int yj = y_orig ? y_orig[tj[q]] : tj[q];
+      const double dd = exact_dist(X + (int64_t)xi * KD, Y + (int64_t)yj * KD);
+      if (dd < bd || (dd == bd && yj < bj)) { bd = dd; bj = yj; }
+    }
+    nn[xi] = bj;
+    dist[xi] = bd;
+  }
+}
+
+// exact full scans for overflow rows: one block per row, threads stride Y
+template <class T>
+__global__ void exact_rows(const int32_t* __restrict__ rows, const int32_t* __restrict__ n_rows,
+                           const int32_t* __restrict__ x_orig, const T* __restrict__ X, const T* __restrict__ Y,
+                           int64_t ny, int32_t* __restrict__ nn, double* __restrict__ dist) {
+  __shared__ double sd[32];
+  __shared__ int sj[32];
+  const int n = *n_rows;
+  for (int q = blockIdx.x; q < n; q += gridDim.x) {
+    const int u = rows[q];
+    const int xi = x_orig ? x_orig[u] : u;
+    double bd = INFINITY;
+    int bj = INT32_MAX;
+    for (int64_t j = threadIdx.x; j < ny; j += blockDim.x) {
+      const double dd = exact_dist(X + (int64_t)xi * KD, Y + j * KD);
+      if (dd < bd || (dd == bd && (int)j < bj)) { bd = dd; bj = (int)j; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const double d2 = __shfl_xor_sync(0xffffffffu, bd, o);
+      const int j2 = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (d2 < bd || (d2 == bd && j2 < bj)) { bd = d2; bj = j2; }
+    }
+    if ((threadIdx.x & 31) == 0) { sd[threadIdx.x >> 5] = bd; sj[threadIdx.x >> 5] = bj; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+        if (sd[w] < bd || (sd[w] == bd && sj[w] < bj)) { bd = sd[w]; bj = sj[w]; }
+      nn[xi] = bj;
+      dist[xi] = bd;
+    }
+    __syncthreads();
+  }
+}
+
+// ---- duplicate rows --------------------------------------------------------------------
+template <class T>
+__global__ void row_hash(const T* __restrict__ X, int64_t n, unsigned long long* __restrict__ keys,
+                         int32_t* __restrict__ vals) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
+       i += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    unsigned long long h = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const T v = X[i * KD + lane * 4 + e];
+      unsigned long long bits;
+      if (sizeof(T) == 8) bits = (unsigned long long)__double_as_longlong((double)v);
+      else bits = (unsigned long long)__float_as_uint((float)v);
+      // splitmix64 of (bits, position)
+      unsigned long long z = bits + 0x9E3779B97F4A7C15ull * (unsigned long long)(lane * 4 + e + 1);
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      h += z ^ (z >> 31);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if (lane == 0) {
+      keys[i] = h;
+      vals[i] = (int32_t)i;
+    }
+  }
+}
+
+// sorted (hash, index): rep = first index of the equal-hash run when the rows
+// are bitwise equal to it, else itself.  flag[i] = (rep == i).
+template <class T>
+__global__ void mark_reps(const T* __restrict__ X, int64_t n, const unsigned long long* __restrict__ hs,
+                          const int32_t* __restrict__ idx, int32_t* __restrict__ rep, int32_t* __restrict__ flag) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    int64_t s = p;
+    while (s > 0 && hs[s - 1] == hs[p]) --s;  // runs are tiny except for saturated clusters
+    const int i = idx[p], l = idx[s];
+    bool same = true;
+    if (l != i)
+      for (int k = 0; k < KD && same; ++k) same = X[(int64_t)i * KD + k] == X[(int64_t)l * KD + k];
+    const int r = same ? l : i;
+    rep[i] = r;
+    flag[i] = r == i;
+  }
+}
+
+__global__ void iota32(int32_t* v, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    v[i] = (int32_t)i;
+}
+
+// columns worth checking: nn12 of rows with d < delta_s
+__global__ void mark_columns(const int32_t* __restrict__ a_uniq, const int32_t* __restrict__ n_auniq,
+                             const int32_t* __restrict__ nn12, const double* __restrict__ d12, double delta_s,
+                             int32_t* __restrict__ colflag) {
+  const int n = *n_auniq;
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+    const int i = a_uniq[u];
+    if (d12[i] < delta_s) colflag[nn12[i]] = 1;
+  }
+}
+
+// acceptance over original rows (matcher.py:74-79); only representatives can be mutual
+__global__ void accept_pairs(const int32_t* __restrict__ a_rep, int64_t n1, const int32_t* __restrict__ nn12,
+                             const double* __restrict__ d12, const int32_t* __restrict__ nn21, double delta_s,
+                             unsigned long long* __restrict__ keys_pair, unsigned long long* __restrict__ keys_delta,
+                             unsigned long long* __restrict__ counter) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n1; i += (int64_t)gridDim.x * blockDim.x) {
+    if (a_rep[i] != (int32_t)i) continue;
+    const int j = nn12[i];
+    if (d12[i] < delta_s && nn21[j] == (int32_t)i) {
+      const unsigned long long slot = atomicAdd(counter, 1ull);
+      keys_pair[slot] = ((unsigned long long)i << 32) | (unsigned long long)j;
+      keys_delta[slot] = (unsigned long long)__double_as_longlong(d12[i]);
+    }
+  }
+}
+
+// ---- host orchestration ------------------------------------------------------------
+struct Side {  // a descriptor matrix with its duplicate-row structure
+  int32_t *iota, *vals_sorted, *rep, *flag, *uniq, *n_uniq;
+  unsigned long long *keys, *keys_sorted;
+};
+
+struct TcWs {
+  Side a, b;
+  void* cub_tmp;
+  size_t cub_bytes;
+  uint8_t *xt, *yt;
+  float *yn, *xn, *topv;
+  double *xinfo, *yinfo;
+  unsigned* ymax;
+  int32_t *topj, *nn12, *nn21, *overflow, *n_overflow, *colflag, *cols, *n_cols;
+  double *d12, *d21;
+};
+
+inline int64_t rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+size_t cub_need(int64_t n) {
+  size_t a = 0, b = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+  cub::DeviceSelect::Flagged(nullptr, b, (const int32_t*)nullptr, (const int32_t*)nullptr, (int32_t*)nullptr,
+                             (int32_t*)nullptr, (int)n);
+  return std::max(a, b);
+}
+
+TcWs carve_tc(void* base, int64_t n1, int64_t n2, size_t* used) {
+  Arena ar{(char*)base, 0, 0};
+  TcWs w{};
+  auto side = [&](Side& s, int64_t n) {
+    s.iota = ar.take<int32_t>(n);
+    s.vals_sorted = ar.take<int32_t>(n);
+    s.rep = ar.take<int32_t>(n);
+    s.flag = ar.take<int32_t>(n);
+    s.uniq = ar.take<int32_t>(n);
+    s.n_uniq = ar.take<int32_t>(1);
+    s.keys = ar.take<unsigned long long>(n);
+    s.keys_sorted = ar.take<unsigned long long>(n);
+  };
+  side(w.a, n1);
+  side(w.b, n2);
+  const int64_t nmax = std::max(n1, n2);
+  w.cub_bytes = cub_need(nmax);
+  w.cub_tmp = ar.take<char>(w.cub_bytes);
+  const int64_t xrows = rup(nmax, BM), yrows = rup(nmax, BN);
+  w.xt = ar.take<uint8_t>((size_t)xrows * KD * 2);
+  w.yt = ar.take<uint8_t>((size_t)yrows * KD * 2);
+  w.yn = ar.take<float>(yrows);
+  w.xn = ar.take<float>(xrows);
+  w.xinfo = ar.take<double>(3 * xrows);
+  w.yinfo = ar.take<double>(3 * yrows);
+  w.ymax = ar.take<unsigned>(4);
+  w.topv = ar.take<float>(xrows * TOPK);
+  w.topj = ar.take<int32_t>(xrows * TOPK);
+  w.nn12 = ar.take<int32_t>(n1);
+  w.d12 = ar.take<double>(n1);
+  w.nn21 = ar.take<int32_t>(n2);
+  w.d21 = ar.take<double>(n2);
+  w.overflow = ar.take<int32_t>(nmax);
+  w.n_overflow = ar.take<int32_t>(1);
+  w.colflag = ar.take<int32_t>(n2);
+  w.cols = ar.take<int32_t>(n2);
+  w.n_cols = ar.take<int32_t>(1);
+  *used = ar.used + 256;
+  return w;
+}
+
+int grid_for(int64_t work, int per) {
+  int64_t g = (work + per - 1) / per;
+  if (g > 148 * 16) g = 148 * 16;
+  return (int)(g < 1 ? 1 : g);
+}
+
+template <class T>
+int dedupe(const T* X, int64_t n, Side& s, const TcWs& w, cudaStream_t st) {
+  iota32<<<grid_for(n, 256), 256, 0, st>>>(s.iota, n);
+  PS_LAUNCHED("iota32");
+  row_hash<T><<<grid_for(n, 8), 256, 0, st>>>(X, n, s.keys, s.iota);
+  PS_LAUNCHED("row_hash");
+  size_t tb = w.cub_bytes;
+  cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, s.keys, s.keys_sorted, s.iota, s.vals_sorted, (int)n, 0, 64, st);
+  PS_LAUNCHED("cub_sort(hash)");
+  mark_reps<T><<<grid_for(n, 256), 256, 0, st>>>(X, n, s.keys_sorted, s.vals_sorted, s.rep, s.flag);
+  PS_LAUNCHED("mark_reps");
+  iota32<<<grid_for(n, 256), 256, 0, st>>>(s.iota, n);
+  PS_LAUNCHED("iota32");
+  tb = w.cub_bytes;
+  cub::DeviceSelect::Flagged(w.cub_tmp, tb, s.iota, s.flag, s.uniq, s.n_uniq, (int)n, st);
+  PS_LAUNCHED("cub_select(reps)");
+  return PS_OK;
+}
+
+// One direction: for every row X[x_idx[u]] (u < *n_x) the exact first argmin
+// over Y rows (candidates from tensor cores, all Y rows reachable through
+// y_idx[0..*n_y) which must include every distinct row of Y).
+template <class T>
+int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t* n_x, const T* Y, int64_t ny_all,
+                 const int32_t* y_idx, const int32_t* n_y, int32_t* nn, double* dist, const TcWs& w,
+                 cudaStream_t st) {
+  const int64_t xrows = rup(nx_max, BM), yrows = rup(ny_all, BN);
+  cudaMemsetAsync(w.ymax, 0, 4 * sizeof(unsigned), st);
+  cudaMemsetAsync(w.n_overflow, 0, sizeof(int32_t), st);
+  prep_tiles<T><<<grid_for(xrows, 8), 256, 0, st>>>(X, x_idx, n_x, 0, xrows, BM, w.xt, w.xn, w.xinfo,
+                                                      nullptr, 0);
+  PS_LAUNCHED("prep_tiles(X)");
+  prep_tiles<T><<<grid_for(yrows, 8), 256, 0, st>>>(Y, y_idx, n_y, 0, yrows, BN, w.yt, w.yn, w.yinfo, w.ymax, 1);
+  PS_LAUNCHED("prep_tiles(Y)");
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(nn_topk_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    attr = true;
+  }
+  nn_topk_tc<<<(unsigned)(xrows / BM), kThreads, kSmemBytes, st>>>(w.xt, w.yt, w.yn, n_x, n_y, w.topv, w.topj);
+  PS_LAUNCHED("nn_topk_tc");
+  certify_exact<T><<<grid_for(nx_max, 128), 128, 0, st>>>(w.topv, w.topj, n_x, x_idx, y_idx, w.xinfo, w.ymax, X, Y,
+                                                          nn, dist, w.overflow, w.n_overflow);
+  PS_LAUNCHED("certify_exact");
+  exact_rows<T><<<148 * 4, 256, 0, st>>>(w.overflow, w.n_overflow, x_idx, X, Y, ny_all, nn, dist);
+  PS_LAUNCHED("exact_rows");
+  return PS_OK;
+}
+
+}  // namespace tc
+}  // namespace ps
+
+// Candidate accepted pairs of nearest_neighbor matching on tensor cores; the
+// caller sorts (keys_pair, keys_delta) and reads *counter.
+template <class T>
+int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double delta_s, unsigned long long* keys_pair,
+                       unsigned long long* keys_delta, unsigned long long* counter, void* ws, size_t ws_bytes,
+                       cudaStream_t st) {
+  using namespace ps::tc;
+  size_t need = 0;
+  carve_tc(nullptr, n1, n2, &need);
+  PS_REQUIRE(ws && ws_bytes >= need, PS_ERR_ARGUMENT, "tensor-core match workspace %zu < %zu", ws_bytes, need);
+  TcWs w = carve_tc(ws, n1, n2, &need);
+  int rc = dedupe(A, n1, w.a, w, st);
+  if (rc) return rc;
+  rc = dedupe(B, n2, w.b, w, st);
+  if (rc) return rc;
+  // pass 1: rows of A (representatives) against the distinct rows of B
+  rc = nearest_pass(A, n1, w.a.uniq, w.a.n_uniq, B, n2, w.b.uniq, w.b.n_uniq, w.nn12, w.d12, w, st);
+  if (rc) return rc;
+  // pass 2: the columns that can be matched against the distinct rows of A
+  cudaMemsetAsync(w.colflag, 0, n2 * sizeof(int32_t), st);
+  mark_columns<<<grid_for(n1, 256), 256, 0, st>>>(w.a.uniq, w.a.n_uniq, w.nn12, w.d12, delta_s, w.colflag);
+  PS_LAUNCHED("mark_columns");
+  iota32<<<grid_for(n2, 256), 256, 0, st>>>(w.b.iota, n2);
+  PS_LAUNCHED("iota32");
+  size_t tb = w.cub_bytes;
+  cub::DeviceSelect::Flagged(w.cub_tmp, tb, w.b.iota, w.colflag, w.cols, w.n_cols, (int)n2, st);
+  PS_LAUNCHED("cub_select(columns)");
+  rc = nearest_pass(B, n2, w.cols, w.n_cols, A, n1, w.a.uniq, w.a.n_uniq, w.nn21, w.d21, w, st);
+  if (rc) return rc;
+  accept_pairs<<<grid_for(n1, 256), 256, 0, st>>>(w.a.rep, n1, w.nn12, w.d12, w.nn21, delta_s, keys_pair, keys_delta,
+                                                  counter);
+  PS_LAUNCHED("accept_pairs");
+  return PS_OK;
+}
+
+size_t ps_tc_nearest_ws(int64_t n1, int64_t n2) {
+  size_t need = 0;
+  ps::tc::carve_tc(nullptr, n1, n2, &need);
+  return need;
+}
+
+template int ps_tc_nearest_impl<float>(const float*, int64_t, const float*, int64_t, double, unsigned long long*,
+                                       unsigned long long*, unsigned long long*, void*, size_t, cudaStream_t);
+template int ps_tc_nearest_impl<double>(const double*, int64_t, const double*, int64_t, double, unsigned long long*,
+                                        unsigned long long*, unsigned long long*, void*, size_t, cudaStream_t);
