@@ -25,8 +25,13 @@ namespace ps {
 namespace {
 
 // tensor-core path: 128-d nearest_neighbor problems large enough to pay off
+// (PS_MATCH_EXACT=1 forces the float64 CUDA-core path; PS_TC_MIN_PAIRS sets
+// the size threshold -- both for tests and diagnostics)
 bool use_tc(int64_t n1, int64_t n2, int dim, int strategy) {
-  return strategy == PS_MATCH_NEAREST && dim == 128 && n1 * n2 >= (int64_t)1 << 20 && getenv("PS_MATCH_EXACT") == nullptr;
+  if (strategy != PS_MATCH_NEAREST || dim != 128 || getenv("PS_MATCH_EXACT") != nullptr) return false;
+  const char* m = getenv("PS_TC_MIN_PAIRS");
+  const int64_t min_pairs = m ? atoll(m) : ((int64_t)1 << 20);
+  return n1 * n2 >= min_pairs;
 }
 
 constexpr int TILE = 32;     // rows x cols per tile
