@@ -52,3 +52,20 @@ for im in (a, b):
     ds.append(device.describe(t, kp, cfg)[0])
 ok &= compare("C1", ds[0], ds[1])
 sys.exit(0 if ok else 1)
+
+if len(sys.argv) > 1 and sys.argv[1] == "c4":
+    t0 = time.time()
+    a, b = scenes.config4_pair(0)
+    print(f"C4 scene {time.time()-t0:.1f}s", flush=True)
+    cfg = DescriptorConfig(0.0625, 4, 36, True)
+    ds = []
+    for im in (a, b):
+        t = torch.from_numpy(im).cuda()
+        kp = device.detect(t, (36,), meta=False)
+        ds.append(device.describe(t, kp, cfg, scale_set=(36,))[0])
+    print("C4 keypoints", ds[0].shape[0], ds[1].shape[0], flush=True)
+    ok &= compare("C4", ds[0], ds[1])
+    for _ in range(3):
+        _, tg = run(ds[0], ds[1], False)
+        print(f"C4 tc {tg*1e3:.2f} ms  pair-matches/s {ds[0].shape[0]*ds[1].shape[0]/tg:.3e}", flush=True)
+    sys.exit(0 if ok else 1)
