@@ -51,7 +51,6 @@ for im in (a, b):
     kp = device.detect(t, (16, 32, 64), meta=False)
     ds.append(device.describe(t, kp, cfg)[0])
 ok &= compare("C1", ds[0], ds[1])
-sys.exit(0 if ok else 1)
 
 if len(sys.argv) > 1 and sys.argv[1] == "c4":
     t0 = time.time()
@@ -69,3 +68,4 @@ if len(sys.argv) > 1 and sys.argv[1] == "c4":
         _, tg = run(ds[0], ds[1], False)
         print(f"C4 tc {tg*1e3:.2f} ms  pair-matches/s {ds[0].shape[0]*ds[1].shape[0]/tg:.3e}", flush=True)
     sys.exit(0 if ok else 1)
+sys.exit(0 if ok else 1)
