@@ -23,6 +23,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include <cuda_fp16.h>
 
@@ -568,13 +570,32 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   carve_tc(nullptr, n1, n2, &need);
   PS_REQUIRE(ws && ws_bytes >= need, PS_ERR_ARGUMENT, "tensor-core match workspace %zu < %zu", ws_bytes, need);
   TcWs w = carve_tc(ws, n1, n2, &need);
+  // PS_TC_PROFILE=1: per-stage timing and counters on stderr (diagnostic; syncs)
+  const bool prof = getenv("PS_TC_PROFILE") != nullptr;
+  cudaEvent_t ev[8];
+  int nev = 0;
+  auto mark = [&]() {
+    if (!prof) return;
+    cudaEventCreate(&ev[nev]);
+    cudaEventRecord(ev[nev++], st);
+  };
+  auto count_of = [&](const int32_t* p) {
+    int32_t h = 0;
+    cudaMemcpyAsync(&h, p, 4, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    return h;
+  };
+  mark();
   int rc = dedupe(A, n1, w.a, w, st);
   if (rc) return rc;
   rc = dedupe(B, n2, w.b, w, st);
   if (rc) return rc;
+  mark();
   // pass 1: rows of A (representatives) against the distinct rows of B
   rc = nearest_pass(A, n1, w.a.uniq, w.a.n_uniq, B, n2, w.b.uniq, w.b.n_uniq, w.nn12, w.d12, w, st);
   if (rc) return rc;
+  mark();
+  const int of1 = prof ? count_of(w.n_overflow) : 0;
   // pass 2: the columns that can be matched against the distinct rows of A
   cudaMemsetAsync(w.colflag, 0, n2 * sizeof(int32_t), st);
   mark_columns<<<grid_for(n1, 256), 256, 0, st>>>(w.a.uniq, w.a.n_uniq, w.nn12, w.d12, delta_s, w.colflag);
@@ -584,11 +605,24 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   size_t tb = w.cub_bytes;
   cub::DeviceSelect::Flagged(w.cub_tmp, tb, w.b.iota, w.colflag, w.cols, w.n_cols, (int)n2, st);
   PS_LAUNCHED("cub_select(columns)");
+  mark();
   rc = nearest_pass(B, n2, w.cols, w.n_cols, A, n1, w.a.uniq, w.a.n_uniq, w.nn21, w.d21, w, st);
   if (rc) return rc;
+  mark();
   accept_pairs<<<grid_for(n1, 256), 256, 0, st>>>(w.a.rep, n1, w.nn12, w.d12, w.nn21, delta_s, keys_pair, keys_delta,
                                                   counter);
   PS_LAUNCHED("accept_pairs");
+  if (prof) {
+    cudaStreamSynchronize(st);
+    float t[8] = {0};
+    for (int i = 1; i < nev; ++i) cudaEventElapsedTime(&t[i], ev[i - 1], ev[i]);
+    fprintf(stderr,
+            "[tc] n1=%lld n2=%lld uniqA=%d uniqB=%d cols=%d overflow1=%d overflow2=%d | dedupe %.3f ms pass1 %.3f ms "
+            "select %.3f ms pass2 %.3f ms\n",
+            (long long)n1, (long long)n2, count_of(w.a.n_uniq), count_of(w.b.n_uniq), count_of(w.n_cols), of1,
+            count_of(w.n_overflow), t[1], t[2], t[3], t[4]);
+    for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
+  }
   return PS_OK;
 }
 
