@@ -116,11 +116,16 @@ __device__ __forceinline__ void topk_insert(float v, int j, float (&tv)[TOPK], i
   if (v < tv[0]) { tv[0] = v; tj[0] = j; }
 }
 
+// MODE 0: per-row top-4 of v.  MODE 1: enumerate every (row, column) with
+// v <= lim[row] into pairs (row << 32 | column), capacity `cap`.
+template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Yt,
                                                           const float* __restrict__ yn,
                                                           const int32_t* __restrict__ cnt_x,
                                                           const int32_t* __restrict__ cnt_y, float* __restrict__ topv,
-                                                          int32_t* __restrict__ topj) {
+                                                          int32_t* __restrict__ topj, const float* __restrict__ lim,
+                                                          unsigned long long* __restrict__ pairs,
+                                                          unsigned long long* __restrict__ n_pairs, int64_t cap) {
   extern __shared__ uint8_t smem_raw[];
   const int nx = *cnt_x, ny = *cnt_y;
   const int rb = blockIdx.x;
@@ -196,6 +201,8 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
     int tj[TOPK];
 #pragma unroll
     for (int q = 0; q < TOPK; ++q) { tv[q] = INFINITY; tj[q] = -1; }
+    const int64_t grow = (int64_t)rb * BM + row;
+    const float my_lim = (MODE == 1 && grow < nx) ? lim[grow] : -INFINITY;
     for (int t = 0; t < n_tiles; ++t) {
       const int ab = t & 1;
       mbar_wait(acc_full + ab, (t >> 1) & 1);
@@ -218,18 +225,35 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
           m = fminf(m, fmaf(-2.0f, __uint_as_float(r[4 * q + 3]), y.w));
         }
       }
-      const bool mine = m < tv[TOPK - 1];
+      const bool mine = MODE == 0 ? m < tv[TOPK - 1] : m <= my_lim;
       if (__any_sync(0xffffffffu, mine)) {  // rescan (tcgen05.ld must stay warp-converged)
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 64) {
           uint32_t r[64];
           tmem_ld64(tbase + c0, r);
           tmem_ld_wait();
-          if (mine) {
+          if (MODE == 0) {
+            if (mine) {
+#pragma unroll
+              for (int c = 0; c < 64; ++c) {
+                const float v = fmaf(-2.0f, __uint_as_float(r[c]), __ldg(ynt + c0 + c));
+                if (v < tv[TOPK - 1]) topk_insert(v, t * BN + c0 + c, tv, tj);
+              }
+            }
+          } else {
 #pragma unroll
             for (int c = 0; c < 64; ++c) {
               const float v = fmaf(-2.0f, __uint_as_float(r[c]), __ldg(ynt + c0 + c));
-              if (v < tv[TOPK - 1]) topk_insert(v, t * BN + c0 + c, tv, tj);
+              const bool hit = mine && v <= my_lim;
+              const unsigned bal = __ballot_sync(0xffffffffu, hit);
+              if (bal) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(n_pairs, (unsigned long long)__popc(bal));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                const unsigned long long slot = base + __popc(bal & ((1u << lane) - 1u));
+                if (hit && (int64_t)slot < cap)
+                  pairs[slot] = ((unsigned long long)grow << 32) | (unsigned long long)(t * BN + c0 + c);
+              }
             }
           }
         }
@@ -237,12 +261,11 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
       tc_fence_before();
       mbar_arrive(acc_empty + ab);
     }
-    const int64_t g = (int64_t)rb * BM + row;
-    if (g < nx) {
+    if (MODE == 0 && grow < nx) {
 #pragma unroll
       for (int q = 0; q < TOPK; ++q) {
-        topv[g * TOPK + q] = tv[q];
-        topj[g * TOPK + q] = tj[q];
+        topv[grow * TOPK + q] = tv[q];
+        topj[grow * TOPK + q] = tj[q];
       }
     }
   }
@@ -280,7 +303,7 @@ __global__ void certify_exact(const float* __restrict__ topv, const int32_t* __r
                               const int32_t* __restrict__ y_orig, const double* __restrict__ xinfo,
                               const unsigned* __restrict__ ymax, const T* __restrict__ X, const T* __restrict__ Y,
                               int32_t* __restrict__ nn, double* __restrict__ dist, int32_t* __restrict__ overflow,
-                              int32_t* __restrict__ n_overflow) {
+                              int32_t* __restrict__ n_overflow, float* __restrict__ overflow_lim) {
   const int nx = *cnt_x;
   const double Nmax = __uint_as_float(ymax[0]), Rmax = __uint_as_float(ymax[1]), Hmax = __uint_as_float(ymax[2]);
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < nx; u += gridDim.x * blockDim.x) {
@@ -301,6 +324,7 @@ __global__ void certify_exact(const float* __restrict__ topv, const int32_t* __r
     if ((double)tv[TOPK - 1] <= lim) {  // candidates may extend past the top-4
       const int slot = atomicAdd(n_overflow, 1);
       overflow[slot] = u;
+      overflow_lim[slot] = __double2float_ru(lim);
       continue;
     }
     double bd = INFINITY;
@@ -317,13 +341,62 @@ __global__ void certify_exact(const float* __restrict__ topv, const int32_t* __r
   }
 }
 
-// exact full scans for overflow rows: one block per row, threads stride Y
+// overflow row q -> source row of X (composition of the two index lists)
+__global__ void gather_rows(const int32_t* __restrict__ overflow, const int32_t* __restrict__ n_overflow,
+                            const int32_t* __restrict__ x_idx, int32_t* __restrict__ out) {
+  const int n = *n_overflow;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x)
+    out[q] = x_idx ? x_idx[overflow[q]] : overflow[q];
+}
+
+// exact distance of every enumerated (overflow row, column) pair; per row the
+// minimum distance bits, then the lowest original column at that distance
+template <class T>
+__global__ void pair_dist_min(const unsigned long long* __restrict__ pairs,
+                              const unsigned long long* __restrict__ n_pairs, int64_t cap,
+                              const int32_t* __restrict__ xsrc, const int32_t* __restrict__ y_idx,
+                              const T* __restrict__ X, const T* __restrict__ Y, double* __restrict__ pd,
+                              unsigned long long* __restrict__ best_bits) {
+  const int64_t n = min((int64_t)*n_pairs, cap);
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(pairs[k] >> 32), jt = (int)(pairs[k] & 0xffffffffu);
+    const int yj = y_idx ? y_idx[jt] : jt;
+    const double d = exact_dist(X + (int64_t)xsrc[q] * KD, Y + (int64_t)yj * KD);
+    pd[k] = d;
+    atomicMin(best_bits + q, (unsigned long long)__double_as_longlong(d));
+  }
+}
+
+template <class T>
+__global__ void pair_argmin(const unsigned long long* __restrict__ pairs, const unsigned long long* __restrict__ n_pairs,
+                            int64_t cap, const int32_t* __restrict__ y_idx, const double* __restrict__ pd,
+                            const unsigned long long* __restrict__ best_bits, int* __restrict__ best_j) {
+  const int64_t n = min((int64_t)*n_pairs, cap);
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(pairs[k] >> 32), jt = (int)(pairs[k] & 0xffffffffu);
+    if ((unsigned long long)__double_as_longlong(pd[k]) == best_bits[q]) atomicMin(best_j + q, y_idx ? y_idx[jt] : jt);
+  }
+}
+
+__global__ void pair_write(const int32_t* __restrict__ n_overflow, const int32_t* __restrict__ xsrc,
+                           const unsigned long long* __restrict__ best_bits, const int* __restrict__ best_j,
+                           int32_t* __restrict__ nn, double* __restrict__ dist) {
+  const int n = *n_overflow;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+    nn[xsrc[q]] = best_j[q];
+    dist[xsrc[q]] = __longlong_as_double((long long)best_bits[q]);
+  }
+}
+
+// exact full scans (only if the enumerated pairs overflowed their buffer)
 template <class T>
 __global__ void exact_rows(const int32_t* __restrict__ rows, const int32_t* __restrict__ n_rows,
                            const int32_t* __restrict__ x_orig, const T* __restrict__ X, const T* __restrict__ Y,
-                           int64_t ny, int32_t* __restrict__ nn, double* __restrict__ dist) {
+                           int64_t ny, int32_t* __restrict__ nn, double* __restrict__ dist,
+                           const unsigned long long* __restrict__ n_pairs, int64_t cap) {
   __shared__ double sd[32];
   __shared__ int sj[32];
+  if (n_pairs && (int64_t)*n_pairs <= cap) return;  // the enumeration was complete
   const int n = *n_rows;
   for (int q = blockIdx.x; q < n; q += gridDim.x) {
     const int u = rows[q];
@@ -383,12 +456,16 @@ __global__ void row_hash(const T* __restrict__ X, int64_t n, unsigned long long*
 
 // sorted (hash, index): rep = first index of the equal-hash run when the rows
 // are bitwise equal to it, else itself.  flag[i] = (rep == i).
+__global__ void run_heads(const unsigned long long* __restrict__ hs, int64_t n, int32_t* __restrict__ head) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+    head[p] = (p == 0 || hs[p - 1] != hs[p]) ? (int32_t)p : 0;
+}
+
 template <class T>
-__global__ void mark_reps(const T* __restrict__ X, int64_t n, const unsigned long long* __restrict__ hs,
+__global__ void mark_reps(const T* __restrict__ X, int64_t n, const int32_t* __restrict__ run_start,
                           const int32_t* __restrict__ idx, int32_t* __restrict__ rep, int32_t* __restrict__ flag) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-    int64_t s = p;
-    while (s > 0 && hs[s - 1] == hs[p]) --s;  // runs are tiny except for saturated clusters
+    const int64_t s = run_start[p];
     const int i = idx[p], l = idx[s];
     bool same = true;
     if (l != i)
@@ -445,19 +522,23 @@ struct TcWs {
   float *yn, *xn, *topv;
   double *xinfo, *yinfo;
   unsigned* ymax;
-  int32_t *topj, *nn12, *nn21, *overflow, *n_overflow, *colflag, *cols, *n_cols;
-  double *d12, *d21;
+  int32_t *topj, *nn12, *nn21, *overflow, *n_overflow, *colflag, *cols, *n_cols, *xsrc, *best_j;
+  double *d12, *d21, *pd;
+  float* lim;
+  unsigned long long *pairs, *n_pairs, *best_bits;
+  int64_t pair_cap;
 };
 
 inline int64_t rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 size_t cub_need(int64_t n) {
-  size_t a = 0, b = 0;
+  size_t a = 0, b = 0, c = 0;
+  cub::DeviceScan::InclusiveScan(nullptr, c, (const int32_t*)nullptr, (int32_t*)nullptr, cub::Max(), (int)n);
   cub::DeviceRadixSort::SortPairs(nullptr, a, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
                                   (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
   cub::DeviceSelect::Flagged(nullptr, b, (const int32_t*)nullptr, (const int32_t*)nullptr, (int32_t*)nullptr,
                              (int32_t*)nullptr, (int)n);
-  return std::max(a, b);
+  return std::max(std::max(a, b), c);
 }
 
 TcWs carve_tc(void* base, int64_t n1, int64_t n2, size_t* used) {
@@ -494,6 +575,14 @@ TcWs carve_tc(void* base, int64_t n1, int64_t n2, size_t* used) {
   w.d21 = ar.take<double>(n2);
   w.overflow = ar.take<int32_t>(nmax);
   w.n_overflow = ar.take<int32_t>(1);
+  w.lim = ar.take<float>(rup(nmax, BM));
+  w.xsrc = ar.take<int32_t>(nmax);
+  w.best_j = ar.take<int32_t>(nmax);
+  w.best_bits = ar.take<unsigned long long>(nmax);
+  w.pair_cap = std::max<int64_t>(1 << 22, 64 * nmax);
+  w.pairs = ar.take<unsigned long long>(w.pair_cap);
+  w.pd = ar.take<double>(w.pair_cap);
+  w.n_pairs = ar.take<unsigned long long>(1);
   w.colflag = ar.take<int32_t>(n2);
   w.cols = ar.take<int32_t>(n2);
   w.n_cols = ar.take<int32_t>(1);
@@ -516,7 +605,12 @@ int dedupe(const T* X, int64_t n, Side& s, const TcWs& w, cudaStream_t st) {
   size_t tb = w.cub_bytes;
   cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, s.keys, s.keys_sorted, s.iota, s.vals_sorted, (int)n, 0, 64, st);
   PS_LAUNCHED("cub_sort(hash)");
-  mark_reps<T><<<grid_for(n, 256), 256, 0, st>>>(X, n, s.keys_sorted, s.vals_sorted, s.rep, s.flag);
+  run_heads<<<grid_for(n, 256), 256, 0, st>>>(s.keys_sorted, n, s.flag);
+  PS_LAUNCHED("run_heads");
+  tb = w.cub_bytes;
+  cub::DeviceScan::InclusiveScan(w.cub_tmp, tb, s.flag, s.uniq, cub::Max(), (int)n, st);  // run start per position
+  PS_LAUNCHED("cub_scan(run_start)");
+  mark_reps<T><<<grid_for(n, 256), 256, 0, st>>>(X, n, s.uniq, s.vals_sorted, s.rep, s.flag);
   PS_LAUNCHED("mark_reps");
   iota32<<<grid_for(n, 256), 256, 0, st>>>(s.iota, n);
   PS_LAUNCHED("iota32");
@@ -543,15 +637,37 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   PS_LAUNCHED("prep_tiles(Y)");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(nn_topk_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    cudaFuncSetAttribute(nn_topk_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    cudaFuncSetAttribute(nn_topk_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
     attr = true;
   }
-  nn_topk_tc<<<(unsigned)(xrows / BM), kThreads, kSmemBytes, st>>>(w.xt, w.yt, w.yn, n_x, n_y, w.topv, w.topj);
-  PS_LAUNCHED("nn_topk_tc");
+  nn_topk_tc<0><<<(unsigned)(xrows / BM), kThreads, kSmemBytes, st>>>(w.xt, w.yt, w.yn, n_x, n_y, w.topv, w.topj,
+                                                                       nullptr, nullptr, nullptr, 0);
+  PS_LAUNCHED("nn_topk_tc<top4>");
   certify_exact<T><<<grid_for(nx_max, 128), 128, 0, st>>>(w.topv, w.topj, n_x, x_idx, y_idx, w.xinfo, w.ymax, X, Y,
-                                                          nn, dist, w.overflow, w.n_overflow);
+                                                          nn, dist, w.overflow, w.n_overflow, w.lim);
   PS_LAUNCHED("certify_exact");
-  exact_rows<T><<<148 * 4, 256, 0, st>>>(w.overflow, w.n_overflow, x_idx, X, Y, ny_all, nn, dist);
+  // rows with more near-tied candidates than the top-4: enumerate every
+  // column within their certified limit on the tensor cores, then decide exactly
+  gather_rows<<<grid_for(nx_max, 256), 256, 0, st>>>(w.overflow, w.n_overflow, x_idx, w.xsrc);
+  PS_LAUNCHED("gather_rows");
+  prep_tiles<T><<<grid_for(xrows, 8), 256, 0, st>>>(X, w.xsrc, w.n_overflow, 0, xrows, BM, w.xt, w.xn, w.xinfo,
+                                                      nullptr, 0);
+  PS_LAUNCHED("prep_tiles(overflow)");
+  cudaMemsetAsync(w.n_pairs, 0, sizeof(unsigned long long), st);
+  cudaMemsetAsync(w.best_bits, 0xff, nx_max * sizeof(unsigned long long), st);
+  cudaMemsetAsync(w.best_j, 0x7f, nx_max * sizeof(int32_t), st);
+  nn_topk_tc<1><<<(unsigned)(xrows / BM), kThreads, kSmemBytes, st>>>(w.xt, w.yt, w.yn, w.n_overflow, n_y, nullptr,
+                                                                       nullptr, w.lim, w.pairs, w.n_pairs, w.pair_cap);
+  PS_LAUNCHED("nn_topk_tc<enumerate>");
+  pair_dist_min<T><<<148 * 8, 256, 0, st>>>(w.pairs, w.n_pairs, w.pair_cap, w.xsrc, y_idx, X, Y, w.pd, w.best_bits);
+  PS_LAUNCHED("pair_dist_min");
+  pair_argmin<T><<<148 * 8, 256, 0, st>>>(w.pairs, w.n_pairs, w.pair_cap, y_idx, w.pd, w.best_bits, w.best_j);
+  PS_LAUNCHED("pair_argmin");
+  pair_write<<<grid_for(nx_max, 256), 256, 0, st>>>(w.n_overflow, w.xsrc, w.best_bits, w.best_j, nn, dist);
+  PS_LAUNCHED("pair_write");
+  exact_rows<T><<<148 * 4, 256, 0, st>>>(w.overflow, w.n_overflow, x_idx, X, Y, ny_all, nn, dist, w.n_pairs,
+                                         w.pair_cap);
   PS_LAUNCHED("exact_rows");
   return PS_OK;
 }
@@ -596,6 +712,11 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   if (rc) return rc;
   mark();
   const int of1 = prof ? count_of(w.n_overflow) : 0;
+  unsigned long long np1 = 0;
+  if (prof) {
+    cudaMemcpyAsync(&np1, w.n_pairs, 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+  }
   // pass 2: the columns that can be matched against the distinct rows of A
   cudaMemsetAsync(w.colflag, 0, n2 * sizeof(int32_t), st);
   mark_columns<<<grid_for(n1, 256), 256, 0, st>>>(w.a.uniq, w.a.n_uniq, w.nn12, w.d12, delta_s, w.colflag);
@@ -617,9 +738,9 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
     float t[8] = {0};
     for (int i = 1; i < nev; ++i) cudaEventElapsedTime(&t[i], ev[i - 1], ev[i]);
     fprintf(stderr,
-            "[tc] n1=%lld n2=%lld uniqA=%d uniqB=%d cols=%d overflow1=%d overflow2=%d | dedupe %.3f ms pass1 %.3f ms "
-            "select %.3f ms pass2 %.3f ms\n",
-            (long long)n1, (long long)n2, count_of(w.a.n_uniq), count_of(w.b.n_uniq), count_of(w.n_cols), of1,
+            "[tc] n1=%lld n2=%lld uniqA=%d uniqB=%d cols=%d overflow1=%d pairs1=%llu overflow2=%d | dedupe %.3f ms "
+            "pass1 %.3f ms select %.3f ms pass2 %.3f ms\n",
+            (long long)n1, (long long)n2, count_of(w.a.n_uniq), count_of(w.b.n_uniq), count_of(w.n_cols), of1, np1,
             count_of(w.n_overflow), t[1], t[2], t[3], t[4]);
     for (int i = 0; i < nev; ++i) cudaEventDestroy(ev[i]);
   }
