@@ -294,6 +294,24 @@ __device__ __forceinline__ double exact_dist(const T* __restrict__ a, const T* _
                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7]))));
 }
 
+// The same distance computed by an aligned group of 8 lanes: lane t of the
+// group owns accumulator r[t] (elements 8m + t, m sequential), and the groups'
+// lanes combine in the reference's ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) order.
+// Loads of the group are 32-byte contiguous per step.  Result valid in lane t=0.
+template <class T>
+__device__ __forceinline__ double exact_dist8(const T* __restrict__ a, const T* __restrict__ b, int t) {
+  double r = 0.0;
+#pragma unroll
+  for (int m = 0; m < KD / 8; ++m) {
+    const double e = __dsub_rn((double)b[8 * m + t], (double)a[8 * m + t]);
+    r = __dadd_rn(r, __dmul_rn(e, e));
+  }
+  const double p1 = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 1));   // t even: r_t + r_{t+1}
+  const double p2 = __dadd_rn(p1, __shfl_down_sync(0xffffffffu, p1, 2)); // t % 4 == 0
+  const double p4 = __dadd_rn(p2, __shfl_down_sync(0xffffffffu, p2, 4)); // t == 0
+  return __dsqrt_rn(p4);
+}
+
 // One thread per X' row u.  x_orig[u] / y_orig[j'] map tile rows to original
 // indices (ties break on original indices).  Writes nn[x_orig[u]] and d[...];
 // rows whose candidates may not fit the top-4 are appended to `overflow`.
@@ -306,9 +324,14 @@ __global__ void certify_exact(const float* __restrict__ topv, const int32_t* __r
                               int32_t* __restrict__ n_overflow, float* __restrict__ overflow_lim) {
   const int nx = *cnt_x;
   const double Nmax = __uint_as_float(ymax[0]), Rmax = __uint_as_float(ymax[1]), Hmax = __uint_as_float(ymax[2]);
-  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < nx; u += gridDim.x * blockDim.x) {
-    const int xi = x_orig ? x_orig[u] : u;
-    const double rx = xinfo[3 * u + 1], hx = xinfo[3 * u + 2];
+  const int t = threadIdx.x & 7;
+  const int per_block = blockDim.x >> 3;
+  for (int ub = blockIdx.x * per_block; ub < nx; ub += gridDim.x * per_block) {  // 8 lanes per row
+    const int u = ub + (threadIdx.x >> 3);
+    const bool live = u < nx;
+    const int uu = live ? u : 0;
+    const int xi = x_orig ? x_orig[uu] : uu;
+    const double rx = xinfo[3 * uu + 1], hx = xinfo[3 * uu + 2];
     // |v - (d^2 - |x|^2)| <= 2(|x - x_h||y| + |x_h||y - y_h|) + 2 g |x_h||y_h| + rounding of v
     const double gamma = 128.0 * 2.384185791015625e-07;  // 128 * 2^-22 (fp32 accumulation)
     const double E = 1.01 * (2.0 * (rx * Nmax + hx * Rmax) + 2.0 * gamma * hx * Hmax +
@@ -317,27 +340,30 @@ __global__ void certify_exact(const float* __restrict__ topv, const int32_t* __r
     int tj[TOPK];
 #pragma unroll
     for (int q = 0; q < TOPK; ++q) {
-      tv[q] = topv[(int64_t)u * TOPK + q];
-      tj[q] = topj[(int64_t)u * TOPK + q];
+      tv[q] = topv[(int64_t)uu * TOPK + q];
+      tj[q] = topj[(int64_t)uu * TOPK + q];
     }
     const double lim = (double)tv[0] + 2.0 * E;
-    if ((double)tv[TOPK - 1] <= lim) {  // candidates may extend past the top-4
+    const bool over = (double)tv[TOPK - 1] <= lim;  // candidates may extend past the top-4
+    if (live && over && t == 0) {
       const int slot = atomicAdd(n_overflow, 1);
       overflow[slot] = u;
       overflow_lim[slot] = __double2float_ru(lim);
-      continue;
     }
     double bd = INFINITY;
     int bj = INT32_MAX;
 #pragma unroll
     for (int q = 0; q < TOPK; ++q) {
-      if (tj[q] < 0 || (double)tv[q] > lim) continue;
-      const int yj = y_orig ? y_orig[tj[q]] : tj[q];
-      const double dd = exact_dist(X + (int64_t)xi * KD, Y + (int64_t)yj * KD);
-      if (dd < bd || (dd == bd && yj < bj)) { bd = dd; bj = yj; }
+      const bool cand = live && !over && tj[q] >= 0 && (double)tv[q] <= lim;
+      if (!__any_sync(0xffffffffu, cand)) continue;  // warp-uniform skip
+      const int yj = cand ? (y_orig ? y_orig[tj[q]] : tj[q]) : 0;
+      const double dd = exact_dist8(X + (int64_t)xi * KD, Y + (int64_t)yj * KD, t);
+      if (cand && (dd < bd || (dd == bd && yj < bj))) { bd = dd; bj = yj; }
     }
-    nn[xi] = bj;
-    dist[xi] = bd;
+    if (live && !over && t == 0) {
+      nn[xi] = bj;
+      dist[xi] = bd;
+    }
   }
 }
 
@@ -358,12 +384,21 @@ __global__ void pair_dist_min(const unsigned long long* __restrict__ pairs,
                               const T* __restrict__ X, const T* __restrict__ Y, double* __restrict__ pd,
                               unsigned long long* __restrict__ best_bits) {
   const int64_t n = min((int64_t)*n_pairs, cap);
-  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-    const int q = (int)(pairs[k] >> 32), jt = (int)(pairs[k] & 0xffffffffu);
-    const int yj = y_idx ? y_idx[jt] : jt;
-    const double d = exact_dist(X + (int64_t)xsrc[q] * KD, Y + (int64_t)yj * KD);
-    pd[k] = d;
-    atomicMin(best_bits + q, (unsigned long long)__double_as_longlong(d));
+  const int t = threadIdx.x & 7;
+  const int64_t per_block = blockDim.x >> 3;
+  // the loop bound depends only on the block, so whole warps stay converged for the shuffles
+  for (int64_t kb = (int64_t)blockIdx.x * per_block; kb < n; kb += (int64_t)gridDim.x * per_block) {
+    const int64_t k = kb + (threadIdx.x >> 3);
+    const bool live = k < n;
+    const unsigned long long pr = live ? pairs[k] : 0ull;
+    const int q = (int)(pr >> 32), jt = (int)(pr & 0xffffffffu);
+    const int yj = live ? (y_idx ? y_idx[jt] : jt) : 0;
+    const int xs = live ? xsrc[q] : 0;
+    const double d = exact_dist8(X + (int64_t)xs * KD, Y + (int64_t)yj * KD, t);
+    if (live && t == 0) {
+      pd[k] = d;
+      atomicMin(best_bits + q, (unsigned long long)__double_as_longlong(d));
+    }
   }
 }
 
@@ -644,7 +679,7 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   nn_topk_tc<0><<<(unsigned)(xrows / BM), kThreads, kSmemBytes, st>>>(w.xt, w.yt, w.yn, n_x, n_y, w.topv, w.topj,
                                                                        nullptr, nullptr, nullptr, 0);
   PS_LAUNCHED("nn_topk_tc<top4>");
-  certify_exact<T><<<grid_for(nx_max, 128), 128, 0, st>>>(w.topv, w.topj, n_x, x_idx, y_idx, w.xinfo, w.ymax, X, Y,
+  certify_exact<T><<<grid_for(nx_max, 32), 256, 0, st>>>(w.topv, w.topj, n_x, x_idx, y_idx, w.xinfo, w.ymax, X, Y,
                                                           nn, dist, w.overflow, w.n_overflow, w.lim);
   PS_LAUNCHED("certify_exact");
   // rows with more near-tied candidates than the top-4: enumerate every
@@ -660,7 +695,7 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   nn_topk_tc<1><<<(unsigned)(xrows / BM), kThreads, kSmemBytes, st>>>(w.xt, w.yt, w.yn, w.n_overflow, n_y, nullptr,
                                                                        nullptr, w.lim, w.pairs, w.n_pairs, w.pair_cap);
   PS_LAUNCHED("nn_topk_tc<enumerate>");
-  pair_dist_min<T><<<148 * 8, 256, 0, st>>>(w.pairs, w.n_pairs, w.pair_cap, w.xsrc, y_idx, X, Y, w.pd, w.best_bits);
+  pair_dist_min<T><<<148 * 16, 256, 0, st>>>(w.pairs, w.n_pairs, w.pair_cap, w.xsrc, y_idx, X, Y, w.pd, w.best_bits);
   PS_LAUNCHED("pair_dist_min");
   pair_argmin<T><<<148 * 8, 256, 0, st>>>(w.pairs, w.n_pairs, w.pair_cap, y_idx, w.pd, w.best_bits, w.best_j);
   PS_LAUNCHED("pair_argmin");
