@@ -327,3 +327,52 @@ def test_end_to_end_small_pair(golden):
     got_pairs = {(p.ref1, p.ref2) for p in pairs}
     assert len(want_pairs ^ got_pairs) <= 0.02 * len(want_pairs)
     assert corner_error((res.transform.theta, res.transform.t_x, res.transform.t_y), g["r__model"], 384, 400) <= 1e-3
+
+
+# ---------------------------------------------------------------------------
+# P3 on the tensor-core path (forced on for small problems)
+# ---------------------------------------------------------------------------
+
+@pytest.fixture()
+def force_tc(monkeypatch):
+    monkeypatch.setenv("PS_TC_MIN_PAIRS", "0")
+    monkeypatch.delenv("PS_MATCH_EXACT", raising=False)
+
+
+def test_matcher_tc_path_matches_reference_fixtures(golden, force_tc):
+    g = golden("matcher.npz")
+    for m in json.loads(str(g["meta"])):
+        if m["strategy"] != "nearest_neighbor":
+            continue
+        A, B = g[f"{m['label']}__A"], g[f"{m['label']}__B"]
+        for arr_a, arr_b in ((A, B), (A.astype(np.float64), B.astype(np.float64))):
+            pairs = Mt.match_features(described(arr_a), described(arr_b), R.MatcherConfig(m["delta_s"], m["strategy"]))
+            assert np.array_equal([p.ref1 for p in pairs], g[f"{m['tag']}__ref1"]), m["tag"]
+            assert np.array_equal([p.ref2 for p in pairs], g[f"{m['tag']}__ref2"]), m["tag"]
+            assert np.array_equal(np.array([p.delta for p in pairs]), g[f"{m['tag']}__delta"]), m["tag"]
+
+
+def test_matcher_tc_near_duplicate_clusters(force_tc):
+    """Clusters of bit-identical and of 1-ulp-apart rows: top-4 overflow, the
+    tensor-core enumeration of near-ties and the exact decision all engage."""
+    rng = np.random.default_rng(11)
+    base = rng.random((40, 128)).astype(np.float32)
+    base /= np.linalg.norm(base, axis=1, keepdims=True)
+    rows_a, rows_b = [], []
+    for c in range(40):
+        for _ in range(int(rng.integers(1, 30))):
+            v = base[c].copy()
+            if rng.random() < 0.5:  # perturb a few elements by one ulp
+                k = rng.integers(0, 128, size=3)
+                v[k] = np.nextafter(v[k], np.float32(2.0))
+            rows_a.append(v)
+        for _ in range(int(rng.integers(1, 30))):
+            v = base[c] + (rng.normal(0, 0.02, 128).astype(np.float32) if rng.random() < 0.3 else 0)
+            rows_b.append(v.astype(np.float32))
+    A, B = np.stack(rows_a), np.stack(rows_b)
+    A, B = A[rng.permutation(len(A))], B[rng.permutation(len(B))]
+    r1, r2, dl = device.match(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    w1, w2, wd = O.match(A.astype(np.float64), B.astype(np.float64))
+    assert np.array_equal(r1.cpu().numpy(), w1) and np.array_equal(r2.cpu().numpy(), w2)
+    assert np.array_equal(dl.cpu().numpy(), wd)
+    assert len(w1) >= 20
