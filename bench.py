@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--images", type=int, default=N_IMAGES)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-match", action="store_true", help="skip the C4 matching measurement")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run N steps untimed and exit")
     return ap.parse_args()
 
@@ -107,6 +108,75 @@ def cpu_baseline(steps=1, warmup=0, n_kp=CPU_SAMPLE_KP):
                 sample=(f"{P} processes x 1 image each: full detect + describe of the first {n_kp} of "
                         f"134400 keypoints, describe time extrapolated x{134400 / n_kp:.1f}; oracle port "
                         f"(numpy) of the reference algorithm"))
+
+
+# ---------------------------------------------------------------------------
+# C4 matching (BASELINE.json configs[3]): pair-matches/s on tensor cores
+# ---------------------------------------------------------------------------
+
+def _cpu_match_job(args):
+    """Oracle port: exact float64 MNN matching of an m x m sub-block."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    a, b = args
+    from oracle import lpsift_oracle as O
+
+    t0 = time.perf_counter()
+    O.match(a, b)
+    return a.shape[0] * b.shape[0] / (time.perf_counter() - t0)
+
+
+def bench_c4_matching(args, with_cpu=True, steps=5):
+    import torch
+
+    from paper_2405_08578_b200 import device, scenes
+    from paper_2405_08578_b200.records import DescriptorConfig
+
+    a, b = scenes.config4_pair(0)
+    cfg = DescriptorConfig(0.0625, 4, 36, True)  # L = 36 (SURVEY F4: literal {4,8,16} is rejected)
+    ds = []
+    for im in (a, b):
+        t = torch.from_numpy(im).cuda()
+        kp = device.detect(t, (36,), meta=False)
+        ds.append(device.describe(t, kp, cfg, scale_set=(36,))[0])
+        del t
+    n1, n2 = ds[0].shape[0], ds[1].shape[0]
+    for _ in range(2):
+        r = device.match(ds[0], ds[1])
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    times = []
+    for _ in range(steps):
+        s.record()
+        r = device.match(ds[0], ds[1])
+        e.record()
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e))
+    ms = statistics.median(times)
+    flops = 2.0 * n1 * n2 * 128
+    peak = 1641.9
+    pj = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(pj):
+        with open(pj) as f:
+            peak = float(json.load(f)["bf16_tflops"])
+    out = {"metric": "pair-matches/s (C4, 2x 8192x8192 crops, L=36, 128-d MNN, delta_s 0.35)",
+           "value": n1 * n2 / (ms / 1e3), "unit": "pair-matches/s", "ms_per_pair": round(ms, 3),
+           "n1": n1, "n2": n2, "matches": int(r[0].shape[0]),
+           "roofline": {"bound": "tensor", "achieved": round(flops / (ms / 1e3) / 1e12, 2), "peak": peak,
+                        "unit": "TFLOP/s", "frac": round(flops / (ms / 1e3) / 1e12 / peak, 4),
+                        "note": "algorithmic 2*n1*n2*128 over the whole match call (fp16 tcgen05 + exact f64 recheck)"},
+           "exactness": "bit-exact vs float64 reference arithmetic (tests/test_gpu_parity.py P3)"}
+    if with_cpu:
+        import multiprocessing as mp
+
+        m = 2000
+        A = ds[0][:m].double().cpu().numpy()
+        B = ds[1][:m].double().cpu().numpy()
+        P = os.cpu_count() or 1
+        with mp.get_context("fork").Pool(P) as pool:
+            rates = pool.map(_cpu_match_job, [(A, B)] * P)
+        out["cpu_baseline"] = {"value": float(sum(rates)), "unit": "pair-matches/s", "cores": P, "kind": "port",
+                               "sample": f"{P} processes x exact MNN of a {m}x{m} sub-block (oracle port)"}
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -306,6 +376,12 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(steps=1, warmup=0)
 
+    matching = None
+    if rank == 0 and world == 1 and not args.no_match:
+        del desc, imgs, dimg
+        torch.cuda.empty_cache()
+        matching = bench_c4_matching(args, with_cpu=not args.no_cpu)
+
     if rank == 0:
         out = {
             "metric": "Mpixel/s LP-SIFT detect+describe", "value": round(value, 2), "unit": "Mpixel/s",
@@ -315,7 +391,7 @@ def run_ours(args):
             "config": {"workload": WORKLOAD, "images": args.images, "image_hw": [NR, NC], "scales": list(SCALES),
                        "keypoints_per_image": K, "descriptor": "float32 128-d", "l2": "inputs larger than L2",
                        "parallelism": f"images sharded over {world} rank(s)"},
-            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "matching_c4": matching,
             "gpu_launches": int(launches), "clocks": clocks,
         }
         print(json.dumps(out), flush=True)
