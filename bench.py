@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-match", action="store_true", help="skip the C4 matching measurement")
+    ap.add_argument("--no-stitch", action="store_true", help="skip the C3 nine-image stitch measurement")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run N steps untimed and exit")
     return ap.parse_args()
 
@@ -177,6 +178,47 @@ def bench_c4_matching(args, with_cpu=True, steps=5):
         out["cpu_baseline"] = {"value": float(sum(rates)), "unit": "pair-matches/s", "cores": P, "kind": "port",
                                "sample": f"{P} processes x exact MNN of a {m}x{m} sub-block (oracle port)"}
     return out
+
+
+# ---------------------------------------------------------------------------
+# C3 nine-image stitch (BASELINE.json configs[2]): seconds at N GPUs
+# ---------------------------------------------------------------------------
+
+def bench_c3_stitch(args, world, rank, dev, steps=3):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_08578_b200 import mosaic, scenes
+    from paper_2405_08578_b200.pipeline import PipelineConfig
+
+    images, truth = scenes.config3_images(0)
+    ids = [f"img{k}" for k in range(9)]
+    cfg = PipelineConfig(window_min=32, window_max=128, ransac_iters=2000, ransac_tol=3.0)
+    engine = mosaic.GpuEngine(cfg)
+    mosaic.build_pairwise_table(images, cfg, engine=engine)  # warm-up (all ranks)
+    times = []
+    for _ in range(steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        table = mosaic.build_pairwise_table(images, cfg, engine=engine)
+        plan, placed = mosaic.plan_mosaic(table, ids)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = t.item()
+        times.append(dt)
+    n_pairs = len(table.entries) // 2
+    return {"metric": "9-image stitch seconds (C3: detect/describe 9 x 2688x1600, 36 pairs match + RANSAC, plan)",
+            "value": round(statistics.median(times), 4), "unit": "s", "higher_is_better": False,
+            "n_gpus": world, "registered_pairs": n_pairs, "placed": len(placed),
+            "rounds": len(plan.rounds), "unmatched": plan.final_unmatched,
+            "timing": "host wall clock around the whole call, CUDA-synchronized, max over ranks",
+            "parallelism": f"images then pairs sharded over {world} rank(s); NCCL all-gather of keypoint/descriptor "
+                           "slots and of the pair results"}
 
 
 # ---------------------------------------------------------------------------
@@ -376,6 +418,10 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(steps=1, warmup=0)
 
+    stitch = None
+    if not args.no_stitch:
+        stitch = bench_c3_stitch(args, world, rank, dev)
+
     matching = None
     if rank == 0 and world == 1 and not args.no_match:
         del desc, imgs, dimg
@@ -392,6 +438,7 @@ def run_ours(args):
                        "keypoints_per_image": K, "descriptor": "float32 128-d", "l2": "inputs larger than L2",
                        "parallelism": f"images sharded over {world} rank(s)"},
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "matching_c4": matching,
+            "stitch_c3": stitch,
             "gpu_launches": int(launches), "clocks": clocks,
         }
         print(json.dumps(out), flush=True)

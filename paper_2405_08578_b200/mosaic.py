@@ -1,0 +1,239 @@
+"""Pairwise registration table and mosaic planning, sharded over GPUs
+(reference mosaic.py:28-180).
+
+``build_pairwise_table`` runs the hot path for every image and every
+unordered image pair, exactly as the reference does (same per-pair seeds,
+same table convention), but partitions the work over the ranks of a
+``torch.distributed`` process group (one process per GPU):
+
+  phase 1  images   k  with k % world == rank  are detected + described;
+  exchange one all-gather of the fixed-size keypoint / descriptor slots
+           (the only data-path collective: every pair needs both images);
+  phase 2  pairs (a, b), a < b, in reference order, are split round-robin;
+  gather   one all-gather of the per-pair results (theta, t_x, t_y,
+           inliers, ok), after which every rank holds the same table.
+
+The compute is pluggable (``engine``) so the orchestration is testable on
+CPU with gloo; the product engine is ``GpuEngine`` (C-ABI kernels).
+``plan_mosaic`` is the reference's greedy host planner on the table.
+Compositing (warp_and_blend) is out of scope.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from .errors import ConfigError
+from .pipeline import pair_seed
+from .records import RigidTransform
+
+
+# ---- table (mosaic.py:28-53) -------------------------------------------------------
+
+@dataclass(frozen=True)
+class PairEntry:
+    transform: RigidTransform  # maps the column image's coordinates into the row image's frame
+    inlier_count: int
+
+
+@dataclass(eq=False)
+class PairwiseTransformTable:
+    n: int
+    entries: dict = field(default_factory=dict)
+
+    def present(self, a: int, b: int) -> bool:
+        return (a, b) in self.entries
+
+    def get(self, a: int, b: int) -> PairEntry:
+        return self.entries[(a, b)]
+
+    def set_pair(self, a: int, b: int, b_to_a: RigidTransform, inliers: int) -> None:
+        if a == b:
+            raise ValueError("diagonal entries are not allowed")
+        self.entries[(a, b)] = PairEntry(b_to_a, inliers)
+        self.entries[(b, a)] = PairEntry(b_to_a.inverse(), inliers)
+
+    def neighbor_count(self, a: int, among: set) -> int:
+        return sum(1 for b in among if b != a and (a, b) in self.entries)
+
+
+# ---- engines ----------------------------------------------------------------------------
+
+class GpuEngine:
+    """Hot path on the local GPU through the C-ABI (device.py)."""
+
+    def __init__(self, cfg):
+        self.cfg = cfg
+        self.device = torch.device("cuda", torch.cuda.current_device())
+
+    def comm_device(self):
+        return self.device
+
+    def prepare(self, images: list) -> tuple:
+        """images -> (rows int32 [B, cap], cols, desc float32 [B, cap, D], count int32 [B]) on device."""
+        from . import device
+
+        cfg = self.cfg
+        batch = torch.stack([torch.from_numpy(np.ascontiguousarray(im)) for im in images]).to(self.device)
+        alpha = cfg.alpha if cfg.alpha is not None else device.default_alpha(batch.shape[1], batch.shape[2])
+        kp = device.detect(batch, cfg.scale_set().sizes, alpha=alpha, meta=False)
+        desc = device.describe(batch, kp, cfg.descriptor_config(), alpha=alpha, scale_set=kp.scale_set)
+        return kp.row, kp.col, desc, kp.count
+
+    def register(self, ra, ca, da, na, rb, cb, db, nb, seed):
+        """match + RANSAC of one pair -> (ok, theta, t_x, t_y, n_inliers)."""
+        from . import device
+
+        cfg = self.cfg
+        mc, rc = cfg.matcher_config(), cfg.ransac_config(seed)
+        r1, r2, _ = device.match(da[:na], db[:nb], mc.delta_s, mc.strategy)
+        if int(r1.shape[0]) < rc.min_inliers:
+            return (False, 0.0, 0.0, 0.0, 0)
+        src, dst = device.pair_points(r1, r2, ra, ca, rb, cb)
+        out = device.ransac(src, dst, rc.iterations, rc.inlier_tol, rc.min_inliers, rc.seed)
+        if not out.ok:
+            return (False, 0.0, 0.0, 0.0, 0)
+        return (True, out.theta, out.t_x, out.t_y, int(out.inliers.shape[0]))
+
+
+# ---- distributed table -------------------------------------------------------------------
+
+def _group_info(group):
+    import torch.distributed as dist
+
+    if group is None and not (dist.is_available() and dist.is_initialized()):
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def _all_gather(t: torch.Tensor, world: int, group) -> torch.Tensor:
+    import torch.distributed as dist
+
+    if world == 1:
+        return t.unsqueeze(0)
+    out = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+    return out.view((world,) + tuple(t.shape))
+
+
+def build_pairwise_table(images: Sequence, cfg, *, engine=None, group=None) -> PairwiseTransformTable:
+    """mosaic.py:79-112 over the ranks of ``group`` (see module docstring)."""
+    n = len(images)
+    if n < 2:
+        raise ConfigError("pairwise table needs at least 2 images")
+    shapes = {tuple(np.asarray(im).shape) for im in images}
+    if len(shapes) != 1:
+        raise ConfigError("all images of a pairwise table must have the same size")
+    engine = engine or GpuEngine(cfg)
+    rank, world = _group_info(group)
+    dev = engine.comm_device()
+
+    # phase 1: my images (k % world == rank); slots padded to `per` images per rank
+    mine = list(range(rank, n, world))
+    per = -(-n // world)
+    rows, cols, desc, cnt = engine.prepare([np.asarray(images[k]) for k in mine]) if mine else (None,) * 4
+    if rows is None:  # ranks without images contribute empty slots of the agreed shape
+        probe = engine.prepare([np.asarray(images[0])])
+        rows, cols, desc, cnt = (x[:0] for x in probe)
+    cap, D = desc.shape[1], desc.shape[2]
+
+    def pad(t, fill=0):
+        if t.shape[0] == per:
+            return t
+        extra = torch.full((per - t.shape[0],) + tuple(t.shape[1:]), fill, dtype=t.dtype, device=t.device)
+        return torch.cat([t, extra])
+
+    # exchange: every rank receives every image's slots (image k = slot k // world ... see order below)
+    g_rows = _all_gather(pad(rows).to(dev), world, group)
+    g_cols = _all_gather(pad(cols).to(dev), world, group)
+    g_desc = _all_gather(pad(desc).to(dev), world, group)
+    g_cnt = _all_gather(pad(cnt).to(dev), world, group)
+
+    def img(k):  # image k lives on rank k % world, slot k // world
+        r, s = k % world, k // world
+        return g_rows[r, s], g_cols[r, s], g_desc[r, s], int(g_cnt[r, s])
+
+    # phase 2: pairs in reference order, round-robin over ranks
+    jobs = [(a, b) for a in range(n) for b in range(a + 1, n)]
+    res = torch.zeros((len(jobs), 5), dtype=torch.float64, device=dev)
+    for q in range(rank, len(jobs), world):
+        a, b = jobs[q]
+        ra, ca, da, na = img(a)
+        rb, cb, db, nb = img(b)
+        ok, th, tx, ty, ni = engine.register(ra, ca, da, na, rb, cb, db, nb, pair_seed(cfg.seed, a, b))
+        res[q] = torch.tensor([float(ok), th, tx, ty, float(ni)], dtype=torch.float64)
+    # gather: each pair was computed by exactly one rank, the others hold zeros
+    allres = _all_gather(res, world, group).sum(dim=0).cpu().numpy()
+    table = PairwiseTransformTable(n=n)
+    for q, (a, b) in enumerate(jobs):
+        ok, th, tx, ty, ni = allres[q]
+        if ok > 0.5:
+            # ransac gives a -> b; the (a, b) entry maps b into a's frame (mosaic.py:108-111)
+            table.set_pair(a, b, RigidTransform(th, tx, ty).inverse(), int(ni))
+    return table
+
+
+# ---- planning (mosaic.py:115-180) -----------------------------------------------------------
+
+@dataclass(eq=False)
+class MosaicRound:
+    reference_id: str
+    stitched_ids: list
+
+
+@dataclass(eq=False)
+class MosaicPlan:
+    rounds: list
+    final_unmatched: list
+    placements: dict = field(default_factory=dict)
+
+
+def select_reference(table: PairwiseTransformTable, remaining: set) -> int:
+    if not remaining:
+        raise ValueError("remaining set is empty")
+    return min(remaining, key=lambda a: (-table.neighbor_count(a, remaining), a))
+
+
+def _best_link(table: PairwiseTransformTable, candidate: int, placed: dict):
+    links = [p for p in placed if table.present(p, candidate)]
+    if not links:
+        return None
+    return min(links, key=lambda p: (-table.get(p, candidate).inlier_count, p))
+
+
+def plan_mosaic(table: PairwiseTransformTable, ids: Sequence[str]):
+    """Greedy rounds: the most-connected remaining image anchors a round and
+    every reachable image is placed by composing along its best link."""
+    remaining = set(range(table.n))
+    placed: dict = {}
+    rounds, unmatched = [], []
+    while remaining:
+        ref = select_reference(table, remaining)
+        if not placed:
+            placed[ref] = RigidTransform.identity()
+        else:
+            link = _best_link(table, ref, placed)
+            if link is None:
+                remaining.discard(ref)
+                unmatched.append(ref)
+                continue
+            placed[ref] = placed[link].compose(table.get(link, ref).transform)
+        remaining.discard(ref)
+        stitched, progress = [], True
+        while progress:
+            progress = False
+            for cand in sorted(remaining):
+                link = _best_link(table, cand, placed)
+                if link is None:
+                    continue
+                placed[cand] = placed[link].compose(table.get(link, cand).transform)
+                remaining.discard(cand)
+                stitched.append(cand)
+                progress = True
+        rounds.append(MosaicRound(ids[ref], [ids[i] for i in stitched]))
+    plan = MosaicPlan(rounds, [ids[i] for i in sorted(unmatched)], {ids[i]: t for i, t in placed.items()})
+    return plan, placed

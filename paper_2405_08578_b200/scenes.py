@@ -114,3 +114,41 @@ def config4_pair(seed: int = 0) -> tuple[np.ndarray, np.ndarray]:
     """C4: two 8192x8192 crops of scene(8192, 12288) with 50% overlap."""
     s = scene(8192, 12288, seed)
     return s[:, 0:8192].copy(), s[:, 4096:12288].copy()
+
+
+def _warp_crop(src: np.ndarray, r0: int, c0: int, h: int, w: int, theta: float, scale: float) -> np.ndarray:
+    """Crop [r0:r0+h, c0:c0+w] of src rotated by theta and scaled about its
+    centre: output (r, c) samples src at centre + R(theta) (p - centre) / scale,
+    bilinear, clamp-to-edge."""
+    from scipy.ndimage import map_coordinates
+
+    cy, cx = r0 + (h - 1) / 2.0, c0 + (w - 1) / 2.0
+    rr, cc = np.meshgrid(np.arange(h, dtype=np.float64) + r0 - cy, np.arange(w, dtype=np.float64) + c0 - cx,
+                         indexing="ij")
+    ct, st = math.cos(theta), math.sin(theta)
+    sx = (ct * cc - st * rr) / scale + cx
+    sy = (st * cc + ct * rr) / scale + cy
+    return map_coordinates(src.astype(np.float64), [sy, sx], order=1, mode="nearest")
+
+
+def config3_images(seed: int = 0) -> tuple[list, list]:
+    """C3: 3x3 grid of 1600x2688 crops of scene(4200, 7000).
+
+    Each crop gets rotation U[-5, 5] deg and scale U[0.95, 1.05] about its
+    centre (bilinear, clamp-to-edge), + N(0, 2^2) noise, rint/clip to uint8;
+    the order is shuffled by default_rng(seed).permutation(9).  Returns
+    (images, truth) with truth[k] = (row0, col0, theta, scale) of image k.
+    """
+    src = scene(4200, 7000, seed)
+    rng = np.random.default_rng(seed + 1000)
+    h, w = 1600, 2688
+    out, truth = [], []
+    for r0 in (180, 1300, 2420):
+        for c0 in (274, 2156, 4037):
+            theta = math.radians(rng.uniform(-5.0, 5.0))
+            sc = rng.uniform(0.95, 1.05)
+            img = _warp_crop(src, r0, c0, h, w, theta, sc) + rng.normal(0.0, 2.0, size=(h, w))
+            out.append(np.clip(np.rint(img), 0, 255).astype(np.uint8))
+            truth.append((r0, c0, theta, sc))
+    order = np.random.default_rng(seed).permutation(9)
+    return [out[k] for k in order], [truth[k] for k in order]
