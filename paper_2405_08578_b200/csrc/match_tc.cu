@@ -38,11 +38,17 @@ constexpr int BM = 128;   // X rows per CTA (= TMEM lanes)
 constexpr int BN = 256;   // Y rows per tile (= MMA N, TMEM columns)
 constexpr int KD = 128;   // descriptor length
 constexpr int TOPK = 4;
-constexpr int STAGES = 3;
+constexpr int STAGES_TOP = 3;   // Y-tile stages of the top-4 pass
+constexpr int STAGES_ENUM = 2;  // the enumeration pass trades one stage for per-warp hit buffers
+constexpr int HITBUF = 1024;    // hits staged per epilogue warp before one bulk append
 constexpr uint32_t A_BYTES = BM * KD * 2;  // 32 KB
 constexpr uint32_t B_BYTES = BN * KD * 2;  // 64 KB
 constexpr int kThreads = 192;              // warp 0 TMA, warp 1 MMA/TMEM, warps 2-5 epilogue
-constexpr size_t kSmemBytes = 1024 + A_BYTES + STAGES * (size_t)B_BYTES + 256;
+template <int MODE>
+constexpr size_t smem_bytes() {
+  return 1024 + A_BYTES + (MODE == 0 ? STAGES_TOP : STAGES_ENUM) * (size_t)B_BYTES + 256 +
+         (MODE == 0 ? 0 : 4 * (HITBUF * 8 + 16));
+}
 
 // ---- operand preparation ----------------------------------------------------------
 // Row u of the output (u < count) is source row idx[u] (or u); rows >= count are
@@ -126,6 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
                                                           int32_t* __restrict__ topj, const float* __restrict__ lim,
                                                           unsigned long long* __restrict__ pairs,
                                                           unsigned long long* __restrict__ n_pairs, int64_t cap) {
+  constexpr int STAGES = MODE == 0 ? STAGES_TOP : STAGES_ENUM;
   extern __shared__ uint8_t smem_raw[];
   const int nx = *cnt_x, ny = *cnt_y;
   const int rb = blockIdx.x;
@@ -141,8 +148,12 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
   uint64_t* acc_full = b_empty + STAGES;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  // MODE 1: per-epilogue-warp hit buffer + fill counter
+  unsigned long long* hitbuf = reinterpret_cast<unsigned long long*>(bars + 32);
+  int* hitcnt = reinterpret_cast<int*>(hitbuf + 4 * HITBUF);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  if (MODE == 1 && threadIdx.x < 4) hitcnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     mbar_init(a_full, 1);
     for (int s = 0; s < STAGES; ++s) {
@@ -209,7 +220,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
       tc_fence_after();
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + ab * BN;
       const float* ynt = yn + (size_t)t * BN;
-      float m = INFINITY;
+      float m0 = INFINITY, m1 = INFINITY, m2 = INFINITY, m3 = INFINITY;  // independent chains
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 64) {
         uint32_t r[64];
@@ -219,12 +230,13 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
           const float4 y = __ldg(y4 + q);
-          m = fminf(m, fmaf(-2.0f, __uint_as_float(r[4 * q + 0]), y.x));
-          m = fminf(m, fmaf(-2.0f, __uint_as_float(r[4 * q + 1]), y.y));
-          m = fminf(m, fmaf(-2.0f, __uint_as_float(r[4 * q + 2]), y.z));
-          m = fminf(m, fmaf(-2.0f, __uint_as_float(r[4 * q + 3]), y.w));
+          m0 = fminf(m0, fmaf(-2.0f, __uint_as_float(r[4 * q + 0]), y.x));
+          m1 = fminf(m1, fmaf(-2.0f, __uint_as_float(r[4 * q + 1]), y.y));
+          m2 = fminf(m2, fmaf(-2.0f, __uint_as_float(r[4 * q + 2]), y.z));
+          m3 = fminf(m3, fmaf(-2.0f, __uint_as_float(r[4 * q + 3]), y.w));
         }
       }
+      const float m = fminf(fminf(m0, m1), fminf(m2, m3));
       const bool mine = MODE == 0 ? m < tv[TOPK - 1] : m <= my_lim;
       if (__any_sync(0xffffffffu, mine)) {  // rescan (tcgen05.ld must stay warp-converged)
 #pragma unroll 1
@@ -241,25 +253,47 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
               }
             }
           } else {
+            unsigned long long* hb = hitbuf + quarter * HITBUF;
+            int fill = hitcnt[quarter];
 #pragma unroll
             for (int c = 0; c < 64; ++c) {
               const float v = fmaf(-2.0f, __uint_as_float(r[c]), __ldg(ynt + c0 + c));
               const bool hit = mine && v <= my_lim;
               const unsigned bal = __ballot_sync(0xffffffffu, hit);
               if (bal) {
-                unsigned long long base = 0;
-                if (lane == 0) base = atomicAdd(n_pairs, (unsigned long long)__popc(bal));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                const unsigned long long slot = base + __popc(bal & ((1u << lane) - 1u));
-                if (hit && (int64_t)slot < cap)
-                  pairs[slot] = ((unsigned long long)grow << 32) | (unsigned long long)(t * BN + c0 + c);
+                if (hit)
+                  hb[fill + __popc(bal & ((1u << lane) - 1u))] =
+                      ((unsigned long long)grow << 32) | (unsigned long long)(t * BN + c0 + c);
+                fill += __popc(bal);
+                if (fill > HITBUF - 32) {  // flush: one global atomic per buffer
+                  __syncwarp();
+                  unsigned long long base = 0;
+                  if (lane == 0) base = atomicAdd(n_pairs, (unsigned long long)fill);
+                  base = __shfl_sync(0xffffffffu, base, 0);
+                  for (int e = lane; e < fill; e += 32)
+                    if ((int64_t)(base + e) < cap) pairs[base + e] = hb[e];
+                  __syncwarp();
+                  fill = 0;
+                }
               }
             }
+            __syncwarp();
+            if (lane == 0) hitcnt[quarter] = fill;
+            __syncwarp();
           }
         }
       }
       tc_fence_before();
       mbar_arrive(acc_empty + ab);
+    }
+    if (MODE == 1) {
+      unsigned long long* hb = hitbuf + quarter * HITBUF;
+      const int fill = hitcnt[quarter];
+      unsigned long long base = 0;
+      if (lane == 0 && fill) base = atomicAdd(n_pairs, (unsigned long long)fill);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      for (int e = lane; e < fill; e += 32)
+        if ((int64_t)(base + e) < cap) pairs[base + e] = hb[e];
     }
     if (MODE == 0 && grow < nx) {
 #pragma unroll
@@ -672,11 +706,11 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   PS_LAUNCHED("prep_tiles(Y)");
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(nn_topk_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-    cudaFuncSetAttribute(nn_topk_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    cudaFuncSetAttribute(nn_topk_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<0>());
+    cudaFuncSetAttribute(nn_topk_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<1>());
     attr = true;
   }
-  nn_topk_tc<0><<<(unsigned)(xrows / BM), kThreads, kSmemBytes, st>>>(w.xt, w.yt, w.yn, n_x, n_y, w.topv, w.topj,
+  nn_topk_tc<0><<<(unsigned)(xrows / BM), kThreads, smem_bytes<0>(), st>>>(w.xt, w.yt, w.yn, n_x, n_y, w.topv, w.topj,
                                                                        nullptr, nullptr, nullptr, 0);
   PS_LAUNCHED("nn_topk_tc<top4>");
   certify_exact<T><<<grid_for(nx_max, 32), 256, 0, st>>>(w.topv, w.topj, n_x, x_idx, y_idx, w.xinfo, w.ymax, X, Y,
@@ -692,7 +726,7 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   cudaMemsetAsync(w.n_pairs, 0, sizeof(unsigned long long), st);
   cudaMemsetAsync(w.best_bits, 0xff, nx_max * sizeof(unsigned long long), st);
   cudaMemsetAsync(w.best_j, 0x7f, nx_max * sizeof(int32_t), st);
-  nn_topk_tc<1><<<(unsigned)(xrows / BM), kThreads, kSmemBytes, st>>>(w.xt, w.yt, w.yn, w.n_overflow, n_y, nullptr,
+  nn_topk_tc<1><<<(unsigned)(xrows / BM), kThreads, smem_bytes<1>(), st>>>(w.xt, w.yt, w.yn, w.n_overflow, n_y, nullptr,
                                                                        nullptr, w.lim, w.pairs, w.n_pairs, w.pair_cap);
   PS_LAUNCHED("nn_topk_tc<enumerate>");
   pair_dist_min<T><<<148 * 16, 256, 0, st>>>(w.pairs, w.n_pairs, w.pair_cap, w.xsrc, y_idx, X, Y, w.pd, w.best_bits);
