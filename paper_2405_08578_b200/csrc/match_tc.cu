@@ -40,14 +40,15 @@ constexpr int KD = 128;   // descriptor length
 constexpr int TOPK = 4;
 constexpr int STAGES_TOP = 3;   // Y-tile stages of the top-4 pass
 constexpr int STAGES_ENUM = 2;  // the enumeration pass trades one stage for per-warp hit buffers
-constexpr int HITBUF = 1024;    // hits staged per epilogue warp before one bulk append
+constexpr int HITBUF = 512;     // hits staged per epilogue warp before one bulk append
+constexpr int kEpiWarps = 8;    // two warps per TMEM lane quarter, 128 accumulator columns each
 constexpr uint32_t A_BYTES = BM * KD * 2;  // 32 KB
 constexpr uint32_t B_BYTES = BN * KD * 2;  // 64 KB
-constexpr int kThreads = 192;              // warp 0 TMA, warp 1 MMA/TMEM, warps 2-5 epilogue
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // warp 0 bulk copies, warp 1 MMA/TMEM, warps 2-9 epilogue
 template <int MODE>
 constexpr size_t smem_bytes() {
   return 1024 + A_BYTES + (MODE == 0 ? STAGES_TOP : STAGES_ENUM) * (size_t)B_BYTES + 256 +
-         (MODE == 0 ? 0 : 4 * (HITBUF * 8 + 16));
+         (MODE == 0 ? 0 : kEpiWarps * (HITBUF * 8 + 16));
 }
 
 // ---- operand preparation ----------------------------------------------------------
@@ -124,6 +125,9 @@ __device__ __forceinline__ void topk_insert(float v, int j, float (&tv)[TOPK], i
 
 // MODE 0: per-row top-4 of v.  MODE 1: enumerate every (row, column) with
 // v <= lim[row] into pairs (row << 32 | column), capacity `cap`.
+// grid = (row blocks, splits): CTA (rb, sp) streams the sp-th contiguous
+// share of the Y tiles; MODE 0 writes one top-4 list per (split, half) --
+// list index sp * 2 + half of row g at topv[(list * nx_pad + g) * TOPK].
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Yt,
                                                           const float* __restrict__ yn,
@@ -136,8 +140,12 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
   extern __shared__ uint8_t smem_raw[];
   const int nx = *cnt_x, ny = *cnt_y;
   const int rb = blockIdx.x;
-  if (rb * BM >= nx || ny <= 0) return;  // uniform for the whole CTA
-  const int n_tiles = (ny + BN - 1) / BN;
+  if (rb * BM >= nx) return;  // uniform for the whole CTA
+  const int n_all = ny > 0 ? (ny + BN - 1) / BN : 0;
+  const int per = (n_all + gridDim.y - 1) / gridDim.y;
+  const int t_begin = min(n_all, (int)blockIdx.y * per);
+  const int n_tiles = min(n_all, t_begin + per) - t_begin;  // may be 0 (then lists stay empty)
+  const int64_t nx_pad = (int64_t)gridDim.x * BM;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + A_BYTES;
@@ -150,10 +158,10 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   // MODE 1: per-epilogue-warp hit buffer + fill counter
   unsigned long long* hitbuf = reinterpret_cast<unsigned long long*>(bars + 32);
-  int* hitcnt = reinterpret_cast<int*>(hitbuf + 4 * HITBUF);
+  int* hitcnt = reinterpret_cast<int*>(hitbuf + kEpiWarps * HITBUF);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  if (MODE == 1 && threadIdx.x < 4) hitcnt[threadIdx.x] = 0;
+  if (MODE == 1 && threadIdx.x < kEpiWarps) hitcnt[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     mbar_init(a_full, 1);
     for (int s = 0; s < STAGES; ++s) {
@@ -162,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(acc_full + s, 1);
-      mbar_init(acc_empty + s, 4 * 32);
+      mbar_init(acc_empty + s, kEpiWarps * 32);
     }
     mbar_fence_init();
   }
@@ -180,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
         const int s = t % STAGES;
         mbar_wait(b_empty + s, ((t / STAGES) & 1) ^ 1);
         mbar_arrive_expect_tx(b_full + s, B_BYTES);
-        bulk_g2s(sB + s * B_BYTES, Yt + (size_t)t * B_BYTES, B_BYTES, b_full + s);
+        bulk_g2s(sB + s * B_BYTES, Yt + (size_t)(t_begin + t) * B_BYTES, B_BYTES, b_full + s);
       }
     }
   } else if (warp == 1) {
@@ -205,8 +213,9 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
         mma_commit(acc_full + ab);
       }
     }
-  } else {  // ---- epilogue: thread = row
+  } else {  // ---- epilogue: thread = row, warp pair per lane quarter splits the columns
     const int quarter = warp & 3;
+    const int ew = warp - 2, half = ew >> 2;
     const int row = quarter * 32 + lane;
     float tv[TOPK];
     int tj[TOPK];
@@ -218,11 +227,12 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
       const int ab = t & 1;
       mbar_wait(acc_full + ab, (t >> 1) & 1);
       tc_fence_after();
-      const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + ab * BN;
-      const float* ynt = yn + (size_t)t * BN;
+      const int tg = t_begin + t;  // global tile index
+      const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + ab * BN + half * (BN / 2);
+      const float* ynt = yn + (size_t)tg * BN + half * (BN / 2);
       float m0 = INFINITY, m1 = INFINITY, m2 = INFINITY, m3 = INFINITY;  // independent chains
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 64) {
+      for (int c0 = 0; c0 < BN / 2; c0 += 64) {
         uint32_t r[64];
         tmem_ld64(tbase + c0, r);
         tmem_ld_wait();
@@ -240,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
       const bool mine = MODE == 0 ? m < tv[TOPK - 1] : m <= my_lim;
       if (__any_sync(0xffffffffu, mine)) {  // rescan (tcgen05.ld must stay warp-converged)
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 64) {
+        for (int c0 = 0; c0 < BN / 2; c0 += 64) {
           uint32_t r[64];
           tmem_ld64(tbase + c0, r);
           tmem_ld_wait();
@@ -249,12 +259,12 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
 #pragma unroll
               for (int c = 0; c < 64; ++c) {
                 const float v = fmaf(-2.0f, __uint_as_float(r[c]), __ldg(ynt + c0 + c));
-                if (v < tv[TOPK - 1]) topk_insert(v, t * BN + c0 + c, tv, tj);
+                if (v < tv[TOPK - 1]) topk_insert(v, tg * BN + half * (BN / 2) + c0 + c, tv, tj);
               }
             }
           } else {
-            unsigned long long* hb = hitbuf + quarter * HITBUF;
-            int fill = hitcnt[quarter];
+            unsigned long long* hb = hitbuf + ew * HITBUF;
+            int fill = hitcnt[ew];
 #pragma unroll
             for (int c = 0; c < 64; ++c) {
               const float v = fmaf(-2.0f, __uint_as_float(r[c]), __ldg(ynt + c0 + c));
@@ -263,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
               if (bal) {
                 if (hit)
                   hb[fill + __popc(bal & ((1u << lane) - 1u))] =
-                      ((unsigned long long)grow << 32) | (unsigned long long)(t * BN + c0 + c);
+                      ((unsigned long long)grow << 32) | (unsigned long long)(tg * BN + half * (BN / 2) + c0 + c);
                 fill += __popc(bal);
                 if (fill > HITBUF - 32) {  // flush: one global atomic per buffer
                   __syncwarp();
@@ -278,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
               }
             }
             __syncwarp();
-            if (lane == 0) hitcnt[quarter] = fill;
+            if (lane == 0) hitcnt[ew] = fill;
             __syncwarp();
           }
         }
@@ -287,8 +297,8 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
       mbar_arrive(acc_empty + ab);
     }
     if (MODE == 1) {
-      unsigned long long* hb = hitbuf + quarter * HITBUF;
-      const int fill = hitcnt[quarter];
+      unsigned long long* hb = hitbuf + ew * HITBUF;
+      const int fill = hitcnt[ew];
       unsigned long long base = 0;
       if (lane == 0 && fill) base = atomicAdd(n_pairs, (unsigned long long)fill);
       base = __shfl_sync(0xffffffffu, base, 0);
@@ -296,10 +306,11 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
         if ((int64_t)(base + e) < cap) pairs[base + e] = hb[e];
     }
     if (MODE == 0 && grow < nx) {
+      const int64_t list = (int64_t)blockIdx.y * 2 + half;
 #pragma unroll
       for (int q = 0; q < TOPK; ++q) {
-        topv[grow * TOPK + q] = tv[q];
-        topj[grow * TOPK + q] = tj[q];
+        topv[(list * nx_pad + grow) * TOPK + q] = tv[q];
+        topj[(list * nx_pad + grow) * TOPK + q] = tj[q];
       }
     }
   }
@@ -355,7 +366,8 @@ __global__ void certify_exact(const float* __restrict__ topv, const int32_t* __r
                               const int32_t* __restrict__ y_orig, const double* __restrict__ xinfo,
                               const unsigned* __restrict__ ymax, const T* __restrict__ X, const T* __restrict__ Y,
                               int32_t* __restrict__ nn, double* __restrict__ dist, int32_t* __restrict__ overflow,
-                              int32_t* __restrict__ n_overflow, float* __restrict__ overflow_lim) {
+                              int32_t* __restrict__ n_overflow, float* __restrict__ overflow_lim, int n_lists,
+                              int64_t nx_pad) {
   const int nx = *cnt_x;
   const double Nmax = __uint_as_float(ymax[0]), Rmax = __uint_as_float(ymax[1]), Hmax = __uint_as_float(ymax[2]);
   const int t = threadIdx.x & 7;
@@ -373,10 +385,13 @@ __global__ void certify_exact(const float* __restrict__ topv, const int32_t* __r
     float tv[TOPK];
     int tj[TOPK];
 #pragma unroll
-    for (int q = 0; q < TOPK; ++q) {
-      tv[q] = topv[(int64_t)uu * TOPK + q];
-      tj[q] = topj[(int64_t)uu * TOPK + q];
-    }
+    for (int q = 0; q < TOPK; ++q) { tv[q] = INFINITY; tj[q] = -1; }
+    for (int l = 0; l < n_lists; ++l)  // the 4 smallest of the per-split lists are the global top-4
+#pragma unroll
+      for (int q = 0; q < TOPK; ++q) {
+        const float v = topv[((int64_t)l * nx_pad + uu) * TOPK + q];
+        if (v < tv[TOPK - 1]) topk_insert(v, topj[((int64_t)l * nx_pad + uu) * TOPK + q], tv, tj);
+      }
     const double lim = (double)tv[0] + 2.0 * E;
     const bool over = (double)tv[TOPK - 1] <= lim;  // candidates may extend past the top-4
     if (live && over && t == 0) {
@@ -600,6 +615,23 @@ struct TcWs {
 
 inline int64_t rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+constexpr int kMaxSplit = 16;
+
+int32_t read_count(const int32_t* p, cudaStream_t st) {
+  int32_t h = 0;
+  cudaMemcpyAsync(&h, p, sizeof(h), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  return h;
+}
+
+// row blocks x column splits so that about two CTAs per SM are in flight
+dim3 tc_grid(int64_t rows, int64_t cols) {
+  const int rb = (int)std::max<int64_t>(1, (rows + BM - 1) / BM);
+  const int tiles = (int)std::max<int64_t>(1, (cols + BN - 1) / BN);
+  const int split = std::max(1, std::min({kMaxSplit, tiles, (2 * 148 + rb - 1) / rb}));
+  return dim3(rb, split);
+}
+
 size_t cub_need(int64_t n) {
   size_t a = 0, b = 0, c = 0;
   cub::DeviceScan::InclusiveScan(nullptr, c, (const int32_t*)nullptr, (int32_t*)nullptr, cub::Max(), (int)n);
@@ -636,8 +668,8 @@ TcWs carve_tc(void* base, int64_t n1, int64_t n2, size_t* used) {
   w.xinfo = ar.take<double>(3 * xrows);
   w.yinfo = ar.take<double>(3 * yrows);
   w.ymax = ar.take<unsigned>(4);
-  w.topv = ar.take<float>(xrows * TOPK);
-  w.topj = ar.take<int32_t>(xrows * TOPK);
+  w.topv = ar.take<float>(xrows * TOPK * 2 * kMaxSplit);
+  w.topj = ar.take<int32_t>(xrows * TOPK * 2 * kMaxSplit);
   w.nn12 = ar.take<int32_t>(n1);
   w.d12 = ar.take<double>(n1);
   w.nn21 = ar.take<int32_t>(n2);
@@ -710,11 +742,15 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
     cudaFuncSetAttribute(nn_topk_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<1>());
     attr = true;
   }
-  nn_topk_tc<0><<<(unsigned)(xrows / BM), kThreads, smem_bytes<0>(), st>>>(w.xt, w.yt, w.yn, n_x, n_y, w.topv, w.topj,
-                                                                       nullptr, nullptr, nullptr, 0);
+  const int64_t nx = read_count(n_x, st), ny = read_count(n_y, st);
+  if (nx <= 0) return PS_OK;
+  const dim3 g0 = tc_grid(nx, ny);
+  nn_topk_tc<0><<<g0, kThreads, smem_bytes<0>(), st>>>(w.xt, w.yt, w.yn, n_x, n_y, w.topv, w.topj, nullptr, nullptr,
+                                                      nullptr, 0);
   PS_LAUNCHED("nn_topk_tc<top4>");
-  certify_exact<T><<<grid_for(nx_max, 32), 256, 0, st>>>(w.topv, w.topj, n_x, x_idx, y_idx, w.xinfo, w.ymax, X, Y,
-                                                          nn, dist, w.overflow, w.n_overflow, w.lim);
+  certify_exact<T><<<grid_for(nx, 32), 256, 0, st>>>(w.topv, w.topj, n_x, x_idx, y_idx, w.xinfo, w.ymax, X, Y, nn,
+                                                      dist, w.overflow, w.n_overflow, w.lim, 2 * (int)g0.y,
+                                                      (int64_t)g0.x * BM);
   PS_LAUNCHED("certify_exact");
   // rows with more near-tied candidates than the top-4: enumerate every
   // column within their certified limit on the tensor cores, then decide exactly
@@ -726,9 +762,13 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   cudaMemsetAsync(w.n_pairs, 0, sizeof(unsigned long long), st);
   cudaMemsetAsync(w.best_bits, 0xff, nx_max * sizeof(unsigned long long), st);
   cudaMemsetAsync(w.best_j, 0x7f, nx_max * sizeof(int32_t), st);
-  nn_topk_tc<1><<<(unsigned)(xrows / BM), kThreads, smem_bytes<1>(), st>>>(w.xt, w.yt, w.yn, w.n_overflow, n_y, nullptr,
-                                                                       nullptr, w.lim, w.pairs, w.n_pairs, w.pair_cap);
-  PS_LAUNCHED("nn_topk_tc<enumerate>");
+  const int64_t n_over = read_count(w.n_overflow, st);
+  if (n_over > 0) {
+    nn_topk_tc<1><<<tc_grid(n_over, ny), kThreads, smem_bytes<1>(), st>>>(w.xt, w.yt, w.yn, w.n_overflow, n_y, nullptr,
+                                                                          nullptr, w.lim, w.pairs, w.n_pairs,
+                                                                          w.pair_cap);
+    PS_LAUNCHED("nn_topk_tc<enumerate>");
+  }
   pair_dist_min<T><<<148 * 16, 256, 0, st>>>(w.pairs, w.n_pairs, w.pair_cap, w.xsrc, y_idx, X, Y, w.pd, w.best_bits);
   PS_LAUNCHED("pair_dist_min");
   pair_argmin<T><<<148 * 8, 256, 0, st>>>(w.pairs, w.n_pairs, w.pair_cap, y_idx, w.pd, w.best_bits, w.best_j);
