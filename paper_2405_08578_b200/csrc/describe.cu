@@ -81,6 +81,29 @@ struct FxHist {
   }
 };
 
+// Stage P over rows [r0, r0+PR) x cols [c0, c0+PC) into stage[y * SP + x]:
+// lane (sx, sy) owns column sx and rows sy, sy + 2, ...
+template <class Img>
+__device__ __forceinline__ void stage_box(const Img& im, double* stage, int SP, int r0, int c0, int PR, int PC, int sx,
+                                          int sy) {
+  if (sx >= PC) return;
+  for (int y = sy; y < PR; y += 2) stage[y * SP + sx] = im.at(r0 + y, c0 + sx);
+}
+// 8-bit raster: incremental pixel pointer and ramp index, no per-element multiplies
+__device__ __forceinline__ void stage_box(const RampU8& im, double* stage, int SP, int r0, int c0, int PR, int PC,
+                                          int sx, int sy) {
+  if (sx >= PC) return;
+  const int pitch = (int)im.pitch;
+  const uint8_t* p = im.p + (r0 + sy) * pitch + (c0 + sx);
+  unsigned k = (unsigned)((r0 + sy) * im.nc + c0 + sx + 1);
+  const unsigned kstep = 2u * (unsigned)im.nc;
+  for (int y = sy; y < PR; y += 2) {
+    stage[y * SP + sx] = __dadd_rn(u32_to_f64(__ldg(p)), __dmul_rn(u32_to_f64(k), im.alpha));
+    p += 2 * pitch;
+    k += kstep;
+  }
+}
+
 template <class Img>
 __device__ __forceinline__ void axis_sample(const Img& im, int r, int c, double& a, double& b) {
   // descriptor.py:135-136 (gradient_at convention, :98-115)
@@ -173,10 +196,7 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
   h36.zero(lane);
   const int sx_ = lane & 15, sy_ = lane >> 4;  // staging: 2 rows x 16 columns per step
   if (kStaged) {  // P over rows r0-1..r0+w, cols c0-1..c0+w
-    constexpr int E = W + 2;
-#pragma unroll
-    for (int y = sy_; y < E; y += 2)
-      if (sx_ < E) stage[y * SP + sx_] = im.at(r0 - 1 + y, c0 - 1 + sx_);
+    stage_box(im, stage, SP, r0 - 1, c0 - 1, W + 2, W + 2, sx_, sy_);
   }
   __syncwarp();
   auto axis_ab = [&](int iv, int iu, double& a, double& b) {
@@ -268,8 +288,7 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
     if (kStaged) {
       __syncwarp();
       const int PC = FC + 2, PR = FR + 2;
-      for (int y = sy_; y < PR; y += 2)
-        if (sx_ < PC) stage[y * SP + sx_] = im.at(pr0 - 1 + y, pc0 - 1 + sx_);
+      stage_box(im, stage, SP, pr0 - 1, pc0 - 1, PR, PC, sx_, sy_);
       __syncwarp();
       for (int y = sy_; y < FR; y += 2)
         if (sx_ < FC) {
@@ -425,6 +444,262 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
   __syncwarp();
 }
 
+
+// ---- 8-bit fast path, w = 8 (C1/C2/C4/C5 L_min) -----------------------------------
+// float32 atan2 for the screen: octant reduction + degree-8 (in t^2) fit of
+// atan on [0, 1]; max error 1.4e-7 rad in float32 evaluation (plus ~2e-7 from
+// the reduction), far inside the 1.7e-5 rad (1e-4 bin) screen margin.
+__device__ __forceinline__ float fast_atan2f(float y, float x) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float mn = fminf(ax, ay), mx = fmaxf(ax, ay);
+  const float t = mx > 0.0f ? __fdividef(mn, mx) : 0.0f;
+  const float z = t * t;
+  float p = -0.00405279453843832f;
+  p = __fmaf_rn(p, z, 0.021855242550373077f);
+  p = __fmaf_rn(p, z, -0.05589873343706131f);
+  p = __fmaf_rn(p, z, 0.09640958160161972f);
+  p = __fmaf_rn(p, z, -0.13908010721206665f);
+  p = __fmaf_rn(p, z, 0.19946402311325073f);
+  p = __fmaf_rn(p, z, -0.3332984149456024f);
+  p = __fmaf_rn(p, z, 0.9999993443489075f);
+  float r = p * t;
+  if (ay > ax) r = 1.5707963267948966f - r;
+  if (x < 0.0f) r = 3.141592653589793f - r;
+  return y < 0.0f ? -r : r;
+}
+
+__device__ __forceinline__ float warp_max_f(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Fixed-point scale 2^e for one histogram pass: every bin sum of nsamp
+// magnitudes <= mx stays below 2^31 (one native 32-bit atomic per sample);
+// the quantum is then ~2^-31 * nsamp * mx, i.e. ~1e-8 of the descriptor norm.
+__device__ __forceinline__ float fx_scale32(float mx, int nsamp) {
+  if (!(mx > 0.0f)) return 1.0f;
+  int e;
+  frexpf(mx * (float)nsamp * 1.0001f, &e);  // mx * nsamp < 2^e
+  return ldexpf(1.0f, 31 - e);
+}
+
+template <int W, class Img>
+__device__ __forceinline__ void describe_keypoint_w8u8(const Img& im, int row, int col, int w_rt, double fx64,
+                                                       int lb, const DescParams& prm, unsigned* hbase, double* stage,
+                                                       float* __restrict__ o32, double* __restrict__ o64) {
+  static_assert(W == kStageW, "fast path is staged");
+  constexpr int NS = W * W, SPL = NS / 32, D = 128, SP = Stage<W>::kStride;
+  constexpr int WS = W / 4;
+  const int lane = threadIdx.x & 31;
+  const int nr = im.nr, nc = im.nc;
+  const int r0 = min(max(row - W / 2, 1), nr - 1 - W);
+  const int c0 = min(max(col - W / 2, 1), nc - 1 - W);
+  unsigned* h128 = hbase;
+  unsigned* h36 = hbase + D;
+  for (int q = lane; q < D + 36; q += 32) hbase[q] = 0u;
+  const int sx_ = lane & 15, sy_ = lane >> 4;
+  stage_box(im, stage, SP, r0 - 1, c0 - 1, W + 2, W + 2, sx_, sy_);
+  __syncwarp();
+  auto axis_ab = [&](int iv, int iu, double& a, double& b) {
+    a = __dsub_rn(stage[(iv + 2) * SP + iu + 1], stage[iv * SP + iu + 1]);
+    b = __dsub_rn(stage[(iv + 1) * SP + iu + 2], stage[(iv + 1) * SP + iu]);
+  };
+  auto bin64 = [&](double a, double b, double shift, double k, int nbins) {
+    const double ori = mod_two_pi(__dsub_rn(atan2(b, a), shift), prm.two_pi);
+    return min((int)__dmul_rn(ori, k), nbins - 1);
+  };
+  float mg[SPL];
+  int bn[SPL];
+  if (!prm.orient) {
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) {
+      const int s = lane + 32 * j, iv = s / W, iu = s % W;
+      double a, b;
+      axis_ab(iv, iu, a, b);
+      const float af = (float)a, bf = (float)b;
+      const float xb = wrap_two_pi_f(fast_atan2f(bf, af)) * 1.2732395447351628f;
+      int ob;
+      if (!certified_bin(xb, 8, ob)) {
+        const int m = min(max(__float2int_rn(xb), 0), 8);
+        ob = side_bin(a, b, prm.c8[m], prm.s8[m], m, 8);
+        if (ob < 0) ob = bin64(a, b, 0.0, prm.k8, 8);
+      }
+      mg[j] = __fsqrt_rn(__fmaf_rn(af, af, bf * bf));
+      bn[j] = ((iv / WS) * 4 + iu / WS) * 8 + ob;
+    }
+  } else {
+    // --- 36-bin dominant orientation over the axis region (descriptor.py:142-146)
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) {
+      const int s = lane + 32 * j;
+      double a, b;
+      axis_ab(s / W, s % W, a, b);
+      const float af = (float)a, bf = (float)b;
+      const float x = wrap_two_pi_f(fast_atan2f(bf, af)) * 5.729577951308232f;
+      int bin;
+      if (!certified_bin(x, 36, bin)) {
+        const int m = min(max(__float2int_rn(x), 0), 36);
+        bin = side_bin(a, b, prm.cb36[m], prm.sb36[m], m, 36);
+        if (bin < 0) bin = bin64(a, b, 0.0, prm.k36, 36);
+      }
+      mg[j] = __fsqrt_rn(__fmaf_rn(af, af, bf * bf));
+      bn[j] = bin;
+    }
+    float mx = mg[0];
+#pragma unroll
+    for (int j = 1; j < SPL; ++j) mx = fmaxf(mx, mg[j]);
+    const float f36 = fx_scale32(warp_max_f(mx), NS);
+#pragma unroll
+    for (int j = 0; j < SPL; ++j)
+      if (mg[j] > 0.0f) atomicAdd(h36 + bn[j], __float2uint_rn(mg[j] * f36));
+    __syncwarp();
+    // argmax with a clear lead (else the whole keypoint is redone in float64)
+    const unsigned v1 = h36[lane], v2 = lane < 4 ? h36[lane + 32] : 0u;
+    const unsigned k1 = (__float_as_uint((float)v1) & ~63u) | (63u - lane);
+    const unsigned k2 = lane < 4 ? ((__float_as_uint((float)v2) & ~63u) | (31u - lane)) : 0u;
+    const unsigned top = __reduce_max_sync(0xffffffffu, max(k1, k2));
+    const unsigned sec = __reduce_max_sync(0xffffffffu, max(k1 == top ? 0u : k1, k2 == top ? 0u : k2));
+    const float tv = __uint_as_float(top & ~63u), sv = __uint_as_float(sec & ~63u);
+    if (!(sv < tv * 0.99994f)) {  // warp-uniform
+      __syncwarp();
+      describe_keypoint<W, 4, false>(im, row, col, w_rt, 4, fx64, lb, prm, hbase, stage, o32, o64);
+      return;
+    }
+    const int hk = 63 - (int)(top & 63u);
+    const double theta0 = prm.theta[hk], ct = prm.cos_t[hk], st = prm.sin_t[hk];
+    const float theta0f = (float)theta0;
+    // --- rotated grid (descriptor.py:164-216, 237-240)
+    constexpr double half = (double)(W - 1) / 2.0;
+    const double cy = fmin(fmax((double)row, 1.0 + half), __dsub_rn((double)nr - 2.0, half));
+    const double cx = fmin(fmax((double)col, 1.0 + half), __dsub_rn((double)nc - 2.0, half));
+    const double xmin = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, ct >= 0.0 ? -half : half)), __dmul_rn(st, st >= 0.0 ? half : -half));
+    const double xmax = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, ct >= 0.0 ? half : -half)), __dmul_rn(st, st >= 0.0 ? -half : half));
+    const double ymin = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, st >= 0.0 ? -half : half)), __dmul_rn(ct, ct >= 0.0 ? -half : half));
+    const double ymax = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, st >= 0.0 ? half : -half)), __dmul_rn(ct, ct >= 0.0 ? half : -half));
+    const int pr0 = max((int)floor(ymin), 1), pr1 = min((int)ceil(ymax), nr - 2);
+    const int pc0 = max((int)floor(xmin), 1), pc1 = min((int)ceil(xmax), nc - 2);
+    const int xcap = max(pc1 - pc0 - 1, 0), ycap = max(pr1 - pr0 - 1, 0);
+    const double xhi = (double)(nc - 2), yhi = (double)(nr - 2);
+    const int FR = pr1 - pr0 + 1, FC = pc1 - pc0 + 1;
+    double* fa = stage + Stage<W>::kP;
+    double* fb = fa + Stage<W>::kF;
+    __syncwarp();
+    stage_box(im, stage, SP, pr0 - 1, pc0 - 1, FR + 2, FC + 2, sx_, sy_);
+    __syncwarp();
+    for (int y = sy_; y < FR; y += 2)
+      if (sx_ < FC) {
+        fa[y * SP + sx_] = __dsub_rn(stage[(y + 2) * SP + sx_ + 1], stage[y * SP + sx_ + 1]);
+        fb[y * SP + sx_] = __dsub_rn(stage[(y + 1) * SP + sx_ + 2], stage[(y + 1) * SP + sx_]);
+      }
+    __syncwarp();
+    const double c0t = ct, s0t = -st;  // cos / sin of theta0
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) {
+      const int s = lane + 32 * j, iv = s / W, iu = s % W;
+      const double u = (double)iu - half, v = (double)iv - half;  // exact
+      const double x = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, u)), __dmul_rn(st, v));
+      const double y = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, u)), __dmul_rn(ct, v));
+      mg[j] = 0.0f;
+      bn[j] = 0;
+      if (!(x >= 1.0 && x <= xhi && y >= 1.0 && y <= yhi)) continue;  // hypot * valid = 0
+      const double lx = __dsub_rn(fmin(fmax(x, (double)pc0), (double)pc1), (double)pc0);
+      const double ly = __dsub_rn(fmin(fmax(y, (double)pr0), (double)pr1), (double)pr0);
+      const int x0 = min((int)floor(lx), xcap), y0 = min((int)floor(ly), ycap);
+      const double fxx = __dsub_rn(lx, (double)x0), fyy = __dsub_rn(ly, (double)y0);
+      const int x1 = min(x0 + 1, pc1 - pc0), y1 = min(y0 + 1, pr1 - pr0);
+      const double a00 = fa[y0 * SP + x0], b00 = fb[y0 * SP + x0], a01 = fa[y0 * SP + x1], b01 = fb[y0 * SP + x1];
+      const double a10 = fa[y1 * SP + x0], b10 = fb[y1 * SP + x0], a11 = fa[y1 * SP + x1], b11 = fb[y1 * SP + x1];
+      const double sy = __dsub_rn(1.0, fyy), sx = __dsub_rn(1.0, fxx);
+      const double as = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(a00, sy), sx), __dmul_rn(__dmul_rn(a01, sy), fxx)),
+                                            __dmul_rn(__dmul_rn(a10, fyy), sx)),
+                                  __dmul_rn(__dmul_rn(a11, fyy), fxx));
+      const double bs = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(b00, sy), sx), __dmul_rn(__dmul_rn(b01, sy), fxx)),
+                                            __dmul_rn(__dmul_rn(b10, fyy), sx)),
+                                  __dmul_rn(__dmul_rn(b11, fyy), fxx));
+      const float af = (float)as, bf = (float)bs;
+      const float xb = wrap_two_pi_f(fast_atan2f(bf, af) - theta0f) * 1.2732395447351628f;
+      int ob;
+      if (!certified_bin(xb, 8, ob)) {
+        const int m = min(max(__float2int_rn(xb), 0), 8);
+        const double ce = __dsub_rn(__dmul_rn(c0t, prm.c8[m]), __dmul_rn(s0t, prm.s8[m]));
+        const double se = __dadd_rn(__dmul_rn(s0t, prm.c8[m]), __dmul_rn(c0t, prm.s8[m]));
+        ob = side_bin(as, bs, ce, se, m, 8);
+        if (ob < 0) ob = bin64(as, bs, theta0, prm.k8, 8);
+      }
+      mg[j] = __fsqrt_rn(__fmaf_rn(af, af, bf * bf));
+      bn[j] = ((iv / WS) * 4 + iu / WS) * 8 + ob;
+    }
+  }
+  float mx = mg[0];
+#pragma unroll
+  for (int j = 1; j < SPL; ++j) mx = fmaxf(mx, mg[j]);
+  const float fx = fx_scale32(warp_max_f(mx), NS);
+#pragma unroll
+  for (int j = 0; j < SPL; ++j)
+    if (mg[j] > 0.0f) atomicAdd(h128 + bn[j], __float2uint_rn(mg[j] * fx));
+  __syncwarp();
+  // --- L2 normalise, clamp at 0.2, renormalise (descriptor.py:250-255)
+  constexpr int kPer = D / 32;
+  if (o64 == nullptr) {
+    const float inv = 1.0f / fx;
+    float vals[kPer];
+    float ss = 0.0f;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      vals[j] = (float)h128[lane + 32 * j] * inv;
+      ss = __fmaf_rn(vals[j], vals[j], ss);
+    }
+    ss = warp_sum_f(ss);
+    if (ss > 0.0f) {
+      const float r1 = rsqrtf(ss);
+      float ss2 = 0.0f;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        vals[j] = fminf(vals[j] * r1, 0.2f);
+        ss2 = __fmaf_rn(vals[j], vals[j], ss2);
+      }
+      const float r2 = rsqrtf(warp_sum_f(ss2));
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) vals[j] *= r2;
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) o32[lane + 32 * j] = vals[j];
+  } else {
+    const double inv = 1.0 / (double)fx;
+    double vals[kPer];
+    double ss = 0.0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      vals[j] = __dmul_rn((double)h128[lane + 32 * j], inv);
+      ss = __dadd_rn(ss, __dmul_rn(vals[j], vals[j]));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+    const double n1 = __dsqrt_rn(ss);
+    double n2 = 0.0;
+    if (n1 > 0.0) {
+      const double r1 = __drcp_rn(n1);
+      double ss2 = 0.0;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        vals[j] = fmin(__dmul_rn(vals[j], r1), 0.2);
+        ss2 = __dadd_rn(ss2, __dmul_rn(vals[j], vals[j]));
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ss2 = __dadd_rn(ss2, __shfl_xor_sync(0xffffffffu, ss2, o));
+      n2 = __drcp_rn(__dsqrt_rn(ss2));
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const double v = n1 > 0.0 ? __dmul_rn(vals[j], n2) : 0.0;
+      if (o32) o32[lane + 32 * j] = __double2float_rn(v);
+      o64[lane + 32 * j] = v;
+    }
+  }
+  __syncwarp();
+}
+
 template <class Img>
 __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64_t img_stride, int B,
                                                                   const int32_t* __restrict__ kp_row,
@@ -462,7 +737,9 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
     float* o32 = out32 ? out32 + g * D : nullptr;
     double* o64 = out64 ? out64 + g * D : nullptr;
     constexpr bool kFast = std::is_same<Img, RampU8>::value;
-    if (prm.d == 4 && w == 8) {
+    if (kFast && prm.d == 4 && w == 8) {
+      describe_keypoint_w8u8<8>(im, row, col, w, fx, lb, prm, hw, stage, o32, o64);
+    } else if (prm.d == 4 && w == 8) {
       describe_keypoint<8, 4, kFast>(im, row, col, w, 4, fx, lb, prm, hw, stage, o32, o64);
     } else if (prm.d == 4 && w == 16) {
       describe_keypoint<16, 4, kFast>(im, row, col, w, 4, fx, lb, prm, hw, stage, o32, o64);
