@@ -89,19 +89,23 @@ __device__ __forceinline__ void stage_box(const Img& im, double* stage, int SP, 
   if (sx >= PC) return;
   for (int y = sy; y < PR; y += 2) stage[y * SP + sx] = im.at(r0 + y, c0 + sx);
 }
-// 8-bit raster: incremental pixel pointer and ramp index, no per-element multiplies
-__device__ __forceinline__ void stage_box(const RampU8& im, double* stage, int SP, int r0, int c0, int PR, int PC,
-                                          int sx, int sy) {
+// 8-bit raster, at most 2*MAXR rows: all pixel loads are issued before any is
+// consumed (one memory latency per box), then the ramp is applied.
+template <int MAXR>
+__device__ __forceinline__ void stage_box_u8(const RampU8& im, double* stage, int SP, int r0, int c0, int PR, int PC,
+                                             int sx, int sy) {
   if (sx >= PC) return;
   const int pitch = (int)im.pitch;
   const uint8_t* p = im.p + (r0 + sy) * pitch + (c0 + sx);
-  unsigned k = (unsigned)((r0 + sy) * im.nc + c0 + sx + 1);
+  const unsigned k0 = (unsigned)((r0 + sy) * im.nc + c0 + sx + 1);
   const unsigned kstep = 2u * (unsigned)im.nc;
-  for (int y = sy; y < PR; y += 2) {
-    stage[y * SP + sx] = __dadd_rn(u32_to_f64(__ldg(p)), __dmul_rn(u32_to_f64(k), im.alpha));
-    p += 2 * pitch;
-    k += kstep;
-  }
+  unsigned v[MAXR];
+#pragma unroll
+  for (int i = 0; i < MAXR; ++i) v[i] = (sy + 2 * i < PR) ? (unsigned)__ldg(p + 2 * i * pitch) : 0u;
+#pragma unroll
+  for (int i = 0; i < MAXR; ++i)
+    if (sy + 2 * i < PR)
+      stage[(sy + 2 * i) * SP + sx] = __dadd_rn(u32_to_f64(v[i]), __dmul_rn(u32_to_f64(k0 + i * kstep), im.alpha));
 }
 
 template <class Img>
@@ -499,7 +503,7 @@ __device__ __forceinline__ void describe_keypoint_w8u8(const Img& im, int row, i
   unsigned* h36 = hbase + D;
   for (int q = lane; q < D + 36; q += 32) hbase[q] = 0u;
   const int sx_ = lane & 15, sy_ = lane >> 4;
-  stage_box(im, stage, SP, r0 - 1, c0 - 1, W + 2, W + 2, sx_, sy_);
+  stage_box_u8<(W + 3) / 2>(im, stage, SP, r0 - 1, c0 - 1, W + 2, W + 2, sx_, sy_);
   __syncwarp();
   auto axis_ab = [&](int iv, int iu, double& a, double& b) {
     a = __dsub_rn(stage[(iv + 2) * SP + iu + 1], stage[iv * SP + iu + 1]);
@@ -585,7 +589,7 @@ __device__ __forceinline__ void describe_keypoint_w8u8(const Img& im, int row, i
     double* fa = stage + Stage<W>::kP;
     double* fb = fa + Stage<W>::kF;
     __syncwarp();
-    stage_box(im, stage, SP, pr0 - 1, pc0 - 1, FR + 2, FC + 2, sx_, sy_);
+    stage_box_u8<(Stage<W>::kSpan + 3) / 2>(im, stage, SP, pr0 - 1, pc0 - 1, FR + 2, FC + 2, sx_, sy_);
     __syncwarp();
     for (int y = sy_; y < FR; y += 2)
       if (sx_ < FC) {
@@ -716,6 +720,10 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
   unsigned* hw = reinterpret_cast<unsigned*>(dsm + kWarps * kStageDoubles) + wid * 3 * (D + 36);
   const int64_t total = (int64_t)B * cap;
   const bool small = total < (1ll << 31);
+  int w_def = -1, lb_def = 0;
+  double fx_def = 0.0;
+  for (int s = 0; s < prm.n_scales; ++s)
+    if (prm.scale[s] == default_scale) { w_def = prm.w[s]; fx_def = prm.fx[s]; lb_def = prm.lb[s]; }
   for (int64_t g = (int64_t)blockIdx.x * kWarps + wid; g < total; g += (int64_t)gridDim.x * kWarps) {
     const int b = small ? (int)((unsigned)g / (unsigned)cap) : (int)(g / cap);
     const int64_t i = g - (int64_t)b * cap;
@@ -723,13 +731,11 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
     Img im = img;
     im.p = img.p + (int64_t)b * img_stride;
     const int row = kp_row[g], col = kp_col[g];
-    const int scale = kp_scale ? kp_scale[g] : default_scale;
-    int w = -1;
-    double fx = 0.0;
-    int lb = 0;
-    if (prm.n_scales == 1) {
-      if (prm.scale[0] == scale) { w = prm.w[0]; fx = prm.fx[0]; lb = prm.lb[0]; }
-    } else {
+    int w = w_def, lb = lb_def;
+    double fx = fx_def;
+    if (kp_scale) {
+      const int scale = kp_scale[g];
+      w = -1;
       for (int s = 0; s < prm.n_scales; ++s)
         if (prm.scale[s] == scale) { w = prm.w[s]; fx = prm.fx[s]; lb = prm.lb[s]; }
     }
