@@ -488,8 +488,8 @@ __device__ __forceinline__ float fx_scale32(float mx, int nsamp) {
   return ldexpf(1.0f, 31 - e);
 }
 
-template <int W, class Img>
-__device__ __forceinline__ void describe_keypoint_w8u8(const Img& im, int row, int col, int w_rt, double fx64,
+template <int W>
+__device__ __forceinline__ void describe_keypoint_w8u8(const RampU8& im, int row, int col, int w_rt, double fx64,
                                                        int lb, const DescParams& prm, unsigned* hbase, double* stage,
                                                        float* __restrict__ o32, double* __restrict__ o64) {
   static_assert(W == kStageW, "fast path is staged");
@@ -743,8 +743,14 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
     float* o32 = out32 ? out32 + g * D : nullptr;
     double* o64 = out64 ? out64 + g * D : nullptr;
     constexpr bool kFast = std::is_same<Img, RampU8>::value;
-    if (kFast && prm.d == 4 && w == 8) {
-      describe_keypoint_w8u8<8>(im, row, col, w, fx, lb, prm, hw, stage, o32, o64);
+    bool done = false;
+    if constexpr (kFast) {
+      if (prm.d == 4 && w == 8) {
+        describe_keypoint_w8u8<8>(im, row, col, w, fx, lb, prm, hw, stage, o32, o64);
+        done = true;
+      }
+    }
+    if (done) {
     } else if (prm.d == 4 && w == 8) {
       describe_keypoint<8, 4, kFast>(im, row, col, w, 4, fx, lb, prm, hw, stage, o32, o64);
     } else if (prm.d == 4 && w == 16) {
