@@ -488,10 +488,12 @@ __device__ __forceinline__ float fx_scale32(float mx, int nsamp) {
   return ldexpf(1.0f, 31 - e);
 }
 
+// Returns false (nothing written) when the 36-bin argmax has no clear lead;
+// the caller then queues the keypoint for the float64 kernel.
 template <int W>
-__device__ __forceinline__ void describe_keypoint_w8u8(const RampU8& im, int row, int col, int w_rt, double fx64,
-                                                       int lb, const DescParams& prm, unsigned* hbase, double* stage,
-                                                       float* __restrict__ o32, double* __restrict__ o64) {
+__device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row, int col, const DescParams& prm,
+                                                       unsigned* hbase, double* stage, float* __restrict__ o32,
+                                                       double* __restrict__ o64) {
   static_assert(W == kStageW, "fast path is staged");
   constexpr int NS = W * W, SPL = NS / 32, D = 128, SP = Stage<W>::kStride;
   constexpr int WS = W / 4;
@@ -567,8 +569,7 @@ __device__ __forceinline__ void describe_keypoint_w8u8(const RampU8& im, int row
     const float tv = __uint_as_float(top & ~63u), sv = __uint_as_float(sec & ~63u);
     if (!(sv < tv * 0.99994f)) {  // warp-uniform
       __syncwarp();
-      describe_keypoint<W, 4, false>(im, row, col, w_rt, 4, fx64, lb, prm, hbase, stage, o32, o64);
-      return;
+      return false;
     }
     const int hk = 63 - (int)(top & 63u);
     const double theta0 = prm.theta[hk], ct = prm.cos_t[hk], st = prm.sin_t[hk];
@@ -702,6 +703,7 @@ __device__ __forceinline__ void describe_keypoint_w8u8(const RampU8& im, int row
     }
   }
   __syncwarp();
+  return true;
 }
 
 template <class Img>
@@ -712,19 +714,22 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
                                                                   int32_t default_scale,
                                                                   const int32_t* __restrict__ counts, int64_t cap,
                                                                   DescParams prm, float* __restrict__ out32,
-                                                                  double* __restrict__ out64) {
+                                                                  double* __restrict__ out64,
+                                                                  const int64_t* __restrict__ work,
+                                                                  const unsigned long long* __restrict__ n_work) {
   extern __shared__ double dsm[];
   const int wid = threadIdx.x >> 5;
   const int D = prm.D;
   double* stage = dsm + wid * kStageDoubles;
   unsigned* hw = reinterpret_cast<unsigned*>(dsm + kWarps * kStageDoubles) + wid * 3 * (D + 36);
-  const int64_t total = (int64_t)B * cap;
+  const int64_t total = work ? (int64_t)*n_work : (int64_t)B * cap;
   const bool small = total < (1ll << 31);
   int w_def = -1, lb_def = 0;
   double fx_def = 0.0;
   for (int s = 0; s < prm.n_scales; ++s)
     if (prm.scale[s] == default_scale) { w_def = prm.w[s]; fx_def = prm.fx[s]; lb_def = prm.lb[s]; }
-  for (int64_t g = (int64_t)blockIdx.x * kWarps + wid; g < total; g += (int64_t)gridDim.x * kWarps) {
+  for (int64_t gi = (int64_t)blockIdx.x * kWarps + wid; gi < total; gi += (int64_t)gridDim.x * kWarps) {
+    const int64_t g = work ? work[gi] : gi;
     const int b = small ? (int)((unsigned)g / (unsigned)cap) : (int)(g / cap);
     const int64_t i = g - (int64_t)b * cap;
     if (counts && i >= counts[b]) continue;
@@ -743,15 +748,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
     float* o32 = out32 ? out32 + g * D : nullptr;
     double* o64 = out64 ? out64 + g * D : nullptr;
     constexpr bool kFast = std::is_same<Img, RampU8>::value;
-    bool done = false;
-    if constexpr (kFast) {
-      if (prm.d == 4 && w == 8) {
-        describe_keypoint_w8u8<8>(im, row, col, w, fx, lb, prm, hw, stage, o32, o64);
-        done = true;
-      }
-    }
-    if (done) {
-    } else if (prm.d == 4 && w == 8) {
+    if (prm.d == 4 && w == 8) {
       describe_keypoint<8, 4, kFast>(im, row, col, w, 4, fx, lb, prm, hw, stage, o32, o64);
     } else if (prm.d == 4 && w == 16) {
       describe_keypoint<16, 4, kFast>(im, row, col, w, 4, fx, lb, prm, hw, stage, o32, o64);
@@ -760,6 +757,54 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
     } else {
       describe_keypoint<0, 0, kFast>(im, row, col, w, prm.d, fx, lb, prm, hw, stage, o32, o64);
     }
+  }
+}
+
+// 8-bit rasters: w = 8 keypoints through the lean fast path (more resident
+// warps); everything else -- other region sides and 36-bin near-ties -- is
+// queued for describe_kernel.
+constexpr int kFastWarps = 8;
+constexpr int kFastHist = 128 + 36;
+
+__global__ void __launch_bounds__(kFastWarps * 32, 4) describe_fast_u8(RampU8 img, int64_t img_stride, int B,
+                                                                       const int32_t* __restrict__ kp_row,
+                                                                       const int32_t* __restrict__ kp_col,
+                                                                       const int32_t* __restrict__ kp_scale,
+                                                                       int32_t default_scale,
+                                                                       const int32_t* __restrict__ counts, int64_t cap,
+                                                                       DescParams prm, float* __restrict__ out32,
+                                                                       double* __restrict__ out64,
+                                                                       int64_t* __restrict__ work,
+                                                                       unsigned long long* __restrict__ n_work) {
+  extern __shared__ double dsm[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* stage = dsm + wid * kStageDoubles;
+  unsigned* hw = reinterpret_cast<unsigned*>(dsm + kFastWarps * kStageDoubles) + wid * kFastHist;
+  const int64_t total = (int64_t)B * cap;
+  const bool small = total < (1ll << 31);
+  int w_def = -1;
+  for (int s = 0; s < prm.n_scales; ++s)
+    if (prm.scale[s] == default_scale) w_def = prm.w[s];
+  for (int64_t g = (int64_t)blockIdx.x * kFastWarps + wid; g < total; g += (int64_t)gridDim.x * kFastWarps) {
+    const int b = small ? (int)((unsigned)g / (unsigned)cap) : (int)(g / cap);
+    const int64_t i = g - (int64_t)b * cap;
+    if (counts && i >= counts[b]) continue;
+    RampU8 im = img;
+    im.p = img.p + (int64_t)b * img_stride;
+    const int row = kp_row[g], col = kp_col[g];
+    int w = w_def;
+    if (kp_scale) {
+      const int scale = kp_scale[g];
+      w = -1;
+      for (int s = 0; s < prm.n_scales; ++s)
+        if (prm.scale[s] == scale) w = prm.w[s];
+    }
+    if (w < 0 || row < 0 || row >= im.nr || col < 0 || col >= im.nc) continue;  // validated by the caller
+    bool ok = false;
+    if (prm.d == 4 && w == 8)
+      ok = describe_keypoint_w8u8<8>(im, row, col, prm, hw, stage, out32 ? out32 + g * 128 : nullptr,
+                                     out64 ? out64 + g * 128 : nullptr);
+    if (!ok && lane == 0) work[atomicAdd(n_work, 1ull)] = g;
   }
 }
 
@@ -878,20 +923,38 @@ extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, in
   cudaFuncSetAttribute(describe_kernel<RampF64Raw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
   if (img->pixel_type == PS_PIXELS_U8) {
     RampU8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
-    describe_kernel<<<(unsigned)blocks, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,
-                                                                  kp->scale, default_scale, kp->count, kp->cap, prm,
-                                                                  out_desc32, out_desc64);
+    // queue for keypoints the fast kernel leaves to the general one
+    int64_t* work = nullptr;
+    cudaMallocAsync(&work, (size_t)total * sizeof(int64_t) + 16, s);
+    int st = check_cuda("cudaMallocAsync(describe work list)");
+    if (st) return st;
+    unsigned long long* n_work = reinterpret_cast<unsigned long long*>(work + total);
+    cudaMemsetAsync(n_work, 0, sizeof(unsigned long long), s);
+    const size_t fshmem = (size_t)kFastWarps * (kStageDoubles * sizeof(double) + kFastHist * sizeof(unsigned));
+    cudaFuncSetAttribute(describe_fast_u8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fshmem);
+    int64_t fblocks = (total + kFastWarps - 1) / kFastWarps;
+    if (fblocks > 148 * 16) fblocks = 148 * 16;
+    describe_fast_u8<<<(unsigned)fblocks, kFastWarps * 32, fshmem, s>>>(
+        im, img->image_stride, img->batch, kp->row, kp->col, kp->scale, default_scale, kp->count, kp->cap, prm,
+        out_desc32, out_desc64, work, n_work);
+    PS_LAUNCHED("describe_fast_u8");
+    describe_kernel<<<148 * 2, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,
+                                                        kp->scale, default_scale, kp->count, kp->cap, prm, out_desc32,
+                                                        out_desc64, work, n_work);
+    PS_LAUNCHED("describe_kernel(queued)");
+    cudaFreeAsync(work, s);
+    return check_cuda("cudaFreeAsync");
   } else if (img->pixel_type == PS_PIXELS_F64_RAW) {
     RampF64Raw im{(const double*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
     describe_kernel<<<(unsigned)blocks, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,
                                                                   kp->scale, default_scale, kp->count, kp->cap, prm,
-                                                                  out_desc32, out_desc64);
+                                                                  out_desc32, out_desc64, nullptr, nullptr);
   } else {
     PS_REQUIRE(img->pixel_type == PS_PIXELS_F64, PS_ERR_ARGUMENT, "unknown pixel type");
     RampF64 im{(const double*)img->data, img->row_pitch, img->nr, img->nc};
     describe_kernel<<<(unsigned)blocks, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,
                                                                   kp->scale, default_scale, kp->count, kp->cap, prm,
-                                                                  out_desc32, out_desc64);
+                                                                  out_desc32, out_desc64, nullptr, nullptr);
   }
   PS_LAUNCHED("describe_kernel");
   return PS_OK;
