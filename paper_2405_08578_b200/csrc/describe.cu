@@ -132,6 +132,17 @@ struct Stage {
 constexpr int kStageW = 8;  // region side served from shared memory
 constexpr int kStageDoubles = Stage<kStageW>::kTotal;
 
+// Fast-path (w = 8) layout, chosen for conflict-free shared-memory phases:
+// P rows at a stride of 24 doubles (axis reads of a half-warp hit 16
+// distinct 8-byte banks), gradient fields at an odd stride of 13.
+struct FastStage {
+  static constexpr int kSpan = Stage<8>::kSpan;  // 12
+  static constexpr int SPP = 24, SPF = 13;
+  static constexpr int kP = (kSpan + 2) * SPP;   // 336
+  static constexpr int kF = kSpan * SPF;         // 156
+  static constexpr int kTotal = kP + 2 * kF;     // 648 doubles
+};
+
 // ---- float32 screening of the discrete decisions -------------------------------
 // On 8-bit rasters the gradients (exact float64 differences of the ramped
 // raster) are bounded and well scaled, so the orientation bin of a sample is
@@ -495,7 +506,7 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
                                                        unsigned* hbase, double* stage, float* __restrict__ o32,
                                                        double* __restrict__ o64) {
   static_assert(W == kStageW, "fast path is staged");
-  constexpr int NS = W * W, SPL = NS / 32, D = 128, SP = Stage<W>::kStride;
+  constexpr int NS = W * W, SPL = NS / 32, D = 128, SP = FastStage::SPP, SF = FastStage::SPF;
   constexpr int WS = W / 4;
   const int lane = threadIdx.x & 31;
   const int nr = im.nr, nc = im.nc;
@@ -587,15 +598,15 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
     const int xcap = max(pc1 - pc0 - 1, 0), ycap = max(pr1 - pr0 - 1, 0);
     const double xhi = (double)(nc - 2), yhi = (double)(nr - 2);
     const int FR = pr1 - pr0 + 1, FC = pc1 - pc0 + 1;
-    double* fa = stage + Stage<W>::kP;
-    double* fb = fa + Stage<W>::kF;
+    double* fa = stage + FastStage::kP;
+    double* fb = fa + FastStage::kF;
     __syncwarp();
-    stage_box_u8<(Stage<W>::kSpan + 3) / 2>(im, stage, SP, pr0 - 1, pc0 - 1, FR + 2, FC + 2, sx_, sy_);
+    stage_box_u8<(FastStage::kSpan + 3) / 2>(im, stage, SP, pr0 - 1, pc0 - 1, FR + 2, FC + 2, sx_, sy_);
     __syncwarp();
     for (int y = sy_; y < FR; y += 2)
       if (sx_ < FC) {
-        fa[y * SP + sx_] = __dsub_rn(stage[(y + 2) * SP + sx_ + 1], stage[y * SP + sx_ + 1]);
-        fb[y * SP + sx_] = __dsub_rn(stage[(y + 1) * SP + sx_ + 2], stage[(y + 1) * SP + sx_]);
+        fa[y * SF + sx_] = __dsub_rn(stage[(y + 2) * SP + sx_ + 1], stage[y * SP + sx_ + 1]);
+        fb[y * SF + sx_] = __dsub_rn(stage[(y + 1) * SP + sx_ + 2], stage[(y + 1) * SP + sx_]);
       }
     __syncwarp();
     const double c0t = ct, s0t = -st;  // cos / sin of theta0
@@ -613,8 +624,8 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
       const int x0 = min((int)floor(lx), xcap), y0 = min((int)floor(ly), ycap);
       const double fxx = __dsub_rn(lx, (double)x0), fyy = __dsub_rn(ly, (double)y0);
       const int x1 = min(x0 + 1, pc1 - pc0), y1 = min(y0 + 1, pr1 - pr0);
-      const double a00 = fa[y0 * SP + x0], b00 = fb[y0 * SP + x0], a01 = fa[y0 * SP + x1], b01 = fb[y0 * SP + x1];
-      const double a10 = fa[y1 * SP + x0], b10 = fb[y1 * SP + x0], a11 = fa[y1 * SP + x1], b11 = fb[y1 * SP + x1];
+      const double a00 = fa[y0 * SF + x0], b00 = fb[y0 * SF + x0], a01 = fa[y0 * SF + x1], b01 = fb[y0 * SF + x1];
+      const double a10 = fa[y1 * SF + x0], b10 = fb[y1 * SF + x0], a11 = fa[y1 * SF + x1], b11 = fb[y1 * SF + x1];
       const double sy = __dsub_rn(1.0, fyy), sx = __dsub_rn(1.0, fxx);
       const double as = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(a00, sy), sx), __dmul_rn(__dmul_rn(a01, sy), fxx)),
                                             __dmul_rn(__dmul_rn(a10, fyy), sx)),
@@ -778,8 +789,8 @@ __global__ void __launch_bounds__(kFastWarps * 32, 4) describe_fast_u8(RampU8 im
                                                                        unsigned long long* __restrict__ n_work) {
   extern __shared__ double dsm[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* stage = dsm + wid * kStageDoubles;
-  unsigned* hw = reinterpret_cast<unsigned*>(dsm + kFastWarps * kStageDoubles) + wid * kFastHist;
+  double* stage = dsm + wid * FastStage::kTotal;
+  unsigned* hw = reinterpret_cast<unsigned*>(dsm + kFastWarps * FastStage::kTotal) + wid * kFastHist;
   const int64_t total = (int64_t)B * cap;
   const bool small = total < (1ll << 31);
   int w_def = -1;
@@ -930,7 +941,7 @@ extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, in
     if (st) return st;
     unsigned long long* n_work = reinterpret_cast<unsigned long long*>(work + total);
     cudaMemsetAsync(n_work, 0, sizeof(unsigned long long), s);
-    const size_t fshmem = (size_t)kFastWarps * (kStageDoubles * sizeof(double) + kFastHist * sizeof(unsigned));
+    const size_t fshmem = (size_t)kFastWarps * (FastStage::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
     cudaFuncSetAttribute(describe_fast_u8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fshmem);
     int64_t fblocks = (total + kFastWarps - 1) / kFastWarps;
     if (fblocks > 148 * 16) fblocks = 148 * 16;
