@@ -936,6 +936,17 @@ extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, in
     RampU8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
     // queue for keypoints the fast kernel leaves to the general one
     int64_t* work = nullptr;
+    static bool pool_set = false;  // keep freed queue memory in the stream-ordered pool
+    if (!pool_set) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      pool_set = true;
+    }
     cudaMallocAsync(&work, (size_t)total * sizeof(int64_t) + 16, s);
     int st = check_cuda("cudaMallocAsync(describe work list)");
     if (st) return st;
