@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-match", action="store_true", help="skip the C4 matching measurement")
     ap.add_argument("--no-stitch", action="store_true", help="skip the C3 nine-image stitch measurement")
+    ap.add_argument("--no-pairs", action="store_true", help="skip the C5 pairs/s measurement")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run N steps untimed and exit")
     return ap.parse_args()
 
@@ -219,6 +220,63 @@ def bench_c3_stitch(args, world, rank, dev, steps=3):
             "timing": "host wall clock around the whole call, CUDA-synchronized, max over ranks",
             "parallelism": f"images then pairs sharded over {world} rank(s); NCCL all-gather of keypoint/descriptor "
                            "slots and of the pair results"}
+
+
+# ---------------------------------------------------------------------------
+# C5 illumination pairs (BASELINE.json configs[4]): pairs/s
+# ---------------------------------------------------------------------------
+
+def bench_c5_pairs(args, world, rank, dev, n_pairs=16, steps=2):
+    """Full path per pair (detect, describe both images; match; RANSAC) on
+    BT.601 grey (reference to_grayscale on the host, as load_image does);
+    pairs sharded over ranks, no collective on the data path."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_08578_b200 import device, scenes
+    from paper_2405_08578_b200.pipeline import PipelineConfig
+
+    cfg = PipelineConfig(window_min=16, window_max=64)
+    mine = [p for p in range(n_pairs) if p % world == rank]
+    grey = []
+    for p in mine:
+        a, b, _ = scenes.config5_pair(p)
+        grey.append(torch.from_numpy(np.stack([scenes.gray_bt601(a), scenes.gray_bt601(b)])).to(dev))
+    sizes, dcfg = cfg.scale_set().sizes, cfg.descriptor_config()
+
+    def run_pair(g):
+        kp = device.detect(g, sizes, meta=False)
+        d = device.describe(g, kp, dcfg, scale_set=kp.scale_set)
+        r1, r2, _ = device.match(d[0][: kp.cap], d[1][: kp.cap])
+        n = int(r1.shape[0])
+        ok = False
+        if n >= cfg.min_inliers:
+            src, dst = device.pair_points(r1, r2, kp.row[0], kp.col[0], kp.row[1], kp.col[1])
+            ok = device.ransac(src, dst, cfg.ransac_iters, cfg.ransac_tol, cfg.min_inliers, cfg.seed).ok
+        return n, ok
+
+    stats = [run_pair(g) for g in grey]  # warm-up
+    times = []
+    for _ in range(steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        stats = [run_pair(g) for g in grey]
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = t.item()
+        times.append(dt)
+    dt = statistics.median(times)
+    return {"metric": "pairs/s (C5: 1920x1080 RGB pairs, BT.601 grey, homography warp + gain/offset/noise, "
+                      "L 16..64, full detect/describe/match/RANSAC)",
+            "value": round(n_pairs / dt, 3), "unit": "pairs/s", "pairs": n_pairs, "n_gpus": world,
+            "mean_matches": float(np.mean([s[0] for s in stats])), "registered": int(sum(s[1] for s in stats)),
+            "timing": "host wall clock, CUDA-synchronized, max over ranks; inputs resident on the GPU",
+            "note": "grey conversion is the reference's float64 to_grayscale on the host (ingest, out of scope)"}
 
 
 # ---------------------------------------------------------------------------
@@ -422,6 +480,10 @@ def run_ours(args):
     if not args.no_stitch:
         stitch = bench_c3_stitch(args, world, rank, dev)
 
+    pairs5 = None
+    if not args.no_pairs:
+        pairs5 = bench_c5_pairs(args, world, rank, dev)
+
     matching = None
     if rank == 0 and world == 1 and not args.no_match:
         del desc, imgs, dimg
@@ -438,7 +500,7 @@ def run_ours(args):
                        "keypoints_per_image": K, "descriptor": "float32 128-d", "l2": "inputs larger than L2",
                        "parallelism": f"images sharded over {world} rank(s)"},
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "matching_c4": matching,
-            "stitch_c3": stitch,
+            "stitch_c3": stitch, "pairs_c5": pairs5,
             "gpu_launches": int(launches), "clocks": clocks,
         }
         print(json.dumps(out), flush=True)

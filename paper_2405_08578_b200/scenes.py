@@ -152,3 +152,48 @@ def config3_images(seed: int = 0) -> tuple[list, list]:
             truth.append((r0, c0, theta, sc))
     order = np.random.default_rng(seed).permutation(9)
     return [out[k] for k in order], [truth[k] for k in order]
+
+
+LUMA = np.array([0.299, 0.587, 0.114])  # BT.601 weights (reference imaging.py:38)
+
+
+def gray_bt601(rgb: np.ndarray) -> np.ndarray:
+    """The reference's to_grayscale (imaging.py:83-85): float64 rgb @ weights."""
+    return np.asarray(rgb, dtype=np.float64) @ LUMA
+
+
+def _homography_warp(img: np.ndarray, H: np.ndarray) -> np.ndarray:
+    """Output (r, c) samples img at H^-1 (c, r, 1), bilinear, clamp-to-edge."""
+    from scipy.ndimage import map_coordinates
+
+    h, w = img.shape[:2]
+    Hi = np.linalg.inv(H)
+    rr, cc = np.meshgrid(np.arange(h, dtype=np.float64), np.arange(w, dtype=np.float64), indexing="ij")
+    den = Hi[2, 0] * cc + Hi[2, 1] * rr + Hi[2, 2]
+    sx = (Hi[0, 0] * cc + Hi[0, 1] * rr + Hi[0, 2]) / den
+    sy = (Hi[1, 0] * cc + Hi[1, 1] * rr + Hi[1, 2]) / den
+    chans = img[..., None] if img.ndim == 2 else img
+    out = np.stack([map_coordinates(chans[..., k].astype(np.float64), [sy, sx], order=1, mode="nearest")
+                    for k in range(chans.shape[-1])], axis=-1)
+    return out if img.ndim == 3 else out[..., 0]
+
+
+def config5_pair(p: int, h: int = 1080, w: int = 1920) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """C5 pair p: RGB image 1 (channel c = scene(h, w, 3p + c)) and image 2 =
+    centre-anchored homography warp of it (rotation U[-10, 10] deg, scale
+    U[0.92, 1.08], perspective p1, p2 in U[-1e-4, 1e-4]) with gain U[0.7, 1.3],
+    offset U[-20, 20] and N(0, 5^2) noise; both uint8 (h, w, 3).  Returns
+    (img1, img2, H) with H mapping image-1 (x, y) to image-2 (x, y)."""
+    img1 = np.stack([scene(h, w, 3 * p + c) for c in range(3)], axis=-1)
+    rng = np.random.default_rng(10_000 + p)
+    th = math.radians(rng.uniform(-10.0, 10.0))
+    s = rng.uniform(0.92, 1.08)
+    p1, p2 = rng.uniform(-1e-4, 1e-4, size=2)
+    cx, cy = (w - 1) / 2.0, (h - 1) / 2.0
+    T = np.array([[1, 0, -cx], [0, 1, -cy], [0, 0, 1.0]])
+    A = np.array([[s * math.cos(th), -s * math.sin(th), 0], [s * math.sin(th), s * math.cos(th), 0], [p1, p2, 1.0]])
+    H = np.linalg.inv(T) @ A @ T
+    warped = _homography_warp(img1, H)
+    gain, off = rng.uniform(0.7, 1.3), rng.uniform(-20.0, 20.0)
+    img2 = warped * gain + off + rng.normal(0.0, 5.0, size=warped.shape)
+    return img1, np.clip(np.rint(img2), 0, 255).astype(np.uint8), H
