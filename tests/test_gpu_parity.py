@@ -376,3 +376,23 @@ def test_matcher_tc_near_duplicate_clusters(force_tc):
     assert np.array_equal(r1.cpu().numpy(), w1) and np.array_equal(r2.cpu().numpy(), w2)
     assert np.array_equal(dl.cpu().numpy(), wd)
     assert len(w1) >= 20
+
+
+def test_float_grey_raster_path_matches_oracle():
+    """BT.601 grey (non-integral float64) rasters: detection on the recomputed
+    float64 P with first-occurrence ties, descriptors by the float64 kernel."""
+    rgb = np.stack([scenes.scene(200, 320, 50 + c) for c in range(3)], axis=-1)
+    grey = scenes.gray_bt601(rgb)
+    alpha = O.default_alpha(*grey.shape)
+    P = O.ramp(grey, alpha)
+    want = O.detect(P, (16, 32, 64))
+    t = torch.from_numpy(grey).cuda()
+    kp = device.detect(t, (16, 32, 64), alpha=alpha)
+    h = kp.image(0)
+    h["pol"] = h.pop("polarity")
+    assert_kp_equal(h, want, "grey")
+    d = device.describe(t, kp, R.DescriptorConfig(0.0625, 4, 64, True), alpha=alpha, out64=True, out32=False)
+    for k in range(0, len(want), 37):
+        ref = O.describe_one(P, int(want["row"][k]), int(want["col"][k]), int(want["scale"][k]), 0.0625, 4, 64)
+        got = d[0, k].cpu().numpy()
+        assert np.max(np.abs(got - ref)) <= P2_TOL * max(np.linalg.norm(ref), 1e-300)
