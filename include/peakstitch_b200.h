@@ -142,6 +142,16 @@ PS_API int ps_match(const void* desc1, int64_t n1, const void* desc2, int64_t n2
              double* out_delta, int64_t* out_count, int64_t cap, void* workspace,
              size_t workspace_bytes, void* stream);
 
+/* One direction of nearest_neighbor matching: out_index[i] / out_dist[i] =
+ * the exact first argmin over the rows of Y of the reference distance to row
+ * i of X (matcher.py:74 with _distance_matrix :48-54).  The building block of
+ * row-sharded matching across GPUs (each rank: its rows of A vs all of B,
+ * and the candidate columns vs its rows). */
+PS_API int ps_nearest_plan(int64_t nx, int64_t ny, int32_t dim, size_t* workspace_bytes_out);
+PS_API int ps_nearest(const void* X, int64_t nx, const void* Y, int64_t ny, int32_t dim, int32_t desc_is_f64,
+                      int32_t* out_index, double* out_dist, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
 /* Gather (x, y) = (col, row) float64 point pairs of matches
  * (registration.py:143-146) from two keypoint arrays. */
 PS_API int ps_pair_points(const int32_t* ref1, const int32_t* ref2, const int64_t* count,

@@ -20,6 +20,9 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
                        unsigned long long* keys_delta, unsigned long long* counter, void* ws, size_t ws_bytes,
                        cudaStream_t st);
 size_t ps_tc_nearest_ws(int64_t n1, int64_t n2);
+template <class T>
+int ps_tc_rows_impl(const T* X, int64_t nx, const T* Y, int64_t ny, int32_t* nn, double* dist, void* ws,
+                    size_t ws_bytes, cudaStream_t st);
 
 namespace ps {
 namespace {
@@ -399,5 +402,40 @@ extern "C" int ps_pair_points(const int32_t* ref1, const int32_t* ref2, const in
   pair_points_kernel<<<grid_blocks(cap, 256), 256, 0, (cudaStream_t)stream>>>(ref1, ref2, count, row1, col1, row2,
                                                                               col2, src_xy, dst_xy, cap);
   PS_LAUNCHED("pair_points");
+  return PS_OK;
+}
+
+extern "C" int ps_nearest_plan(int64_t nx, int64_t ny, int32_t dim, size_t* workspace_bytes_out) {
+  PS_REQUIRE(nx >= 0 && ny >= 0, PS_ERR_ARGUMENT, "bad sizes");
+  PS_REQUIRE(dim >= 8 && dim % 8 == 0 && dim <= kMaxDim, PS_ERR_ARGUMENT, "descriptor length %d unsupported", dim);
+  if (workspace_bytes_out)
+    *workspace_bytes_out = use_tc(nx, ny, dim, PS_MATCH_NEAREST) ? ps_tc_nearest_ws(nx, ny) : 256;
+  return PS_OK;
+}
+
+extern "C" int ps_nearest(const void* X, int64_t nx, const void* Y, int64_t ny, int32_t dim, int32_t desc_is_f64,
+                          int32_t* out_index, double* out_dist, void* workspace, size_t workspace_bytes, void* stream) {
+  PS_REQUIRE(dim >= 8 && dim % 8 == 0 && dim <= kMaxDim, PS_ERR_ARGUMENT, "descriptor length %d unsupported", dim);
+  PS_REQUIRE(nx < INT32_MAX && ny < INT32_MAX, PS_ERR_ARGUMENT, "too many descriptors");
+  if (nx == 0) return PS_OK;
+  PS_REQUIRE(X && Y && out_index && out_dist && ny > 0, PS_ERR_ARGUMENT, "null argument / empty Y in ps_nearest");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (use_tc(nx, ny, dim, PS_MATCH_NEAREST)) {
+    return desc_is_f64 ? ps_tc_rows_impl((const double*)X, nx, (const double*)Y, ny, out_index, out_dist, workspace,
+                                         workspace_bytes, st)
+                       : ps_tc_rows_impl((const float*)X, nx, (const float*)Y, ny, out_index, out_dist, workspace,
+                                         workspace_bytes, st);
+  }
+  const size_t shmem = 2 * TILE * SPAD * sizeof(double);
+  if (desc_is_f64) {
+    cudaFuncSetAttribute(nn_pass<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
+    nn_pass<double><<<grid_blocks(nx, TILE), 256, shmem, st>>>((const double*)X, nx, (const double*)Y, ny, dim,
+                                                               out_index, out_dist);
+  } else {
+    cudaFuncSetAttribute(nn_pass<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
+    nn_pass<float><<<grid_blocks(nx, TILE), 256, shmem, st>>>((const float*)X, nx, (const float*)Y, ny, dim, out_index,
+                                                              out_dist);
+  }
+  PS_LAUNCHED("nn_pass");
   return PS_OK;
 }

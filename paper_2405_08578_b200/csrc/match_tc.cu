@@ -560,6 +560,17 @@ __global__ void mark_reps(const T* __restrict__ X, int64_t n, const int32_t* __r
   }
 }
 
+__global__ void copy_from_rep(const int32_t* __restrict__ rep, int64_t n, int32_t* __restrict__ nn,
+                              double* __restrict__ dist) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = rep[i];
+    if (r != (int32_t)i) {
+      nn[i] = nn[r];
+      dist[i] = dist[r];
+    }
+  }
+}
+
 __global__ void iota32(int32_t* v, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     v[i] = (int32_t)i;
@@ -855,6 +866,31 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   }
   return PS_OK;
 }
+
+// One direction only: nn[i] / dist[i] = exact first argmin over the rows of
+// Y of dist(X_i, Y_j) for every row i of X (reference matcher.py:74, 43-54).
+template <class T>
+int ps_tc_rows_impl(const T* X, int64_t nx, const T* Y, int64_t ny, int32_t* nn, double* dist, void* ws,
+                    size_t ws_bytes, cudaStream_t st) {
+  using namespace ps::tc;
+  size_t need = 0;
+  carve_tc(nullptr, nx, ny, &need);
+  PS_REQUIRE(ws && ws_bytes >= need, PS_ERR_ARGUMENT, "tensor-core nearest workspace %zu < %zu", ws_bytes, need);
+  TcWs w = carve_tc(ws, nx, ny, &need);
+  int rc = dedupe(X, nx, w.a, w, st);
+  if (rc) return rc;
+  rc = dedupe(Y, ny, w.b, w, st);
+  if (rc) return rc;
+  rc = nearest_pass(X, nx, w.a.uniq, w.a.n_uniq, Y, ny, w.b.uniq, w.b.n_uniq, nn, dist, w, st);
+  if (rc) return rc;
+  copy_from_rep<<<grid_for(nx, 256), 256, 0, st>>>(w.a.rep, nx, nn, dist);  // duplicates share the answer
+  PS_LAUNCHED("copy_from_rep");
+  return PS_OK;
+}
+template int ps_tc_rows_impl<float>(const float*, int64_t, const float*, int64_t, int32_t*, double*, void*, size_t,
+                                    cudaStream_t);
+template int ps_tc_rows_impl<double>(const double*, int64_t, const double*, int64_t, int32_t*, double*, void*, size_t,
+                                     cudaStream_t);
 
 size_t ps_tc_nearest_ws(int64_t n1, int64_t n2) {
   size_t need = 0;

@@ -354,3 +354,23 @@ def estimate(src: torch.Tensor, dst: torch.Tensor, stream=None):
 
 def kernel_launches() -> int:
     return _lib.kernel_launches()
+
+
+def nearest(X: torch.Tensor, Y: torch.Tensor, stream=None):
+    """Exact first-argmin nearest row of Y for every row of X (one direction of
+    nearest_neighbor matching).  Returns (index int32 [nx], dist float64 [nx])."""
+    dt = torch.float64 if (X.dtype == torch.float64 or Y.dtype == torch.float64) else torch.float32
+    X, Y = X.to(dt).contiguous(), Y.to(dt).contiguous()
+    _require_cuda(X, "X")
+    nx, ny, dim = int(X.shape[0]), int(Y.shape[0]), int(X.shape[1])
+    idx = torch.empty(nx, dtype=torch.int32, device=X.device)
+    dist = torch.empty(nx, dtype=torch.float64, device=X.device)
+    if nx == 0:
+        return idx, dist
+    L = _lib.lib()
+    wsb = C.c_size_t()
+    _lib.check(L.ps_nearest_plan(nx, ny, dim, C.byref(wsb)), "nearest")
+    ws = _workspace(wsb.value, X.device)
+    _lib.check(L.ps_nearest(_ptr(X), nx, _ptr(Y), ny, dim, int(dt == torch.float64), _ptr(idx), _ptr(dist), _ptr(ws),
+                            wsb.value, C.c_void_p(_stream_ptr(stream))), "nearest")
+    return idx, dist

@@ -396,3 +396,37 @@ def test_float_grey_raster_path_matches_oracle():
         ref = O.describe_one(P, int(want["row"][k]), int(want["col"][k]), int(want["scale"][k]), 0.0625, 4, 64)
         got = d[0, k].cpu().numpy()
         assert np.max(np.abs(got - ref)) <= P2_TOL * max(np.linalg.norm(ref), 1e-300)
+
+
+def test_rowshard_single_rank_equals_match_on_c1():
+    from paper_2405_08578_b200.rowshard import match_rows_sharded
+
+    a, b = scenes.config1_pair(0)
+    cfg = R.DescriptorConfig(0.0625, 4, 64, True)
+    ds = []
+    for im in (a, b):
+        t = torch.from_numpy(im).cuda()
+        kp = device.detect(t, (16, 32, 64), meta=False)
+        ds.append(device.describe(t, kp, cfg)[0])
+    r1, r2, dl = device.match(ds[0], ds[1])
+    # two "ranks" emulated sequentially is not possible without a group; world 1 exercises the path
+    s1, s2, sd = match_rows_sharded(ds[0], 0, ds[1], 0.35)
+    assert torch.equal(s1.cpu(), r1.long().cpu()) and torch.equal(s2.cpu(), r2.long().cpu())
+    assert torch.equal(sd.cpu(), dl.cpu())
+
+
+def test_nearest_matches_oracle_both_paths(monkeypatch):
+    rng = np.random.default_rng(8)
+    X = rng.random((300, 128)).astype(np.float32)
+    Y = rng.random((500, 128)).astype(np.float32)
+    Y[7] = Y[9]
+    for env in ("0", None):
+        if env is None:
+            monkeypatch.setenv("PS_MATCH_EXACT", "1")
+        else:
+            monkeypatch.setenv("PS_TC_MIN_PAIRS", env)
+        idx, d = device.nearest(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda())
+        for i0, D in O.distances(X.astype(np.float64), Y.astype(np.float64)):
+            j = np.argmin(D, axis=1)
+            assert np.array_equal(idx[i0:i0 + D.shape[0]].cpu().numpy(), j)
+            assert np.array_equal(d[i0:i0 + D.shape[0]].cpu().numpy(), D[np.arange(D.shape[0]), j])
