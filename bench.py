@@ -127,11 +127,13 @@ def _cpu_match_job(args):
     return a.shape[0] * b.shape[0] / (time.perf_counter() - t0)
 
 
-def bench_c4_matching(args, with_cpu=True, steps=5):
+def bench_c4_matching(args, world=1, rank=0, dev=None, with_cpu=True, steps=5):
     import torch
+    import torch.distributed as dist
 
     from paper_2405_08578_b200 import device, scenes
     from paper_2405_08578_b200.records import DescriptorConfig
+    from paper_2405_08578_b200.rowshard import match_rows_sharded
 
     a, b = scenes.config4_pair(0)
     cfg = DescriptorConfig(0.0625, 4, 36, True)  # L = 36 (literal {4,8,16} is rejected)
@@ -142,17 +144,30 @@ def bench_c4_matching(args, with_cpu=True, steps=5):
         ds.append(device.describe(t, kp, cfg, scale_set=(36,))[0])
         del t
     n1, n2 = ds[0].shape[0], ds[1].shape[0]
+    lo, hi = (rank * n1) // world, ((rank + 1) * n1) // world  # my row block of A
+
+    def once():
+        if world == 1:
+            return device.match(ds[0], ds[1])
+        return match_rows_sharded(ds[0][lo:hi], lo, ds[1], 0.35)
+
     for _ in range(2):
-        r = device.match(ds[0], ds[1])
+        r = once()
     torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     times = []
     for _ in range(steps):
-        s.record()
-        r = device.match(ds[0], ds[1])
-        e.record()
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
-        times.append(s.elapsed_time(e))
+        t0 = time.perf_counter()
+        r = once()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) * 1e3
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = t.item()
+        times.append(dt)
     ms = statistics.median(times)
     flops = 2.0 * n1 * n2 * 128
     peak = 1641.9
@@ -166,7 +181,11 @@ def bench_c4_matching(args, with_cpu=True, steps=5):
            "roofline": {"bound": "tensor", "achieved": round(flops / (ms / 1e3) / 1e12, 2), "peak": peak,
                         "unit": "TFLOP/s", "frac": round(flops / (ms / 1e3) / 1e12 / peak, 4),
                         "note": "algorithmic 2*n1*n2*128 over the whole match call (fp16 tcgen05 + exact f64 recheck)"},
-           "exactness": "bit-exact vs float64 reference arithmetic (tests/test_gpu_parity.py P3)"}
+           "exactness": "bit-exact vs float64 reference arithmetic (tests/test_gpu_parity.py P3)",
+           "n_gpus": world, "parallelism": ("single GPU" if world == 1 else
+                                            f"rows of A sharded over {world} ranks; NCCL all-reduce of candidate "
+                                            "columns and of packed column minima (rowshard.py)"),
+           "timing": "host wall clock around the match call, CUDA-synchronized, max over ranks"}
     if with_cpu:
         import multiprocessing as mp
 
@@ -485,10 +504,10 @@ def run_ours(args):
         pairs5 = bench_c5_pairs(args, world, rank, dev)
 
     matching = None
-    if rank == 0 and world == 1 and not args.no_match:
+    if not args.no_match:
         del desc, imgs, dimg
         torch.cuda.empty_cache()
-        matching = bench_c4_matching(args, with_cpu=not args.no_cpu)
+        matching = bench_c4_matching(args, world, rank, dev, with_cpu=(not args.no_cpu and world == 1))
 
     if rank == 0:
         out = {
