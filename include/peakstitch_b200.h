@@ -152,6 +152,12 @@ PS_API int ps_nearest(const void* X, int64_t nx, const void* Y, int64_t ny, int3
                       int32_t* out_index, double* out_dist, void* workspace, size_t workspace_bytes,
                       void* stream);
 
+/* Statistics of the calling thread's last tensor-core ps_match (diagnostic):
+ * out[0..5] = distinct rows of desc1, of desc2, candidate columns, rows
+ * whose near-ties were enumerated, enumerated pairs (0: not tracked),
+ * tensor-core FLOPs issued (fp16 MMA, both passes). */
+PS_API int ps_match_stats(int64_t* out, int32_t n);
+
 /* Gather (x, y) = (col, row) float64 point pairs of matches
  * (registration.py:143-146) from two keypoint arrays. */
 PS_API int ps_pair_points(const int32_t* ref1, const int32_t* ref2, const int64_t* count,

@@ -628,6 +628,9 @@ inline int64_t rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 constexpr int kMaxSplit = 16;
 
+// statistics of the last tensor-core match on this thread (ps_match_stats)
+thread_local int64_t g_stats[8];  // uniq_a, uniq_b, cols, overflow rows, enumerated pairs, mma flops, -, -
+
 int32_t read_count(const int32_t* p, cudaStream_t st) {
   int32_t h = 0;
   cudaMemcpyAsync(&h, p, sizeof(h), cudaMemcpyDeviceToHost, st);
@@ -756,6 +759,8 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   const int64_t nx = read_count(n_x, st), ny = read_count(n_y, st);
   if (nx <= 0) return PS_OK;
   const dim3 g0 = tc_grid(nx, ny);
+  const int64_t flops_tile = 2ll * BM * BN * KD;
+  g_stats[5] += (int64_t)g0.x * ((ny + BN - 1) / BN) * flops_tile;
   nn_topk_tc<0><<<g0, kThreads, smem_bytes<0>(), st>>>(w.xt, w.yt, w.yn, n_x, n_y, w.topv, w.topj, nullptr, nullptr,
                                                       nullptr, 0);
   PS_LAUNCHED("nn_topk_tc<top4>");
@@ -774,7 +779,9 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   cudaMemsetAsync(w.best_bits, 0xff, nx_max * sizeof(unsigned long long), st);
   cudaMemsetAsync(w.best_j, 0x7f, nx_max * sizeof(int32_t), st);
   const int64_t n_over = read_count(w.n_overflow, st);
+  g_stats[3] += n_over;
   if (n_over > 0) {
+    g_stats[5] += (int64_t)tc_grid(n_over, ny).x * ((ny + BN - 1) / BN) * flops_tile;
     nn_topk_tc<1><<<tc_grid(n_over, ny), kThreads, smem_bytes<1>(), st>>>(w.xt, w.yt, w.yn, w.n_overflow, n_y, nullptr,
                                                                           nullptr, w.lim, w.pairs, w.n_pairs,
                                                                           w.pair_cap);
@@ -806,6 +813,7 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   carve_tc(nullptr, n1, n2, &need);
   PS_REQUIRE(ws && ws_bytes >= need, PS_ERR_ARGUMENT, "tensor-core match workspace %zu < %zu", ws_bytes, need);
   TcWs w = carve_tc(ws, n1, n2, &need);
+  for (int q = 0; q < 8; ++q) g_stats[q] = 0;
   // PS_TC_PROFILE=1: per-stage timing and counters on stderr (diagnostic; syncs)
   const bool prof = getenv("PS_TC_PROFILE") != nullptr;
   cudaEvent_t ev[8];
@@ -830,6 +838,8 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   // pass 1: rows of A (representatives) against the distinct rows of B
   rc = nearest_pass(A, n1, w.a.uniq, w.a.n_uniq, B, n2, w.b.uniq, w.b.n_uniq, w.nn12, w.d12, w, st);
   if (rc) return rc;
+  g_stats[0] = read_count(w.a.n_uniq, st);
+  g_stats[1] = read_count(w.b.n_uniq, st);
   mark();
   const int of1 = prof ? count_of(w.n_overflow) : 0;
   unsigned long long np1 = 0;
@@ -850,6 +860,7 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   rc = nearest_pass(B, n2, w.cols, w.n_cols, A, n1, w.a.uniq, w.a.n_uniq, w.nn21, w.d21, w, st);
   if (rc) return rc;
   mark();
+  g_stats[2] = read_count(w.n_cols, st);
   accept_pairs<<<grid_for(n1, 256), 256, 0, st>>>(w.a.rep, n1, w.nn12, w.d12, w.nn21, delta_s, keys_pair, keys_delta,
                                                   counter);
   PS_LAUNCHED("accept_pairs");
@@ -891,6 +902,11 @@ template int ps_tc_rows_impl<float>(const float*, int64_t, const float*, int64_t
                                     cudaStream_t);
 template int ps_tc_rows_impl<double>(const double*, int64_t, const double*, int64_t, int32_t*, double*, void*, size_t,
                                      cudaStream_t);
+
+extern "C" int ps_match_stats(int64_t* out, int32_t n) {
+  for (int q = 0; q < n && q < 8; ++q) out[q] = ps::tc::g_stats[q];
+  return PS_OK;
+}
 
 size_t ps_tc_nearest_ws(int64_t n1, int64_t n2) {
   size_t need = 0;

@@ -374,3 +374,12 @@ def nearest(X: torch.Tensor, Y: torch.Tensor, stream=None):
     _lib.check(L.ps_nearest(_ptr(X), nx, _ptr(Y), ny, dim, int(dt == torch.float64), _ptr(idx), _ptr(dist), _ptr(ws),
                             wsb.value, C.c_void_p(_stream_ptr(stream))), "nearest")
     return idx, dist
+
+
+def match_stats() -> dict:
+    """Counters of this thread's last tensor-core match (see ps_match_stats)."""
+    arr = (C.c_int64 * 8)()
+    _lib.lib().ps_match_stats(arr, 8)
+    keys = ("distinct_rows_a", "distinct_rows_b", "candidate_columns", "enumerated_rows", "enumerated_pairs",
+            "mma_flops")
+    return {k: int(arr[i]) for i, k in enumerate(keys)}
