@@ -230,68 +230,62 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
       const int tg = t_begin + t;  // global tile index
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + ab * BN + half * (BN / 2);
       const float* ynt = yn + (size_t)tg * BN + half * (BN / 2);
-      float m0 = INFINITY, m1 = INFINITY, m2 = INFINITY, m3 = INFINITY;  // independent chains
+      // one pass per 64-column chunk; groups of 4 columns are tested against the
+      // row's threshold (4th best, or the enumeration limit) with one branch
+      unsigned long long* hb = hitbuf + ew * HITBUF;
+      int fill = MODE == 1 ? hitcnt[ew] : 0;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN / 2; c0 += 64) {
         uint32_t r[64];
         tmem_ld64(tbase + c0, r);
         tmem_ld_wait();
         const float4* y4 = reinterpret_cast<const float4*>(ynt + c0);
+        const int jb = tg * BN + half * (BN / 2) + c0;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
           const float4 y = __ldg(y4 + q);
-          m0 = fminf(m0, fmaf(-2.0f, __uint_as_float(r[4 * q + 0]), y.x));
-          m1 = fminf(m1, fmaf(-2.0f, __uint_as_float(r[4 * q + 1]), y.y));
-          m2 = fminf(m2, fmaf(-2.0f, __uint_as_float(r[4 * q + 2]), y.z));
-          m3 = fminf(m3, fmaf(-2.0f, __uint_as_float(r[4 * q + 3]), y.w));
-        }
-      }
-      const float m = fminf(fminf(m0, m1), fminf(m2, m3));
-      const bool mine = MODE == 0 ? m < tv[TOPK - 1] : m <= my_lim;
-      if (__any_sync(0xffffffffu, mine)) {  // rescan (tcgen05.ld must stay warp-converged)
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN / 2; c0 += 64) {
-          uint32_t r[64];
-          tmem_ld64(tbase + c0, r);
-          tmem_ld_wait();
+          const float v0 = fmaf(-2.0f, __uint_as_float(r[4 * q + 0]), y.x);
+          const float v1 = fmaf(-2.0f, __uint_as_float(r[4 * q + 1]), y.y);
+          const float v2 = fmaf(-2.0f, __uint_as_float(r[4 * q + 2]), y.z);
+          const float v3 = fmaf(-2.0f, __uint_as_float(r[4 * q + 3]), y.w);
+          const float m4 = fminf(fminf(v0, v1), fminf(v2, v3));
           if (MODE == 0) {
-            if (mine) {
-#pragma unroll
-              for (int c = 0; c < 64; ++c) {
-                const float v = fmaf(-2.0f, __uint_as_float(r[c]), __ldg(ynt + c0 + c));
-                if (v < tv[TOPK - 1]) topk_insert(v, tg * BN + half * (BN / 2) + c0 + c, tv, tj);
-              }
+            if (m4 < tv[TOPK - 1]) {  // rare after the first tiles
+              if (v0 < tv[TOPK - 1]) topk_insert(v0, jb + 4 * q + 0, tv, tj);
+              if (v1 < tv[TOPK - 1]) topk_insert(v1, jb + 4 * q + 1, tv, tj);
+              if (v2 < tv[TOPK - 1]) topk_insert(v2, jb + 4 * q + 2, tv, tj);
+              if (v3 < tv[TOPK - 1]) topk_insert(v3, jb + 4 * q + 3, tv, tj);
             }
-          } else {
-            unsigned long long* hb = hitbuf + ew * HITBUF;
-            int fill = hitcnt[ew];
+          } else if (__any_sync(0xffffffffu, m4 <= my_lim)) {
+            const float vv[4] = {v0, v1, v2, v3};
 #pragma unroll
-            for (int c = 0; c < 64; ++c) {
-              const float v = fmaf(-2.0f, __uint_as_float(r[c]), __ldg(ynt + c0 + c));
-              const bool hit = mine && v <= my_lim;
+            for (int e = 0; e < 4; ++e) {
+              const bool hit = vv[e] <= my_lim;
               const unsigned bal = __ballot_sync(0xffffffffu, hit);
               if (bal) {
                 if (hit)
                   hb[fill + __popc(bal & ((1u << lane) - 1u))] =
-                      ((unsigned long long)grow << 32) | (unsigned long long)(tg * BN + half * (BN / 2) + c0 + c);
+                      ((unsigned long long)grow << 32) | (unsigned long long)(jb + 4 * q + e);
                 fill += __popc(bal);
                 if (fill > HITBUF - 32) {  // flush: one global atomic per buffer
                   __syncwarp();
                   unsigned long long base = 0;
                   if (lane == 0) base = atomicAdd(n_pairs, (unsigned long long)fill);
                   base = __shfl_sync(0xffffffffu, base, 0);
-                  for (int e = lane; e < fill; e += 32)
-                    if ((int64_t)(base + e) < cap) pairs[base + e] = hb[e];
+                  for (int f = lane; f < fill; f += 32)
+                    if ((int64_t)(base + f) < cap) pairs[base + f] = hb[f];
                   __syncwarp();
                   fill = 0;
                 }
               }
             }
-            __syncwarp();
-            if (lane == 0) hitcnt[ew] = fill;
-            __syncwarp();
           }
         }
+      }
+      if (MODE == 1) {
+        __syncwarp();
+        if (lane == 0) hitcnt[ew] = fill;
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(acc_empty + ab);
