@@ -501,6 +501,33 @@ __device__ __forceinline__ float fx_scale32(float mx, int nsamp) {
 
 // Returns false (nothing written) when the 36-bin argmax has no clear lead;
 // the caller then queues the keypoint for the float64 kernel.
+// Fast-path histograms: exact fixed point, two 26-bit limbs per bin (two
+// native 32-bit shared atomics per sample; 64 samples x 2^26 < 2^32), scale
+// 2^e chosen per keypoint from the largest magnitude so a bin sum stays
+// below 2^52: quantum ~2^-46 of the largest bin -- far below float32
+// resolution, so near-identical regions keep distinct descriptors (F6).
+constexpr int kLimb = 26;
+__device__ __forceinline__ double fx_scale52(double mx, int nsamp) {
+  if (!(mx > 0.0)) return 1.0;
+  int e;
+  frexp(mx * (double)nsamp * 1.0000001, &e);  // mx * nsamp < 2^e
+  return ldexp(1.0, 52 - e);
+}
+__device__ __forceinline__ void h2_add(unsigned* h, int nb, int bin, double mag, double fx) {
+  if (!(mag > 0.0)) return;
+  const unsigned long long q = __double2ull_rn(__dmul_rn(mag, fx));
+  atomicAdd(h + bin, (unsigned)(q & ((1u << kLimb) - 1u)));
+  atomicAdd(h + nb + bin, (unsigned)(q >> kLimb));
+}
+__device__ __forceinline__ unsigned long long h2_get(const unsigned* h, int nb, int bin) {
+  return ((unsigned long long)h[nb + bin] << kLimb) + (unsigned long long)h[bin];
+}
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
 template <int W>
 __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row, int col, const DescParams& prm,
                                                        unsigned* hbase, double* stage, float* __restrict__ o32,
@@ -512,9 +539,9 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
   const int nr = im.nr, nc = im.nc;
   const int r0 = min(max(row - W / 2, 1), nr - 1 - W);
   const int c0 = min(max(col - W / 2, 1), nc - 1 - W);
-  unsigned* h128 = hbase;
-  unsigned* h36 = hbase + D;
-  for (int q = lane; q < D + 36; q += 32) hbase[q] = 0u;
+  unsigned* h128 = hbase;         // [2][128]
+  unsigned* h36 = hbase + 2 * D;  // [2][36]
+  for (int q = lane; q < 2 * (D + 36); q += 32) hbase[q] = 0u;
   const int sx_ = lane & 15, sy_ = lane >> 4;
   stage_box_u8<(W + 3) / 2>(im, stage, SP, r0 - 1, c0 - 1, W + 2, W + 2, sx_, sy_);
   __syncwarp();
@@ -526,7 +553,7 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
     const double ori = mod_two_pi(__dsub_rn(atan2(b, a), shift), prm.two_pi);
     return min((int)__dmul_rn(ori, k), nbins - 1);
   };
-  float mg[SPL];
+  double mg[SPL];  // float64 magnitudes (~1 ulp): descriptors stay ~1e-15 accurate
   int bn[SPL];
   if (!prm.orient) {
 #pragma unroll
@@ -542,7 +569,7 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
         ob = side_bin(a, b, prm.c8[m], prm.s8[m], m, 8);
         if (ob < 0) ob = bin64(a, b, 0.0, prm.k8, 8);
       }
-      mg[j] = __fsqrt_rn(__fmaf_rn(af, af, bf * bf));
+      mg[j] = __dsqrt_rn(__fma_rn(a, a, __dmul_rn(b, b)));
       bn[j] = ((iv / WS) * 4 + iu / WS) * 8 + ob;
     }
   } else {
@@ -560,19 +587,18 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
         bin = side_bin(a, b, prm.cb36[m], prm.sb36[m], m, 36);
         if (bin < 0) bin = bin64(a, b, 0.0, prm.k36, 36);
       }
-      mg[j] = __fsqrt_rn(__fmaf_rn(af, af, bf * bf));
+      mg[j] = __dsqrt_rn(__fma_rn(a, a, __dmul_rn(b, b)));
       bn[j] = bin;
     }
-    float mx = mg[0];
+    double mx = mg[0];
 #pragma unroll
-    for (int j = 1; j < SPL; ++j) mx = fmaxf(mx, mg[j]);
-    const float f36 = fx_scale32(warp_max_f(mx), NS);
+    for (int j = 1; j < SPL; ++j) mx = fmax(mx, mg[j]);
+    const double f36 = fx_scale52(warp_max_d(mx), NS);
 #pragma unroll
-    for (int j = 0; j < SPL; ++j)
-      if (mg[j] > 0.0f) atomicAdd(h36 + bn[j], __float2uint_rn(mg[j] * f36));
+    for (int j = 0; j < SPL; ++j) h2_add(h36, 36, bn[j], mg[j], f36);
     __syncwarp();
     // argmax with a clear lead (else the whole keypoint is redone in float64)
-    const unsigned v1 = h36[lane], v2 = lane < 4 ? h36[lane + 32] : 0u;
+    const unsigned long long v1 = h2_get(h36, 36, lane), v2 = lane < 4 ? h2_get(h36, 36, lane + 32) : 0ull;
     const unsigned k1 = (__float_as_uint((float)v1) & ~63u) | (63u - lane);
     const unsigned k2 = lane < 4 ? ((__float_as_uint((float)v2) & ~63u) | (31u - lane)) : 0u;
     const unsigned top = __reduce_max_sync(0xffffffffu, max(k1, k2));
@@ -616,7 +642,7 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
       const double u = (double)iu - half, v = (double)iv - half;  // exact
       const double x = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, u)), __dmul_rn(st, v));
       const double y = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, u)), __dmul_rn(ct, v));
-      mg[j] = 0.0f;
+      mg[j] = 0.0;
       bn[j] = 0;
       if (!(x >= 1.0 && x <= xhi && y >= 1.0 && y <= yhi)) continue;  // hypot * valid = 0
       const double lx = __dsub_rn(fmin(fmax(x, (double)pc0), (double)pc1), (double)pc0);
@@ -643,51 +669,26 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
         ob = side_bin(as, bs, ce, se, m, 8);
         if (ob < 0) ob = bin64(as, bs, theta0, prm.k8, 8);
       }
-      mg[j] = __fsqrt_rn(__fmaf_rn(af, af, bf * bf));
+      mg[j] = __dsqrt_rn(__fma_rn(as, as, __dmul_rn(bs, bs)));
       bn[j] = ((iv / WS) * 4 + iu / WS) * 8 + ob;
     }
   }
-  float mx = mg[0];
+  double mx = mg[0];
 #pragma unroll
-  for (int j = 1; j < SPL; ++j) mx = fmaxf(mx, mg[j]);
-  const float fx = fx_scale32(warp_max_f(mx), NS);
+  for (int j = 1; j < SPL; ++j) mx = fmax(mx, mg[j]);
+  const double fx = fx_scale52(warp_max_d(mx), NS);
 #pragma unroll
-  for (int j = 0; j < SPL; ++j)
-    if (mg[j] > 0.0f) atomicAdd(h128 + bn[j], __float2uint_rn(mg[j] * fx));
+  for (int j = 0; j < SPL; ++j) h2_add(h128, D, bn[j], mg[j], fx);
   __syncwarp();
   // --- L2 normalise, clamp at 0.2, renormalise (descriptor.py:250-255)
   constexpr int kPer = D / 32;
-  if (o64 == nullptr) {
-    const float inv = 1.0f / fx;
-    float vals[kPer];
-    float ss = 0.0f;
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      vals[j] = (float)h128[lane + 32 * j] * inv;
-      ss = __fmaf_rn(vals[j], vals[j], ss);
-    }
-    ss = warp_sum_f(ss);
-    if (ss > 0.0f) {
-      const float r1 = rsqrtf(ss);
-      float ss2 = 0.0f;
-#pragma unroll
-      for (int j = 0; j < kPer; ++j) {
-        vals[j] = fminf(vals[j] * r1, 0.2f);
-        ss2 = __fmaf_rn(vals[j], vals[j], ss2);
-      }
-      const float r2 = rsqrtf(warp_sum_f(ss2));
-#pragma unroll
-      for (int j = 0; j < kPer; ++j) vals[j] *= r2;
-    }
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) o32[lane + 32 * j] = vals[j];
-  } else {
-    const double inv = 1.0 / (double)fx;
+  {
+    const double inv = 1.0 / fx;  // exact (power of two)
     double vals[kPer];
     double ss = 0.0;
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
-      vals[j] = __dmul_rn((double)h128[lane + 32 * j], inv);
+      vals[j] = __dmul_rn((double)h2_get(h128, D, lane + 32 * j), inv);
       ss = __dadd_rn(ss, __dmul_rn(vals[j], vals[j]));
     }
 #pragma unroll
@@ -710,7 +711,7 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
     for (int j = 0; j < kPer; ++j) {
       const double v = n1 > 0.0 ? __dmul_rn(vals[j], n2) : 0.0;
       if (o32) o32[lane + 32 * j] = __double2float_rn(v);
-      o64[lane + 32 * j] = v;
+      if (o64) o64[lane + 32 * j] = v;
     }
   }
   __syncwarp();
@@ -775,7 +776,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
 // warps); everything else -- other region sides and 36-bin near-ties -- is
 // queued for describe_kernel.
 constexpr int kFastWarps = 8;
-constexpr int kFastHist = 128 + 36;
+constexpr int kFastHist = 2 * (128 + 36);
 
 __global__ void __launch_bounds__(kFastWarps * 32, 4) describe_fast_u8(RampU8 img, int64_t img_stride, int B,
                                                                        const int32_t* __restrict__ kp_row,
