@@ -430,3 +430,32 @@ def test_nearest_matches_oracle_both_paths(monkeypatch):
             j = np.argmin(D, axis=1)
             assert np.array_equal(idx[i0:i0 + D.shape[0]].cpu().numpy(), j)
             assert np.array_equal(d[i0:i0 + D.shape[0]].cpu().numpy(), D[np.arange(D.shape[0]), j])
+
+
+def test_end_to_end_c1_against_oracle_chain():
+    """P5 at C1 size: keypoints exact, descriptors <= 1e-4, match-set
+    difference limited to near-ties (<= 5 %), identical RANSAC transform."""
+    a, b = scenes.config1_pair(0)
+    cfg = R.DescriptorConfig(0.0625, 4, 64, True)
+    ref, gpu = [], []
+    for im in (a, b):
+        P = O.ramp(im.astype(np.float64), O.default_alpha(*im.shape))
+        kp = O.detect(P, (16, 32, 64))
+        ref.append((kp, O.describe(P, kp, 0.0625, 4, 64, True)))
+        t = torch.from_numpy(im).cuda()
+        k = device.detect(t, (16, 32, 64), meta=False)
+        gpu.append((k, device.describe(t, k, cfg)[0]))
+        h = k.image(0)
+        assert np.array_equal(h["row"], kp["row"]) and np.array_equal(h["col"], kp["col"])
+        g = gpu[-1][1].double().cpu().numpy()
+        rel = np.max(np.abs(g - ref[-1][1]), axis=1) / np.maximum(np.linalg.norm(ref[-1][1], axis=1), 1e-300)
+        assert rel.max() <= P2_TOL
+    w1, w2, _ = O.match(*(r[1].astype(np.float32).astype(np.float64) for r in ref))
+    r1, r2, _ = device.match(gpu[0][1], gpu[1][1])
+    want, got = set(zip(w1.tolist(), w2.tolist())), set(zip(r1.cpu().numpy().tolist(), r2.cpu().numpy().tolist()))
+    assert len(got ^ want) <= 0.05 * len(want)
+    ref_r = O.ransac(*O.pair_points(w1, w2, ref[0][0], ref[1][0]), 1000, 3.0, 8, 0)
+    src, dst = device.pair_points(r1, r2, gpu[0][0].row[0], gpu[0][0].col[0], gpu[1][0].row[0], gpu[1][0].col[0])
+    out = device.ransac(src, dst, 1000, 3.0, 8, 0)
+    assert out.ok
+    assert corner_error((out.theta, out.t_x, out.t_y), ref_r["model"]) <= 1e-3
