@@ -45,9 +45,10 @@ constexpr int kEpiWarps = 8;    // two warps per TMEM lane quarter, 128 accumula
 constexpr uint32_t A_BYTES = BM * KD * 2;  // 32 KB
 constexpr uint32_t B_BYTES = BN * KD * 2;  // 64 KB
 constexpr int kThreads = 64 + 32 * kEpiWarps;  // warp 0 bulk copies, warp 1 MMA/TMEM, warps 2-9 epilogue
+constexpr uint32_t YN_BYTES = BN * 4;  // |y|^2 of one tile, staged per accumulator slot
 template <int MODE>
 constexpr size_t smem_bytes() {
-  return 1024 + A_BYTES + (MODE == 0 ? STAGES_TOP : STAGES_ENUM) * (size_t)B_BYTES + 256 +
+  return A_BYTES + (MODE == 0 ? STAGES_TOP : STAGES_ENUM) * (size_t)B_BYTES + 2 * YN_BYTES + 256 +
          (MODE == 0 ? 0 : kEpiWarps * (HITBUF * 8 + 16));
 }
 
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
                                                           unsigned long long* __restrict__ pairs,
                                                           unsigned long long* __restrict__ n_pairs, int64_t cap) {
   constexpr int STAGES = MODE == 0 ? STAGES_TOP : STAGES_ENUM;
-  extern __shared__ uint8_t smem_raw[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int nx = *cnt_x, ny = *cnt_y;
   const int rb = blockIdx.x;
   if (rb * BM >= nx) return;  // uniform for the whole CTA
@@ -146,16 +147,18 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
   const int t_begin = min(n_all, (int)blockIdx.y * per);
   const int n_tiles = min(n_all, t_begin + per) - t_begin;  // may be 0 (then lists stay empty)
   const int64_t nx_pad = (int64_t)gridDim.x * BM;
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw;  // 1024-aligned (SWIZZLE_128B atoms)
   uint8_t* sA = smem;
   uint8_t* sB = smem + A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  float* ysm = reinterpret_cast<float*>(sB + STAGES * B_BYTES);  // [2][BN]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ysm) + 2 * YN_BYTES);
   uint64_t* a_full = bars;
   uint64_t* b_full = bars + 1;
   uint64_t* b_empty = b_full + STAGES;
   uint64_t* acc_full = b_empty + STAGES;
   uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* y_full = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(y_full + 2);
   // MODE 1: per-epilogue-warp hit buffer + fill counter
   unsigned long long* hitbuf = reinterpret_cast<unsigned long long*>(bars + 32);
   int* hitcnt = reinterpret_cast<int*>(hitbuf + kEpiWarps * HITBUF);
@@ -171,6 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
     for (int s = 0; s < 2; ++s) {
       mbar_init(acc_full + s, 1);
       mbar_init(acc_empty + s, kEpiWarps * 32);
+      mbar_init(y_full + s, 1);
     }
     mbar_fence_init();
   }
@@ -189,6 +193,11 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
         mbar_wait(b_empty + s, ((t / STAGES) & 1) ^ 1);
         mbar_arrive_expect_tx(b_full + s, B_BYTES);
         bulk_g2s(sB + s * B_BYTES, Yt + (size_t)(t_begin + t) * B_BYTES, B_BYTES, b_full + s);
+        // |y|^2 of the tile into the slot of its accumulator, once the epilogue released it
+        const int ab = t & 1;
+        mbar_wait(acc_empty + ab, ((t >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(y_full + ab, YN_BYTES);
+        bulk_g2s(ysm + ab * BN, yn + (size_t)(t_begin + t) * BN, YN_BYTES, y_full + ab);
       }
     }
   } else if (warp == 1) {
@@ -226,10 +235,11 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
     for (int t = 0; t < n_tiles; ++t) {
       const int ab = t & 1;
       mbar_wait(acc_full + ab, (t >> 1) & 1);
+      mbar_wait(y_full + ab, (t >> 1) & 1);
       tc_fence_after();
       const int tg = t_begin + t;  // global tile index
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + ab * BN + half * (BN / 2);
-      const float* ynt = yn + (size_t)tg * BN + half * (BN / 2);
+      const float* ynt = ysm + ab * BN + half * (BN / 2);
       // one pass per 64-column chunk; groups of 4 columns are tested against the
       // row's threshold (4th best, or the enumeration limit) with one branch
       unsigned long long* hb = hitbuf + ew * HITBUF;
@@ -243,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
         const int jb = tg * BN + half * (BN / 2) + c0;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          const float4 y = __ldg(y4 + q);
+          const float4 y = y4[q];  // shared-memory broadcast
           const float v0 = fmaf(-2.0f, __uint_as_float(r[4 * q + 0]), y.x);
           const float v1 = fmaf(-2.0f, __uint_as_float(r[4 * q + 1]), y.y);
           const float v2 = fmaf(-2.0f, __uint_as_float(r[4 * q + 2]), y.z);
