@@ -40,11 +40,15 @@ constexpr int KD = 128;   // descriptor length
 constexpr int TOPK = 4;
 constexpr int STAGES_TOP = 3;   // Y-tile stages of the top-4 pass
 constexpr int STAGES_ENUM = 2;  // the enumeration pass trades one stage for per-warp hit buffers
-constexpr int HITBUF = 512;     // hits staged per epilogue warp before one bulk append
-constexpr int kEpiWarps = 8;    // two warps per TMEM lane quarter, 128 accumulator columns each
+#ifndef PS_EPI_WARPS
+#define PS_EPI_WARPS 16
+#endif
+constexpr int kEpiWarps = PS_EPI_WARPS;  // kParts warps per TMEM lane quarter, BN / kParts columns each
+constexpr int kParts = kEpiWarps / 4;    // top-4 lists per (row, split)
+constexpr int HITBUF = 4096 / kEpiWarps;  // hits staged per epilogue warp before one bulk append
 constexpr uint32_t A_BYTES = BM * KD * 2;  // 32 KB
 constexpr uint32_t B_BYTES = BN * KD * 2;  // 64 KB
-constexpr int kThreads = 64 + 32 * kEpiWarps;  // warp 0 bulk copies, warp 1 MMA/TMEM, warps 2-9 epilogue
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // warp 0 bulk copies, warp 1 MMA/TMEM, warps 2.. epilogue
 constexpr uint32_t YN_BYTES = BN * 4;  // |y|^2 of one tile, staged per accumulator slot
 template <int MODE>
 constexpr size_t smem_bytes() {
@@ -127,8 +131,8 @@ __device__ __forceinline__ void topk_insert(float v, int j, float (&tv)[TOPK], i
 // MODE 0: per-row top-4 of v.  MODE 1: enumerate every (row, column) with
 // v <= lim[row] into pairs (row << 32 | column), capacity `cap`.
 // grid = (row blocks, splits): CTA (rb, sp) streams the sp-th contiguous
-// share of the Y tiles; MODE 0 writes one top-4 list per (split, half) --
-// list index sp * 2 + half of row g at topv[(list * nx_pad + g) * TOPK].
+// share of the Y tiles; MODE 0 writes one top-4 list per (split, part) --
+// list index sp * kParts + part of row g at topv[(list * nx_pad + g) * TOPK].
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Yt,
                                                           const float* __restrict__ yn,
@@ -222,9 +226,10 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
         mma_commit(acc_full + ab);
       }
     }
-  } else {  // ---- epilogue: thread = row, warp pair per lane quarter splits the columns
+  } else {  // ---- epilogue: thread = row, kParts warps per lane quarter split the columns
     const int quarter = warp & 3;
-    const int ew = warp - 2, half = ew >> 2;
+    const int ew = warp - 2, part = ew >> 2;
+    constexpr int kCols = BN / kParts;
     const int row = quarter * 32 + lane;
     float tv[TOPK];
     int tj[TOPK];
@@ -238,19 +243,19 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
       mbar_wait(y_full + ab, (t >> 1) & 1);
       tc_fence_after();
       const int tg = t_begin + t;  // global tile index
-      const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + ab * BN + half * (BN / 2);
-      const float* ynt = ysm + ab * BN + half * (BN / 2);
+      const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + ab * BN + part * kCols;
+      const float* ynt = ysm + ab * BN + part * kCols;
       // one pass per 64-column chunk; groups of 4 columns are tested against the
       // row's threshold (4th best, or the enumeration limit) with one branch
       unsigned long long* hb = hitbuf + ew * HITBUF;
       int fill = MODE == 1 ? hitcnt[ew] : 0;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN / 2; c0 += 64) {
+      for (int c0 = 0; c0 < kCols; c0 += 64) {
         uint32_t r[64];
         tmem_ld64(tbase + c0, r);
         tmem_ld_wait();
         const float4* y4 = reinterpret_cast<const float4*>(ynt + c0);
-        const int jb = tg * BN + half * (BN / 2) + c0;
+        const int jb = tg * BN + part * kCols + c0;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
           const float4 y = y4[q];  // shared-memory broadcast
@@ -310,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
         if ((int64_t)(base + e) < cap) pairs[base + e] = hb[e];
     }
     if (MODE == 0 && grow < nx) {
-      const int64_t list = (int64_t)blockIdx.y * 2 + half;
+      const int64_t list = (int64_t)blockIdx.y * kParts + part;
 #pragma unroll
       for (int q = 0; q < TOPK; ++q) {
         topv[(list * nx_pad + grow) * TOPK + q] = tv[q];
@@ -686,8 +691,8 @@ TcWs carve_tc(void* base, int64_t n1, int64_t n2, size_t* used) {
   w.xinfo = ar.take<double>(3 * xrows);
   w.yinfo = ar.take<double>(3 * yrows);
   w.ymax = ar.take<unsigned>(4);
-  w.topv = ar.take<float>(xrows * TOPK * 2 * kMaxSplit);
-  w.topj = ar.take<int32_t>(xrows * TOPK * 2 * kMaxSplit);
+  w.topv = ar.take<float>(xrows * TOPK * kParts * kMaxSplit);
+  w.topj = ar.take<int32_t>(xrows * TOPK * kParts * kMaxSplit);
   w.nn12 = ar.take<int32_t>(n1);
   w.d12 = ar.take<double>(n1);
   w.nn21 = ar.take<int32_t>(n2);
@@ -769,7 +774,7 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
                                                       nullptr, 0);
   PS_LAUNCHED("nn_topk_tc<top4>");
   certify_exact<T><<<grid_for(nx, 32), 256, 0, st>>>(w.topv, w.topj, n_x, x_idx, y_idx, w.xinfo, w.ymax, X, Y, nn,
-                                                      dist, w.overflow, w.n_overflow, w.lim, 2 * (int)g0.y,
+                                                      dist, w.overflow, w.n_overflow, w.lim, kParts * (int)g0.y,
                                                       (int64_t)g0.x * BM);
   PS_LAUNCHED("certify_exact");
   // rows with more near-tied candidates than the top-4: enumerate every
