@@ -38,7 +38,7 @@ constexpr int BM = 128;   // X rows per CTA (= TMEM lanes)
 constexpr int BN = 256;   // Y rows per tile (= MMA N, TMEM columns)
 constexpr int KD = 128;   // descriptor length
 constexpr int TOPK = 4;
-constexpr int STAGES_TOP = 3;   // Y-tile stages of the top-4 pass
+constexpr int STAGES_TOP = 2;   // Y-tile stages (2 x 72 KB)
 constexpr int STAGES_ENUM = 2;  // the enumeration pass trades one stage for per-warp hit buffers
 #ifndef PS_EPI_WARPS
 #define PS_EPI_WARPS 16
@@ -46,26 +46,33 @@ constexpr int STAGES_ENUM = 2;  // the enumeration pass trades one stage for per
 constexpr int kEpiWarps = PS_EPI_WARPS;  // kParts warps per TMEM lane quarter, BN / kParts columns each
 constexpr int kParts = kEpiWarps / 4;    // top-4 lists per (row, split)
 constexpr int HITBUF = 4096 / kEpiWarps;  // hits staged per epilogue warp before one bulk append
-constexpr uint32_t A_BYTES = BM * KD * 2;  // 32 KB
-constexpr uint32_t B_BYTES = BN * KD * 2;  // 64 KB
+// Each operand tile is the K-major SW128 image of the 128 descriptor columns
+// followed by a 16-column augmentation block (no swizzle, 32 B per row): X rows
+// carry (1, 1, 1, 0...), Y rows carry -- with the descriptor part scaled by -2
+// (exact) -- the three-term fp16 split of |y|^2 (padding: +inf).  The ninth
+// MMA k-step then leaves v = |y|^2 - 2 x.y in TMEM.
+constexpr int KA = 16;                           // augmentation columns
+constexpr uint32_t ROW_BYTES = KD * 2 + KA * 2;  // 288
+constexpr uint32_t A_BYTES = BM * ROW_BYTES;     // 36 KB
+constexpr uint32_t B_BYTES = BN * ROW_BYTES;     // 72 KB
 constexpr int kThreads = 64 + 32 * kEpiWarps;  // warp 0 bulk copies, warp 1 MMA/TMEM, warps 2.. epilogue
-constexpr uint32_t YN_BYTES = BN * 4;  // |y|^2 of one tile, staged per accumulator slot
 template <int MODE>
 constexpr size_t smem_bytes() {
-  return A_BYTES + (MODE == 0 ? STAGES_TOP : STAGES_ENUM) * (size_t)B_BYTES + 2 * YN_BYTES + 256 +
+  return A_BYTES + (MODE == 0 ? STAGES_TOP : STAGES_ENUM) * (size_t)B_BYTES + 256 +
          (MODE == 0 ? 0 : kEpiWarps * (HITBUF * 8 + 16));
 }
 
 // ---- operand preparation ----------------------------------------------------------
 // Row u of the output (u < count) is source row idx[u] (or u); rows >= count are
-// zero.  Writes the fp16 K-major SW128 tile image, |x|^2 as float (+inf for
-// padding when pad_inf), and float64 |x|, |x - x_h|, |x_h|; folds their maxima
-// into maxes[0..2] (non-negative float bits).
+// zero.  Writes the tile image (fp16 K-major SW128 descriptor part, then the
+// augmentation block; `is_y` selects the Y form: -2 x_h and the split |y|^2,
+// +inf for padding rows), and float64 |x|, |x - x_h|, |x_h|; folds their
+// maxima into maxes[0..2] (non-negative float bits).
 template <class T>
 __global__ void prep_tiles(const T* __restrict__ src, const int32_t* __restrict__ idx,
                            const int32_t* __restrict__ count_p, int64_t count_const, int64_t n_pad, int R,
-                           uint8_t* __restrict__ tiles, float* __restrict__ norm2, double* __restrict__ info,
-                           unsigned* __restrict__ maxes, int pad_inf) {
+                           uint8_t* __restrict__ tiles, double* __restrict__ info, unsigned* __restrict__ maxes,
+                           int is_y) {
   const int lane = threadIdx.x & 31;
   const int64_t count = count_p ? (int64_t)*count_p : count_const;
   for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < n_pad;
@@ -94,15 +101,39 @@ __global__ void prep_tiles(const T* __restrict__ src, const int32_t* __restrict_
     }
     const int64_t tile = u / R;
     const int r = (int)(u % R);
-    uint8_t* base = tiles + tile * (int64_t)R * KD * 2;
+    uint8_t* base = tiles + tile * (int64_t)R * ROW_BYTES;
     const uint32_t off = sw128_offset(R, r, lane * 4);
+    if (is_y) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) h[e] = __hmul(h[e], __float2half(-2.0f));  // exact
+    }
     __half2 p0 = __halves2half2(h[0], h[1]), p1 = __halves2half2(h[2], h[3]);
     uint2 pk;
     pk.x = *reinterpret_cast<uint32_t*>(&p0);
     pk.y = *reinterpret_cast<uint32_t*>(&p1);
     *reinterpret_cast<uint2*>(base + off) = pk;
+    if (lane < 2) {  // augmentation block: core matrix (r / 8, k / 8), 16 B per row
+      uint4 q = make_uint4(0u, 0u, 0u, 0u);
+      if (lane == 0) {
+        __half a0, a1, a2;
+        if (!is_y) {
+          a0 = a1 = a2 = __float2half(1.0f);
+        } else if (!live) {
+          a0 = __float2half(INFINITY);
+          a1 = a2 = __float2half(0.0f);
+        } else {  // |y|^2 = a0 + a1 + a2 (to ~2^-33 relative, or a0 = inf when out of range)
+          a0 = __double2half(sx);
+          const double r1 = __hisinf(a0) ? 0.0 : sx - (double)__half2float(a0);
+          a1 = __double2half(r1);
+          a2 = __double2half(r1 - (double)__half2float(a1));
+        }
+        const __half2 q0 = __halves2half2(a0, a1), q1 = __halves2half2(a2, __float2half(0.0f));
+        q.x = *reinterpret_cast<const uint32_t*>(&q0);
+        q.y = *reinterpret_cast<const uint32_t*>(&q1);
+      }
+      *reinterpret_cast<uint4*>(base + R * KD * 2 + (r >> 3) * 256 + lane * 128 + (r & 7) * 16) = q;
+    }
     if (lane == 0) {
-      norm2[u] = live ? (float)sx : (pad_inf ? INFINITY : 0.0f);
       info[3 * u + 0] = sqrt(sx);
       info[3 * u + 1] = sqrt(sr);
       info[3 * u + 2] = sqrt(sh);
@@ -135,7 +166,6 @@ __device__ __forceinline__ void topk_insert(float v, int j, float (&tv)[TOPK], i
 // list index sp * kParts + part of row g at topv[(list * nx_pad + g) * TOPK].
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Yt,
-                                                          const float* __restrict__ yn,
                                                           const int32_t* __restrict__ cnt_x,
                                                           const int32_t* __restrict__ cnt_y, float* __restrict__ topv,
                                                           int32_t* __restrict__ topj, const float* __restrict__ lim,
@@ -154,15 +184,13 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
   uint8_t* smem = smem_raw;  // 1024-aligned (SWIZZLE_128B atoms)
   uint8_t* sA = smem;
   uint8_t* sB = smem + A_BYTES;
-  float* ysm = reinterpret_cast<float*>(sB + STAGES * B_BYTES);  // [2][BN]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(ysm) + 2 * YN_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
   uint64_t* a_full = bars;
   uint64_t* b_full = bars + 1;
   uint64_t* b_empty = b_full + STAGES;
   uint64_t* acc_full = b_empty + STAGES;
   uint64_t* acc_empty = acc_full + 2;
-  uint64_t* y_full = acc_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(y_full + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   // MODE 1: per-epilogue-warp hit buffer + fill counter
   unsigned long long* hitbuf = reinterpret_cast<unsigned long long*>(bars + 32);
   int* hitcnt = reinterpret_cast<int*>(hitbuf + kEpiWarps * HITBUF);
@@ -178,7 +206,6 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
     for (int s = 0; s < 2; ++s) {
       mbar_init(acc_full + s, 1);
       mbar_init(acc_empty + s, kEpiWarps * 32);
-      mbar_init(y_full + s, 1);
     }
     mbar_fence_init();
   }
@@ -197,11 +224,6 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
         mbar_wait(b_empty + s, ((t / STAGES) & 1) ^ 1);
         mbar_arrive_expect_tx(b_full + s, B_BYTES);
         bulk_g2s(sB + s * B_BYTES, Yt + (size_t)(t_begin + t) * B_BYTES, B_BYTES, b_full + s);
-        // |y|^2 of the tile into the slot of its accumulator, once the epilogue released it
-        const int ab = t & 1;
-        mbar_wait(acc_empty + ab, ((t >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(y_full + ab, YN_BYTES);
-        bulk_g2s(ysm + ab * BN, yn + (size_t)(t_begin + t) * BN, YN_BYTES, y_full + ab);
       }
     }
   } else if (warp == 1) {
@@ -222,6 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
           const uint64_t bd = sdesc_k_sw128(b0 + (k >> 2) * (BN * 128) + koff);
           mma_f16(tmem + ab * BN, ad, bd, idesc, k > 0 ? 1u : 0u);
         }
+        mma_f16(tmem + ab * BN, sdesc_k_none(a0 + BM * KD * 2), sdesc_k_none(b0 + BN * KD * 2), idesc, 1u);
         mma_commit(b_empty + s);
         mma_commit(acc_full + ab);
       }
@@ -240,11 +263,9 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
     for (int t = 0; t < n_tiles; ++t) {
       const int ab = t & 1;
       mbar_wait(acc_full + ab, (t >> 1) & 1);
-      mbar_wait(y_full + ab, (t >> 1) & 1);
       tc_fence_after();
       const int tg = t_begin + t;  // global tile index
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + ab * BN + part * kCols;
-      const float* ynt = ysm + ab * BN + part * kCols;
       // one pass per 64-column chunk; groups of 4 columns are tested against the
       // row's threshold (4th best, or the enumeration limit) with one branch
       unsigned long long* hb = hitbuf + ew * HITBUF;
@@ -254,15 +275,13 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
         uint32_t r[64];
         tmem_ld64(tbase + c0, r);
         tmem_ld_wait();
-        const float4* y4 = reinterpret_cast<const float4*>(ynt + c0);
         const int jb = tg * BN + part * kCols + c0;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          const float4 y = y4[q];  // shared-memory broadcast
-          const float v0 = fmaf(-2.0f, __uint_as_float(r[4 * q + 0]), y.x);
-          const float v1 = fmaf(-2.0f, __uint_as_float(r[4 * q + 1]), y.y);
-          const float v2 = fmaf(-2.0f, __uint_as_float(r[4 * q + 2]), y.z);
-          const float v3 = fmaf(-2.0f, __uint_as_float(r[4 * q + 3]), y.w);
+          const float v0 = __uint_as_float(r[4 * q + 0]);
+          const float v1 = __uint_as_float(r[4 * q + 1]);
+          const float v2 = __uint_as_float(r[4 * q + 2]);
+          const float v3 = __uint_as_float(r[4 * q + 3]);
           const float m4 = fminf(fminf(v0, v1), fminf(v2, v3));
           if (MODE == 0) {
             if (m4 < tv[TOPK - 1]) {  // rare after the first tiles
@@ -271,11 +290,12 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
               if (v2 < tv[TOPK - 1]) topk_insert(v2, jb + 4 * q + 2, tv, tj);
               if (v3 < tv[TOPK - 1]) topk_insert(v3, jb + 4 * q + 3, tv, tj);
             }
-          } else if (__any_sync(0xffffffffu, m4 <= my_lim)) {
+          } else if (__any_sync(0xffffffffu, !(m4 > my_lim))) {
             const float vv[4] = {v0, v1, v2, v3};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const bool hit = vv[e] <= my_lim;
+              // NaN / inf limits enumerate every real column (padding columns hold +inf)
+            const bool hit = !(vv[e] > my_lim) && jb + 4 * q + e < ny;
               const unsigned bal = __ballot_sync(0xffffffffu, hit);
               if (bal) {
                 if (hit)
@@ -388,9 +408,14 @@ __global__ void certify_exact(const float* __restrict__ topv, const int32_t* __r
     const int xi = x_orig ? x_orig[uu] : uu;
     const double rx = xinfo[3 * uu + 1], hx = xinfo[3 * uu + 2];
     // |v - (d^2 - |x|^2)| <= 2(|x - x_h||y| + |x_h||y - y_h|) + 2 g |x_h||y_h| + rounding of v
-    const double gamma = 128.0 * 2.384185791015625e-07;  // 128 * 2^-22 (fp32 accumulation)
-    const double E = 1.01 * (2.0 * (rx * Nmax + hx * Rmax) + 2.0 * gamma * hx * Hmax +
-                             4.8e-7 * (1.0 + Nmax * Nmax) + 4.8e-7 * 2.0 * hx * Hmax);
+    // v = fp32-accumulated sum of 144 fp16 products: x_h . (-2 y_h) plus the
+    // three-term split of |y|^2 (split error <= 2^-33 |y|^2 + fp16 underflow)
+    const double gamma = 144.0 * 2.384185791015625e-07;  // 144 * 2^-22 (fp32 accumulation)
+    double E = 1.01 * (2.0 * (rx * Nmax + hx * Rmax) + gamma * (2.0 * hx * Hmax + Nmax * Nmax) +
+                       1e-9 * Nmax * Nmax + 1.2e-7);
+    // out of the fp16 range (|y|^2 split to inf, or elements): no certificate --
+    // every column is enumerated and the rows fall back to the exact scan
+    if (!(E < 1e30) || !(Nmax * Nmax < 6.0e4)) E = INFINITY;
     float tv[TOPK];
     int tj[TOPK];
 #pragma unroll
@@ -623,7 +648,7 @@ struct TcWs {
   void* cub_tmp;
   size_t cub_bytes;
   uint8_t *xt, *yt;
-  float *yn, *xn, *topv;
+  float* topv;
   double *xinfo, *yinfo;
   unsigned* ymax;
   int32_t *topj, *nn12, *nn21, *overflow, *n_overflow, *colflag, *cols, *n_cols, *xsrc, *best_j;
@@ -684,10 +709,8 @@ TcWs carve_tc(void* base, int64_t n1, int64_t n2, size_t* used) {
   w.cub_bytes = cub_need(nmax);
   w.cub_tmp = ar.take<char>(w.cub_bytes);
   const int64_t xrows = rup(nmax, BM), yrows = rup(nmax, BN);
-  w.xt = ar.take<uint8_t>((size_t)xrows * KD * 2);
-  w.yt = ar.take<uint8_t>((size_t)yrows * KD * 2);
-  w.yn = ar.take<float>(yrows);
-  w.xn = ar.take<float>(xrows);
+  w.xt = ar.take<uint8_t>((size_t)xrows * ROW_BYTES);
+  w.yt = ar.take<uint8_t>((size_t)yrows * ROW_BYTES);
   w.xinfo = ar.take<double>(3 * xrows);
   w.yinfo = ar.take<double>(3 * yrows);
   w.ymax = ar.take<unsigned>(4);
@@ -754,10 +777,9 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   const int64_t xrows = rup(nx_max, BM), yrows = rup(ny_all, BN);
   cudaMemsetAsync(w.ymax, 0, 4 * sizeof(unsigned), st);
   cudaMemsetAsync(w.n_overflow, 0, sizeof(int32_t), st);
-  prep_tiles<T><<<grid_for(xrows, 8), 256, 0, st>>>(X, x_idx, n_x, 0, xrows, BM, w.xt, w.xn, w.xinfo,
-                                                      nullptr, 0);
+  prep_tiles<T><<<grid_for(xrows, 8), 256, 0, st>>>(X, x_idx, n_x, 0, xrows, BM, w.xt, w.xinfo, nullptr, 0);
   PS_LAUNCHED("prep_tiles(X)");
-  prep_tiles<T><<<grid_for(yrows, 8), 256, 0, st>>>(Y, y_idx, n_y, 0, yrows, BN, w.yt, w.yn, w.yinfo, w.ymax, 1);
+  prep_tiles<T><<<grid_for(yrows, 8), 256, 0, st>>>(Y, y_idx, n_y, 0, yrows, BN, w.yt, w.yinfo, w.ymax, 1);
   PS_LAUNCHED("prep_tiles(Y)");
   static bool attr = false;
   if (!attr) {
@@ -770,7 +792,7 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   const dim3 g0 = tc_grid(nx, ny);
   const int64_t flops_tile = 2ll * BM * BN * KD;
   g_stats[5] += (int64_t)g0.x * ((ny + BN - 1) / BN) * flops_tile;
-  nn_topk_tc<0><<<g0, kThreads, smem_bytes<0>(), st>>>(w.xt, w.yt, w.yn, n_x, n_y, w.topv, w.topj, nullptr, nullptr,
+  nn_topk_tc<0><<<g0, kThreads, smem_bytes<0>(), st>>>(w.xt, w.yt, n_x, n_y, w.topv, w.topj, nullptr, nullptr,
                                                       nullptr, 0);
   PS_LAUNCHED("nn_topk_tc<top4>");
   certify_exact<T><<<grid_for(nx, 32), 256, 0, st>>>(w.topv, w.topj, n_x, x_idx, y_idx, w.xinfo, w.ymax, X, Y, nn,
@@ -781,8 +803,7 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   // column within their certified limit on the tensor cores, then decide exactly
   gather_rows<<<grid_for(nx_max, 256), 256, 0, st>>>(w.overflow, w.n_overflow, x_idx, w.xsrc);
   PS_LAUNCHED("gather_rows");
-  prep_tiles<T><<<grid_for(xrows, 8), 256, 0, st>>>(X, w.xsrc, w.n_overflow, 0, xrows, BM, w.xt, w.xn, w.xinfo,
-                                                      nullptr, 0);
+  prep_tiles<T><<<grid_for(xrows, 8), 256, 0, st>>>(X, w.xsrc, w.n_overflow, 0, xrows, BM, w.xt, w.xinfo, nullptr, 0);
   PS_LAUNCHED("prep_tiles(overflow)");
   cudaMemsetAsync(w.n_pairs, 0, sizeof(unsigned long long), st);
   cudaMemsetAsync(w.best_bits, 0xff, nx_max * sizeof(unsigned long long), st);
@@ -791,7 +812,7 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   g_stats[3] += n_over;
   if (n_over > 0) {
     g_stats[5] += (int64_t)tc_grid(n_over, ny).x * ((ny + BN - 1) / BN) * flops_tile;
-    nn_topk_tc<1><<<tc_grid(n_over, ny), kThreads, smem_bytes<1>(), st>>>(w.xt, w.yt, w.yn, w.n_overflow, n_y, nullptr,
+    nn_topk_tc<1><<<tc_grid(n_over, ny), kThreads, smem_bytes<1>(), st>>>(w.xt, w.yt, w.n_overflow, n_y, nullptr,
                                                                           nullptr, w.lim, w.pairs, w.n_pairs,
                                                                           w.pair_cap);
     PS_LAUNCHED("nn_topk_tc<enumerate>");

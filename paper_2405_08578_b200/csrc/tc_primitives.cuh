@@ -112,6 +112,17 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t saddr) {
   return d;
 }
 
+// Shared-memory matrix descriptor, K-major, no swizzle, one 16-column K slice:
+// 8-row x 16-B core matrices, the two K-adjacent ones 128 B apart (LBO), the
+// 8-row groups 256 B apart (SBO); layout type 0.
+__device__ __forceinline__ uint64_t sdesc_k_none(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(128u >> 4) << 16;
+  d |= (uint64_t)(256u >> 4) << 32;
+  d |= (uint64_t)1u << 46;
+  return d;
+}
+
 // Instruction descriptor, kind::f16: D f32 [4,6)=1, A/B f16 [7,10)/[10,13)=0,
 // both K-major, N >> 3 at [17,23), M >> 4 at [24,29).
 __host__ __device__ constexpr uint32_t idesc_f16_f32(int M, int N) {

@@ -432,6 +432,24 @@ def test_nearest_matches_oracle_both_paths(monkeypatch):
             assert np.array_equal(d[i0:i0 + D.shape[0]].cpu().numpy(), D[np.arange(D.shape[0]), j])
 
 
+@pytest.mark.parametrize("scale", [1e-3, 3.0, 50.0])
+def test_nearest_tc_unnormalised_magnitudes(monkeypatch, scale):
+    """Tensor-core path on unnormalised rows: tiny values (fp16 subnormals in the
+    |y|^2 split), moderate ones, and |y|^2 beyond the fp16 range (no
+    certificate: every row must fall back to the exact scan)."""
+    monkeypatch.setenv("PS_TC_MIN_PAIRS", "0")
+    monkeypatch.delenv("PS_MATCH_EXACT", raising=False)
+    rng = np.random.default_rng(int(scale * 1000))
+    X = (rng.random((260, 128)) * scale).astype(np.float32)
+    Y = (rng.random((300, 128)) * scale).astype(np.float32)
+    Y[:100] = X[:100] + np.float32(0.01 * scale) * rng.standard_normal((100, 128)).astype(np.float32)
+    idx, d = device.nearest(torch.from_numpy(X).cuda(), torch.from_numpy(Y).cuda())
+    for i0, D in O.distances(X.astype(np.float64), Y.astype(np.float64)):
+        j = np.argmin(D, axis=1)
+        assert np.array_equal(idx[i0:i0 + D.shape[0]].cpu().numpy(), j)
+        assert np.array_equal(d[i0:i0 + D.shape[0]].cpu().numpy(), D[np.arange(D.shape[0]), j])
+
+
 def test_end_to_end_c1_against_oracle_chain():
     """P5 at C1 size: keypoints exact, descriptors <= 1e-4, match-set
     difference limited to near-ties (<= 5 %), identical RANSAC transform."""
