@@ -68,6 +68,9 @@ constexpr size_t smem_bytes() {
 // augmentation block; `is_y` selects the Y form: -2 x_h and the split |y|^2,
 // +inf for padding rows), and float64 |x|, |x - x_h|, |x_h|; folds their
 // maxima into maxes[0..2] (non-negative float bits).
+// max that propagates NaN (its bits order above +inf as unsigned)
+__device__ __forceinline__ float nan_max(float a, float b) { return (b != b || b > a) ? b : a; }
+
 template <class T>
 __global__ void prep_tiles(const T* __restrict__ src, const int32_t* __restrict__ idx,
                            const int32_t* __restrict__ count_p, int64_t count_const, int64_t n_pad, int R,
@@ -75,7 +78,10 @@ __global__ void prep_tiles(const T* __restrict__ src, const int32_t* __restrict_
                            int is_y) {
   const int lane = threadIdx.x & 31;
   const int64_t count = count_p ? (int64_t)*count_p : count_const;
-  for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < n_pad;
+  // only the tiles that hold live rows are ever read
+  const int64_t n_used = min(n_pad, (count + R - 1) / R * R);
+  float mx0 = 0.0f, mx1 = 0.0f, mx2 = 0.0f;  // lane 0: running maxima of this warp's rows
+  for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < n_used;
        u += (int64_t)gridDim.x * (blockDim.x >> 5)) {
     const bool live = u < count;
     const int64_t s = live ? (idx ? (int64_t)idx[u] : u) : 0;
@@ -137,12 +143,23 @@ __global__ void prep_tiles(const T* __restrict__ src, const int32_t* __restrict_
       info[3 * u + 0] = sqrt(sx);
       info[3 * u + 1] = sqrt(sr);
       info[3 * u + 2] = sqrt(sh);
-      if (live && maxes) {
-        atomicMax(maxes + 0, __float_as_uint((float)(sqrt(sx) * (1.0 + 1e-6))));
-        atomicMax(maxes + 1, __float_as_uint((float)(sqrt(sr) * (1.0 + 1e-6))));
-        atomicMax(maxes + 2, __float_as_uint((float)(sqrt(sh) * (1.0 + 1e-6))));
+      if (live) {
+        mx0 = nan_max(mx0, (float)(sqrt(sx) * (1.0 + 1e-6)));
+        mx1 = nan_max(mx1, (float)(sqrt(sr) * (1.0 + 1e-6)));
+        mx2 = nan_max(mx2, (float)(sqrt(sh) * (1.0 + 1e-6)));
       }
     }
+  }
+  if (!maxes) return;
+  // one atomic per block and quantity (same-address atomics per row serialise)
+  __shared__ float smx[3][32];
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) { smx[0][w] = mx0; smx[1][w] = mx1; smx[2][w] = mx2; }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    float m = 0.0f;
+    for (int q = 0; q < nw; ++q) m = nan_max(m, smx[threadIdx.x][q]);
+    if (m != 0.0f) atomicMax(maxes + threadIdx.x, __float_as_uint(m));
   }
 }
 
@@ -660,7 +677,8 @@ struct TcWs {
 
 inline int64_t rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
-constexpr int kMaxSplit = 16;
+constexpr int kMaxSplit = 8;
+constexpr int kSMs = 148;
 
 // statistics of the last tensor-core match on this thread (ps_match_stats)
 thread_local int64_t g_stats[8];  // uniq_a, uniq_b, cols, overflow rows, enumerated pairs, mma flops, -, -
@@ -672,12 +690,21 @@ int32_t read_count(const int32_t* p, cudaStream_t st) {
   return h;
 }
 
-// row blocks x column splits so that about two CTAs per SM are in flight
+// row blocks x column splits.  One CTA per SM is resident (~180 KB of shared
+// memory), so the split minimises waves x (tiles per CTA + per-CTA overhead,
+// about four tiles' worth: launch, TMEM allocation, X tile, pipeline fill).
 dim3 tc_grid(int64_t rows, int64_t cols) {
   const int rb = (int)std::max<int64_t>(1, (rows + BM - 1) / BM);
   const int tiles = (int)std::max<int64_t>(1, (cols + BN - 1) / BN);
-  const int split = std::max(1, std::min({kMaxSplit, tiles, (2 * 148 + rb - 1) / rb}));
-  return dim3(rb, split);
+  int best = 1;
+  int64_t best_cost = INT64_MAX;
+  for (int s = 1; s <= std::min(kMaxSplit, tiles); ++s) {
+    const int64_t waves = ((int64_t)rb * s + kSMs - 1) / kSMs;
+    const int64_t cost = waves * ((tiles + s - 1) / s + 4);
+    if (cost < best_cost) { best_cost = cost; best = s; }
+  }
+  if (const char* e = getenv("PS_TC_SPLIT")) best = std::max(1, std::min({atoi(e), kMaxSplit, tiles}));  // diagnostic
+  return dim3(rb, best);
 }
 
 size_t cub_need(int64_t n) {
