@@ -11,6 +11,7 @@
 // Accepted pairs are sorted by (delta, ref1, ref2) with stable radix sorts.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "ps_common.cuh"
@@ -376,9 +377,18 @@ extern "C" int ps_match(const void* desc1, int64_t n1, const void* desc2, int64_
   if (rc) return rc;
   // Sort by (delta, ref1, ref2): two stable radix passes, pair key first,
   // then delta bits (non-negative doubles order like their bit patterns).
-  // cub needs a host-side length, so the whole candidate capacity is sorted
-  // with unused slots padded by all-ones keys (they sort last).
-  const int n = (int)(cand > 0 ? cand : 1);
+  // cub needs a host-side length: the tensor-core path has synchronised with
+  // the host already, so its accepted count is read back and only those keys
+  // are sorted; the asynchronous CUDA-core path sorts the whole candidate
+  // capacity with unused slots padded by all-ones keys (they sort last).
+  int n = (int)(cand > 0 ? cand : 1);
+  if (tc) {
+    unsigned long long c = 0;
+    cudaMemcpyAsync(&c, w.counter, sizeof(c), cudaMemcpyDeviceToHost, st);
+    const cudaError_t e = cudaStreamSynchronize(st);
+    PS_REQUIRE(e == cudaSuccess, PS_ERR_CUDA, "match count: %s", cudaGetErrorString(e));
+    n = (int)std::max<unsigned long long>(1ull, std::min<unsigned long long>(c, (unsigned long long)n));
+  }
   pad_unused<<<grid_blocks(n, 256), 256, 0, st>>>(w.kp, w.kd, w.counter, n);
   PS_LAUNCHED("pad_unused");
   size_t tb = w.tmp_bytes;

@@ -593,21 +593,30 @@ __global__ void row_hash(const T* __restrict__ X, int64_t n, unsigned long long*
 // are bitwise equal to it, else itself.  flag[i] = (rep == i).
 __global__ void run_heads(const unsigned long long* __restrict__ hs, int64_t n, int32_t* __restrict__ head) {
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
-    head[p] = (p == 0 || hs[p - 1] != hs[p]) ? (int32_t)p : 0;
+    head[p] = (p == 0 || (uint32_t)hs[p - 1] != (uint32_t)hs[p]) ? (int32_t)p : 0;  // sort key: low 32 bits
 }
 
 template <class T>
 __global__ void mark_reps(const T* __restrict__ X, int64_t n, const int32_t* __restrict__ run_start,
                           const int32_t* __restrict__ idx, int32_t* __restrict__ rep, int32_t* __restrict__ flag) {
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+  // one warp per sorted position: lanes compare 4 elements each, coalesced
+  const int lane = threadIdx.x & 31;
+  for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < n;
+       p += (int64_t)gridDim.x * (blockDim.x >> 5)) {
     const int64_t s = run_start[p];
     const int i = idx[p], l = idx[s];
     bool same = true;
-    if (l != i)
-      for (int k = 0; k < KD && same; ++k) same = X[(int64_t)i * KD + k] == X[(int64_t)l * KD + k];
-    const int r = same ? l : i;
-    rep[i] = r;
-    flag[i] = r == i;
+    if (l != i) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        same &= X[(int64_t)i * KD + lane * 4 + e] == X[(int64_t)l * KD + lane * 4 + e];
+      same = __all_sync(0xffffffffu, same);
+    }
+    if (lane == 0) {
+      const int r = same ? l : i;
+      rep[i] = r;
+      flag[i] = r == i;
+    }
   }
 }
 
@@ -777,14 +786,16 @@ int dedupe(const T* X, int64_t n, Side& s, const TcWs& w, cudaStream_t st) {
   row_hash<T><<<grid_for(n, 8), 256, 0, st>>>(X, n, s.keys, s.iota);
   PS_LAUNCHED("row_hash");
   size_t tb = w.cub_bytes;
-  cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, s.keys, s.keys_sorted, s.iota, s.vals_sorted, (int)n, 0, 64, st);
+  // 32 hash bits suffice: a collision only splits a group (each row is compared
+  // with its run head), it never merges distinct rows
+  cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, s.keys, s.keys_sorted, s.iota, s.vals_sorted, (int)n, 0, 32, st);
   PS_LAUNCHED("cub_sort(hash)");
   run_heads<<<grid_for(n, 256), 256, 0, st>>>(s.keys_sorted, n, s.flag);
   PS_LAUNCHED("run_heads");
   tb = w.cub_bytes;
   cub::DeviceScan::InclusiveScan(w.cub_tmp, tb, s.flag, s.uniq, cub::Max(), (int)n, st);  // run start per position
   PS_LAUNCHED("cub_scan(run_start)");
-  mark_reps<T><<<grid_for(n, 256), 256, 0, st>>>(X, n, s.uniq, s.vals_sorted, s.rep, s.flag);
+  mark_reps<T><<<grid_for(n, 8), 256, 0, st>>>(X, n, s.uniq, s.vals_sorted, s.rep, s.flag);
   PS_LAUNCHED("mark_reps");
   iota32<<<grid_for(n, 256), 256, 0, st>>>(s.iota, n);
   PS_LAUNCHED("iota32");
