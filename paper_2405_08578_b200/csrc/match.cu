@@ -220,6 +220,45 @@ __global__ void pad_unused(unsigned long long* __restrict__ kp, unsigned long lo
     }
 }
 
+// One-CTA bitonic sort of up to kSmallSort (delta bits, pair key) entries by
+// (delta, ref1, ref2), in place.  Pair keys are unique, so stability is moot.
+constexpr int kSmallSort = 8192;
+__global__ void __launch_bounds__(1024) sort_small(unsigned long long* __restrict__ kd,
+                                                   unsigned long long* __restrict__ kp,
+                                                   const unsigned long long* __restrict__ counter, int n_max, int n2) {
+  extern __shared__ unsigned long long ssort[];
+  unsigned long long* sd = ssort;
+  unsigned long long* sp = ssort + n2;
+  const int n = (int)min((unsigned long long)n_max, *counter);
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    sd[i] = i < n ? kd[i] : ~0ull;
+    sp[i] = i < n ? kp[i] : ~0ull;
+  }
+  __syncthreads();
+  for (int k = 2; k <= n2; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const bool gt = sd[i] > sd[l] || (sd[i] == sd[l] && sp[i] > sp[l]);
+          if (gt == up) {
+            const unsigned long long td = sd[i], tp = sp[i];
+            sd[i] = sd[l];
+            sp[i] = sp[l];
+            sd[l] = td;
+            sp[l] = tp;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    kd[i] = sd[i];
+    kp[i] = sp[i];
+  }
+}
+
 __global__ void unpack_pairs(const unsigned long long* __restrict__ keys_delta,
                              const unsigned long long* __restrict__ vals_pair, const unsigned long long* __restrict__ counter,
                              int64_t cap, int32_t* __restrict__ ref1, int32_t* __restrict__ ref2,
@@ -388,6 +427,22 @@ extern "C" int ps_match(const void* desc1, int64_t n1, const void* desc2, int64_
     const cudaError_t e = cudaStreamSynchronize(st);
     PS_REQUIRE(e == cudaSuccess, PS_ERR_CUDA, "match count: %s", cudaGetErrorString(e));
     n = (int)std::max<unsigned long long>(1ull, std::min<unsigned long long>(c, (unsigned long long)n));
+  }
+  if (n <= kSmallSort) {
+    int n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    const int smem = 2 * n2 * (int)sizeof(unsigned long long);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSmallSort * 8);
+      attr = true;
+    }
+    sort_small<<<1, 1024, smem, st>>>(w.kd, w.kp, w.counter, n, n2);
+    PS_LAUNCHED("sort_small");
+    unpack_pairs<<<grid_blocks(n, 256), 256, 0, st>>>(w.kd, w.kp, w.counter, cap, out_ref1, out_ref2, out_delta,
+                                                      out_count);
+    PS_LAUNCHED("unpack_pairs");
+    return PS_OK;
   }
   pad_unused<<<grid_blocks(n, 256), 256, 0, st>>>(w.kp, w.kd, w.counter, n);
   PS_LAUNCHED("pad_unused");
