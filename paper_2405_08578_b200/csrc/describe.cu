@@ -33,6 +33,8 @@ struct DescParams {
   double theta[36], cos_t[36], sin_t[36];  // theta0_k and cos/sin(-theta0_k)
   double cb36[37], sb36[37];                // cos/sin of the 36-bin edges m*2pi/36
   double c8[9], s8[9];                      // cos/sin of m*pi/4 (8-bin edges relative to theta0)
+  int n_w8, w8_scale[kMaxDescScales];       // scales whose region side is 8 (fast path, d = 4)
+  int default_w8;                           // the default scale is one of them
 };
 
 // numpy mod(x, 2*pi) for -4*pi < x < 2*pi (descriptor.py:138, 215): fmod is
@@ -133,14 +135,16 @@ constexpr int kStageW = 8;  // region side served from shared memory
 constexpr int kStageDoubles = Stage<kStageW>::kTotal;
 
 // Fast-path (w = 8) layout, chosen for conflict-free shared-memory phases:
-// P rows at a stride of 24 doubles (axis reads of a half-warp hit 16
-// distinct 8-byte banks), gradient fields at an odd stride of 13.
+// one 16 x 16 box of P (rows at a stride of 24 doubles: axis reads of a
+// half-warp hit 16 distinct 8-byte banks) that holds both the axis region and
+// every rotated patch, then the gradient fields at an odd stride of 13.
 struct FastStage {
-  static constexpr int kSpan = Stage<8>::kSpan;  // 12
+  static constexpr int kSpan = Stage<8>::kSpan;  // 12: rotated field side
+  static constexpr int kBox = 16;                // staged P box side
   static constexpr int SPP = 24, SPF = 13;
-  static constexpr int kP = (kSpan + 2) * SPP;   // 336
+  static constexpr int kP = kBox * SPP;          // 384
   static constexpr int kF = kSpan * SPF;         // 156
-  static constexpr int kTotal = kP + 2 * kF;     // 648 doubles
+  static constexpr int kTotal = kP + 2 * kF;     // 696 doubles
 };
 
 // ---- float32 screening of the discrete decisions -------------------------------
@@ -483,22 +487,6 @@ __device__ __forceinline__ float fast_atan2f(float y, float x) {
   return y < 0.0f ? -r : r;
 }
 
-__device__ __forceinline__ float warp_max_f(float v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-// Fixed-point scale 2^e for one histogram pass: every bin sum of nsamp
-// magnitudes <= mx stays below 2^31 (one native 32-bit atomic per sample);
-// the quantum is then ~2^-31 * nsamp * mx, i.e. ~1e-8 of the descriptor norm.
-__device__ __forceinline__ float fx_scale32(float mx, int nsamp) {
-  if (!(mx > 0.0f)) return 1.0f;
-  int e;
-  frexpf(mx * (float)nsamp * 1.0001f, &e);  // mx * nsamp < 2^e
-  return ldexpf(1.0f, 31 - e);
-}
-
 // Returns false (nothing written) when the 36-bin argmax has no clear lead;
 // the caller then queues the keypoint for the float64 kernel.
 // Fast-path histograms: exact fixed point, two 26-bit limbs per bin (two
@@ -507,12 +495,6 @@ __device__ __forceinline__ float fx_scale32(float mx, int nsamp) {
 // below 2^52: quantum ~2^-46 of the largest bin -- far below float32
 // resolution, so near-identical regions keep distinct descriptors (F6).
 constexpr int kLimb = 26;
-__device__ __forceinline__ double fx_scale52(double mx, int nsamp) {
-  if (!(mx > 0.0)) return 1.0;
-  int e;
-  frexp(mx * (double)nsamp * 1.0000001, &e);  // mx * nsamp < 2^e
-  return ldexp(1.0, 52 - e);
-}
 __device__ __forceinline__ void h2_add(unsigned* h, int nb, int bin, double mag, double fx) {
   if (!(mag > 0.0)) return;
   const unsigned long long q = __double2ull_rn(__dmul_rn(mag, fx));
@@ -522,10 +504,15 @@ __device__ __forceinline__ void h2_add(unsigned* h, int nb, int bin, double mag,
 __device__ __forceinline__ unsigned long long h2_get(const unsigned* h, int nb, int bin) {
   return ((unsigned long long)h[nb + bin] << kLimb) + (unsigned long long)h[bin];
 }
-__device__ __forceinline__ double warp_max_d(double v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+// Warp-uniform fixed-point scale from the lanes' largest magnitudes: the max
+// of the (non-negative) doubles' high words (one REDUX) bounds the exponent eb,
+// every magnitude is < 2^(eb - 1022) and a bin sum of NS = 64 of them is
+// < 2^(eb - 1016), so 2^(1068 - eb) keeps every sum below 2^52.
+__device__ __forceinline__ double fx_scale52_warp(double mx) {
+  const unsigned eb = __reduce_max_sync(0xffffffffu, (unsigned)__double2hiint(mx)) >> 20;
+  if (eb == 0u) return 1.0;  // all magnitudes zero (or subnormal)
+  const int be = min(2091 - (int)eb, 2046);
+  return __hiloint2double(be << 20, 0);
 }
 
 template <int W>
@@ -533,21 +520,31 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
                                                        unsigned* hbase, double* stage, float* __restrict__ o32,
                                                        double* __restrict__ o64) {
   static_assert(W == kStageW, "fast path is staged");
+  static_assert(W * W == 64, "fx_scale52_warp assumes 64 samples");
   constexpr int NS = W * W, SPL = NS / 32, D = 128, SP = FastStage::SPP, SF = FastStage::SPF;
   constexpr int WS = W / 4;
   const int lane = threadIdx.x & 31;
   const int nr = im.nr, nc = im.nc;
+  constexpr int BX = FastStage::kBox;
   const int r0 = min(max(row - W / 2, 1), nr - 1 - W);
   const int c0 = min(max(col - W / 2, 1), nc - 1 - W);
+  constexpr double half = (double)(W - 1) / 2.0;
+  const double cy = fmin(fmax((double)row, 1.0 + half), __dsub_rn((double)nr - 2.0, half));
+  const double cx = fmin(fmax((double)col, 1.0 + half), __dsub_rn((double)nc - 2.0, half));
+  // One staged box for both phases: the axis region spans rows r0-1..r0+W and
+  // any rotated patch pr0-1..pr1+1 lies within cy -/+ (3.5 sqrt(2) + 2), so
+  // rows floor(cy)-7 .. floor(cy)+8 (clamped to the image) hold both.
+  const int BR = max(0, min((int)cy - 7, nr - BX)), BC = max(0, min((int)cx - 7, nc - BX));
   unsigned* h128 = hbase;         // [2][128]
   unsigned* h36 = hbase + 2 * D;  // [2][36]
   for (int q = lane; q < 2 * (D + 36); q += 32) hbase[q] = 0u;
   const int sx_ = lane & 15, sy_ = lane >> 4;
-  stage_box_u8<(W + 3) / 2>(im, stage, SP, r0 - 1, c0 - 1, W + 2, W + 2, sx_, sy_);
+  stage_box_u8<BX / 2>(im, stage, SP, BR, BC, BX, BX, sx_, sy_);
   __syncwarp();
+  const double* pa = stage + (r0 - 1 - BR) * SP + (c0 - 1 - BC);  // axis region origin
   auto axis_ab = [&](int iv, int iu, double& a, double& b) {
-    a = __dsub_rn(stage[(iv + 2) * SP + iu + 1], stage[iv * SP + iu + 1]);
-    b = __dsub_rn(stage[(iv + 1) * SP + iu + 2], stage[(iv + 1) * SP + iu]);
+    a = __dsub_rn(pa[(iv + 2) * SP + iu + 1], pa[iv * SP + iu + 1]);
+    b = __dsub_rn(pa[(iv + 1) * SP + iu + 2], pa[(iv + 1) * SP + iu]);
   };
   auto bin64 = [&](double a, double b, double shift, double k, int nbins) {
     const double ori = mod_two_pi(__dsub_rn(atan2(b, a), shift), prm.two_pi);
@@ -593,7 +590,7 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
     double mx = mg[0];
 #pragma unroll
     for (int j = 1; j < SPL; ++j) mx = fmax(mx, mg[j]);
-    const double f36 = fx_scale52(warp_max_d(mx), NS);
+    const double f36 = fx_scale52_warp(mx);
 #pragma unroll
     for (int j = 0; j < SPL; ++j) h2_add(h36, 36, bn[j], mg[j], f36);
     __syncwarp();
@@ -612,9 +609,6 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
     const double theta0 = prm.theta[hk], ct = prm.cos_t[hk], st = prm.sin_t[hk];
     const float theta0f = (float)theta0;
     // --- rotated grid (descriptor.py:164-216, 237-240)
-    constexpr double half = (double)(W - 1) / 2.0;
-    const double cy = fmin(fmax((double)row, 1.0 + half), __dsub_rn((double)nr - 2.0, half));
-    const double cx = fmin(fmax((double)col, 1.0 + half), __dsub_rn((double)nc - 2.0, half));
     const double xmin = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, ct >= 0.0 ? -half : half)), __dmul_rn(st, st >= 0.0 ? half : -half));
     const double xmax = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, ct >= 0.0 ? half : -half)), __dmul_rn(st, st >= 0.0 ? -half : half));
     const double ymin = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, st >= 0.0 ? -half : half)), __dmul_rn(ct, ct >= 0.0 ? -half : half));
@@ -624,15 +618,21 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
     const int xcap = max(pc1 - pc0 - 1, 0), ycap = max(pr1 - pr0 - 1, 0);
     const double xhi = (double)(nc - 2), yhi = (double)(nr - 2);
     const int FR = pr1 - pr0 + 1, FC = pc1 - pc0 + 1;
+    if (pr0 - 1 < BR || pr1 + 1 >= BR + BX || pc0 - 1 < BC || pc1 + 1 >= BC + BX) {  // cannot happen; be safe
+      __syncwarp();
+      return false;
+    }
+    if (pr0 - 1 < BR || pr1 + 1 >= BR + BX || pc0 - 1 < BC || pc1 + 1 >= BC + BX) {  // cannot happen; be safe
+      __syncwarp();
+      return false;
+    }
     double* fa = stage + FastStage::kP;
     double* fb = fa + FastStage::kF;
-    __syncwarp();
-    stage_box_u8<(FastStage::kSpan + 3) / 2>(im, stage, SP, pr0 - 1, pc0 - 1, FR + 2, FC + 2, sx_, sy_);
-    __syncwarp();
+    const double* pb = stage + (pr0 - 1 - BR) * SP + (pc0 - 1 - BC);  // rotated patch box origin
     for (int y = sy_; y < FR; y += 2)
       if (sx_ < FC) {
-        fa[y * SF + sx_] = __dsub_rn(stage[(y + 2) * SP + sx_ + 1], stage[y * SP + sx_ + 1]);
-        fb[y * SF + sx_] = __dsub_rn(stage[(y + 1) * SP + sx_ + 2], stage[(y + 1) * SP + sx_]);
+        fa[y * SF + sx_] = __dsub_rn(pb[(y + 2) * SP + sx_ + 1], pb[y * SP + sx_ + 1]);
+        fb[y * SF + sx_] = __dsub_rn(pb[(y + 1) * SP + sx_ + 2], pb[(y + 1) * SP + sx_]);
       }
     __syncwarp();
     const double c0t = ct, s0t = -st;  // cos / sin of theta0
@@ -676,7 +676,7 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
   double mx = mg[0];
 #pragma unroll
   for (int j = 1; j < SPL; ++j) mx = fmax(mx, mg[j]);
-  const double fx = fx_scale52(warp_max_d(mx), NS);
+  const double fx = fx_scale52_warp(mx);
 #pragma unroll
   for (int j = 0; j < SPL; ++j) h2_add(h128, D, bn[j], mg[j], fx);
   __syncwarp();
@@ -794,9 +794,6 @@ __global__ void __launch_bounds__(kFastWarps * 32, 4) describe_fast_u8(RampU8 im
   unsigned* hw = reinterpret_cast<unsigned*>(dsm + kFastWarps * FastStage::kTotal) + wid * kFastHist;
   const int64_t total = (int64_t)B * cap;
   const bool small = total < (1ll << 31);
-  int w_def = -1;
-  for (int s = 0; s < prm.n_scales; ++s)
-    if (prm.scale[s] == default_scale) w_def = prm.w[s];
   for (int64_t g = (int64_t)blockIdx.x * kFastWarps + wid; g < total; g += (int64_t)gridDim.x * kFastWarps) {
     const int b = small ? (int)((unsigned)g / (unsigned)cap) : (int)(g / cap);
     const int64_t i = g - (int64_t)b * cap;
@@ -804,19 +801,19 @@ __global__ void __launch_bounds__(kFastWarps * 32, 4) describe_fast_u8(RampU8 im
     RampU8 im = img;
     im.p = img.p + (int64_t)b * img_stride;
     const int row = kp_row[g], col = kp_col[g];
-    int w = w_def;
+    if (row < 0 || row >= im.nr || col < 0 || col >= im.nc) continue;  // validated by the caller
+    bool fast = prm.default_w8 && im.nr >= FastStage::kBox && im.nc >= FastStage::kBox;
     if (kp_scale) {
       const int scale = kp_scale[g];
-      w = -1;
-      for (int s = 0; s < prm.n_scales; ++s)
-        if (prm.scale[s] == scale) w = prm.w[s];
+      fast = false;
+      for (int k = 0; k < prm.n_w8; ++k) fast |= prm.w8_scale[k] == scale;
+      fast &= im.nr >= FastStage::kBox && im.nc >= FastStage::kBox;
     }
-    if (w < 0 || row < 0 || row >= im.nr || col < 0 || col >= im.nc) continue;  // validated by the caller
     bool ok = false;
-    if (prm.d == 4 && w == 8)
+    if (fast)
       ok = describe_keypoint_w8u8<8>(im, row, col, prm, hw, stage, out32 ? out32 + g * 128 : nullptr,
                                      out64 ? out64 + g * 128 : nullptr);
-    if (!ok && lane == 0) work[atomicAdd(n_work, 1ull)] = g;
+    if (!ok && lane == 0) work[atomicAdd(n_work, 1ull)] = g;  // other sides and near-ties: general kernel
   }
 }
 
@@ -904,6 +901,11 @@ extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, in
     prm.lb[si] = lb;
     prm.fx[si] = std::ldexp(1.0, (int)std::floor(3.0 * lb - std::log2(nsamp * 2.9 * pmax)));
   }
+  for (int si = 0; si < n_scale_set; ++si)
+    if (d == 4 && prm.w[si] == 8) {
+      prm.w8_scale[prm.n_w8++] = prm.scale[si];
+      if (prm.scale[si] == default_scale) prm.default_w8 = 1;
+    }
   const double two_pi = 2.0 * M_PI;  // descriptor.py:31
   prm.d = d;
   prm.D = d * d * 8;
