@@ -99,15 +99,16 @@ __device__ __forceinline__ void stage_box_u8(const RampU8& im, double* stage, in
   if (sx >= PC) return;
   const int pitch = (int)im.pitch;
   const uint8_t* p = im.p + (r0 + sy) * pitch + (c0 + sx);
-  const unsigned k0 = (unsigned)((r0 + sy) * im.nc + c0 + sx + 1);
-  const unsigned kstep = 2u * (unsigned)im.nc;
   unsigned v[MAXR];
 #pragma unroll
   for (int i = 0; i < MAXR; ++i) v[i] = (sy + 2 * i < PR) ? (unsigned)__ldg(p + 2 * i * pitch) : 0u;
+  double k = u32_to_f64((unsigned)((r0 + sy) * im.nc + c0 + sx + 1));  // ramp index, exact in float64
+  const double kstep = u32_to_f64(2u * (unsigned)im.nc);
 #pragma unroll
-  for (int i = 0; i < MAXR; ++i)
-    if (sy + 2 * i < PR)
-      stage[(sy + 2 * i) * SP + sx] = __dadd_rn(u32_to_f64(v[i]), __dmul_rn(u32_to_f64(k0 + i * kstep), im.alpha));
+  for (int i = 0; i < MAXR; ++i) {
+    if (sy + 2 * i < PR) stage[(sy + 2 * i) * SP + sx] = __dadd_rn(u32_to_f64(v[i]), __dmul_rn(k, im.alpha));
+    k = __dadd_rn(k, kstep);
+  }
 }
 
 template <class Img>
@@ -537,7 +538,8 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
   const int BR = max(0, min((int)cy - 7, nr - BX)), BC = max(0, min((int)cx - 7, nc - BX));
   unsigned* h128 = hbase;         // [2][128]
   unsigned* h36 = hbase + 2 * D;  // [2][36]
-  for (int q = lane; q < 2 * (D + 36); q += 32) hbase[q] = 0u;
+  static_assert((2 * (D + 36)) % 4 == 0, "vector zeroing");
+  for (int q = lane; q < 2 * (D + 36) / 4; q += 32) reinterpret_cast<uint4*>(hbase)[q] = make_uint4(0u, 0u, 0u, 0u);
   const int sx_ = lane & 15, sy_ = lane >> 4;
   stage_box_u8<BX / 2>(im, stage, SP, BR, BC, BX, BX, sx_, sy_);
   __syncwarp();
@@ -793,10 +795,16 @@ __global__ void __launch_bounds__(kFastWarps * 32, 4) describe_fast_u8(RampU8 im
   double* stage = dsm + wid * FastStage::kTotal;
   unsigned* hw = reinterpret_cast<unsigned*>(dsm + kFastWarps * FastStage::kTotal) + wid * kFastHist;
   const int64_t total = (int64_t)B * cap;
-  const bool small = total < (1ll << 31);
-  for (int64_t g = (int64_t)blockIdx.x * kFastWarps + wid; g < total; g += (int64_t)gridDim.x * kFastWarps) {
-    const int b = small ? (int)((unsigned)g / (unsigned)cap) : (int)(g / cap);
-    const int64_t i = g - (int64_t)b * cap;
+  const int64_t S = (int64_t)gridDim.x * kFastWarps;
+  // grid-stride over (image b, slot i); (b, i) advance without a division
+  int64_t g = (int64_t)blockIdx.x * kFastWarps + wid;
+  int b = (int)(g / cap);
+  int64_t i = g - (int64_t)b * cap;
+  for (; g < total; g += S, i += S) {
+    while (i >= cap) {
+      i -= cap;
+      ++b;
+    }
     if (counts && i >= counts[b]) continue;
     RampU8 im = img;
     im.p = img.p + (int64_t)b * img_stride;
