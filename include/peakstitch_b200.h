@@ -183,6 +183,35 @@ PS_API int ps_ransac_rigid(const double* src_xy, const double* dst_xy, int64_t n
 PS_API int ps_estimate_rigid(const double* src_xy, const double* dst_xy, int64_t n,
                       double* out_model, int64_t* out_info, void* stream);
 
+/* ---- compositor --------------------------------------
+ * ps_warp_and_blend <- warp_and_blend(images, placements, canvas, blend,
+ *                      resample)                         compositor.py:84-160
+ * One placed image.  The caller supplies the INVERSE transform's cos / sin /
+ * translation exactly as RigidTransform.inverse() + transform_points compute
+ * them (registration.py:49-55, 66-73; host libm) and the canvas block the
+ * reference derives from the snapped corners (compositor.py:122-129). */
+typedef struct ps_placement {
+  const void* data;   /* device pointer, pixel (0,0)                          */
+  int32_t pixel_type; /* PS_PIXELS_U8 (uint8) or PS_PIXELS_F64 (float64)      */
+  int32_t nr, nc;
+  int32_t r_lo, r_hi, c_lo, c_hi; /* canvas block [r_lo,r_hi) x [c_lo,c_hi)  */
+  int32_t pad_;
+  int64_t row_pitch;  /* elements                                            */
+  double cos_t, sin_t, t_x, t_y;  /* inverse transform: canvas frame -> image */
+} ps_placement;
+
+enum ps_blend { PS_BLEND_FEATHER = 0, PS_BLEND_OVERWRITE = 1 };
+enum ps_resample { PS_RESAMPLE_BILINEAR = 0, PS_RESAMPLE_NEAREST = 1 };
+
+/* Composite n placements (host array, in placement order) into a
+ * height x width float64 canvas whose pixel (r, c) is frame point
+ * (c + dx, r + dy).  out and weightmap are device arrays of height*width
+ * doubles (row-major); weightmap receives the raw accumulated weights
+ * (Canvas.weightmap).  Unknown blend / resample -> PS_ERR_VALUE. */
+PS_API int ps_warp_and_blend(const ps_placement* host_placements, int32_t n, int32_t height,
+                             int32_t width, int32_t dx, int32_t dy, int32_t blend,
+                             int32_t resample, double* out, double* weightmap, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -424,3 +424,95 @@ def pair_points(ref1, ref2, kp1, kp2):
     src = np.stack([kp1["col"][ref1], kp1["row"][ref1]], axis=1).astype(np.float64)
     dst = np.stack([kp2["col"][ref2], kp2["row"][ref2]], axis=1).astype(np.float64)
     return src, dst
+
+
+# ---------------------------------------------------------------------------
+# compositor.py:20-160 -- canvas bounds, inverse-mapped resampling, blending
+# (SURVEY.md §8(f) #2).  Transforms are (theta, t_x, t_y) triples with the
+# RigidTransform semantics of registration.py:33-73.
+# ---------------------------------------------------------------------------
+
+SNAP = 1e-6  # compositor.py:20
+
+
+def apply_rigid(theta: float, tx: float, ty: float, x, y):
+    """RigidTransform.transform_points (registration.py:66-73): numpy order
+    (c*x - s*y) + t_x, (s*x + c*y) + t_y with host-libm cos / sin."""
+    theta = norm_theta(theta)
+    c, s = math.cos(theta), math.sin(theta)
+    return c * x - s * y + tx, s * x + c * y + ty
+
+
+def invert_rigid(theta: float, tx: float, ty: float):
+    """RigidTransform.inverse (registration.py:49-55)."""
+    theta = norm_theta(theta)
+    c, s = math.cos(theta), math.sin(theta)
+    return norm_theta(-theta), -(c * tx + s * ty), -(-s * tx + c * ty)
+
+
+def snapped_corners(transform, nr: int, nc: int):
+    """Transformed image corners snapped to 1e-6 (compositor.py:40-41, 51, 122-123)."""
+    x = np.array([0.0, nc, 0.0, nc])
+    y = np.array([0.0, 0.0, nr, nr])
+    cx, cy = apply_rigid(*transform, x, y)
+    return np.round(cx / SNAP) * SNAP, np.round(cy / SNAP) * SNAP
+
+
+def canvas_bounds(transforms, dims):
+    """compute_canvas (compositor.py:44-58) -> (width, height, dx, dy)."""
+    if not transforms:
+        raise ValueError("need at least one placement")
+    xs, ys = zip(*(snapped_corners(t, *d) for t, d in zip(transforms, dims)))
+    xs, ys = np.concatenate(xs), np.concatenate(ys)
+    dx, dy = math.floor(xs.min()), math.floor(ys.min())
+    return math.ceil(xs.max()) - dx, math.ceil(ys.max()) - dy, dx, dy
+
+
+def composite(images, transforms, bounds, blend: str = "feather", resample: str = "bilinear"):
+    """warp_and_blend (compositor.py:84-160) -> (pixels, weightmap)."""
+    if blend not in ("feather", "overwrite"):
+        raise ValueError(f"unknown blend mode {blend!r}")
+    if resample not in ("bilinear", "nearest"):
+        raise ValueError(f"unknown resample mode {resample!r}")
+    width, height, dx, dy = bounds
+    acc = np.zeros((height, width))
+    wsum = np.zeros((height, width))
+    cnt = np.zeros((height, width), dtype=np.int64)
+    solo = np.zeros((height, width))
+    for img, t in zip(images, transforms):
+        nr, nc = img.shape
+        cx, cy = snapped_corners(t, nr, nc)
+        r0, r1 = max(math.floor(cy.min()) - dy, 0), min(math.ceil(cy.max()) - dy, height)
+        c0, c1 = max(math.floor(cx.min()) - dx, 0), min(math.ceil(cx.max()) - dx, width)
+        if r0 >= r1 or c0 >= c1:
+            continue
+        Y, X = np.meshgrid(np.arange(r0, r1, dtype=np.float64) + dy, np.arange(c0, c1, dtype=np.float64) + dx,
+                           indexing="ij")
+        sx, sy = apply_rigid(*invert_rigid(*t), X, Y)
+        ok = (sx >= 0) & (sx <= nc - 1) & (sy >= 0) & (sy <= nr - 1)
+        xs, ys = np.clip(sx, 0, nc - 1), np.clip(sy, 0, nr - 1)
+        if resample == "bilinear":  # _sample_bilinear (compositor.py:61-74)
+            ix = np.clip(np.floor(xs).astype(np.int64), 0, max(nc - 2, 0))
+            iy = np.clip(np.floor(ys).astype(np.int64), 0, max(nr - 2, 0))
+            fx, fy = xs - ix, ys - iy
+            jx, jy = np.minimum(ix + 1, nc - 1), np.minimum(iy + 1, nr - 1)
+            v = (img[iy, ix] * (1.0 - fy) * (1.0 - fx) + img[iy, jx] * (1.0 - fy) * fx
+                 + img[jy, ix] * fy * (1.0 - fx) + img[jy, jx] * fy * fx)
+        else:  # _sample_nearest (compositor.py:77-81)
+            v = img[np.clip(np.rint(ys).astype(np.int64), 0, nr - 1), np.clip(np.rint(xs).astype(np.int64), 0, nc - 1)]
+            v = v.astype(np.float64)
+        blk = (slice(r0, r1), slice(c0, c1))
+        if blend == "overwrite":
+            acc[blk][ok] = v[ok]
+            wsum[blk][ok] = 1.0
+            cnt[blk][ok] = 1
+        else:
+            w = 1.0 + np.minimum(np.minimum(sx, nc - 1 - sx), np.minimum(sy, nr - 1 - sy))
+            acc[blk] += np.where(ok, w * v, 0.0)
+            wsum[blk] += np.where(ok, w, 0.0)
+            cnt[blk] += ok
+        solo[blk][ok] = v[ok]
+    out = np.zeros((height, width))
+    np.divide(acc, wsum, out=out, where=wsum > 0)
+    out[cnt == 1] = solo[cnt == 1]
+    return out, wsum

@@ -32,6 +32,16 @@ class KeypointsC(C.Structure):
                 ("count", C.c_void_p), ("cap", C.c_int64)]
 
 
+class PlacementC(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("pixel_type", C.c_int32), ("nr", C.c_int32), ("nc", C.c_int32),
+                ("r_lo", C.c_int32), ("r_hi", C.c_int32), ("c_lo", C.c_int32), ("c_hi", C.c_int32),
+                ("pad_", C.c_int32), ("row_pitch", C.c_int64), ("cos_t", C.c_double), ("sin_t", C.c_double),
+                ("t_x", C.c_double), ("t_y", C.c_double)]
+
+
+PS_BLEND_FEATHER, PS_BLEND_OVERWRITE = 0, 1
+PS_RESAMPLE_BILINEAR, PS_RESAMPLE_NEAREST = 0, 1
+
 # exported symbol -> (restype, argtypes); mirrors include/peakstitch_b200.h
 SIGNATURES = {
     "ps_abi_version": (C.c_int, []),
@@ -61,6 +71,8 @@ SIGNATURES = {
                                   C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "ps_estimate_rigid": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                     C.c_void_p]),
+    "ps_warp_and_blend": (C.c_int, [C.POINTER(PlacementC), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                    C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
 }
 
 _lib = None

@@ -14,6 +14,7 @@ test / bench time on the GPU box reads /root/reference.
 from __future__ import annotations
 
 import json
+import math
 import os
 import sys
 import time
@@ -318,6 +319,56 @@ def make_e2e():
     print("e2e matches", len(pairs), "inliers", len(res.inliers))
 
 
+def compositor_cases():
+    """(label, [(image, theta, tx, ty)], blend, resample) -- seeded."""
+    rng = np.random.default_rng(2405)
+    cases = []
+    f = lambda h, w: rng.uniform(0, 255, size=(h, w))  # noqa: E731
+    u = lambda h, w: rng.integers(0, 256, size=(h, w)).astype(np.uint8)  # noqa: E731
+    cases.append(("identity_bilinear", [(f(40, 60), 0.0, 0.0, 0.0)], "feather", "bilinear"))
+    cases.append(("identity_nearest", [(f(33, 29), 0.0, 0.0, 0.0)], "feather", "nearest"))
+    cases.append(("offset_pair", [(f(30, 50), 0.0, 0.0, 0.0), (f(30, 50), 0.0, 20.0, 0.0)], "feather", "bilinear"))
+    cases.append(("negative_offset", [(f(40, 40), 0.0, 0.0, 0.0), (f(40, 40), 0.0, -13.0, -7.0)], "feather",
+                  "bilinear"))
+    cases.append(("rotated_trio_u8", [(u(48, 64), 0.0, 0.0, 0.0), (u(48, 64), math.radians(3.0), 30.25, -4.75),
+                                      (u(40, 56), math.radians(-7.0), -11.5, 17.125)], "feather", "bilinear"))
+    cases.append(("rotated_trio_nearest", [(f(48, 64), 0.0, 0.0, 0.0), (f(48, 64), math.radians(5.0), 20.5, 3.5),
+                                           (f(40, 56), math.radians(-2.0), -9.0, 12.0)], "feather", "nearest"))
+    cases.append(("overwrite_rot", [(f(36, 52), 0.0, 0.0, 0.0), (f(36, 52), math.radians(11.0), 14.0, -6.0)],
+                  "overwrite", "bilinear"))
+    cases.append(("overwrite_nearest_u8", [(u(36, 52), 0.3, 5.0, 5.0), (u(30, 44), -0.2, 20.0, -3.0)],
+                  "overwrite", "nearest"))
+    cases.append(("half_turn", [(f(25, 31), 0.0, 0.0, 0.0), (f(25, 31), math.pi, 40.0, 30.0)], "feather",
+                  "bilinear"))
+    src = scenes.scene(120, 200, 4).astype(np.float64)
+    cases.append(("crop_restitch", [(src[:, :120], 0.0, 0.0, 0.0), (src[:, 60:], 0.0, 60.0, 0.0)], "feather",
+                  "bilinear"))
+    cases.append(("quarter_turn", [(f(50, 50), 0.0, 0.0, 0.0), (f(50, 50), math.pi / 2, 50.0, 0.0)], "feather",
+                  "bilinear"))
+    return cases
+
+
+def make_compositor():
+    from peakstitch import compositor as R_comp
+
+    out, meta = {}, []
+    for label, items, blend, resample in compositor_cases():
+        ids = [f"i{k}" for k in range(len(items))]
+        placements = [R_comp.Placement(i, R_reg.RigidTransform(th, tx, ty)) for i, (_, th, tx, ty) in zip(ids, items)]
+        dims = {i: it[0].shape for i, it in zip(ids, items)}
+        canvas = R_comp.compute_canvas(placements, dims)
+        pix = R_comp.warp_and_blend({i: it[0] for i, it in zip(ids, items)}, placements, canvas, blend=blend,
+                                    resample=resample)
+        for k, it in enumerate(items):
+            out[f"{label}__img{k}"] = it[0]
+        out[f"{label}__pixels"] = pix
+        out[f"{label}__weightmap"] = canvas.weightmap
+        meta.append(dict(label=label, blend=blend, resample=resample,
+                         transforms=[[float(th), float(tx), float(ty)] for (_, th, tx, ty) in items],
+                         canvas=[canvas.width, canvas.height, *canvas.origin_offset]))
+    save("compositor.npz", meta=json.dumps(meta), **out)
+
+
 def make_scene_digests():
     d = {}
     for (h, w, seed) in [(64, 96, 0), (256, 256, 1), (512, 512, 7), (1600, 2688, 0), (2048, 2048, 0)]:
@@ -328,10 +379,11 @@ def make_scene_digests():
 
 if __name__ == "__main__":
     t = time.time()
-    what = sys.argv[1:] or ["detector", "descriptor", "matcher", "ransac", "e2e", "digests"]
+    what = sys.argv[1:] or ["detector", "descriptor", "matcher", "ransac", "e2e", "compositor", "digests"]
     for w in what:
         {"detector": make_detector, "descriptor": make_descriptor, "matcher": make_matcher,
-         "ransac": make_ransac, "e2e": make_e2e, "digests": make_scene_digests}[w]()
+         "ransac": make_ransac, "e2e": make_e2e, "compositor": make_compositor,
+         "digests": make_scene_digests}[w]()
     env = dict(numpy=np.__version__, python=sys.version.split()[0])
     with open(os.path.join(HERE, "ENV.json"), "w") as f:
         json.dump(env, f)

@@ -101,3 +101,18 @@ def test_match_plan_and_config_errors():
     cnt = C.c_int64()
     assert L.ps_match(None, 1, None, 1, 128, 0, 0.0, 0, None, None, None, C.byref(cnt), 1, None, 0, None) == \
         _lib.PS_ERR_CONFIG
+
+
+def test_placement_struct_layout_matches_header():
+    """ps_placement (include/peakstitch_b200.h): natural C alignment, 80 bytes."""
+    P = _lib.PlacementC
+    assert C.sizeof(P) == 80
+    offs = {name: getattr(P, name).offset for name, _ in P._fields_}
+    assert offs["row_pitch"] == 40 and offs["cos_t"] == 48 and offs["t_y"] == 72
+
+
+def test_warp_and_blend_rejects_unknown_modes_before_any_launch():
+    L = _lib.lib()
+    arr = (_lib.PlacementC * 1)()
+    assert L.ps_warp_and_blend(arr, 0, 4, 4, 0, 0, 7, 0, None, None, None) == _lib.PS_ERR_VALUE
+    assert L.ps_warp_and_blend(arr, 0, 4, 4, 0, 0, 0, 9, None, None, None) == _lib.PS_ERR_VALUE

@@ -477,3 +477,71 @@ def test_end_to_end_c1_against_oracle_chain():
     out = device.ransac(src, dst, 1000, 3.0, 8, 0)
     assert out.ok
     assert corner_error((out.theta, out.t_x, out.t_y), ref_r["model"]) <= 1e-3
+
+
+# ---------------------------------------------------------------------------
+# §8(f) #2: compositor on the device, bit-exact against the reference
+# ---------------------------------------------------------------------------
+
+def test_compositor_matches_reference_fixtures(golden):
+    from paper_2405_08578_b200 import compositor as K
+
+    g = golden("compositor.npz")
+    n = 0
+    for m in json.loads(str(g["meta"])):
+        ids = [f"i{k}" for k in range(len(m["transforms"]))]
+        imgs = {i: g[f"{m['label']}__img{k}"] for k, i in enumerate(ids)}
+        pl = [K.Placement(i, R.RigidTransform(*t)) for i, t in zip(ids, m["transforms"])]
+        canvas = K.compute_canvas(pl, {i: a.shape for i, a in imgs.items()})
+        out = K.warp_and_blend(imgs, pl, canvas, blend=m["blend"], resample=m["resample"])
+        assert np.array_equal(out, g[f"{m['label']}__pixels"]), m["label"]
+        assert np.array_equal(canvas.weightmap, g[f"{m['label']}__weightmap"]), m["label"]
+        n += 1
+    assert n >= 10
+
+
+def test_compositor_reference_properties():
+    """The reference's compositor tests (test_compositor.py) on the device path."""
+    from paper_2405_08578_b200 import compositor as K
+
+    I = R.RigidTransform.identity()
+    rng = np.random.default_rng(0)
+    px = rng.uniform(0, 255, size=(40, 60))
+    c = K.compute_canvas([K.Placement("a", I)], {"a": px.shape})
+    assert np.array_equal(K.warp_and_blend({"a": px}, [K.Placement("a", I)], c), px)  # identity bit-exact
+    c = K.compute_canvas([K.Placement("a", I)], {"a": px.shape})
+    assert np.array_equal(K.warp_and_blend({"a": px}, [K.Placement("a", I)], c, resample="nearest"), px)
+    pl = [K.Placement("a", I), K.Placement("b", R.RigidTransform(0.0, 80.0, 0.0))]
+    flat = np.full((40, 40), 200.0)
+    c = K.compute_canvas(pl, {"a": (40, 40), "b": (40, 40)})
+    out = K.warp_and_blend({"a": flat, "b": flat}, pl, c)
+    assert (c.height, c.width) == (40, 120)
+    assert np.all(out[:, 41:79] == 0.0) and np.all(c.weightmap[:, 41:79] == 0.0)
+    assert np.all(c.weightmap[:, :40] > 0.0)
+    a, b = np.full((20, 20), 10.0), np.full((20, 20), 250.0)
+    pl = [K.Placement("a", I), K.Placement("b", I)]
+    c = K.compute_canvas(pl, {"a": a.shape, "b": b.shape})
+    assert np.all(K.warp_and_blend({"a": a, "b": b}, pl, c, blend="overwrite") == 250.0)
+    with pytest.raises(ValueError):
+        K.warp_and_blend({"a": a}, [K.Placement("a", I)], c, blend="average")
+    with pytest.raises(ValueError):
+        K.warp_and_blend({"a": a}, [K.Placement("a", I)], c, resample="cubic")
+
+
+def test_compositor_many_placements_carry_state_between_launches():
+    """More placements than one kernel-parameter batch (64): the per-pixel
+    state crosses launches; result still equals the oracle bit for bit."""
+    from paper_2405_08578_b200 import compositor as K
+
+    rng = np.random.default_rng(3)
+    imgs, tr = [], []
+    for k in range(70):
+        imgs.append(rng.uniform(0, 255, size=(12, 16)))
+        tr.append((float(rng.uniform(-0.3, 0.3)), float(rng.uniform(0, 40)), float(rng.uniform(0, 30))))
+    ids = [f"i{k}" for k in range(70)]
+    pl = [K.Placement(i, R.RigidTransform(*t)) for i, t in zip(ids, tr)]
+    canvas = K.compute_canvas(pl, {i: a.shape for i, a in zip(ids, imgs)})
+    out = K.warp_and_blend(dict(zip(ids, imgs)), pl, canvas)
+    bounds = O.canvas_bounds(tr, [a.shape for a in imgs])
+    want, wm = O.composite(imgs, tr, bounds)
+    assert np.array_equal(out, want) and np.array_equal(canvas.weightmap, wm)

@@ -82,3 +82,40 @@ def test_apply_linear_ramp_validation_and_lazy_view():
         R.apply_linear_ramp(img, 0.0)
     with pytest.raises(ConfigError):
         R.apply_linear_ramp(img, 1.0)
+
+
+# ---- compositor canvas sizing (host side of §8(f) #2) -------------------------
+
+def test_compute_canvas_matches_reference_cases():
+    """The reference's own canvas cases (test_compositor.py) plus the golden
+    fixtures' canvases."""
+    from paper_2405_08578_b200.compositor import Placement, compute_canvas
+
+    I = R.RigidTransform.identity()
+    c = compute_canvas([Placement("a", I)], {"a": (100, 100)})
+    assert (c.height, c.width, c.origin_offset) == (100, 100, (0, 0))
+    c = compute_canvas([Placement("a", I), Placement("b", R.RigidTransform(0.0, 50.0, 0.0))],
+                       {"a": (100, 100), "b": (100, 100)})
+    assert (c.height, c.width, c.origin_offset) == (100, 150, (0, 0))
+    c = compute_canvas([Placement("a", I), Placement("b", R.RigidTransform(0.0, -30.0, -20.0))],
+                       {"a": (100, 100), "b": (100, 100)})
+    assert (c.height, c.width, c.origin_offset) == (120, 130, (-30, -20))
+    h = 50.0
+    quarter = R.RigidTransform(math.pi / 2, h - (math.cos(math.pi / 2) * h - math.sin(math.pi / 2) * h),
+                               h - (math.sin(math.pi / 2) * h + math.cos(math.pi / 2) * h))
+    c = compute_canvas([Placement("a", I), Placement("b", quarter)], {"a": (100, 100), "b": (100, 100)})
+    assert (c.height, c.width) == (100, 100)
+    with pytest.raises(ValueError):
+        compute_canvas([], {})
+
+
+def test_compute_canvas_matches_golden(golden):
+    from paper_2405_08578_b200.compositor import Placement, compute_canvas
+
+    g = golden("compositor.npz")
+    for m in json.loads(str(g["meta"])):
+        ids = [f"i{k}" for k in range(len(m["transforms"]))]
+        pl = [Placement(i, R.RigidTransform(*t)) for i, t in zip(ids, m["transforms"])]
+        dims = {i: g[f"{m['label']}__img{k}"].shape for k, i in enumerate(ids)}
+        c = compute_canvas(pl, dims)
+        assert [c.width, c.height, *c.origin_offset] == m["canvas"], m["label"]

@@ -128,3 +128,32 @@ def test_scene_digests_pinned():
         hw, seed = key.split("_seed")
         h, w = map(int, hw.split("x"))
         assert scenes.scene_digest(scenes.scene(h, w, int(seed))) == want[key], key
+
+
+def compositor_cases(golden):
+    g = golden("compositor.npz")
+    for m in json.loads(str(g["meta"])):
+        imgs = [g[f"{m['label']}__img{k}"] for k in range(len(m["transforms"]))]
+        yield g, m, imgs
+
+
+def test_oracle_compositor_matches_reference(golden):
+    """compute_canvas + warp_and_blend restatement: canvas, pixels and
+    weightmap bit-identical to the reference's (compositor.py:44-160)."""
+    n = 0
+    for g, m, imgs in compositor_cases(golden):
+        tr = [tuple(t) for t in m["transforms"]]
+        bounds = O.canvas_bounds(tr, [im.shape for im in imgs])
+        assert list(bounds) == m["canvas"], m["label"]
+        pix, wm = O.composite(imgs, tr, bounds, m["blend"], m["resample"])
+        assert np.array_equal(pix, g[f"{m['label']}__pixels"]), m["label"]
+        assert np.array_equal(wm, g[f"{m['label']}__weightmap"]), m["label"]
+        n += 1
+    assert n >= 10
+
+
+def test_oracle_compositor_rejects_unknown_modes():
+    with pytest.raises(ValueError):
+        O.composite([np.zeros((4, 4))], [(0.0, 0.0, 0.0)], (4, 4, 0, 0), blend="average")
+    with pytest.raises(ValueError):
+        O.composite([np.zeros((4, 4))], [(0.0, 0.0, 0.0)], (4, 4, 0, 0), resample="cubic")
