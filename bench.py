@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -57,6 +58,7 @@ def parse():
     ap.add_argument("--no-match", action="store_true", help="skip the C4 matching measurement")
     ap.add_argument("--no-stitch", action="store_true", help="skip the C3 nine-image stitch measurement")
     ap.add_argument("--no-pairs", action="store_true", help="skip the C5 pairs/s measurement")
+    ap.add_argument("--no-composite", action="store_true", help="skip the C3 composite measurement")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run N steps untimed and exit")
     return ap.parse_args()
 
@@ -244,6 +246,79 @@ def bench_c3_stitch(args, world, rank, dev, steps=3):
             "timing": "host wall clock around the whole call, CUDA-synchronized, max over ranks",
             "parallelism": f"images then pairs sharded over {world} rank(s); NCCL all-gather of keypoint/descriptor "
                            "slots and of the pair results"}
+
+
+# ---------------------------------------------------------------------------
+# C3 composite: the nine crops warped into one canvas
+# ---------------------------------------------------------------------------
+
+def c3_placements():
+    """The nine C3 crops placed rigidly by their generator truth (rotation
+    about the crop centre onto the source frame; the +-5 % scale is ignored)."""
+    from paper_2405_08578_b200 import compositor as K, scenes
+    from paper_2405_08578_b200.records import RigidTransform
+
+    images, truth = scenes.config3_images(0)
+    ids, pl = [], []
+    for k, (img, (r0, c0, th, _)) in enumerate(zip(images, truth)):
+        h, w = img.shape
+        hx, hy = (w - 1) / 2.0, (h - 1) / 2.0
+        c, s = math.cos(th), math.sin(th)
+        tx = c0 + hx - (c * hx - s * hy)
+        ty = r0 + hy - (s * hx + c * hy)
+        ids.append(f"img{k}")
+        pl.append(K.Placement(f"img{k}", RigidTransform(th, tx, ty)))
+    return dict(zip(ids, images)), pl
+
+
+def bench_c3_composite(args, rank, dev, with_cpu, steps=5):
+    """Feather + bilinear composite of the nine C3 crops on one GPU (rank 0;
+    the canvas is one output, no data-path collective)."""
+    import torch
+
+    from paper_2405_08578_b200 import compositor as K
+
+    if rank != 0:
+        return None
+    images, pl = c3_placements()
+    canvas = K.compute_canvas(pl, {k: v.shape for k, v in images.items()})
+    dimg = {k: torch.from_numpy(v).to(dev) for k, v in images.items()}
+    for _ in range(2):
+        K.warp_and_blend_device(dimg, pl, canvas)
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        K.warp_and_blend_device(dimg, pl, canvas)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    npx = canvas.width * canvas.height
+    nbytes = 16 * npx + sum(v.size for v in images.values())  # pixels + weightmap out, every source read once
+    peak, _ = measured_peaks()
+    out = {"metric": "canvas Mpixel/s (C3 composite: 9 x 2688x1600 u8 crops, feather, bilinear, float64 canvas)",
+           "value": round(npx / 1e6 / (ms / 1e3), 1), "unit": "Mpixel/s", "ms": round(ms, 4),
+           "canvas_hw": [canvas.height, canvas.width], "placements": len(pl),
+           "roofline": {"bound": "hbm", "achieved": round(nbytes / (ms / 1e3) / 1e9, 1), "peak": peak,
+                        "unit": "GB/s", "frac": round(nbytes / (ms / 1e3) / 1e9 / peak, 4),
+                        "algorithmic_bytes": nbytes},
+           "exactness": "bit-identical to the reference warp_and_blend (tests/test_gpu_parity.py)",
+           "timing": "CUDA events, inputs resident"}
+    if with_cpu:
+        from oracle import lpsift_oracle as O
+
+        row = [k for k in images][:3]  # one grid row of crops: bounded CPU sample
+        tr = [(p.transform.theta, p.transform.t_x, p.transform.t_y) for p in pl if p.image_id in row]
+        imgs = [images[k] for k in row]
+        bounds = O.canvas_bounds(tr, [a.shape for a in imgs])
+        t0 = time.perf_counter()
+        O.composite(imgs, tr, bounds)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": round(bounds[0] * bounds[1] / 1e6 / dt, 2), "unit": "Mpixel/s", "cores": 1,
+                               "kind": "port", "sample": f"oracle composite of 3 of the 9 crops "
+                               f"({bounds[1]}x{bounds[0]} canvas), numpy, one process"}
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -504,6 +579,10 @@ def run_ours(args):
     if not args.no_stitch:
         stitch = bench_c3_stitch(args, world, rank, dev)
 
+    composite = None
+    if not args.no_composite:
+        composite = bench_c3_composite(args, rank, dev, with_cpu=(not args.no_cpu and world == 1))
+
     pairs5 = None
     if not args.no_pairs:
         pairs5 = bench_c5_pairs(args, world, rank, dev)
@@ -524,7 +603,7 @@ def run_ours(args):
                        "keypoints_per_image": K, "descriptor": "float32 128-d", "l2": "inputs larger than L2",
                        "parallelism": f"images sharded over {world} rank(s)"},
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "matching_c4": matching,
-            "stitch_c3": stitch, "pairs_c5": pairs5,
+            "stitch_c3": stitch, "composite_c3": composite, "pairs_c5": pairs5,
             "gpu_launches": int(launches), "clocks": clocks,
         }
         print(json.dumps(out), flush=True)
