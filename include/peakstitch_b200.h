@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 1
+#define PS_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define PS_API __attribute__((visibility("default")))
@@ -65,8 +65,14 @@ enum ps_pixel_type {
                         apply_linear_ramp (imaging.py:130-149) is fused:
                         P[r,c] = fl(I[r,c] + fl((r*nc+c+1) * alpha))        */
   PS_PIXELS_F64 = 1, /* an already-ramped float64 raster (RampedImage.pixels) */
-  PS_PIXELS_F64_RAW = 2 /* float64 intensities (IntensityImage.pixels); ramp
+  PS_PIXELS_F64_RAW = 2, /* float64 intensities (IntensityImage.pixels); ramp
                            fused as for PS_PIXELS_U8                          */
+  PS_PIXELS_RGB8 = 3  /* interleaved 8-bit RGB (load_image of an RGB file,
+                         imaging.py:71-93): the grey of a pixel is
+                         gray_lut[R<<16 | G<<8 | B] -- the run host's own
+                         to_grayscale bits (imaging.py:66-68) --
+                         and the ramp is fused as for PS_PIXELS_U8.
+                         row_pitch / image_stride count pixels (3 bytes).   */
 };
 
 enum ps_match_strategy {
@@ -82,7 +88,8 @@ typedef struct ps_image_batch {
   int32_t nr, nc;       /* rows, columns                                     */
   int64_t row_pitch;    /* elements between consecutive rows  (>= nc)        */
   int64_t image_stride; /* elements between consecutive images              */
-  double alpha;         /* ramp coefficient (PS_PIXELS_U8 only)              */
+  double alpha;         /* ramp coefficient (fused-ramp pixel types)         */
+  const double* gray_lut; /* PS_PIXELS_RGB8: device table of 2^24 greys      */
 } ps_image_batch;
 
 /* Keypoints of a batch, image b occupying slots [b*cap, b*cap + count[b]).

@@ -16,14 +16,15 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpeakstit
 
 PS_OK, PS_ERR_CONFIG, PS_ERR_VALUE, PS_ERR_DEGENERATE, PS_ERR_REGISTRATION = 0, 1, 2, 3, 4
 PS_ERR_CUDA, PS_ERR_ARGUMENT, PS_ERR_CAPACITY = 5, 6, 7
-PS_PIXELS_U8, PS_PIXELS_F64, PS_PIXELS_F64_RAW = 0, 1, 2
+PS_PIXELS_U8, PS_PIXELS_F64, PS_PIXELS_F64_RAW, PS_PIXELS_RGB8 = 0, 1, 2, 3
+ABI_VERSION = 2
 PS_MATCH_NEAREST, PS_MATCH_THRESHOLD_ALL = 0, 1
 
 
 class ImageBatch(C.Structure):
     _fields_ = [("data", C.c_void_p), ("pixel_type", C.c_int32), ("batch", C.c_int32),
                 ("nr", C.c_int32), ("nc", C.c_int32), ("row_pitch", C.c_int64),
-                ("image_stride", C.c_int64), ("alpha", C.c_double)]
+                ("image_stride", C.c_int64), ("alpha", C.c_double), ("gray_lut", C.c_void_p)]
 
 
 class KeypointsC(C.Structure):
@@ -92,7 +93,7 @@ def lib():
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
-        if handle.ps_abi_version() != 1:
+        if handle.ps_abi_version() != ABI_VERSION:
             raise ImportError("libpeakstitch_b200 ABI version mismatch")
         _lib = handle
     return _lib

@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
     const int64_t i = g - (int64_t)b * cap;
     if (counts && i >= counts[b]) continue;
     Img im = img;
-    im.p = img.p + (int64_t)b * img_stride;
+    im.p = img.p + (int64_t)b * img_stride * decltype(img)::kElem;
     const int row = kp_row[g], col = kp_col[g];
     int w = w_def, lb = lb_def;
     double fx = fx_def;
@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, 4) describe_fast_u8(RampU8 im
     }
     if (counts && i >= counts[b]) continue;
     RampU8 im = img;
-    im.p = img.p + (int64_t)b * img_stride;
+    im.p = img.p + (int64_t)b * img_stride * decltype(img)::kElem;
     const int row = kp_row[g], col = kp_col[g];
     if (row < 0 || row >= im.nr || col < 0 || col >= im.nc) continue;  // validated by the caller
     bool fast = prm.default_w8 && im.nr >= FastStage::kBox && im.nc >= FastStage::kBox;
@@ -876,7 +876,7 @@ extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, in
   cudaStream_t s = (cudaStream_t)stream;
   // bound on |P| for the fixed-point histogram scale
   double pmax = 255.0 + 0.05 * 255.0;
-  if (img->pixel_type != PS_PIXELS_U8) {
+  if (img->pixel_type != PS_PIXELS_U8 && img->pixel_type != PS_PIXELS_RGB8) {  // greys of RGB8 are <= 255 too
     unsigned long long* dmax = nullptr;
     cudaMallocAsync(&dmax, sizeof(unsigned long long), s);
     cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), s);
@@ -977,6 +977,13 @@ extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, in
     PS_LAUNCHED("describe_kernel(queued)");
     cudaFreeAsync(work, s);
     return check_cuda("cudaFreeAsync");
+  } else if (img->pixel_type == PS_PIXELS_RGB8) {
+    PS_REQUIRE(img->gray_lut != nullptr, PS_ERR_ARGUMENT, "RGB8 pixels need gray_lut");
+    RampRGB8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha, img->gray_lut};
+    cudaFuncSetAttribute(describe_kernel<RampRGB8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
+    describe_kernel<<<(unsigned)blocks, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,
+                                                                  kp->scale, default_scale, kp->count, kp->cap, prm,
+                                                                  out_desc32, out_desc64, nullptr, nullptr);
   } else if (img->pixel_type == PS_PIXELS_F64_RAW) {
     RampF64Raw im{(const double*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
     describe_kernel<<<(unsigned)blocks, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,

@@ -59,7 +59,8 @@ __device__ __forceinline__ bool better_min(double v, int32_t k, double bv, int32
 }
 
 // ---- generic kernel: one warp per window -----------------------------------
-// MODE 0: u8 integer key (valid ramp); MODE 1: float64 compare on P[r,c].
+// MODE 0: integer key (u8 value or RGB luma, valid ramp); MODE 1: float64
+// compare on P[r,c].
 template <int MODE, class Img>
 __global__ void __launch_bounds__(256) window_extrema_warp(
     Img img, int64_t img_stride, int B, int L, int wc, int nwin, int32_t* __restrict__ tmax,
@@ -72,18 +73,17 @@ __global__ void __launch_bounds__(256) window_extrema_warp(
     const int b = (int)(g / nwin);
     const int w = (int)(g % nwin);
     Img im = img;
-    im.p = img.p + (int64_t)b * img_stride;
+    im.p = img.p + (int64_t)b * img_stride * decltype(img)::kElem;
     const int r0 = (w / wc) * L, c0 = (w % wc) * L;
     const int h = min(L, nr - r0), wd = min(L, nc - c0);
     int32_t kmax, kmin;
-    if (MODE == 0) {
+    if constexpr (MODE == 0) {
       uint64_t best_hi = 0, best_lo = ~0ull;
       for (int r = 0; r < h; ++r) {
         const int64_t rowbase = (int64_t)(r0 + r) * nc;
         for (int c = lane; c < wd; c += 32) {
-          const uint8_t* pp = reinterpret_cast<const uint8_t*>(im.p);
-          uint64_t v = pp[(int64_t)(r0 + r) * im.pitch + c0 + c];
-          uint64_t key = (v << 32) | (uint64_t)(rowbase + c0 + c);
+          const uint64_t v = im.key(r0 + r, c0 + c);
+          const uint64_t key = (v << 32) | (uint64_t)(rowbase + c0 + c);
           best_hi = key > best_hi ? key : best_hi;
           best_lo = key < best_lo ? key : best_lo;
         }
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(256) detect_u8_w8(RampU8 img, int64_t img_stri
   const int wr = rem / pairs_per_row, q = rem % pairs_per_row;
   const int nr = img.nr, nc = img.nc;
   RampU8 im = img;
-  im.p = img.p + (int64_t)b * img_stride;
+  im.p = img.p + (int64_t)b * img_stride * decltype(img)::kElem;
   const int r0 = wr * 8, cbase = q * 16;
   const int w0 = wr * wc_n + 2 * q;
   const bool second = (2 * q + 1) < wc_n;
@@ -294,7 +294,7 @@ __global__ void scatter_kept(ScalePlan sp, Tables tb, Img img, int64_t img_strid
     const int w = (int)(loc >> 1), pol = (int)(loc & 1);
     const int32_t k = pol ? tb.tmin[si][(int64_t)b * sp.nwin[si] + w] : tb.tmax[si][(int64_t)b * sp.nwin[si] + w];
     Img im = img;
-    im.p = img.p + (int64_t)b * img_stride;
+    im.p = img.p + (int64_t)b * img_stride * decltype(img)::kElem;
     const int r = k / img.nc, c = k % img.nc;
     const int64_t s = (int64_t)b * out.cap + (pos[g] - base);
     out.row[s] = r;
@@ -345,8 +345,11 @@ ScalePlan make_plan(int nr, int nc, const int32_t* s, int n, int dedupe) {
   return sp;
 }
 
-bool key_rule_valid(int nr, int nc, double alpha) {
-  return alpha >= 9.094947017729282e-13 /* 2^-40 */ && alpha * (double)nr * (double)nc <= 0.5;
+// The ramp must separate equal keys (alpha >= 2^-40, far above the grey's
+// rounding noise) and stay below half the smallest grey step: 1 for u8,
+// 0.001 (integer luma / 1000) for RGB8.
+bool key_rule_valid(int nr, int nc, double alpha, double step = 1.0) {
+  return alpha >= 9.094947017729282e-13 /* 2^-40 */ && alpha * (double)nr * (double)nc <= 0.5 * step;
 }
 
 size_t scan_temp_bytes(int64_t n) {
@@ -382,6 +385,15 @@ int launch_key(const Img&, const ps_image_batch*, int, int, int, int, bool, cons
   return PS_ERR_ARGUMENT;
 }
 
+// RGB8 with a valid ramp: integer luma key, generic warp-per-window kernel.
+int launch_key(const RampRGB8& img, const ps_image_batch* ib, int B, int L, int wc, int nwin, bool,
+               const KpOut& ko, int32_t* tmax, int32_t* tmin, cudaStream_t st) {
+  window_extrema_warp<0><<<grid_for((int64_t)B * nwin, 8), 256, 0, st>>>(img, ib->image_stride, B, L, wc, nwin,
+                                                                           tmax, tmin, ko, L);
+  PS_LAUNCHED("window_extrema_warp<rgb key>");
+  return PS_OK;
+}
+
 // u8 pixels with a valid ramp: integer-key kernels (L == 8 vectorised path).
 int launch_key(const RampU8& img, const ps_image_batch* ib, int B, int L, int wc, int nwin, bool aligned,
                const KpOut& ko, int32_t* tmax, int32_t* tmin, cudaStream_t st) {
@@ -404,7 +416,8 @@ int run_detect(const ps_image_batch* ib, Img img, bool u8, const int32_t* s, int
                void* ws, size_t ws_bytes, cudaStream_t st) {
   const int B = ib->batch, nr = ib->nr, nc = ib->nc;
   ScalePlan sp = make_plan(nr, nc, s, n, dedupe);
-  const bool keymode = u8 && key_rule_valid(nr, nc, ib->alpha);
+  const bool rgb = ib->pixel_type == PS_PIXELS_RGB8;
+  const bool keymode = (u8 || rgb) && key_rule_valid(nr, nc, ib->alpha, rgb ? 0.001 : 1.0);
   const bool direct = sp.n == 1;  // one evaluated scale: no cross-scale dedupe needed
   PS_REQUIRE(out->cap >= sp.raw_off[sp.n], PS_ERR_CAPACITY, "keypoint capacity %lld < %lld",
              (long long)out->cap, (long long)sp.raw_off[sp.n]);
@@ -497,6 +510,15 @@ extern "C" int ps_detect(const ps_image_batch* img, const int32_t* host_scales, 
     PS_REQUIRE(img->alpha > 0 && img->alpha * img->nr * img->nc <= 0.05 * 255.0, PS_ERR_CONFIG,
                "alpha=%g outside the ramp limits (imaging.py:138-145)", img->alpha);
     RampF64Raw im{(const double*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
+    return run_detect(img, im, false, host_scales, n_scales, dedupe, out, workspace, workspace_bytes, s);
+  }
+  if (img->pixel_type == PS_PIXELS_RGB8) {
+    PS_REQUIRE(img->alpha > 0 && img->alpha * img->nr * img->nc <= 0.05 * 255.0, PS_ERR_CONFIG,
+               "alpha=%g outside the ramp limits (imaging.py:138-145)", img->alpha);
+    PS_REQUIRE(img->gray_lut != nullptr, PS_ERR_ARGUMENT, "RGB8 pixels need gray_lut");
+    PS_REQUIRE((int64_t)img->nr * img->row_pitch * 3 < (int64_t)INT32_MAX, PS_ERR_ARGUMENT,
+               "image too large (3*nr*pitch >= 2^31)");
+    RampRGB8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha, img->gray_lut};
     return run_detect(img, im, false, host_scales, n_scales, dedupe, out, workspace, workspace_bytes, s);
   }
   PS_REQUIRE(img->pixel_type == PS_PIXELS_F64, PS_ERR_ARGUMENT, "unknown pixel type %d", img->pixel_type);

@@ -70,6 +70,7 @@ __device__ __forceinline__ double u32_to_f64(unsigned x) {
 
 // (callers guarantee nr * nc < 2^31 and nr * pitch < 2^31: 32-bit offsets)
 struct RampU8 {
+  static constexpr int kElem = 1;  // elements of *p per pixel
   const uint8_t* p;
   int64_t pitch;
   int32_t nr, nc;
@@ -78,9 +79,35 @@ struct RampU8 {
     const double k = u32_to_f64((unsigned)(r * nc + c + 1));
     return __dadd_rn(u32_to_f64(p[r * (int)pitch + c]), __dmul_rn(k, alpha));
   }
+  __device__ __forceinline__ unsigned key(int r, int c) const { return p[r * (int)pitch + c]; }
+};
+
+// Interleaved RGB8: the grey is the host's own BT.601 bits from
+// a 2^24-entry table; key() is the exact integer luma 299R + 587G + 114B,
+// whose order equals the grey order (distinct greys differ by >= 0.001).
+struct RampRGB8 {
+  static constexpr int kElem = 3;
+  const uint8_t* p;
+  int64_t pitch;  // pixels
+  int32_t nr, nc;
+  double alpha;
+  const double* lut;
+  __device__ __forceinline__ unsigned rgb(int r, int c) const {
+    const uint8_t* q = p + 3 * (r * (int)pitch + c);
+    return ((unsigned)q[0] << 16) | ((unsigned)q[1] << 8) | (unsigned)q[2];
+  }
+  __device__ __forceinline__ unsigned key(int r, int c) const {
+    const uint8_t* q = p + 3 * (r * (int)pitch + c);
+    return 299u * q[0] + 587u * q[1] + 114u * q[2];
+  }
+  __device__ __forceinline__ double at(int r, int c) const {
+    const double k = u32_to_f64((unsigned)(r * nc + c + 1));
+    return __dadd_rn(__ldg(lut + rgb(r, c)), __dmul_rn(k, alpha));
+  }
 };
 
 struct RampF64 {
+  static constexpr int kElem = 1;
   const double* p;
   int64_t pitch;
   int32_t nr, nc;
@@ -99,6 +126,7 @@ __host__ __device__ __forceinline__ double dadd(double a, double b) {
 }
 
 struct RampF64Raw {
+  static constexpr int kElem = 1;
   const double* p;
   int64_t pitch;
   int32_t nr, nc;

@@ -46,12 +46,15 @@ class DeviceImages:
 
     kind "u8"     : raw 8-bit intensities, ramp fused with ``alpha``;
     kind "f64raw" : float64 intensities, ramp fused with ``alpha``;
-    kind "f64"    : already-ramped float64 raster (alpha informational).
+    kind "f64"    : already-ramped float64 raster (alpha informational);
+    kind "rgb8"   : interleaved 8-bit RGB [B, nr, nc, 3]; grey from the run
+                    host's BT.601 table (``ingest.gray_lut``), ramp fused.
     """
 
-    data: torch.Tensor  # [B, nr, nc]
+    data: torch.Tensor  # [B, nr, nc] (rgb8: [B, nr, nc, 3])
     kind: str
     alpha: float
+    lut: torch.Tensor | None = None
 
     @property
     def batch(self) -> int:
@@ -67,18 +70,40 @@ class DeviceImages:
 
     def c_struct(self) -> _lib.ImageBatch:
         d = self.data
+        if self.kind == "rgb8":
+            if d.dim() != 4 or d.shape[3] != 3 or d.stride(3) != 1 or d.stride(2) != 3 or d.stride(1) % 3 \
+                    or d.stride(0) % 3:
+                raise ValueError("RGB images must be [B, nr, nc, 3] with interleaved channels")
+            return _lib.ImageBatch(d.data_ptr(), _lib.PS_PIXELS_RGB8, d.shape[0], d.shape[1], d.shape[2],
+                                   d.stride(1) // 3, (d.stride(0) if d.shape[0] > 1 else d.stride(1) * d.shape[1]) // 3,
+                                   float(self.alpha), self.lut.data_ptr())
         if d.dim() != 3 or d.stride(2) != 1:
             raise ValueError("images must be [B, nr, nc] with unit column stride")
         ptype = {"u8": _lib.PS_PIXELS_U8, "f64": _lib.PS_PIXELS_F64, "f64raw": _lib.PS_PIXELS_F64_RAW}[self.kind]
         return _lib.ImageBatch(d.data_ptr(), ptype, d.shape[0], d.shape[1], d.shape[2], d.stride(1),
-                               d.stride(0) if d.shape[0] > 1 else d.stride(1) * d.shape[1], float(self.alpha))
+                               d.stride(0) if d.shape[0] > 1 else d.stride(1) * d.shape[1], float(self.alpha), None)
 
 
-def as_device_images(images, alpha=None, *, ramped=False, device=None) -> DeviceImages:
-    """Wrap a [B, nr, nc] / [nr, nc] uint8 or float64 tensor (uploads if on CPU)."""
+def as_device_images(images, alpha=None, *, ramped=False, rgb=False, device=None) -> DeviceImages:
+    """Wrap a [B, nr, nc] / [nr, nc] uint8 or float64 tensor (uploads if on
+    CPU); with ``rgb=True`` (or a 4-D tensor) a [B, nr, nc, 3] / [nr, nc, 3]
+    uint8 RGB batch whose grey is the reference's BT.601 (imaging.py:66-68)."""
     if isinstance(images, DeviceImages):
         return images
     t = images if isinstance(images, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(images))
+    if rgb or t.dim() == 4:
+        from .ingest import gray_lut
+
+        if t.dim() == 3:
+            t = t.unsqueeze(0)
+        if t.dim() != 4 or t.shape[3] != 3 or t.dtype != torch.uint8:
+            raise ValueError("RGB input must be uint8 [B, nr, nc, 3] or [nr, nc, 3]")
+        if not t.is_cuda:
+            t = t.to(device or "cuda", non_blocking=False)
+        t = t.contiguous()
+        if alpha is None:
+            alpha = default_alpha(t.shape[1], t.shape[2])
+        return DeviceImages(t, "rgb8", float(alpha), gray_lut(t.device))
     if t.dim() == 2:
         t = t.unsqueeze(0)
     if not t.is_cuda:

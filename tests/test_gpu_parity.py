@@ -545,3 +545,53 @@ def test_compositor_many_placements_carry_state_between_launches():
     bounds = O.canvas_bounds(tr, [a.shape for a in imgs])
     want, wm = O.composite(imgs, tr, bounds)
     assert np.array_equal(out, want) and np.array_equal(canvas.weightmap, wm)
+
+
+# ---------------------------------------------------------------------------
+# §8(f) #3: RGB ingest on the device (integer luma key, host grey table)
+# ---------------------------------------------------------------------------
+
+def test_rgb_ingest_grey_detect_describe_match_oracle():
+    """C5-size RGB image: device grey == reference to_grayscale bits;
+    keypoints (integer luma key) bit-exact against the oracle on that grey;
+    descriptors identical to the float64-grey path's and <= 1e-4 from the oracle."""
+    from paper_2405_08578_b200 import ingest
+
+    a, b, _ = scenes.config5_pair(1)
+    grey = scenes.gray_bt601(a)
+    ta = torch.from_numpy(a).cuda()
+    assert np.array_equal(ingest.to_grayscale_device(ta).cpu().numpy(), grey)
+    alpha = O.default_alpha(*grey.shape)
+    want = O.detect(O.ramp(grey, alpha), (16, 32, 64))
+    im_rgb = device.as_device_images(ta, alpha, rgb=True)
+    kp = device.detect(im_rgb, (16, 32, 64))
+    h = kp.image(0)
+    h["pol"] = h.pop("polarity")
+    assert_kp_equal(h, want, "rgb")
+    cfg = R.DescriptorConfig(0.0625, 4, 64, True)
+    d_rgb = device.describe(im_rgb, kp, cfg, out64=True, out32=False)
+    tg = torch.from_numpy(grey).cuda()
+    kp_g = device.detect(tg, (16, 32, 64), alpha=alpha)
+    assert torch.equal(kp_g.row, kp.row) and torch.equal(kp_g.value, kp.value)
+    d_g = device.describe(tg, kp_g, cfg, alpha=alpha, out64=True, out32=False)
+    assert torch.equal(d_rgb, d_g)  # same raster bits -> same descriptors
+    P = O.ramp(grey, alpha)
+    for k in range(0, len(want), 211):
+        ref = O.describe_one(P, int(want["row"][k]), int(want["col"][k]), int(want["scale"][k]), 0.0625, 4, 64)
+        got = d_rgb[0, k].cpu().numpy()
+        assert np.max(np.abs(got - ref)) <= P2_TOL * max(np.linalg.norm(ref), 1e-300)
+
+
+def test_rgb_batch_and_tiny_alpha_float_compare():
+    """RGB batches use per-image offsets of 3 bytes per pixel; an alpha below
+    the key rule falls back to the exact float64 compare on the table grey."""
+    rng = np.random.default_rng(21)
+    imgs = rng.integers(0, 256, size=(3, 96, 120, 3)).astype(np.uint8)
+    imgs[1, 10:40, 20:70] = (12, 200, 77)  # flat region: ties resolved by the ramp
+    for alpha in (O.default_alpha(96, 120), 1e-14):
+        kp = device.detect(torch.from_numpy(imgs).cuda(), (8, 16), alpha=alpha)
+        for i in range(3):
+            want = O.detect(O.ramp(scenes.gray_bt601(imgs[i]), alpha), (8, 16))
+            h = kp.image(i)
+            h["pol"] = h.pop("polarity")
+            assert_kp_equal(h, want, f"rgb{i}/{alpha}")

@@ -119,3 +119,20 @@ def test_compute_canvas_matches_golden(golden):
         dims = {i: g[f"{m['label']}__img{k}"].shape for k, i in enumerate(ids)}
         c = compute_canvas(pl, dims)
         assert [c.width, c.height, *c.origin_offset] == m["canvas"], m["label"]
+
+
+def test_gray_table_reproduces_reference_to_grayscale():
+    """The 2^24-entry grey table (ingest.host_gray_lut) gives the bits of the
+    reference's float64 `rgb @ LUMA` (imaging.py:66-68) for whole images of
+    awkward sizes (BLAS tails) -- the premise of the RGB8 ingest path."""
+    from paper_2405_08578_b200 import ingest, scenes
+
+    lut = ingest.host_gray_lut()
+    rng = np.random.default_rng(12)
+    for h, w in [(7, 13), (33, 29), (301, 517), (1080, 1920)]:
+        img = rng.integers(0, 256, size=(h, w, 3)).astype(np.uint8)
+        key = (img[..., 0].astype(np.int64) << 16) | (img[..., 1].astype(np.int64) << 8) | img[..., 2]
+        assert np.array_equal(lut[key], scenes.gray_bt601(img)), (h, w)
+    a, _, _ = scenes.config5_pair(0)
+    key = (a[..., 0].astype(np.int64) << 16) | (a[..., 1].astype(np.int64) << 8) | a[..., 2]
+    assert np.array_equal(lut[key], scenes.gray_bt601(a))
