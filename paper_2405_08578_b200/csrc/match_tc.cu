@@ -561,9 +561,11 @@ __global__ void exact_rows(const int32_t* __restrict__ rows, const int32_t* __re
 }
 
 // ---- duplicate rows --------------------------------------------------------------------
+// Open-addressing table of row hashes (tsize a power of two, keys 0 = empty):
+// per hash the lowest row index.  slot_of[i] receives row i's slot.
 template <class T>
-__global__ void row_hash(const T* __restrict__ X, int64_t n, unsigned long long* __restrict__ keys,
-                         int32_t* __restrict__ vals) {
+__global__ void hash_insert(const T* __restrict__ X, int64_t n, unsigned long long* __restrict__ tkey,
+                            int32_t* __restrict__ tidx, int64_t tsize, int32_t* __restrict__ slot_of) {
   const int lane = threadIdx.x & 31;
   for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
        i += (int64_t)gridDim.x * (blockDim.x >> 5)) {
@@ -574,7 +576,6 @@ __global__ void row_hash(const T* __restrict__ X, int64_t n, unsigned long long*
       unsigned long long bits;
       if (sizeof(T) == 8) bits = (unsigned long long)__double_as_longlong((double)v);
       else bits = (unsigned long long)__float_as_uint((float)v);
-      // splitmix64 of (bits, position)
       unsigned long long z = bits + 0x9E3779B97F4A7C15ull * (unsigned long long)(lane * 4 + e + 1);
       z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
       z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
@@ -583,39 +584,40 @@ __global__ void row_hash(const T* __restrict__ X, int64_t n, unsigned long long*
 #pragma unroll
     for (int o = 16; o; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
     if (lane == 0) {
-      keys[i] = h;
-      vals[i] = (int32_t)i;
+      const unsigned long long key = h | 1ull;
+      int64_t slot = (int64_t)((h >> 20) & (unsigned long long)(tsize - 1));
+      for (;;) {  // plain read first: duplicate rows find their slot without an atomic
+        unsigned long long prev = *(volatile unsigned long long*)(tkey + slot);
+        if (prev == 0ull) prev = atomicCAS(tkey + slot, 0ull, key);
+        if (prev == 0ull || prev == key) break;
+        slot = (slot + 1) & (tsize - 1);
+      }
+      if (*(volatile int32_t*)(tidx + slot) > (int32_t)i) atomicMin(tidx + slot, (int32_t)i);
+      slot_of[i] = (int32_t)slot;
     }
   }
 }
 
-// sorted (hash, index): rep = first index of the equal-hash run when the rows
-// are bitwise equal to it, else itself.  flag[i] = (rep == i).
-__global__ void run_heads(const unsigned long long* __restrict__ hs, int64_t n, int32_t* __restrict__ head) {
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
-    head[p] = (p == 0 || (uint32_t)hs[p - 1] != (uint32_t)hs[p]) ? (int32_t)p : 0;  // sort key: low 32 bits
-}
-
+// rep[i] = the lowest row with row i's hash when bitwise equal to row i, else
+// i itself (a hash collision only splits a group); flag[i] = (rep == i).
 template <class T>
-__global__ void mark_reps(const T* __restrict__ X, int64_t n, const int32_t* __restrict__ run_start,
-                          const int32_t* __restrict__ idx, int32_t* __restrict__ rep, int32_t* __restrict__ flag) {
-  // one warp per sorted position: lanes compare 4 elements each, coalesced
+__global__ void mark_reps_table(const T* __restrict__ X, int64_t n, const int32_t* __restrict__ tidx,
+                                const int32_t* __restrict__ slot_of, int32_t* __restrict__ rep,
+                                int32_t* __restrict__ flag) {
   const int lane = threadIdx.x & 31;
-  for (int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); p < n;
-       p += (int64_t)gridDim.x * (blockDim.x >> 5)) {
-    const int64_t s = run_start[p];
-    const int i = idx[p], l = idx[s];
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
+       i += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int l = tidx[slot_of[i]];
     bool same = true;
-    if (l != i) {
+    if (l != (int)i) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        same &= X[(int64_t)i * KD + lane * 4 + e] == X[(int64_t)l * KD + lane * 4 + e];
+      for (int e = 0; e < 4; ++e) same &= X[i * KD + lane * 4 + e] == X[(int64_t)l * KD + lane * 4 + e];
       same = __all_sync(0xffffffffu, same);
     }
     if (lane == 0) {
-      const int r = same ? l : i;
+      const int r = same ? l : (int)i;
       rep[i] = r;
-      flag[i] = r == i;
+      flag[i] = r == (int)i;
     }
   }
 }
@@ -665,8 +667,10 @@ __global__ void accept_pairs(const int32_t* __restrict__ a_rep, int64_t n1, cons
 
 // ---- host orchestration ------------------------------------------------------------
 struct Side {  // a descriptor matrix with its duplicate-row structure
-  int32_t *iota, *vals_sorted, *rep, *flag, *uniq, *n_uniq;
-  unsigned long long *keys, *keys_sorted;
+  int32_t *iota, *slot_of, *rep, *flag, *uniq, *n_uniq;
+  unsigned long long* tkey;  // hash table of rows
+  int32_t* tidx;
+  int64_t tsize;
 };
 
 struct TcWs {
@@ -716,14 +720,11 @@ dim3 tc_grid(int64_t rows, int64_t cols) {
   return dim3(rb, best);
 }
 
-size_t cub_need(int64_t n) {
-  size_t a = 0, b = 0, c = 0;
-  cub::DeviceScan::InclusiveScan(nullptr, c, (const int32_t*)nullptr, (int32_t*)nullptr, cub::Max(), (int)n);
-  cub::DeviceRadixSort::SortPairs(nullptr, a, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
-                                  (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+size_t cub_need(int64_t n) {  // the order-preserving selections
+  size_t b = 0;
   cub::DeviceSelect::Flagged(nullptr, b, (const int32_t*)nullptr, (const int32_t*)nullptr, (int32_t*)nullptr,
                              (int32_t*)nullptr, (int)n);
-  return std::max(std::max(a, b), c);
+  return b;
 }
 
 TcWs carve_tc(void* base, int64_t n1, int64_t n2, size_t* used) {
@@ -731,13 +732,15 @@ TcWs carve_tc(void* base, int64_t n1, int64_t n2, size_t* used) {
   TcWs w{};
   auto side = [&](Side& s, int64_t n) {
     s.iota = ar.take<int32_t>(n);
-    s.vals_sorted = ar.take<int32_t>(n);
+    s.slot_of = ar.take<int32_t>(n);
     s.rep = ar.take<int32_t>(n);
     s.flag = ar.take<int32_t>(n);
     s.uniq = ar.take<int32_t>(n);
     s.n_uniq = ar.take<int32_t>(1);
-    s.keys = ar.take<unsigned long long>(n);
-    s.keys_sorted = ar.take<unsigned long long>(n);
+    s.tsize = 64;
+    while (s.tsize < 2 * n) s.tsize <<= 1;
+    s.tkey = ar.take<unsigned long long>(s.tsize);
+    s.tidx = ar.take<int32_t>(s.tsize);
   };
   side(w.a, n1);
   side(w.b, n2);
@@ -781,25 +784,15 @@ int grid_for(int64_t work, int per) {
 
 template <class T>
 int dedupe(const T* X, int64_t n, Side& s, const TcWs& w, cudaStream_t st) {
+  cudaMemsetAsync(s.tkey, 0, s.tsize * sizeof(unsigned long long), st);
+  cudaMemsetAsync(s.tidx, 0x7f, s.tsize * sizeof(int32_t), st);
+  hash_insert<T><<<grid_for(n, 8), 256, 0, st>>>(X, n, s.tkey, s.tidx, s.tsize, s.slot_of);
+  PS_LAUNCHED("hash_insert");
+  mark_reps_table<T><<<grid_for(n, 8), 256, 0, st>>>(X, n, s.tidx, s.slot_of, s.rep, s.flag);
+  PS_LAUNCHED("mark_reps_table");
   iota32<<<grid_for(n, 256), 256, 0, st>>>(s.iota, n);
   PS_LAUNCHED("iota32");
-  row_hash<T><<<grid_for(n, 8), 256, 0, st>>>(X, n, s.keys, s.iota);
-  PS_LAUNCHED("row_hash");
   size_t tb = w.cub_bytes;
-  // 32 hash bits suffice: a collision only splits a group (each row is compared
-  // with its run head), it never merges distinct rows
-  cub::DeviceRadixSort::SortPairs(w.cub_tmp, tb, s.keys, s.keys_sorted, s.iota, s.vals_sorted, (int)n, 0, 32, st);
-  PS_LAUNCHED("cub_sort(hash)");
-  run_heads<<<grid_for(n, 256), 256, 0, st>>>(s.keys_sorted, n, s.flag);
-  PS_LAUNCHED("run_heads");
-  tb = w.cub_bytes;
-  cub::DeviceScan::InclusiveScan(w.cub_tmp, tb, s.flag, s.uniq, cub::Max(), (int)n, st);  // run start per position
-  PS_LAUNCHED("cub_scan(run_start)");
-  mark_reps<T><<<grid_for(n, 8), 256, 0, st>>>(X, n, s.uniq, s.vals_sorted, s.rep, s.flag);
-  PS_LAUNCHED("mark_reps");
-  iota32<<<grid_for(n, 256), 256, 0, st>>>(s.iota, n);
-  PS_LAUNCHED("iota32");
-  tb = w.cub_bytes;
   cub::DeviceSelect::Flagged(w.cub_tmp, tb, s.iota, s.flag, s.uniq, s.n_uniq, (int)n, st);
   PS_LAUNCHED("cub_select(reps)");
   return PS_OK;
