@@ -292,7 +292,7 @@ def pair_points(r1, r2, kp1_row, kp1_col, kp2_row, kp2_col, stream=None):
     src = torch.empty((n, 2), dtype=torch.float64, device=dev)
     dst = torch.empty((n, 2), dtype=torch.float64, device=dev)
     if n:
-        cnt = torch.tensor([n], dtype=torch.int64, device=dev)
+        cnt = torch.full((1,), n, dtype=torch.int64, device=dev)  # fill kernel: no host sync
         _lib.check(_lib.lib().ps_pair_points(_ptr(r1), _ptr(r2), _ptr(cnt), _ptr(kp1_row), _ptr(kp1_col),
                                              _ptr(kp2_row), _ptr(kp2_col), _ptr(src), _ptr(dst), n,
                                              C.c_void_p(_stream_ptr(stream))), "pair_points")
@@ -347,19 +347,20 @@ def ransac(src: torch.Tensor, dst: torch.Tensor, iterations=2000, inlier_tol=3.0
     wsb = C.c_size_t()
     _lib.check(L.ps_ransac_plan(n, iterations, C.byref(wsb)), "ransac")
     ws = _workspace(wsb.value, dev)
-    model = torch.empty(3, dtype=torch.float64, device=dev)
-    mask = torch.empty(n, dtype=torch.uint8, device=dev)
-    info = torch.empty(4, dtype=torch.int64, device=dev)
-    rms = torch.empty(1, dtype=torch.float64, device=dev)
+    # one result block: model[3] | rms | info[4] (int64 bits) | mask[n] -- a single device-to-host read
+    out = torch.empty(8 + (n + 7) // 8, dtype=torch.float64, device=dev)
+    ob = out.view(torch.uint8)
+    model, rms, info, mask = out[0:3], out[3:4], out[4:8].view(torch.int64), ob[64:64 + n]
     _lib.check(L.ps_ransac_rigid(_ptr(src), _ptr(dst), n, _ptr(samples), iterations, float(inlier_tol),
                                  int(min_inliers), _ptr(model), _ptr(mask), _ptr(info), _ptr(rms), _ptr(ws),
                                  wsb.value, C.c_void_p(_stream_ptr(stream))), "ransac")
-    info_h = info.cpu().numpy()
-    model_h = model.cpu().numpy()
-    inl = torch.nonzero(mask).flatten().cpu().numpy().astype(np.int64)
+    h = out.cpu()
+    model_h, rms_h = h[0:3].numpy(), float(h[3])
+    info_h = h[4:8].view(torch.int64).numpy()
+    inl = np.flatnonzero(h.view(torch.uint8)[64:64 + n].numpy()).astype(np.int64)
     st = int(info_h[0])
     return RansacOutcome(ok=st == _lib.PS_OK, status=st, theta=float(model_h[0]), t_x=float(model_h[1]),
-                         t_y=float(model_h[2]), inliers=inl, consensus=int(info_h[1]), rms=float(rms.item()),
+                         t_y=float(model_h[2]), inliers=inl, consensus=int(info_h[1]), rms=rms_h,
                          best_iteration=int(info_h[3]))
 
 
