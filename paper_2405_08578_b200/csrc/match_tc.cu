@@ -702,6 +702,15 @@ int32_t read_count(const int32_t* p, cudaStream_t st) {
   cudaStreamSynchronize(st);
   return h;
 }
+// two device counts with one synchronisation
+void read_counts(const int32_t* p, const int32_t* q, int64_t* hp, int64_t* hq, cudaStream_t st) {
+  int32_t h[2] = {0, 0};
+  cudaMemcpyAsync(&h[0], p, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&h[1], q, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  *hp = h[0];
+  *hq = h[1];
+}
 
 // row blocks x column splits.  One CTA per SM is resident (~180 KB of shared
 // memory), so the split minimises waves x (tiles per CTA + per-CTA overhead,
@@ -804,7 +813,7 @@ int dedupe(const T* X, int64_t n, Side& s, const TcWs& w, cudaStream_t st) {
 template <class T>
 int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t* n_x, const T* Y, int64_t ny_all,
                  const int32_t* y_idx, const int32_t* n_y, int32_t* nn, double* dist, const TcWs& w,
-                 cudaStream_t st) {
+                 cudaStream_t st, int64_t* nx_io = nullptr, int64_t* ny_io = nullptr) {
   const int64_t xrows = rup(nx_max, BM), yrows = rup(ny_all, BN);
   cudaMemsetAsync(w.ymax, 0, 4 * sizeof(unsigned), st);
   cudaMemsetAsync(w.n_overflow, 0, sizeof(int32_t), st);
@@ -818,7 +827,13 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
     cudaFuncSetAttribute(nn_topk_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<1>());
     attr = true;
   }
-  const int64_t nx = read_count(n_x, st), ny = read_count(n_y, st);
+  // the counts size the grids; a caller that already knows one passes it in (>= 0)
+  int64_t nx = nx_io && *nx_io >= 0 ? *nx_io : -1, ny = ny_io && *ny_io >= 0 ? *ny_io : -1;
+  if (nx < 0 && ny < 0) read_counts(n_x, n_y, &nx, &ny, st);
+  else if (nx < 0) nx = read_count(n_x, st);
+  else if (ny < 0) ny = read_count(n_y, st);
+  if (nx_io) *nx_io = nx;
+  if (ny_io) *ny_io = ny;
   if (nx <= 0) return PS_OK;
   const dim3 g0 = tc_grid(nx, ny);
   const int64_t flops_tile = 2ll * BM * BN * KD;
@@ -897,10 +912,11 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   if (rc) return rc;
   mark();
   // pass 1: rows of A (representatives) against the distinct rows of B
-  rc = nearest_pass(A, n1, w.a.uniq, w.a.n_uniq, B, n2, w.b.uniq, w.b.n_uniq, w.nn12, w.d12, w, st);
+  int64_t ua = -1, ub = -1;
+  rc = nearest_pass(A, n1, w.a.uniq, w.a.n_uniq, B, n2, w.b.uniq, w.b.n_uniq, w.nn12, w.d12, w, st, &ua, &ub);
   if (rc) return rc;
-  g_stats[0] = read_count(w.a.n_uniq, st);
-  g_stats[1] = read_count(w.b.n_uniq, st);
+  g_stats[0] = ua;
+  g_stats[1] = ub;
   mark();
   const int of1 = prof ? count_of(w.n_overflow) : 0;
   unsigned long long np1 = 0;
@@ -918,10 +934,11 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   cub::DeviceSelect::Flagged(w.cub_tmp, tb, w.b.iota, w.colflag, w.cols, w.n_cols, (int)n2, st);
   PS_LAUNCHED("cub_select(columns)");
   mark();
-  rc = nearest_pass(B, n2, w.cols, w.n_cols, A, n1, w.a.uniq, w.a.n_uniq, w.nn21, w.d21, w, st);
+  int64_t ncols = -1;
+  rc = nearest_pass(B, n2, w.cols, w.n_cols, A, n1, w.a.uniq, w.a.n_uniq, w.nn21, w.d21, w, st, &ncols, &ua);
   if (rc) return rc;
   mark();
-  g_stats[2] = read_count(w.n_cols, st);
+  g_stats[2] = ncols;
   accept_pairs<<<grid_for(n1, 256), 256, 0, st>>>(w.a.rep, n1, w.nn12, w.d12, w.nn21, delta_s, keys_pair, keys_delta,
                                                   counter);
   PS_LAUNCHED("accept_pairs");
