@@ -89,7 +89,8 @@ typedef struct ps_image_batch {
   int64_t row_pitch;    /* elements between consecutive rows  (>= nc)        */
   int64_t image_stride; /* elements between consecutive images              */
   double alpha;         /* ramp coefficient (fused-ramp pixel types)         */
-  const double* gray_lut; /* PS_PIXELS_RGB8: device table of 2^24 greys      */
+  const double* gray_lut; /* PS_PIXELS_RGB8: device table of 2^24 greys, or
+                             NULL for the checked FMA formula (see below)    */
 } ps_image_batch;
 
 /* Keypoints of a batch, image b occupying slots [b*cap, b*cap + count[b]).
@@ -189,6 +190,17 @@ PS_API int ps_ransac_rigid(const double* src_xy, const double* dst_xy, int64_t n
  * PS_OK or PS_ERR_DEGENERATE. */
 PS_API int ps_estimate_rigid(const double* src_xy, const double* dst_xy, int64_t n,
                       double* out_model, int64_t* out_info, void* stream);
+
+/* ---- RGB ingest ------------------------------------
+ * The grey of an RGB8 pixel is the reference's `rgb @ LUMA` (imaging.py:66-68)
+ * as the run host's BLAS computes it: either gray_lut (all 2^24 triples,
+ * built on the host with numpy) or -- gray_lut == NULL -- the fused formula
+ * fma(B, .114, fma(R, .299, G * .587)), which ps_gray_table_check verifies
+ * against such a table (out_mismatches = 0 means the formula is exact here). */
+PS_API int ps_gray_table_check(const double* gray_lut, unsigned long long* out_mismatches, void* stream);
+/* to_grayscale of an RGB8 batch into a float64 [B, nr, nc] raster (row-major,
+ * dense). */
+PS_API int ps_rgb_to_gray(const ps_image_batch* img, double* out, void* stream);
 
 /* ---- compositor --------------------------------------
  * ps_warp_and_blend <- warp_and_blend(images, placements, canvas, blend,

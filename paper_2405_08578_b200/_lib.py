@@ -72,6 +72,8 @@ SIGNATURES = {
                                   C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "ps_estimate_rigid": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                     C.c_void_p]),
+    "ps_gray_table_check": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ps_rgb_to_gray": (C.c_int, [C.POINTER(ImageBatch), C.c_void_p, C.c_void_p]),
     "ps_warp_and_blend": (C.c_int, [C.POINTER(PlacementC), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                     C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
 }

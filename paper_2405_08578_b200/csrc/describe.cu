@@ -111,6 +111,32 @@ __device__ __forceinline__ void stage_box_u8(const RampU8& im, double* stage, in
   }
 }
 
+// RGB8 raster: the three channel bytes of every pixel, then the table greys,
+// are all requested before any is consumed.
+template <int MAXR>
+__device__ __forceinline__ void stage_box_rgb8(const RampRGB8& im, double* stage, int SP, int r0, int c0, int PR,
+                                               int PC, int sx, int sy) {
+  if (sx >= PC) return;
+  unsigned key[MAXR];
+#pragma unroll
+  for (int i = 0; i < MAXR; ++i) key[i] = (sy + 2 * i < PR) ? im.rgb(r0 + sy + 2 * i, c0 + sx) : 0u;
+  double g[MAXR];
+  if (im.lut) {
+#pragma unroll
+    for (int i = 0; i < MAXR; ++i) g[i] = __ldg(im.lut + key[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < MAXR; ++i) g[i] = bt601_fma(key[i] >> 16, (key[i] >> 8) & 255u, key[i] & 255u);
+  }
+  double k = u32_to_f64((unsigned)((r0 + sy) * im.nc + c0 + sx + 1));
+  const double kstep = u32_to_f64(2u * (unsigned)im.nc);
+#pragma unroll
+  for (int i = 0; i < MAXR; ++i) {
+    if (sy + 2 * i < PR) stage[(sy + 2 * i) * SP + sx] = __dadd_rn(g[i], __dmul_rn(k, im.alpha));
+    k = __dadd_rn(k, kstep);
+  }
+}
+
 template <class Img>
 __device__ __forceinline__ void axis_sample(const Img& im, int r, int c, double& a, double& b) {
   // descriptor.py:135-136 (gradient_at convention, :98-115)
@@ -516,8 +542,8 @@ __device__ __forceinline__ double fx_scale52_warp(double mx) {
   return __hiloint2double(be << 20, 0);
 }
 
-template <int W>
-__device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row, int col, const DescParams& prm,
+template <int W, class Img>
+__device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, int col, const DescParams& prm,
                                                        unsigned* hbase, double* stage, float* __restrict__ o32,
                                                        double* __restrict__ o64) {
   static_assert(W == kStageW, "fast path is staged");
@@ -541,7 +567,10 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const RampU8& im, int row
   static_assert((2 * (D + 36)) % 4 == 0, "vector zeroing");
   for (int q = lane; q < 2 * (D + 36) / 4; q += 32) reinterpret_cast<uint4*>(hbase)[q] = make_uint4(0u, 0u, 0u, 0u);
   const int sx_ = lane & 15, sy_ = lane >> 4;
-  stage_box_u8<BX / 2>(im, stage, SP, BR, BC, BX, BX, sx_, sy_);
+  if constexpr (std::is_same<Img, RampRGB8>::value)
+    stage_box_rgb8<BX / 2>(im, stage, SP, BR, BC, BX, BX, sx_, sy_);
+  else
+    stage_box_u8<BX / 2>(im, stage, SP, BR, BC, BX, BX, sx_, sy_);
   __syncwarp();
   const double* pa = stage + (r0 - 1 - BR) * SP + (c0 - 1 - BC);  // axis region origin
   auto axis_ab = [&](int iv, int iu, double& a, double& b) {
@@ -780,7 +809,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
 constexpr int kFastWarps = 8;
 constexpr int kFastHist = 2 * (128 + 36);
 
-__global__ void __launch_bounds__(kFastWarps * 32, 4) describe_fast_u8(RampU8 img, int64_t img_stride, int B,
+template <class Img>
+__global__ void __launch_bounds__(kFastWarps * 32, 4) describe_fast_u8(Img img, int64_t img_stride, int B,
                                                                        const int32_t* __restrict__ kp_row,
                                                                        const int32_t* __restrict__ kp_col,
                                                                        const int32_t* __restrict__ kp_scale,
@@ -806,7 +836,7 @@ __global__ void __launch_bounds__(kFastWarps * 32, 4) describe_fast_u8(RampU8 im
       ++b;
     }
     if (counts && i >= counts[b]) continue;
-    RampU8 im = img;
+    Img im = img;
     im.p = img.p + (int64_t)b * img_stride * decltype(img)::kElem;
     const int row = kp_row[g], col = kp_col[g];
     if (row < 0 || row >= im.nr || col < 0 || col >= im.nc) continue;  // validated by the caller
@@ -858,6 +888,45 @@ int region_width(int scale, double beta0, int d, int l_max, int nr, int nc, int*
 }  // namespace ps
 
 using namespace ps;
+
+// 8-bit rasters (grey or RGB): w = 8 keypoints through the fast kernel, the
+// rest (other sides, 36-bin near-ties) queued for the general kernel.
+template <class Img>
+int launch_fast(const Img& im, const ps_image_batch* img, const ps_keypoints* kp, int32_t default_scale,
+                const DescParams& prm, float* out_desc32, double* out_desc64, int64_t total, size_t shmem,
+                cudaStream_t s) {
+  int64_t* work = nullptr;
+  static bool pool_set = false;  // keep freed queue memory in the stream-ordered pool
+  if (!pool_set) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_set = true;
+  }
+  cudaMallocAsync(&work, (size_t)total * sizeof(int64_t) + 16, s);
+  int st = check_cuda("cudaMallocAsync(describe work list)");
+  if (st) return st;
+  unsigned long long* n_work = reinterpret_cast<unsigned long long*>(work + total);
+  cudaMemsetAsync(n_work, 0, sizeof(unsigned long long), s);
+  const size_t fshmem = (size_t)kFastWarps * (FastStage::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
+  cudaFuncSetAttribute(describe_fast_u8<Img>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fshmem);
+  int64_t fblocks = (total + kFastWarps - 1) / kFastWarps;
+  if (fblocks > 148 * 16) fblocks = 148 * 16;
+  describe_fast_u8<Img><<<(unsigned)fblocks, kFastWarps * 32, fshmem, s>>>(
+      im, img->image_stride, img->batch, kp->row, kp->col, kp->scale, default_scale, kp->count, kp->cap, prm,
+      out_desc32, out_desc64, work, n_work);
+  PS_LAUNCHED("describe_fast_u8");
+  describe_kernel<Img><<<148 * 2, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,
+                                                           kp->scale, default_scale, kp->count, kp->cap, prm,
+                                                           out_desc32, out_desc64, work, n_work);
+  PS_LAUNCHED("describe_kernel(queued)");
+  cudaFreeAsync(work, s);
+  return check_cuda("cudaFreeAsync");
+}
 
 extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, int32_t default_scale,
                            const int32_t* host_scale_set, int32_t n_scale_set, double beta0, int32_t d, int32_t l_max,
@@ -945,45 +1014,11 @@ extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, in
   cudaFuncSetAttribute(describe_kernel<RampF64Raw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
   if (img->pixel_type == PS_PIXELS_U8) {
     RampU8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
-    // queue for keypoints the fast kernel leaves to the general one
-    int64_t* work = nullptr;
-    static bool pool_set = false;  // keep freed queue memory in the stream-ordered pool
-    if (!pool_set) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      }
-      pool_set = true;
-    }
-    cudaMallocAsync(&work, (size_t)total * sizeof(int64_t) + 16, s);
-    int st = check_cuda("cudaMallocAsync(describe work list)");
-    if (st) return st;
-    unsigned long long* n_work = reinterpret_cast<unsigned long long*>(work + total);
-    cudaMemsetAsync(n_work, 0, sizeof(unsigned long long), s);
-    const size_t fshmem = (size_t)kFastWarps * (FastStage::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
-    cudaFuncSetAttribute(describe_fast_u8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fshmem);
-    int64_t fblocks = (total + kFastWarps - 1) / kFastWarps;
-    if (fblocks > 148 * 16) fblocks = 148 * 16;
-    describe_fast_u8<<<(unsigned)fblocks, kFastWarps * 32, fshmem, s>>>(
-        im, img->image_stride, img->batch, kp->row, kp->col, kp->scale, default_scale, kp->count, kp->cap, prm,
-        out_desc32, out_desc64, work, n_work);
-    PS_LAUNCHED("describe_fast_u8");
-    describe_kernel<<<148 * 2, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,
-                                                        kp->scale, default_scale, kp->count, kp->cap, prm, out_desc32,
-                                                        out_desc64, work, n_work);
-    PS_LAUNCHED("describe_kernel(queued)");
-    cudaFreeAsync(work, s);
-    return check_cuda("cudaFreeAsync");
+    return launch_fast(im, img, kp, default_scale, prm, out_desc32, out_desc64, total, shmem, s);
   } else if (img->pixel_type == PS_PIXELS_RGB8) {
-    PS_REQUIRE(img->gray_lut != nullptr, PS_ERR_ARGUMENT, "RGB8 pixels need gray_lut");
     RampRGB8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha, img->gray_lut};
     cudaFuncSetAttribute(describe_kernel<RampRGB8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
-    describe_kernel<<<(unsigned)blocks, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,
-                                                                  kp->scale, default_scale, kp->count, kp->cap, prm,
-                                                                  out_desc32, out_desc64, nullptr, nullptr);
+    return launch_fast(im, img, kp, default_scale, prm, out_desc32, out_desc64, total, shmem, s);
   } else if (img->pixel_type == PS_PIXELS_F64_RAW) {
     RampF64Raw im{(const double*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
     describe_kernel<<<(unsigned)blocks, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,

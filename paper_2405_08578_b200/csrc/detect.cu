@@ -515,7 +515,6 @@ extern "C" int ps_detect(const ps_image_batch* img, const int32_t* host_scales, 
   if (img->pixel_type == PS_PIXELS_RGB8) {
     PS_REQUIRE(img->alpha > 0 && img->alpha * img->nr * img->nc <= 0.05 * 255.0, PS_ERR_CONFIG,
                "alpha=%g outside the ramp limits (imaging.py:138-145)", img->alpha);
-    PS_REQUIRE(img->gray_lut != nullptr, PS_ERR_ARGUMENT, "RGB8 pixels need gray_lut");
     PS_REQUIRE((int64_t)img->nr * img->row_pitch * 3 < (int64_t)INT32_MAX, PS_ERR_ARGUMENT,
                "image too large (3*nr*pitch >= 2^31)");
     RampRGB8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha, img->gray_lut};

@@ -3,6 +3,8 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <algorithm>
+#include <cmath>
 
 #include <cstdarg>
 #include <cstdio>
@@ -82,9 +84,22 @@ struct RampU8 {
   __device__ __forceinline__ unsigned key(int r, int c) const { return p[r * (int)pitch + c]; }
 };
 
-// Interleaved RGB8: the grey is the host's own BT.601 bits from
-// a 2^24-entry table; key() is the exact integer luma 299R + 587G + 114B,
-// whose order equals the grey order (distinct greys differ by >= 0.001).
+// BT.601 grey in the evaluation order of the x86-64 OpenBLAS dgemv kernel
+// behind numpy's `rgb @ LUMA` (two FMAs around the green product; measured
+// on all 2^24 triples -- the host check `ps_gray_table_check` decides at run
+// time whether this formula reproduces the run host's own bits).
+__host__ __device__ __forceinline__ double bt601_fma(unsigned r, unsigned g, unsigned b) {
+#ifdef __CUDA_ARCH__
+  return __fma_rn((double)b, 0.114, __fma_rn((double)r, 0.299, __dmul_rn((double)g, 0.587)));
+#else
+  return std::fma((double)b, 0.114, std::fma((double)r, 0.299, (double)g * 0.587));
+#endif
+}
+
+// Interleaved RGB8: the grey is the host's own BT.601 bits -- from
+// a 2^24-entry table, or (lut == nullptr) from bt601_fma once the table has
+// been checked equal to it; key() is the exact integer luma 299R + 587G +
+// 114B, whose order equals the grey order (distinct greys differ by >= 0.001).
 struct RampRGB8 {
   static constexpr int kElem = 3;
   const uint8_t* p;
@@ -100,9 +115,14 @@ struct RampRGB8 {
     const uint8_t* q = p + 3 * (r * (int)pitch + c);
     return 299u * q[0] + 587u * q[1] + 114u * q[2];
   }
+  __device__ __forceinline__ double gray(int r, int c) const {
+    const uint8_t* q = p + 3 * (r * (int)pitch + c);
+    if (lut) return __ldg(lut + (((unsigned)q[0] << 16) | ((unsigned)q[1] << 8) | (unsigned)q[2]));
+    return bt601_fma(q[0], q[1], q[2]);
+  }
   __device__ __forceinline__ double at(int r, int c) const {
     const double k = u32_to_f64((unsigned)(r * nc + c + 1));
-    return __dadd_rn(__ldg(lut + rgb(r, c)), __dmul_rn(k, alpha));
+    return __dadd_rn(gray(r, c), __dmul_rn(k, alpha));
   }
 };
 

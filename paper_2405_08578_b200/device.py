@@ -76,7 +76,7 @@ class DeviceImages:
                 raise ValueError("RGB images must be [B, nr, nc, 3] with interleaved channels")
             return _lib.ImageBatch(d.data_ptr(), _lib.PS_PIXELS_RGB8, d.shape[0], d.shape[1], d.shape[2],
                                    d.stride(1) // 3, (d.stride(0) if d.shape[0] > 1 else d.stride(1) * d.shape[1]) // 3,
-                                   float(self.alpha), self.lut.data_ptr())
+                                   float(self.alpha), self.lut.data_ptr() if self.lut is not None else None)
         if d.dim() != 3 or d.stride(2) != 1:
             raise ValueError("images must be [B, nr, nc] with unit column stride")
         ptype = {"u8": _lib.PS_PIXELS_U8, "f64": _lib.PS_PIXELS_F64, "f64raw": _lib.PS_PIXELS_F64_RAW}[self.kind]
@@ -92,7 +92,7 @@ def as_device_images(images, alpha=None, *, ramped=False, rgb=False, device=None
         return images
     t = images if isinstance(images, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(images))
     if rgb or t.dim() == 4:
-        from .ingest import gray_lut
+        from .ingest import gray_source
 
         if t.dim() == 3:
             t = t.unsqueeze(0)
@@ -103,7 +103,7 @@ def as_device_images(images, alpha=None, *, ramped=False, rgb=False, device=None
         t = t.contiguous()
         if alpha is None:
             alpha = default_alpha(t.shape[1], t.shape[2])
-        return DeviceImages(t, "rgb8", float(alpha), gray_lut(t.device))
+        return DeviceImages(t, "rgb8", float(alpha), gray_source(t.device))
     if t.dim() == 2:
         t = t.unsqueeze(0)
     if not t.is_cuda:

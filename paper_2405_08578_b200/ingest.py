@@ -15,6 +15,10 @@ table.  With it the RGB8 pixel type of the C-ABI
   descriptor's raster are the reference's bits;
 
 and ``to_grayscale_device`` returns the reference's grey image itself.
+Once per device the table is compared on the GPU with the two-FMA formula
+the x86-64 OpenBLAS dgemv kernel evaluates; when all 2^24 entries agree (they
+do on this image's hosts) the kernels compute the grey instead of gathering
+it from the 128 MB table.
 Uploading RGB moves 3 bytes per pixel instead of the 8 of a float64 grey.
 """
 
@@ -46,11 +50,16 @@ def host_gray_lut() -> np.ndarray:
         return _host_lut
 
 
-def gray_lut(device=None) -> torch.Tensor:
-    """The grey table on ``device`` (cached per device)."""
+def _cuda_device(device):
     dev = torch.device(device if device is not None else "cuda")
     if dev.type == "cuda" and dev.index is None:
         dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+def gray_lut(device=None) -> torch.Tensor:
+    """The grey table on ``device`` (cached per device)."""
+    dev = _cuda_device(device)
     with _lock:
         t = _dev_luts.get(dev)
     if t is None:
@@ -58,6 +67,36 @@ def gray_lut(device=None) -> torch.Tensor:
         with _lock:
             _dev_luts[dev] = t
     return t
+
+
+_formula_ok: dict = {}
+
+
+def gray_source(device=None):
+    """What the RGB8 kernels read the grey from: None when the fused formula
+    fma(B, .114, fma(R, .299, G * .587)) reproduces this host's table on all
+    2^24 triples (checked once per device with ps_gray_table_check), else
+    the table itself."""
+    import ctypes as C
+
+    from . import _lib
+
+    dev = _cuda_device(device)
+    with _lock:
+        ok = _formula_ok.get(dev)
+    if ok is None:
+        lut = gray_lut(dev)
+        bad = torch.zeros(1, dtype=torch.int64, device=dev)
+        with torch.cuda.device(dev):
+            st = torch.cuda.current_stream().cuda_stream
+            _lib.check(_lib.lib().ps_gray_table_check(C.c_void_p(lut.data_ptr()), C.c_void_p(bad.data_ptr()),
+                                                      C.c_void_p(st)), "gray_table_check")
+        ok = int(bad.item()) == 0
+        with _lock:
+            _formula_ok[dev] = ok
+            if ok:
+                _dev_luts.pop(dev, None)  # the formula replaces the 128 MB table
+    return None if ok else gray_lut(dev)
 
 
 def rgb_key(rgb: torch.Tensor) -> torch.Tensor:
@@ -68,9 +107,17 @@ def rgb_key(rgb: torch.Tensor) -> torch.Tensor:
 
 def to_grayscale_device(rgb: torch.Tensor) -> torch.Tensor:
     """Device twin of the reference's to_grayscale (imaging.py:66-68) for
-    uint8 RGB: a float64 [..., nr, nc] tensor with the reference's bits."""
-    if rgb.dtype != torch.uint8 or rgb.shape[-1] != 3:
-        raise ValueError("expected uint8 [..., 3] RGB")
-    if not rgb.is_cuda:
-        rgb = rgb.cuda()
-    return gray_lut(rgb.device)[rgb_key(rgb)]
+    uint8 RGB [nr, nc, 3] / [B, nr, nc, 3]: float64 greys with the
+    reference's bits (through ps_rgb_to_gray)."""
+    import ctypes as C
+
+    from . import _lib
+    from .device import as_device_images
+
+    if rgb.dtype != torch.uint8 or rgb.shape[-1] != 3 or rgb.dim() not in (3, 4):
+        raise ValueError("expected uint8 [nr, nc, 3] or [B, nr, nc, 3] RGB")
+    im = as_device_images(rgb, rgb=True)
+    out = torch.empty(im.data.shape[:3], dtype=torch.float64, device=im.data.device)
+    _lib.check(_lib.lib().ps_rgb_to_gray(C.byref(im.c_struct()), C.c_void_p(out.data_ptr()),
+                                         C.c_void_p(torch.cuda.current_stream().cuda_stream)), "rgb_to_gray")
+    return out if rgb.dim() == 4 else out[0]
