@@ -807,10 +807,13 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
 // warps); everything else -- other region sides and 36-bin near-ties -- is
 // queued for describe_kernel.
 constexpr int kFastWarps = 8;
+#ifndef PS_FAST_MINB
+#define PS_FAST_MINB 4
+#endif
 constexpr int kFastHist = 2 * (128 + 36);
 
 template <class Img>
-__global__ void __launch_bounds__(kFastWarps * 32, 4) describe_fast_u8(Img img, int64_t img_stride, int B,
+__global__ void __launch_bounds__(kFastWarps * 32, PS_FAST_MINB) describe_fast_u8(Img img, int64_t img_stride, int B,
                                                                        const int32_t* __restrict__ kp_row,
                                                                        const int32_t* __restrict__ kp_col,
                                                                        const int32_t* __restrict__ kp_scale,
