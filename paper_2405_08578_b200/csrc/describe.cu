@@ -711,38 +711,49 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
 #pragma unroll
   for (int j = 0; j < SPL; ++j) h2_add(h128, D, bn[j], mg[j], fx);
   __syncwarp();
-  // --- L2 normalise, clamp at 0.2, renormalise (descriptor.py:250-255)
-  constexpr int kPer = D / 32;
+  // --- L2 normalise, clamp at 0.2, renormalise (descriptor.py:250-255).
+  // Lane l owns bins 4l..4l+3 (one 16-byte shared load per limb array, one
+  // 16-byte store of the float32 row); 1/||v|| comes from rsqrt (~1 ulp).
+  static_assert(D == 128, "four bins per lane");
   {
     const double inv = 1.0 / fx;  // exact (power of two)
-    double vals[kPer];
-    double ss = 0.0;
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      vals[j] = __dmul_rn((double)h2_get(h128, D, lane + 32 * j), inv);
-      ss = __dadd_rn(ss, __dmul_rn(vals[j], vals[j]));
-    }
+    const uint4 lo = *reinterpret_cast<const uint4*>(h128 + 4 * lane);
+    const uint4 hi = *reinterpret_cast<const uint4*>(h128 + D + 4 * lane);
+    double v0 = __dmul_rn((double)(((unsigned long long)hi.x << kLimb) + lo.x), inv);
+    double v1 = __dmul_rn((double)(((unsigned long long)hi.y << kLimb) + lo.y), inv);
+    double v2 = __dmul_rn((double)(((unsigned long long)hi.z << kLimb) + lo.z), inv);
+    double v3 = __dmul_rn((double)(((unsigned long long)hi.w << kLimb) + lo.w), inv);
+    double ss = __dadd_rn(__dadd_rn(__dmul_rn(v0, v0), __dmul_rn(v1, v1)), __dadd_rn(__dmul_rn(v2, v2), __dmul_rn(v3, v3)));
 #pragma unroll
     for (int o = 16; o; o >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
-    const double n1 = __dsqrt_rn(ss);
-    double n2 = 0.0;
-    if (n1 > 0.0) {
-      const double r1 = __drcp_rn(n1);
-      double ss2 = 0.0;
+    if (ss > 0.0) {
+      const double r1 = rsqrt(ss);
+      v0 = __dmul_rn(v0, r1);
+      v1 = __dmul_rn(v1, r1);
+      v2 = __dmul_rn(v2, r1);
+      v3 = __dmul_rn(v3, r1);
+      v0 = v0 < 0.2 ? v0 : 0.2;  // non-negative values: no NaN handling needed
+      v1 = v1 < 0.2 ? v1 : 0.2;
+      v2 = v2 < 0.2 ? v2 : 0.2;
+      v3 = v3 < 0.2 ? v3 : 0.2;
+      double s2 =
+          __dadd_rn(__dadd_rn(__dmul_rn(v0, v0), __dmul_rn(v1, v1)), __dadd_rn(__dmul_rn(v2, v2), __dmul_rn(v3, v3)));
 #pragma unroll
-      for (int j = 0; j < kPer; ++j) {
-        vals[j] = fmin(__dmul_rn(vals[j], r1), 0.2);
-        ss2 = __dadd_rn(ss2, __dmul_rn(vals[j], vals[j]));
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) ss2 = __dadd_rn(ss2, __shfl_xor_sync(0xffffffffu, ss2, o));
-      n2 = __drcp_rn(__dsqrt_rn(ss2));
+      for (int o = 16; o; o >>= 1) s2 = __dadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, o));
+      const double r2 = rsqrt(s2);
+      v0 = __dmul_rn(v0, r2);
+      v1 = __dmul_rn(v1, r2);
+      v2 = __dmul_rn(v2, r2);
+      v3 = __dmul_rn(v3, r2);
+    } else {
+      v0 = v1 = v2 = v3 = 0.0;
     }
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const double v = n1 > 0.0 ? __dmul_rn(vals[j], n2) : 0.0;
-      if (o32) o32[lane + 32 * j] = __double2float_rn(v);
-      if (o64) o64[lane + 32 * j] = v;
+    if (o32)
+      reinterpret_cast<float4*>(o32)[lane] =
+          make_float4(__double2float_rn(v0), __double2float_rn(v1), __double2float_rn(v2), __double2float_rn(v3));
+    if (o64) {
+      reinterpret_cast<double2*>(o64)[2 * lane] = make_double2(v0, v1);
+      reinterpret_cast<double2*>(o64)[2 * lane + 1] = make_double2(v2, v3);
     }
   }
   __syncwarp();
