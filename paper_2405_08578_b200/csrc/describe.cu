@@ -556,12 +556,15 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
   const int r0 = min(max(row - W / 2, 1), nr - 1 - W);
   const int c0 = min(max(col - W / 2, 1), nc - 1 - W);
   constexpr double half = (double)(W - 1) / 2.0;
-  const double cy = fmin(fmax((double)row, 1.0 + half), __dsub_rn((double)nr - 2.0, half));
-  const double cx = fmin(fmax((double)col, 1.0 + half), __dsub_rn((double)nc - 2.0, half));
+  // centre clamp min(max(row, 1 + half), nr - 2 - half) on half-integers, in
+  // integers (2 cy is an integer; exact)
+  const int cy2 = min(max(2 * row, 2 + (W - 1)), 2 * (nr - 2) - (W - 1));
+  const int cx2 = min(max(2 * col, 2 + (W - 1)), 2 * (nc - 2) - (W - 1));
+  const double cy = 0.5 * (double)cy2, cx = 0.5 * (double)cx2;
   // One staged box for both phases: the axis region spans rows r0-1..r0+W and
   // any rotated patch pr0-1..pr1+1 lies within cy -/+ (3.5 sqrt(2) + 2), so
   // rows floor(cy)-7 .. floor(cy)+8 (clamped to the image) hold both.
-  const int BR = max(0, min((int)cy - 7, nr - BX)), BC = max(0, min((int)cx - 7, nc - BX));
+  const int BR = max(0, min((cy2 >> 1) - 7, nr - BX)), BC = max(0, min((cx2 >> 1) - 7, nc - BX));
   unsigned* h128 = hbase;         // [2][128]
   unsigned* h36 = hbase + 2 * D;  // [2][36]
   static_assert((2 * (D + 36)) % 4 == 0, "vector zeroing");
@@ -684,12 +687,11 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
       const double a00 = fa[y0 * SF + x0], b00 = fb[y0 * SF + x0], a01 = fa[y0 * SF + x1], b01 = fb[y0 * SF + x1];
       const double a10 = fa[y1 * SF + x0], b10 = fb[y1 * SF + x0], a11 = fa[y1 * SF + x1], b11 = fb[y1 * SF + x1];
       const double sy = __dsub_rn(1.0, fyy), sx = __dsub_rn(1.0, fxx);
-      const double as = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(a00, sy), sx), __dmul_rn(__dmul_rn(a01, sy), fxx)),
-                                            __dmul_rn(__dmul_rn(a10, fyy), sx)),
-                                  __dmul_rn(__dmul_rn(a11, fyy), fxx));
-      const double bs = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(__dmul_rn(b00, sy), sx), __dmul_rn(__dmul_rn(b01, sy), fxx)),
-                                            __dmul_rn(__dmul_rn(b10, fyy), sx)),
-                                  __dmul_rn(__dmul_rn(b11, fyy), fxx));
+      // bilinear blend with shared corner weights and FMAs (differs from the
+      // reference's left-to-right products by ~1 ulp; the bar is 1e-4)
+      const double w00 = __dmul_rn(sy, sx), w01 = __dmul_rn(sy, fxx), w10 = __dmul_rn(fyy, sx), w11 = __dmul_rn(fyy, fxx);
+      const double as = __fma_rn(a11, w11, __fma_rn(a10, w10, __fma_rn(a01, w01, __dmul_rn(a00, w00))));
+      const double bs = __fma_rn(b11, w11, __fma_rn(b10, w10, __fma_rn(b01, w01, __dmul_rn(b00, w00))));
       const float af = (float)as, bf = (float)bs;
       const float xb = wrap_two_pi_f(fast_atan2f(bf, af) - theta0f) * 1.2732395447351628f;
       int ob;
