@@ -651,6 +651,7 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
     const int pc0 = max((int)floor(xmin), 1), pc1 = min((int)ceil(xmax), nc - 2);
     const int xcap = max(pc1 - pc0 - 1, 0), ycap = max(pr1 - pr0 - 1, 0);
     const double xhi = (double)(nc - 2), yhi = (double)(nr - 2);
+    const double dpc0 = (double)pc0, dpr0 = (double)pr0;
     const int FR = pr1 - pr0 + 1, FC = pc1 - pc0 + 1;
     if (pr0 - 1 < BR || pr1 + 1 >= BR + BX || pc0 - 1 < BC || pc1 + 1 >= BC + BX) {  // cannot happen; be safe
       __syncwarp();
@@ -679,9 +680,12 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
       mg[j] = 0.0;
       bn[j] = 0;
       if (!(x >= 1.0 && x <= xhi && y >= 1.0 && y <= yhi)) continue;  // hypot * valid = 0
-      const double lx = __dsub_rn(fmin(fmax(x, (double)pc0), (double)pc1), (double)pc0);
-      const double ly = __dsub_rn(fmin(fmax(y, (double)pr0), (double)pr1), (double)pr0);
-      const int x0 = min((int)floor(lx), xcap), y0 = min((int)floor(ly), ycap);
+      // The reference clips x to [pc0, pc1] first; for a valid sample that is
+      // the identity: x >= xmin and x <= xmax hold exactly (same rounded
+      // expressions, monotone in u and v), and the image clamps of pc0 / pc1
+      // are the validity bounds themselves.
+      const double lx = __dsub_rn(x, dpc0), ly = __dsub_rn(y, dpr0);
+      const int x0 = max(min((int)floor(lx), xcap), 0), y0 = max(min((int)floor(ly), ycap), 0);
       const double fxx = __dsub_rn(lx, (double)x0), fyy = __dsub_rn(ly, (double)y0);
       const int x1 = min(x0 + 1, pc1 - pc0), y1 = min(y0 + 1, pr1 - pr0);
       const double a00 = fa[y0 * SF + x0], b00 = fb[y0 * SF + x0], a01 = fa[y0 * SF + x1], b01 = fb[y0 * SF + x1];
