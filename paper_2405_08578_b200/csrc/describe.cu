@@ -161,17 +161,15 @@ struct Stage {
 constexpr int kStageW = 8;  // region side served from shared memory
 constexpr int kStageDoubles = Stage<kStageW>::kTotal;
 
-// Fast-path (w = 8) layout, chosen for conflict-free shared-memory phases:
-// one 16 x 16 box of P (rows at a stride of 24 doubles: axis reads of a
-// half-warp hit 16 distinct 8-byte banks) that holds both the axis region and
-// every rotated patch, then the gradient fields at an odd stride of 13.
+// Fast-path (w = 8) layout: one 16 x 16 box of P (rows at a stride of 24
+// doubles: axis reads of a half-warp hit 16 distinct 8-byte banks) that holds
+// both the axis region and every rotated patch; the rotated samples form
+// their gradient-field corners from it directly.
 struct FastStage {
-  static constexpr int kSpan = Stage<8>::kSpan;  // 12: rotated field side
-  static constexpr int kBox = 16;                // staged P box side
-  static constexpr int SPP = 24, SPF = 13;
-  static constexpr int kP = kBox * SPP;          // 384
-  static constexpr int kF = kSpan * SPF;         // 156
-  static constexpr int kTotal = kP + 2 * kF;     // 696 doubles
+  static constexpr int kBox = 16;        // staged P box side
+  static constexpr int SPP = 24;
+  static constexpr int kP = kBox * SPP;  // 384
+  static constexpr int kTotal = kP;      // doubles per warp
 };
 
 // ---- float32 screening of the discrete decisions -------------------------------
@@ -548,7 +546,7 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
                                                        double* __restrict__ o64) {
   static_assert(W == kStageW, "fast path is staged");
   static_assert(W * W == 64, "fx_scale52_warp assumes 64 samples");
-  constexpr int NS = W * W, SPL = NS / 32, D = 128, SP = FastStage::SPP, SF = FastStage::SPF;
+  constexpr int NS = W * W, SPL = NS / 32, D = 128, SP = FastStage::SPP;
   constexpr int WS = W / 4;
   const int lane = threadIdx.x & 31;
   const int nr = im.nr, nc = im.nc;
@@ -652,24 +650,16 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
     const int xcap = max(pc1 - pc0 - 1, 0), ycap = max(pr1 - pr0 - 1, 0);
     const double xhi = (double)(nc - 2), yhi = (double)(nr - 2);
     const double dpc0 = (double)pc0, dpr0 = (double)pr0;
-    const int FR = pr1 - pr0 + 1, FC = pc1 - pc0 + 1;
-    if (pr0 - 1 < BR || pr1 + 1 >= BR + BX || pc0 - 1 < BC || pc1 + 1 >= BC + BX) {  // cannot happen; be safe
+    // the patch lies in the staged box and is at least 2 x 2 (cannot fail for
+    // images >= 16 x 16; be safe)
+    if (pr0 - 1 < BR || pr1 + 1 >= BR + BX || pc0 - 1 < BC || pc1 + 1 >= BC + BX || pr1 <= pr0 || pc1 <= pc0) {
       __syncwarp();
       return false;
     }
-    if (pr0 - 1 < BR || pr1 + 1 >= BR + BX || pc0 - 1 < BC || pc1 + 1 >= BC + BX) {  // cannot happen; be safe
-      __syncwarp();
-      return false;
-    }
-    double* fa = stage + FastStage::kP;
-    double* fb = fa + FastStage::kF;
-    const double* pb = stage + (pr0 - 1 - BR) * SP + (pc0 - 1 - BC);  // rotated patch box origin
-    for (int y = sy_; y < FR; y += 2)
-      if (sx_ < FC) {
-        fa[y * SF + sx_] = __dsub_rn(pb[(y + 2) * SP + sx_ + 1], pb[y * SP + sx_ + 1]);
-        fb[y * SF + sx_] = __dsub_rn(pb[(y + 1) * SP + sx_ + 2], pb[(y + 1) * SP + sx_]);
-      }
-    __syncwarp();
+    // gradient fields fa(y, x) = P(y+1, x) - P(y-1, x), fb(y, x) = P(y, x+1) -
+    // P(y, x-1) of the patch (descriptor.py:192-193), formed at the four
+    // corners of each sample straight from the staged raster
+    const double* pb = stage + (pr0 - 1 - BR) * SP + (pc0 - 1 - BC);  // P(pr0 - 1, pc0 - 1)
     const double c0t = ct, s0t = -st;  // cos / sin of theta0
 #pragma unroll
     for (int j = 0; j < SPL; ++j) {
@@ -687,9 +677,16 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
       const double lx = __dsub_rn(x, dpc0), ly = __dsub_rn(y, dpr0);
       const int x0 = max(min((int)floor(lx), xcap), 0), y0 = max(min((int)floor(ly), ycap), 0);
       const double fxx = __dsub_rn(lx, (double)x0), fyy = __dsub_rn(ly, (double)y0);
-      const int x1 = min(x0 + 1, pc1 - pc0), y1 = min(y0 + 1, pr1 - pr0);
-      const double a00 = fa[y0 * SF + x0], b00 = fb[y0 * SF + x0], a01 = fa[y0 * SF + x1], b01 = fb[y0 * SF + x1];
-      const double a10 = fa[y1 * SF + x0], b10 = fb[y1 * SF + x0], a11 = fa[y1 * SF + x1], b11 = fb[y1 * SF + x1];
+      // corners (y0, x0) .. (y0 + 1, x0 + 1): x0 <= pc1 - pc0 - 1 since pc1 > pc0
+      const double* q = pb + y0 * SP + x0;  // P(pr0 + y0 - 1, pc0 + x0 - 1)
+      const double p01 = q[1], p02 = q[2];
+      const double p10 = q[SP], p11 = q[SP + 1], p12 = q[SP + 2], p13 = q[SP + 3];
+      const double p20 = q[2 * SP], p21 = q[2 * SP + 1], p22 = q[2 * SP + 2], p23 = q[2 * SP + 3];
+      const double p31 = q[3 * SP + 1], p32 = q[3 * SP + 2];
+      const double a00 = __dsub_rn(p21, p01), a01 = __dsub_rn(p22, p02);
+      const double a10 = __dsub_rn(p31, p11), a11 = __dsub_rn(p32, p12);
+      const double b00 = __dsub_rn(p12, p10), b01 = __dsub_rn(p13, p11);
+      const double b10 = __dsub_rn(p22, p20), b11 = __dsub_rn(p23, p21);
       const double sy = __dsub_rn(1.0, fyy), sx = __dsub_rn(1.0, fxx);
       // bilinear blend with shared corner weights and FMAs (differs from the
       // reference's left-to-right products by ~1 ulp; the bar is 1e-4)
