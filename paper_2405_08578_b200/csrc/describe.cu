@@ -10,6 +10,7 @@
 // atan2 / hypot are CUDA's float64 versions (numpy's own differ from libm by
 // ~1 ulp), hence the 1e-4 relative parity bar of contract P2.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 #include <vector>
@@ -906,6 +907,277 @@ int region_width(int scale, double beta0, int d, int l_max, int nr, int nc, int*
 
 using namespace ps;
 
+// ---- two keypoints per warp (half-warp each) --------------------------------
+// The same arithmetic as describe_keypoint_w8u8 with 16 lanes per keypoint
+// (4 samples per lane per phase, 8 descriptor bins per lane): the
+// per-keypoint scalar work -- centre, extents, argmax, reductions -- is issued
+// once for two keypoints.  Half-warp reductions: butterflies with xor < 16 and
+// full-warp REDUX over values masked to one half.
+__device__ __forceinline__ unsigned half_max_u32(unsigned v, int hsel) {
+  const unsigned a = __reduce_max_sync(0xffffffffu, hsel == 0 ? v : 0u);
+  const unsigned b = __reduce_max_sync(0xffffffffu, hsel == 1 ? v : 0u);
+  return hsel ? b : a;
+}
+// fixed-point scale from the half's largest magnitude (64 samples per keypoint)
+__device__ __forceinline__ double fx_scale52_half(double mx, int hsel) {
+  const unsigned eb = half_max_u32((unsigned)__double2hiint(mx), hsel) >> 20;
+  if (eb == 0u) return 1.0;
+  const int be = min(2091 - (int)eb, 2046);
+  return __hiloint2double(be << 20, 0);
+}
+
+template <class Img>
+__device__ __forceinline__ bool describe_pair_w8(const Img& im, int row, int col, bool act, const DescParams& prm,
+                                                 unsigned* hbase, double* stage, float* __restrict__ o32,
+                                                 double* __restrict__ o64) {
+  constexpr int W = 8, SPL = 4, D = 128, SP = FastStage::SPP, WS = W / 4, BX = FastStage::kBox;
+  const int lane = threadIdx.x & 31, hl = lane & 15, hsel = lane >> 4;
+  const int nr = im.nr, nc = im.nc;
+  const int r0 = min(max(row - W / 2, 1), nr - 1 - W);
+  const int c0 = min(max(col - W / 2, 1), nc - 1 - W);
+  constexpr double half = (double)(W - 1) / 2.0;
+  const int cy2 = min(max(2 * row, 2 + (W - 1)), 2 * (nr - 2) - (W - 1));
+  const int cx2 = min(max(2 * col, 2 + (W - 1)), 2 * (nc - 2) - (W - 1));
+  const double cy = 0.5 * (double)cy2, cx = 0.5 * (double)cx2;
+  const int BR = max(0, min((cy2 >> 1) - 7, nr - BX)), BC = max(0, min((cx2 >> 1) - 7, nc - BX));
+  unsigned* h128 = hbase;
+  unsigned* h36 = hbase + 2 * D;
+#pragma unroll
+  for (int q = hl; q < 2 * (D + 36) / 4; q += 16) reinterpret_cast<uint4*>(hbase)[q] = make_uint4(0u, 0u, 0u, 0u);
+  if constexpr (std::is_same<Img, RampRGB8>::value) {
+    stage_box_rgb8<BX / 2>(im, stage, SP, BR, BC, BX, BX, hl, 0);
+    stage_box_rgb8<BX / 2>(im, stage, SP, BR, BC, BX, BX, hl, 1);
+  } else {
+    stage_box_u8<BX / 2>(im, stage, SP, BR, BC, BX, BX, hl, 0);
+    stage_box_u8<BX / 2>(im, stage, SP, BR, BC, BX, BX, hl, 1);
+  }
+  __syncwarp();
+  const double* pa = stage + (r0 - 1 - BR) * SP + (c0 - 1 - BC);
+  auto axis_ab = [&](int iv, int iu, double& a, double& b) {
+    a = __dsub_rn(pa[(iv + 2) * SP + iu + 1], pa[iv * SP + iu + 1]);
+    b = __dsub_rn(pa[(iv + 1) * SP + iu + 2], pa[(iv + 1) * SP + iu]);
+  };
+  auto bin64 = [&](double a, double b, double shift, double k, int nbins) {
+    const double ori = mod_two_pi(__dsub_rn(atan2(b, a), shift), prm.two_pi);
+    return min((int)__dmul_rn(ori, k), nbins - 1);
+  };
+  double mg[SPL];
+  int bn[SPL];
+  bool ok = act;
+  if (!prm.orient) {
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) {
+      const int s = hl + 16 * j, iv = s / W, iu = s % W;
+      double a, b;
+      axis_ab(iv, iu, a, b);
+      const float xb = wrap_two_pi_f(fast_atan2f((float)b, (float)a)) * 1.2732395447351628f;
+      int ob;
+      if (!certified_bin(xb, 8, ob)) {
+        const int m = min(max(__float2int_rn(xb), 0), 8);
+        ob = side_bin(a, b, prm.c8[m], prm.s8[m], m, 8);
+        if (ob < 0) ob = bin64(a, b, 0.0, prm.k8, 8);
+      }
+      mg[j] = __dsqrt_rn(__fma_rn(a, a, __dmul_rn(b, b)));
+      bn[j] = ((iv / WS) * 4 + iu / WS) * 8 + ob;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) {
+      const int s = hl + 16 * j;
+      double a, b;
+      axis_ab(s / W, s % W, a, b);
+      const float x = wrap_two_pi_f(fast_atan2f((float)b, (float)a)) * 5.729577951308232f;
+      int bin;
+      if (!certified_bin(x, 36, bin)) {
+        const int m = min(max(__float2int_rn(x), 0), 36);
+        bin = side_bin(a, b, prm.cb36[m], prm.sb36[m], m, 36);
+        if (bin < 0) bin = bin64(a, b, 0.0, prm.k36, 36);
+      }
+      mg[j] = __dsqrt_rn(__fma_rn(a, a, __dmul_rn(b, b)));
+      bn[j] = bin;
+    }
+    double mx = fmax(fmax(mg[0], mg[1]), fmax(mg[2], mg[3]));
+    const double f36 = fx_scale52_half(mx, hsel);
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) h2_add(h36, 36, bn[j], mg[j], f36);
+    __syncwarp();
+    // argmax with a clear lead over the half's 36 bins (3 per lane)
+    unsigned k1 = 0u, k2 = 0u;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const int bin = hl + 16 * t;
+      const unsigned k = bin < 36 ? ((__float_as_uint((float)h2_get(h36, 36, bin)) & ~63u) | (63u - bin)) : 0u;
+      if (k > k1) { k2 = k1; k1 = k; } else if (k > k2) { k2 = k; }
+    }
+    const unsigned top = half_max_u32(k1, hsel);
+    const unsigned sec = half_max_u32(k1 == top ? k2 : k1, hsel);
+    const float tv = __uint_as_float(top & ~63u), sv = __uint_as_float(sec & ~63u);
+    ok = ok && (sv < tv * 0.99994f);
+    const int hk = 63 - (int)(top & 63u);
+    const double theta0 = prm.theta[hk], ct = prm.cos_t[hk], st = prm.sin_t[hk];
+    const float theta0f = (float)theta0;
+    const double xmin = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, ct >= 0.0 ? -half : half)), __dmul_rn(st, st >= 0.0 ? half : -half));
+    const double xmax = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, ct >= 0.0 ? half : -half)), __dmul_rn(st, st >= 0.0 ? -half : half));
+    const double ymin = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, st >= 0.0 ? -half : half)), __dmul_rn(ct, ct >= 0.0 ? -half : half));
+    const double ymax = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, st >= 0.0 ? half : -half)), __dmul_rn(ct, ct >= 0.0 ? half : -half));
+    int pr0 = max((int)floor(ymin), 1), pr1 = min((int)ceil(ymax), nr - 2);
+    int pc0 = max((int)floor(xmin), 1), pc1 = min((int)ceil(xmax), nc - 2);
+    if (pr0 - 1 < BR || pr1 + 1 >= BR + BX || pc0 - 1 < BC || pc1 + 1 >= BC + BX || pr1 <= pr0 || pc1 <= pc0) {
+      ok = false;  // cannot happen for images >= 16 x 16; keep the addresses inside the box
+      pr0 = BR + 1; pr1 = BR + 2; pc0 = BC + 1; pc1 = BC + 2;
+    }
+    if (!__any_sync(0xffffffffu, ok)) return false;
+    const int xcap = max(pc1 - pc0 - 1, 0), ycap = max(pr1 - pr0 - 1, 0);
+    const double xhi = (double)(nc - 2), yhi = (double)(nr - 2);
+    const double dpc0 = (double)pc0, dpr0 = (double)pr0;
+    const double* pb = stage + (pr0 - 1 - BR) * SP + (pc0 - 1 - BC);
+    const double c0t = ct, s0t = -st;
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) {
+      const int s = hl + 16 * j, iv = s / W, iu = s % W;
+      const double u = (double)iu - half, v = (double)iv - half;
+      const double x = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, u)), __dmul_rn(st, v));
+      const double y = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, u)), __dmul_rn(ct, v));
+      mg[j] = 0.0;
+      bn[j] = 0;
+      if (!(x >= 1.0 && x <= xhi && y >= 1.0 && y <= yhi)) continue;
+      const double lx = __dsub_rn(x, dpc0), ly = __dsub_rn(y, dpr0);
+      const int x0 = max(min((int)floor(lx), xcap), 0), y0 = max(min((int)floor(ly), ycap), 0);
+      const double fxx = __dsub_rn(lx, (double)x0), fyy = __dsub_rn(ly, (double)y0);
+      const double* q = pb + y0 * SP + x0;
+      const double p01 = q[1], p02 = q[2];
+      const double p10 = q[SP], p11 = q[SP + 1], p12 = q[SP + 2], p13 = q[SP + 3];
+      const double p20 = q[2 * SP], p21 = q[2 * SP + 1], p22 = q[2 * SP + 2], p23 = q[2 * SP + 3];
+      const double p31 = q[3 * SP + 1], p32 = q[3 * SP + 2];
+      const double a00 = __dsub_rn(p21, p01), a01 = __dsub_rn(p22, p02);
+      const double a10 = __dsub_rn(p31, p11), a11 = __dsub_rn(p32, p12);
+      const double b00 = __dsub_rn(p12, p10), b01 = __dsub_rn(p13, p11);
+      const double b10 = __dsub_rn(p22, p20), b11 = __dsub_rn(p23, p21);
+      const double sy = __dsub_rn(1.0, fyy), sx = __dsub_rn(1.0, fxx);
+      const double w00 = __dmul_rn(sy, sx), w01 = __dmul_rn(sy, fxx), w10 = __dmul_rn(fyy, sx), w11 = __dmul_rn(fyy, fxx);
+      const double as = __fma_rn(a11, w11, __fma_rn(a10, w10, __fma_rn(a01, w01, __dmul_rn(a00, w00))));
+      const double bs = __fma_rn(b11, w11, __fma_rn(b10, w10, __fma_rn(b01, w01, __dmul_rn(b00, w00))));
+      const float xb = wrap_two_pi_f(fast_atan2f((float)bs, (float)as) - theta0f) * 1.2732395447351628f;
+      int ob;
+      if (!certified_bin(xb, 8, ob)) {
+        const int m = min(max(__float2int_rn(xb), 0), 8);
+        const double ce = __dsub_rn(__dmul_rn(c0t, prm.c8[m]), __dmul_rn(s0t, prm.s8[m]));
+        const double se = __dadd_rn(__dmul_rn(s0t, prm.c8[m]), __dmul_rn(c0t, prm.s8[m]));
+        ob = side_bin(as, bs, ce, se, m, 8);
+        if (ob < 0) ob = bin64(as, bs, theta0, prm.k8, 8);
+      }
+      mg[j] = __dsqrt_rn(__fma_rn(as, as, __dmul_rn(bs, bs)));
+      bn[j] = ((iv / WS) * 4 + iu / WS) * 8 + ob;
+    }
+  }
+  const double fx = fx_scale52_half(fmax(fmax(mg[0], mg[1]), fmax(mg[2], mg[3])), hsel);
+#pragma unroll
+  for (int j = 0; j < SPL; ++j) h2_add(h128, D, bn[j], mg[j], fx);
+  __syncwarp();
+  // L2 normalise, clamp at 0.2, renormalise: lane owns bins 8 hl .. 8 hl + 7
+  const double inv = 1.0 / fx;
+  double v[8];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const uint4 lo = *reinterpret_cast<const uint4*>(h128 + 8 * hl + 4 * t);
+    const uint4 hi = *reinterpret_cast<const uint4*>(h128 + D + 8 * hl + 4 * t);
+    v[4 * t + 0] = __dmul_rn((double)(((unsigned long long)hi.x << kLimb) + lo.x), inv);
+    v[4 * t + 1] = __dmul_rn((double)(((unsigned long long)hi.y << kLimb) + lo.y), inv);
+    v[4 * t + 2] = __dmul_rn((double)(((unsigned long long)hi.z << kLimb) + lo.z), inv);
+    v[4 * t + 3] = __dmul_rn((double)(((unsigned long long)hi.w << kLimb) + lo.w), inv);
+  }
+  double ss = 0.0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) ss = __fma_rn(v[t], v[t], ss);
+#pragma unroll
+  for (int o = 8; o; o >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
+  if (ss > 0.0) {
+    const double r1 = rsqrt(ss);
+    double s2 = 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const double w = __dmul_rn(v[t], r1);
+      v[t] = w < 0.2 ? w : 0.2;
+      s2 = __fma_rn(v[t], v[t], s2);
+    }
+#pragma unroll
+    for (int o = 8; o; o >>= 1) s2 = __dadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, o));
+    const double r2 = rsqrt(s2);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) v[t] = __dmul_rn(v[t], r2);
+  } else {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) v[t] = 0.0;
+  }
+  if (ok) {
+    if (o32) {
+      float4* d = reinterpret_cast<float4*>(o32) + 2 * hl;
+      d[0] = make_float4(__double2float_rn(v[0]), __double2float_rn(v[1]), __double2float_rn(v[2]), __double2float_rn(v[3]));
+      d[1] = make_float4(__double2float_rn(v[4]), __double2float_rn(v[5]), __double2float_rn(v[6]), __double2float_rn(v[7]));
+    }
+    if (o64) {
+      double2* d = reinterpret_cast<double2*>(o64) + 4 * hl;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) d[t] = make_double2(v[2 * t], v[2 * t + 1]);
+    }
+  }
+  __syncwarp();
+  return ok;
+}
+
+constexpr int kPairWarps = 8;
+template <class Img>
+__global__ void __launch_bounds__(kPairWarps * 32, 3) describe_pair_kernel(Img img, int64_t img_stride, int B,
+                                                                           const int32_t* __restrict__ kp_row,
+                                                                           const int32_t* __restrict__ kp_col,
+                                                                           const int32_t* __restrict__ kp_scale,
+                                                                           const int32_t* __restrict__ counts,
+                                                                           int64_t cap, DescParams prm,
+                                                                           float* __restrict__ out32,
+                                                                           double* __restrict__ out64,
+                                                                           int64_t* __restrict__ work,
+                                                                           unsigned long long* __restrict__ n_work) {
+  extern __shared__ double dsm[];
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, hsel = lane >> 4, hl = lane & 15;
+  double* stage = dsm + (2 * wid + hsel) * FastStage::kTotal;
+  unsigned* hw = reinterpret_cast<unsigned*>(dsm + 2 * kPairWarps * FastStage::kTotal) + (2 * wid + hsel) * kFastHist;
+  const int64_t total = (int64_t)B * cap;
+  const int64_t npairs = (total + 1) / 2;
+  const bool box_ok = img.nr >= FastStage::kBox && img.nc >= FastStage::kBox;
+  for (int64_t pi = (int64_t)blockIdx.x * kPairWarps + wid; pi < npairs; pi += (int64_t)gridDim.x * kPairWarps) {
+    const int64_t g = 2 * pi + hsel;  // this half's slot
+    bool live = g < total;
+    int b = 0;
+    if (live) {
+      b = (int)(g / cap);
+      live = !counts || g - (int64_t)b * cap < counts[b];
+    }
+    int row = live ? kp_row[g] : 8, col = live ? kp_col[g] : 8;
+    if (live && (row < 0 || row >= img.nr || col < 0 || col >= img.nc)) live = false;  // validated by the caller
+    bool fast = live && box_ok;
+    if (fast) {
+      if (kp_scale) {
+        const int scale = kp_scale[g];
+        bool f = false;
+        for (int k = 0; k < prm.n_w8; ++k) f |= prm.w8_scale[k] == scale;
+        fast = f;
+      } else {
+        fast = prm.default_w8;
+      }
+    }
+    if (!__any_sync(0xffffffffu, fast)) {  // neither keypoint takes the fast path
+      if (live && hl == 0) work[atomicAdd(n_work, 1ull)] = g;
+      continue;
+    }
+    if (!fast) { row = 8; col = 8; b = 0; }
+    Img im = img;
+    im.p = img.p + (int64_t)b * img_stride * decltype(img)::kElem;
+    const bool ok = describe_pair_w8(im, row, col, fast, prm, hw, stage, out32 ? out32 + g * 128 : nullptr,
+                                     out64 ? out64 + g * 128 : nullptr);
+    if (live && !ok && hl == 0) work[atomicAdd(n_work, 1ull)] = g;  // other sides and near-ties: general kernel
+  }
+}
+
 // 8-bit rasters (grey or RGB): w = 8 keypoints through the fast kernel, the
 // rest (other sides, 36-bin near-ties) queued for the general kernel.
 template <class Img>
@@ -929,14 +1201,27 @@ int launch_fast(const Img& im, const ps_image_batch* img, const ps_keypoints* kp
   if (st) return st;
   unsigned long long* n_work = reinterpret_cast<unsigned long long*>(work + total);
   cudaMemsetAsync(n_work, 0, sizeof(unsigned long long), s);
-  const size_t fshmem = (size_t)kFastWarps * (FastStage::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
-  cudaFuncSetAttribute(describe_fast_u8<Img>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fshmem);
-  int64_t fblocks = (total + kFastWarps - 1) / kFastWarps;
-  if (fblocks > 148 * 16) fblocks = 148 * 16;
-  describe_fast_u8<Img><<<(unsigned)fblocks, kFastWarps * 32, fshmem, s>>>(
-      im, img->image_stride, img->batch, kp->row, kp->col, kp->scale, default_scale, kp->count, kp->cap, prm,
-      out_desc32, out_desc64, work, n_work);
-  PS_LAUNCHED("describe_fast_u8");
+  static const bool pair = getenv("PS_DESCRIBE_SINGLE") == nullptr;  // A/B switch (diagnostic)
+  if (pair) {
+    const size_t pshmem =
+        (size_t)2 * kPairWarps * (FastStage::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
+    cudaFuncSetAttribute(describe_pair_kernel<Img>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pshmem);
+    int64_t pblocks = ((total + 1) / 2 + kPairWarps - 1) / kPairWarps;
+    if (pblocks > 148 * 12) pblocks = 148 * 12;
+    describe_pair_kernel<Img><<<(unsigned)pblocks, kPairWarps * 32, pshmem, s>>>(
+        im, img->image_stride, img->batch, kp->row, kp->col, kp->scale, kp->count, kp->cap, prm, out_desc32,
+        out_desc64, work, n_work);
+    PS_LAUNCHED("describe_pair_kernel");
+  } else {
+    const size_t fshmem = (size_t)kFastWarps * (FastStage::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
+    cudaFuncSetAttribute(describe_fast_u8<Img>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fshmem);
+    int64_t fblocks = (total + kFastWarps - 1) / kFastWarps;
+    if (fblocks > 148 * 16) fblocks = 148 * 16;
+    describe_fast_u8<Img><<<(unsigned)fblocks, kFastWarps * 32, fshmem, s>>>(
+        im, img->image_stride, img->batch, kp->row, kp->col, kp->scale, default_scale, kp->count, kp->cap, prm,
+        out_desc32, out_desc64, work, n_work);
+    PS_LAUNCHED("describe_fast_u8");
+  }
   describe_kernel<Img><<<148 * 2, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,
                                                            kp->scale, default_scale, kp->count, kp->cap, prm,
                                                            out_desc32, out_desc64, work, n_work);
