@@ -926,7 +926,22 @@ __device__ __forceinline__ double fx_scale52_half(double mx, int hsel) {
   return __hiloint2double(be << 20, 0);
 }
 
-template <class Img>
+// Exact bin of a sample whose float32 screen fell near an edge (rare): the
+// side of edge m, else the float64 atan2 path.
+// (ce, se) is the edge direction rotated by theta0 (c0, s0).
+__device__ __forceinline__ int exact_bin(double a, double b, double c0, double s0, double cm, double sm, int m,
+                                      int nbins, double shift, double k, double two_pi) {
+  const double ce = __dsub_rn(__dmul_rn(c0, cm), __dmul_rn(s0, sm));
+  const double se = __dadd_rn(__dmul_rn(s0, cm), __dmul_rn(c0, sm));
+  int bin = side_bin(a, b, ce, se, m, nbins);
+  if (bin < 0) {
+    const double ori = mod_two_pi(__dsub_rn(atan2(b, a), shift), two_pi);
+    bin = min((int)__dmul_rn(ori, k), nbins - 1);
+  }
+  return bin;
+}
+
+template <bool ORIENT, class Img>
 __device__ __forceinline__ bool describe_pair_w8(const Img& im, int row, int col, bool act, const DescParams& prm,
                                                  unsigned* hbase, double* stage, float* __restrict__ o32,
                                                  double* __restrict__ o64) {
@@ -957,14 +972,10 @@ __device__ __forceinline__ bool describe_pair_w8(const Img& im, int row, int col
     a = __dsub_rn(pa[(iv + 2) * SP + iu + 1], pa[iv * SP + iu + 1]);
     b = __dsub_rn(pa[(iv + 1) * SP + iu + 2], pa[(iv + 1) * SP + iu]);
   };
-  auto bin64 = [&](double a, double b, double shift, double k, int nbins) {
-    const double ori = mod_two_pi(__dsub_rn(atan2(b, a), shift), prm.two_pi);
-    return min((int)__dmul_rn(ori, k), nbins - 1);
-  };
   double mg[SPL];
   int bn[SPL];
   bool ok = act;
-  if (!prm.orient) {
+  if constexpr (!ORIENT) {
 #pragma unroll
     for (int j = 0; j < SPL; ++j) {
       const int s = hl + 16 * j, iv = s / W, iu = s % W;
@@ -974,8 +985,7 @@ __device__ __forceinline__ bool describe_pair_w8(const Img& im, int row, int col
       int ob;
       if (!certified_bin(xb, 8, ob)) {
         const int m = min(max(__float2int_rn(xb), 0), 8);
-        ob = side_bin(a, b, prm.c8[m], prm.s8[m], m, 8);
-        if (ob < 0) ob = bin64(a, b, 0.0, prm.k8, 8);
+        ob = exact_bin(a, b, 1.0, 0.0, prm.c8[m], prm.s8[m], m, 8, 0.0, prm.k8, prm.two_pi);
       }
       mg[j] = __dsqrt_rn(__fma_rn(a, a, __dmul_rn(b, b)));
       bn[j] = ((iv / WS) * 4 + iu / WS) * 8 + ob;
@@ -990,8 +1000,7 @@ __device__ __forceinline__ bool describe_pair_w8(const Img& im, int row, int col
       int bin;
       if (!certified_bin(x, 36, bin)) {
         const int m = min(max(__float2int_rn(x), 0), 36);
-        bin = side_bin(a, b, prm.cb36[m], prm.sb36[m], m, 36);
-        if (bin < 0) bin = bin64(a, b, 0.0, prm.k36, 36);
+        bin = exact_bin(a, b, 1.0, 0.0, prm.cb36[m], prm.sb36[m], m, 36, 0.0, prm.k36, prm.two_pi);
       }
       mg[j] = __dsqrt_rn(__fma_rn(a, a, __dmul_rn(b, b)));
       bn[j] = bin;
@@ -1061,10 +1070,7 @@ __device__ __forceinline__ bool describe_pair_w8(const Img& im, int row, int col
       int ob;
       if (!certified_bin(xb, 8, ob)) {
         const int m = min(max(__float2int_rn(xb), 0), 8);
-        const double ce = __dsub_rn(__dmul_rn(c0t, prm.c8[m]), __dmul_rn(s0t, prm.s8[m]));
-        const double se = __dadd_rn(__dmul_rn(s0t, prm.c8[m]), __dmul_rn(c0t, prm.s8[m]));
-        ob = side_bin(as, bs, ce, se, m, 8);
-        if (ob < 0) ob = bin64(as, bs, theta0, prm.k8, 8);
+        ob = exact_bin(as, bs, c0t, s0t, prm.c8[m], prm.s8[m], m, 8, theta0, prm.k8, prm.two_pi);
       }
       mg[j] = __dsqrt_rn(__fma_rn(as, as, __dmul_rn(bs, bs)));
       bn[j] = ((iv / WS) * 4 + iu / WS) * 8 + ob;
@@ -1126,7 +1132,7 @@ __device__ __forceinline__ bool describe_pair_w8(const Img& im, int row, int col
 }
 
 constexpr int kPairWarps = 8;
-template <class Img>
+template <bool ORIENT, class Img>
 __global__ void __launch_bounds__(kPairWarps * 32, 3) describe_pair_kernel(Img img, int64_t img_stride, int B,
                                                                            const int32_t* __restrict__ kp_row,
                                                                            const int32_t* __restrict__ kp_col,
@@ -1172,7 +1178,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, 3) describe_pair_kernel(Img i
     if (!fast) { row = 8; col = 8; b = 0; }
     Img im = img;
     im.p = img.p + (int64_t)b * img_stride * decltype(img)::kElem;
-    const bool ok = describe_pair_w8(im, row, col, fast, prm, hw, stage, out32 ? out32 + g * 128 : nullptr,
+    const bool ok = describe_pair_w8<ORIENT>(im, row, col, fast, prm, hw, stage, out32 ? out32 + g * 128 : nullptr,
                                      out64 ? out64 + g * 128 : nullptr);
     if (live && !ok && hl == 0) work[atomicAdd(n_work, 1ull)] = g;  // other sides and near-ties: general kernel
   }
@@ -1205,12 +1211,13 @@ int launch_fast(const Img& im, const ps_image_batch* img, const ps_keypoints* kp
   if (pair) {
     const size_t pshmem =
         (size_t)2 * kPairWarps * (FastStage::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
-    cudaFuncSetAttribute(describe_pair_kernel<Img>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pshmem);
+    auto kern = prm.orient ? describe_pair_kernel<true, Img> : describe_pair_kernel<false, Img>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pshmem);
     int64_t pblocks = ((total + 1) / 2 + kPairWarps - 1) / kPairWarps;
     if (pblocks > 148 * 12) pblocks = 148 * 12;
-    describe_pair_kernel<Img><<<(unsigned)pblocks, kPairWarps * 32, pshmem, s>>>(
-        im, img->image_stride, img->batch, kp->row, kp->col, kp->scale, kp->count, kp->cap, prm, out_desc32,
-        out_desc64, work, n_work);
+    kern<<<(unsigned)pblocks, kPairWarps * 32, pshmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,
+                                                             kp->scale, kp->count, kp->cap, prm, out_desc32,
+                                                             out_desc64, work, n_work);
     PS_LAUNCHED("describe_pair_kernel");
   } else {
     const size_t fshmem = (size_t)kFastWarps * (FastStage::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
