@@ -519,6 +519,12 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total, det_ms, des_ms = t.tolist()
     ms_step = ms_total / args.steps
+    # output sanity (not a parity test -- tests/ does that): every described
+    # keypoint row is unit-norm, so a failed launch cannot pass as a fast one
+    nrm = desc[:, : min(K, 4096)].double().norm(dim=-1)
+    bad = int(((nrm - 1.0).abs() > 1e-5).sum())
+    if bad:
+        raise RuntimeError(f"describe produced {bad} non-unit descriptor rows")
     total_px = args.images * NR * NC
     value = total_px / 1e6 / (ms_step / 1e3)
 
