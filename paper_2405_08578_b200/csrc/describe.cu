@@ -1207,7 +1207,7 @@ int launch_fast(const Img& im, const ps_image_batch* img, const ps_keypoints* kp
   if (st) return st;
   unsigned long long* n_work = reinterpret_cast<unsigned long long*>(work + total);
   cudaMemsetAsync(n_work, 0, sizeof(unsigned long long), s);
-  static const bool pair = getenv("PS_DESCRIBE_SINGLE") == nullptr;  // A/B switch (diagnostic)
+  const bool pair = getenv("PS_DESCRIBE_SINGLE") == nullptr;  // A/B switch (diagnostic, read per call)
   if (pair) {
     const size_t pshmem =
         (size_t)2 * kPairWarps * (FastStage::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));

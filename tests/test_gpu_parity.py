@@ -618,3 +618,26 @@ def test_rgb_table_and_formula_modes_agree():
     assert torch.equal(d1, d2)
     g = ingest.to_grayscale_device(t)[0].cpu().numpy()
     assert np.array_equal(g, scenes.gray_bt601(a))
+
+
+def test_describe_pair_and_single_kernels_agree(monkeypatch):
+    """The two-keypoints-per-warp kernel and the one-keypoint kernel compute
+    the same descriptors (to float64 rounding) -- on a full C2 image (even
+    counts) and on a deduplicated multi-scale list with an odd count (a
+    half-idle last warp)."""
+    img = scenes.scene(640, 960, 3)
+    t = torch.from_numpy(img).cuda()
+    cfg = R.DescriptorConfig(0.0625, 4, 64, True)
+    for scales, meta in (((8, 16, 32), False), ((8, 12, 24), True)):
+        kp = device.detect(t, scales, meta=meta)
+        if meta and int(kp.count[0]) % 2 == 0:
+            kp.count[0] -= 1  # an odd count: the last warp has one live half
+        monkeypatch.delenv("PS_DESCRIBE_SINGLE", raising=False)
+        d_pair = device.describe(t, kp, cfg, scale_set=kp.scale_set, out64=True, out32=False)
+        monkeypatch.setenv("PS_DESCRIBE_SINGLE", "1")
+        d_one = device.describe(t, kp, cfg, scale_set=kp.scale_set, out64=True, out32=False)
+        n = int(kp.count[0])
+        a, b = d_pair[0, :n], d_one[0, :n]
+        rel = (a - b).abs().amax(dim=-1) / b.norm(dim=-1).clamp_min(1e-300)
+        assert float(rel.max()) <= 1e-12, (scales, float(rel.max()))
+        assert torch.all((a.norm(dim=-1) - 1).abs() < 1e-9)
