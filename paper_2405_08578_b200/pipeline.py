@@ -248,21 +248,30 @@ def alloc_host_features(batch: int, nr: int, nc: int, cfg: PipelineConfig) -> Ho
 
 
 class BatchPreparer:
-    """Host-to-host detect + describe of many same-sized 8-bit images.
+    """Host-to-host detect + describe of many same-sized 8-bit images (grey
+    [B, nr, nc], or RGB [B, nr, nc, 3] with ``rgb=True``: BT.601 grey on the
+    device).
 
     Chunks of ``chunk`` images flow through a 3-deep stream pipeline: the
     host->device copy of chunk i+1 and the device->host copy of chunk i-1
     overlap the kernels of chunk i.  Device buffers are allocated once.
     """
 
-    def __init__(self, nr: int, nc: int, cfg: PipelineConfig, chunk: int = 8, depth: int = 3, device_id=None):
+    def __init__(self, nr: int, nc: int, cfg: PipelineConfig, chunk: int = 8, depth: int = 3, device_id=None,
+                 rgb: bool = False):
         self.cfg, self.nr, self.nc, self.chunk, self.depth = cfg, nr, nc, chunk, depth
         self.alpha = cfg.alpha if cfg.alpha is not None else default_alpha(nr, nc)
         self.sizes = cfg.scale_set().sizes
         self.dcfg = cfg.descriptor_config()
         dev = torch.device("cuda", torch.cuda.current_device() if device_id is None else device_id)
         self.streams = [torch.cuda.Stream(dev) for _ in range(depth)]
-        self.img = [torch.empty((chunk, nr, nc), dtype=torch.uint8, device=dev) for _ in range(depth)]
+        shape = (chunk, nr, nc, 3) if rgb else (chunk, nr, nc)
+        self.img = [torch.empty(shape, dtype=torch.uint8, device=dev) for _ in range(depth)]
+        self.kind, self.lut = "u8", None
+        if rgb:
+            from .ingest import gray_source
+
+            self.kind, self.lut = "rgb8", gray_source(dev)
         K = alloc_plan_cap(nr, nc, cfg)
         D = cfg.d * cfg.d * 8
         self.desc = [torch.empty((chunk, K, D), dtype=torch.float32, device=dev) for _ in range(depth)]
@@ -281,7 +290,7 @@ class BatchPreparer:
                 done[slot].synchronize()  # slot's previous D2H finished -> buffers reusable
             with torch.cuda.stream(s):
                 self.img[slot][:n].copy_(host_images[b0:b1], non_blocking=True)
-                dimg = device.DeviceImages(self.img[slot][:n], "u8", self.alpha)
+                dimg = device.DeviceImages(self.img[slot][:n], self.kind, self.alpha, self.lut)
                 kp = device.detect(dimg, self.sizes, dedupe=True, meta=False, stream=s)
                 d32 = self.desc[slot][:n]
                 device.describe_into(dimg, kp, self.dcfg, d32, scale_set=kp.scale_set, stream=s)
@@ -301,9 +310,11 @@ class BatchPreparer:
 
 
 def prepare_batch_host(host_images, cfg: PipelineConfig, out: HostFeatures | None = None, chunk: int = 8):
-    """Host 8-bit images [B, nr, nc] -> host keypoints + float32 descriptors."""
+    """Host 8-bit images [B, nr, nc] (or RGB [B, nr, nc, 3]) -> host keypoints
+    + float32 descriptors."""
     t = host_images if isinstance(host_images, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(host_images))
-    B, nr, nc = t.shape
+    rgb = t.dim() == 4
+    B, nr, nc = t.shape[:3]
     if out is None:
         out = alloc_host_features(B, nr, nc, cfg)
-    return BatchPreparer(nr, nc, cfg, chunk=chunk).run(t, out)
+    return BatchPreparer(nr, nc, cfg, chunk=chunk, rgb=rgb).run(t, out)

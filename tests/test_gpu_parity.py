@@ -641,3 +641,25 @@ def test_describe_pair_and_single_kernels_agree(monkeypatch):
         rel = (a - b).abs().amax(dim=-1) / b.norm(dim=-1).clamp_min(1e-300)
         assert float(rel.max()) <= 1e-12, (scales, float(rel.max()))
         assert torch.all((a.norm(dim=-1) - 1).abs() < 1e-9)
+
+
+def test_host_batch_pipeline_grey_and_rgb():
+    """pipeline.prepare_batch_host (pinned host in/out, 3-stream pipeline) gives
+    the device path's keypoints and descriptors, for grey and RGB batches
+    (5 images, chunk 2: partial last chunk, slot reuse)."""
+    from paper_2405_08578_b200 import pipeline as PL
+
+    cfg = PL.PipelineConfig(window_min=16, window_max=64)
+    grey = np.stack([scenes.scene(200, 288, s) for s in range(5)])
+    rgb = np.stack([np.stack([scenes.scene(200, 288, 10 * s + c) for c in range(3)], axis=-1) for s in range(5)])
+    for imgs in (grey, rgb):
+        out = PL.prepare_batch_host(torch.from_numpy(imgs).pin_memory(), cfg, chunk=2)
+        dimg = device.as_device_images(torch.from_numpy(imgs).cuda(), rgb=imgs.ndim == 4)
+        kp = device.detect(dimg, cfg.scale_set().sizes, meta=False)
+        d = device.describe(dimg, kp, cfg.descriptor_config(), scale_set=kp.scale_set)
+        for b in range(5):
+            n = int(out.count[b])
+            assert n == int(kp.count[b])
+            assert np.array_equal(out.row[b, :n].numpy(), kp.row[b, :n].cpu().numpy())
+            assert np.array_equal(out.value[b, :n].numpy(), kp.value[b, :n].cpu().numpy())
+            assert np.array_equal(out.descriptors[b, :n].numpy(), d[b, :n].cpu().numpy())
