@@ -322,6 +322,51 @@ def bench_c3_composite(args, rank, dev, with_cpu, steps=5):
 
 
 # ---------------------------------------------------------------------------
+# K4 RANSAC: hypothesis-pair evaluations per second
+# ---------------------------------------------------------------------------
+
+def bench_ransac(args, rank, dev, with_cpu, n=1000, iters=2000, steps=5):
+    """Seeded correspondences (60 % inliers of a rigid motion + 1 px noise,
+    40 % uniform outliers): iterations x n transfer errors per call."""
+    import torch
+
+    from paper_2405_08578_b200 import device
+
+    if rank != 0:
+        return None
+    rng = np.random.default_rng(7)
+    src = rng.uniform(0, 1000, size=(n, 2))
+    th, t = 0.2, np.array([35.0, -12.0])
+    R = np.array([[math.cos(th), -math.sin(th)], [math.sin(th), math.cos(th)]])
+    dst = src @ R.T + t + rng.normal(0, 1.0, size=(n, 2))
+    out = rng.random(n) < 0.4
+    dst[out] = rng.uniform(0, 1000, size=(int(out.sum()), 2))
+    s_d, d_d = torch.from_numpy(src).to(dev), torch.from_numpy(dst).to(dev)
+    for _ in range(2):
+        device.ransac(s_d, d_d, iters, 3.0, 8, 0)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        r = device.ransac(s_d, d_d, iters, 3.0, 8, 0)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / steps
+    res = {"metric": "RANSAC hypothesis-pair evaluations/s (2-point rigid, n=1000, 2000 iterations)",
+           "value": round(iters * n / dt, 1), "unit": "evaluations/s", "ms_per_call": round(dt * 1e3, 4),
+           "consensus": int(r.consensus), "inliers": int(len(r.inliers)),
+           "timing": "host wall clock per device.ransac call (includes the host PCG64 sample stream and the "
+                     "result read-back), CUDA-synchronized"}
+    if with_cpu:
+        from oracle import lpsift_oracle as O
+
+        t0 = time.perf_counter()
+        O.ransac(src, dst, iters, 3.0, 8, 0)
+        c = time.perf_counter() - t0
+        res["cpu_baseline"] = {"value": round(iters * n / c, 1), "unit": "evaluations/s", "cores": 1,
+                               "kind": "port", "sample": "the same call, numpy oracle port, one process"}
+    return res
+
+
+# ---------------------------------------------------------------------------
 # C5 illumination pairs (BASELINE.json configs[4]): pairs/s
 # ---------------------------------------------------------------------------
 
@@ -591,6 +636,10 @@ def run_ours(args):
     if not args.no_composite:
         composite = bench_c3_composite(args, rank, dev, with_cpu=(not args.no_cpu and world == 1))
 
+    ransac_k4 = None
+    if not args.no_pairs:
+        ransac_k4 = bench_ransac(args, rank, dev, with_cpu=(not args.no_cpu and world == 1))
+
     pairs5 = None
     if not args.no_pairs:
         pairs5 = bench_c5_pairs(args, world, rank, dev)
@@ -611,7 +660,7 @@ def run_ours(args):
                        "keypoints_per_image": K, "descriptor": "float32 128-d", "l2": "inputs larger than L2",
                        "parallelism": f"images sharded over {world} rank(s)"},
             "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "matching_c4": matching,
-            "stitch_c3": stitch, "composite_c3": composite, "pairs_c5": pairs5,
+            "stitch_c3": stitch, "composite_c3": composite, "pairs_c5": pairs5, "ransac_k4": ransac_k4,
             "gpu_launches": int(launches), "clocks": clocks,
         }
         print(json.dumps(out), flush=True)
