@@ -66,9 +66,10 @@ class PairwiseTransformTable:
 class GpuEngine:
     """Hot path on the local GPU through the C-ABI (device.py)."""
 
-    def __init__(self, cfg):
+    def __init__(self, cfg, pair_workers: int = 1):
         self.cfg = cfg
         self.device = torch.device("cuda", torch.cuda.current_device())
+        self.pair_workers = pair_workers  # concurrent pair registrations (host threads, one stream each)
 
     def comm_device(self):
         return self.device
@@ -157,14 +158,40 @@ def build_pairwise_table(images: Sequence, cfg, *, engine=None, group=None) -> P
         r, s = k % world, k // world
         return g_rows[r, s], g_cols[r, s], g_desc[r, s], int(g_cnt[r, s])
 
-    # phase 2: pairs in reference order, round-robin over ranks
+    # phase 2: pairs in reference order, round-robin over ranks; on a GPU the
+    # rank's pairs run concurrently on a few streams (each pair's small
+    # kernels and count read-backs overlap the others')
     jobs = [(a, b) for a in range(n) for b in range(a + 1, n)]
     res = torch.zeros((len(jobs), 5), dtype=torch.float64, device=dev)
-    for q in range(rank, len(jobs), world):
+    mine_q = list(range(rank, len(jobs), world))
+
+    def run(q):
         a, b = jobs[q]
         ra, ca, da, na = img(a)
         rb, cb, db, nb = img(b)
-        ok, th, tx, ty, ni = engine.register(ra, ca, da, na, rb, cb, db, nb, pair_seed(cfg.seed, a, b))
+        return engine.register(ra, ca, da, na, rb, cb, db, nb, pair_seed(cfg.seed, a, b))
+
+    workers = getattr(engine, "pair_workers", 1)
+    if workers > 1 and len(mine_q) > 1:
+        import threading
+        from concurrent.futures import ThreadPoolExecutor
+
+        local = threading.local()
+        torch.cuda.current_stream(dev).synchronize()  # gathered slots ready before other streams read them
+
+        def run_on_stream(q):
+            if not hasattr(local, "stream"):
+                local.stream = torch.cuda.Stream(dev)
+            with torch.cuda.stream(local.stream):
+                out = run(q)
+            local.stream.synchronize()
+            return out
+
+        with ThreadPoolExecutor(max_workers=workers) as ex:
+            outs = list(ex.map(run_on_stream, mine_q))
+    else:
+        outs = [run(q) for q in mine_q]
+    for q, (ok, th, tx, ty, ni) in zip(mine_q, outs):
         res[q] = torch.tensor([float(ok), th, tx, ty, float(ni)], dtype=torch.float64)
     # gather: each pair was computed by exactly one rank, the others hold zeros
     allres = _all_gather(res, world, group).sum(dim=0).cpu().numpy()
