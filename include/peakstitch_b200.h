@@ -186,6 +186,15 @@ PS_API int ps_ransac_rigid(const double* src_xy, const double* dst_xy, int64_t n
                     int32_t min_inliers, double* out_model, uint8_t* out_mask,
                     int64_t* out_info, double* out_rms, void* workspace,
                     size_t workspace_bytes, void* stream);
+/* The reference's RANSAC index stream (registration.py:164, 170-173) on the
+ * device: numpy's PCG64 state (Generator.bit_generator.state: 128-bit state
+ * and increment as hi/lo words, has_uint32, uinteger) -> out_samples[2*iters]
+ * = (i, j) per iteration, bit-identical to the scalar draws
+ * rng.integers(0, n), rng.integers(0, n - 1), j += j >= i.  scratch: one
+ * device int32.  2 <= n < 2^31. */
+PS_API int ps_ransac_samples(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
+                             int32_t has_uint32, uint32_t uinteger, int64_t n, int32_t iterations,
+                             int32_t* out_samples, int32_t* scratch, void* stream);
 /* Least-squares rigid fit of dst ~ H(src) over all n points; out_info[0] is
  * PS_OK or PS_ERR_DEGENERATE. */
 PS_API int ps_estimate_rigid(const double* src_xy, const double* dst_xy, int64_t n,

@@ -317,6 +317,22 @@ def sample_stream(seed: int, n: int, iterations: int) -> np.ndarray:
     return v.astype(np.int32)
 
 
+def sample_stream_device(seed: int, n: int, iterations: int, device=None, stream=None) -> torch.Tensor:
+    """The same stream generated on the GPU (ps_ransac_samples): only the
+    seeded PCG64 state comes from numpy (SeedSequence seeding on the host),
+    the draws -- jump-ahead per iteration, Lemire bounds, exact sequential
+    replay when a rejection occurs -- run on the device.  int32 [iters, 2]."""
+    st = np.random.default_rng(seed).bit_generator.state
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    m64 = (1 << 64) - 1
+    out = torch.empty(2 * iterations + 1, dtype=torch.int32, device=device or "cuda")
+    _lib.check(_lib.lib().ps_ransac_samples(s >> 64, s & m64, inc >> 64, inc & m64, int(st["has_uint32"]),
+                                            int(st["uinteger"]), int(n), int(iterations), _ptr(out),
+                                            C.c_void_p(out.data_ptr() + 8 * iterations),
+                                            C.c_void_p(_stream_ptr(stream))), "ransac_samples")
+    return out[: 2 * iterations].view(iterations, 2)
+
+
 @dataclass
 class RansacOutcome:
     ok: bool
@@ -342,7 +358,7 @@ def ransac(src: torch.Tensor, dst: torch.Tensor, iterations=2000, inlier_tol=3.0
     dev = src.device
     src = src.to(torch.float64).contiguous()
     dst = dst.to(torch.float64).contiguous()
-    samples = torch.from_numpy(sample_stream(seed, n, iterations)).to(dev, non_blocking=True)
+    samples = sample_stream_device(seed, n, iterations, dev, stream)
     L = _lib.lib()
     wsb = C.c_size_t()
     _lib.check(L.ps_ransac_plan(n, iterations, C.byref(wsb)), "ransac")

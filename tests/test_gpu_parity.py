@@ -663,3 +663,15 @@ def test_host_batch_pipeline_grey_and_rgb():
             assert np.array_equal(out.row[b, :n].numpy(), kp.row[b, :n].cpu().numpy())
             assert np.array_equal(out.value[b, :n].numpy(), kp.value[b, :n].cpu().numpy())
             assert np.array_equal(out.descriptors[b, :n].numpy(), d[b, :n].cpu().numpy())
+
+
+@pytest.mark.parametrize("n", [2, 3, 8, 97, 1000, 65537, 3 * 2**29 + 5, 2**31 - 1])
+def test_sample_stream_on_device_matches_numpy(n):
+    """ps_ransac_samples reproduces numpy's PCG64 bounded draws exactly --
+    the jump-ahead fast path and the sequential replay (n = 2: one-value
+    ranges consume nothing; n near 2^31: frequent Lemire rejections)."""
+    for seed in (0, 1, 99, 2**40 + 7):
+        for iters in (1, 7, 2000):
+            want = device.sample_stream(seed, n, iters)
+            got = device.sample_stream_device(seed, n, iters).cpu().numpy()
+            assert np.array_equal(got, want), (n, seed, iters)
