@@ -36,6 +36,8 @@ struct DescParams {
   double c8[9], s8[9];                      // cos/sin of m*pi/4 (8-bin edges relative to theta0)
   int n_w8, w8_scale[kMaxDescScales];       // scales whose region side is 8 (fast path, d = 4)
   int default_w8;                           // the default scale is one of them
+  int n_w16, w16_scale[kMaxDescScales];     // ... region side 16
+  int default_w16;
 };
 
 // numpy mod(x, 2*pi) for -4*pi < x < 2*pi (descriptor.py:138, 215): fmod is
@@ -166,12 +168,25 @@ constexpr int kStageDoubles = Stage<kStageW>::kTotal;
 // doubles: axis reads of a half-warp hit 16 distinct 8-byte banks) that holds
 // both the axis region and every rotated patch; the rotated samples form
 // their gradient-field corners from it directly.
-struct FastStage {
+template <int W>
+struct FastBox;
+template <>
+struct FastBox<8> {
   static constexpr int kBox = 16;        // staged P box side
+  static constexpr int kOff = 7;         // box starts at floor(cy) - kOff (clamped)
   static constexpr int SPP = 24;
-  static constexpr int kP = kBox * SPP;  // 384
-  static constexpr int kTotal = kP;      // doubles per warp
+  static constexpr int kTotal = kBox * SPP;  // doubles per keypoint
 };
+// w = 16 (the reference's default 32..128 windows): the axis region spans
+// 18 rows and a rotated patch lies within cy -/+ (7.5 sqrt(2) + 2).
+template <>
+struct FastBox<16> {
+  static constexpr int kBox = 26;
+  static constexpr int kOff = 12;
+  static constexpr int SPP = 26;
+  static constexpr int kTotal = kBox * SPP;
+};
+using FastStage = FastBox<8>;
 
 // ---- float32 screening of the discrete decisions -------------------------------
 // On 8-bit rasters the gradients (exact float64 differences of the ramped
@@ -520,24 +535,27 @@ __device__ __forceinline__ float fast_atan2f(float y, float x) {
 // 2^e chosen per keypoint from the largest magnitude so a bin sum stays
 // below 2^52: quantum ~2^-46 of the largest bin -- far below float32
 // resolution, so near-identical regions keep distinct descriptors (F6).
-constexpr int kLimb = 26;
+constexpr int kLimb = 26;  // w = 8: 64 samples; w = 16 (256 samples) uses 24-bit limbs
+template <int L = kLimb>
 __device__ __forceinline__ void h2_add(unsigned* h, int nb, int bin, double mag, double fx) {
   if (!(mag > 0.0)) return;
   const unsigned long long q = __double2ull_rn(__dmul_rn(mag, fx));
-  atomicAdd(h + bin, (unsigned)(q & ((1u << kLimb) - 1u)));
-  atomicAdd(h + nb + bin, (unsigned)(q >> kLimb));
+  atomicAdd(h + bin, (unsigned)(q & ((1u << L) - 1u)));
+  atomicAdd(h + nb + bin, (unsigned)(q >> L));
 }
+template <int L = kLimb>
 __device__ __forceinline__ unsigned long long h2_get(const unsigned* h, int nb, int bin) {
-  return ((unsigned long long)h[nb + bin] << kLimb) + (unsigned long long)h[bin];
+  return ((unsigned long long)h[nb + bin] << L) + (unsigned long long)h[bin];
 }
 // Warp-uniform fixed-point scale from the lanes' largest magnitudes: the max
 // of the (non-negative) doubles' high words (one REDUX) bounds the exponent eb,
 // every magnitude is < 2^(eb - 1022) and a bin sum of NS = 64 of them is
 // < 2^(eb - 1016), so 2^(1068 - eb) keeps every sum below 2^52.
+template <int LOG = 6>  // log2(samples per keypoint)
 __device__ __forceinline__ double fx_scale52_warp(double mx) {
   const unsigned eb = __reduce_max_sync(0xffffffffu, (unsigned)__double2hiint(mx)) >> 20;
   if (eb == 0u) return 1.0;  // all magnitudes zero (or subnormal)
-  const int be = min(2091 - (int)eb, 2046);
+  const int be = min(2097 - LOG - (int)eb, 2046);  // 2^(52 - (eb - 1022 + LOG)), biased
   return __hiloint2double(be << 20, 0);
 }
 
@@ -545,13 +563,13 @@ template <int W, class Img>
 __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, int col, const DescParams& prm,
                                                        unsigned* hbase, double* stage, float* __restrict__ o32,
                                                        double* __restrict__ o64) {
-  static_assert(W == kStageW, "fast path is staged");
-  static_assert(W * W == 64, "fx_scale52_warp assumes 64 samples");
-  constexpr int NS = W * W, SPL = NS / 32, D = 128, SP = FastStage::SPP;
+  static_assert(W == 8 || W == 16, "fast path: w = 8 or 16");
+  constexpr int NS = W * W, SPL = NS / 32, D = 128, SP = FastBox<W>::SPP;
+  constexpr int LOG = W == 8 ? 6 : 8, LIMB = 32 - LOG;  // limb sums of NS samples stay below 2^32
   constexpr int WS = W / 4;
   const int lane = threadIdx.x & 31;
   const int nr = im.nr, nc = im.nc;
-  constexpr int BX = FastStage::kBox;
+  constexpr int BX = FastBox<W>::kBox;
   const int r0 = min(max(row - W / 2, 1), nr - 1 - W);
   const int c0 = min(max(col - W / 2, 1), nc - 1 - W);
   constexpr double half = (double)(W - 1) / 2.0;
@@ -561,18 +579,29 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
   const int cx2 = min(max(2 * col, 2 + (W - 1)), 2 * (nc - 2) - (W - 1));
   const double cy = 0.5 * (double)cy2, cx = 0.5 * (double)cx2;
   // One staged box for both phases: the axis region spans rows r0-1..r0+W and
-  // any rotated patch pr0-1..pr1+1 lies within cy -/+ (3.5 sqrt(2) + 2), so
-  // rows floor(cy)-7 .. floor(cy)+8 (clamped to the image) hold both.
-  const int BR = max(0, min((cy2 >> 1) - 7, nr - BX)), BC = max(0, min((cx2 >> 1) - 7, nc - BX));
+  // any rotated patch pr0-1..pr1+1 lies within cy -/+ ((W-1)/2 sqrt(2) + 2), so
+  // rows floor(cy)-kOff .. floor(cy)-kOff+BX-1 (clamped to the image) hold both.
+  constexpr int OFF = FastBox<W>::kOff;
+  const int BR = max(0, min((cy2 >> 1) - OFF, nr - BX)), BC = max(0, min((cx2 >> 1) - OFF, nc - BX));
   unsigned* h128 = hbase;         // [2][128]
   unsigned* h36 = hbase + 2 * D;  // [2][36]
   static_assert((2 * (D + 36)) % 4 == 0, "vector zeroing");
   for (int q = lane; q < 2 * (D + 36) / 4; q += 32) reinterpret_cast<uint4*>(hbase)[q] = make_uint4(0u, 0u, 0u, 0u);
-  const int sx_ = lane & 15, sy_ = lane >> 4;
-  if constexpr (std::is_same<Img, RampRGB8>::value)
-    stage_box_rgb8<BX / 2>(im, stage, SP, BR, BC, BX, BX, sx_, sy_);
-  else
-    stage_box_u8<BX / 2>(im, stage, SP, BR, BC, BX, BX, sx_, sy_);
+  if constexpr (W == 8) {  // 16 columns: half-warps take alternate rows
+    const int sx_ = lane & 15, sy_ = lane >> 4;
+    if constexpr (std::is_same<Img, RampRGB8>::value)
+      stage_box_rgb8<BX / 2>(im, stage, SP, BR, BC, BX, BX, sx_, sy_);
+    else
+      stage_box_u8<BX / 2>(im, stage, SP, BR, BC, BX, BX, sx_, sy_);
+  } else {  // 26 columns: lane = column, even rows then odd rows
+#pragma unroll
+    for (int sy = 0; sy < 2; ++sy) {
+      if constexpr (std::is_same<Img, RampRGB8>::value)
+        stage_box_rgb8<BX / 2>(im, stage, SP, BR, BC, BX, BX, lane, sy);
+      else
+        stage_box_u8<BX / 2>(im, stage, SP, BR, BC, BX, BX, lane, sy);
+    }
+  }
   __syncwarp();
   const double* pa = stage + (r0 - 1 - BR) * SP + (c0 - 1 - BC);  // axis region origin
   auto axis_ab = [&](int iv, int iu, double& a, double& b) {
@@ -623,12 +652,12 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
     double mx = mg[0];
 #pragma unroll
     for (int j = 1; j < SPL; ++j) mx = fmax(mx, mg[j]);
-    const double f36 = fx_scale52_warp(mx);
+    const double f36 = fx_scale52_warp<LOG>(mx);
 #pragma unroll
-    for (int j = 0; j < SPL; ++j) h2_add(h36, 36, bn[j], mg[j], f36);
+    for (int j = 0; j < SPL; ++j) h2_add<LIMB>(h36, 36, bn[j], mg[j], f36);
     __syncwarp();
     // argmax with a clear lead (else the whole keypoint is redone in float64)
-    const unsigned long long v1 = h2_get(h36, 36, lane), v2 = lane < 4 ? h2_get(h36, 36, lane + 32) : 0ull;
+    const unsigned long long v1 = h2_get<LIMB>(h36, 36, lane), v2 = lane < 4 ? h2_get<LIMB>(h36, 36, lane + 32) : 0ull;
     const unsigned k1 = (__float_as_uint((float)v1) & ~63u) | (63u - lane);
     const unsigned k2 = lane < 4 ? ((__float_as_uint((float)v2) & ~63u) | (31u - lane)) : 0u;
     const unsigned top = __reduce_max_sync(0xffffffffu, max(k1, k2));
@@ -711,9 +740,9 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
   double mx = mg[0];
 #pragma unroll
   for (int j = 1; j < SPL; ++j) mx = fmax(mx, mg[j]);
-  const double fx = fx_scale52_warp(mx);
+  const double fx = fx_scale52_warp<LOG>(mx);
 #pragma unroll
-  for (int j = 0; j < SPL; ++j) h2_add(h128, D, bn[j], mg[j], fx);
+  for (int j = 0; j < SPL; ++j) h2_add<LIMB>(h128, D, bn[j], mg[j], fx);
   __syncwarp();
   // --- L2 normalise, clamp at 0.2, renormalise (descriptor.py:250-255).
   // Lane l owns bins 4l..4l+3 (one 16-byte shared load per limb array, one
@@ -723,10 +752,10 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
     const double inv = 1.0 / fx;  // exact (power of two)
     const uint4 lo = *reinterpret_cast<const uint4*>(h128 + 4 * lane);
     const uint4 hi = *reinterpret_cast<const uint4*>(h128 + D + 4 * lane);
-    double v0 = __dmul_rn((double)(((unsigned long long)hi.x << kLimb) + lo.x), inv);
-    double v1 = __dmul_rn((double)(((unsigned long long)hi.y << kLimb) + lo.y), inv);
-    double v2 = __dmul_rn((double)(((unsigned long long)hi.z << kLimb) + lo.z), inv);
-    double v3 = __dmul_rn((double)(((unsigned long long)hi.w << kLimb) + lo.w), inv);
+    double v0 = __dmul_rn((double)(((unsigned long long)hi.x << LIMB) + lo.x), inv);
+    double v1 = __dmul_rn((double)(((unsigned long long)hi.y << LIMB) + lo.y), inv);
+    double v2 = __dmul_rn((double)(((unsigned long long)hi.z << LIMB) + lo.z), inv);
+    double v3 = __dmul_rn((double)(((unsigned long long)hi.w << LIMB) + lo.w), inv);
     double ss = __dadd_rn(__dadd_rn(__dmul_rn(v0, v0), __dmul_rn(v1, v1)), __dadd_rn(__dmul_rn(v2, v2), __dmul_rn(v3, v3)));
 #pragma unroll
     for (int o = 16; o; o >>= 1) ss = __dadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, o));
@@ -827,8 +856,8 @@ constexpr int kFastWarps = 8;
 #endif
 constexpr int kFastHist = 2 * (128 + 36);
 
-template <class Img>
-__global__ void __launch_bounds__(kFastWarps * 32, PS_FAST_MINB) describe_fast_u8(Img img, int64_t img_stride, int B,
+template <int W, class Img>
+__global__ void __launch_bounds__(kFastWarps * 32, W == 8 ? PS_FAST_MINB : 3) describe_fast_u8(Img img, int64_t img_stride, int B,
                                                                        const int32_t* __restrict__ kp_row,
                                                                        const int32_t* __restrict__ kp_col,
                                                                        const int32_t* __restrict__ kp_scale,
@@ -840,8 +869,11 @@ __global__ void __launch_bounds__(kFastWarps * 32, PS_FAST_MINB) describe_fast_u
                                                                        unsigned long long* __restrict__ n_work) {
   extern __shared__ double dsm[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* stage = dsm + wid * FastStage::kTotal;
-  unsigned* hw = reinterpret_cast<unsigned*>(dsm + kFastWarps * FastStage::kTotal) + wid * kFastHist;
+  constexpr int BX = FastBox<W>::kBox;
+  double* stage = dsm + wid * FastBox<W>::kTotal;
+  unsigned* hw = reinterpret_cast<unsigned*>(dsm + kFastWarps * FastBox<W>::kTotal) + wid * kFastHist;
+  const int n_fast = W == 8 ? prm.n_w8 : prm.n_w16;
+  const int* fast_scale = W == 8 ? prm.w8_scale : prm.w16_scale;
   const int64_t total = (int64_t)B * cap;
   const int64_t S = (int64_t)gridDim.x * kFastWarps;
   // grid-stride over (image b, slot i); (b, i) advance without a division
@@ -858,16 +890,16 @@ __global__ void __launch_bounds__(kFastWarps * 32, PS_FAST_MINB) describe_fast_u
     im.p = img.p + (int64_t)b * img_stride * decltype(img)::kElem;
     const int row = kp_row[g], col = kp_col[g];
     if (row < 0 || row >= im.nr || col < 0 || col >= im.nc) continue;  // validated by the caller
-    bool fast = prm.default_w8 && im.nr >= FastStage::kBox && im.nc >= FastStage::kBox;
+    bool fast = (W == 8 ? prm.default_w8 : prm.default_w16) && im.nr >= BX && im.nc >= BX;
     if (kp_scale) {
       const int scale = kp_scale[g];
       fast = false;
-      for (int k = 0; k < prm.n_w8; ++k) fast |= prm.w8_scale[k] == scale;
-      fast &= im.nr >= FastStage::kBox && im.nc >= FastStage::kBox;
+      for (int k = 0; k < n_fast; ++k) fast |= fast_scale[k] == scale;
+      fast &= im.nr >= BX && im.nc >= BX;
     }
     bool ok = false;
     if (fast)
-      ok = describe_keypoint_w8u8<8>(im, row, col, prm, hw, stage, out32 ? out32 + g * 128 : nullptr,
+      ok = describe_keypoint_w8u8<W>(im, row, col, prm, hw, stage, out32 ? out32 + g * 128 : nullptr,
                                      out64 ? out64 + g * 128 : nullptr);
     if (!ok && lane == 0) work[atomicAdd(n_work, 1ull)] = g;  // other sides and near-ties: general kernel
   }
@@ -1190,6 +1222,16 @@ template <class Img>
 int launch_fast(const Img& im, const ps_image_batch* img, const ps_keypoints* kp, int32_t default_scale,
                 const DescParams& prm, float* out_desc32, double* out_desc64, int64_t total, size_t shmem,
                 cudaStream_t s) {
+  if (getenv("PS_DESCRIBE_GENERIC") != nullptr) {  // diagnostic: the general kernel for every keypoint
+    int64_t blocks = (total + kWarps - 1) / kWarps;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    describe_kernel<Img><<<(unsigned)blocks, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row,
+                                                                      kp->col, kp->scale, default_scale, kp->count,
+                                                                      kp->cap, prm, out_desc32, out_desc64, nullptr,
+                                                                      nullptr);
+    PS_LAUNCHED("describe_kernel");
+    return check_cuda("describe_kernel");
+  }
   int64_t* work = nullptr;
   static bool pool_set = false;  // keep freed queue memory in the stream-ordered pool
   if (!pool_set) {
@@ -1208,7 +1250,16 @@ int launch_fast(const Img& im, const ps_image_batch* img, const ps_keypoints* kp
   unsigned long long* n_work = reinterpret_cast<unsigned long long*>(work + total);
   cudaMemsetAsync(n_work, 0, sizeof(unsigned long long), s);
   const bool pair = getenv("PS_DESCRIBE_SINGLE") == nullptr;  // A/B switch (diagnostic, read per call)
-  if (pair) {
+  if (prm.n_w8 == 0 && prm.n_w16 > 0) {  // w = 16 scales only (e.g. the default 32..128 windows)
+    const size_t fshmem = (size_t)kFastWarps * (FastBox<16>::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
+    cudaFuncSetAttribute(describe_fast_u8<16, Img>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fshmem);
+    int64_t fblocks = (total + kFastWarps - 1) / kFastWarps;
+    if (fblocks > 148 * 16) fblocks = 148 * 16;
+    describe_fast_u8<16, Img><<<(unsigned)fblocks, kFastWarps * 32, fshmem, s>>>(
+        im, img->image_stride, img->batch, kp->row, kp->col, kp->scale, default_scale, kp->count, kp->cap, prm,
+        out_desc32, out_desc64, work, n_work);
+    PS_LAUNCHED("describe_fast_u8<16>");
+  } else if (pair) {
     const size_t pshmem =
         (size_t)2 * kPairWarps * (FastStage::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
     auto kern = prm.orient ? describe_pair_kernel<true, Img> : describe_pair_kernel<false, Img>;
@@ -1221,10 +1272,10 @@ int launch_fast(const Img& im, const ps_image_batch* img, const ps_keypoints* kp
     PS_LAUNCHED("describe_pair_kernel");
   } else {
     const size_t fshmem = (size_t)kFastWarps * (FastStage::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
-    cudaFuncSetAttribute(describe_fast_u8<Img>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fshmem);
+    cudaFuncSetAttribute(describe_fast_u8<8, Img>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fshmem);
     int64_t fblocks = (total + kFastWarps - 1) / kFastWarps;
     if (fblocks > 148 * 16) fblocks = 148 * 16;
-    describe_fast_u8<Img><<<(unsigned)fblocks, kFastWarps * 32, fshmem, s>>>(
+    describe_fast_u8<8, Img><<<(unsigned)fblocks, kFastWarps * 32, fshmem, s>>>(
         im, img->image_stride, img->batch, kp->row, kp->col, kp->scale, default_scale, kp->count, kp->cap, prm,
         out_desc32, out_desc64, work, n_work);
     PS_LAUNCHED("describe_fast_u8");
@@ -1287,11 +1338,16 @@ extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, in
     prm.lb[si] = lb;
     prm.fx[si] = std::ldexp(1.0, (int)std::floor(3.0 * lb - std::log2(nsamp * 2.9 * pmax)));
   }
-  for (int si = 0; si < n_scale_set; ++si)
+  for (int si = 0; si < n_scale_set; ++si) {
     if (d == 4 && prm.w[si] == 8) {
       prm.w8_scale[prm.n_w8++] = prm.scale[si];
       if (prm.scale[si] == default_scale) prm.default_w8 = 1;
     }
+    if (d == 4 && prm.w[si] == 16) {
+      prm.w16_scale[prm.n_w16++] = prm.scale[si];
+      if (prm.scale[si] == default_scale) prm.default_w16 = 1;
+    }
+  }
   const double two_pi = 2.0 * M_PI;  // descriptor.py:31
   prm.d = d;
   prm.D = d * d * 8;

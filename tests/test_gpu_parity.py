@@ -675,3 +675,29 @@ def test_sample_stream_on_device_matches_numpy(n):
             want = device.sample_stream(seed, n, iters)
             got = device.sample_stream_device(seed, n, iters).cpu().numpy()
             assert np.array_equal(got, want), (n, seed, iters)
+
+
+@pytest.mark.parametrize("scales,l_max", [((32, 64, 128), 128), ((16, 32, 64), 64), ((8, 16, 32), 32)])
+def test_fast_describe_kernels_agree_with_general_kernel(monkeypatch, scales, l_max):
+    """w = 8 (pair kernel) and w = 16 (the reference's default 32..128
+    windows) fast kernels against the general float64 kernel, and a sample
+    against the oracle."""
+    img = scenes.scene(700, 900, 21)
+    t = torch.from_numpy(img).cuda()
+    cfg = R.DescriptorConfig(0.0625, 4, l_max, True)
+    kp = device.detect(t, scales, meta=False)
+    monkeypatch.delenv("PS_DESCRIBE_GENERIC", raising=False)
+    d_fast = device.describe(t, kp, cfg, scale_set=kp.scale_set, out64=True, out32=False)
+    monkeypatch.setenv("PS_DESCRIBE_GENERIC", "1")
+    d_gen = device.describe(t, kp, cfg, scale_set=kp.scale_set, out64=True, out32=False)
+    n = int(kp.count[0])
+    a, b = d_fast[0, :n], d_gen[0, :n]
+    rel = (a - b).abs().amax(dim=-1) / b.norm(dim=-1).clamp_min(1e-300)
+    # the general kernel screens 8-bit rasters with float32 magnitudes (~1e-7)
+    assert float(rel.max()) <= 1e-6, float(rel.max())
+    alpha = O.default_alpha(*img.shape)
+    P = O.ramp(img.astype(np.float64), alpha)
+    h = kp.image(0)
+    for k in range(0, n, max(1, n // 40)):
+        ref = O.describe_one(P, int(h["row"][k]), int(h["col"][k]), scales[0], 0.0625, 4, l_max)
+        assert np.max(np.abs(a[k].cpu().numpy() - ref)) <= P2_TOL * max(np.linalg.norm(ref), 1e-300)
