@@ -69,14 +69,6 @@ struct FxHist {
     atomicAdd(h + nbins + bin, (unsigned)((q >> lb) & m));
     atomicAdd(h + 2 * nbins + bin, (unsigned)(q >> (2 * lb)));
   }
-  __device__ __forceinline__ void add_f(int bin, float mag, float fx) const {
-    if (mag == 0.0f) return;
-    const unsigned long long q = __float2ull_rn(mag * fx);
-    const unsigned m = (1u << lb) - 1u;
-    atomicAdd(h + bin, (unsigned)(q & m));
-    atomicAdd(h + nbins + bin, (unsigned)((q >> lb) & m));
-    atomicAdd(h + 2 * nbins + bin, (unsigned)(q >> (2 * lb)));
-  }
   __device__ __forceinline__ unsigned long long get(int bin) const {
     return (unsigned long long)h[bin] + ((unsigned long long)h[nbins + bin] << lb) +
            ((unsigned long long)h[2 * nbins + bin] << (2 * lb));
@@ -158,7 +150,7 @@ struct Stage {
   static constexpr int kStride = kSpan + 2 > 16 ? kSpan + 2 : 16;           // row stride (>= kSpan + 2)
   static constexpr int kP = (kSpan + 2) * kStride;
   static constexpr int kF = kSpan * kStride;
-  static constexpr int kTotal = W > 0 ? kP + 2 * kF : 0;
+  static constexpr int kTotal = W > 0 ? kP + 2 * kF : 0;  // doubles per warp
   static_assert(W <= 0 || W + 2 <= kStride, "stage stride too small");
 };
 constexpr int kStageW = 8;  // region side served from shared memory
@@ -194,10 +186,11 @@ using FastStage = FastBox<8>;
 // first taken from float32 atan2 and accepted only when the float32 bin
 // coordinate lies at least kBinMargin from a bin edge (its error is < 2e-5
 // bins: f32 rounding of the inputs, atan2f, the theta0 shift, the scaling);
-// otherwise the float64 path decides.  Magnitudes enter the histograms in
-// float32 (relative error < 3e-7, inside contract P2's 1e-4), and the argmax
-// of the 36-bin histogram is accepted only when the top bin leads the next by
-// more than the accumulated error, else that histogram is rebuilt in float64.
+// otherwise the float64 path decides.  Magnitudes stay float64 (a float32
+// magnitude merges near-identical flat-region descriptors); in the
+// general kernel the 36-bin argmax is accepted only when the top bin leads the
+// next by more than the screening error, else that histogram is rebuilt in
+// float64 (the fast kernels queue such keypoints for the general kernel).
 constexpr float kBinMargin = 1e-4f;
 
 __device__ __forceinline__ bool certified_bin(float x, int nbins, int& bin) {
@@ -220,12 +213,6 @@ __device__ __forceinline__ int side_bin(double a, double b, double ce, double se
   return -1;
 }
 
-__device__ __forceinline__ float warp_sum_f(float v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
 __device__ __forceinline__ float wrap_two_pi_f(float x) {
   const float tp = 6.283185307179586f;
   if (x < 0.0f) x += tp;
@@ -246,7 +233,6 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
   const int ws = w / d, nsamp = w * w;
   const int nr = im.nr, nc = im.nc;
   const double two_pi = prm.two_pi;
-  const float fxf = (float)fx;  // a power of two, exact in float32
   // _fit_region (descriptor.py:129-130)
   const int r0 = min(max(row - w / 2, 1), nr - 1 - w);
   const int c0 = min(max(col - w / 2, 1), nc - 1 - w);
@@ -294,7 +280,7 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
           h36.add(bin64(a, b, 0.0, prm.k36, 36), hypot(a, b), fx);
         } else {
           const float af = (float)a, bf = (float)b;
-          h36.add_f(bin36(a, b, af, bf), __fsqrt_rn(__fmaf_rn(af, af, bf * bf)), fxf);
+          h36.add(bin36(a, b, af, bf), __dsqrt_rn(__fma_rn(a, a, __dmul_rn(b, b))), fx);
         }
       }
       __syncwarp();
@@ -405,7 +391,7 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
           ob = side_bin(as, bs, ce, se, m, 8);
           if (ob < 0) ob = bin64(as, bs, theta0, prm.k8, 8);
         }
-        h128.add_f(cell + ob, __fsqrt_rn(__fmaf_rn(af, af, bf * bf)), fxf);
+        h128.add(cell + ob, __dsqrt_rn(__fma_rn(as, as, __dmul_rn(bs, bs))), fx);
       } else {
         h128.add(cell + bin64(as, bs, theta0, prm.k8, 8), hypot(as, bs), fx);
       }
@@ -426,7 +412,7 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
           ob = side_bin(a, b, prm.c8[m], prm.s8[m], m, 8);
           if (ob < 0) ob = bin64(a, b, 0.0, prm.k8, 8);
         }
-        h128.add_f(cell + ob, __fsqrt_rn(__fmaf_rn(af, af, bf * bf)), fxf);
+        h128.add(cell + ob, __dsqrt_rn(__fma_rn(a, a, __dmul_rn(b, b))), fx);
       } else {
         h128.add(cell + bin64(a, b, 0.0, prm.k8, 8), hypot(a, b), fx);
       }
@@ -435,38 +421,6 @@ __device__ __forceinline__ void describe_keypoint(const Img& im, int row, int co
   __syncwarp();
   // --- L2 normalise, clamp at 0.2, renormalise (descriptor.py:250-255)
   constexpr int kPer = DD > 0 ? (DD * DD * 8 + 31) / 32 : 16;
-  if (FAST && o64 == nullptr) {
-    // float32 output only: float32 arithmetic (relative error ~1e-6, P2 bar 1e-4)
-    const float inv_fx = 1.0f / fxf;
-    float vals[kPer];
-    float ss = 0.0f;
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const int q = lane + 32 * j;
-      vals[j] = q < D ? (float)h128.get(q) * inv_fx : 0.0f;
-      ss = __fmaf_rn(vals[j], vals[j], ss);
-    }
-    ss = warp_sum_f(ss);
-    if (ss > 0.0f) {
-      const float r1 = rsqrtf(ss);
-      float ss2 = 0.0f;
-#pragma unroll
-      for (int j = 0; j < kPer; ++j) {
-        vals[j] = fminf(vals[j] * r1, 0.2f);
-        ss2 = __fmaf_rn(vals[j], vals[j], ss2);
-      }
-      const float r2 = rsqrtf(warp_sum_f(ss2));
-#pragma unroll
-      for (int j = 0; j < kPer; ++j) vals[j] *= r2;
-    }
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const int q = lane + 32 * j;
-      if (q < D) o32[q] = vals[j];
-    }
-    __syncwarp();
-    return;
-  }
   const double inv_fx = 1.0 / fx;  // exact: fx is a power of two
   double vals[kPer];
   double ss = 0.0;
