@@ -220,42 +220,38 @@ __global__ void pad_unused(unsigned long long* __restrict__ kp, unsigned long lo
     }
 }
 
-// One-CTA bitonic sort of up to kSmallSort (delta bits, pair key) entries by
-// (delta, ref1, ref2), in place.  Pair keys are unique, so stability is moot.
-constexpr int kSmallSort = 8192;
-__global__ void __launch_bounds__(1024) sort_small(unsigned long long* __restrict__ kd,
-                                                   unsigned long long* __restrict__ kp,
-                                                   const unsigned long long* __restrict__ counter, int n_max, int n2) {
-  extern __shared__ unsigned long long ssort[];
-  unsigned long long* sd = ssort;
-  unsigned long long* sp = ssort + n2;
+// Sort of up to kSmallSort (delta bits, pair key) entries by (delta, ref1,
+// ref2) by ranking: entry e goes to slot #{f : (kd_f, kp_f) < (kd_e, kp_e)}
+// (pair keys are unique, so the ranks are a permutation).  n^2 comparisons
+// spread over the whole GPU beat a one-CTA sort at these sizes.
+constexpr int kSmallSort = 16384;
+constexpr int kRankTile = 1024;
+__global__ void __launch_bounds__(256) rank_scatter(const unsigned long long* __restrict__ kd,
+                                                    const unsigned long long* __restrict__ kp,
+                                                    const unsigned long long* __restrict__ counter, int n_max,
+                                                    unsigned long long* __restrict__ kd_out,
+                                                    unsigned long long* __restrict__ kp_out) {
+  __shared__ unsigned long long td[kRankTile], tp[kRankTile];
   const int n = (int)min((unsigned long long)n_max, *counter);
-  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-    sd[i] = i < n ? kd[i] : ~0ull;
-    sp[i] = i < n ? kp[i] : ~0ull;
-  }
-  __syncthreads();
-  for (int k = 2; k <= n2; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-        const int l = i ^ j;
-        if (l > i) {
-          const bool up = (i & k) == 0;
-          const bool gt = sd[i] > sd[l] || (sd[i] == sd[l] && sp[i] > sp[l]);
-          if (gt == up) {
-            const unsigned long long td = sd[i], tp = sp[i];
-            sd[i] = sd[l];
-            sp[i] = sp[l];
-            sd[l] = td;
-            sp[l] = tp;
-          }
-        }
-      }
-      __syncthreads();
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if ((int)(blockIdx.x * blockDim.x) >= n) return;  // uniform per block
+  const unsigned long long d = e < n ? kd[e] : 0ull, p = e < n ? kp[e] : 0ull;
+  int rank = 0;
+  for (int t0 = 0; t0 < n; t0 += kRankTile) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < kRankTile; q += blockDim.x) {
+      const int f = t0 + q;
+      td[q] = f < n ? kd[f] : ~0ull;
+      tp[q] = f < n ? kp[f] : ~0ull;
     }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    kd[i] = sd[i];
-    kp[i] = sp[i];
+    __syncthreads();
+    const int m = min(kRankTile, n - t0);
+#pragma unroll 8
+    for (int q = 0; q < m; ++q) rank += (td[q] < d) | ((td[q] == d) & (tp[q] < p));
+  }
+  if (e < n) {
+    kd_out[rank] = d;
+    kp_out[rank] = p;
   }
 }
 
@@ -429,17 +425,9 @@ extern "C" int ps_match(const void* desc1, int64_t n1, const void* desc2, int64_
     n = (int)std::max<unsigned long long>(1ull, std::min<unsigned long long>(c, (unsigned long long)n));
   }
   if (n <= kSmallSort) {
-    int n2 = 1;
-    while (n2 < n) n2 <<= 1;
-    const int smem = 2 * n2 * (int)sizeof(unsigned long long);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(sort_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kSmallSort * 8);
-      attr = true;
-    }
-    sort_small<<<1, 1024, smem, st>>>(w.kd, w.kp, w.counter, n, n2);
-    PS_LAUNCHED("sort_small");
-    unpack_pairs<<<grid_blocks(n, 256), 256, 0, st>>>(w.kd, w.kp, w.counter, cap, out_ref1, out_ref2, out_delta,
+    rank_scatter<<<(n + 255) / 256, 256, 0, st>>>(w.kd, w.kp, w.counter, n, w.kd2, w.kp2);
+    PS_LAUNCHED("rank_scatter");
+    unpack_pairs<<<grid_blocks(n, 256), 256, 0, st>>>(w.kd2, w.kp2, w.counter, cap, out_ref1, out_ref2, out_delta,
                                                       out_count);
     PS_LAUNCHED("unpack_pairs");
     return PS_OK;
