@@ -217,6 +217,8 @@ class MosaicPlan:
     rounds: list
     final_unmatched: list
     placements: dict = field(default_factory=dict)
+    pair_inliers: dict = field(default_factory=dict)
+    stage_seconds: dict = field(default_factory=dict)
 
 
 def select_reference(table: PairwiseTransformTable, remaining: set) -> int:
@@ -264,3 +266,34 @@ def plan_mosaic(table: PairwiseTransformTable, ids: Sequence[str]):
         rounds.append(MosaicRound(ids[ref], [ids[i] for i in stitched]))
     plan = MosaicPlan(rounds, [ids[i] for i in sorted(unmatched)], {ids[i]: t for i, t in placed.items()})
     return plan, placed
+
+
+def plan_and_stitch(images: Sequence, cfg, *, engine=None, group=None):
+    """mosaic.py:183-225 on the GPU: pairwise table (sharded over ``group``),
+    plan, and the device composite of the placed images -> (plan, composite).
+    ``images`` are IntensityImage-like objects (``pixels``, ``image_id``)."""
+    import time
+
+    from . import compositor as K
+
+    if len(images) < 2:
+        raise ConfigError("mosaic needs at least 2 images")
+    ids = [img.image_id for img in images]
+    if len(set(ids)) != len(ids):
+        raise ConfigError("image ids must be unique")
+    t0 = time.perf_counter()
+    pixels = [img.pixels for img in images]
+    table = build_pairwise_table(pixels, cfg, engine=engine, group=group)
+    t1 = time.perf_counter()
+    plan, placed = plan_mosaic(table, ids)
+    plan.pair_inliers = {(ids[a], ids[b]): e.inlier_count for (a, b), e in table.entries.items() if a < b}
+    t2 = time.perf_counter()
+    placements = [K.Placement(ids[i], placed[i]) for i in sorted(placed)]
+    dims = {ids[i]: tuple(np.asarray(images[i].pixels).shape[:2]) for i in placed}
+    canvas = K.compute_canvas(placements, dims)
+    composite = K.warp_and_blend({ids[i]: images[i].pixels for i in placed}, placements, canvas,
+                                 blend=cfg.blend, resample=cfg.resample)
+    t3 = time.perf_counter()
+    plan.stage_seconds = {"pairwise_table": t1 - t0, "planning": t2 - t1, "compositing": t3 - t2}
+    return plan, composite
+

@@ -206,6 +206,60 @@ def register_prepared(prep_a: PreparedImage, prep_b: PreparedImage, cfg: Pipelin
     return pairs, result, t1 - t0, t2 - t1
 
 
+@dataclass(eq=False)
+class StitchResult:
+    """pipeline.py:212-218."""
+
+    success: bool
+    transform: object | None
+    registration: RegistrationResult | None
+    composite: np.ndarray | None
+    report: dict
+
+
+def _compositor_pixels(img):
+    """The image as the compositor samples it (IntensityImage pixels)."""
+    px = img.pixels if hasattr(img, "pixels") else img
+    return px if isinstance(px, torch.Tensor) else np.asarray(px)
+
+
+def stitch_pair(img_a, img_b, cfg: PipelineConfig) -> StitchResult:
+    """pipeline.py:232-290 on the GPU: detect + describe both images, match,
+    RANSAC, and (on success) the device composite in the first image's frame."""
+    from . import compositor as K
+
+    start = time.perf_counter()
+    if tuple(_compositor_pixels(img_a).shape[:2]) == tuple(_compositor_pixels(img_b).shape[:2]):
+        prep_a, prep_b = prepare_batch([img_a, img_b], cfg, meta=True)
+    else:
+        prep_a, prep_b = prepare_image(img_a, cfg), prepare_image(img_b, cfg)
+    pairs, result, match_s, ransac_s = register_prepared(prep_a, prep_b, cfg)
+    stitch_s = ransac_s
+    composite = None
+    registration = {"theta_deg": 0.0, "t_x": 0.0, "t_y": 0.0, "inliers": 0, "pairs_in": len(pairs),
+                    "residual_rms": 0.0}
+    ida, idb = getattr(img_a, "image_id", "a"), getattr(img_b, "image_id", "b")
+    if result is not None:
+        t0 = time.perf_counter()
+        placements = [K.Placement(ida, RigidTransform.identity()), K.Placement(idb, result.transform.inverse())]
+        pa, pb = _compositor_pixels(img_a), _compositor_pixels(img_b)
+        canvas = K.compute_canvas(placements, {ida: tuple(pa.shape[:2]), idb: tuple(pb.shape[:2])})
+        composite = K.warp_and_blend({ida: pa, idb: pb}, placements, canvas, blend=cfg.blend, resample=cfg.resample)
+        stitch_s += time.perf_counter() - t0
+        registration.update(theta_deg=math.degrees(result.transform.theta), t_x=result.transform.t_x,
+                            t_y=result.transform.t_y, inliers=len(result.inliers), residual_rms=result.residual_rms)
+    report = {
+        "success": result is not None, "image_a": ida, "image_b": idb,
+        "features": {ida: prep_a.feature_count, idb: prep_b.feature_count},
+        "matched_pairs": len(pairs), "registration": registration,
+        "stage_seconds": {"detection": prep_a.detect_seconds + prep_b.detect_seconds,
+                          "description": prep_a.describe_seconds + prep_b.describe_seconds,
+                          "matching": match_s, "stitching": stitch_s},
+        "total_seconds": time.perf_counter() - start,
+    }
+    return StitchResult(result is not None, result.transform if result else None, result, composite, report)
+
+
 def pair_seed(seed: int, a: int, b: int) -> int:
     """mosaic.py:75-76."""
     return int(np.random.SeedSequence([seed, a, b]).generate_state(1)[0])

@@ -701,3 +701,34 @@ def test_fast_describe_kernels_agree_with_general_kernel(monkeypatch, scales, l_
     for k in range(0, n, max(1, n // 40)):
         ref = O.describe_one(P, int(h["row"][k]), int(h["col"][k]), scales[0], 0.0625, 4, l_max)
         assert np.max(np.abs(a[k].cpu().numpy() - ref)) <= P2_TOL * max(np.linalg.norm(ref), 1e-300)
+
+
+def test_stitch_pair_and_plan_and_stitch_on_device():
+    """pipeline.stitch_pair and mosaic.plan_and_stitch (the callers of the
+    path, with the device compositor): crops of one scene register at their
+    true offsets and the composite reproduces the scene where it is covered."""
+    from paper_2405_08578_b200 import mosaic, pipeline as PL
+
+    src = scenes.scene(360, 480, 11).astype(np.float64)
+    cfg = PL.PipelineConfig(window_min=16, window_max=64, seed=7)
+    a = R.IntensityImage(src[:, :300].copy(), "a")
+    b = R.IntensityImage(src[:, 180:].copy(), "b")
+    res = PL.stitch_pair(a, b, cfg)
+    assert res.success and res.report["matched_pairs"] > 50
+    # the transform maps a's pixels onto b: x_b = x_a - 180
+    assert abs(res.transform.t_x + 180) < 0.5 and abs(res.transform.t_y) < 0.5
+    assert res.composite.shape == (360, 480)
+    cov = res.composite != 0  # a ~1e-19 rad rotation can leave a border column uncovered (as in the reference)
+    assert cov.mean() > 0.99
+    assert float(np.sqrt(np.mean((res.composite[cov] - src[cov]) ** 2))) < 1.0
+    frags, offs = [], {}
+    for k, (r0, c0) in enumerate([(0, 0), (0, 200), (140, 0), (140, 200)]):
+        frags.append(R.IntensityImage(src[r0:r0 + 220, c0:c0 + 280].copy(), f"f{k}"))
+        offs[f"f{k}"] = (r0, c0)
+    plan, comp = mosaic.plan_and_stitch(frags, cfg)
+    assert plan.final_unmatched == []
+    ref = plan.rounds[0].reference_id
+    assert comp.shape == (360, 480)
+    cov = comp != 0
+    assert cov.mean() > 0.99
+    assert float(np.sqrt(np.mean((comp[cov] - src[cov]) ** 2))) < 1.0, ref

@@ -136,3 +136,67 @@ def test_gray_table_reproduces_reference_to_grayscale():
     a, _, _ = scenes.config5_pair(0)
     key = (a[..., 0].astype(np.int64) << 16) | (a[..., 1].astype(np.int64) << 8) | a[..., 2]
     assert np.array_equal(lut[key], scenes.gray_bt601(a))
+
+
+# ---- mosaic planning (reference test_mosaic.py table / selection / planning cases) ----
+
+def _chain_table(n):
+    from paper_2405_08578_b200.mosaic import PairwiseTransformTable
+
+    table = PairwiseTransformTable(n=n)
+    step = R.RigidTransform(0.0, 40.0, 0.0)  # maps (k+1)'s coordinates into k's frame
+    for k in range(n - 1):
+        table.set_pair(k, k + 1, step, inliers=20)
+    return table
+
+
+def test_mosaic_table_and_reference_selection():
+    from paper_2405_08578_b200.mosaic import PairwiseTransformTable, select_reference
+
+    t = _chain_table(3)
+    assert t.present(0, 1) and t.present(1, 0) and not t.present(0, 2)
+    both = t.get(0, 1).transform.compose(t.get(1, 0).transform)
+    assert np.allclose(both.matrix, np.eye(3), atol=1e-6)
+    assert select_reference(_chain_table(3), {0, 1, 2}) == 1
+    assert select_reference(_chain_table(2), {0, 1}) == 0
+    assert select_reference(PairwiseTransformTable(n=6), {5}) == 5
+    assert select_reference(_chain_table(4), {1, 2, 3}) == 2
+
+
+def test_mosaic_planning_cases():
+    from paper_2405_08578_b200.mosaic import PairwiseTransformTable, plan_mosaic
+
+    plan, placed = plan_mosaic(_chain_table(2), ["x", "y"])
+    assert len(plan.rounds) == 1 and plan.rounds[0].reference_id == "x"
+    assert plan.rounds[0].stitched_ids == ["y"] and plan.final_unmatched == []
+    assert placed[0] == R.RigidTransform.identity()
+    plan, placed = plan_mosaic(_chain_table(4), ["a", "b", "c", "d"])
+    assert plan.final_unmatched == [] and set(placed) == {0, 1, 2, 3}
+    for k in range(3):
+        assert placed[k].t_x - placed[k + 1].t_x == pytest.approx(-40.0, abs=1e-9)
+    t = PairwiseTransformTable(n=3)
+    t.set_pair(0, 1, R.RigidTransform(0.0, 25.0, 0.0), inliers=15)
+    plan, placed = plan_mosaic(t, ["a", "b", "lonely"])
+    assert plan.final_unmatched == ["lonely"] and set(placed) == {0, 1}
+    t = _chain_table(5)
+    t.entries.pop((3, 4))
+    t.entries.pop((4, 3))
+    plan, _ = plan_mosaic(t, list("abcde"))
+    seen = list(plan.final_unmatched)
+    for r in plan.rounds:
+        seen.append(r.reference_id)
+        seen.extend(r.stitched_ids)
+    assert sorted(seen) == list("abcde")
+
+
+def test_plan_and_stitch_argument_errors():
+    from paper_2405_08578_b200.mosaic import plan_and_stitch
+    from paper_2405_08578_b200.pipeline import PipelineConfig
+
+    cfg = PipelineConfig(window_min=32, window_max=64, seed=7)
+    with pytest.raises(ConfigError):
+        plan_and_stitch([R.IntensityImage(np.zeros((64, 64)), "solo")], cfg)
+    rng = np.random.default_rng(1)
+    with pytest.raises(ConfigError):
+        plan_and_stitch([R.IntensityImage(rng.uniform(0, 255, (64, 64)), "same"),
+                         R.IntensityImage(rng.uniform(0, 255, (64, 64)), "same")], cfg)
