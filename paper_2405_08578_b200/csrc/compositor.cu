@@ -57,6 +57,28 @@ __global__ void __launch_bounds__(256) composite_kernel(PlaceBatch pb, int heigh
                                                         int first, int last, double* __restrict__ out,
                                                         double* __restrict__ weightmap, double* __restrict__ acc_g,
                                                         int* __restrict__ cnt_g, double* __restrict__ solo_g) {
+  // placements whose canvas block meets this CTA's tile, in placement order
+  __shared__ int list[kBatch];
+  __shared__ int n_list;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  if (tid < 32) {
+    const int tc0 = blockIdx.x * blockDim.x, tc1 = tc0 + blockDim.x;
+    const int tr0 = blockIdx.y * blockDim.y, tr1 = tr0 + blockDim.y;
+    int base = 0;
+    for (int k0 = 0; k0 < pb.n; k0 += 32) {
+      const int k = k0 + tid;
+      bool hit = false;
+      if (k < pb.n) {
+        const ps_placement& P = pb.p[k];
+        hit = P.r_lo < tr1 && P.r_hi > tr0 && P.c_lo < tc1 && P.c_hi > tc0;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, hit);
+      if (hit) list[base + __popc(bal & ((1u << tid) - 1u))] = k;
+      base += __popc(bal);
+    }
+    if (tid == 0) n_list = base;
+  }
+  __syncthreads();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int r = blockIdx.y * blockDim.y + threadIdx.y;
   if (c >= width || r >= height) return;
@@ -70,41 +92,43 @@ __global__ void __launch_bounds__(256) composite_kernel(PlaceBatch pb, int heigh
     solo = solo_g[o];
   }
   const double X = (double)c + (double)dx, Y = (double)r + (double)dy;  // np.arange(...) + dx
-  for (int k = 0; k < pb.n; ++k) {
-    const ps_placement& P = pb.p[k];
+  const int nl = n_list;
+  for (int q = 0; q < nl; ++q) {
+    const ps_placement& P = pb.p[list[q]];
     if (r < P.r_lo || r >= P.r_hi || c < P.c_lo || c >= P.c_hi) continue;  // outside this image's block
     // inverse.transform_points (registration.py:66-73)
     const double sx = __dadd_rn(__dsub_rn(__dmul_rn(P.cos_t, X), __dmul_rn(P.sin_t, Y)), P.t_x);
     const double sy = __dadd_rn(__dadd_rn(__dmul_rn(P.sin_t, X), __dmul_rn(P.cos_t, Y)), P.t_y);
     const double xmax = (double)(P.nc - 1), ymax = (double)(P.nr - 1);
     const bool valid = sx >= 0.0 && sx <= xmax && sy >= 0.0 && sy <= ymax;
-    if (BLEND == PS_BLEND_OVERWRITE && !valid) continue;
-    double v = 0.0;
-    if (valid) {
-      const double xs = fmin(fmax(sx, 0.0), xmax), ys = fmin(fmax(sy, 0.0), ymax);
-      if (RESAMPLE == PS_RESAMPLE_BILINEAR)
-        v = P.pixel_type == PS_PIXELS_U8 ? sample_bilinear<uint8_t>(P, xs, ys) : sample_bilinear<double>(P, xs, ys);
-      else
-        v = P.pixel_type == PS_PIXELS_U8 ? sample_nearest<uint8_t>(P, xs, ys) : sample_nearest<double>(P, xs, ys);
-    }
+    // an invalid sample adds +0.0 to the (non-negative) accumulators: a no-op
+    if (!valid) continue;
+    // the reference clips (sx, sy) to the image first: the identity for a valid sample
+    double v;
+    if (RESAMPLE == PS_RESAMPLE_BILINEAR)
+      v = P.pixel_type == PS_PIXELS_U8 ? sample_bilinear<uint8_t>(P, sx, sy) : sample_bilinear<double>(P, sx, sy);
+    else
+      v = P.pixel_type == PS_PIXELS_U8 ? sample_nearest<uint8_t>(P, sx, sy) : sample_nearest<double>(P, sx, sy);
     if (BLEND == PS_BLEND_OVERWRITE) {
       acc = v;
       wsum = 1.0;
       cnt = 1;
       solo = v;
     } else {
-      // feather weight 1 + distance to the nearest source border (compositor.py:146-148)
-      const double w =
-          __dadd_rn(1.0, fmin(fmin(sx, __dsub_rn(xmax, sx)), fmin(sy, __dsub_rn(ymax, sy))));
-      acc = __dadd_rn(acc, valid ? __dmul_rn(w, v) : 0.0);
-      wsum = __dadd_rn(wsum, valid ? w : 0.0);
-      cnt += valid ? 1 : 0;
-      if (valid) solo = v;
+      // feather weight 1 + distance to the nearest source border (compositor.py:146-148);
+      // all four distances are >= 0 here, so plain compares pick the minimum
+      const double ex = __dsub_rn(xmax, sx), ey = __dsub_rn(ymax, sy);
+      const double mx = sx < ex ? sx : ex, my = sy < ey ? sy : ey;
+      const double w = __dadd_rn(1.0, mx < my ? mx : my);
+      acc = __dadd_rn(acc, __dmul_rn(w, v));
+      wsum = __dadd_rn(wsum, w);
+      cnt += 1;
+      solo = v;
     }
   }
   if (last) {
-    double res = wsum > 0.0 ? __ddiv_rn(acc, wsum) : 0.0;
-    if (cnt == 1) res = solo;  // single cover: the sample verbatim (compositor.py:155-157)
+    // single cover: the sample verbatim (compositor.py:155-157); else accum / weights
+    const double res = cnt == 1 ? solo : (wsum > 0.0 ? __ddiv_rn(acc, wsum) : 0.0);
     out[o] = res;
     weightmap[o] = wsum;
   } else {
