@@ -8,6 +8,7 @@ There is no CPU path: on a machine without CUDA these functions raise.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 from dataclasses import dataclass
 
 import numpy as np
@@ -317,17 +318,24 @@ def sample_stream(seed: int, n: int, iterations: int) -> np.ndarray:
     return v.astype(np.int32)
 
 
+@functools.lru_cache(maxsize=256)
+def _pcg_state(seed: int) -> tuple:
+    """(state, inc, has_uint32, uinteger) of default_rng(seed) -- SeedSequence
+    hashing is the host-side cost of a RANSAC call, so it is cached per seed."""
+    st = np.random.default_rng(seed).bit_generator.state
+    return int(st["state"]["state"]), int(st["state"]["inc"]), int(st["has_uint32"]), int(st["uinteger"])
+
+
 def sample_stream_device(seed: int, n: int, iterations: int, device=None, stream=None) -> torch.Tensor:
     """The same stream generated on the GPU (ps_ransac_samples): only the
     seeded PCG64 state comes from numpy (SeedSequence seeding on the host),
     the draws -- jump-ahead per iteration, Lemire bounds, exact sequential
     replay when a rejection occurs -- run on the device.  int32 [iters, 2]."""
-    st = np.random.default_rng(seed).bit_generator.state
-    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    s, inc, has_u32, u32 = _pcg_state(int(seed))
     m64 = (1 << 64) - 1
     out = torch.empty(2 * iterations + 1, dtype=torch.int32, device=device or "cuda")
-    _lib.check(_lib.lib().ps_ransac_samples(s >> 64, s & m64, inc >> 64, inc & m64, int(st["has_uint32"]),
-                                            int(st["uinteger"]), int(n), int(iterations), _ptr(out),
+    _lib.check(_lib.lib().ps_ransac_samples(s >> 64, s & m64, inc >> 64, inc & m64, has_u32,
+                                            u32, int(n), int(iterations), _ptr(out),
                                             C.c_void_p(out.data_ptr() + 8 * iterations),
                                             C.c_void_p(_stream_ptr(stream))), "ransac_samples")
     return out[: 2 * iterations].view(iterations, 2)
