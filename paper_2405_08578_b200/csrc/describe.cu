@@ -977,31 +977,42 @@ __device__ __forceinline__ bool describe_pair_w8(const Img& im, int row, int col
       bn[j] = ((iv / WS) * 4 + iu / WS) * 8 + ob;
     }
   } else {
+    // The 36-bin histogram only decides the dominant orientation, and only
+    // with a clear lead (6e-5 relative), so float32 magnitudes (~2^-22) and
+    // one 32-bit fixed-point limb suffice; the descriptor's own magnitudes
+    // (the rotated phase) stay float64.
+    float mgf[SPL];
 #pragma unroll
     for (int j = 0; j < SPL; ++j) {
       const int s = hl + 16 * j;
       double a, b;
       axis_ab(s / W, s % W, a, b);
-      const float x = wrap_two_pi_f(fast_atan2f((float)b, (float)a)) * 5.729577951308232f;
+      const float af = (float)a, bf = (float)b;
+      const float x = wrap_two_pi_f(fast_atan2f(bf, af)) * 5.729577951308232f;
       int bin;
       if (!certified_bin(x, 36, bin)) {
         const int m = min(max(__float2int_rn(x), 0), 36);
         bin = exact_bin(a, b, 1.0, 0.0, prm.cb36[m], prm.sb36[m], m, 36, 0.0, prm.k36, prm.two_pi);
       }
-      mg[j] = __dsqrt_rn(__fma_rn(a, a, __dmul_rn(b, b)));
+      const float s2 = __fmaf_rn(af, af, __fmul_rn(bf, bf));
+      mgf[j] = s2 > 0.0f ? __fmul_rn(s2, rsqrtf(s2)) : 0.0f;
       bn[j] = bin;
     }
-    double mx = fmax(fmax(mg[0], mg[1]), fmax(mg[2], mg[3]));
-    const double f36 = fx_scale52_half(mx, hsel);
+    {
+      // 64 sums stay below 2^31: scale 2^(151 - e) for a largest magnitude < 2^(e - 126)
+      const float mx = fmaxf(fmaxf(mgf[0], mgf[1]), fmaxf(mgf[2], mgf[3]));
+      const unsigned eb = half_max_u32(__float_as_uint(mx), hsel) >> 23;
+      const float f36 = eb == 0u ? 1.0f : __uint_as_float((unsigned)min(max(278 - (int)eb, 1), 254) << 23);
 #pragma unroll
-    for (int j = 0; j < SPL; ++j) h2_add(h36, 36, bn[j], mg[j], f36);
+      for (int j = 0; j < SPL; ++j) atomicAdd(h36 + bn[j], __float2uint_rn(__fmul_rn(mgf[j], f36)));
+    }
     __syncwarp();
     // argmax with a clear lead over the half's 36 bins (3 per lane)
     unsigned k1 = 0u, k2 = 0u;
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
       const int bin = hl + 16 * t;
-      const unsigned k = bin < 36 ? ((__float_as_uint((float)h2_get(h36, 36, bin)) & ~63u) | (63u - bin)) : 0u;
+      const unsigned k = bin < 36 ? ((__float_as_uint((float)h36[bin]) & ~63u) | (63u - bin)) : 0u;
       if (k > k1) { k2 = k1; k1 = k; } else if (k > k2) { k2 = k; }
     }
     const unsigned top = half_max_u32(k1, hsel);
