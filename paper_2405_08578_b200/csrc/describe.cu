@@ -567,6 +567,7 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
     return min((int)__dmul_rn(ori, k), nbins - 1);
   };
   double mg[SPL];  // float64 magnitudes (~1 ulp): descriptors stay ~1e-15 accurate
+  float mgf[SPL];  // orientation-histogram magnitudes
   int bn[SPL];
   if (!prm.orient) {
 #pragma unroll
@@ -600,18 +601,24 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
         bin = side_bin(a, b, prm.cb36[m], prm.sb36[m], m, 36);
         if (bin < 0) bin = bin64(a, b, 0.0, prm.k36, 36);
       }
-      mg[j] = __dsqrt_rn(__fma_rn(a, a, __dmul_rn(b, b)));
+      // float32 magnitudes: this histogram only decides a certified argmax
+      const float s2 = __fmaf_rn(af, af, __fmul_rn(bf, bf));
+      mgf[j] = s2 > 0.0f ? __fmul_rn(s2, rsqrtf(s2)) : 0.0f;
       bn[j] = bin;
     }
-    double mx = mg[0];
+    {
+      // NS sums stay below 2^31: scale 2^(157 - LOG - e) for a largest magnitude < 2^(e - 126)
+      float mx = mgf[0];
 #pragma unroll
-    for (int j = 1; j < SPL; ++j) mx = fmax(mx, mg[j]);
-    const double f36 = fx_scale52_warp<LOG>(mx);
+      for (int j = 1; j < SPL; ++j) mx = fmaxf(mx, mgf[j]);
+      const unsigned eb = __reduce_max_sync(0xffffffffu, __float_as_uint(mx)) >> 23;
+      const float f36 = eb == 0u ? 1.0f : __uint_as_float((unsigned)min(max(284 - LOG - (int)eb, 1), 254) << 23);
 #pragma unroll
-    for (int j = 0; j < SPL; ++j) h2_add<LIMB>(h36, 36, bn[j], mg[j], f36);
+      for (int j = 0; j < SPL; ++j) atomicAdd(h36 + bn[j], __float2uint_rn(__fmul_rn(mgf[j], f36)));
+    }
     __syncwarp();
     // argmax with a clear lead (else the whole keypoint is redone in float64)
-    const unsigned long long v1 = h2_get<LIMB>(h36, 36, lane), v2 = lane < 4 ? h2_get<LIMB>(h36, 36, lane + 32) : 0ull;
+    const unsigned v1 = h36[lane], v2 = lane < 4 ? h36[lane + 32] : 0u;
     const unsigned k1 = (__float_as_uint((float)v1) & ~63u) | (63u - lane);
     const unsigned k2 = lane < 4 ? ((__float_as_uint((float)v2) & ~63u) | (31u - lane)) : 0u;
     const unsigned top = __reduce_max_sync(0xffffffffu, max(k1, k2));
