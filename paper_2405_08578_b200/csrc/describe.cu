@@ -200,6 +200,21 @@ __device__ __forceinline__ bool certified_bin(float x, int nbins, int& bin) {
   return fr > kBinMargin && fr < 1.0f - kBinMargin && x > 0.0f && x < (float)nbins;
 }
 
+// 8-bin octant of phi = atan2(v, u) in [0, 2 pi) from signs and |u| vs |v|,
+// certified when phi is more than kBinMargin bins (7.85e-5 rad) from an edge:
+// min(|u|, |v|) and ||u| - |v|| / sqrt(2) bound the distance to the axes and to
+// the diagonals (relative to |u| + |v| >= r).  float32 error is ~3e-7 rad.
+__device__ __forceinline__ bool octant_bin(float u, float v, int& bin) {
+  const float au = fabsf(u), av = fabsf(v), sum = au + av;
+  const bool upper = v >= 0.0f;
+  const bool q_odd = upper ? !(u > 0.0f) : !(u < 0.0f);  // quadrants 1 and 3
+  const int q = upper ? (q_odd ? 1 : 0) : (q_odd ? 3 : 2);
+  const bool second = q_odd ? av < au : av > au;
+  bin = 2 * q + (second ? 1 : 0);
+  const float d = 7.854e-5f * sum;
+  return fminf(au, av) > d && fabsf(au - av) > 1.4143f * d;
+}
+
 // Bin of a float64 gradient (a, b) whose float32 bin coordinate fell within
 // kBinMargin of edge m (angle of the edge: cos ce, sin se).  The exact angle
 // lies more than 1e-12 rad from the edge unless |b ce - a se| is tiny, and
@@ -1028,7 +1043,7 @@ __device__ __forceinline__ bool describe_pair_w8(const Img& im, int row, int col
     ok = ok && (sv < tv * 0.99994f);
     const int hk = 63 - (int)(top & 63u);
     const double theta0 = prm.theta[hk], ct = prm.cos_t[hk], st = prm.sin_t[hk];
-    const float theta0f = (float)theta0;
+    const float theta0f = (float)theta0, ctf = (float)ct, stf = (float)st;
     const double xmin = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, ct >= 0.0 ? -half : half)), __dmul_rn(st, st >= 0.0 ? half : -half));
     const double xmax = __dsub_rn(__dadd_rn(cx, __dmul_rn(ct, ct >= 0.0 ? half : -half)), __dmul_rn(st, st >= 0.0 ? -half : half));
     const double ymin = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, st >= 0.0 ? -half : half)), __dmul_rn(ct, ct >= 0.0 ? -half : half));
@@ -1070,9 +1085,11 @@ __device__ __forceinline__ bool describe_pair_w8(const Img& im, int row, int col
       const double w00 = __dmul_rn(sy, sx), w01 = __dmul_rn(sy, fxx), w10 = __dmul_rn(fyy, sx), w11 = __dmul_rn(fyy, fxx);
       const double as = __fma_rn(a11, w11, __fma_rn(a10, w10, __fma_rn(a01, w01, __dmul_rn(a00, w00))));
       const double bs = __fma_rn(b11, w11, __fma_rn(b10, w10, __fma_rn(b01, w01, __dmul_rn(b00, w00))));
-      const float xb = wrap_two_pi_f(fast_atan2f((float)bs, (float)as) - theta0f) * 1.2732395447351628f;
+      // orientation relative to theta0: rotate by -theta0 (ct = cos theta0, st = -sin theta0), octant test
+      const float af = (float)as, bf = (float)bs;
       int ob;
-      if (!certified_bin(xb, 8, ob)) {
+      if (!octant_bin(__fmaf_rn(af, ctf, -__fmul_rn(bf, stf)), __fmaf_rn(bf, ctf, __fmul_rn(af, stf)), ob)) {
+        const float xb = wrap_two_pi_f(fast_atan2f(bf, af) - theta0f) * 1.2732395447351628f;
         const int m = min(max(__float2int_rn(xb), 0), 8);
         ob = exact_bin(as, bs, c0t, s0t, prm.c8[m], prm.s8[m], m, 8, theta0, prm.k8, prm.two_pi);
       }
