@@ -700,9 +700,10 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
       const double as = __fma_rn(a11, w11, __fma_rn(a10, w10, __fma_rn(a01, w01, __dmul_rn(a00, w00))));
       const double bs = __fma_rn(b11, w11, __fma_rn(b10, w10, __fma_rn(b01, w01, __dmul_rn(b00, w00))));
       const float af = (float)as, bf = (float)bs;
-      const float xb = wrap_two_pi_f(fast_atan2f(bf, af) - theta0f) * 1.2732395447351628f;
-      int ob;
-      if (!certified_bin(xb, 8, ob)) {
+      int ob;  // octant of the theta0-rotated gradient (ct = cos theta0, st = -sin theta0)
+      if (!octant_bin(__fmaf_rn(af, (float)ct, -__fmul_rn(bf, (float)st)),
+                      __fmaf_rn(bf, (float)ct, __fmul_rn(af, (float)st)), ob)) {
+        const float xb = wrap_two_pi_f(fast_atan2f(bf, af) - theta0f) * 1.2732395447351628f;
         const int m = min(max(__float2int_rn(xb), 0), 8);
         const double ce = __dsub_rn(__dmul_rn(c0t, prm.c8[m]), __dmul_rn(s0t, prm.s8[m]));
         const double se = __dadd_rn(__dmul_rn(s0t, prm.c8[m]), __dmul_rn(c0t, prm.s8[m]));
