@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 2
+#define PS_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define PS_API __attribute__((visibility("default")))
@@ -149,6 +149,16 @@ PS_API int ps_match(const void* desc1, int64_t n1, const void* desc2, int64_t n2
              int32_t desc_is_f64, double delta_s, int32_t strategy, int32_t* out_ref1, int32_t* out_ref2,
              double* out_delta, int64_t* out_count, int64_t cap, void* workspace,
              size_t workspace_bytes, void* stream);
+
+/* As ps_match without any host synchronisation: every grid is sized from
+ * n1 / n2 (the kernels read the device-side counts), so a sequence of calls
+ * -- e.g. the pairs of a pairwise table -- is enqueued back to back and the
+ * caller reads all *out_count values with one copy.  Same results as
+ * ps_match; cap must be >= min(n1, n2) for nearest_neighbor. */
+PS_API int ps_match_async(const void* desc1, int64_t n1, const void* desc2, int64_t n2, int32_t dim,
+                   int32_t desc_is_f64, double delta_s, int32_t strategy, int32_t* out_ref1,
+                   int32_t* out_ref2, double* out_delta, int64_t* out_count, int64_t cap,
+                   void* workspace, size_t workspace_bytes, void* stream);
 
 /* One direction of nearest_neighbor matching: out_index[i] / out_dist[i] =
  * the exact first argmin over the rows of Y of the reference distance to row

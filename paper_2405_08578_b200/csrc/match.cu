@@ -19,7 +19,7 @@
 template <class T>
 int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double delta_s, unsigned long long* keys_pair,
                        unsigned long long* keys_delta, unsigned long long* counter, void* ws, size_t ws_bytes,
-                       cudaStream_t st);
+                       cudaStream_t st, bool sync);
 size_t ps_tc_nearest_ws(int64_t n1, int64_t n2);
 template <class T>
 int ps_tc_rows_impl(const T* X, int64_t nx, const T* Y, int64_t ny, int32_t* nn, double* dist, void* ws,
@@ -372,10 +372,10 @@ extern "C" int ps_match_plan(int64_t n1, int64_t n2, int32_t dim, int32_t strate
   return PS_OK;
 }
 
-extern "C" int ps_match(const void* desc1, int64_t n1, const void* desc2, int64_t n2, int32_t dim,
-                        int32_t desc_is_f64, double delta_s,
-                        int32_t strategy, int32_t* out_ref1, int32_t* out_ref2, double* out_delta, int64_t* out_count,
-                        int64_t cap, void* workspace, size_t workspace_bytes, void* stream) {
+namespace {
+int match_impl(const void* desc1, int64_t n1, const void* desc2, int64_t n2, int32_t dim, int32_t desc_is_f64,
+               double delta_s, int32_t strategy, int32_t* out_ref1, int32_t* out_ref2, double* out_delta,
+               int64_t* out_count, int64_t cap, void* workspace, size_t workspace_bytes, void* stream, bool sync) {
   PS_REQUIRE(delta_s > 0, PS_ERR_CONFIG, "delta_s must be positive, got %g", delta_s);
   PS_REQUIRE(strategy == PS_MATCH_NEAREST || strategy == PS_MATCH_THRESHOLD_ALL, PS_ERR_CONFIG,
              "unknown match strategy %d", strategy);
@@ -401,9 +401,9 @@ extern "C" int ps_match(const void* desc1, int64_t n1, const void* desc2, int64_
   int rc;
   if (tc) {
     rc = desc_is_f64 ? ps_tc_nearest_impl((const double*)desc1, n1, (const double*)desc2, n2, delta_s, w.kp, w.kd,
-                                          w.counter, w.extra, w.extra_bytes, st)
+                                          w.counter, w.extra, w.extra_bytes, st, sync)
                      : ps_tc_nearest_impl((const float*)desc1, n1, (const float*)desc2, n2, delta_s, w.kp, w.kd,
-                                          w.counter, w.extra, w.extra_bytes, st);
+                                          w.counter, w.extra, w.extra_bytes, st, sync);
   } else {
     rc = desc_is_f64
              ? launch_match((const double*)desc1, n1, (const double*)desc2, n2, dim, delta_s, strategy, w, cand, st)
@@ -415,9 +415,10 @@ extern "C" int ps_match(const void* desc1, int64_t n1, const void* desc2, int64_
   // cub needs a host-side length: the tensor-core path has synchronised with
   // the host already, so its accepted count is read back and only those keys
   // are sorted; the asynchronous CUDA-core path sorts the whole candidate
-  // capacity with unused slots padded by all-ones keys (they sort last).
+  // capacity with unused slots padded by all-ones keys (they sort last), and
+  // so does the tensor-core path in asynchronous mode.
   int n = (int)(cand > 0 ? cand : 1);
-  if (tc) {
+  if (tc && sync) {
     unsigned long long c = 0;
     cudaMemcpyAsync(&c, w.counter, sizeof(c), cudaMemcpyDeviceToHost, st);
     const cudaError_t e = cudaStreamSynchronize(st);
@@ -444,6 +445,23 @@ extern "C" int ps_match(const void* desc1, int64_t n1, const void* desc2, int64_
                                                     out_count);
   PS_LAUNCHED("unpack_pairs");
   return PS_OK;
+}
+}  // namespace
+
+extern "C" int ps_match(const void* desc1, int64_t n1, const void* desc2, int64_t n2, int32_t dim,
+                        int32_t desc_is_f64, double delta_s, int32_t strategy, int32_t* out_ref1, int32_t* out_ref2,
+                        double* out_delta, int64_t* out_count, int64_t cap, void* workspace, size_t workspace_bytes,
+                        void* stream) {
+  return match_impl(desc1, n1, desc2, n2, dim, desc_is_f64, delta_s, strategy, out_ref1, out_ref2, out_delta,
+                    out_count, cap, workspace, workspace_bytes, stream, true);
+}
+
+extern "C" int ps_match_async(const void* desc1, int64_t n1, const void* desc2, int64_t n2, int32_t dim,
+                              int32_t desc_is_f64, double delta_s, int32_t strategy, int32_t* out_ref1,
+                              int32_t* out_ref2, double* out_delta, int64_t* out_count, int64_t cap, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  return match_impl(desc1, n1, desc2, n2, dim, desc_is_f64, delta_s, strategy, out_ref1, out_ref2, out_delta,
+                    out_count, cap, workspace, workspace_bytes, stream, false);
 }
 
 extern "C" int ps_pair_points(const int32_t* ref1, const int32_t* ref2, const int64_t* count, const int32_t* row1,

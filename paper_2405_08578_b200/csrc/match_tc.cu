@@ -813,7 +813,7 @@ int dedupe(const T* X, int64_t n, Side& s, const TcWs& w, cudaStream_t st) {
 template <class T>
 int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t* n_x, const T* Y, int64_t ny_all,
                  const int32_t* y_idx, const int32_t* n_y, int32_t* nn, double* dist, const TcWs& w,
-                 cudaStream_t st, int64_t* nx_io = nullptr, int64_t* ny_io = nullptr) {
+                 cudaStream_t st, int64_t* nx_io = nullptr, int64_t* ny_io = nullptr, bool sync = true) {
   const int64_t xrows = rup(nx_max, BM), yrows = rup(ny_all, BN);
   cudaMemsetAsync(w.ymax, 0, 4 * sizeof(unsigned), st);
   cudaMemsetAsync(w.n_overflow, 0, sizeof(int32_t), st);
@@ -829,15 +829,18 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   }
   // the counts size the grids; a caller that already knows one passes it in (>= 0)
   int64_t nx = nx_io && *nx_io >= 0 ? *nx_io : -1, ny = ny_io && *ny_io >= 0 ? *ny_io : -1;
-  if (nx < 0 && ny < 0) read_counts(n_x, n_y, &nx, &ny, st);
+  if (!sync) {  // no host round trip: grids sized by the upper bounds, the kernels read the device counts
+    nx = nx_max;
+    ny = ny_all;
+  } else if (nx < 0 && ny < 0) read_counts(n_x, n_y, &nx, &ny, st);
   else if (nx < 0) nx = read_count(n_x, st);
   else if (ny < 0) ny = read_count(n_y, st);
-  if (nx_io) *nx_io = nx;
-  if (ny_io) *ny_io = ny;
+  if (nx_io && sync) *nx_io = nx;
+  if (ny_io && sync) *ny_io = ny;
   if (nx <= 0) return PS_OK;
   const dim3 g0 = tc_grid(nx, ny);
   const int64_t flops_tile = 2ll * BM * BN * KD;
-  g_stats[5] += (int64_t)g0.x * ((ny + BN - 1) / BN) * flops_tile;
+  if (sync) g_stats[5] += (int64_t)g0.x * ((ny + BN - 1) / BN) * flops_tile;
   nn_topk_tc<0><<<g0, kThreads, smem_bytes<0>(), st>>>(w.xt, w.yt, n_x, n_y, w.topv, w.topj, nullptr, nullptr,
                                                       nullptr, 0);
   PS_LAUNCHED("nn_topk_tc<top4>");
@@ -854,13 +857,24 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   cudaMemsetAsync(w.n_pairs, 0, sizeof(unsigned long long), st);
   cudaMemsetAsync(w.best_bits, 0xff, nx_max * sizeof(unsigned long long), st);
   cudaMemsetAsync(w.best_j, 0x7f, nx_max * sizeof(int32_t), st);
-  const int64_t n_over = read_count(w.n_overflow, st);
-  g_stats[3] += n_over;
-  if (n_over > 0) {
-    g_stats[5] += (int64_t)tc_grid(n_over, ny).x * ((ny + BN - 1) / BN) * flops_tile;
-    nn_topk_tc<1><<<tc_grid(n_over, ny), kThreads, smem_bytes<1>(), st>>>(w.xt, w.yt, w.n_overflow, n_y, nullptr,
-                                                                          nullptr, w.lim, w.pairs, w.n_pairs,
-                                                                          w.pair_cap);
+  if (sync) {
+    const int64_t n_over = read_count(w.n_overflow, st);
+    g_stats[3] += n_over;
+    if (n_over > 0) {
+      g_stats[5] += (int64_t)tc_grid(n_over, ny).x * ((ny + BN - 1) / BN) * flops_tile;
+      nn_topk_tc<1><<<tc_grid(n_over, ny), kThreads, smem_bytes<1>(), st>>>(w.xt, w.yt, w.n_overflow, n_y, nullptr,
+                                                                            nullptr, w.lim, w.pairs, w.n_pairs,
+                                                                            w.pair_cap);
+      PS_LAUNCHED("nn_topk_tc<enumerate>");
+    }
+  } else {
+    // the overflow count is unknown on the host: a grid for every row, each
+    // row block beyond *n_overflow exits at once; the few live row blocks get
+    // the widest column split (near-ties are rare, so they are few)
+    const int tiles = (int)std::max<int64_t>(1, (ny + BN - 1) / BN);
+    const dim3 ge((unsigned)((nx + BM - 1) / BM), (unsigned)std::min(kMaxSplit, tiles));
+    nn_topk_tc<1><<<ge, kThreads, smem_bytes<1>(), st>>>(w.xt, w.yt, w.n_overflow, n_y, nullptr, nullptr, w.lim,
+                                                         w.pairs, w.n_pairs, w.pair_cap);
     PS_LAUNCHED("nn_topk_tc<enumerate>");
   }
   pair_dist_min<T><<<148 * 16, 256, 0, st>>>(w.pairs, w.n_pairs, w.pair_cap, w.xsrc, y_idx, X, Y, w.pd, w.best_bits);
@@ -883,7 +897,7 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
 template <class T>
 int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double delta_s, unsigned long long* keys_pair,
                        unsigned long long* keys_delta, unsigned long long* counter, void* ws, size_t ws_bytes,
-                       cudaStream_t st) {
+                       cudaStream_t st, bool sync) {
   using namespace ps::tc;
   size_t need = 0;
   carve_tc(nullptr, n1, n2, &need);
@@ -891,7 +905,7 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   TcWs w = carve_tc(ws, n1, n2, &need);
   for (int q = 0; q < 8; ++q) g_stats[q] = 0;
   // PS_TC_PROFILE=1: per-stage timing and counters on stderr (diagnostic; syncs)
-  const bool prof = getenv("PS_TC_PROFILE") != nullptr;
+  const bool prof = sync && getenv("PS_TC_PROFILE") != nullptr;
   cudaEvent_t ev[8];
   int nev = 0;
   auto mark = [&]() {
@@ -913,7 +927,7 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   mark();
   // pass 1: rows of A (representatives) against the distinct rows of B
   int64_t ua = -1, ub = -1;
-  rc = nearest_pass(A, n1, w.a.uniq, w.a.n_uniq, B, n2, w.b.uniq, w.b.n_uniq, w.nn12, w.d12, w, st, &ua, &ub);
+  rc = nearest_pass(A, n1, w.a.uniq, w.a.n_uniq, B, n2, w.b.uniq, w.b.n_uniq, w.nn12, w.d12, w, st, &ua, &ub, sync);
   if (rc) return rc;
   g_stats[0] = ua;
   g_stats[1] = ub;
@@ -935,7 +949,7 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   PS_LAUNCHED("cub_select(columns)");
   mark();
   int64_t ncols = -1;
-  rc = nearest_pass(B, n2, w.cols, w.n_cols, A, n1, w.a.uniq, w.a.n_uniq, w.nn21, w.d21, w, st, &ncols, &ua);
+  rc = nearest_pass(B, n2, w.cols, w.n_cols, A, n1, w.a.uniq, w.a.n_uniq, w.nn21, w.d21, w, st, &ncols, &ua, sync);
   if (rc) return rc;
   mark();
   g_stats[2] = ncols;
@@ -993,6 +1007,6 @@ size_t ps_tc_nearest_ws(int64_t n1, int64_t n2) {
 }
 
 template int ps_tc_nearest_impl<float>(const float*, int64_t, const float*, int64_t, double, unsigned long long*,
-                                       unsigned long long*, unsigned long long*, void*, size_t, cudaStream_t);
+                                       unsigned long long*, unsigned long long*, void*, size_t, cudaStream_t, bool);
 template int ps_tc_nearest_impl<double>(const double*, int64_t, const double*, int64_t, double, unsigned long long*,
-                                        unsigned long long*, unsigned long long*, void*, size_t, cudaStream_t);
+                                        unsigned long long*, unsigned long long*, void*, size_t, cudaStream_t, bool);

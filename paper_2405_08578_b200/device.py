@@ -286,6 +286,71 @@ def match(desc1: torch.Tensor, desc2: torch.Tensor, delta_s: float = 0.35, strat
         cap = m  # threshold_all overflow: retry with the exact size
 
 
+def match_async(desc1: torch.Tensor, desc2: torch.Tensor, delta_s: float = 0.35, *, out_count=None, stream=None):
+    """nearest_neighbor matching enqueued with no host synchronisation
+    (ps_match_async; same results as ``match``).  Returns device tensors
+    (ref1 int32 [cap], ref2 int32 [cap], delta float64 [cap], count int64 [1]);
+    rows [0, count) are valid, sorted by (delta, ref1, ref2).  ``out_count``
+    may be a caller-provided int64 [1] view (e.g. one slot of a batch)."""
+    if delta_s <= 0:
+        raise ConfigError(f"delta_s must be positive, got {delta_s}")
+    dt = torch.float64 if (desc1.dtype == torch.float64 or desc2.dtype == torch.float64) else torch.float32
+    d1, d2 = desc1.to(dt).contiguous(), desc2.to(dt).contiguous()
+    _require_cuda(d1, "desc1")
+    n1, n2 = int(d1.shape[0]), int(d2.shape[0])
+    dim = int(d1.shape[1]) if d1.dim() == 2 else 128
+    dev = d1.device
+    cap = max(min(n1, n2), 1)
+    cnt = out_count if out_count is not None else torch.zeros(1, dtype=torch.int64, device=dev)
+    r1 = torch.empty(cap, dtype=torch.int32, device=dev)
+    r2 = torch.empty(cap, dtype=torch.int32, device=dev)
+    dl = torch.empty(cap, dtype=torch.float64, device=dev)
+    if n1 == 0 or n2 == 0:
+        cnt.zero_()
+        return r1, r2, dl, cnt
+    L = _lib.lib()
+    wsb = C.c_size_t()
+    _lib.check(L.ps_match_plan(n1, n2, dim, _lib.PS_MATCH_NEAREST, cap, C.byref(wsb)), "match")
+    ws = _workspace(wsb.value, dev)
+    _lib.check(L.ps_match_async(_ptr(d1), n1, _ptr(d2), n2, dim, int(dt == torch.float64), float(delta_s),
+                                _lib.PS_MATCH_NEAREST, _ptr(r1), _ptr(r2), _ptr(dl), _ptr(cnt), cap, _ptr(ws),
+                                wsb.value, C.c_void_p(_stream_ptr(stream))), "match")
+    return r1, r2, dl, cnt
+
+
+def match_many(pairs, delta_s: float = 0.35, *, streams=None):
+    """nearest_neighbor matching of many descriptor-set pairs with ONE host
+    synchronisation: every pair is enqueued asynchronously (round-robin over
+    ``streams`` when given, each joined back to the current stream), then all
+    match counts are read with one copy.  ``pairs`` = [(desc1, desc2), ...];
+    returns [(ref1, ref2, delta), ...] device tensors trimmed to their counts."""
+    if not pairs:
+        return []
+    dev = pairs[0][0].device
+    cur = torch.cuda.current_stream(dev)
+    counts = torch.zeros(len(pairs), dtype=torch.int64, device=dev)
+    outs = []
+    if streams:
+        ready = cur.record_event()
+        for s in streams:
+            s.wait_event(ready)
+    for q, (a, b) in enumerate(pairs):
+        s = streams[q % len(streams)] if streams else None
+        if s is not None:
+            with torch.cuda.stream(s):
+                o = match_async(a, b, delta_s, out_count=counts[q:q + 1], stream=s)
+                for t in (a, b) + o[:3]:
+                    t.record_stream(s)
+        else:
+            o = match_async(a, b, delta_s, out_count=counts[q:q + 1])
+        outs.append(o)
+    if streams:
+        for s in streams:
+            cur.wait_stream(s)
+    m = counts.cpu().tolist()
+    return [(r1[:k], r2[:k], dl[:k]) for (r1, r2, dl, _), k in zip(outs, m)]
+
+
 def pair_points(r1, r2, kp1_row, kp1_col, kp2_row, kp2_col, stream=None):
     """(x, y) = (col, row) float64 coordinates of matched pairs (registration.py:143-146)."""
     n = int(r1.shape[0])
@@ -386,6 +451,80 @@ def ransac(src: torch.Tensor, dst: torch.Tensor, iterations=2000, inlier_tol=3.0
     return RansacOutcome(ok=st == _lib.PS_OK, status=st, theta=float(model_h[0]), t_x=float(model_h[1]),
                          t_y=float(model_h[2]), inliers=inl, consensus=int(info_h[1]), rms=rms_h,
                          best_iteration=int(info_h[3]))
+
+
+def ransac_async(src: torch.Tensor, dst: torch.Tensor, iterations=2000, inlier_tol=3.0, min_inliers=8, seed=0,
+                 *, out=None, stream=None) -> torch.Tensor:
+    """``ransac`` enqueued without reading the result back: returns the
+    device result block (float64 [8 + ceil(n/8)]: model[3] | rms | info[4] as
+    int64 bits | inlier mask bytes) for ``ransac_result``.  ``out`` may be a
+    caller-provided block (e.g. one row of a batch)."""
+    if iterations < 1 or inlier_tol <= 0 or min_inliers < 2:
+        raise ConfigError("invalid RANSAC parameters")
+    n = int(src.shape[0])
+    if n < min_inliers:
+        raise RegistrationError(f"only {n} candidate pairs, need at least {min_inliers}")
+    _require_cuda(src, "src")
+    dev = src.device
+    src = src.to(torch.float64).contiguous()
+    dst = dst.to(torch.float64).contiguous()
+    samples = sample_stream_device(seed, n, iterations, dev, stream)
+    L = _lib.lib()
+    wsb = C.c_size_t()
+    _lib.check(L.ps_ransac_plan(n, iterations, C.byref(wsb)), "ransac")
+    ws = _workspace(wsb.value, dev)
+    if out is None:
+        out = torch.empty(8 + (n + 7) // 8, dtype=torch.float64, device=dev)
+    ob = out.view(torch.uint8)
+    model, rms, info, mask = out[0:3], out[3:4], out[4:8].view(torch.int64), ob[64:64 + n]
+    _lib.check(L.ps_ransac_rigid(_ptr(src), _ptr(dst), n, _ptr(samples), iterations, float(inlier_tol),
+                                 int(min_inliers), _ptr(model), _ptr(mask), _ptr(info), _ptr(rms), _ptr(ws),
+                                 wsb.value, C.c_void_p(_stream_ptr(stream))), "ransac")
+    return out
+
+
+def ransac_result(h: torch.Tensor, n: int) -> RansacOutcome:
+    """Decode a host copy of a ``ransac_async`` result block."""
+    model_h, rms_h = h[0:3].numpy(), float(h[3])
+    info_h = h[4:8].view(torch.int64).numpy()
+    inl = np.flatnonzero(h.view(torch.uint8)[64:64 + n].numpy()).astype(np.int64)
+    st = int(info_h[0])
+    return RansacOutcome(ok=st == _lib.PS_OK, status=st, theta=float(model_h[0]), t_x=float(model_h[1]),
+                         t_y=float(model_h[2]), inliers=inl, consensus=int(info_h[1]), rms=rms_h,
+                         best_iteration=int(info_h[3]))
+
+
+def ransac_many(jobs, *, streams=None) -> list:
+    """Many RANSAC runs with ONE result read-back.  ``jobs`` = [(src, dst,
+    iterations, inlier_tol, min_inliers, seed), ...] (every src with at least
+    min_inliers rows); returns [RansacOutcome, ...] in order."""
+    if not jobs:
+        return []
+    dev = jobs[0][0].device
+    width = max(8 + (int(j[0].shape[0]) + 7) // 8 for j in jobs)
+    block = torch.empty((len(jobs), width), dtype=torch.float64, device=dev)
+    cur = torch.cuda.current_stream(dev)
+    if streams:
+        ready = cur.record_event()
+        for s in streams:
+            s.wait_event(ready)
+    for q, (src, dst, iters, tol, mi, seed) in enumerate(jobs):
+        n = int(src.shape[0])
+        row = block[q, : 8 + (n + 7) // 8]
+        s = streams[q % len(streams)] if streams else None
+        if s is not None:
+            with torch.cuda.stream(s):
+                ransac_async(src, dst, iters, tol, mi, seed, out=row, stream=s)
+                src.record_stream(s)
+                dst.record_stream(s)
+        else:
+            ransac_async(src, dst, iters, tol, mi, seed, out=row)
+    if streams:
+        for s in streams:
+            cur.wait_stream(s)
+        block.record_stream(cur)
+    h = block.cpu()
+    return [ransac_result(h[q], int(j[0].shape[0])) for q, j in enumerate(jobs)]
 
 
 def estimate(src: torch.Tensor, dst: torch.Tensor, stream=None):

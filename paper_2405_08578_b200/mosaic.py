@@ -66,10 +66,12 @@ class PairwiseTransformTable:
 class GpuEngine:
     """Hot path on the local GPU through the C-ABI (device.py)."""
 
-    def __init__(self, cfg, pair_workers: int = 1):
+    def __init__(self, cfg, pair_workers: int = 1, batched: bool = True, n_streams: int = 4):
         self.cfg = cfg
         self.device = torch.device("cuda", torch.cuda.current_device())
         self.pair_workers = pair_workers  # concurrent pair registrations (host threads, one stream each)
+        self.batched = batched  # register a rank's pairs with register_many (two host syncs in all)
+        self.n_streams = n_streams  # streams the batched pairs are spread over
 
     def comm_device(self):
         return self.device
@@ -84,6 +86,41 @@ class GpuEngine:
         kp = device.detect(batch, cfg.scale_set().sizes, alpha=alpha, meta=False)
         desc = device.describe(batch, kp, cfg.descriptor_config(), alpha=alpha, scale_set=kp.scale_set)
         return kp.row, kp.col, desc, kp.count
+
+    def register_many(self, items):
+        """Every pair of ``items`` = [(ra, ca, da, na, rb, cb, db, nb, seed), ...]
+        with two host synchronisations in total: all matches enqueued
+        asynchronously and their counts read at once, then every RANSAC run
+        enqueued and all results read at once (device.match_many /
+        ransac_many; pairs spread over ``self.streams``)."""
+        from . import device
+
+        cfg = self.cfg
+        mc = cfg.matcher_config()
+        if mc.strategy != "nearest_neighbor":
+            return [self.register(*it) for it in items]
+        streams = self._streams()
+        matches = device.match_many([(it[2][: it[3]], it[6][: it[7]]) for it in items], mc.delta_s, streams=streams)
+        jobs, where = [], []
+        for q, (it, (r1, r2, _)) in enumerate(zip(items, matches)):
+            rc = cfg.ransac_config(it[8])
+            if int(r1.shape[0]) < rc.min_inliers:
+                continue
+            src, dst = device.pair_points(r1, r2, it[0], it[1], it[4], it[5])
+            jobs.append((src, dst, rc.iterations, rc.inlier_tol, rc.min_inliers, rc.seed))
+            where.append(q)
+        outs = [(False, 0.0, 0.0, 0.0, 0)] * len(items)
+        for q, o in zip(where, device.ransac_many(jobs, streams=streams)):
+            if o.ok:
+                outs[q] = (True, o.theta, o.t_x, o.t_y, int(o.inliers.shape[0]))
+        return outs
+
+    def _streams(self):
+        if self.n_streams <= 1:
+            return None
+        if getattr(self, "_stream_pool", None) is None:
+            self._stream_pool = [torch.cuda.Stream(self.device) for _ in range(self.n_streams)]
+        return self._stream_pool
 
     def register(self, ra, ca, da, na, rb, cb, db, nb, seed):
         """match + RANSAC of one pair -> (ok, theta, t_x, t_y, n_inliers)."""
@@ -154,9 +191,11 @@ def build_pairwise_table(images: Sequence, cfg, *, engine=None, group=None) -> P
     g_desc = _all_gather(pad(desc).to(dev), world, group)
     g_cnt = _all_gather(pad(cnt).to(dev), world, group)
 
+    h_cnt = g_cnt.cpu().numpy()  # one read of every image's keypoint count
+
     def img(k):  # image k lives on rank k % world, slot k // world
         r, s = k % world, k // world
-        return g_rows[r, s], g_cols[r, s], g_desc[r, s], int(g_cnt[r, s])
+        return g_rows[r, s], g_cols[r, s], g_desc[r, s], int(h_cnt[r, s])
 
     # phase 2: pairs in reference order, round-robin over ranks; on a GPU the
     # rank's pairs run concurrently on a few streams (each pair's small
@@ -172,7 +211,10 @@ def build_pairwise_table(images: Sequence, cfg, *, engine=None, group=None) -> P
         return engine.register(ra, ca, da, na, rb, cb, db, nb, pair_seed(cfg.seed, a, b))
 
     workers = getattr(engine, "pair_workers", 1)
-    if workers > 1 and len(mine_q) > 1:
+    if getattr(engine, "batched", False) and hasattr(engine, "register_many"):
+        outs = engine.register_many([img(jobs[q][0]) + img(jobs[q][1]) + (pair_seed(cfg.seed, *jobs[q]),)
+                                     for q in mine_q])
+    elif workers > 1 and len(mine_q) > 1:
         import threading
         from concurrent.futures import ThreadPoolExecutor
 
@@ -191,8 +233,9 @@ def build_pairwise_table(images: Sequence, cfg, *, engine=None, group=None) -> P
             outs = list(ex.map(run_on_stream, mine_q))
     else:
         outs = [run(q) for q in mine_q]
-    for q, (ok, th, tx, ty, ni) in zip(mine_q, outs):
-        res[q] = torch.tensor([float(ok), th, tx, ty, float(ni)], dtype=torch.float64)
+    if mine_q:  # one host-to-device copy of this rank's rows
+        res[mine_q] = torch.tensor([[float(ok), th, tx, ty, float(ni)] for ok, th, tx, ty, ni in outs],
+                                   dtype=torch.float64).to(dev)
     # gather: each pair was computed by exactly one rank, the others hold zeros
     allres = _all_gather(res, world, group).sum(dim=0).cpu().numpy()
     table = PairwiseTransformTable(n=n)

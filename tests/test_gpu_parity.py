@@ -732,3 +732,70 @@ def test_stitch_pair_and_plan_and_stitch_on_device():
     cov = comp != 0
     assert cov.mean() > 0.99
     assert float(np.sqrt(np.mean((comp[cov] - src[cov]) ** 2))) < 1.0, ref
+
+
+def test_match_many_and_ransac_many_equal_single_calls(monkeypatch):
+    """The batched, synchronisation-free pair path (ps_match_async through
+    device.match_many, device.ransac_many) gives exactly the results of the
+    one-pair calls and of the oracle, on one stream and spread over streams:
+    tensor-core pairs of C1 crops, a near-duplicate cluster pair (top-4
+    overflow + enumeration), an empty side, a CUDA-core (small) pair."""
+    cfg = R.DescriptorConfig(0.0625, 4, 64, True)
+    descs, kps = [], []
+    for p in range(2):
+        a, b = scenes.config1_pair(p)
+        for im in (a, b):
+            t = torch.from_numpy(im).cuda()
+            kp = device.detect(t, (16, 32, 64), meta=False)
+            kps.append(kp)
+            descs.append(device.describe(t, kp, cfg)[0])
+    rng = np.random.default_rng(5)
+    base = rng.random((12, 128)).astype(np.float32)
+    A = np.repeat(base, 20, axis=0)
+    A[::3, 5] = np.nextafter(A[::3, 5], np.float32(2))
+    B = base[rng.integers(0, 12, 200)] + np.where(rng.random((200, 1)) < 0.3, 0.01, 0).astype(np.float32)
+    small = torch.from_numpy(rng.random((40, 128)).astype(np.float32)).cuda()
+    pairs = [(descs[0], descs[1]), (descs[2], descs[3]), (descs[0], descs[3]),
+             (torch.from_numpy(A).cuda(), torch.from_numpy(B.astype(np.float32)).cuda()),
+             (descs[0][:0], descs[1]), (small, small.flip(0))]
+    for streams in (None, [torch.cuda.Stream() for _ in range(3)]):
+        got = device.match_many(pairs, 0.35, streams=streams)
+        for q, ((x, y), (r1, r2, dl)) in enumerate(zip(pairs, got)):
+            s1, s2, sd = device.match(x, y)
+            assert torch.equal(r1, s1) and torch.equal(r2, s2) and torch.equal(dl, sd), q
+            if q in (0, 3, 5):
+                w1, w2, wd = O.match(x.double().cpu().numpy(), y.double().cpu().numpy())
+                assert np.array_equal(r1.cpu().numpy(), w1) and np.array_equal(dl.cpu().numpy(), wd), q
+    # RANSAC of the registered C1 pairs, batched vs one call each
+    got = device.match_many(pairs[:2], 0.35)
+    jobs = []
+    for q, (r1, r2, _) in enumerate(got):
+        k1, k2 = kps[2 * q], kps[2 * q + 1]
+        src, dst = device.pair_points(r1, r2, k1.row[0], k1.col[0], k2.row[0], k2.col[0])
+        jobs.append((src, dst, 1000, 3.0, 8, 10 + q))
+    for streams in (None, [torch.cuda.Stream() for _ in range(2)]):
+        many = device.ransac_many(jobs, streams=streams)
+        for (src, dst, it, tol, mi, seed), o in zip(jobs, many):
+            one = device.ransac(src, dst, it, tol, mi, seed)
+            assert o.ok and one.ok and np.array_equal(o.inliers, one.inliers)
+            assert (o.theta, o.t_x, o.t_y, o.rms, o.consensus) == (one.theta, one.t_x, one.t_y, one.rms, one.consensus)
+            ref = O.ransac(src.cpu().numpy(), dst.cpu().numpy(), it, tol, mi, seed)
+            assert np.array_equal(o.inliers, ref["inliers"])
+
+
+def test_pairwise_table_batched_equals_per_pair():
+    """build_pairwise_table with the batched engine (two host syncs for all
+    pairs) and with one pair at a time give the same table."""
+    from paper_2405_08578_b200 import mosaic, pipeline as PL
+
+    src = scenes.scene(420, 560, 21)
+    cfg = PL.PipelineConfig(window_min=16, window_max=64, seed=3)
+    frags = [src[r0:r0 + 260, c0:c0 + 340].copy() for r0, c0 in [(0, 0), (0, 220), (160, 0), (160, 220), (80, 110)]]
+    t1 = mosaic.build_pairwise_table(frags, cfg, engine=mosaic.GpuEngine(cfg, batched=True, n_streams=3))
+    t2 = mosaic.build_pairwise_table(frags, cfg, engine=mosaic.GpuEngine(cfg, batched=False))
+    assert t1.entries.keys() == t2.entries.keys() and len(t1.entries) >= 8
+    for k, e in t1.entries.items():
+        f = t2.entries[k]
+        assert e.inlier_count == f.inlier_count
+        assert (e.transform.theta, e.transform.t_x, e.transform.t_y) == \
+               (f.transform.theta, f.transform.t_x, f.transform.t_y)
