@@ -241,15 +241,18 @@ def bench_c3_stitch(args, world, rank, dev, steps=3):
         return statistics.median(times), table, plan, placed
 
     t_pp, table1, _, _ = timed(mosaic.GpuEngine(cfg, batched=False))
-    t_b, table, plan, placed = timed(mosaic.GpuEngine(cfg))
-    assert table.entries.keys() == table1.entries.keys()
+    t_b, table2, _, _ = timed(mosaic.GpuEngine(cfg))
+    t_g, table, plan, placed = timed(mosaic.GraphEngine(cfg))
+    assert table.entries.keys() == table1.entries.keys() == table2.entries.keys()
     n_pairs = len(table.entries) // 2
     return {"metric": "9-image stitch seconds (C3: detect/describe 9 x 2688x1600, 36 pairs match + RANSAC, plan)",
-            "value": round(t_b, 4), "unit": "s", "higher_is_better": False,
-            "per_pair_calls_value": round(t_pp, 4),
-            "batching": "a rank's pairs matched asynchronously (ps_match_async) over 4 streams with one count "
-                        "read-back, then all RANSAC runs with one result read-back; per_pair_calls_value = one "
-                        "synchronous pair at a time",
+            "value": round(t_g, 4), "unit": "s", "higher_is_better": False,
+            "batched_eager_value": round(t_b, 4), "per_pair_calls_value": round(t_pp, 4),
+            "batching": "value: mosaic.GraphEngine -- the 9 images uploaded through pinned staging every step, "
+                        "detect+describe and the whole pair phase (36 x match -> point gather -> RANSAC, the "
+                        "match counts feeding RANSAC on the device) replayed as two CUDA graphs over 4 streams, "
+                        "one result read; batched_eager_value: the same chain launched eagerly (one host sync for "
+                        "all pairs); per_pair_calls_value: one synchronous pair at a time",
             "n_gpus": world, "registered_pairs": n_pairs, "placed": len(placed),
             "rounds": len(plan.rounds), "unmatched": plan.final_unmatched,
             "timing": "host wall clock around the whole call, CUDA-synchronized, max over ranks",

@@ -205,6 +205,21 @@ PS_API int ps_ransac_rigid(const double* src_xy, const double* dst_xy, int64_t n
 PS_API int ps_ransac_samples(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo,
                              int32_t has_uint32, uint32_t uinteger, int64_t n, int32_t iterations,
                              int32_t* out_samples, int32_t* scratch, void* stream);
+/* Asynchronous forms for a chain with no host round trip (match ->
+ * pair_points -> RANSAC, e.g. a pairwise table captured in one CUDA graph):
+ * the correspondence count is read on the device from *n_dev (a ps_match
+ * out_count); n_cap >= *n_dev sizes the workspace (ps_ransac_plan(n_cap)).
+ * A count below min_inliers (or below 2) yields status PS_ERR_REGISTRATION
+ * in out_info[0] instead of an error return. */
+PS_API int ps_ransac_rigid_async(const double* src_xy, const double* dst_xy, const int64_t* n_dev,
+                          int64_t n_cap, const int32_t* samples, int32_t iterations, double inlier_tol,
+                          int32_t min_inliers, double* out_model, uint8_t* out_mask,
+                          int64_t* out_info, double* out_rms, void* workspace,
+                          size_t workspace_bytes, void* stream);
+PS_API int ps_ransac_samples_async(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                            uint64_t inc_lo, int32_t has_uint32, uint32_t uinteger,
+                            const int64_t* n_dev, int32_t iterations, int32_t* out_samples,
+                            int32_t* scratch, void* stream);
 /* Least-squares rigid fit of dst ~ H(src) over all n points; out_info[0] is
  * PS_OK or PS_ERR_DEGENERATE. */
 PS_API int ps_estimate_rigid(const double* src_xy, const double* dst_xy, int64_t n,

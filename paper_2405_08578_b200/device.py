@@ -318,17 +318,15 @@ def match_async(desc1: torch.Tensor, desc2: torch.Tensor, delta_s: float = 0.35,
     return r1, r2, dl, cnt
 
 
-def match_many(pairs, delta_s: float = 0.35, *, streams=None):
-    """nearest_neighbor matching of many descriptor-set pairs with ONE host
-    synchronisation: every pair is enqueued asynchronously (round-robin over
-    ``streams`` when given, each joined back to the current stream), then all
-    match counts are read with one copy.  ``pairs`` = [(desc1, desc2), ...];
-    returns [(ref1, ref2, delta), ...] device tensors trimmed to their counts."""
+def match_many_async(pairs, delta_s: float, counts: torch.Tensor, *, streams=None) -> list:
+    """Enqueue nearest_neighbor matching of every pair with no host
+    synchronisation (capturable in a CUDA graph): pair q's count goes to
+    counts[q] (device int64).  Returns [(ref1, ref2, delta), ...] full-capacity
+    device buffers, valid rows [0, counts[q])."""
     if not pairs:
         return []
     dev = pairs[0][0].device
     cur = torch.cuda.current_stream(dev)
-    counts = torch.zeros(len(pairs), dtype=torch.int64, device=dev)
     outs = []
     if streams:
         ready = cur.record_event()
@@ -343,12 +341,25 @@ def match_many(pairs, delta_s: float = 0.35, *, streams=None):
                     t.record_stream(s)
         else:
             o = match_async(a, b, delta_s, out_count=counts[q:q + 1])
-        outs.append(o)
+        outs.append(o[:3])
     if streams:
         for s in streams:
             cur.wait_stream(s)
+    return outs
+
+
+def match_many(pairs, delta_s: float = 0.35, *, streams=None):
+    """nearest_neighbor matching of many descriptor-set pairs with ONE host
+    synchronisation: every pair is enqueued asynchronously (round-robin over
+    ``streams`` when given, each joined back to the current stream), then all
+    match counts are read with one copy.  ``pairs`` = [(desc1, desc2), ...];
+    returns [(ref1, ref2, delta), ...] device tensors trimmed to their counts."""
+    if not pairs:
+        return []
+    counts = torch.zeros(len(pairs), dtype=torch.int64, device=pairs[0][0].device)
+    outs = match_many_async(pairs, delta_s, counts, streams=streams)
     m = counts.cpu().tolist()
-    return [(r1[:k], r2[:k], dl[:k]) for (r1, r2, dl, _), k in zip(outs, m)]
+    return [(r1[:k], r2[:k], dl[:k]) for (r1, r2, dl), k in zip(outs, m)]
 
 
 def pair_points(r1, r2, kp1_row, kp1_col, kp2_row, kp2_col, stream=None):
@@ -360,6 +371,20 @@ def pair_points(r1, r2, kp1_row, kp1_col, kp2_row, kp2_col, stream=None):
     if n:
         cnt = torch.full((1,), n, dtype=torch.int64, device=dev)  # fill kernel: no host sync
         _lib.check(_lib.lib().ps_pair_points(_ptr(r1), _ptr(r2), _ptr(cnt), _ptr(kp1_row), _ptr(kp1_col),
+                                             _ptr(kp2_row), _ptr(kp2_col), _ptr(src), _ptr(dst), n,
+                                             C.c_void_p(_stream_ptr(stream))), "pair_points")
+    return src, dst
+
+
+def pair_points_dev(r1, r2, count: torch.Tensor, kp1_row, kp1_col, kp2_row, kp2_col, stream=None):
+    """``pair_points`` for full-capacity match buffers whose count is on the
+    device (int64 [1]); rows >= count are left unwritten."""
+    n = int(r1.shape[0])
+    dev = r1.device
+    src = torch.empty((n, 2), dtype=torch.float64, device=dev)
+    dst = torch.empty((n, 2), dtype=torch.float64, device=dev)
+    if n:
+        _lib.check(_lib.lib().ps_pair_points(_ptr(r1), _ptr(r2), _ptr(count), _ptr(kp1_row), _ptr(kp1_col),
                                              _ptr(kp2_row), _ptr(kp2_col), _ptr(src), _ptr(dst), n,
                                              C.c_void_p(_stream_ptr(stream))), "pair_points")
     return src, dst
@@ -481,6 +506,38 @@ def ransac_async(src: torch.Tensor, dst: torch.Tensor, iterations=2000, inlier_t
                                  int(min_inliers), _ptr(model), _ptr(mask), _ptr(info), _ptr(rms), _ptr(ws),
                                  wsb.value, C.c_void_p(_stream_ptr(stream))), "ransac")
     return out
+
+
+def ransac_async_dev(src: torch.Tensor, dst: torch.Tensor, n_dev: torch.Tensor, n_cap: int, iterations: int,
+                     inlier_tol: float, min_inliers: int, seed: int, out: torch.Tensor, stream=None) -> None:
+    """RANSAC whose correspondence count exists only on the device (n_dev,
+    int64 [1], e.g. a match count; src/dst hold >= n_cap rows): the sample
+    stream and every kernel read the count there, so a match -> RANSAC chain
+    needs no host round trip (ps_ransac_samples_async / ps_ransac_rigid_async).
+    Writes the ``ransac_async`` result block layout into ``out`` (length
+    >= 8 + ceil(n_cap / 8)); a count below min_inliers reports
+    PS_ERR_REGISTRATION in its status word."""
+    if iterations < 1 or inlier_tol <= 0 or min_inliers < 2:
+        raise ConfigError("invalid RANSAC parameters")
+    if n_cap < min_inliers:
+        raise RegistrationError(f"only {n_cap} candidate pairs, need at least {min_inliers}")
+    dev = src.device
+    st, inc, has_u32, u32 = _pcg_state(int(seed))
+    m64 = (1 << 64) - 1
+    smp = torch.empty(2 * iterations + 1, dtype=torch.int32, device=dev)
+    L = _lib.lib()
+    sp = C.c_void_p(_stream_ptr(stream))
+    _lib.check(L.ps_ransac_samples_async(st >> 64, st & m64, inc >> 64, inc & m64, has_u32, u32, _ptr(n_dev),
+                                         int(iterations), _ptr(smp), C.c_void_p(smp.data_ptr() + 8 * iterations),
+                                         sp), "ransac_samples")
+    wsb = C.c_size_t()
+    _lib.check(L.ps_ransac_plan(n_cap, iterations, C.byref(wsb)), "ransac")
+    ws = _workspace(wsb.value, dev)
+    ob = out.view(torch.uint8)
+    _lib.check(L.ps_ransac_rigid_async(_ptr(src), _ptr(dst), _ptr(n_dev), int(n_cap), _ptr(smp), int(iterations),
+                                       float(inlier_tol), int(min_inliers), _ptr(out[0:3]),
+                                       C.c_void_p(ob.data_ptr() + 64), _ptr(out[4:8]), _ptr(out[3:4]), _ptr(ws),
+                                       wsb.value, sp), "ransac")
 
 
 def ransac_result(h: torch.Tensor, n: int) -> RansacOutcome:

@@ -78,10 +78,13 @@ class GpuEngine:
 
     def prepare(self, images: list) -> tuple:
         """images -> (rows int32 [B, cap], cols, desc float32 [B, cap, D], count int32 [B]) on device."""
+        batch = torch.stack([torch.from_numpy(np.ascontiguousarray(im)) for im in images]).to(self.device)
+        return self._prepare_dev(batch)
+
+    def _prepare_dev(self, batch: torch.Tensor) -> tuple:
         from . import device
 
         cfg = self.cfg
-        batch = torch.stack([torch.from_numpy(np.ascontiguousarray(im)) for im in images]).to(self.device)
         alpha = cfg.alpha if cfg.alpha is not None else device.default_alpha(batch.shape[1], batch.shape[2])
         kp = device.detect(batch, cfg.scale_set().sizes, alpha=alpha, meta=False)
         desc = device.describe(batch, kp, cfg.descriptor_config(), alpha=alpha, scale_set=kp.scale_set)
@@ -89,31 +92,63 @@ class GpuEngine:
 
     def register_many(self, items):
         """Every pair of ``items`` = [(ra, ca, da, na, rb, cb, db, nb, seed), ...]
-        with two host synchronisations in total: all matches enqueued
-        asynchronously and their counts read at once, then every RANSAC run
-        enqueued and all results read at once (device.match_many /
-        ransac_many; pairs spread over ``self.streams``)."""
+        with ONE host synchronisation: all matches, point gathers and RANSAC
+        runs are enqueued back to back (device.match_many_async, the match
+        counts stay on the device and feed ransac_async_dev; pairs spread over
+        ``self.streams``), then the result words of every pair are read at once."""
+        cfg = self.cfg
+        if cfg.matcher_config().strategy != "nearest_neighbor":
+            return [self.register(*it) for it in items]
+        block, live = self._pairs_dev(items)
+        return self._decode(block[:, :8].cpu(), live)
+
+    def _pairs_dev(self, items):
+        """Enqueue the whole pair phase; returns (result block [P, W] float64,
+        live flags).  No host synchronisation (capturable in a CUDA graph)."""
         from . import device
 
         cfg = self.cfg
         mc = cfg.matcher_config()
-        if mc.strategy != "nearest_neighbor":
-            return [self.register(*it) for it in items]
         streams = self._streams()
-        matches = device.match_many([(it[2][: it[3]], it[6][: it[7]]) for it in items], mc.delta_s, streams=streams)
-        jobs, where = [], []
-        for q, (it, (r1, r2, _)) in enumerate(zip(items, matches)):
+        counts = torch.zeros(len(items), dtype=torch.int64, device=self.device)
+        outs = device.match_many_async([(it[2][: it[3]], it[6][: it[7]]) for it in items], mc.delta_s, counts,
+                                       streams=streams)
+        caps = [min(int(it[3]), int(it[7])) for it in items]
+        width = 8 + (max(caps + [8]) + 7) // 8
+        block = torch.zeros((len(items), width), dtype=torch.float64, device=self.device)
+        live = [False] * len(items)
+        cur = torch.cuda.current_stream(self.device)
+        if streams:
+            ready = cur.record_event()
+            for s in streams:
+                s.wait_event(ready)
+        for q, (it, (r1, r2, _)) in enumerate(zip(items, outs)):
             rc = cfg.ransac_config(it[8])
-            if int(r1.shape[0]) < rc.min_inliers:
+            if caps[q] < rc.min_inliers:  # cannot reach min_inliers whatever the count (registration.py:158-162)
                 continue
-            src, dst = device.pair_points(r1, r2, it[0], it[1], it[4], it[5])
-            jobs.append((src, dst, rc.iterations, rc.inlier_tol, rc.min_inliers, rc.seed))
-            where.append(q)
-        outs = [(False, 0.0, 0.0, 0.0, 0)] * len(items)
-        for q, o in zip(where, device.ransac_many(jobs, streams=streams)):
-            if o.ok:
-                outs[q] = (True, o.theta, o.t_x, o.t_y, int(o.inliers.shape[0]))
-        return outs
+            live[q] = True
+            s = streams[q % len(streams)] if streams else None
+            with torch.cuda.stream(s) if s is not None else _nullcontext():
+                src, dst = device.pair_points_dev(r1, r2, counts[q:q + 1], it[0], it[1], it[4], it[5])
+                device.ransac_async_dev(src, dst, counts[q:q + 1], caps[q], rc.iterations, rc.inlier_tol,
+                                        rc.min_inliers, rc.seed, block[q])
+        if streams:
+            for s in streams:
+                cur.wait_stream(s)
+        return block, live
+
+    @staticmethod
+    def _decode(h: torch.Tensor, live) -> list:
+        from . import _lib
+
+        out = []
+        info = h[:, 4:8].contiguous().view(torch.int64)
+        for q, ok in enumerate(live):
+            if ok and int(info[q, 0]) == _lib.PS_OK:
+                out.append((True, float(h[q, 0]), float(h[q, 1]), float(h[q, 2]), int(info[q, 2])))
+            else:
+                out.append((False, 0.0, 0.0, 0.0, 0))
+        return out
 
     def _streams(self):
         if self.n_streams <= 1:
@@ -136,6 +171,79 @@ class GpuEngine:
         if not out.ok:
             return (False, 0.0, 0.0, 0.0, 0)
         return (True, out.theta, out.t_x, out.t_y, int(out.inliers.shape[0]))
+
+
+class GraphEngine(GpuEngine):
+    """GpuEngine for repeated tables of same-shaped image sets (e.g. a camera
+    rig stitched frame after frame): each phase is captured once as a CUDA
+    graph and then replayed, so the ~40 kernels per pair and the per-image
+    detect/describe cost one graph launch per phase instead of ~1,500 host
+    launches.  Inputs are re-uploaded (pinned staging) and everything is
+    recomputed on every call; a phase is re-captured when its shapes, counts
+    or input addresses change."""
+
+    def __init__(self, cfg, n_streams: int = 4):
+        super().__init__(cfg, batched=True, n_streams=n_streams)
+        self._prep_graphs = {}
+        self._pair_graphs = {}
+
+    def prepare(self, images: list) -> tuple:
+        arrs = [np.asarray(im) for im in images]
+        key = (len(arrs), arrs[0].shape, arrs[0].dtype.str)
+        ent = self._prep_graphs.get(key)
+        if ent is None:
+            pinned = torch.empty((len(arrs),) + arrs[0].shape, dtype=torch.from_numpy(arrs[0][:1]).dtype,
+                                 pin_memory=True)
+            static = torch.empty(pinned.shape, dtype=pinned.dtype, device=self.device)
+            ent = {"pinned": pinned, "static": static, "graph": None, "done": None}
+            self._prep_graphs[key] = ent
+        self._upload(arrs, ent)
+        if ent["graph"] is None:
+            self._prepare_dev(ent["static"])  # eager warm-up (attributes, allocator) ...
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):  # ... then capture
+                ent["outs"] = self._prepare_dev(ent["static"])
+            ent["graph"] = g
+        ent["graph"].replay()
+        return ent["outs"]
+
+    def _upload(self, arrs, ent):
+        if ent["done"] is not None:
+            ent["done"].synchronize()  # the previous copy out of the pinned buffer has finished
+        pv = ent["pinned"].numpy()
+        for k, a in enumerate(arrs):
+            np.copyto(pv[k], a)
+        ent["static"].copy_(ent["pinned"], non_blocking=True)
+        ent["done"] = torch.cuda.current_stream(self.device).record_event()
+
+    def register_many(self, items):
+        if self.cfg.matcher_config().strategy != "nearest_neighbor":
+            return [self.register(*it) for it in items]
+        key = tuple((it[0].data_ptr(), it[1].data_ptr(), it[2].data_ptr(), int(it[3]), it[4].data_ptr(),
+                     it[5].data_ptr(), it[6].data_ptr(), int(it[7]), int(it[8])) for it in items)
+        ent = self._pair_graphs.get(key)
+        if ent is None:
+            block, live = self._pairs_dev(items)  # eager warm-up; its results are this call's
+            res = self._decode(block[:, :8].cpu(), live)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                gblock, glive = self._pairs_dev(items)
+            if len(self._pair_graphs) > 8:
+                self._pair_graphs.clear()
+            self._pair_graphs[key] = (g, gblock, glive)
+            return res
+        g, block, live = ent
+        g.replay()
+        return self._decode(block[:, :8].cpu(), live)
+
+
+class _nullcontext:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
 
 
 # ---- distributed table -------------------------------------------------------------------

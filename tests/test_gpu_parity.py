@@ -793,9 +793,17 @@ def test_pairwise_table_batched_equals_per_pair():
     frags = [src[r0:r0 + 260, c0:c0 + 340].copy() for r0, c0 in [(0, 0), (0, 220), (160, 0), (160, 220), (80, 110)]]
     t1 = mosaic.build_pairwise_table(frags, cfg, engine=mosaic.GpuEngine(cfg, batched=True, n_streams=3))
     t2 = mosaic.build_pairwise_table(frags, cfg, engine=mosaic.GpuEngine(cfg, batched=False))
+    ge = mosaic.GraphEngine(cfg, n_streams=3)
+    t3 = mosaic.build_pairwise_table(frags, cfg, engine=ge)  # eager warm-up + capture
+    t4 = mosaic.build_pairwise_table(frags, cfg, engine=ge)  # graph replays
+    other = [f[::-1].copy() for f in frags]  # new pixels through the same graphs
+    t5 = mosaic.build_pairwise_table(other, cfg, engine=ge)
+    t6 = mosaic.build_pairwise_table(other, cfg, engine=mosaic.GpuEngine(cfg, batched=False))
     assert t1.entries.keys() == t2.entries.keys() and len(t1.entries) >= 8
-    for k, e in t1.entries.items():
-        f = t2.entries[k]
-        assert e.inlier_count == f.inlier_count
-        assert (e.transform.theta, e.transform.t_x, e.transform.t_y) == \
-               (f.transform.theta, f.transform.t_x, f.transform.t_y)
+    for ta, tb in ((t1, t2), (t3, t2), (t4, t2), (t5, t6)):
+        assert ta.entries.keys() == tb.entries.keys()
+        for k, e in ta.entries.items():
+            f = tb.entries[k]
+            assert e.inlier_count == f.inlier_count
+            assert (e.transform.theta, e.transform.t_x, e.transform.t_y) == \
+                   (f.transform.theta, f.transform.t_x, f.transform.t_y)
