@@ -807,3 +807,32 @@ def test_pairwise_table_batched_equals_per_pair():
             assert e.inlier_count == f.inlier_count
             assert (e.transform.theta, e.transform.t_x, e.transform.t_y) == \
                    (f.transform.theta, f.transform.t_x, f.transform.t_y)
+
+
+def test_ransac_with_device_count_equals_host_count():
+    """ps_ransac_rigid_async reads the correspondence count on the device:
+    same result as the host-count call for the prefix of a larger buffer, and
+    PS_ERR_REGISTRATION in the status word when the count is below
+    min_inliers (registration.py:158-162)."""
+    from paper_2405_08578_b200 import _lib
+
+    rng = np.random.default_rng(2)
+    n = 900
+    src = rng.uniform(0, 800, (n, 2))
+    th = 0.1
+    R2 = np.array([[math.cos(th), -math.sin(th)], [math.sin(th), math.cos(th)]])
+    dst = src @ R2.T + [20.0, -7.0] + rng.normal(0, 0.8, (n, 2))
+    dst[::3] = rng.uniform(0, 800, (len(dst[::3]), 2))
+    S, D = torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda()
+    for m, seed in ((900, 0), (437, 5), (9, 1), (5, 2), (1, 3), (0, 4)):
+        cnt = torch.tensor([m], dtype=torch.int64, device="cuda")
+        out = torch.zeros(8 + (n + 7) // 8, dtype=torch.float64, device="cuda")
+        device.ransac_async_dev(S, D, cnt, n, 700, 3.0, 8, seed, out)
+        got = device.ransac_result(out.cpu(), m)
+        if m < 8:
+            assert got.status == _lib.PS_ERR_REGISTRATION and not got.ok, m
+            continue
+        one = device.ransac(S[:m], D[:m], 700, 3.0, 8, seed)
+        assert got.ok == one.ok and np.array_equal(got.inliers, one.inliers), m
+        assert (got.theta, got.t_x, got.t_y, got.rms, got.consensus) == (one.theta, one.t_x, one.t_y, one.rms,
+                                                                          one.consensus)
