@@ -219,6 +219,7 @@ def bench_c3_stitch(args, world, rank, dev, steps=3):
     from paper_2405_08578_b200.pipeline import PipelineConfig
 
     images, truth = scenes.config3_images(0)
+    images = [torch.from_numpy(np.ascontiguousarray(im)).pin_memory() for im in images]  # host inputs, pinned
     ids = [f"img{k}" for k in range(9)]
     cfg = PipelineConfig(window_min=32, window_max=128, ransac_iters=2000, ransac_tol=3.0)
     def timed(engine):
@@ -248,7 +249,7 @@ def bench_c3_stitch(args, world, rank, dev, steps=3):
     return {"metric": "9-image stitch seconds (C3: detect/describe 9 x 2688x1600, 36 pairs match + RANSAC, plan)",
             "value": round(t_g, 4), "unit": "s", "higher_is_better": False,
             "batched_eager_value": round(t_b, 4), "per_pair_calls_value": round(t_pp, 4),
-            "batching": "value: mosaic.GraphEngine -- the 9 images uploaded through pinned staging every step, "
+            "batching": "value: mosaic.GraphEngine -- the 9 images (pinned host memory) uploaded every step, "
                         "detect+describe and the whole pair phase (36 x match -> point gather -> RANSAC, the "
                         "match counts feeding RANSAC on the device) replayed as two CUDA graphs over 4 streams, "
                         "one result read; batched_eager_value: the same chain launched eagerly (one host sync for "

@@ -515,8 +515,8 @@ __global__ void pair_argmin(const unsigned long long* __restrict__ pairs, const 
 
 __global__ void pair_write(const int32_t* __restrict__ n_overflow, const int32_t* __restrict__ xsrc,
                            const unsigned long long* __restrict__ best_bits, const int* __restrict__ best_j,
-                           int32_t* __restrict__ nn, double* __restrict__ dist) {
-  const int n = *n_overflow;
+                           int32_t* __restrict__ nn, double* __restrict__ dist, int enum_rows) {
+  const int n = min(*n_overflow, enum_rows);  // rows beyond were not enumerated (exact_rows decides them)
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
     nn[xsrc[q]] = best_j[q];
     dist[xsrc[q]] = __longlong_as_double((long long)best_bits[q]);
@@ -528,12 +528,14 @@ template <class T>
 __global__ void exact_rows(const int32_t* __restrict__ rows, const int32_t* __restrict__ n_rows,
                            const int32_t* __restrict__ x_orig, const T* __restrict__ X, const T* __restrict__ Y,
                            int64_t ny, int32_t* __restrict__ nn, double* __restrict__ dist,
-                           const unsigned long long* __restrict__ n_pairs, int64_t cap) {
+                           const unsigned long long* __restrict__ n_pairs, int64_t cap, int enum_rows) {
   __shared__ double sd[32];
   __shared__ int sj[32];
-  if (n_pairs && (int64_t)*n_pairs <= cap) return;  // the enumeration was complete
+  // rows [0, enum_rows) were enumerated on the tensor cores; when their pairs
+  // fit the buffer only the rows beyond need the exact scan
+  const int q0 = (n_pairs && (int64_t)*n_pairs <= cap) ? enum_rows : 0;
   const int n = *n_rows;
-  for (int q = blockIdx.x; q < n; q += gridDim.x) {
+  for (int q = q0 + blockIdx.x; q < n; q += gridDim.x) {
     const int u = rows[q];
     const int xi = x_orig ? x_orig[u] : u;
     double bd = INFINITY;
@@ -692,6 +694,9 @@ inline int64_t rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
 constexpr int kMaxSplit = 8;
 constexpr int kSMs = 148;
+// asynchronous mode: row blocks of the near-tie enumeration launched blind
+// (the rest of a larger overflow list is decided by the exact scan)
+constexpr int kEnumBlocksAsync = 4;
 
 // statistics of the last tensor-core match on this thread (ps_match_stats)
 thread_local int64_t g_stats[8];  // uniq_a, uniq_b, cols, overflow rows, enumerated pairs, mma flops, -, -
@@ -857,6 +862,7 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   cudaMemsetAsync(w.n_pairs, 0, sizeof(unsigned long long), st);
   cudaMemsetAsync(w.best_bits, 0xff, nx_max * sizeof(unsigned long long), st);
   cudaMemsetAsync(w.best_j, 0x7f, nx_max * sizeof(int32_t), st);
+  int enum_rows = INT32_MAX;
   if (sync) {
     const int64_t n_over = read_count(w.n_overflow, st);
     g_stats[3] += n_over;
@@ -872,7 +878,8 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
     // row block beyond *n_overflow exits at once; the few live row blocks get
     // the widest column split (near-ties are rare, so they are few)
     const int tiles = (int)std::max<int64_t>(1, (ny + BN - 1) / BN);
-    const dim3 ge((unsigned)((nx + BM - 1) / BM), (unsigned)std::min(kMaxSplit, tiles));
+    const dim3 ge((unsigned)std::min<int64_t>(kEnumBlocksAsync, (nx + BM - 1) / BM), (unsigned)std::min(kMaxSplit, tiles));
+    enum_rows = (int)ge.x * BM;  // overflow rows beyond these take the exact scan
     nn_topk_tc<1><<<ge, kThreads, smem_bytes<1>(), st>>>(w.xt, w.yt, w.n_overflow, n_y, nullptr, nullptr, w.lim,
                                                          w.pairs, w.n_pairs, w.pair_cap);
     PS_LAUNCHED("nn_topk_tc<enumerate>");
@@ -881,10 +888,11 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   PS_LAUNCHED("pair_dist_min");
   pair_argmin<T><<<148 * 8, 256, 0, st>>>(w.pairs, w.n_pairs, w.pair_cap, y_idx, w.pd, w.best_bits, w.best_j);
   PS_LAUNCHED("pair_argmin");
-  pair_write<<<grid_for(nx_max, 256), 256, 0, st>>>(w.n_overflow, w.xsrc, w.best_bits, w.best_j, nn, dist);
+  pair_write<<<grid_for(nx_max, 256), 256, 0, st>>>(w.n_overflow, w.xsrc, w.best_bits, w.best_j, nn, dist,
+                                                     enum_rows);
   PS_LAUNCHED("pair_write");
   exact_rows<T><<<148 * 4, 256, 0, st>>>(w.overflow, w.n_overflow, x_idx, X, Y, ny_all, nn, dist, w.n_pairs,
-                                         w.pair_cap);
+                                         w.pair_cap, enum_rows);
   PS_LAUNCHED("exact_rows");
   return PS_OK;
 }

@@ -78,7 +78,8 @@ class GpuEngine:
 
     def prepare(self, images: list) -> tuple:
         """images -> (rows int32 [B, cap], cols, desc float32 [B, cap, D], count int32 [B]) on device."""
-        batch = torch.stack([torch.from_numpy(np.ascontiguousarray(im)) for im in images]).to(self.device)
+        batch = torch.stack([im if isinstance(im, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(im))
+                             for im in images]).to(self.device)
         return self._prepare_dev(batch)
 
     def _prepare_dev(self, batch: torch.Tensor) -> tuple:
@@ -188,12 +189,12 @@ class GraphEngine(GpuEngine):
         self._pair_graphs = {}
 
     def prepare(self, images: list) -> tuple:
-        arrs = [np.asarray(im) for im in images]
-        key = (len(arrs), arrs[0].shape, arrs[0].dtype.str)
+        arrs = [im if isinstance(im, torch.Tensor) else np.asarray(im) for im in images]
+        key = (len(arrs), tuple(arrs[0].shape), str(arrs[0].dtype))
         ent = self._prep_graphs.get(key)
         if ent is None:
-            pinned = torch.empty((len(arrs),) + arrs[0].shape, dtype=torch.from_numpy(arrs[0][:1]).dtype,
-                                 pin_memory=True)
+            dt = arrs[0].dtype if isinstance(arrs[0], torch.Tensor) else torch.from_numpy(arrs[0][:1]).dtype
+            pinned = torch.empty((len(arrs),) + tuple(arrs[0].shape), dtype=dt, pin_memory=True)
             static = torch.empty(pinned.shape, dtype=pinned.dtype, device=self.device)
             ent = {"pinned": pinned, "static": static, "graph": None, "done": None}
             self._prep_graphs[key] = ent
@@ -209,13 +210,18 @@ class GraphEngine(GpuEngine):
         return ent["outs"]
 
     def _upload(self, arrs, ent):
+        if all(isinstance(a, torch.Tensor) and a.is_pinned() for a in arrs):  # caller-pinned: straight to HBM
+            for k, a in enumerate(arrs):
+                ent["static"][k].copy_(a, non_blocking=True)
+            return
         if ent["done"] is not None:
             ent["done"].synchronize()  # the previous copy out of the pinned buffer has finished
         pv = ent["pinned"].numpy()
-        for k, a in enumerate(arrs):
-            np.copyto(pv[k], a)
-        ent["static"].copy_(ent["pinned"], non_blocking=True)
-        ent["done"] = torch.cuda.current_stream(self.device).record_event()
+        cur = torch.cuda.current_stream(self.device)
+        for k, a in enumerate(arrs):  # image k's upload overlaps the staging of image k + 1
+            np.copyto(pv[k], a.numpy() if isinstance(a, torch.Tensor) else a)
+            ent["static"][k].copy_(ent["pinned"][k], non_blocking=True)
+        ent["done"] = cur.record_event()
 
     def register_many(self, items):
         if self.cfg.matcher_config().strategy != "nearest_neighbor":
@@ -281,9 +287,9 @@ def build_pairwise_table(images: Sequence, cfg, *, engine=None, group=None) -> P
     # phase 1: my images (k % world == rank); slots padded to `per` images per rank
     mine = list(range(rank, n, world))
     per = -(-n // world)
-    rows, cols, desc, cnt = engine.prepare([np.asarray(images[k]) for k in mine]) if mine else (None,) * 4
+    rows, cols, desc, cnt = engine.prepare([images[k] for k in mine]) if mine else (None,) * 4
     if rows is None:  # ranks without images contribute empty slots of the agreed shape
-        probe = engine.prepare([np.asarray(images[0])])
+        probe = engine.prepare([images[0]])
         rows, cols, desc, cnt = (x[:0] for x in probe)
     cap, D = desc.shape[1], desc.shape[2]
 

@@ -755,15 +755,22 @@ def test_match_many_and_ransac_many_equal_single_calls(monkeypatch):
     A[::3, 5] = np.nextafter(A[::3, 5], np.float32(2))
     B = base[rng.integers(0, 12, 200)] + np.where(rng.random((200, 1)) < 0.3, 0.01, 0).astype(np.float32)
     small = torch.from_numpy(rng.random((40, 128)).astype(np.float32)).cuda()
+    # > 512 distinct rows with near-tied candidates: beyond the blind
+    # enumeration row blocks of the asynchronous mode, the exact scan decides
+    cl = base[rng.integers(0, 12, 1500)].copy()
+    cl[np.arange(1500), rng.integers(0, 128, 1500)] += np.float32(1e-6)
+    cb = base[rng.integers(0, 12, 900)].copy()
+    cb[np.arange(900), rng.integers(0, 128, 900)] -= np.float32(1e-6)
     pairs = [(descs[0], descs[1]), (descs[2], descs[3]), (descs[0], descs[3]),
              (torch.from_numpy(A).cuda(), torch.from_numpy(B.astype(np.float32)).cuda()),
-             (descs[0][:0], descs[1]), (small, small.flip(0))]
+             (descs[0][:0], descs[1]), (small, small.flip(0)),
+             (torch.from_numpy(cl).cuda(), torch.from_numpy(cb).cuda())]
     for streams in (None, [torch.cuda.Stream() for _ in range(3)]):
         got = device.match_many(pairs, 0.35, streams=streams)
         for q, ((x, y), (r1, r2, dl)) in enumerate(zip(pairs, got)):
             s1, s2, sd = device.match(x, y)
             assert torch.equal(r1, s1) and torch.equal(r2, s2) and torch.equal(dl, sd), q
-            if q in (0, 3, 5):
+            if q in (0, 3, 5, 6):
                 w1, w2, wd = O.match(x.double().cpu().numpy(), y.double().cpu().numpy())
                 assert np.array_equal(r1.cpu().numpy(), w1) and np.array_equal(dl.cpu().numpy(), wd), q
     # RANSAC of the registered C1 pairs, batched vs one call each
