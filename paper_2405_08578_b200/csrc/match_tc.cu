@@ -535,6 +535,7 @@ __global__ void exact_rows(const int32_t* __restrict__ rows, const int32_t* __re
   // fit the buffer only the rows beyond need the exact scan
   const int q0 = (n_pairs && (int64_t)*n_pairs <= cap) ? enum_rows : 0;
   const int n = *n_rows;
+  if (q0 >= n) return;
   for (int q = q0 + blockIdx.x; q < n; q += gridDim.x) {
     const int u = rows[q];
     const int xi = x_orig ? x_orig[u] : u;
