@@ -82,11 +82,15 @@ class GpuEngine:
                              for im in images]).to(self.device)
         return self._prepare_dev(batch)
 
-    def _prepare_dev(self, batch: torch.Tensor) -> tuple:
+    def _prepare_dev(self, batch) -> tuple:
+        """detect + describe a device batch (uint8 [B, nr, nc] tensor or device.DeviceImages, e.g. RGB)."""
         from . import device
 
         cfg = self.cfg
-        alpha = cfg.alpha if cfg.alpha is not None else device.default_alpha(batch.shape[1], batch.shape[2])
+        nr, nc = (batch.nr, batch.nc) if isinstance(batch, device.DeviceImages) else batch.shape[1:3]
+        alpha = cfg.alpha if cfg.alpha is not None else device.default_alpha(nr, nc)
+        if isinstance(batch, device.DeviceImages):
+            alpha = batch.alpha
         kp = device.detect(batch, cfg.scale_set().sizes, alpha=alpha, meta=False)
         desc = device.describe(batch, kp, cfg.descriptor_config(), alpha=alpha, scale_set=kp.scale_set)
         return kp.row, kp.col, desc, kp.count
@@ -206,6 +210,25 @@ class GraphEngine(GpuEngine):
             with torch.cuda.graph(g):  # ... then capture
                 ent["outs"] = self._prepare_dev(ent["static"])
             ent["graph"] = g
+        ent["graph"].replay()
+        return ent["outs"]
+
+    def prepare_device(self, batch) -> tuple:
+        """detect + describe of a device-resident batch (uint8 tensor or
+        device.DeviceImages) as a replayed CUDA graph; the batch's memory is
+        the graph's input (re-captured when its address or shape changes)."""
+        from . import device
+
+        data = batch.data if isinstance(batch, device.DeviceImages) else batch
+        key = ("dev", data.data_ptr(), tuple(data.shape), str(data.dtype))
+        ent = self._prep_graphs.get(key)
+        if ent is None:
+            self._prepare_dev(batch)  # eager warm-up
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                outs = self._prepare_dev(batch)
+            ent = self._prep_graphs[key] = {"graph": g, "outs": outs}
         ent["graph"].replay()
         return ent["outs"]
 
