@@ -131,7 +131,8 @@ def _warp_crop(src: np.ndarray, r0: int, c0: int, h: int, w: int, theta: float, 
     return map_coordinates(src.astype(np.float64), [sy, sx], order=1, mode="nearest")
 
 
-def config3_images(seed: int = 0) -> tuple[list, list]:
+def config3_images(seed: int = 0, rot_deg: float = 5.0, scale_range=(0.95, 1.05),
+                   noise: float = 2.0) -> tuple[list, list]:
     """C3: 3x3 grid of 1600x2688 crops of scene(4200, 7000).
 
     Each crop gets rotation U[-5, 5] deg and scale U[0.95, 1.05] about its
@@ -145,9 +146,9 @@ def config3_images(seed: int = 0) -> tuple[list, list]:
     out, truth = [], []
     for r0 in (180, 1300, 2420):
         for c0 in (274, 2156, 4037):
-            theta = math.radians(rng.uniform(-5.0, 5.0))
-            sc = rng.uniform(0.95, 1.05)
-            img = _warp_crop(src, r0, c0, h, w, theta, sc) + rng.normal(0.0, 2.0, size=(h, w))
+            theta = math.radians(rng.uniform(-rot_deg, rot_deg))  # the defaults are the config; other
+            sc = rng.uniform(*scale_range)  # values (diagnostics) consume the same draws
+            img = _warp_crop(src, r0, c0, h, w, theta, sc) + rng.normal(0.0, noise, size=(h, w))
             out.append(np.clip(np.rint(img), 0, 255).astype(np.uint8))
             truth.append((r0, c0, theta, sc))
     order = np.random.default_rng(seed).permutation(9)
