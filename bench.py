@@ -246,6 +246,12 @@ def bench_c3_stitch(args, world, rank, dev, steps=3):
     t_g, table, plan, placed = timed(mosaic.GraphEngine(cfg))
     assert table.entries.keys() == table1.entries.keys() == table2.entries.keys()
     n_pairs = len(table.entries) // 2
+    # control (untimed): the same generator with the perturbations off registers the overlapping pairs --
+    # the timed set registers none because LP-SIFT's window peaks do not survive its rotation / noise
+    # (tools/c3_variants.py; the CPU oracle agrees pair by pair)
+    ctl_images, _ = scenes.config3_images(0, rot_deg=0.0, scale_range=(1.0, 1.0), noise=0.0)
+    ctl = mosaic.build_pairwise_table(ctl_images, cfg)
+    _, ctl_placed = mosaic.plan_mosaic(ctl, ids)
     return {"metric": "9-image stitch seconds (C3: detect/describe 9 x 2688x1600, 36 pairs match + RANSAC, plan)",
             "value": round(t_g, 4), "unit": "s", "higher_is_better": False,
             "batched_eager_value": round(t_b, 4), "per_pair_calls_value": round(t_pp, 4),
@@ -256,6 +262,7 @@ def bench_c3_stitch(args, world, rank, dev, steps=3):
                         "all pairs); per_pair_calls_value: one synchronous pair at a time",
             "n_gpus": world, "registered_pairs": n_pairs, "placed": len(placed),
             "rounds": len(plan.rounds), "unmatched": plan.final_unmatched,
+            "control_translation_only_noise0": {"registered_pairs": len(ctl.entries) // 2, "placed": len(ctl_placed)},
             "timing": "host wall clock around the whole call, CUDA-synchronized, max over ranks",
             "parallelism": f"images then pairs sharded over {world} rank(s); NCCL all-gather of keypoint/descriptor "
                            "slots and of the pair results"}

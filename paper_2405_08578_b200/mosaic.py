@@ -187,7 +187,7 @@ class GraphEngine(GpuEngine):
     recomputed on every call; a phase is re-captured when its shapes, counts
     or input addresses change."""
 
-    def __init__(self, cfg, n_streams: int = 4):
+    def __init__(self, cfg, n_streams: int = 8):
         super().__init__(cfg, batched=True, n_streams=n_streams)
         self._prep_graphs = {}
         self._pair_graphs = {}
