@@ -191,6 +191,7 @@ class GraphEngine(GpuEngine):
         super().__init__(cfg, batched=True, n_streams=n_streams)
         self._prep_graphs = {}
         self._pair_graphs = {}
+        self.gather_cache = {}  # build_pairwise_table's all-gather outputs, kept at fixed addresses
 
     def prepare(self, images: list) -> tuple:
         arrs = [im if isinstance(im, torch.Tensor) else np.asarray(im) for im in images]
@@ -285,12 +286,21 @@ def _group_info(group):
     return dist.get_rank(group), dist.get_world_size(group)
 
 
-def _all_gather(t: torch.Tensor, world: int, group) -> torch.Tensor:
+def _all_gather(t: torch.Tensor, world: int, group, cache: dict | None = None, tag: str = "") -> torch.Tensor:
+    """All-gather of equal-shaped slots -> [world, ...].  With ``cache`` the
+    output buffer is kept per (tag, shape, dtype) so its address is stable
+    across calls (graph-replaying engines key their graphs on it)."""
     import torch.distributed as dist
 
     if world == 1:
         return t.unsqueeze(0)
-    out = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    shape = (world * t.shape[0],) + tuple(t.shape[1:])
+    key = (tag, shape, t.dtype)
+    out = cache.get(key) if cache is not None else None
+    if out is None:
+        out = torch.empty(shape, dtype=t.dtype, device=t.device)
+        if cache is not None:
+            cache[key] = out
     dist.all_gather_into_tensor(out, t.contiguous(), group=group)
     return out.view((world,) + tuple(t.shape))
 
@@ -323,10 +333,11 @@ def build_pairwise_table(images: Sequence, cfg, *, engine=None, group=None) -> P
         return torch.cat([t, extra])
 
     # exchange: every rank receives every image's slots (image k = slot k // world ... see order below)
-    g_rows = _all_gather(pad(rows).to(dev), world, group)
-    g_cols = _all_gather(pad(cols).to(dev), world, group)
-    g_desc = _all_gather(pad(desc).to(dev), world, group)
-    g_cnt = _all_gather(pad(cnt).to(dev), world, group)
+    gcache = getattr(engine, "gather_cache", None)  # stable gather buffers (GraphEngine)
+    g_rows = _all_gather(pad(rows).to(dev), world, group, gcache, "rows")
+    g_cols = _all_gather(pad(cols).to(dev), world, group, gcache, "cols")
+    g_desc = _all_gather(pad(desc).to(dev), world, group, gcache, "desc")
+    g_cnt = _all_gather(pad(cnt).to(dev), world, group, gcache, "cnt")
 
     h_cnt = g_cnt.cpu().numpy()  # one read of every image's keypoint count
 

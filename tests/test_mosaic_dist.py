@@ -70,6 +70,13 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         t = mosaic.build_pairwise_table(fragments(), CFG, engine=OracleEngine(CFG))
+        # an engine with persistent gather buffers (as GraphEngine): two tables through the same buffers
+        eng = OracleEngine(CFG)
+        eng.gather_cache = {}
+        t1 = mosaic.build_pairwise_table(fragments(), CFG, engine=eng)
+        t2 = mosaic.build_pairwise_table(fragments(), CFG, engine=eng)
+        assert len(eng.gather_cache) == 4
+        assert table_digest(t1) == table_digest(t2) == table_digest(t)
         q.put((rank, table_digest(t)))
     finally:
         dist.destroy_process_group()
