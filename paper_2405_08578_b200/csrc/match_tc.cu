@@ -698,6 +698,7 @@ constexpr int kSMs = 148;
 // asynchronous mode: row blocks of the near-tie enumeration launched blind
 // (the rest of a larger overflow list is decided by the exact scan)
 constexpr int kEnumBlocksAsync = 4;
+constexpr int kThroughputRowBlocks = 32;
 
 // statistics of the last tensor-core match on this thread (ps_match_stats)
 thread_local int64_t g_stats[8];  // uniq_a, uniq_b, cols, overflow rows, enumerated pairs, mma flops, -, -
@@ -721,12 +722,16 @@ void read_counts(const int32_t* p, const int32_t* q, int64_t* hp, int64_t* hq, c
 // row blocks x column splits.  One CTA per SM is resident (~180 KB of shared
 // memory), so the split minimises waves x (tiles per CTA + per-CTA overhead,
 // about four tiles' worth: launch, TMEM allocation, X tile, pipeline fill).
-dim3 tc_grid(int64_t rows, int64_t cols) {
+// throughput = true (asynchronous mode, where matches of other pairs run
+// concurrently): no column split once there are enough row blocks -- every
+// CTA pays its fixed cost (TMEM allocation, X tile, pipeline fill and drain)
+// once, so fewer, longer CTAs leave more of the machine to the other pairs.
+dim3 tc_grid(int64_t rows, int64_t cols, bool throughput = false) {
   const int rb = (int)std::max<int64_t>(1, (rows + BM - 1) / BM);
   const int tiles = (int)std::max<int64_t>(1, (cols + BN - 1) / BN);
   int best = 1;
   int64_t best_cost = INT64_MAX;
-  for (int s = 1; s <= std::min(kMaxSplit, tiles); ++s) {
+  for (int s = 1; s <= std::min(kMaxSplit, tiles) && !(throughput && rb >= kThroughputRowBlocks); ++s) {
     const int64_t waves = ((int64_t)rb * s + kSMs - 1) / kSMs;
     const int64_t cost = waves * ((tiles + s - 1) / s + 4);
     if (cost < best_cost) { best_cost = cost; best = s; }
@@ -844,7 +849,7 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   if (nx_io && sync) *nx_io = nx;
   if (ny_io && sync) *ny_io = ny;
   if (nx <= 0) return PS_OK;
-  const dim3 g0 = tc_grid(nx, ny);
+  const dim3 g0 = tc_grid(nx, ny, !sync);
   const int64_t flops_tile = 2ll * BM * BN * KD;
   if (sync) g_stats[5] += (int64_t)g0.x * ((ny + BN - 1) / BN) * flops_tile;
   nn_topk_tc<0><<<g0, kThreads, smem_bytes<0>(), st>>>(w.xt, w.yt, n_x, n_y, w.topv, w.topj, nullptr, nullptr,
