@@ -390,7 +390,7 @@ def bench_ransac(args, rank, dev, with_cpu, n=1000, iters=2000, steps=5):
 # C5 illumination pairs (BASELINE.json configs[4]): pairs/s
 # ---------------------------------------------------------------------------
 
-def bench_c5_pairs(args, world, rank, dev, n_pairs=16, steps=2):
+def bench_c5_pairs(args, world, rank, dev, n_pairs=256, steps=2):
     """Full path per pair (detect, describe both images; match; RANSAC) on
     the RGB pixels: BT.601 grey through the device ingest path (integer luma
     key for detection, the run host's grey table for values and the
@@ -405,9 +405,11 @@ def bench_c5_pairs(args, world, rank, dev, n_pairs=16, steps=2):
     cfg = PipelineConfig(window_min=16, window_max=64)
     mine = [p for p in range(n_pairs) if p % world == rank]
     grey = []
-    for p in mine:
-        a, b, _ = scenes.config5_pair(p)
-        grey.append(device.as_device_images(torch.from_numpy(np.stack([a, b])).to(dev), rgb=True))
+    import multiprocessing as mp
+
+    with mp.get_context("fork").Pool(max(1, min(16, (os.cpu_count() or 1) // max(world, 1)))) as pool:
+        for a, b in pool.imap(scenes._c5_job, mine):
+            grey.append(device.as_device_images(torch.from_numpy(np.stack([a, b])).to(dev), rgb=True))
     sizes, dcfg = cfg.scale_set().sizes, cfg.descriptor_config()
 
     def run_pair(g):
@@ -476,15 +478,16 @@ def bench_c5_pairs(args, world, rank, dev, n_pairs=16, steps=2):
                   desc[2 * q + 1], h[2 * q + 1], cfg.seed) for q in range(len(grey))]
         return [(None, o[0]) for o in geng.register_many(items)]
 
-    dt1, stats1 = timed(lambda: [run_pair(g) for g in grey])
+    n_sub = min(len(grey), 16)  # the one-pair-at-a-time variant on a bounded subset
+    dt1, stats1 = timed(lambda: [run_pair(g) for g in grey[:n_sub]])
     dtb, stats = timed(run_batched)
     dt, statsg = timed(run_graph)
-    assert [s[0] for s in stats] == [s[0] for s in stats1] and [s[1] for s in stats] == [s[1] for s in stats1]
-    assert [s[1] for s in statsg] == [s[1] for s in stats1]
+    assert [s[0] for s in stats[:n_sub]] == [s[0] for s in stats1]
+    assert [s[1] for s in stats[:n_sub]] == [s[1] for s in stats1] and [s[1] for s in statsg] == [s[1] for s in stats]
     return {"metric": "pairs/s (C5: 1920x1080 RGB pairs, BT.601 grey, homography warp + gain/offset/noise, "
                       "L 16..64, full detect/describe/match/RANSAC)",
             "value": round(n_pairs / dt, 3), "unit": "pairs/s", "pairs": n_pairs, "n_gpus": world,
-            "per_pair_calls_value": round(n_pairs / dt1, 3), "batched_eager_value": round(n_pairs / dtb, 3),
+            "per_pair_calls_value": round(n_sub * world / dt1, 3), "batched_eager_value": round(n_pairs / dtb, 3),
             "mean_matches": float(np.mean([s[0] for s in stats])) if stats else 0.0,
             "registered": int(sum(s[1] for s in stats)),
             "timing": "host wall clock, CUDA-synchronized, max over ranks; RGB inputs resident on the GPU",
@@ -492,7 +495,7 @@ def bench_c5_pairs(args, world, rank, dev, n_pairs=16, steps=2):
                         "CUDA graph, one count read, then every pair's match -> point gather -> RANSAC chain "
                         "(device-side counts) replayed as one graph over 8 streams, one result read; "
                         "batched_eager_value: the same batches launched eagerly with one count and one result "
-                        "read-back; per_pair_calls_value: one synchronous pair at a time",
+                        "read-back; per_pair_calls_value: one synchronous pair at a time (first 16 pairs of each rank)",
             "ingest": "RGB8 pixel type: luma-key detection, host-built 2^24 grey table (ingest.py)"}
 
 

@@ -179,6 +179,12 @@ def _homography_warp(img: np.ndarray, H: np.ndarray) -> np.ndarray:
     return out if img.ndim == 3 else out[..., 0]
 
 
+def _c5_job(p: int):
+    """Pool worker: the two RGB images of C5 pair p."""
+    a, b, _ = config5_pair(p)
+    return a, b
+
+
 def config5_pair(p: int, h: int = 1080, w: int = 1920) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
     """C5 pair p: RGB image 1 (channel c = scene(h, w, 3p + c)) and image 2 =
     centre-anchored homography warp of it (rotation U[-10, 10] deg, scale
