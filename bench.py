@@ -675,6 +675,27 @@ def run_ours(args):
                "describe_kernel": {"ms": round(des_ms, 4), "GB/s": round(ach_des, 1),
                                    "keypoints_per_s": round(n_kp / (des_ms / 1e3), 1)}}
 
+    # detect alone, back to back (its inputs, 275 MB, exceed L2): the kernel's own roofline fraction,
+    # without the write-back of the previous describe's dirty descriptor lines that it absorbs in the step
+    iso = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for _ in range(3):
+        device.detect(dimg, SCALES, meta=False)
+    iso[0].record(stream)
+    n_iso = 20
+    for _ in range(n_iso):
+        device.detect(dimg, SCALES, meta=False)
+    iso[1].record(stream)
+    torch.cuda.synchronize()
+    det_iso_ms = iso[0].elapsed_time(iso[1]) / n_iso
+    if world > 1:
+        t = torch.tensor([det_iso_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        det_iso_ms = t.item()
+    ach_iso = bytes_detect / (det_iso_ms / 1e3) / 1e9
+    kernels["detect_u8_w8"]["isolated"] = {"ms": round(det_iso_ms, 4), "GB/s": round(ach_iso, 1),
+                                           "frac_hbm": round(ach_iso / peak, 4),
+                                           "timing": f"CUDA events over {n_iso} back-to-back launches"}
+
     # ---- e2e through the public host API ----
     e2e = None
     if not args.no_e2e:
