@@ -667,6 +667,7 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
     // corners of each sample straight from the staged raster
     const double* pb = stage + (pr0 - 1 - BR) * SP + (pc0 - 1 - BC);  // P(pr0 - 1, pc0 - 1)
     const double c0t = ct, s0t = -st;  // cos / sin of theta0
+    const bool all_valid = xmin >= 1.0 && xmax <= xhi && ymin >= 1.0 && ymax <= yhi;  // corner extent inside
 #pragma unroll
     for (int j = 0; j < SPL; ++j) {
       const int s = lane + 32 * j, iv = s / W, iu = s % W;
@@ -675,7 +676,7 @@ __device__ __forceinline__ bool describe_keypoint_w8u8(const Img& im, int row, i
       const double y = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, u)), __dmul_rn(ct, v));
       mg[j] = 0.0;
       bn[j] = 0;
-      if (!(x >= 1.0 && x <= xhi && y >= 1.0 && y <= yhi)) continue;  // hypot * valid = 0
+      if (!all_valid && !(x >= 1.0 && x <= xhi && y >= 1.0 && y <= yhi)) continue;  // hypot * valid = 0
       // The reference clips x to [pc0, pc1] first; for a valid sample that is
       // the identity: x >= xmin and x <= xmax hold exactly (same rounded
       // expressions, monotone in u and v), and the image clamps of pc0 / pc1
@@ -1061,6 +1062,9 @@ __device__ __forceinline__ bool describe_pair_w8(const Img& im, int row, int col
     const double dpc0 = (double)pc0, dpr0 = (double)pr0;
     const double* pb = stage + (pr0 - 1 - BR) * SP + (pc0 - 1 - BC);
     const double c0t = ct, s0t = -st;
+    // x and y are monotone in u and v under round-to-nearest, so the grid's
+    // corner extent bounds every sample: one test per keypoint when it is inside
+    const bool all_valid = xmin >= 1.0 && xmax <= xhi && ymin >= 1.0 && ymax <= yhi;
 #pragma unroll
     for (int j = 0; j < SPL; ++j) {
       const int s = hl + 16 * j, iv = s / W, iu = s % W;
@@ -1069,7 +1073,7 @@ __device__ __forceinline__ bool describe_pair_w8(const Img& im, int row, int col
       const double y = __dadd_rn(__dadd_rn(cy, __dmul_rn(st, u)), __dmul_rn(ct, v));
       mg[j] = 0.0;
       bn[j] = 0;
-      if (!(x >= 1.0 && x <= xhi && y >= 1.0 && y <= yhi)) continue;
+      if (!all_valid && !(x >= 1.0 && x <= xhi && y >= 1.0 && y <= yhi)) continue;
       const double lx = __dsub_rn(x, dpc0), ly = __dsub_rn(y, dpr0);
       const int x0 = max(min((int)floor(lx), xcap), 0), y0 = max(min((int)floor(ly), ycap), 0);
       const double fxx = __dsub_rn(lx, (double)x0), fyy = __dsub_rn(ly, (double)y0);
