@@ -34,17 +34,23 @@
 namespace ps {
 namespace tc {
 
-constexpr int BM = 128;   // X rows per CTA (= TMEM lanes)
-constexpr int BN = 256;   // Y rows per tile (= MMA N, TMEM columns)
-constexpr int KD = 128;   // descriptor length
+// A CTA owns XH = 2 X operand tiles of BMH = 128 rows (one M = 128 MMA each,
+// the same Y tile as B): every Y byte brought into shared memory feeds 256
+// rows, which halves the operand traffic per MMA -- the bulk-copy service
+// per SM, not the tensor pipe, bounded the one-tile-per-CTA design.
+constexpr int BMH = 128;       // X rows per operand tile / MMA (= TMEM lanes)
+constexpr int XH = 2;          // X tiles per CTA
+constexpr int BM = BMH * XH;   // X rows per CTA
+constexpr int BN = 128;        // Y rows per tile (= MMA N)
+constexpr int KD = 128;        // descriptor length
 constexpr int TOPK = 4;
-constexpr int STAGES_TOP = 2;   // Y-tile stages (2 x 72 KB)
-constexpr int STAGES_ENUM = 2;  // the enumeration pass trades one stage for per-warp hit buffers
+constexpr int STAGES_TOP = 4;   // Y-tile stages (4 x 36 KB)
+constexpr int STAGES_ENUM = 3;  // the enumeration pass trades one stage for per-warp hit buffers
 #ifndef PS_EPI_WARPS
 #define PS_EPI_WARPS 16
 #endif
 constexpr int kEpiWarps = PS_EPI_WARPS;  // kParts warps per TMEM lane quarter, BN / kParts columns each
-constexpr int kParts = kEpiWarps / 4;    // top-4 lists per (row, split)
+constexpr int kParts = kEpiWarps / (4 * XH);  // top-4 lists per (row, split)
 constexpr int HITBUF = 4096 / kEpiWarps;  // hits staged per epilogue warp before one bulk append
 // Each operand tile is the K-major SW128 image of the 128 descriptor columns
 // followed by a 16-column augmentation block (no swizzle, 32 B per row): X rows
@@ -53,12 +59,12 @@ constexpr int HITBUF = 4096 / kEpiWarps;  // hits staged per epilogue warp befor
 // MMA k-step then leaves v = |y|^2 - 2 x.y in TMEM.
 constexpr int KA = 16;                           // augmentation columns
 constexpr uint32_t ROW_BYTES = KD * 2 + KA * 2;  // 288
-constexpr uint32_t A_BYTES = BM * ROW_BYTES;     // 36 KB
-constexpr uint32_t B_BYTES = BN * ROW_BYTES;     // 72 KB
+constexpr uint32_t A_BYTES = BMH * ROW_BYTES;    // 36 KB per X tile (XH per CTA)
+constexpr uint32_t B_BYTES = BN * ROW_BYTES;     // 36 KB
 constexpr int kThreads = 64 + 32 * kEpiWarps;  // warp 0 bulk copies, warp 1 MMA/TMEM, warps 2.. epilogue
 template <int MODE>
 constexpr size_t smem_bytes() {
-  return A_BYTES + (MODE == 0 ? STAGES_TOP : STAGES_ENUM) * (size_t)B_BYTES + 256 +
+  return XH * A_BYTES + (MODE == 0 ? STAGES_TOP : STAGES_ENUM) * (size_t)B_BYTES + 256 +
          (MODE == 0 ? 0 : kEpiWarps * (HITBUF * 8 + 16));
 }
 
@@ -75,11 +81,11 @@ template <class T>
 __global__ void prep_tiles(const T* __restrict__ src, const int32_t* __restrict__ idx,
                            const int32_t* __restrict__ count_p, int64_t count_const, int64_t n_pad, int R,
                            uint8_t* __restrict__ tiles, double* __restrict__ info, unsigned* __restrict__ maxes,
-                           int is_y) {
+                           int is_y, int align) {
   const int lane = threadIdx.x & 31;
   const int64_t count = count_p ? (int64_t)*count_p : count_const;
-  // only the tiles that hold live rows are ever read
-  const int64_t n_used = min(n_pad, (count + R - 1) / R * R);
+  // only the row blocks that hold live rows are ever read (align = rows per reader)
+  const int64_t n_used = min(n_pad, (count + align - 1) / align * align);
   float mx0 = 0.0f, mx1 = 0.0f, mx2 = 0.0f;  // lane 0: running maxima of this warp's rows
   for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < n_used;
        u += (int64_t)gridDim.x * (blockDim.x >> 5)) {
@@ -200,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
   const int64_t nx_pad = (int64_t)gridDim.x * BM;
   uint8_t* smem = smem_raw;  // 1024-aligned (SWIZZLE_128B atoms)
   uint8_t* sA = smem;
-  uint8_t* sB = smem + A_BYTES;
+  uint8_t* sB = smem + XH * A_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
   uint64_t* a_full = bars;
   uint64_t* b_full = bars + 1;
@@ -234,8 +240,8 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
 
   if (warp == 0) {
     if (lane == 0) {  // ---- bulk-copy producer
-      mbar_arrive_expect_tx(a_full, A_BYTES);
-      bulk_g2s(sA, Xt + (size_t)rb * A_BYTES, A_BYTES, a_full);
+      mbar_arrive_expect_tx(a_full, XH * A_BYTES);
+      bulk_g2s(sA, Xt + (size_t)rb * XH * A_BYTES, XH * A_BYTES, a_full);  // the CTA's XH tiles are contiguous
       for (int t = 0; t < n_tiles; ++t) {
         const int s = t % STAGES;
         mbar_wait(b_empty + s, ((t / STAGES) & 1) ^ 1);
@@ -245,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer
-      const uint32_t idesc = idesc_f16_f32(BM, BN);
+      const uint32_t idesc = idesc_f16_f32(BMH, BN);
       const uint32_t a0 = smem_u32(sA);
       mbar_wait(a_full, 0);
       for (int t = 0; t < n_tiles; ++t) {
@@ -255,22 +261,26 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
         tc_fence_after();
         const uint32_t b0 = smem_u32(sB + s * B_BYTES);
 #pragma unroll
-        for (int k = 0; k < KD / 16; ++k) {
-          const uint32_t koff = (uint32_t)((k & 3) * 32);  // 16 fp16 = 32 B within the atom
-          const uint64_t ad = sdesc_k_sw128(a0 + (k >> 2) * (BM * 128) + koff);
-          const uint64_t bd = sdesc_k_sw128(b0 + (k >> 2) * (BN * 128) + koff);
-          mma_f16(tmem + ab * BN, ad, bd, idesc, k > 0 ? 1u : 0u);
+        for (int h = 0; h < XH; ++h) {  // accumulator (ab, h): TMEM columns (ab * XH + h) * BN
+          const uint32_t ah = a0 + h * A_BYTES, acc = tmem + (uint32_t)((ab * XH + h) * BN);
+#pragma unroll
+          for (int k = 0; k < KD / 16; ++k) {
+            const uint32_t koff = (uint32_t)((k & 3) * 32);  // 16 fp16 = 32 B within the atom
+            const uint64_t ad = sdesc_k_sw128(ah + (k >> 2) * (BMH * 128) + koff);
+            const uint64_t bd = sdesc_k_sw128(b0 + (k >> 2) * (BN * 128) + koff);
+            mma_f16(acc, ad, bd, idesc, k > 0 ? 1u : 0u);
+          }
+          mma_f16(acc, sdesc_k_none(ah + BMH * KD * 2), sdesc_k_none(b0 + BN * KD * 2), idesc, 1u);
         }
-        mma_f16(tmem + ab * BN, sdesc_k_none(a0 + BM * KD * 2), sdesc_k_none(b0 + BN * KD * 2), idesc, 1u);
         mma_commit(b_empty + s);
         mma_commit(acc_full + ab);
       }
     }
   } else {  // ---- epilogue: thread = row, kParts warps per lane quarter split the columns
     const int quarter = warp & 3;
-    const int ew = warp - 2, part = ew >> 2;
+    const int ew = warp - 2, sub = ew >> 2, h = sub / kParts, part = sub % kParts;
     constexpr int kCols = BN / kParts;
-    const int row = quarter * 32 + lane;
+    const int row = h * BMH + quarter * 32 + lane;
     float tv[TOPK];
     int tj[TOPK];
 #pragma unroll
@@ -282,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
       mbar_wait(acc_full + ab, (t >> 1) & 1);
       tc_fence_after();
       const int tg = t_begin + t;  // global tile index
-      const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + ab * BN + part * kCols;
+      const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (ab * XH + h) * BN + part * kCols;
       // one pass per 64-column chunk; groups of 4 columns are tested against the
       // row's threshold (4th best, or the enumeration limit) with one branch
       unsigned long long* hb = hitbuf + ew * HITBUF;
@@ -307,12 +317,12 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
               if (v2 < tv[TOPK - 1]) topk_insert(v2, jb + 4 * q + 2, tv, tj);
               if (v3 < tv[TOPK - 1]) topk_insert(v3, jb + 4 * q + 3, tv, tj);
             }
-          } else if (__any_sync(0xffffffffu, !(m4 > my_lim))) {
+          } else if (__any_sync(0xffffffffu, !(m4 > my_lim) && grow < nx)) {
             const float vv[4] = {v0, v1, v2, v3};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               // NaN / inf limits enumerate every real column (padding columns hold +inf)
-            const bool hit = !(vv[e] > my_lim) && jb + 4 * q + e < ny;
+            const bool hit = !(vv[e] > my_lim) && jb + 4 * q + e < ny && grow < nx;  // (NaN v of dead rows)
               const unsigned bal = __ballot_sync(0xffffffffu, hit);
               if (bal) {
                 if (hit)
@@ -733,7 +743,7 @@ dim3 tc_grid(int64_t rows, int64_t cols, bool throughput = false) {
   int64_t best_cost = INT64_MAX;
   for (int s = 1; s <= std::min(kMaxSplit, tiles) && !(throughput && rb >= kThroughputRowBlocks); ++s) {
     const int64_t waves = ((int64_t)rb * s + kSMs - 1) / kSMs;
-    const int64_t cost = waves * ((tiles + s - 1) / s + 4);
+    const int64_t cost = waves * ((tiles + s - 1) / s + 8);
     if (cost < best_cost) { best_cost = cost; best = s; }
   }
   if (const char* e = getenv("PS_TC_SPLIT")) best = std::max(1, std::min({atoi(e), kMaxSplit, tiles}));  // diagnostic
@@ -828,9 +838,9 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   const int64_t xrows = rup(nx_max, BM), yrows = rup(ny_all, BN);
   cudaMemsetAsync(w.ymax, 0, 4 * sizeof(unsigned), st);
   cudaMemsetAsync(w.n_overflow, 0, sizeof(int32_t), st);
-  prep_tiles<T><<<grid_for(xrows, 8), 256, 0, st>>>(X, x_idx, n_x, 0, xrows, BM, w.xt, w.xinfo, nullptr, 0);
+  prep_tiles<T><<<grid_for(xrows, 8), 256, 0, st>>>(X, x_idx, n_x, 0, xrows, BMH, w.xt, w.xinfo, nullptr, 0, BM);
   PS_LAUNCHED("prep_tiles(X)");
-  prep_tiles<T><<<grid_for(yrows, 8), 256, 0, st>>>(Y, y_idx, n_y, 0, yrows, BN, w.yt, w.yinfo, w.ymax, 1);
+  prep_tiles<T><<<grid_for(yrows, 8), 256, 0, st>>>(Y, y_idx, n_y, 0, yrows, BN, w.yt, w.yinfo, w.ymax, 1, BN);
   PS_LAUNCHED("prep_tiles(Y)");
   static bool attr = false;
   if (!attr) {
@@ -863,7 +873,7 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   // column within their certified limit on the tensor cores, then decide exactly
   gather_rows<<<grid_for(nx_max, 256), 256, 0, st>>>(w.overflow, w.n_overflow, x_idx, w.xsrc);
   PS_LAUNCHED("gather_rows");
-  prep_tiles<T><<<grid_for(xrows, 8), 256, 0, st>>>(X, w.xsrc, w.n_overflow, 0, xrows, BM, w.xt, w.xinfo, nullptr, 0);
+  prep_tiles<T><<<grid_for(xrows, 8), 256, 0, st>>>(X, w.xsrc, w.n_overflow, 0, xrows, BMH, w.xt, w.xinfo, nullptr, 0, BM);
   PS_LAUNCHED("prep_tiles(overflow)");
   cudaMemsetAsync(w.n_pairs, 0, sizeof(unsigned long long), st);
   cudaMemsetAsync(w.best_bits, 0xff, nx_max * sizeof(unsigned long long), st);
