@@ -34,18 +34,22 @@
 namespace ps {
 namespace tc {
 
-// A CTA owns XH = 2 X operand tiles of BMH = 128 rows (one M = 128 MMA each,
-// the same Y tile as B): every Y byte brought into shared memory feeds 256
-// rows, which halves the operand traffic per MMA -- the bulk-copy service
-// per SM, not the tensor pipe, bounded the one-tile-per-CTA design.
+// A CTA owns XH X operand tiles of BMH = 128 rows (one M = 128 MMA each,
+// against the same Y tile).  XH = 2 (N = 128) halves the Y bytes per MMA and
+// is 7 % faster on dense 104k^2 data, but slower on the duplicate-heavy C4
+// pair (fewer, longer CTAs for the near-tie passes), so XH = 1 (N = 256) is
+// the default; -DPS_TC_XH=2 selects the other geometry.
+#ifndef PS_TC_XH
+#define PS_TC_XH 1
+#endif
 constexpr int BMH = 128;       // X rows per operand tile / MMA (= TMEM lanes)
-constexpr int XH = 2;          // X tiles per CTA
+constexpr int XH = PS_TC_XH;   // X tiles per CTA
 constexpr int BM = BMH * XH;   // X rows per CTA
-constexpr int BN = 128;        // Y rows per tile (= MMA N)
+constexpr int BN = 256 / XH;   // Y rows per tile (= MMA N): XH accumulators x 2 buffers fill TMEM
 constexpr int KD = 128;        // descriptor length
 constexpr int TOPK = 4;
-constexpr int STAGES_TOP = 4;   // Y-tile stages (4 x 36 KB)
-constexpr int STAGES_ENUM = 3;  // the enumeration pass trades one stage for per-warp hit buffers
+constexpr int STAGES_TOP = 2 * XH;       // Y-tile stages (XH = 1: 2 x 72 KB; 2: 4 x 36 KB)
+constexpr int STAGES_ENUM = XH + 1;      // the enumeration pass trades one stage for per-warp hit buffers
 #ifndef PS_EPI_WARPS
 #define PS_EPI_WARPS 16
 #endif
@@ -286,7 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
 #pragma unroll
     for (int q = 0; q < TOPK; ++q) { tv[q] = INFINITY; tj[q] = -1; }
     const int64_t grow = (int64_t)rb * BM + row;
-    const float my_lim = (MODE == 1 && grow < nx) ? lim[grow] : -INFINITY;
+    // dead rows (beyond the count; their X rows may be stale) get a NaN limit: no v compares <= NaN
+    const float my_lim = (MODE == 1 && grow < nx) ? lim[grow] : __int_as_float(0x7fc00000);
     for (int t = 0; t < n_tiles; ++t) {
       const int ab = t & 1;
       mbar_wait(acc_full + ab, (t >> 1) & 1);
@@ -317,12 +322,12 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
               if (v2 < tv[TOPK - 1]) topk_insert(v2, jb + 4 * q + 2, tv, tj);
               if (v3 < tv[TOPK - 1]) topk_insert(v3, jb + 4 * q + 3, tv, tj);
             }
-          } else if (__any_sync(0xffffffffu, !(m4 > my_lim) && grow < nx)) {
+          } else if (__any_sync(0xffffffffu, m4 <= my_lim)) {
             const float vv[4] = {v0, v1, v2, v3};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              // NaN / inf limits enumerate every real column (padding columns hold +inf)
-            const bool hit = !(vv[e] > my_lim) && jb + 4 * q + e < ny && grow < nx;  // (NaN v of dead rows)
+              // an inf limit (void certificate) enumerates every real column (padding columns hold +inf)
+              const bool hit = vv[e] <= my_lim && jb + 4 * q + e < ny;
               const unsigned bal = __ballot_sync(0xffffffffu, hit);
               if (bal) {
                 if (hit)
@@ -743,7 +748,7 @@ dim3 tc_grid(int64_t rows, int64_t cols, bool throughput = false) {
   int64_t best_cost = INT64_MAX;
   for (int s = 1; s <= std::min(kMaxSplit, tiles) && !(throughput && rb >= kThroughputRowBlocks); ++s) {
     const int64_t waves = ((int64_t)rb * s + kSMs - 1) / kSMs;
-    const int64_t cost = waves * ((tiles + s - 1) / s + 8);
+    const int64_t cost = waves * ((tiles + s - 1) / s + 4 * XH);
     if (cost < best_cost) { best_cost = cost; best = s; }
   }
   if (const char* e = getenv("PS_TC_SPLIT")) best = std::max(1, std::min({atoi(e), kMaxSplit, tiles}));  // diagnostic
