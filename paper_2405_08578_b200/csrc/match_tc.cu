@@ -56,6 +56,10 @@ constexpr int STAGES_ENUM = XH + 1;      // the enumeration pass trades one stag
 constexpr int kEpiWarps = PS_EPI_WARPS;  // kParts warps per TMEM lane quarter, BN / kParts columns each
 constexpr int kParts = kEpiWarps / (4 * XH);  // top-4 lists per (row, split)
 constexpr int HITBUF = 4096 / kEpiWarps;  // hits staged per epilogue warp before one bulk append
+#ifndef PS_TC_COPY_PARTS
+#define PS_TC_COPY_PARTS 8
+#endif
+constexpr int kCopyParts = PS_TC_COPY_PARTS;  // bulk copies per Y tile (lanes of the producer warp)
 // Each operand tile is the K-major SW128 image of the 128 descriptor columns
 // followed by a 16-column augmentation block (no swizzle, 32 B per row): X rows
 // carry (1, 1, 1, 0...), Y rows carry -- with the descriptor part scaled by -2
@@ -69,7 +73,7 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;  // warp 0 bulk copies, warp 1 MMA
 template <int MODE>
 constexpr size_t smem_bytes() {
   return XH * A_BYTES + (MODE == 0 ? STAGES_TOP : STAGES_ENUM) * (size_t)B_BYTES + 256 +
-         (MODE == 0 ? 0 : kEpiWarps * (HITBUF * 8 + 16));
+         (MODE == 0 ? kParts * BM * sizeof(float) : kEpiWarps * (HITBUF * 8 + 16));
 }
 
 // ---- operand preparation ----------------------------------------------------------
@@ -207,6 +211,12 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
   const int per = (n_all + gridDim.y - 1) / gridDim.y;
   const int t_begin = min(n_all, (int)blockIdx.y * per);
   const int n_tiles = min(n_all, t_begin + per) - t_begin;  // may be 0 (then lists stay empty)
+  // The row blocks walk their Y tiles from staggered starting points (a ring):
+  // in lockstep every CTA would request the same tile from the same L2 lines
+  // at once.  Results do not depend on the order: candidates within the
+  // certified margin are strictly below the 4th best, so ties at the 4th
+  // place never decide them, and the enumeration collects every hit.
+  const int t_rot = n_tiles > 0 ? (int)(((int64_t)rb * n_tiles) / gridDim.x) % n_tiles : 0;
   const int64_t nx_pad = (int64_t)gridDim.x * BM;
   uint8_t* smem = smem_raw;  // 1024-aligned (SWIZZLE_128B atoms)
   uint8_t* sA = smem;
@@ -223,7 +233,11 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
   int* hitcnt = reinterpret_cast<int*>(hitbuf + kEpiWarps * HITBUF);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  // MODE 0: each (row, part) thread publishes its list's 4th best; the row's
+  // other parts prune with the smallest of them (see the epilogue)
+  float* sthr = reinterpret_cast<float*>(bars + 32);
   if (MODE == 1 && threadIdx.x < kEpiWarps) hitcnt[threadIdx.x] = 0;
+  if (MODE == 0 && threadIdx.x < kParts * BM) sthr[threadIdx.x] = INFINITY;
   if (threadIdx.x == 0) {
     mbar_init(a_full, 1);
     for (int s = 0; s < STAGES; ++s) {
@@ -232,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(acc_full + s, 1);
-      mbar_init(acc_empty + s, kEpiWarps * 32);
+      mbar_init(acc_empty + s, kEpiWarps);  // one arrival per epilogue warp (512 thread arrivals serialised)
     }
     mbar_fence_init();
   }
@@ -241,16 +255,39 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+#ifdef PS_TC_DIAG_EARLY  // diagnostic builds only: launch + barrier init + TMEM allocation cost
+  if (MODE == 0) {
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 512);
+    return;
+  }
+#endif
 
   if (warp == 0) {
-    if (lane == 0) {  // ---- bulk-copy producer
+    // ---- bulk-copy producer: each tile in kCopyParts pieces issued by as
+    // many lanes (one 72 KB request at a time left the copy engine idle
+    // between tiles: the pipeline ran at ~2 us per tile, twice the MMA time)
+    if (lane == 0) {
       mbar_arrive_expect_tx(a_full, XH * A_BYTES);
       bulk_g2s(sA, Xt + (size_t)rb * XH * A_BYTES, XH * A_BYTES, a_full);  // the CTA's XH tiles are contiguous
+    }
+    if (lane < kCopyParts) {
+      constexpr uint32_t piece = B_BYTES / kCopyParts;
+      static_assert(B_BYTES % (16 * kCopyParts) == 0, "16-byte pieces");
       for (int t = 0; t < n_tiles; ++t) {
         const int s = t % STAGES;
         mbar_wait(b_empty + s, ((t / STAGES) & 1) ^ 1);
-        mbar_arrive_expect_tx(b_full + s, B_BYTES);
-        bulk_g2s(sB + s * B_BYTES, Yt + (size_t)(t_begin + t) * B_BYTES, B_BYTES, b_full + s);
+#ifdef PS_TC_DIAG_NOCOPY  // diagnostic builds only: MMA rate on the resident stages (wrong results)
+        if (MODE == 0 && t >= STAGES) {
+          if (lane == 0) mbar_arrive(b_full + s);
+          continue;
+        }
+#endif
+        if (lane == 0) mbar_arrive_expect_tx(b_full + s, B_BYTES);
+        __syncwarp((1u << kCopyParts) - 1u);  // the expectation is posted before any piece can complete
+        const int tr = t + t_rot < n_tiles ? t + t_rot : t + t_rot - n_tiles;
+        bulk_g2s(sB + s * B_BYTES + lane * piece, Yt + (size_t)(t_begin + tr) * B_BYTES + lane * piece, piece,
+                 b_full + s);
       }
     }
   } else if (warp == 1) {
@@ -296,8 +333,19 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
       const int ab = t & 1;
       mbar_wait(acc_full + ab, (t >> 1) & 1);
       tc_fence_after();
-      const int tg = t_begin + t;  // global tile index
+      const int tg = t_begin + (t + t_rot < n_tiles ? t + t_rot : t + t_rot - n_tiles);  // global tile index
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (ab * XH + h) * BN + part * kCols;
+      // Pruning bound shared by the row's kParts threads: every published 4th
+      // best has four real values at or below it, so the row's final top-4
+      // lies strictly below the smallest of them (ties at the bound cannot be
+      // certification candidates: the merged 4th best is then <= them).
+      // Stale reads are safe -- the published values only decrease.
+      float tsh = INFINITY;
+      if (MODE == 0) {
+#pragma unroll
+        for (int p2 = 0; p2 < kParts; ++p2)
+          if (p2 != part) tsh = fminf(tsh, *(volatile float*)(sthr + p2 * BM + row));
+      }
       // one pass per 64-column chunk; groups of 4 columns are tested against the
       // row's threshold (4th best, or the enumeration limit) with one branch
       unsigned long long* hb = hitbuf + ew * HITBUF;
@@ -316,11 +364,11 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
           const float v3 = __uint_as_float(r[4 * q + 3]);
           const float m4 = fminf(fminf(v0, v1), fminf(v2, v3));
           if (MODE == 0) {
-            if (m4 < tv[TOPK - 1]) {  // rare after the first tiles
-              if (v0 < tv[TOPK - 1]) topk_insert(v0, jb + 4 * q + 0, tv, tj);
-              if (v1 < tv[TOPK - 1]) topk_insert(v1, jb + 4 * q + 1, tv, tj);
-              if (v2 < tv[TOPK - 1]) topk_insert(v2, jb + 4 * q + 2, tv, tj);
-              if (v3 < tv[TOPK - 1]) topk_insert(v3, jb + 4 * q + 3, tv, tj);
+            if (m4 < fminf(tv[TOPK - 1], tsh)) {  // rare after the first tiles
+              if (v0 < fminf(tv[TOPK - 1], tsh)) topk_insert(v0, jb + 4 * q + 0, tv, tj);
+              if (v1 < fminf(tv[TOPK - 1], tsh)) topk_insert(v1, jb + 4 * q + 1, tv, tj);
+              if (v2 < fminf(tv[TOPK - 1], tsh)) topk_insert(v2, jb + 4 * q + 2, tv, tj);
+              if (v3 < fminf(tv[TOPK - 1], tsh)) topk_insert(v3, jb + 4 * q + 3, tv, tj);
             }
           } else if (__any_sync(0xffffffffu, m4 <= my_lim)) {
             const float vv[4] = {v0, v1, v2, v3};
@@ -353,9 +401,12 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
         __syncwarp();
         if (lane == 0) hitcnt[ew] = fill;
         __syncwarp();
+      } else {
+        *(volatile float*)(sthr + part * BM + row) = tv[TOPK - 1];
       }
       tc_fence_before();
-      mbar_arrive(acc_empty + ab);
+      __syncwarp();  // every lane's TMEM reads are complete (tcgen05.wait::ld) before lane 0 releases
+      if (lane == 0) mbar_arrive(acc_empty + ab);
     }
     if (MODE == 1) {
       unsigned long long* hb = hitbuf + ew * HITBUF;
