@@ -381,11 +381,16 @@ def build_pairwise_table(images: Sequence, cfg, *, engine=None, group=None) -> P
             outs = list(ex.map(run_on_stream, mine_q))
     else:
         outs = [run(q) for q in mine_q]
-    if mine_q:  # one host-to-device copy of this rank's rows
-        res[mine_q] = torch.tensor([[float(ok), th, tx, ty, float(ni)] for ok, th, tx, ty, ni in outs],
-                                   dtype=torch.float64).to(dev)
-    # gather: each pair was computed by exactly one rank, the others hold zeros
-    allres = _all_gather(res, world, group).sum(dim=0).cpu().numpy()
+    rows_h = np.array([[float(ok), th, tx, ty, float(ni)] for ok, th, tx, ty, ni in outs],
+                      dtype=np.float64).reshape(-1, 5)
+    if world == 1:  # every pair is local: no device round trip
+        allres = np.zeros((len(jobs), 5))
+        allres[mine_q] = rows_h
+    else:
+        if mine_q:  # one host-to-device copy of this rank's rows
+            res[mine_q] = torch.from_numpy(rows_h).to(dev)
+        # gather: each pair was computed by exactly one rank, the others hold zeros
+        allres = _all_gather(res, world, group).sum(dim=0).cpu().numpy()
     table = PairwiseTransformTable(n=n)
     for q, (a, b) in enumerate(jobs):
         ok, th, tx, ty, ni = allres[q]
