@@ -202,6 +202,7 @@ class GraphEngine(GpuEngine):
             pinned = torch.empty((len(arrs),) + tuple(arrs[0].shape), dtype=dt, pin_memory=True)
             static = torch.empty(pinned.shape, dtype=pinned.dtype, device=self.device)
             ent = {"pinned": pinned, "static": static, "graph": None, "done": None}
+            self._bound_cache(self._prep_graphs)
             self._prep_graphs[key] = ent
         self._upload(arrs, ent)
         if ent["graph"] is None:
@@ -229,9 +230,16 @@ class GraphEngine(GpuEngine):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 outs = self._prepare_dev(batch)
+            self._bound_cache(self._prep_graphs)
             ent = self._prep_graphs[key] = {"graph": g, "outs": outs}
         ent["graph"].replay()
         return ent["outs"]
+
+    max_graphs = 8  # per phase; each graph keeps its own memory pool alive
+
+    def _bound_cache(self, cache: dict) -> None:
+        while len(cache) >= self.max_graphs:  # drop the oldest capture (dicts keep insertion order)
+            cache.pop(next(iter(cache)))
 
     def _upload(self, arrs, ent):
         if all(isinstance(a, torch.Tensor) and a.is_pinned() for a in arrs):  # caller-pinned: straight to HBM
@@ -259,8 +267,7 @@ class GraphEngine(GpuEngine):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 gblock, glive = self._pairs_dev(items)
-            if len(self._pair_graphs) > 8:
-                self._pair_graphs.clear()
+            self._bound_cache(self._pair_graphs)
             self._pair_graphs[key] = (g, gblock, glive)
             return res
         g, block, live = ent
