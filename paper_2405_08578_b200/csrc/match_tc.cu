@@ -47,7 +47,10 @@ constexpr int XH = PS_TC_XH;   // X tiles per CTA
 constexpr int BM = BMH * XH;   // X rows per CTA
 constexpr int BN = 256 / XH;   // Y rows per tile (= MMA N): XH accumulators x 2 buffers fill TMEM
 constexpr int KD = 128;        // descriptor length
-constexpr int TOPK = 4;
+#ifndef PS_TC_TOPK
+#define PS_TC_TOPK 4
+#endif
+constexpr int TOPK = PS_TC_TOPK;  // candidates kept per (row, part, split)
 constexpr int STAGES_TOP = 2 * XH;       // Y-tile stages (XH = 1: 2 x 72 KB; 2: 4 x 36 KB)
 constexpr int STAGES_ENUM = XH + 1;      // the enumeration pass trades one stage for per-warp hit buffers
 #ifndef PS_EPI_WARPS
