@@ -193,26 +193,66 @@ class GraphEngine(GpuEngine):
         self._pair_graphs = {}
         self.gather_cache = {}  # build_pairwise_table's all-gather outputs, kept at fixed addresses
 
+    prep_chunk = 3  # images per detect/describe graph: chunk k + 1's upload overlaps chunk k's compute
+
     def prepare(self, images: list) -> tuple:
+        """Upload (pinned) and detect + describe, pipelined in chunks of
+        ``prep_chunk`` images: a copy stream uploads chunk k + 1 while the
+        current stream replays chunk k's graph, which also writes its rows
+        into fixed combined outputs (the pair graphs key on their addresses)."""
         arrs = [im if isinstance(im, torch.Tensor) else np.asarray(im) for im in images]
-        key = (len(arrs), tuple(arrs[0].shape), str(arrs[0].dtype))
+        n = len(arrs)
+        key = (n, tuple(arrs[0].shape), str(arrs[0].dtype))
         ent = self._prep_graphs.get(key)
+        cur = torch.cuda.current_stream(self.device)
         if ent is None:
             dt = arrs[0].dtype if isinstance(arrs[0], torch.Tensor) else torch.from_numpy(arrs[0][:1]).dtype
-            pinned = torch.empty((len(arrs),) + tuple(arrs[0].shape), dtype=dt, pin_memory=True)
+            pinned = torch.empty((n,) + tuple(arrs[0].shape), dtype=dt, pin_memory=True)
             static = torch.empty(pinned.shape, dtype=pinned.dtype, device=self.device)
-            ent = {"pinned": pinned, "static": static, "graph": None, "done": None}
+            chunks = [(k, min(k + self.prep_chunk, n)) for k in range(0, n, self.prep_chunk)]
+            ent = {"pinned": pinned, "static": static, "chunks": chunks, "graphs": None, "done": None,
+                   "copy": torch.cuda.Stream(self.device)}
             self._bound_cache(self._prep_graphs)
             self._prep_graphs[key] = ent
-        self._upload(arrs, ent)
-        if ent["graph"] is None:
-            self._prepare_dev(ent["static"])  # eager warm-up (attributes, allocator) ...
+        chunks, static, copy = ent["chunks"], ent["static"], ent["copy"]
+        caller_pinned = all(isinstance(a, torch.Tensor) and a.is_pinned() for a in arrs)
+        if not caller_pinned and ent["done"] is not None:
+            ent["done"].synchronize()  # the previous copies out of the staging buffer have finished
+        copy.wait_stream(cur)  # the previous call's readers of `static` come first
+        ready = []
+        for k0, k1 in chunks:
+            with torch.cuda.stream(copy):
+                for k in range(k0, k1):
+                    if caller_pinned:
+                        static[k].copy_(arrs[k], non_blocking=True)
+                    else:
+                        pv = ent["pinned"][k].numpy()
+                        np.copyto(pv, arrs[k].numpy() if isinstance(arrs[k], torch.Tensor) else arrs[k])
+                        static[k].copy_(ent["pinned"][k], non_blocking=True)
+                ready.append(copy.record_event())
+        ent["done"] = copy.record_event()
+        if ent["graphs"] is None:
+            cur.wait_stream(copy)
+            outs = [self._prepare_dev(static[k0:k1]) for k0, k1 in chunks]  # eager warm-up
+            rows0, cols0, desc0, cnt0 = outs[0]
+            cap, D = desc0.shape[1], desc0.shape[2]
+            comb = (torch.empty((n, cap), dtype=rows0.dtype, device=self.device),
+                    torch.empty((n, cap), dtype=cols0.dtype, device=self.device),
+                    torch.empty((n, cap, D), dtype=desc0.dtype, device=self.device),
+                    torch.empty((n,), dtype=cnt0.dtype, device=self.device))
             torch.cuda.synchronize(self.device)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):  # ... then capture
-                ent["outs"] = self._prepare_dev(ent["static"])
-            ent["graph"] = g
-        ent["graph"].replay()
+            graphs = []
+            for k0, k1 in chunks:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    part = self._prepare_dev(static[k0:k1])
+                    for dst, src in zip(comb, part):
+                        dst[k0:k1].copy_(src)
+                graphs.append(g)
+            ent["graphs"], ent["outs"] = graphs, comb
+        for g, ev in zip(ent["graphs"], ready):
+            cur.wait_event(ev)
+            g.replay()
         return ent["outs"]
 
     def prepare_device(self, batch) -> tuple:
@@ -240,20 +280,6 @@ class GraphEngine(GpuEngine):
     def _bound_cache(self, cache: dict) -> None:
         while len(cache) >= self.max_graphs:  # drop the oldest capture (dicts keep insertion order)
             cache.pop(next(iter(cache)))
-
-    def _upload(self, arrs, ent):
-        if all(isinstance(a, torch.Tensor) and a.is_pinned() for a in arrs):  # caller-pinned: straight to HBM
-            for k, a in enumerate(arrs):
-                ent["static"][k].copy_(a, non_blocking=True)
-            return
-        if ent["done"] is not None:
-            ent["done"].synchronize()  # the previous copy out of the pinned buffer has finished
-        pv = ent["pinned"].numpy()
-        cur = torch.cuda.current_stream(self.device)
-        for k, a in enumerate(arrs):  # image k's upload overlaps the staging of image k + 1
-            np.copyto(pv[k], a.numpy() if isinstance(a, torch.Tensor) else a)
-            ent["static"][k].copy_(ent["pinned"][k], non_blocking=True)
-        ent["done"] = cur.record_event()
 
     def register_many(self, items):
         if self.cfg.matcher_config().strategy != "nearest_neighbor":
