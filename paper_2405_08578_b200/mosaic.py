@@ -374,15 +374,19 @@ def build_pairwise_table(images: Sequence, cfg, *, engine=None, group=None) -> P
 
     h_cnt = g_cnt.cpu().numpy()  # one read of every image's keypoint count
 
+    views = {}  # per-image slot views, built once (tensor indexing costs microseconds per call)
+
     def img(k):  # image k lives on rank k % world, slot k // world
-        r, s = k % world, k // world
-        return g_rows[r, s], g_cols[r, s], g_desc[r, s], int(h_cnt[r, s])
+        if k not in views:
+            r, s = k % world, k // world
+            views[k] = (g_rows[r, s], g_cols[r, s], g_desc[r, s], int(h_cnt[r, s]))
+        return views[k]
 
     # phase 2: pairs in reference order, round-robin over ranks; on a GPU the
     # rank's pairs run concurrently on a few streams (each pair's small
     # kernels and count read-backs overlap the others')
     jobs = [(a, b) for a in range(n) for b in range(a + 1, n)]
-    res = torch.zeros((len(jobs), 5), dtype=torch.float64, device=dev)
+    res = torch.zeros((len(jobs), 5), dtype=torch.float64, device=dev) if world > 1 else None
     mine_q = list(range(rank, len(jobs), world))
 
     def run(q):
