@@ -9,6 +9,7 @@ Config parsing, reports and compositing are out of scope.
 
 from __future__ import annotations
 
+import functools
 import math
 import time
 from dataclasses import dataclass, fields, replace
@@ -260,8 +261,9 @@ def stitch_pair(img_a, img_b, cfg: PipelineConfig) -> StitchResult:
     return StitchResult(result is not None, result.transform if result else None, result, composite, report)
 
 
+@functools.lru_cache(maxsize=65536)
 def pair_seed(seed: int, a: int, b: int) -> int:
-    """mosaic.py:75-76."""
+    """mosaic.py:75-76 (SeedSequence hashing costs ~10 us: cached, it is a pure function)."""
     return int(np.random.SeedSequence([seed, a, b]).generate_state(1)[0])
 
 
