@@ -474,8 +474,9 @@ def bench_c5_pairs(args, world, rank, dev, n_pairs=256, steps=2):
             return []
         rows, cols, desc, cnt = geng.prepare_device(allimg)
         h = cnt.cpu().tolist()
-        items = [(rows[2 * q], cols[2 * q], desc[2 * q], h[2 * q], rows[2 * q + 1], cols[2 * q + 1],
-                  desc[2 * q + 1], h[2 * q + 1], cfg.seed) for q in range(len(grey))]
+        R, Cc, Dd = rows.unbind(0), cols.unbind(0), desc.unbind(0)  # per-image views in one call each
+        items = [(R[2 * q], Cc[2 * q], Dd[2 * q], h[2 * q], R[2 * q + 1], Cc[2 * q + 1], Dd[2 * q + 1],
+                  h[2 * q + 1], cfg.seed) for q in range(len(grey))]
         return [(None, o[0]) for o in geng.register_many(items)]
 
     n_sub = min(len(grey), 16)  # the one-pair-at-a-time variant on a bounded subset
