@@ -42,17 +42,26 @@ namespace tc {
 #ifndef PS_TC_XH
 #define PS_TC_XH 1
 #endif
+#ifndef PS_TC_BN
+#define PS_TC_BN (256 / PS_TC_XH)
+#endif
 constexpr int BMH = 128;       // X rows per operand tile / MMA (= TMEM lanes)
 constexpr int XH = PS_TC_XH;   // X tiles per CTA
 constexpr int BM = BMH * XH;   // X rows per CTA
-constexpr int BN = 256 / XH;   // Y rows per tile (= MMA N): XH accumulators x 2 buffers fill TMEM
+constexpr int BN = PS_TC_BN;   // Y rows per tile (= MMA N)
+constexpr int NACC = 512 / (XH * BN);  // accumulator buffers in flight (TMEM holds 512 columns)
+static_assert(NACC >= 2 && (NACC & (NACC - 1)) == 0, "TMEM ring");
 constexpr int KD = 128;        // descriptor length
 #ifndef PS_TC_TOPK
 #define PS_TC_TOPK 4
 #endif
 constexpr int TOPK = PS_TC_TOPK;  // candidates kept per (row, part, split)
-constexpr int STAGES_TOP = 2 * XH;       // Y-tile stages (XH = 1: 2 x 72 KB; 2: 4 x 36 KB)
-constexpr int STAGES_ENUM = XH + 1;      // the enumeration pass trades one stage for per-warp hit buffers
+// Y-tile stages: as many as fit beside the X tiles (XH = 1, BN = 256: 2 x 72 KB;
+// BN = 128: 5 x 36 KB); the enumeration pass trades some for per-warp hit buffers
+constexpr int kSmemBudget = 232448 - 2304;
+constexpr int STAGES_TOP = (kSmemBudget - XH * BMH * (128 * 2 + 32)) / (BN * (128 * 2 + 32));
+constexpr int STAGES_ENUM = (kSmemBudget - XH * BMH * (128 * 2 + 32) - 16 * (4096 / 16 * 8 + 16)) / (BN * (128 * 2 + 32));
+static_assert(STAGES_TOP >= 2 && STAGES_ENUM >= 2, "pipeline depth");
 #ifndef PS_EPI_WARPS
 #define PS_EPI_WARPS 16
 #endif
@@ -229,8 +238,8 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
   uint64_t* b_full = bars + 1;
   uint64_t* b_empty = b_full + STAGES;
   uint64_t* acc_full = b_empty + STAGES;
-  uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* acc_empty = acc_full + NACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + NACC);
   // MODE 1: per-epilogue-warp hit buffer + fill counter
   unsigned long long* hitbuf = reinterpret_cast<unsigned long long*>(bars + 32);
   int* hitcnt = reinterpret_cast<int*>(hitbuf + kEpiWarps * HITBUF);
@@ -247,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
       mbar_init(b_full + s, 1);
       mbar_init(b_empty + s, 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NACC; ++s) {
       mbar_init(acc_full + s, 1);
       mbar_init(acc_empty + s, kEpiWarps);  // one arrival per epilogue warp (512 thread arrivals serialised)
     }
@@ -299,8 +308,8 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
       const uint32_t a0 = smem_u32(sA);
       mbar_wait(a_full, 0);
       for (int t = 0; t < n_tiles; ++t) {
-        const int s = t % STAGES, ab = t & 1;
-        mbar_wait(acc_empty + ab, ((t >> 1) & 1) ^ 1);
+        const int s = t % STAGES, ab = t % NACC;
+        mbar_wait(acc_empty + ab, ((t / NACC) & 1) ^ 1);
         mbar_wait(b_full + s, (t / STAGES) & 1);
         tc_fence_after();
         const uint32_t b0 = smem_u32(sB + s * B_BYTES);
@@ -333,8 +342,8 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
     // dead rows (beyond the count; their X rows may be stale) get a NaN limit: no v compares <= NaN
     const float my_lim = (MODE == 1 && grow < nx) ? lim[grow] : __int_as_float(0x7fc00000);
     for (int t = 0; t < n_tiles; ++t) {
-      const int ab = t & 1;
-      mbar_wait(acc_full + ab, (t >> 1) & 1);
+      const int ab = t % NACC;
+      mbar_wait(acc_full + ab, (t / NACC) & 1);
       tc_fence_after();
       const int tg = t_begin + (t + t_rot < n_tiles ? t + t_rot : t + t_rot - n_tiles);  // global tile index
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (ab * XH + h) * BN + part * kCols;
@@ -353,14 +362,15 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
       // row's threshold (4th best, or the enumeration limit) with one branch
       unsigned long long* hb = hitbuf + ew * HITBUF;
       int fill = MODE == 1 ? hitcnt[ew] : 0;
+      constexpr int kChunk = kCols < 64 ? kCols : 64;  // TMEM columns per load (x64 or x32)
 #pragma unroll 1
-      for (int c0 = 0; c0 < kCols; c0 += 64) {
-        uint32_t r[64];
-        tmem_ld64(tbase + c0, r);
+      for (int c0 = 0; c0 < kCols; c0 += kChunk) {
+        uint32_t r[kChunk];
+        tmem_ld_cols(tbase + c0, r);
         tmem_ld_wait();
         const int jb = tg * BN + part * kCols + c0;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+        for (int q = 0; q < kChunk / 4; ++q) {
           const float v0 = __uint_as_float(r[4 * q + 0]);
           const float v1 = __uint_as_float(r[4 * q + 1]);
           const float v2 = __uint_as_float(r[4 * q + 2]);
