@@ -226,15 +226,18 @@ __global__ void pad_unused(unsigned long long* __restrict__ kp, unsigned long lo
 // spread over the whole GPU beat a one-CTA sort at these sizes.
 constexpr int kSmallSort = 16384;
 constexpr int kRankTile = 1024;
+constexpr int kRankLanes = 8;  // lanes per ranked entry (each compares against every 8th key)
 __global__ void __launch_bounds__(256) rank_scatter(const unsigned long long* __restrict__ kd,
                                                     const unsigned long long* __restrict__ kp,
                                                     const unsigned long long* __restrict__ counter, int n_max,
                                                     unsigned long long* __restrict__ kd_out,
                                                     unsigned long long* __restrict__ kp_out) {
   __shared__ unsigned long long td[kRankTile], tp[kRankTile];
+  constexpr int kPerBlock = 256 / kRankLanes;
   const int n = (int)min((unsigned long long)n_max, *counter);
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if ((int)(blockIdx.x * blockDim.x) >= n) return;  // uniform per block
+  if ((int)(blockIdx.x * kPerBlock) >= n) return;  // uniform per block
+  const int g = threadIdx.x & (kRankLanes - 1);
+  const int e = blockIdx.x * kPerBlock + threadIdx.x / kRankLanes;
   const unsigned long long d = e < n ? kd[e] : 0ull, p = e < n ? kp[e] : 0ull;
   int rank = 0;
   for (int t0 = 0; t0 < n; t0 += kRankTile) {
@@ -246,10 +249,12 @@ __global__ void __launch_bounds__(256) rank_scatter(const unsigned long long* __
     }
     __syncthreads();
     const int m = min(kRankTile, n - t0);
-#pragma unroll 8
-    for (int q = 0; q < m; ++q) rank += (td[q] < d) | ((td[q] == d) & (tp[q] < p));
+#pragma unroll 4
+    for (int q = g; q < m; q += kRankLanes) rank += (td[q] < d) | ((td[q] == d) & (tp[q] < p));
   }
-  if (e < n) {
+#pragma unroll
+  for (int o = 1; o < kRankLanes; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+  if (e < n && g == 0) {
     kd_out[rank] = d;
     kp_out[rank] = p;
   }
@@ -426,7 +431,8 @@ int match_impl(const void* desc1, int64_t n1, const void* desc2, int64_t n2, int
     n = (int)std::max<unsigned long long>(1ull, std::min<unsigned long long>(c, (unsigned long long)n));
   }
   if (n <= kSmallSort) {
-    rank_scatter<<<(n + 255) / 256, 256, 0, st>>>(w.kd, w.kp, w.counter, n, w.kd2, w.kp2);
+    rank_scatter<<<(n + 256 / kRankLanes - 1) / (256 / kRankLanes), 256, 0, st>>>(w.kd, w.kp, w.counter, n, w.kd2,
+                                                                                w.kp2);
     PS_LAUNCHED("rank_scatter");
     unpack_pairs<<<grid_blocks(n, 256), 256, 0, st>>>(w.kd2, w.kp2, w.counter, cap, out_ref1, out_ref2, out_delta,
                                                       out_count);

@@ -652,9 +652,11 @@ __global__ void hash_insert(const T* __restrict__ X, int64_t n, unsigned long lo
   for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
        i += (int64_t)gridDim.x * (blockDim.x >> 5)) {
     unsigned long long h = 0;
+    bool same_as_prev = i > 0;  // a run of identical rows: only its first row competes for the minimum
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const T v = X[i * KD + lane * 4 + e];
+      if (i > 0) same_as_prev &= v == X[(i - 1) * KD + lane * 4 + e];
       unsigned long long bits;
       if (sizeof(T) == 8) bits = (unsigned long long)__double_as_longlong((double)v);
       else bits = (unsigned long long)__float_as_uint((float)v);
@@ -665,6 +667,7 @@ __global__ void hash_insert(const T* __restrict__ X, int64_t n, unsigned long lo
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    same_as_prev = __all_sync(0xffffffffu, same_as_prev);
     if (lane == 0) {
       const unsigned long long key = h | 1ull;
       int64_t slot = (int64_t)((h >> 20) & (unsigned long long)(tsize - 1));
@@ -674,7 +677,9 @@ __global__ void hash_insert(const T* __restrict__ X, int64_t n, unsigned long lo
         if (prev == 0ull || prev == key) break;
         slot = (slot + 1) & (tsize - 1);
       }
-      if (*(volatile int32_t*)(tidx + slot) > (int32_t)i) atomicMin(tidx + slot, (int32_t)i);
+      // the run's first row (smaller index, same key) does it: thousands of
+      // identical flat-region rows would otherwise serialise on one address
+      if (!same_as_prev && *(volatile int32_t*)(tidx + slot) > (int32_t)i) atomicMin(tidx + slot, (int32_t)i);
       slot_of[i] = (int32_t)slot;
     }
   }
