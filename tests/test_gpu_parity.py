@@ -843,3 +843,38 @@ def test_ransac_with_device_count_equals_host_count():
         assert got.ok == one.ok and np.array_equal(got.inliers, one.inliers), m
         assert (got.theta, got.t_x, got.t_y, got.rms, got.consensus) == (one.theta, one.t_x, one.t_y, one.rms,
                                                                           one.consensus)
+
+
+def test_graph_engine_device_batch_rgb_pairs_equal_sequential():
+    """GraphEngine.prepare_device (RGB batch, replayed graph) + register_many
+    (replayed pair graph) give the per-pair sequential results on small C5-style
+    pairs, on the capture call and on replays."""
+    from paper_2405_08578_b200 import mosaic
+    from paper_2405_08578_b200.pipeline import PipelineConfig
+
+    cfg = PipelineConfig(window_min=16, window_max=64, ransac_iters=500)
+    pairs = [scenes.config5_pair(p, 270, 480)[:2] for p in range(3)]
+    pairs.append((pairs[0][0], pairs[0][0].copy()))  # an identical pair registers exactly
+    rgb = torch.from_numpy(np.stack([im for pr in pairs for im in pr])).cuda()
+    imgs = device.as_device_images(rgb, rgb=True)
+    sizes, dcfg = cfg.scale_set().sizes, cfg.descriptor_config()
+    kp = device.detect(imgs, sizes, meta=False)
+    d = device.describe(imgs, kp, dcfg, scale_set=kp.scale_set)
+    want = []
+    for q in range(len(pairs)):
+        r1, r2, _ = device.match(d[2 * q], d[2 * q + 1])
+        if int(r1.shape[0]) < cfg.min_inliers:
+            want.append((False, 0.0, 0.0, 0.0, 0))
+            continue
+        src, dst = device.pair_points(r1, r2, kp.row[2 * q], kp.col[2 * q], kp.row[2 * q + 1], kp.col[2 * q + 1])
+        o = device.ransac(src, dst, cfg.ransac_iters, cfg.ransac_tol, cfg.min_inliers, cfg.seed)
+        want.append((True, o.theta, o.t_x, o.t_y, int(o.inliers.shape[0])) if o.ok else (False, 0.0, 0.0, 0.0, 0))
+    eng = mosaic.GraphEngine(cfg, n_streams=3)
+    for _ in range(3):  # capture, then replays
+        rows, cols, desc, cnt = eng.prepare_device(imgs)
+        h = cnt.cpu().tolist()
+        R, Cc, Dd = rows.unbind(0), cols.unbind(0), desc.unbind(0)
+        items = [(R[2 * q], Cc[2 * q], Dd[2 * q], h[2 * q], R[2 * q + 1], Cc[2 * q + 1], Dd[2 * q + 1], h[2 * q + 1],
+                  cfg.seed) for q in range(len(pairs))]
+        assert eng.register_many(items) == want
+    assert want[-1][0] and want[-1][4] > 100  # the identical pair
