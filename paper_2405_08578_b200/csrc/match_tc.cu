@@ -384,29 +384,35 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
               if (v3 < fminf(tv[TOPK - 1], tsh)) topk_insert(v3, jb + 4 * q + 3, tv, tj);
             }
           } else if (__any_sync(0xffffffffu, m4 <= my_lim)) {
-            const float vv[4] = {v0, v1, v2, v3};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              // an inf limit (void certificate) enumerates every real column (padding columns hold +inf)
-              const bool hit = vv[e] <= my_lim && jb + 4 * q + e < ny;
-              const unsigned bal = __ballot_sync(0xffffffffu, hit);
-              if (bal) {
-                if (hit)
-                  hb[fill + __popc(bal & ((1u << lane) - 1u))] =
-                      ((unsigned long long)grow << 32) | (unsigned long long)(jb + 4 * q + e);
-                fill += __popc(bal);
-                if (fill > HITBUF - 32) {  // flush: one global atomic per buffer
-                  __syncwarp();
-                  unsigned long long base = 0;
-                  if (lane == 0) base = atomicAdd(n_pairs, (unsigned long long)fill);
-                  base = __shfl_sync(0xffffffffu, base, 0);
-                  for (int f = lane; f < fill; f += 32)
-                    if ((int64_t)(base + f) < cap) pairs[base + f] = hb[f];
-                  __syncwarp();
-                  fill = 0;
-                }
-              }
+            // an inf limit (void certificate) enumerates every real column (padding columns hold +inf).
+            // The group's hits (<= 4 per lane) are appended with one 3-bit-plane prefix sum.
+            const int jq = jb + 4 * q;
+            const unsigned hm = (unsigned)(v0 <= my_lim && jq < ny) | ((unsigned)(v1 <= my_lim && jq + 1 < ny) << 1) |
+                                ((unsigned)(v2 <= my_lim && jq + 2 < ny) << 2) |
+                                ((unsigned)(v3 <= my_lim && jq + 3 < ny) << 3);
+            const unsigned cnt = __popc(hm), lt = (1u << lane) - 1u;
+            const unsigned p0 = __ballot_sync(0xffffffffu, cnt & 1u), p1 = __ballot_sync(0xffffffffu, cnt & 2u),
+                           p2 = __ballot_sync(0xffffffffu, cnt & 4u);
+            const int pre = __popc(p0 & lt) + 2 * __popc(p1 & lt) + 4 * __popc(p2 & lt);
+            const int tot = __popc(p0) + 2 * __popc(p1) + 4 * __popc(p2);
+            if (fill + tot > HITBUF) {  // flush first (warp-uniform): one global atomic per buffer
+              __syncwarp();
+              unsigned long long base = 0;
+              if (lane == 0) base = atomicAdd(n_pairs, (unsigned long long)fill);
+              base = __shfl_sync(0xffffffffu, base, 0);
+              for (int f = lane; f < fill; f += 32)
+                if ((int64_t)(base + f) < cap) pairs[base + f] = hb[f];
+              __syncwarp();
+              fill = 0;
             }
+            unsigned m = hm;
+            int k = fill + pre;
+            while (m) {
+              const int e = __ffs(m) - 1;
+              m &= m - 1u;
+              hb[k++] = ((unsigned long long)grow << 32) | (unsigned long long)(jq + e);
+            }
+            fill += tot;
           }
         }
       }
