@@ -537,13 +537,40 @@ __global__ void certify_exact(const float* __restrict__ topv, const int32_t* __r
     }
     double bd = INFINITY;
     int bj = INT32_MAX;
+    // the (up to TOPK) candidate distances are computed together: TOPK
+    // independent accumulator chains per lane instead of TOPK serial ones
+    // (each distance keeps the reference's exact operation order)
+    bool cand[TOPK];
+    int yj[TOPK];
+    bool any = false;
 #pragma unroll
     for (int q = 0; q < TOPK; ++q) {
-      const bool cand = live && !over && tj[q] >= 0 && (double)tv[q] <= lim;
-      if (!__any_sync(0xffffffffu, cand)) continue;  // warp-uniform skip
-      const int yj = cand ? (y_orig ? y_orig[tj[q]] : tj[q]) : 0;
-      const double dd = exact_dist8(X + (int64_t)xi * KD, Y + (int64_t)yj * KD, t);
-      if (cand && (dd < bd || (dd == bd && yj < bj))) { bd = dd; bj = yj; }
+      cand[q] = live && !over && tj[q] >= 0 && (double)tv[q] <= lim;
+      yj[q] = cand[q] ? (y_orig ? y_orig[tj[q]] : tj[q]) : 0;
+      any |= cand[q];
+    }
+    if (__any_sync(0xffffffffu, any)) {  // warp-uniform
+      const T* xa = X + (int64_t)xi * KD;
+      double r[TOPK];
+#pragma unroll
+      for (int q = 0; q < TOPK; ++q) r[q] = 0.0;
+#pragma unroll 4
+      for (int m = 0; m < KD / 8; ++m) {
+        const double xe = (double)xa[8 * m + t];
+#pragma unroll
+        for (int q = 0; q < TOPK; ++q) {
+          const double e = __dsub_rn((double)Y[(int64_t)yj[q] * KD + 8 * m + t], xe);
+          r[q] = __dadd_rn(r[q], __dmul_rn(e, e));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < TOPK; ++q) {  // the 8-lane combination of exact_dist8
+        const double p1 = __dadd_rn(r[q], __shfl_down_sync(0xffffffffu, r[q], 1));
+        const double p2 = __dadd_rn(p1, __shfl_down_sync(0xffffffffu, p1, 2));
+        const double p4 = __dadd_rn(p2, __shfl_down_sync(0xffffffffu, p2, 4));
+        const double dd = __dsqrt_rn(p4);
+        if (cand[q] && (dd < bd || (dd == bd && yj[q] < bj))) { bd = dd; bj = yj[q]; }
+      }
     }
     if (live && !over && t == 0) {
       nn[xi] = bj;
