@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
   // certified margin are strictly below the 4th best, so ties at the 4th
   // place never decide them, and the enumeration collects every hit.
   const int t_rot = n_tiles > 0 ? (int)(((int64_t)rb * n_tiles) / gridDim.x) % n_tiles : 0;
+  const int n_pre = min(n_tiles, STAGES);  // Y tiles issued by thread 0 during the set-up
   const int64_t nx_pad = (int64_t)gridDim.x * BM;
   uint8_t* smem = smem_raw;  // 1024-aligned (SWIZZLE_128B atoms)
   uint8_t* sA = smem;
@@ -261,6 +262,16 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
       mbar_init(acc_empty + s, kEpiWarps);  // one arrival per epilogue warp (512 thread arrivals serialised)
     }
     mbar_fence_init();
+    // the operand copies start before the TMEM allocation and the CTA barrier:
+    // the X tiles and the first STAGES Y tiles (their stages start empty)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // initialised barriers -> async proxy
+    mbar_arrive_expect_tx(a_full, XH * A_BYTES);
+    bulk_g2s(sA, Xt + (size_t)rb * XH * A_BYTES, XH * A_BYTES, a_full);  // the CTA's XH tiles are contiguous
+    for (int t = 0; t < n_pre; ++t) {
+      const int tr = t + t_rot < n_tiles ? t + t_rot : t + t_rot - n_tiles;
+      mbar_arrive_expect_tx(b_full + t, B_BYTES);
+      bulk_g2s(sB + t * B_BYTES, Yt + (size_t)(t_begin + tr) * B_BYTES, B_BYTES, b_full + t);
+    }
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
@@ -279,14 +290,10 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
     // ---- bulk-copy producer: each tile in kCopyParts pieces issued by as
     // many lanes (one 72 KB request at a time left the copy engine idle
     // between tiles: the pipeline ran at ~2 us per tile, twice the MMA time)
-    if (lane == 0) {
-      mbar_arrive_expect_tx(a_full, XH * A_BYTES);
-      bulk_g2s(sA, Xt + (size_t)rb * XH * A_BYTES, XH * A_BYTES, a_full);  // the CTA's XH tiles are contiguous
-    }
     if (lane < kCopyParts) {
       constexpr uint32_t piece = B_BYTES / kCopyParts;
       static_assert(B_BYTES % (16 * kCopyParts) == 0, "16-byte pieces");
-      for (int t = 0; t < n_tiles; ++t) {
+      for (int t = n_pre; t < n_tiles; ++t) {
         const int s = t % STAGES;
         mbar_wait(b_empty + s, ((t / STAGES) & 1) ^ 1);
 #ifdef PS_TC_DIAG_NOCOPY  // diagnostic builds only: MMA rate on the resident stages (wrong results)
