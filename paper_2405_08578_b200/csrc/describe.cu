@@ -1167,6 +1167,16 @@ __device__ __forceinline__ bool describe_pair_w8(const Img& im, int row, int col
 }
 
 constexpr int kPairWarps = 8;
+#ifndef PS_PAIR_BLOCKS_PER_SM
+// Grid cap of the pair kernel in blocks per SM (3 are resident).  The grid
+// stride decides which keypoints are in flight together: with many short
+// grid-stride sweeps the resident blocks work on consecutive slots (their
+// 16x16 boxes overlap and the descriptor rows are written in order), with
+// one block per 8 pairs the block set-up dominates.  A/B on C2 (64 images):
+// 12 -> 9.79 ms, 48 -> 9.47, 100 -> 9.33, 200 -> 9.25, 400 -> 9.29,
+// 1200 -> 9.71, uncapped -> 9.84.
+#define PS_PAIR_BLOCKS_PER_SM 200
+#endif
 template <bool ORIENT, class Img>
 __global__ void __launch_bounds__(kPairWarps * 32, 3) describe_pair_kernel(Img img, int64_t img_stride, int B,
                                                                            const int32_t* __restrict__ kp_row,
@@ -1278,7 +1288,7 @@ int launch_fast(const Img& im, const ps_image_batch* img, const ps_keypoints* kp
     auto kern = prm.orient ? describe_pair_kernel<true, Img> : describe_pair_kernel<false, Img>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pshmem);
     int64_t pblocks = ((total + 1) / 2 + kPairWarps - 1) / kPairWarps;
-    if (pblocks > 148 * 12) pblocks = 148 * 12;
+    if (pblocks > 148 * PS_PAIR_BLOCKS_PER_SM) pblocks = 148 * PS_PAIR_BLOCKS_PER_SM;
     kern<<<(unsigned)pblocks, kPairWarps * 32, pshmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,
                                                              kp->scale, kp->count, kp->cap, prm, out_desc32,
                                                              out_desc64, work, n_work);
