@@ -1176,6 +1176,9 @@ constexpr int kPairWarps = 8;
 // 12 -> 9.79 ms, 48 -> 9.47, 100 -> 9.33, 200 -> 9.25, 400 -> 9.29,
 // 1200 -> 9.71, uncapped -> 9.84.
 #define PS_PAIR_BLOCKS_PER_SM 200
+#ifndef PS_W16_BLOCKS_PER_SM
+#define PS_W16_BLOCKS_PER_SM 100  // grid cap of the w = 16 kernel (A/B: 16 -> 0.707 ms, 100 -> 0.685 per 16 images)
+#endif
 #endif
 template <bool ORIENT, class Img>
 __global__ void __launch_bounds__(kPairWarps * 32, 3) describe_pair_kernel(Img img, int64_t img_stride, int B,
@@ -1277,7 +1280,7 @@ int launch_fast(const Img& im, const ps_image_batch* img, const ps_keypoints* kp
     const size_t fshmem = (size_t)kFastWarps * (FastBox<16>::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
     cudaFuncSetAttribute(describe_fast_u8<16, Img>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fshmem);
     int64_t fblocks = (total + kFastWarps - 1) / kFastWarps;
-    if (fblocks > 148 * 16) fblocks = 148 * 16;
+    if (fblocks > 148 * PS_W16_BLOCKS_PER_SM) fblocks = 148 * PS_W16_BLOCKS_PER_SM;
     describe_fast_u8<16, Img><<<(unsigned)fblocks, kFastWarps * 32, fshmem, s>>>(
         im, img->image_stride, img->batch, kp->row, kp->col, kp->scale, default_scale, kp->count, kp->cap, prm,
         out_desc32, out_desc64, work, n_work);
