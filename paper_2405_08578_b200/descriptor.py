@@ -12,7 +12,7 @@ import torch
 
 from . import device
 from .detector import device_images_of
-from .records import (DescribedFeatures, DescriptorConfig, DescriptorVector, region_size)
+from .records import (DescribedFeatures, DescriptorConfig, DescriptorVector, reference_module, region_size)
 
 __all__ = ["describe_features", "compute_descriptor", "DescriptorConfig", "DescribedFeatures", "region_size"]
 
@@ -23,9 +23,8 @@ def _validate(img, features, cfg) -> None:
         region_size(f.scale, cfg)  # ConfigError when scale > l_max (descriptor.py:89-90)
     if min(nr, nc) - 2 < cfg.d:
         raise ValueError(f"{nr}x{nc} image too small for a {cfg.d}x{cfg.d} subregion grid")
-    for f in features:
-        if not (0 <= f.row < nr and 0 <= f.col < nc):
-            raise ValueError(f"feature ({f.row}, {f.col}) outside the {nr}x{nc} image")
+    # features anywhere (even outside the image) are accepted: the region is
+    # translated inward like the reference's _fit_region (descriptor.py:118-131)
 
 
 def describe_tensor(img, features, cfg, out64=True):
@@ -46,11 +45,13 @@ def describe_tensor(img, features, cfg, out64=True):
 
 def describe_features(img, features, cfg) -> DescribedFeatures:
     features = list(features)
+    ref = reference_module("descriptor", img, cfg, *features[:1])
+    cls = ref.DescribedFeatures if ref else DescribedFeatures
     if not features:
-        return DescribedFeatures(image_id=img.source_id, features=[], descriptors=np.zeros((0, cfg.length)))
+        return cls(image_id=img.source_id, features=[], descriptors=np.zeros((0, cfg.length)))
     _validate(img, features, cfg)
     mat = describe_tensor(img, features, cfg, out64=True).cpu().numpy()
-    return DescribedFeatures(image_id=img.source_id, features=features, descriptors=mat)
+    return cls(image_id=img.source_id, features=features, descriptors=mat)
 
 
 def compute_descriptor(img, fp, cfg) -> DescriptorVector:
@@ -60,4 +61,6 @@ def compute_descriptor(img, fp, cfg) -> DescriptorVector:
     cap = min(img.nr, img.nc) - 2
     if w > cap:
         w = cap - cap % cfg.d
-    return DescriptorVector(values=vals, feature=fp, region_size=w, subregion_size=w // cfg.d)
+    ref = reference_module("descriptor", img, fp, cfg)
+    cls = ref.DescriptorVector if ref else DescriptorVector
+    return cls(values=vals, feature=fp, region_size=w, subregion_size=w // cfg.d)

@@ -13,7 +13,7 @@ import torch
 
 from . import device
 from .records import (MIN_WINDOW, POLARITY_MAX, POLARITY_MIN, FeaturePoint, ScaleSet, Window,
-                      partition_windows, window_count)
+                      partition_windows, reference_module, window_count)
 
 __all__ = ["detect_features", "ScaleSet", "FeaturePoint", "Window", "partition_windows", "window_count",
            "MIN_WINDOW", "POLARITY_MAX", "POLARITY_MIN", "device_images_of"]
@@ -47,9 +47,9 @@ def device_images_of(img) -> device.DeviceImages:
     return device.as_device_images(np.asarray(px, dtype=np.float64), img.alpha, ramped=True)
 
 
-def features_from_arrays(h: dict) -> list:
+def features_from_arrays(h: dict, cls=FeaturePoint) -> list:
     pol = (POLARITY_MAX, POLARITY_MIN)
-    return [FeaturePoint(int(r), int(c), int(s), pol[int(p)], int(w), float(v))
+    return [cls(int(r), int(c), int(s), pol[int(p)], int(w), float(v))
             for r, c, s, p, w, v in zip(h["row"], h["col"], h["scale"], h["polarity"], h["window"], h["value"])]
 
 
@@ -57,4 +57,5 @@ def detect_features(img, scales, dedupe: bool = True) -> list:
     """Window extrema over every scale, deduplicated and sorted (scale, window, polarity)."""
     scales.validate_for(img.nr, img.nc)
     kp = device.detect(device_images_of(img), scales.sizes, dedupe=dedupe, meta=True)
-    return features_from_arrays(kp.image(0))
+    ref = reference_module("detector", img, scales)
+    return features_from_arrays(kp.image(0), ref.FeaturePoint if ref else FeaturePoint)

@@ -11,7 +11,7 @@ import numpy as np
 import torch
 
 from . import device
-from .records import STRATEGY_NEAREST, STRATEGY_THRESHOLD_ALL, MatcherConfig, MatchPair
+from .records import STRATEGY_NEAREST, STRATEGY_THRESHOLD_ALL, MatcherConfig, MatchPair, reference_module
 
 __all__ = ["match_features", "MatcherConfig", "MatchPair", "STRATEGY_NEAREST", "STRATEGY_THRESHOLD_ALL",
            "match_tensors"]
@@ -38,5 +38,7 @@ def match_features(set1, set2, cfg) -> list:
     r1, r2, dl = match_tensors(set1.descriptors, set2.descriptors, cfg)
     r1, r2, dl = r1.cpu().numpy(), r2.cpu().numpy(), dl.cpu().numpy()
     f1, f2 = set1.features, set2.features
-    return [MatchPair(p1=(f1[i].row, f1[i].col), p2=(f2[j].row, f2[j].col), delta=float(d), ref1=int(i),
+    ref = reference_module("matcher", set1, set2, cfg)
+    cls = ref.MatchPair if ref else MatchPair
+    return [cls(p1=(f1[i].row, f1[i].col), p2=(f2[j].row, f2[j].col), delta=float(d), ref1=int(i),
                       ref2=int(j)) for i, j, d in zip(r1, r2, dl)]

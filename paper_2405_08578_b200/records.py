@@ -322,3 +322,19 @@ def apply_transform(transform, point) -> tuple:
     x, y = point
     c, s = math.cos(transform.theta), math.sin(transform.theta)
     return (c * x - s * y + transform.t_x, s * x + c * y + transform.t_y)
+
+
+# ---- reference interop ---------------------------------------------------------
+
+def reference_module(name: str, *objs):
+    """``peakstitch.<name>`` when any of ``objs`` is an object of the reference
+    package (its dataclasses), else None.  The drop-ins then build their
+    results from the reference's own classes, so code written against the
+    reference (``==`` on ``FeaturePoint``/``MatchPair``, ``isinstance``) sees
+    exactly its own types."""
+    for o in objs:
+        if type(o).__module__.split(".", 1)[0] == "peakstitch":
+            import importlib
+
+            return importlib.import_module("peakstitch." + name)
+    return None

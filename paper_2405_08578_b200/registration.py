@@ -8,12 +8,14 @@ in the C-ABI library.
 
 from __future__ import annotations
 
+import sys
+
 import numpy as np
 import torch
 
 from . import _lib, device
 from .errors import DegenerateSampleError, RegistrationError
-from .records import (RansacConfig, RegistrationResult, RigidTransform, apply_transform)
+from .records import (RansacConfig, RegistrationResult, RigidTransform, apply_transform, reference_module)
 
 __all__ = ["ransac_rigid", "estimate_rigid", "transfer_errors", "RansacConfig", "RegistrationResult",
            "RigidTransform", "apply_transform", "ransac_points"]
@@ -25,7 +27,7 @@ def _points(pairs):
     return src, dst
 
 
-def ransac_points(src, dst, cfg) -> RegistrationResult:
+def ransac_points(src, dst, cfg, _ref=None) -> RegistrationResult:
     """RANSAC on (n, 2) (x, y) point arrays (numpy or device tensors)."""
     n = int(src.shape[0])
     if n < cfg.min_inliers:
@@ -37,8 +39,10 @@ def ransac_points(src, dst, cfg) -> RegistrationResult:
         raise DegenerateSampleError("source points are coincident")
     if not out.ok:
         raise RegistrationError(f"best consensus {out.consensus} below min_inliers {cfg.min_inliers}")
-    return RegistrationResult(transform=RigidTransform(out.theta, out.t_x, out.t_y),
-                              inliers=out.inliers.tolist(), residual_rms=out.rms, consensus_size=out.consensus)
+    ref = _ref or reference_module("registration", cfg)
+    res_cls, tr_cls = (ref.RegistrationResult, ref.RigidTransform) if ref else (RegistrationResult, RigidTransform)
+    return res_cls(transform=tr_cls(out.theta, out.t_x, out.t_y), inliers=out.inliers.tolist(),
+                   residual_rms=out.rms, consensus_size=out.consensus)
 
 
 def ransac_rigid(pairs, cfg) -> RegistrationResult:
@@ -46,7 +50,7 @@ def ransac_rigid(pairs, cfg) -> RegistrationResult:
     if n < cfg.min_inliers:
         raise RegistrationError(f"only {n} candidate pairs, need at least {cfg.min_inliers}")
     src, dst = _points(pairs)
-    return ransac_points(src, dst, cfg)
+    return ransac_points(src, dst, cfg, reference_module("registration", cfg, pairs[0]))
 
 
 def estimate_rigid(src, dst) -> RigidTransform:
@@ -59,7 +63,9 @@ def estimate_rigid(src, dst) -> RigidTransform:
     th, tx, ty, st = device.estimate(torch.from_numpy(src).cuda(), torch.from_numpy(dst).cuda())
     if st != _lib.PS_OK:
         raise DegenerateSampleError("source points are coincident")
-    return RigidTransform(theta=th, t_x=tx, t_y=ty)
+    # array arguments carry no type: follow the reference when it is loaded
+    ref = sys.modules.get("peakstitch.registration")
+    return (ref.RigidTransform if ref else RigidTransform)(theta=th, t_x=tx, t_y=ty)
 
 
 def transfer_errors(transform, src, dst) -> np.ndarray:
