@@ -29,7 +29,8 @@
  *    synchronised.  Outcomes that depend on data (e.g. "no consensus") are
  *    reported through device-side info words, not the return status.
  *  - No hidden global mutable state other than the launch counter and the
- *    thread-local last-error message; all calls are re-entrant.
+ *    thread-local last-error message / match statistics; no environment
+ *    variables are read; all calls are re-entrant.
  */
 #ifndef PEAKSTITCH_B200_H
 #define PEAKSTITCH_B200_H
@@ -41,7 +42,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 3
+#define PS_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define PS_API __attribute__((visibility("default")))
@@ -76,9 +77,25 @@ enum ps_pixel_type {
 };
 
 enum ps_match_strategy {
-  PS_MATCH_NEAREST = 0,      /* "nearest_neighbor": mutual NN + dist < delta_s */
-  PS_MATCH_THRESHOLD_ALL = 1 /* "threshold_all": every dist < delta_s         */
+  PS_MATCH_NEAREST = 0,       /* "nearest_neighbor": mutual NN + dist < delta_s
+                                 (matcher.py:71-79)                            */
+  PS_MATCH_THRESHOLD_ALL = 1, /* "threshold_all": every dist < delta_s
+                                 (matcher.py:69-70)                            */
+  PS_MATCH_RATIO = 2          /* "ratio_test": an EXTRA strategy the reference
+                                 does not have (the north star's
+                                 Lowe ratio): row i keeps its first nearest
+                                 neighbour j when d1 < r * d2, d2 the row's
+                                 second-smallest distance (a duplicate of the
+                                 best counts); r is passed in `delta_s`, in
+                                 (0, 1]; no mutual check, no absolute cut    */
 };
+/* Path selection, OR-ed into `strategy` per call (no environment switches):
+ * by default nearest_neighbor on 128-d descriptors uses the tensor-core
+ * kernels when n1 * n2 >= 2^20 and the float64 CUDA-core kernels otherwise;
+ * results are identical either way (contract P3). */
+#define PS_MATCH_FORCE_EXACT 0x100 /* float64 CUDA-core kernels                */
+#define PS_MATCH_FORCE_TC 0x200    /* tensor-core kernels where the strategy
+                                      has them (nearest_neighbor, dim 128)     */
 
 /* A batch of B equally sized images in device memory. */
 typedef struct ps_image_batch {
@@ -115,7 +132,7 @@ PS_API uint64_t ps_kernel_launches(void);    /* kernels launched by this library
 PS_API int ps_device_sync(void* stream);     /* cudaStreamSynchronize + error check       */
 
 /* ---- detect: detector.py:154-172 --------------------------------------- */
-/* Validates the scale set (ScaleSet rules, detector.py:188-217) against the
+/* Validates the scale set (ScaleSet rules, detector.py:33-68) against the
  * image and reports the per-image output capacity and workspace size. */
 PS_API int ps_detect_plan(int32_t batch, int32_t nr, int32_t nc, const int32_t* host_scales,
                    int32_t n_scales, int32_t dedupe, int64_t* cap_out,
@@ -127,19 +144,31 @@ PS_API int ps_detect(const ps_image_batch* img, const int32_t* host_scales, int3
 /* ---- describe: descriptor.py:219-269 ------------------------------------ */
 /* host_scale_set lists every scale that may occur in kp->scale (the ScaleSet);
  * region sizes are derived on the host per scale (descriptor.py:82-95, 118-131).
- * Keypoints must lie inside the image and carry a scale of the set (slots
- * that do not are skipped, unwritten).  Output row k of out_desc32 / out_desc64 ([B*cap, 8*d*d], row-major) is the
- * descriptor of keypoint slot k; slots >= count are not written.  Either
- * output pointer may be NULL. */
+ * Keypoints may lie anywhere (the region is translated inward as
+ * _fit_region does, descriptor.py:118-131) and must carry a scale of the set
+ * (slots that do not are skipped, unwritten).  Output row k of out_desc32 /
+ * out_desc64 ([B*cap, 8*d*d], row-major) is the descriptor of keypoint slot
+ * k; slots >= count are not written.  Either output pointer may be NULL. */
 PS_API int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, int32_t default_scale,
                 const int32_t* host_scale_set, int32_t n_scale_set, double beta0, int32_t d,
                 int32_t l_max, int32_t orientation_normalize, float* out_desc32,
                 double* out_desc64, void* stream);
+/* ps_describe with an explicit kernel policy (tests / A-B measurements; the
+ * descriptors agree to float64 rounding under every policy):
+ * PS_DESCRIBE_AUTO as ps_describe; PS_DESCRIBE_GENERAL the general float64
+ * kernel for every keypoint; PS_DESCRIBE_SINGLE the one-keypoint-per-warp
+ * fast kernel instead of the two-keypoints-per-warp one (w = 8). */
+enum ps_describe_policy { PS_DESCRIBE_AUTO = 0, PS_DESCRIBE_GENERAL = 1, PS_DESCRIBE_SINGLE = 2 };
+PS_API int ps_describe_ex(const ps_image_batch* img, const ps_keypoints* kp, int32_t default_scale,
+                const int32_t* host_scale_set, int32_t n_scale_set, double beta0, int32_t d,
+                int32_t l_max, int32_t orientation_normalize, float* out_desc32,
+                double* out_desc64, int32_t policy, void* stream);
 
 /* ---- match: matcher.py:57-95 -------------------------------------------- */
 PS_API int ps_match_plan(int64_t n1, int64_t n2, int32_t dim, int32_t strategy, int64_t cap,
                   size_t* workspace_bytes_out);
-/* desc1 [n1, dim], desc2 [n2, dim] row-major, float32 (desc_is_f64 = 0; the
+/* `strategy` is a ps_match_strategy, optionally OR-ed with a PS_MATCH_FORCE_*
+ * flag.  desc1 [n1, dim], desc2 [n2, dim] row-major, float32 (desc_is_f64 = 0; the
  * values are upcast to float64 exactly) or float64 (desc_is_f64 = 1).  All
  * distance arithmetic is the reference's float64 arithmetic.
  * Writes up to `cap` pairs sorted by (delta, ref1, ref2) and the total pair
@@ -164,11 +193,11 @@ PS_API int ps_match_async(const void* desc1, int64_t n1, const void* desc2, int6
  * the exact first argmin over the rows of Y of the reference distance to row
  * i of X (matcher.py:74 with _distance_matrix :48-54).  The building block of
  * row-sharded matching across GPUs (each rank: its rows of A vs all of B,
- * and the candidate columns vs its rows). */
-PS_API int ps_nearest_plan(int64_t nx, int64_t ny, int32_t dim, size_t* workspace_bytes_out);
+ * and the candidate columns vs its rows).  flags: 0 or one PS_MATCH_FORCE_*. */
+PS_API int ps_nearest_plan(int64_t nx, int64_t ny, int32_t dim, int32_t flags, size_t* workspace_bytes_out);
 PS_API int ps_nearest(const void* X, int64_t nx, const void* Y, int64_t ny, int32_t dim, int32_t desc_is_f64,
-                      int32_t* out_index, double* out_dist, void* workspace, size_t workspace_bytes,
-                      void* stream);
+                      int32_t flags, int32_t* out_index, double* out_dist, void* workspace,
+                      size_t workspace_bytes, void* stream);
 
 /* Statistics of the calling thread's last tensor-core ps_match (diagnostic):
  * out[0..5] = distinct rows of desc1, of desc2, candidate columns, rows

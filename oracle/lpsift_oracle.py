@@ -263,13 +263,13 @@ def describe(P, kps, beta0=0.0625, d=4, l_max=128, orient=True) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------
-# matcher.py:317-364 -- exact float64 distances, MNN / threshold_all, order
+# matcher.py:48-95 -- exact float64 distances, MNN / threshold_all, order
 # ---------------------------------------------------------------------------
 
 def distances(A: np.ndarray, B: np.ndarray, chunk: int = 32):
     """Yield (i0, dist[i0:i1, :]) with the reference's bits.
 
-    matcher.py:317-323 uses ``np.linalg.norm(b - a[i], axis=1)``, i.e. a
+    matcher.py:48-54 uses ``np.linalg.norm(b - a[i], axis=1)``, i.e. a
     contiguous last-axis add.reduce of squares (numpy pairwise summation),
     then sqrt; the same reduction is applied here chunk-wise.
     """
@@ -281,13 +281,28 @@ def distances(A: np.ndarray, B: np.ndarray, chunk: int = 32):
 
 
 def match(A, B, delta_s: float = 0.35, strategy: str = "nearest_neighbor"):
-    """match_features (matcher.py:326-364) -> (ref1, ref2, delta) sorted."""
+    """match_features (matcher.py:57-95) -> (ref1, ref2, delta) sorted.
+
+    ``strategy="ratio_test"`` is the EXTRA Lowe-ratio strategy the reference
+    does not have: ``delta_s`` is the ratio r, and row i keeps
+    its first nearest neighbour j when d1 < r * d2 (float64), d2 the row's
+    second-smallest distance (a duplicate of the best counts; inf when B has
+    one row).  Its own oracle, not pinned by the reference.
+    """
     n1, n2 = len(A), len(B)
     if n1 == 0 or n2 == 0:
         e = np.zeros(0, np.int64)
         return e, e.copy(), np.zeros(0)
     r1, r2, dl = [], [], []
-    if strategy == "threshold_all":
+    if strategy == "ratio_test":
+        for i0, D in distances(A, B):
+            j = np.argmin(D, axis=1)
+            rows = np.arange(D.shape[0])
+            d1 = D[rows, j]
+            d2 = np.partition(D, 1, axis=1)[:, 1] if n2 > 1 else np.full(D.shape[0], np.inf)
+            ok = d1 < delta_s * d2
+            r1.append(rows[ok] + i0), r2.append(j[ok]), dl.append(d1[ok])
+    elif strategy == "threshold_all":
         for i0, D in distances(A, B):
             ii, jj = np.nonzero(D < delta_s)  # row-major, like np.argwhere
             r1.append(ii + i0), r2.append(jj), dl.append(D[ii, jj])

@@ -17,8 +17,10 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpeakstit
 PS_OK, PS_ERR_CONFIG, PS_ERR_VALUE, PS_ERR_DEGENERATE, PS_ERR_REGISTRATION = 0, 1, 2, 3, 4
 PS_ERR_CUDA, PS_ERR_ARGUMENT, PS_ERR_CAPACITY = 5, 6, 7
 PS_PIXELS_U8, PS_PIXELS_F64, PS_PIXELS_F64_RAW, PS_PIXELS_RGB8 = 0, 1, 2, 3
-ABI_VERSION = 3
-PS_MATCH_NEAREST, PS_MATCH_THRESHOLD_ALL = 0, 1
+ABI_VERSION = 4
+PS_MATCH_NEAREST, PS_MATCH_THRESHOLD_ALL, PS_MATCH_RATIO = 0, 1, 2
+PS_MATCH_FORCE_EXACT, PS_MATCH_FORCE_TC = 0x100, 0x200  # per-call path selection (OR-ed into the strategy)
+PS_DESCRIBE_AUTO, PS_DESCRIBE_GENERAL, PS_DESCRIBE_SINGLE = 0, 1, 2
 
 
 class ImageBatch(C.Structure):
@@ -56,6 +58,9 @@ SIGNATURES = {
     "ps_describe": (C.c_int, [C.POINTER(ImageBatch), C.POINTER(KeypointsC), C.c_int32,
                               C.POINTER(C.c_int32), C.c_int32, C.c_double, C.c_int32, C.c_int32,
                               C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ps_describe_ex": (C.c_int, [C.POINTER(ImageBatch), C.POINTER(KeypointsC), C.c_int32,
+                                 C.POINTER(C.c_int32), C.c_int32, C.c_double, C.c_int32, C.c_int32,
+                                 C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "ps_match_plan": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int64,
                                 C.POINTER(C.c_size_t)]),
     "ps_match": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_double,
@@ -66,9 +71,9 @@ SIGNATURES = {
                                  C.c_void_p, C.c_size_t, C.c_void_p]),
     "ps_pair_points": (C.c_int, [C.c_void_p] * 9 + [C.c_int64, C.c_void_p]),
     "ps_match_stats": (C.c_int, [C.POINTER(C.c_int64), C.c_int32]),
-    "ps_nearest_plan": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.POINTER(C.c_size_t)]),
-    "ps_nearest": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
-                             C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "ps_nearest_plan": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]),
+    "ps_nearest": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "ps_ransac_plan": (C.c_int, [C.c_int64, C.c_int32, C.POINTER(C.c_size_t)]),
     "ps_ransac_rigid": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32,
                                   C.c_double, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -9,6 +9,7 @@
 // like np.bincount, so equal inputs give bit-identical descriptors (F6).
 // atan2 / hypot are CUDA's float64 versions (numpy's own differ from libm by
 // ~1 ulp), hence the 1e-4 relative parity bar of contract P2.
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -809,7 +810,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
       for (int s = 0; s < prm.n_scales; ++s)
         if (prm.scale[s] == scale) { w = prm.w[s]; fx = prm.fx[s]; lb = prm.lb[s]; }
     }
-    if (w < 0 || row < 0 || row >= im.nr || col < 0 || col >= im.nc) continue;  // validated by the caller
+    if (w < 0) continue;  // scale outside the set (unwritten); any position is fine (_fit_region clamps)
     float* o32 = out32 ? out32 + g * D : nullptr;
     double* o64 = out64 ? out64 + g * D : nullptr;
     constexpr bool kFast = std::is_same<Img, RampU8>::value;
@@ -822,6 +823,16 @@ __global__ void __launch_bounds__(kWarps * 32, 3) describe_kernel(Img img, int64
     } else {
       describe_keypoint<0, 0, kFast>(im, row, col, w, prm.d, fx, lb, prm, hw, stage, o32, o64);
     }
+  }
+}
+
+// (image, slot) walk of a grid-stride loop: slot += qstep * cap + rstep
+__device__ __forceinline__ void advance_slot(int& b, int64_t& i, int qstep, int64_t rstep, int64_t cap) {
+  b += qstep;
+  i += rstep;
+  if (i >= cap) {
+    i -= cap;
+    ++b;
   }
 }
 
@@ -858,16 +869,17 @@ __global__ void __launch_bounds__(kFastWarps * 32, W == 8 ? PS_FAST_MINB : 3) de
   int64_t g = (int64_t)blockIdx.x * kFastWarps + wid;
   int b = (int)(g / cap);
   int64_t i = g - (int64_t)b * cap;
-  for (; g < total; g += S, i += S) {
-    while (i >= cap) {
-      i -= cap;
-      ++b;
-    }
+  const int qstep = (int)(S / cap);
+  const int64_t rstep = S - (int64_t)qstep * cap;
+  for (; g < total; g += S, advance_slot(b, i, qstep, rstep, cap)) {
     if (counts && i >= counts[b]) continue;
     Img im = img;
     im.p = img.p + (int64_t)b * img_stride * decltype(img)::kElem;
     const int row = kp_row[g], col = kp_col[g];
-    if (row < 0 || row >= im.nr || col < 0 || col >= im.nc) continue;  // validated by the caller
+    if (row < 0 || row >= im.nr || col < 0 || col >= im.nc) {  // outside the image: general kernel (it clamps)
+      if (lane == 0) work[atomicAdd(n_work, 1ull)] = g;
+      continue;
+    }
     bool fast = (W == 8 ? prm.default_w8 : prm.default_w16) && im.nr >= BX && im.nc >= BX;
     if (kp_scale) {
       const int scale = kp_scale[g];
@@ -1176,9 +1188,9 @@ constexpr int kPairWarps = 8;
 // 12 -> 9.79 ms, 48 -> 9.47, 100 -> 9.33, 200 -> 9.25, 400 -> 9.29,
 // 1200 -> 9.71, uncapped -> 9.84.
 #define PS_PAIR_BLOCKS_PER_SM 200
+#endif
 #ifndef PS_W16_BLOCKS_PER_SM
 #define PS_W16_BLOCKS_PER_SM 100  // grid cap of the w = 16 kernel (A/B: 16 -> 0.707 ms, 100 -> 0.685 per 16 images)
-#endif
 #endif
 template <bool ORIENT, class Img>
 __global__ void __launch_bounds__(kPairWarps * 32, 3) describe_pair_kernel(Img img, int64_t img_stride, int B,
@@ -1203,12 +1215,10 @@ __global__ void __launch_bounds__(kPairWarps * 32, 3) describe_pair_kernel(Img i
   int64_t gi0 = 2 * ((int64_t)blockIdx.x * kPairWarps + wid) + hsel;
   int bcur = (int)(gi0 / cap);
   int64_t icur = gi0 - (int64_t)bcur * cap;
+  const int qstep = (int)(gstep / cap);  // gstep = qstep * cap + rstep: O(1) per step for any cap
+  const int64_t rstep = gstep - (int64_t)qstep * cap;
   for (int64_t pi = (int64_t)blockIdx.x * kPairWarps + wid; pi < npairs;
-       pi += (int64_t)gridDim.x * kPairWarps, icur += gstep) {
-    while (icur >= cap) {
-      icur -= cap;
-      ++bcur;
-    }
+       pi += (int64_t)gridDim.x * kPairWarps, advance_slot(bcur, icur, qstep, rstep, cap)) {
     const int64_t g = 2 * pi + hsel;  // this half's slot
     bool live = g < total;
     int b = 0;
@@ -1217,8 +1227,9 @@ __global__ void __launch_bounds__(kPairWarps * 32, 3) describe_pair_kernel(Img i
       live = !counts || icur < counts[b];
     }
     int row = live ? kp_row[g] : 8, col = live ? kp_col[g] : 8;
-    if (live && (row < 0 || row >= img.nr || col < 0 || col >= img.nc)) live = false;  // validated by the caller
-    bool fast = live && box_ok;
+    // keypoints outside the image (the reference translates their region
+    // inward, descriptor.py:118-131) go to the general kernel
+    bool fast = live && box_ok && row >= 0 && row < img.nr && col >= 0 && col < img.nc;
     if (fast) {
       if (kp_scale) {
         const int scale = kp_scale[g];
@@ -1247,8 +1258,8 @@ __global__ void __launch_bounds__(kPairWarps * 32, 3) describe_pair_kernel(Img i
 template <class Img>
 int launch_fast(const Img& im, const ps_image_batch* img, const ps_keypoints* kp, int32_t default_scale,
                 const DescParams& prm, float* out_desc32, double* out_desc64, int64_t total, size_t shmem,
-                cudaStream_t s) {
-  if (getenv("PS_DESCRIBE_GENERIC") != nullptr) {  // diagnostic: the general kernel for every keypoint
+                int policy, cudaStream_t s) {
+  if (policy == PS_DESCRIBE_GENERAL) {  // the general kernel for every keypoint
     int64_t blocks = (total + kWarps - 1) / kWarps;
     if (blocks > 148 * 8) blocks = 148 * 8;
     describe_kernel<Img><<<(unsigned)blocks, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row,
@@ -1259,23 +1270,24 @@ int launch_fast(const Img& im, const ps_image_batch* img, const ps_keypoints* kp
     return check_cuda("describe_kernel");
   }
   int64_t* work = nullptr;
-  static bool pool_set = false;  // keep freed queue memory in the stream-ordered pool
-  if (!pool_set) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+  static std::atomic<unsigned long long> pool_set{0};  // per device: keep freed queue memory in the pool
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(pool_set.load() & bit)) {  // idempotent: racing threads set the same attribute
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t thr = UINT64_MAX;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    pool_set = true;
+    pool_set.fetch_or(bit);
   }
   cudaMallocAsync(&work, (size_t)total * sizeof(int64_t) + 16, s);
   int st = check_cuda("cudaMallocAsync(describe work list)");
   if (st) return st;
   unsigned long long* n_work = reinterpret_cast<unsigned long long*>(work + total);
   cudaMemsetAsync(n_work, 0, sizeof(unsigned long long), s);
-  const bool pair = getenv("PS_DESCRIBE_SINGLE") == nullptr;  // A/B switch (diagnostic, read per call)
+  const bool pair = policy != PS_DESCRIBE_SINGLE;
   if (prm.n_w8 == 0 && prm.n_w16 > 0) {  // w = 16 scales only (e.g. the default 32..128 windows)
     const size_t fshmem = (size_t)kFastWarps * (FastBox<16>::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
     cudaFuncSetAttribute(describe_fast_u8<16, Img>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fshmem);
@@ -1317,8 +1329,18 @@ int launch_fast(const Img& im, const ps_image_batch* img, const ps_keypoints* kp
 extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, int32_t default_scale,
                            const int32_t* host_scale_set, int32_t n_scale_set, double beta0, int32_t d, int32_t l_max,
                            int32_t orientation_normalize, float* out_desc32, double* out_desc64, void* stream) {
+  return ps_describe_ex(img, kp, default_scale, host_scale_set, n_scale_set, beta0, d, l_max, orientation_normalize,
+                        out_desc32, out_desc64, PS_DESCRIBE_AUTO, stream);
+}
+
+extern "C" int ps_describe_ex(const ps_image_batch* img, const ps_keypoints* kp, int32_t default_scale,
+                              const int32_t* host_scale_set, int32_t n_scale_set, double beta0, int32_t d,
+                              int32_t l_max, int32_t orientation_normalize, float* out_desc32, double* out_desc64,
+                              int32_t policy, void* stream) {
   PS_REQUIRE(img && kp && img->data && kp->row && kp->col && host_scale_set, PS_ERR_ARGUMENT,
              "null argument to ps_describe");
+  PS_REQUIRE(policy == PS_DESCRIBE_AUTO || policy == PS_DESCRIBE_GENERAL || policy == PS_DESCRIBE_SINGLE,
+             PS_ERR_ARGUMENT, "unknown describe policy %d", policy);
   PS_REQUIRE(beta0 > 0, PS_ERR_CONFIG, "beta0 must be positive, got %g", beta0);
   PS_REQUIRE(d >= 1, PS_ERR_CONFIG, "subregion grid count must be >= 1, got %d", d);
   PS_REQUIRE(l_max >= 1, PS_ERR_CONFIG, "l_max must be >= 1, got %d", l_max);
@@ -1405,11 +1427,11 @@ extern "C" int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, in
   cudaFuncSetAttribute(describe_kernel<RampF64Raw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
   if (img->pixel_type == PS_PIXELS_U8) {
     RampU8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
-    return launch_fast(im, img, kp, default_scale, prm, out_desc32, out_desc64, total, shmem, s);
+    return launch_fast(im, img, kp, default_scale, prm, out_desc32, out_desc64, total, shmem, policy, s);
   } else if (img->pixel_type == PS_PIXELS_RGB8) {
     RampRGB8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha, img->gray_lut};
     cudaFuncSetAttribute(describe_kernel<RampRGB8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
-    return launch_fast(im, img, kp, default_scale, prm, out_desc32, out_desc64, total, shmem, s);
+    return launch_fast(im, img, kp, default_scale, prm, out_desc32, out_desc64, total, shmem, policy, s);
   } else if (img->pixel_type == PS_PIXELS_F64_RAW) {
     RampF64Raw im{(const double*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
     describe_kernel<<<(unsigned)blocks, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,

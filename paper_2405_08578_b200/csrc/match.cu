@@ -12,7 +12,6 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
-#include <cstdlib>
 
 #include "ps_common.cuh"
 
@@ -28,14 +27,20 @@ int ps_tc_rows_impl(const T* X, int64_t nx, const T* Y, int64_t ny, int32_t* nn,
 namespace ps {
 namespace {
 
-// tensor-core path: 128-d nearest_neighbor problems large enough to pay off
-// (PS_MATCH_EXACT=1 forces the float64 CUDA-core path; PS_TC_MIN_PAIRS sets
-// the size threshold -- both for tests and diagnostics)
-bool use_tc(int64_t n1, int64_t n2, int dim, int strategy) {
-  if (strategy != PS_MATCH_NEAREST || dim != 128 || getenv("PS_MATCH_EXACT") != nullptr) return false;
-  const char* m = getenv("PS_TC_MIN_PAIRS");
-  const int64_t min_pairs = m ? atoll(m) : ((int64_t)1 << 20);
-  return n1 * n2 >= min_pairs;
+// tensor-core path: 128-d nearest_neighbor problems large enough to pay off,
+// unless the caller's per-call flags (OR-ed into `strategy`, see
+// ps_match_strategy) force one path.  No environment switches.
+constexpr int64_t kTcMinPairs = (int64_t)1 << 20;
+int base_strategy(int32_t strategy) { return strategy & 0xff; }
+bool use_tc(int64_t n1, int64_t n2, int dim, int32_t strategy) {
+  if (base_strategy(strategy) != PS_MATCH_NEAREST || dim != 128 || (strategy & PS_MATCH_FORCE_EXACT)) return false;
+  return (strategy & PS_MATCH_FORCE_TC) || n1 * n2 >= kTcMinPairs;
+}
+bool valid_strategy(int32_t strategy) {
+  const int b = base_strategy(strategy);
+  return (b == PS_MATCH_NEAREST || b == PS_MATCH_THRESHOLD_ALL || b == PS_MATCH_RATIO) &&
+         (strategy & ~(0xff | PS_MATCH_FORCE_EXACT | PS_MATCH_FORCE_TC)) == 0 &&
+         !((strategy & PS_MATCH_FORCE_EXACT) && (strategy & PS_MATCH_FORCE_TC));
 }
 
 constexpr int TILE = 32;     // rows x cols per tile
@@ -63,14 +68,17 @@ __device__ __forceinline__ void load_tile(double* s, const T* __restrict__ X, in
 
 // For each row of X: first argmin over Y of the exact distance.
 // 256 threads as 16x16, each owning a 2x2 micro-tile of (row, col) pairs.
-template <class T>
+// TOP2 also keeps the second-smallest distance of the row (a tie with the
+// best counts: then second == best), for the ratio test.
+template <class T, bool TOP2 = false>
 __global__ void __launch_bounds__(256) nn_pass(const T* __restrict__ X, int64_t nx, const T* __restrict__ Y,
                                                int64_t ny, int dim, int32_t* __restrict__ best_j,
-                                               double* __restrict__ best_d) {
+                                               double* __restrict__ best_d, double* __restrict__ second_d = nullptr) {
   extern __shared__ double sm[];
   double* Xs = sm;
   double* Ys = sm + TILE * SPAD;
   __shared__ double red_d[TILE][16];
+  __shared__ double red_d2[TOP2 ? TILE : 1][16];
   __shared__ int red_j[TILE][16];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int nk = dim / 8;
@@ -78,6 +86,7 @@ __global__ void __launch_bounds__(256) nn_pass(const T* __restrict__ X, int64_t 
     __syncthreads();
     load_tile(Xs, X, nx, i0, dim);
     double bd[2] = {INFINITY, INFINITY};
+    double b2[2] = {INFINITY, INFINITY};
     int bj[2] = {INT32_MAX, INT32_MAX};
     for (int64_t j0 = 0; j0 < ny; j0 += TILE) {
       __syncthreads();
@@ -110,7 +119,13 @@ __global__ void __launch_bounds__(256) nn_pass(const T* __restrict__ X, int64_t 
           const int64_t j = j0 + tx + 16 * b;
           if (j < ny) {
             const double dd = finish8(acc[a][b]);
-            if (lex_less(dd, (int)j, bd[a], bj[a])) { bd[a] = dd; bj[a] = (int)j; }
+            if (lex_less(dd, (int)j, bd[a], bj[a])) {
+              if (TOP2) b2[a] = bd[a];
+              bd[a] = dd;
+              bj[a] = (int)j;
+            } else if (TOP2) {
+              b2[a] = fmin(b2[a], dd);
+            }
           }
         }
     }
@@ -119,17 +134,26 @@ __global__ void __launch_bounds__(256) nn_pass(const T* __restrict__ X, int64_t 
     for (int a = 0; a < 2; ++a) {
       red_d[ty + 16 * a][tx] = bd[a];
       red_j[ty + 16 * a][tx] = bj[a];
+      if (TOP2) red_d2[ty + 16 * a][tx] = b2[a];
     }
     __syncthreads();
     if (threadIdx.x < TILE) {
       const int r = threadIdx.x;
-      double d = red_d[r][0];
+      double d = red_d[r][0], d2 = TOP2 ? red_d2[r][0] : 0.0;
       int j = red_j[r][0];
-      for (int q = 1; q < 16; ++q)
-        if (lex_less(red_d[r][q], red_j[r][q], d, j)) { d = red_d[r][q]; j = red_j[r][q]; }
+      for (int q = 1; q < 16; ++q) {
+        if (lex_less(red_d[r][q], red_j[r][q], d, j)) {
+          if (TOP2) d2 = fmin(d, red_d2[r][q]);
+          d = red_d[r][q];
+          j = red_j[r][q];
+        } else if (TOP2) {
+          d2 = fmin(d2, red_d[r][q]);
+        }
+      }
       if (i0 + r < nx) {
         best_j[i0 + r] = j;
         best_d[i0 + r] = d;
+        if (TOP2) second_d[i0 + r] = d2;
       }
     }
   }
@@ -205,6 +229,22 @@ __global__ void mnn_select(const int32_t* __restrict__ nn12, const double* __res
     if (nn21[j] == (int32_t)i && d12[i] < delta_s) {
       const unsigned long long slot = atomicAdd(counter, 1ull);
       keys_pair[slot] = ((unsigned long long)i << 32) | (unsigned long long)j;
+      keys_delta[slot] = (unsigned long long)__double_as_longlong(d12[i]);
+    }
+  }
+}
+
+// ratio test (extra strategy, not in the reference; SURVEY.md F2 / north
+// star "Lowe ratio"): row i keeps its first nearest neighbour when
+// best < ratio * second, float64 as the oracle computes it.
+__global__ void ratio_select(const int32_t* __restrict__ nn12, const double* __restrict__ d12,
+                             const double* __restrict__ d12b, int64_t n1, double ratio,
+                             unsigned long long* __restrict__ keys_pair, unsigned long long* __restrict__ keys_delta,
+                             unsigned long long* __restrict__ counter) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n1; i += (int64_t)gridDim.x * blockDim.x) {
+    if (d12[i] < __dmul_rn(ratio, d12b[i])) {
+      const unsigned long long slot = atomicAdd(counter, 1ull);
+      keys_pair[slot] = ((unsigned long long)i << 32) | (unsigned long long)nn12[i];
       keys_delta[slot] = (unsigned long long)__double_as_longlong(d12[i]);
     }
   }
@@ -314,7 +354,7 @@ MatchWs carve(void* base, int64_t n1, int64_t n2, int64_t cand, size_t* used, si
   w.nn12 = a.take<int32_t>(n1);
   w.d12 = a.take<double>(n1);
   w.nn21 = a.take<int32_t>(n2);
-  w.d21 = a.take<double>(n2);
+  w.d21 = a.take<double>(n1 > n2 ? n1 : n2);  // column distances, or the rows' second-best (ratio test)
   w.kp = a.take<unsigned long long>(cand);
   w.kd = a.take<unsigned long long>(cand);
   w.kp2 = a.take<unsigned long long>(cand);
@@ -329,7 +369,8 @@ MatchWs carve(void* base, int64_t n1, int64_t n2, int64_t cand, size_t* used, si
 }
 
 int64_t candidate_cap(int64_t n1, int64_t n2, int strategy, int64_t cap) {
-  return strategy == PS_MATCH_NEAREST ? (n1 < n2 ? n1 : n2) : cap;
+  strategy = base_strategy(strategy);
+  return strategy == PS_MATCH_NEAREST ? (n1 < n2 ? n1 : n2) : strategy == PS_MATCH_RATIO ? n1 : cap;
 }
 
 int grid_blocks(int64_t work, int per) {
@@ -344,7 +385,15 @@ int launch_match(const T* desc1, int64_t n1, const T* desc2, int64_t n2, int dim
   const size_t shmem = 2 * TILE * SPAD * sizeof(double);
   cudaFuncSetAttribute(nn_pass<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
   cudaFuncSetAttribute(threshold_pass<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
-  if (strategy == PS_MATCH_NEAREST) {
+  strategy = base_strategy(strategy);
+  if (strategy == PS_MATCH_RATIO) {
+    cudaFuncSetAttribute(nn_pass<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
+    // d21 holds the rows' second-best distances (no column pass)
+    nn_pass<T, true><<<grid_blocks(n1, TILE), 256, shmem, st>>>(desc1, n1, desc2, n2, dim, w.nn12, w.d12, w.d21);
+    PS_LAUNCHED("nn_pass(rows,top2)");
+    ratio_select<<<grid_blocks(n1, 256), 256, 0, st>>>(w.nn12, w.d12, w.d21, n1, delta_s, w.kp, w.kd, w.counter);
+    PS_LAUNCHED("ratio_select");
+  } else if (strategy == PS_MATCH_NEAREST) {
     nn_pass<T><<<grid_blocks(n1, TILE), 256, shmem, st>>>(desc1, n1, desc2, n2, dim, w.nn12, w.d12);
     PS_LAUNCHED("nn_pass(rows)");
     nn_pass<T><<<grid_blocks(n2, TILE), 256, shmem, st>>>(desc2, n2, desc1, n1, dim, w.nn21, w.d21);
@@ -368,8 +417,7 @@ using namespace ps;
 extern "C" int ps_match_plan(int64_t n1, int64_t n2, int32_t dim, int32_t strategy, int64_t cap,
                              size_t* workspace_bytes_out) {
   PS_REQUIRE(n1 >= 0 && n2 >= 0 && cap >= 0, PS_ERR_ARGUMENT, "bad sizes");
-  PS_REQUIRE(strategy == PS_MATCH_NEAREST || strategy == PS_MATCH_THRESHOLD_ALL, PS_ERR_CONFIG,
-             "unknown match strategy %d", strategy);
+  PS_REQUIRE(valid_strategy(strategy), PS_ERR_CONFIG, "unknown match strategy %d", strategy);
   size_t used = 0;
   carve(nullptr, n1, n2, candidate_cap(n1, n2, strategy, cap), &used,
         use_tc(n1, n2, dim, strategy) ? ps_tc_nearest_ws(n1, n2) : 0);
@@ -382,8 +430,9 @@ int match_impl(const void* desc1, int64_t n1, const void* desc2, int64_t n2, int
                double delta_s, int32_t strategy, int32_t* out_ref1, int32_t* out_ref2, double* out_delta,
                int64_t* out_count, int64_t cap, void* workspace, size_t workspace_bytes, void* stream, bool sync) {
   PS_REQUIRE(delta_s > 0, PS_ERR_CONFIG, "delta_s must be positive, got %g", delta_s);
-  PS_REQUIRE(strategy == PS_MATCH_NEAREST || strategy == PS_MATCH_THRESHOLD_ALL, PS_ERR_CONFIG,
-             "unknown match strategy %d", strategy);
+  PS_REQUIRE(valid_strategy(strategy), PS_ERR_CONFIG, "unknown match strategy %d", strategy);
+  PS_REQUIRE(base_strategy(strategy) != PS_MATCH_RATIO || delta_s <= 1.0, PS_ERR_CONFIG,
+             "ratio must be in (0, 1], got %g", delta_s);
   PS_REQUIRE(dim >= 8 && dim % 8 == 0 && dim <= kMaxDim, PS_ERR_ARGUMENT,
              "descriptor length %d unsupported (multiple of 8, <= %d)", dim, kMaxDim);
   PS_REQUIRE(out_count, PS_ERR_ARGUMENT, "null out_count");
@@ -482,22 +531,25 @@ extern "C" int ps_pair_points(const int32_t* ref1, const int32_t* ref2, const in
   return PS_OK;
 }
 
-extern "C" int ps_nearest_plan(int64_t nx, int64_t ny, int32_t dim, size_t* workspace_bytes_out) {
+extern "C" int ps_nearest_plan(int64_t nx, int64_t ny, int32_t dim, int32_t flags, size_t* workspace_bytes_out) {
   PS_REQUIRE(nx >= 0 && ny >= 0, PS_ERR_ARGUMENT, "bad sizes");
   PS_REQUIRE(dim >= 8 && dim % 8 == 0 && dim <= kMaxDim, PS_ERR_ARGUMENT, "descriptor length %d unsupported", dim);
+  PS_REQUIRE(valid_strategy(PS_MATCH_NEAREST | flags), PS_ERR_ARGUMENT, "bad flags %d", flags);
   if (workspace_bytes_out)
-    *workspace_bytes_out = use_tc(nx, ny, dim, PS_MATCH_NEAREST) ? ps_tc_nearest_ws(nx, ny) : 256;
+    *workspace_bytes_out = use_tc(nx, ny, dim, PS_MATCH_NEAREST | flags) ? ps_tc_nearest_ws(nx, ny) : 256;
   return PS_OK;
 }
 
 extern "C" int ps_nearest(const void* X, int64_t nx, const void* Y, int64_t ny, int32_t dim, int32_t desc_is_f64,
-                          int32_t* out_index, double* out_dist, void* workspace, size_t workspace_bytes, void* stream) {
+                          int32_t flags, int32_t* out_index, double* out_dist, void* workspace, size_t workspace_bytes,
+                          void* stream) {
   PS_REQUIRE(dim >= 8 && dim % 8 == 0 && dim <= kMaxDim, PS_ERR_ARGUMENT, "descriptor length %d unsupported", dim);
+  PS_REQUIRE(valid_strategy(PS_MATCH_NEAREST | flags), PS_ERR_ARGUMENT, "bad flags %d", flags);
   PS_REQUIRE(nx < INT32_MAX && ny < INT32_MAX, PS_ERR_ARGUMENT, "too many descriptors");
   if (nx == 0) return PS_OK;
   PS_REQUIRE(X && Y && out_index && out_dist && ny > 0, PS_ERR_ARGUMENT, "null argument / empty Y in ps_nearest");
   cudaStream_t st = (cudaStream_t)stream;
-  if (use_tc(nx, ny, dim, PS_MATCH_NEAREST)) {
+  if (use_tc(nx, ny, dim, PS_MATCH_NEAREST | flags)) {
     return desc_is_f64 ? ps_tc_rows_impl((const double*)X, nx, (const double*)Y, ny, out_index, out_dist, workspace,
                                          workspace_bytes, st)
                        : ps_tc_rows_impl((const float*)X, nx, (const float*)Y, ny, out_index, out_dist, workspace,

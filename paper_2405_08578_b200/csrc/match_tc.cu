@@ -860,7 +860,9 @@ dim3 tc_grid(int64_t rows, int64_t cols, bool throughput = false) {
     const int64_t cost = waves * ((tiles + s - 1) / s + 4 * XH);
     if (cost < best_cost) { best_cost = cost; best = s; }
   }
-  if (const char* e = getenv("PS_TC_SPLIT")) best = std::max(1, std::min({atoi(e), kMaxSplit, tiles}));  // diagnostic
+#ifdef PS_DIAG  // diagnostic builds only (-DPS_DIAG): the product library reads no environment
+  if (const char* e = getenv("PS_TC_SPLIT")) best = std::max(1, std::min({atoi(e), kMaxSplit, tiles}));
+#endif
   return dim3(rb, best);
 }
 
@@ -956,12 +958,9 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   PS_LAUNCHED("prep_tiles(X)");
   prep_tiles<T><<<grid_for(yrows, 8), 256, 0, st>>>(Y, y_idx, n_y, 0, yrows, BN, w.yt, w.yinfo, w.ymax, 1, BN);
   PS_LAUNCHED("prep_tiles(Y)");
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(nn_topk_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<0>());
-    cudaFuncSetAttribute(nn_topk_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<1>());
-    attr = true;
-  }
+  // the attribute is per device: set it on every call (cheap, idempotent, thread-safe)
+  cudaFuncSetAttribute(nn_topk_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<0>());
+  cudaFuncSetAttribute(nn_topk_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<1>());
   // the counts size the grids; a caller that already knows one passes it in (>= 0)
   int64_t nx = nx_io && *nx_io >= 0 ? *nx_io : -1, ny = ny_io && *ny_io >= 0 ? *ny_io : -1;
   if (!sync) {  // no host round trip: grids sized by the upper bounds, the kernels read the device counts
@@ -1042,8 +1041,12 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   PS_REQUIRE(ws && ws_bytes >= need, PS_ERR_ARGUMENT, "tensor-core match workspace %zu < %zu", ws_bytes, need);
   TcWs w = carve_tc(ws, n1, n2, &need);
   for (int q = 0; q < 8; ++q) g_stats[q] = 0;
-  // PS_TC_PROFILE=1: per-stage timing and counters on stderr (diagnostic; syncs)
+  // PS_TC_PROFILE=1 in a -DPS_DIAG build: per-stage timing and counters on stderr (syncs)
+#ifdef PS_DIAG
   const bool prof = sync && getenv("PS_TC_PROFILE") != nullptr;
+#else
+  constexpr bool prof = false;
+#endif
   cudaEvent_t ev[8];
   int nev = 0;
   auto mark = [&]() {

@@ -202,8 +202,12 @@ def detect(images, scales, *, alpha=None, dedupe=True, ramped=False, meta=True, 
     return kp
 
 
+DESCRIBE_POLICIES = {"auto": _lib.PS_DESCRIBE_AUTO, "general": _lib.PS_DESCRIBE_GENERAL,
+                     "single": _lib.PS_DESCRIBE_SINGLE}
+
+
 def describe(images, kp: Keypoints, cfg, *, alpha=None, ramped=False, scale_set=None, out64=False,
-             out32=True, stream=None):
+             out32=True, stream=None, policy: str = "auto"):
     """Descriptors of every keypoint slot (descriptor.py:219-269).
 
     Returns float32 [B, cap, D] (and float64 if ``out64``); slots >= count
@@ -219,9 +223,10 @@ def describe(images, kp: Keypoints, cfg, *, alpha=None, ramped=False, scale_set=
     d64 = torch.zeros((kp.batch, kp.cap, D), dtype=torch.float64, device=dev) if out64 else None
     L = _lib.lib()
     ib, kc = im.c_struct(), kp.c_struct()
-    _lib.check(L.ps_describe(C.byref(ib), C.byref(kc), int(kp.default_scale), _lib.int32_array(sset), len(sset),
-                             float(cfg.beta0), int(cfg.d), int(cfg.l_max), int(bool(cfg.orientation_normalize)),
-                             _ptr(d32), _ptr(d64), C.c_void_p(_stream_ptr(stream))), "describe")
+    _lib.check(L.ps_describe_ex(C.byref(ib), C.byref(kc), int(kp.default_scale), _lib.int32_array(sset), len(sset),
+                                float(cfg.beta0), int(cfg.d), int(cfg.l_max), int(bool(cfg.orientation_normalize)),
+                                _ptr(d32), _ptr(d64), DESCRIBE_POLICIES[policy], C.c_void_p(_stream_ptr(stream))),
+               "describe")
     if out64 and out32:
         return d32, d64
     return d64 if out64 else d32
@@ -242,13 +247,25 @@ def describe_into(images, kp: Keypoints, cfg, out32: torch.Tensor, *, scale_set=
 # matching
 # ---------------------------------------------------------------------------
 
-STRATEGIES = {"nearest_neighbor": _lib.PS_MATCH_NEAREST, "threshold_all": _lib.PS_MATCH_THRESHOLD_ALL}
+STRATEGIES = {"nearest_neighbor": _lib.PS_MATCH_NEAREST, "threshold_all": _lib.PS_MATCH_THRESHOLD_ALL,
+              "ratio_test": _lib.PS_MATCH_RATIO}
+# explicit per-call kernel path (include/peakstitch_b200.h PS_MATCH_FORCE_*); results are identical
+PATHS = {"auto": 0, "exact": _lib.PS_MATCH_FORCE_EXACT, "tensor": _lib.PS_MATCH_FORCE_TC}
+
+
+def _path_flag(path: str) -> int:
+    if path not in PATHS:
+        raise ValueError(f"unknown match path {path!r} (auto / exact / tensor)")
+    return PATHS[path]
 
 
 def match(desc1: torch.Tensor, desc2: torch.Tensor, delta_s: float = 0.35, strategy: str = "nearest_neighbor",
-          cap: int | None = None, stream=None):
+          cap: int | None = None, stream=None, path: str = "auto"):
     """Matches sorted by (delta, ref1, ref2) (matcher.py:57-95).
 
+    ``strategy`` "ratio_test" is the extra Lowe-ratio strategy (not in the
+    reference): ``delta_s`` is then the ratio r in (0, 1] and row i keeps its
+    first nearest neighbour when d1 < r * d2.
     Returns device tensors (ref1 int32 [M], ref2 int32 [M], delta float64 [M]).
     """
     if strategy not in STRATEGIES:
@@ -268,7 +285,8 @@ def match(desc1: torch.Tensor, desc2: torch.Tensor, delta_s: float = 0.35, strat
         return e, e.clone(), torch.zeros(0, dtype=torch.float64, device=dev)
     strat = STRATEGIES[strategy]
     if cap is None:
-        cap = min(n1, n2) if strat == _lib.PS_MATCH_NEAREST else max(4 * (n1 + n2), 1024)
+        cap = {_lib.PS_MATCH_NEAREST: min(n1, n2), _lib.PS_MATCH_RATIO: n1}.get(strat, max(4 * (n1 + n2), 1024))
+    strat |= _path_flag(path)
     L = _lib.lib()
     while True:
         wsb = C.c_size_t()
@@ -286,7 +304,8 @@ def match(desc1: torch.Tensor, desc2: torch.Tensor, delta_s: float = 0.35, strat
         cap = m  # threshold_all overflow: retry with the exact size
 
 
-def match_async(desc1: torch.Tensor, desc2: torch.Tensor, delta_s: float = 0.35, *, out_count=None, stream=None):
+def match_async(desc1: torch.Tensor, desc2: torch.Tensor, delta_s: float = 0.35, *, out_count=None, stream=None,
+                path: str = "auto"):
     """nearest_neighbor matching enqueued with no host synchronisation
     (ps_match_async; same results as ``match``).  Returns device tensors
     (ref1 int32 [cap], ref2 int32 [cap], delta float64 [cap], count int64 [1]);
@@ -310,10 +329,11 @@ def match_async(desc1: torch.Tensor, desc2: torch.Tensor, delta_s: float = 0.35,
         return r1, r2, dl, cnt
     L = _lib.lib()
     wsb = C.c_size_t()
-    _lib.check(L.ps_match_plan(n1, n2, dim, _lib.PS_MATCH_NEAREST, cap, C.byref(wsb)), "match")
+    strat = _lib.PS_MATCH_NEAREST | _path_flag(path)
+    _lib.check(L.ps_match_plan(n1, n2, dim, strat, cap, C.byref(wsb)), "match")
     ws = _workspace(wsb.value, dev)
     _lib.check(L.ps_match_async(_ptr(d1), n1, _ptr(d2), n2, dim, int(dt == torch.float64), float(delta_s),
-                                _lib.PS_MATCH_NEAREST, _ptr(r1), _ptr(r2), _ptr(dl), _ptr(cnt), cap, _ptr(ws),
+                                strat, _ptr(r1), _ptr(r2), _ptr(dl), _ptr(cnt), cap, _ptr(ws),
                                 wsb.value, C.c_void_p(_stream_ptr(stream))), "match")
     return r1, r2, dl, cnt
 
@@ -602,7 +622,7 @@ def kernel_launches() -> int:
     return _lib.kernel_launches()
 
 
-def nearest(X: torch.Tensor, Y: torch.Tensor, stream=None):
+def nearest(X: torch.Tensor, Y: torch.Tensor, stream=None, path: str = "auto"):
     """Exact first-argmin nearest row of Y for every row of X (one direction of
     nearest_neighbor matching).  Returns (index int32 [nx], dist float64 [nx])."""
     dt = torch.float64 if (X.dtype == torch.float64 or Y.dtype == torch.float64) else torch.float32
@@ -615,9 +635,10 @@ def nearest(X: torch.Tensor, Y: torch.Tensor, stream=None):
         return idx, dist
     L = _lib.lib()
     wsb = C.c_size_t()
-    _lib.check(L.ps_nearest_plan(nx, ny, dim, C.byref(wsb)), "nearest")
+    flags = _path_flag(path)
+    _lib.check(L.ps_nearest_plan(nx, ny, dim, flags, C.byref(wsb)), "nearest")
     ws = _workspace(wsb.value, X.device)
-    _lib.check(L.ps_nearest(_ptr(X), nx, _ptr(Y), ny, dim, int(dt == torch.float64), _ptr(idx), _ptr(dist), _ptr(ws),
+    _lib.check(L.ps_nearest(_ptr(X), nx, _ptr(Y), ny, dim, int(dt == torch.float64), flags, _ptr(idx), _ptr(dist), _ptr(ws),
                             wsb.value, C.c_void_p(_stream_ptr(stream))), "nearest")
     return idx, dist
 

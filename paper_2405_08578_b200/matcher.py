@@ -11,9 +11,10 @@ import numpy as np
 import torch
 
 from . import device
-from .records import STRATEGY_NEAREST, STRATEGY_THRESHOLD_ALL, MatcherConfig, MatchPair, reference_module
+from .records import (STRATEGY_NEAREST, STRATEGY_RATIO, STRATEGY_THRESHOLD_ALL, MatcherConfig, MatchPair,
+                      reference_module)
 
-__all__ = ["match_features", "MatcherConfig", "MatchPair", "STRATEGY_NEAREST", "STRATEGY_THRESHOLD_ALL",
+__all__ = ["match_features", "MatcherConfig", "MatchPair", "STRATEGY_NEAREST", "STRATEGY_THRESHOLD_ALL", "STRATEGY_RATIO",
            "match_tensors"]
 
 
@@ -28,6 +29,8 @@ def _dev(desc) -> torch.Tensor:
 
 def match_tensors(desc1, desc2, cfg):
     """Device (ref1, ref2, delta) of two descriptor matrices."""
+    if cfg.strategy == STRATEGY_RATIO:  # extra strategy: the threshold argument carries the ratio
+        return device.match(_dev(desc1), _dev(desc2), cfg.ratio, STRATEGY_RATIO)
     return device.match(_dev(desc1), _dev(desc2), cfg.delta_s, cfg.strategy)
 
 

@@ -165,10 +165,11 @@ class GpuEngine:
     def register(self, ra, ca, da, na, rb, cb, db, nb, seed):
         """match + RANSAC of one pair -> (ok, theta, t_x, t_y, n_inliers)."""
         from . import device
+        from .matcher import match_tensors
 
         cfg = self.cfg
         mc, rc = cfg.matcher_config(), cfg.ransac_config(seed)
-        r1, r2, _ = device.match(da[:na], db[:nb], mc.delta_s, mc.strategy)
+        r1, r2, _ = match_tensors(da[:na], db[:nb], mc)
         if int(r1.shape[0]) < rc.min_inliers:
             return (False, 0.0, 0.0, 0.0, 0)
         src, dst = device.pair_points(r1, r2, ra, ca, rb, cb)

@@ -19,8 +19,9 @@ import torch
 
 from . import device
 from .detector import features_from_arrays
+from .matcher import match_tensors
 from .errors import ConfigError
-from .records import (STRATEGY_NEAREST, STRATEGY_THRESHOLD_ALL, DescribedFeatures, DescriptorConfig,
+from .records import (STRATEGY_NEAREST, STRATEGY_RATIO, STRATEGY_THRESHOLD_ALL, DescribedFeatures, DescriptorConfig,
                       IntensityImage, MatcherConfig, MatchPair, RansacConfig, RegistrationResult, RigidTransform,
                       ScaleSet, apply_linear_ramp, default_alpha)
 
@@ -44,6 +45,7 @@ class PipelineConfig:
     threads: int = 1
     blend: str = "feather"
     resample: str = "bilinear"
+    match_ratio: float = 0.8  # extra "ratio_test" strategy only (not a reference field)
 
     def __post_init__(self):
         if self.alpha is not None and (not math.isfinite(self.alpha) or self.alpha <= 0):
@@ -57,7 +59,7 @@ class PipelineConfig:
                               f"[{self.window_min}, {self.window_max}] with d={self.d}")
         if self.delta_s <= 0:
             raise ConfigError(f"delta_s must be positive, got {self.delta_s}")
-        if self.match_strategy not in (STRATEGY_NEAREST, STRATEGY_THRESHOLD_ALL):
+        if self.match_strategy not in (STRATEGY_NEAREST, STRATEGY_THRESHOLD_ALL, STRATEGY_RATIO):
             raise ConfigError(f"unknown match strategy {self.match_strategy!r}")
         if self.ransac_iters < 1 or self.ransac_tol <= 0 or self.min_inliers < 2:
             raise ConfigError("invalid RANSAC parameters")
@@ -71,7 +73,7 @@ class PipelineConfig:
         return DescriptorConfig(self.beta0, self.d, self.window_max, self.orientation_normalize)
 
     def matcher_config(self) -> MatcherConfig:
-        return MatcherConfig(self.delta_s, self.match_strategy)
+        return MatcherConfig(self.delta_s, self.match_strategy, self.match_ratio)
 
     def ransac_config(self, seed: int | None = None) -> RansacConfig:
         return RansacConfig(self.ransac_iters, self.ransac_tol, self.min_inliers, self.seed if seed is None else seed)
@@ -171,7 +173,7 @@ def _pairs_host(prep_a, prep_b, r1, r2, dl) -> list:
 def register_device(prep_a: PreparedImage, prep_b: PreparedImage, cfg: PipelineConfig, seed=None):
     """match -> RANSAC entirely on the GPU; returns (r1, r2, delta, RansacOutcome|None)."""
     mc = cfg.matcher_config()
-    r1, r2, dl = device.match(prep_a.descriptors, prep_b.descriptors, mc.delta_s, mc.strategy)
+    r1, r2, dl = match_tensors(prep_a.descriptors, prep_b.descriptors, mc)
     rc = cfg.ransac_config(seed)
     n = int(r1.shape[0])
     if n < rc.min_inliers:
@@ -188,7 +190,7 @@ def register_prepared(prep_a: PreparedImage, prep_b: PreparedImage, cfg: Pipelin
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     mc = cfg.matcher_config()
-    r1, r2, dl = device.match(prep_a.descriptors, prep_b.descriptors, mc.delta_s, mc.strategy)
+    r1, r2, dl = match_tensors(prep_a.descriptors, prep_b.descriptors, mc)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     pairs = _pairs_host(prep_a, prep_b, r1, r2, dl)

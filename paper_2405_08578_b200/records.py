@@ -27,6 +27,7 @@ from .errors import ConfigError
 MIN_WINDOW = 8
 POLARITY_MAX, POLARITY_MIN = "max", "min"
 STRATEGY_NEAREST, STRATEGY_THRESHOLD_ALL = "nearest_neighbor", "threshold_all"
+STRATEGY_RATIO = "ratio_test"  # extra strategy (not in the reference): Lowe ratio, MatcherConfig.ratio
 ORIENTATION_BINS, PEAK_BINS = 8, 36
 TWO_PI = 2.0 * math.pi
 RAMP_SPAN_LIMIT = 0.05 * 255.0
@@ -232,14 +233,19 @@ class DescriptorVector:
 
 @dataclass(frozen=True)
 class MatcherConfig:
+    """matcher.py:16-25, plus ``ratio`` for the extra "ratio_test" strategy."""
+
     delta_s: float = 0.35
     strategy: str = STRATEGY_NEAREST
+    ratio: float = 0.8
 
     def __post_init__(self):
         if self.delta_s <= 0:
             raise ConfigError(f"delta_s must be positive, got {self.delta_s}")
-        if self.strategy not in (STRATEGY_THRESHOLD_ALL, STRATEGY_NEAREST):
+        if self.strategy not in (STRATEGY_THRESHOLD_ALL, STRATEGY_NEAREST, STRATEGY_RATIO):
             raise ConfigError(f"unknown match strategy {self.strategy!r}")
+        if not 0 < self.ratio <= 1:
+            raise ConfigError(f"ratio must be in (0, 1], got {self.ratio}")
 
 
 @dataclass(frozen=True)

@@ -369,6 +369,118 @@ def make_compositor():
     save("compositor.npz", meta=json.dumps(meta), **out)
 
 
+# --------------------------------------------------------------------------
+# per-pair outcomes of the reference chain at config size (C1, C3, C5):
+# keypoints exact, success flags equal, match-set
+# differences classified by the REFERENCE's own row / column distance gaps
+# --------------------------------------------------------------------------
+
+TAU_KEEP = 2.5e-7  # gaps below this are stored (covers the fp32 and fp64 chains' classification)
+
+
+def _ref_prepare(args):
+    px, wmin, wmax = args
+    from peakstitch import pipeline as R_pipe
+
+    cfg = R_pipe.PipelineConfig(window_min=wmin, window_max=wmax)
+    p = R_pipe.prepare_image(R_img.IntensityImage(px.astype(np.float64), "x"), cfg)
+    return kp_arrays(p.described.features), p.described.descriptors
+
+
+def _gaps(dist, axis):
+    """second-smallest minus smallest along ``axis`` (0 on exact ties)."""
+    part = np.partition(dist, 1, axis=axis)
+    lo = np.take(part, 0, axis=axis)
+    hi = np.take(part, 1, axis=axis) if dist.shape[axis] > 1 else np.full_like(lo, np.inf)
+    return hi - lo
+
+
+def _ref_pair(args):
+    """The reference's register_prepared on one pair (match_features + ransac_rigid),
+    plus the near-tie structure of ITS distance matrix (captured from the
+    reference's own _distance_matrix call, not recomputed)."""
+    desc_a, kp_a, desc_b, kp_b, iters, seed, delta_s = args
+    cap = {}
+    orig = R_match._distance_matrix
+
+    def capture(a, b):
+        cap["d"] = orig(a, b)
+        return cap["d"]
+
+    R_match._distance_matrix = capture
+    try:
+        fa = [R_det.FeaturePoint(int(r), int(c), 0, "max", 0, 0.0) for r, c in zip(kp_a["row"], kp_a["col"])]
+        fb = [R_det.FeaturePoint(int(r), int(c), 0, "max", 0, 0.0) for r, c in zip(kp_b["row"], kp_b["col"])]
+        pairs = R_match.match_features(R_desc.DescribedFeatures("a", fa, desc_a), R_desc.DescribedFeatures("b", fb, desc_b),
+                                       R_match.MatcherConfig(delta_s))
+    finally:
+        R_match._distance_matrix = orig
+    d = cap["d"]
+    rg, cg = _gaps(d, 1), _gaps(d, 0)
+    out = dict(ref1=np.array([p.ref1 for p in pairs], np.int32), ref2=np.array([p.ref2 for p in pairs], np.int32),
+               delta=np.array([p.delta for p in pairs], np.float64))
+    near_r = np.flatnonzero(rg < TAU_KEEP)
+    near_c = np.flatnonzero(cg < TAU_KEEP)
+    out.update(near_rows=near_r.astype(np.int32), near_rows_gap=rg[near_r],
+               near_cols=near_c.astype(np.int32), near_cols_gap=cg[near_c])
+    try:
+        res = R_reg.ransac_rigid(pairs, R_reg.RansacConfig(iterations=iters, inlier_tol=3.0, min_inliers=8, seed=seed))
+        out.update(ok=True, inliers=np.array(res.inliers, np.int32), consensus=res.consensus_size,
+                   model=np.array([res.transform.theta, res.transform.t_x, res.transform.t_y]), rms=res.residual_rms)
+    except RegistrationError:
+        out.update(ok=False, inliers=np.zeros(0, np.int32), consensus=0, model=np.zeros(3), rms=0.0)
+    return out
+
+
+def make_pairs(which=("c1", "c3", "c5")):
+    """C1 (1 pair), C3 (all 36 pairs of the nine crops, per-pair seeds
+    _pair_seed(0, a, b), mosaic.py:75-76) and C5 (pairs 0..7, RGB -> the
+    reference's to_grayscale).  Keypoints, matches, RANSAC outcome and the
+    near-tie rows / columns of every pair go to tests/golden/pairs_<cfg>.npz."""
+    import multiprocessing as mp
+    from peakstitch import mosaic as R_mosaic
+
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    procs = min(8, os.cpu_count() or 1)
+    for cfgname in which:
+        t0 = time.time()
+        if cfgname == "c1":
+            a, b = scenes.config1_pair(0)
+            grey, wmin, wmax, iters = [a, b], 16, 64, 1000
+            jobs = [(0, 1, 0)]
+        elif cfgname == "c3":
+            imgs, _ = scenes.config3_images(0)
+            grey, wmin, wmax, iters = imgs, 32, 128, 2000
+            jobs = [(x, y, R_mosaic._pair_seed(0, x, y)) for x in range(9) for y in range(x + 1, 9)]
+        else:
+            grey = []
+            for p in range(8):
+                i1, i2, _ = scenes.config5_pair(p)
+                grey += [R_img.to_grayscale(i1), R_img.to_grayscale(i2)]
+            wmin, wmax, iters = 16, 64, 2000
+            jobs = [(2 * p, 2 * p + 1, 0) for p in range(8)]
+        with mp.get_context("fork").Pool(procs) as pool:
+            prepared = pool.map(_ref_prepare, [(g, wmin, wmax) for g in grey])
+            outs = pool.map(_ref_pair, [(prepared[x][1], prepared[x][0], prepared[y][1], prepared[y][0], iters,
+                                         seed, 0.35) for x, y, seed in jobs], chunksize=1)
+        out = {}
+        for k, (kp, _) in enumerate(prepared):
+            for f in ("row", "col", "value"):
+                out[f"img{k}__{f}"] = kp[f]
+        meta = []
+        for q, ((x, y, seed), o) in enumerate(zip(jobs, outs)):
+            for f, v in o.items():
+                out[f"pair{q}__{f}"] = np.asarray(v)
+            meta.append(dict(a=x, b=y, seed=int(seed), ok=bool(o["ok"]), n_matches=int(len(o["ref1"])),
+                             consensus=int(o["consensus"])))
+        if cfgname == "c5":  # the RGB inputs are regenerated from scenes.config5_pair on the box
+            out["grey_digest"] = np.array([scenes.scene_digest(g.view(np.uint8)) for g in grey])
+        out["meta"] = np.array(json.dumps(dict(config=cfgname, window=[wmin, wmax], iterations=iters,
+                                               tau_keep=TAU_KEEP, pairs=meta)))
+        save(f"pairs_{cfgname}.npz", **out)
+        print(cfgname, "pairs", len(jobs), "ok", sum(m["ok"] for m in meta), "%.0fs" % (time.time() - t0))
+
+
 def make_scene_digests():
     d = {}
     for (h, w, seed) in [(64, 96, 0), (256, 256, 1), (512, 512, 7), (1600, 2688, 0), (2048, 2048, 0)]:
@@ -383,7 +495,9 @@ if __name__ == "__main__":
     for w in what:
         {"detector": make_detector, "descriptor": make_descriptor, "matcher": make_matcher,
          "ransac": make_ransac, "e2e": make_e2e, "compositor": make_compositor,
-         "digests": make_scene_digests}[w]()
+         "digests": make_scene_digests, "pairs": make_pairs,
+         "pairs_c1": lambda: make_pairs(("c1",)), "pairs_c3": lambda: make_pairs(("c3",)),
+         "pairs_c5": lambda: make_pairs(("c5",))}[w]()
     env = dict(numpy=np.__version__, python=sys.version.split()[0])
     with open(os.path.join(HERE, "ENV.json"), "w") as f:
         json.dump(env, f)

@@ -22,7 +22,7 @@ def declared_symbols():
 
 
 def test_library_loads_and_reports_version():
-    assert _lib.lib().ps_abi_version() == _lib.ABI_VERSION == 3
+    assert _lib.lib().ps_abi_version() == _lib.ABI_VERSION == 4
 
 
 def test_every_declared_symbol_is_exported():
@@ -116,3 +116,39 @@ def test_warp_and_blend_rejects_unknown_modes_before_any_launch():
     arr = (_lib.PlacementC * 1)()
     assert L.ps_warp_and_blend(arr, 0, 4, 4, 0, 0, 7, 0, None, None, None) == _lib.PS_ERR_VALUE
     assert L.ps_warp_and_blend(arr, 0, 4, 4, 0, 0, 0, 9, None, None, None) == _lib.PS_ERR_VALUE
+
+
+def test_match_plan_strategy_flags():
+    """Path flags are explicit per call (no environment switches); the extra
+    ratio strategy plans; contradictory or unknown flags are rejected."""
+    L, ws = _lib.lib(), C.c_size_t()
+    for strat in (_lib.PS_MATCH_NEAREST, _lib.PS_MATCH_THRESHOLD_ALL, _lib.PS_MATCH_RATIO,
+                  _lib.PS_MATCH_NEAREST | _lib.PS_MATCH_FORCE_EXACT, _lib.PS_MATCH_NEAREST | _lib.PS_MATCH_FORCE_TC):
+        assert L.ps_match_plan(1000, 900, 128, strat, 1000, C.byref(ws)) == 0, strat
+    assert L.ps_match_plan(10, 10, 128, _lib.PS_MATCH_FORCE_EXACT | _lib.PS_MATCH_FORCE_TC, 10, C.byref(ws)) == 1
+    assert L.ps_match_plan(10, 10, 128, 3, 10, C.byref(ws)) == 1
+    assert L.ps_match_plan(10, 10, 128, 0x400, 10, C.byref(ws)) == 1
+    # tensor-core workspace only when the TC path will run
+    exact, tc = C.c_size_t(), C.c_size_t()
+    L.ps_match_plan(64, 64, 128, _lib.PS_MATCH_NEAREST, 64, C.byref(exact))
+    L.ps_match_plan(64, 64, 128, _lib.PS_MATCH_NEAREST | _lib.PS_MATCH_FORCE_TC, 64, C.byref(tc))
+    assert tc.value > exact.value
+
+
+def test_library_reads_no_environment():
+    """The product library has no hidden getenv switches (ADVICE/VERDICT r1):
+    every getenv in csrc/ sits inside an ``#ifdef PS_DIAG`` block (diagnostic
+    builds only; the static CUDA runtime's own getenv is not ours)."""
+    csrc = os.path.join(REPO, "paper_2405_08578_b200", "csrc")
+    for name in sorted(os.listdir(csrc)):
+        if not name.endswith((".cu", ".cuh")):
+            continue
+        depth = []  # stack of "is this #if a PS_DIAG guard"
+        for ln, line in enumerate(open(os.path.join(csrc, name)), 1):
+            t = line.strip()
+            if t.startswith("#if"):
+                depth.append("PS_DIAG" in t)
+            elif t.startswith("#endif"):
+                depth.pop()
+            elif "getenv(" in t and not t.startswith("//"):
+                assert any(depth), f"{name}:{ln} reads the environment outside #ifdef PS_DIAG"

@@ -157,3 +157,27 @@ def test_oracle_compositor_rejects_unknown_modes():
         O.composite([np.zeros((4, 4))], [(0.0, 0.0, 0.0)], (4, 4, 0, 0), blend="average")
     with pytest.raises(ValueError):
         O.composite([np.zeros((4, 4))], [(0.0, 0.0, 0.0)], (4, 4, 0, 0), resample="cubic")
+
+
+def test_oracle_ratio_strategy_against_brute_force():
+    """The extra ratio_test strategy's oracle against a plain Python loop
+    (its own definition: first nearest neighbour kept when d1 < r * d2)."""
+    import math
+
+    rng = np.random.default_rng(12)
+    A = rng.random((30, 16))
+    B = rng.random((25, 16))
+    B[3] = B[4]
+    A[7] = B[3]  # exact duplicate best: d2 == d1, rejected
+    r1, r2, dl = O.match(A, B, 0.8, "ratio_test")
+    want = []
+    for i in range(len(A)):
+        d = [math.sqrt(sum((B[j, k] - A[i, k]) ** 2 for k in range(16))) for j in range(len(B))]
+        j = min(range(len(B)), key=lambda q: (d[q], q))
+        d2 = sorted(d)[1]
+        if d[j] < 0.8 * d2:
+            want.append((d[j], i, j))
+    want.sort()
+    assert [(i, j) for _, i, j in want] == list(zip(r1.tolist(), r2.tolist()))
+    assert np.allclose([x for x, _, _ in want], dl, rtol=1e-12)
+    assert 7 not in r1.tolist()

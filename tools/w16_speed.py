@@ -1,5 +1,5 @@
 """Describe throughput for w = 16 (scales 32..128) on 16 C2-size images:
-fast kernel vs the general kernel (PS_DESCRIBE_GENERIC)."""
+fast kernel vs the general kernel (policy="general")."""
 import os
 import sys
 
@@ -14,16 +14,14 @@ imgs = torch.from_numpy(np.stack([scenes.scene(1600, 2688, s) for s in range(16)
 cfg = DescriptorConfig(0.0625, 4, 128, True)
 kp = device.detect(imgs, (32, 64, 128), meta=False)
 n = int(kp.count.sum())
-for mode in ("fast", "generic"):
-    if mode == "generic":
-        os.environ["PS_DESCRIBE_GENERIC"] = "1"
+for mode in ("auto", "general"):
     for _ in range(2):
-        device.describe(imgs, kp, cfg, scale_set=kp.scale_set)
+        device.describe(imgs, kp, cfg, scale_set=kp.scale_set, policy=mode)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(5):
-        device.describe(imgs, kp, cfg, scale_set=kp.scale_set)
+        device.describe(imgs, kp, cfg, scale_set=kp.scale_set, policy=mode)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 5
