@@ -211,7 +211,7 @@ def bench_c4_matching(args, world=1, rank=0, dev=None, with_cpu=True, steps=5):
 # C3 nine-image stitch (BASELINE.json configs[2]): seconds at N GPUs
 # ---------------------------------------------------------------------------
 
-def bench_c3_stitch(args, world, rank, dev, steps=3):
+def bench_c3_stitch(args, world, rank, dev, steps=3, with_cpu=False):
     import torch
     import torch.distributed as dist
 
@@ -252,6 +252,21 @@ def bench_c3_stitch(args, world, rank, dev, steps=3):
     ctl_images, _ = scenes.config3_images(0, rot_deg=0.0, scale_range=(1.0, 1.0), noise=0.0)
     ctl = mosaic.build_pairwise_table(ctl_images, cfg)
     _, ctl_placed = mosaic.plan_mosaic(ctl, ids)
+    cpu = None
+    if with_cpu and rank == 0:
+        import multiprocessing as mp
+
+        P = os.cpu_count() or 1
+        host = [im.numpy() for im in images]
+        with mp.get_context("fork").Pool(P) as pool:
+            ch = oracle_pair_chain(pool, P, host[0], host[1], (32, 64, 128), 128, 2000, 0)
+        core_s = 9 * float(np.mean(ch["prepare_core_s"])) + 36 * (ch["match_core_s"] + ch["ransac_s"])
+        cpu = {"value": round(core_s / P, 3), "unit": "s", "cores": P, "kind": "port",
+               "sample": (f"oracle port chain of pair (0, 1) (2 images prepared, exact float64 MNN of "
+                          f"{ch['n_kp'][0]}x{ch['n_kp'][1]} split over {P} processes, RANSAC 2000 it.); the table "
+                          f"= 9 prepares + 36 pairs extrapolated from its core-seconds ({core_s:.1f}) / {P} cores, "
+                          f"perfect parallel scaling assumed"),
+               "pair_matches": ch["matches"], "pair_registered": ch["registered"]}
     return {"metric": "9-image stitch seconds (C3: detect/describe 9 x 2688x1600, 36 pairs match + RANSAC, plan)",
             "value": round(t_g, 4), "unit": "s", "higher_is_better": False,
             "batched_eager_value": round(t_b, 4), "per_pair_calls_value": round(t_pp, 4),
@@ -264,6 +279,10 @@ def bench_c3_stitch(args, world, rank, dev, steps=3):
             "rounds": len(plan.rounds), "unmatched": plan.final_unmatched,
             "control_translation_only_noise0": {"registered_pairs": len(ctl.entries) // 2, "placed": len(ctl_placed)},
             "timing": "host wall clock around the whole call, CUDA-synchronized, max over ranks",
+            "e2e": {"value": round(t_g, 4), "unit": "s", "h2d_bytes_per_step": int(sum(im.numel() for im in images)),
+                    "d2h_bytes_per_step": 36 * 8 * 8,
+                    "api": "mosaic.build_pairwise_table + plan_mosaic from pinned host images"},
+            "cpu_baseline": cpu,
             "parallelism": f"images then pairs sharded over {world} rank(s); NCCL all-gather of keypoint/descriptor "
                            "slots and of the pair results"}
 
@@ -390,7 +409,7 @@ def bench_ransac(args, rank, dev, with_cpu, n=1000, iters=2000, steps=5):
 # C5 illumination pairs (BASELINE.json configs[4]): pairs/s
 # ---------------------------------------------------------------------------
 
-def bench_c5_pairs(args, world, rank, dev, n_pairs=256, steps=2):
+def bench_c5_pairs(args, world, rank, dev, n_pairs=256, steps=2, with_cpu=False):
     """Full path per pair (detect, describe both images; match; RANSAC) on
     the RGB pixels: BT.601 grey through the device ingest path (integer luma
     key for detection, the run host's grey table for values and the
@@ -479,10 +498,28 @@ def bench_c5_pairs(args, world, rank, dev, n_pairs=256, steps=2):
                   h[2 * q + 1], cfg.seed) for q in range(len(grey))]
         return [(None, o[0]) for o in geng.register_many(items)]
 
+    # e2e: the RGB pairs from pinned host memory, uploaded inside the timed region
+    host_rgb = torch.cat([g.data for g in grey]).cpu().pin_memory() if grey else None
+    dev_rgb = torch.empty_like(host_rgb, device=dev) if grey else None
+    e2e_img = device.as_device_images(dev_rgb, rgb=True) if grey else None
+
+    def run_graph_e2e():
+        if e2e_img is None:
+            return []
+        dev_rgb.copy_(host_rgb, non_blocking=True)
+        rows, cols, desc, cnt = geng.prepare_device(e2e_img)
+        h = cnt.cpu().tolist()
+        R, Cc, Dd = rows.unbind(0), cols.unbind(0), desc.unbind(0)
+        items = [(R[2 * q], Cc[2 * q], Dd[2 * q], h[2 * q], R[2 * q + 1], Cc[2 * q + 1], Dd[2 * q + 1],
+                  h[2 * q + 1], cfg.seed) for q in range(len(grey))]
+        return [(None, o[0]) for o in geng.register_many(items)]
+
     n_sub = min(len(grey), 16)  # the one-pair-at-a-time variant on a bounded subset
     dt1, stats1 = timed(lambda: [run_pair(g) for g in grey[:n_sub]])
     dtb, stats = timed(run_batched)
     dt, statsg = timed(run_graph)
+    dte, statse = timed(run_graph_e2e)
+    assert [s[1] for s in statse] == [s[1] for s in statsg]
     assert [s[0] for s in stats[:n_sub]] == [s[0] for s in stats1]
     assert [s[1] for s in stats[:n_sub]] == [s[1] for s in stats1] and [s[1] for s in statsg] == [s[1] for s in stats]
     return {"metric": "pairs/s (C5: 1920x1080 RGB pairs, BT.601 grey, homography warp + gain/offset/noise, "
@@ -497,7 +534,278 @@ def bench_c5_pairs(args, world, rank, dev, n_pairs=256, steps=2):
                         "(device-side counts) replayed as one graph over 8 streams, one result read; "
                         "batched_eager_value: the same batches launched eagerly with one count and one result "
                         "read-back; per_pair_calls_value: one synchronous pair at a time (first 16 pairs of each rank)",
-            "ingest": "RGB8 pixel type: luma-key detection, host-built 2^24 grey table (ingest.py)"}
+            "ingest": "RGB8 pixel type: luma-key detection, host-built 2^24 grey table (ingest.py)",
+            "e2e": {"value": round(n_pairs / dte, 3), "unit": "pairs/s",
+                    "h2d_bytes_per_step": int(host_rgb.numel()) * world if grey else 0,
+                    "d2h_bytes_per_step": n_pairs * 8 * 8,
+                    "api": "pinned host RGB pairs uploaded each step, then the GraphEngine chain (prepare_device "
+                           "+ register_many), success flags read back"},
+            "cpu_baseline": _c5_cpu(world, rank) if with_cpu else None}
+
+
+def _c5_cpu(world, rank):
+    """Oracle-port chain of C5 pair 0 on this host's cores, extrapolated to pairs/s."""
+    if rank != 0 or world != 1:
+        return None
+    import multiprocessing as mp
+
+    from paper_2405_08578_b200 import scenes
+
+    a, b, _ = scenes.config5_pair(0)
+    P = os.cpu_count() or 1
+    with mp.get_context("fork").Pool(P) as pool:
+        ch = oracle_pair_chain(pool, P, a, b, (16, 32, 64), 64, 2000, 0)
+    core_s = sum(ch["prepare_core_s"]) + ch["match_core_s"] + ch["ransac_s"]
+    return {"value": round(P / core_s, 4), "unit": "pairs/s", "cores": P, "kind": "port",
+            "sample": (f"oracle port chain of C5 pair 0 (BT.601 grey, 2 images prepared, exact float64 MNN of "
+                       f"{ch['n_kp'][0]}x{ch['n_kp'][1]} split over {P} processes, RANSAC 2000 it.): "
+                       f"{core_s:.1f} core-seconds per pair -> pairs/s = {P} cores / that, perfect scaling assumed"),
+            "pair_matches": ch["matches"], "pair_registered": ch["registered"]}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle chain for one pair (C1 latency, C3 / C5 baselines): prepare each
+# image on one core, the exact float64 MNN match split by row blocks over P
+# processes (column minima merged with the first-occurrence rule), RANSAC
+# on one core.  Timed per part so per-config totals can be stated.
+# ---------------------------------------------------------------------------
+
+def _oracle_prepare_job(args):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle import lpsift_oracle as O
+
+    img, scales, l_max = args
+    t0 = time.perf_counter()
+    grey = img.astype(np.float64) if img.ndim == 2 else img.astype(np.float64) @ np.array([0.299, 0.587, 0.114])
+    P = O.ramp(grey, O.default_alpha(*grey.shape))
+    kp = O.detect(P, scales)
+    desc = O.describe(P, kp, 0.0625, 4, l_max, True)
+    return kp, desc, time.perf_counter() - t0
+
+
+def _oracle_rows_job(args):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    from oracle import lpsift_oracle as O
+
+    A, B, i0 = args
+    t0 = time.perf_counter()
+    n2 = B.shape[0]
+    nn = np.empty(A.shape[0], np.int64)
+    best = np.empty(A.shape[0])
+    cbest, carg = np.full(n2, np.inf), np.zeros(n2, np.int64)
+    for j0, D in O.distances(A, B):
+        j = np.argmin(D, axis=1)
+        nn[j0:j0 + len(j)] = j
+        best[j0:j0 + len(j)] = D[np.arange(len(j)), j]
+        ci = np.argmin(D, axis=0)
+        cv = D[ci, np.arange(n2)]
+        upd = cv < cbest
+        cbest[upd], carg[upd] = cv[upd], ci[upd] + j0 + i0
+    return i0, nn, best, cbest, carg, time.perf_counter() - t0
+
+
+def oracle_pair_chain(pool, P, img_a, img_b, scales, l_max, iters, seed):
+    """The oracle port's chain for one pair -> timings and outcome."""
+    from oracle import lpsift_oracle as O
+
+    t0 = time.perf_counter()
+    (ka, da, ta), (kb, db, tb) = pool.map(_oracle_prepare_job, [(img_a, scales, l_max), (img_b, scales, l_max)])
+    t1 = time.perf_counter()
+    da32, db32 = da.astype(np.float32).astype(np.float64), db.astype(np.float32).astype(np.float64)
+    n1 = len(da32)
+    cuts = [(n1 * k) // P for k in range(P + 1)]
+    parts = pool.map(_oracle_rows_job, [(da32[cuts[k]:cuts[k + 1]], db32, cuts[k]) for k in range(P)
+                                        if cuts[k + 1] > cuts[k]])
+    nn12, best12 = np.concatenate([p[1] for p in parts]), np.concatenate([p[2] for p in parts])
+    cbest, carg = parts[0][3].copy(), parts[0][4].copy()
+    for p in parts[1:]:  # blocks in row order: strict < keeps the earliest row on ties
+        upd = p[3] < cbest
+        cbest[upd], carg[upd] = p[3][upd], p[4][upd]
+    rows = np.arange(n1)
+    ok = (carg[nn12] == rows) & (best12 < 0.35)
+    r1, r2, dl = rows[ok], nn12[ok], best12[ok]
+    order = np.lexsort((r2, r1, dl))
+    r1, r2 = r1[order], r2[order]
+    t2 = time.perf_counter()
+    reg = None
+    if len(r1) >= 8:
+        reg = O.ransac(*O.pair_points(r1, r2, ka, kb), iters, 3.0, 8, seed)
+    t3 = time.perf_counter()
+    return {"prepare_core_s": [ta, tb], "match_core_s": float(sum(p[5] for p in parts)), "ransac_s": t3 - t2,
+            "wall_s": t3 - t0, "prepare_wall_s": t1 - t0, "match_wall_s": t2 - t1, "matches": int(len(r1)),
+            "registered": bool(reg is not None and reg["ok"]), "n_kp": [len(ka), len(kb)]}
+
+
+# ---------------------------------------------------------------------------
+# C1 latency (BASELINE.json configs[0]): one pair through the whole chain
+# ---------------------------------------------------------------------------
+
+def bench_c1_latency(args, rank, dev, with_cpu, steps=10):
+    """Device latency (crops resident, detect+describe both, MNN match,
+    RANSAC 1000 it., result read) and e2e latency (host numpy crops in,
+    RegistrationResult out, through pipeline.prepare_image /
+    register_prepared -- the reference's own call sequence, pipeline.py:171-209);
+    the ratio-0.8 strategy (extra) timed on the same descriptors."""
+    import torch
+
+    from paper_2405_08578_b200 import device, matcher, pipeline as PL, scenes
+    from paper_2405_08578_b200.records import IntensityImage, MatcherConfig
+
+    if rank != 0:
+        return None
+    a, b = scenes.config1_pair(0)
+    cfg = PL.PipelineConfig(window_min=16, window_max=64, ransac_iters=1000, ransac_tol=3.0, seed=0)
+    sizes, dcfg = cfg.scale_set().sizes, cfg.descriptor_config()
+    ta, tb = torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev)
+    pair = device.DeviceImages(torch.stack([ta, tb]), "u8", device.default_alpha(*a.shape))
+
+    def dev_once():
+        kp = device.detect(pair, sizes, meta=False)
+        d = device.describe(pair, kp, dcfg, scale_set=kp.scale_set)
+        r1, r2, _ = device.match(d[0], d[1], cfg.delta_s)
+        src, dst = device.pair_points(r1, r2, kp.row[0], kp.col[0], kp.row[1], kp.col[1])
+        return device.ransac(src, dst, cfg.ransac_iters, cfg.ransac_tol, cfg.min_inliers, cfg.seed), d
+
+    def e2e_once():
+        pa = PL.prepare_image(IntensityImage(a, "a"), cfg)
+        pb = PL.prepare_image(IntensityImage(b, "b"), cfg)
+        return PL.register_prepared(pa, pb, cfg, seed=0)
+
+    def timed(fn):
+        for _ in range(3):
+            out = fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out = fn()
+            torch.cuda.synchronize()
+            ts.append((time.perf_counter() - t0) * 1e3)
+        return statistics.median(ts), out
+
+    ms_dev, (reg, d) = timed(dev_once)
+    ms_e2e, (pairs, res, _, _) = timed(e2e_once)
+    ms_ratio, rr = timed(lambda: device.match(d[0], d[1], 0.8, "ratio_test"))
+    out = {"metric": "C1 pair latency (768x1024 crops, L 16..64, detect+describe both, MNN match, RANSAC 1000)",
+           "value": round(ms_dev, 3), "unit": "ms", "higher_is_better": False,
+           "matches": int(len(pairs)), "inliers": int(len(reg.inliers)), "registered": bool(reg.ok),
+           "t_x": round(float(reg.t_x), 6), "t_y": round(float(reg.t_y), 6),
+           "e2e": {"value": round(ms_e2e, 3), "unit": "ms", "api": "pipeline.prepare_image x2 + register_prepared "
+                   "(host numpy crops in, host MatchPair list + RegistrationResult out)",
+                   "h2d_bytes_per_step": int(a.nbytes + b.nbytes),
+                   "d2h_bytes_per_step": int(len(pairs) * (4 * 4 + 8 + 8))},
+           "ratio_test_0_8": {"value": round(ms_ratio, 3), "unit": "ms", "matches": int(rr[0].shape[0]),
+                              "path": "float64 CUDA-core top-2 (nn_pass<top2> + ratio_select), bit-exact vs its "
+                                      "numpy oracle (tests/test_gpu_ratio.py)",
+                              "pair_matches_per_s": round(6144 * 6144 / (ms_ratio / 1e3), 1)},
+           "timing": "host wall clock per call, CUDA-synchronized, median of %d" % steps}
+    if with_cpu:
+        import multiprocessing as mp
+
+        P = os.cpu_count() or 1
+        with mp.get_context("fork").Pool(P) as pool:
+            ch = oracle_pair_chain(pool, P, a, b, (16, 32, 64), 64, 1000, 0)
+        out["cpu_baseline"] = {"value": round(ch["wall_s"] * 1e3, 1), "unit": "ms", "cores": P, "kind": "port",
+                               "sample": "the whole C1 pair through the oracle port (numpy restatement of the "
+                                         "reference): both images prepared in parallel (1 core each), the exact "
+                                         f"float64 match split by row blocks over {P} processes, RANSAC on one "
+                                         "core; wall clock, not extrapolated",
+                               "matches": ch["matches"], "registered": ch["registered"],
+                               "parts_s": {"prepare": round(ch["prepare_wall_s"], 3),
+                                           "match": round(ch["match_wall_s"], 3), "ransac": round(ch["ransac_s"], 3)}}
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Dense tensor-core matching at C4 scale (SURVEY §8(d) K3 >= 50 % of peak)
+# ---------------------------------------------------------------------------
+
+def bench_c4_dense(args, rank, dev, steps=5):
+    """103,968^2 distinct unit descriptors (half of B near-copies of A rows,
+    so pass 2 runs too): the MNN match on the tensor cores, algorithmic
+    2*n1*n2*128 FLOPs / time vs the measured bf16 dense peak."""
+    import torch
+
+    from paper_2405_08578_b200 import device
+
+    if rank != 0:
+        return None
+    n = 103_968
+    g = torch.Generator(device=dev).manual_seed(4)
+    A = torch.randn((n, 128), generator=g, device=dev)
+    A = A / A.norm(dim=1, keepdim=True)
+    B = torch.randn((n, 128), generator=g, device=dev)
+    B = B / B.norm(dim=1, keepdim=True)
+    half = n // 2
+    B[:half] = A[torch.randperm(n, generator=g, device=dev)[:half]] + 0.01 * torch.randn((half, 128), generator=g,
+                                                                                        device=dev)
+    B = B / B.norm(dim=1, keepdim=True)
+    A, B = A.float().contiguous(), B.float().contiguous()
+    for _ in range(2):
+        r = device.match(A, B, 0.35, path="tensor")
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        r = device.match(A, B, 0.35, path="tensor")
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    stats = device.match_stats()
+    ex = device.match(A, B, 0.35, path="exact")  # P3 on this data: the exact float64 path, untimed
+    same = bool(torch.equal(r[0], ex[0]) and torch.equal(r[1], ex[1]) and torch.equal(r[2], ex[2]))
+    flops = 2.0 * n * n * 128
+    peak = _bf16_peak()
+    return {"metric": "dense MNN pair-matches/s (103,968^2 distinct unit 128-d fp32 descriptors, tcgen05)",
+            "value": round(n * n / (ms / 1e3), 1), "unit": "pair-matches/s", "ms_per_pair": round(ms, 3),
+            "matches": int(r[0].shape[0]), "exact_equal": same,
+            "roofline": {"bound": "tensor", "achieved": round(flops / (ms / 1e3) / 1e12, 1), "peak": peak,
+                         "unit": "TFLOP/s", "frac": round(flops / (ms / 1e3) / 1e12 / peak, 4),
+                         "algorithmic_flops": flops,
+                         "executed_mma_flops": stats.get("mma_flops", 0),
+                         "note": "algorithmic 2*n1*n2*128 over the whole call (both passes, the exact float64 "
+                                 "certification and the ordering included); executed counts the fp16 MMA tiles "
+                                 "issued (K = 144 incl. the |y|^2 augmentation)"},
+            "timing": "CUDA events over %d back-to-back calls (each has one host count read)" % steps}
+
+
+def _bf16_peak():
+    pj = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(pj):
+        with open(pj) as f:
+            return float(json.load(f)["bf16_tflops"])
+    return 2250.0
+
+
+def fp64_probe(dev):
+    """FP64-pipe peak of this GPU (ps_probe_fp64_fma, CUDA events)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2405_08578_b200 import _lib
+
+    L = _lib.lib()
+    sink = torch.zeros(148 * 8, dtype=torch.float64, device=dev)
+    fl = C.c_double()
+    st = torch.cuda.current_stream()
+    for _ in range(2):
+        _lib.check(L.ps_probe_fp64_fma(20000, 148 * 8, C.c_void_p(sink.data_ptr()), C.byref(fl),
+                                       C.c_void_p(st.cuda_stream)), "probe")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(5):
+        _lib.check(L.ps_probe_fp64_fma(20000, 148 * 8, C.c_void_p(sink.data_ptr()), C.byref(fl),
+                                       C.c_void_p(st.cuda_stream)), "probe")
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    return {"tflops": round(fl.value / (ms / 1e3) / 1e12, 2), "ms": round(ms, 3),
+            "how": "ps_probe_fp64_fma: 148x8 blocks x 256 threads x 8 independent DFMA chains x 20000 steps, "
+                   "CUDA events, 2 FLOPs per DFMA"}
+
 
 
 # ---------------------------------------------------------------------------
@@ -573,9 +881,10 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    mine = [k for k in range(args.images) if k % world == rank]
+    # weak scaling: every rank runs the full C2 batch of its own seeded images
+    # (seeds rank*64 .. rank*64+63; rank 0's batch is BASELINE configs[1]'s)
+    mine = [rank * args.images + k for k in range(args.images)]
     n = len(mine)
-    # seeds follow the global image index so any N covers the same 64 images
     host = np.empty((n, NR, NC), dtype=np.uint8)
     import multiprocessing as mp
 
@@ -645,7 +954,7 @@ def run_ours(args):
     bad = int(((nrm - 1.0).abs() > 1e-5).sum())
     if bad:
         raise RuntimeError(f"describe produced {bad} non-unit descriptor rows")
-    total_px = args.images * NR * NC
+    total_px = world * args.images * NR * NC  # all ranks' images
     value = total_px / 1e6 / (ms_step / 1e3)
 
     # ---- roofline (per launch on this rank's shard) ----
@@ -720,16 +1029,33 @@ def run_ours(args):
             e_ms = t.item()
         d2h = n * (K * (4 + 4 + 8 + 128 * 4) + 4)
         e2e = {"value": round(total_px / 1e6 / (e_ms / 1e3), 2), "unit": "Mpixel/s", "ms_per_step": round(e_ms, 3),
+               "steps": e_steps,
                "h2d_bytes_per_step": n * NR * NC * world, "d2h_bytes_per_step": d2h * world,
                "api": "paper_2405_08578_b200.pipeline.BatchPreparer.run (pinned host in/out, 3-stream pipeline)"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    with_cpu = rank == 0 and world == 1 and not args.no_cpu
+    if with_cpu:
         cpu = cpu_baseline(steps=1, warmup=0)
+    fp64 = fp64_probe(dev)
+    roof["fp64_pipe"] = {"peak_tflops_measured": fp64["tflops"], "probe": fp64["how"]}
+    tj = os.path.join(REPO, "profiles", "describe_fp64.json")
+    if os.path.exists(tj):  # FP64 FLOPs per launch from an ncu capture of the same launch (committed)
+        with open(tj) as f:
+            fj = json.load(f)
+        if int(fj.get("images", -1)) == n:
+            ach = fj["fp64_flops_per_launch"] / (des_ms / 1e3) / 1e12
+            roof["fp64_pipe"].update({"achieved_tflops": round(ach, 2), "frac": round(ach / fp64["tflops"], 4),
+                                      "fp64_flops_per_launch": fj["fp64_flops_per_launch"],
+                                      "source": fj.get("source")})
+
+    latency = None
+    if not args.no_stitch:
+        latency = bench_c1_latency(args, rank, dev, with_cpu=with_cpu)
 
     stitch = None
     if not args.no_stitch:
-        stitch = bench_c3_stitch(args, world, rank, dev)
+        stitch = bench_c3_stitch(args, world, rank, dev, with_cpu=with_cpu)
 
     composite = None
     if not args.no_composite:
@@ -741,24 +1067,29 @@ def run_ours(args):
 
     pairs5 = None
     if not args.no_pairs:
-        pairs5 = bench_c5_pairs(args, world, rank, dev)
+        pairs5 = bench_c5_pairs(args, world, rank, dev, with_cpu=with_cpu)
 
     matching = None
     if not args.no_match:
         del desc, imgs, dimg
         torch.cuda.empty_cache()
         matching = bench_c4_matching(args, world, rank, dev, with_cpu=(not args.no_cpu and world == 1))
+        torch.cuda.empty_cache()
+        matching_dense = bench_c4_dense(args, rank, dev)
+    else:
+        matching_dense = None
 
     if rank == 0:
         out = {
             "metric": "Mpixel/s LP-SIFT detect+describe", "value": round(value, 2), "unit": "Mpixel/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8/f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/f64",
             "data": "synthetic (seeded noise+shapes generator, paper_2405_08578_b200/scenes.py)",
             "config": {"workload": WORKLOAD, "images": args.images, "image_hw": [NR, NC], "scales": list(SCALES),
                        "keypoints_per_image": K, "descriptor": "float32 128-d", "l2": "inputs larger than L2",
-                       "parallelism": f"images sharded over {world} rank(s)"},
-            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "matching_c4": matching,
+                       "parallelism": f"{world} rank(s) x one 64-image C2 batch each (weak scaling, no collective)"},
+            "roofline": roof, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "latency_c1": latency,
+            "matching_c4": matching, "matching_c4_dense": matching_dense,
             "stitch_c3": stitch, "composite_c3": composite, "pairs_c5": pairs5, "ransac_k4": ransac_k4,
             "gpu_launches": int(launches), "clocks": clocks,
         }
@@ -776,7 +1107,7 @@ def run_reference(args):
     cb = cpu_baseline(steps=max(args.steps, 1), warmup=max(args.warmup, 0) and 1)
     out = {"metric": "Mpixel/s LP-SIFT detect+describe", "value": round(cb["value"], 4), "unit": "Mpixel/s",
            "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded noise+shapes generator)",
            "config": {"workload": WORKLOAD, "images": args.images, "image_hw": [NR, NC], "scales": list(SCALES)},
            "cpu_baseline": cb,
@@ -785,8 +1116,26 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def _spawn_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch this script as N
+    NCCL ranks on this node (torch.distributed.run, 127.0.0.1)."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:
+        sys.exit(_spawn_ranks(args))
+    if world and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.impl == "reference":
         run_reference(args)
     else:

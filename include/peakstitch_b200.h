@@ -130,6 +130,12 @@ PS_API int ps_abi_version(void);
 PS_API const char* ps_last_error(void);      /* thread-local message of the last failure */
 PS_API uint64_t ps_kernel_launches(void);    /* kernels launched by this library so far   */
 PS_API int ps_device_sync(void* stream);     /* cudaStreamSynchronize + error check       */
+/* Roofline probe (bench.py): `blocks` x 256 threads each run 8 independent
+ * float64 FMA chains of `iters` steps; *out_flops = the FLOPs enqueued (2 per
+ * FMA).  Time it with events on `stream` to get the box's FP64-pipe peak --
+ * the denominator of the describe kernel's compute roofline.
+ * sink: device double[blocks] (never written in practice). */
+PS_API int ps_probe_fp64_fma(int64_t iters, int32_t blocks, double* sink, double* out_flops, void* stream);
 
 /* ---- detect: detector.py:154-172 --------------------------------------- */
 /* Validates the scale set (ScaleSet rules, detector.py:33-68) against the

@@ -51,6 +51,7 @@ SIGNATURES = {
     "ps_last_error": (C.c_char_p, []),
     "ps_kernel_launches": (C.c_uint64, []),
     "ps_device_sync": (C.c_int, [C.c_void_p]),
+    "ps_probe_fp64_fma": (C.c_int, [C.c_int64, C.c_int32, C.c_void_p, C.POINTER(C.c_double), C.c_void_p]),
     "ps_detect_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.c_int32,
                                  C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_size_t)]),
     "ps_detect": (C.c_int, [C.POINTER(ImageBatch), C.POINTER(C.c_int32), C.c_int32, C.c_int32,

@@ -148,7 +148,9 @@ def test_p5_match_sets_and_ransac_outcomes(chain, precision):
             if ok:
                 assert np.array_equal(out.inliers, g[f"pair{q}__inliers"]), (name, q)
                 assert out.consensus == int(g[f"pair{q}__consensus"]), (name, q)
-            assert np.array_equal(dlh, g[f"pair{q}__delta"]) or precision == "f32", (name, q)
+            # descriptors differ from the reference's by ~1e-14 (P2), so distances
+            # agree to well inside tau, not bit for bit (P3 pins the bits on identical inputs)
+            assert np.max(np.abs(dlh - g[f"pair{q}__delta"]), initial=0.0) < tau, (name, q)
         if ok:
             assert corner_error((out.theta, out.t_x, out.t_y), g[f"pair{q}__model"], nr, nc) <= 1e-3, (name, q)
         report.append((q, cls["n_diff"], cls["others"]))
