@@ -63,7 +63,7 @@ enum ps_status {
 
 enum ps_pixel_type {
   PS_PIXELS_U8 = 0,  /* raw 8-bit intensities; the linear ramp of
-                        apply_linear_ramp (imaging.py:130-149) is fused:
+                        apply_linear_ramp (imaging.py:113-132) is fused:
                         P[r,c] = fl(I[r,c] + fl((r*nc+c+1) * alpha))        */
   PS_PIXELS_F64 = 1, /* an already-ramped float64 raster (RampedImage.pixels) */
   PS_PIXELS_F64_RAW = 2, /* float64 intensities (IntensityImage.pixels); ramp

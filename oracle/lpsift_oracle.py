@@ -27,7 +27,7 @@ import numpy as np
 
 TWO_PI = 2.0 * math.pi  # descriptor.py:31
 MIN_WINDOW = 8  # detector.py:20
-RAMP_SPAN_LIMIT = 0.05 * 255.0  # imaging.py:41
+RAMP_SPAN_LIMIT = 0.05 * 255.0  # imaging.py:24
 
 POL_MAX = 0  # "max" sorts before "min" (detector.py:171, string order)
 POL_MIN = 1
@@ -43,16 +43,16 @@ class OracleConfigError(ValueError):
 
 
 # ---------------------------------------------------------------------------
-# imaging.py:125-149 -- ramp
+# imaging.py:108-132 -- ramp
 # ---------------------------------------------------------------------------
 
 def default_alpha(nr: int, nc: int) -> float:
-    """imaging.py:125-127."""
+    """imaging.py:108-111."""
     return 1e-6 * 255.0 / (nr * nc)
 
 
 def ramp(pixels: np.ndarray, alpha: float) -> np.ndarray:
-    """P = I + fl(k * alpha), k = r*nc + c + 1 (imaging.py:130-149)."""
+    """P = I + fl(k * alpha), k = r*nc + c + 1 (imaging.py:113-132)."""
     if not math.isfinite(alpha) or alpha <= 0:
         raise OracleConfigError("alpha must be positive")
     nr, nc = pixels.shape
@@ -63,11 +63,11 @@ def ramp(pixels: np.ndarray, alpha: float) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------
-# detector.py:183-321 -- scales, windows, extrema, dedupe, order
+# detector.py:20-172 -- scales, windows, extrema, dedupe, order
 # ---------------------------------------------------------------------------
 
 def scales_from_range(l_min: int, l_max: int) -> tuple[int, ...]:
-    """ScaleSet.from_range (detector.py:200-211)."""
+    """ScaleSet.from_range (detector.py:50-61)."""
     if l_min > l_max:
         raise OracleConfigError("empty range")
     out, s = [], int(l_min)
@@ -79,7 +79,7 @@ def scales_from_range(l_min: int, l_max: int) -> tuple[int, ...]:
 
 
 def check_scales(sizes, nr: int, nc: int) -> None:
-    """ScaleSet.__post_init__ / validate_for (detector.py:188-217)."""
+    """ScaleSet.__post_init__ / validate_for (detector.py:33-68)."""
     if not sizes:
         raise OracleConfigError("empty scale set")
     if any(int(s) != s or s < MIN_WINDOW for s in sizes):
@@ -93,9 +93,9 @@ def check_scales(sizes, nr: int, nc: int) -> None:
 def window_extrema(P: np.ndarray, L: int) -> tuple[np.ndarray, np.ndarray]:
     """Flat image indices of every L-window's first argmax / first argmin.
 
-    Windows are row-major, trailing ones shrunk (detector.py:236-252);
+    Windows are row-major, trailing ones shrunk (detector.py:87-103);
     per window ``np.argmax``/``np.argmin`` on the row-major flattened window
-    (detector.py:263-268).  Padding the shrunk windows with -inf/+inf keeps
+    (detector.py:114-119).  Padding the shrunk windows with -inf/+inf keeps
     the row-major first-occurrence rule.
     """
     nr, nc = P.shape
@@ -115,10 +115,10 @@ def window_extrema(P: np.ndarray, L: int) -> tuple[np.ndarray, np.ndarray]:
 
 
 def detect(P: np.ndarray, sizes, dedupe: bool = True) -> np.ndarray:
-    """detect_features (detector.py:303-321) -> structured KP_DTYPE array.
+    """detect_features (detector.py:154-172) -> structured KP_DTYPE array.
 
     Raw order is (scale ascending, window, max-then-min); dedupe keeps the
-    first occurrence of each (row, col, polarity) (detector.py:288-300), which
+    first occurrence of each (row, col, polarity) (detector.py:139-151), which
     is the smallest scale; the final sort key (scale, window, polarity) is the
     raw order itself.
     """

@@ -314,7 +314,7 @@ __global__ void fill_counts(int32_t* counts, int B, int32_t v) {
 // ---- host planning -----------------------------------------------------------
 
 int validate_scales(int nr, int nc, const int32_t* s, int n) {
-  // ScaleSet.__post_init__ / validate_for (detector.py:188-217)
+  // ScaleSet.__post_init__ / validate_for (detector.py:33-68)
   PS_REQUIRE(n >= 1, PS_ERR_CONFIG, "scale set must contain at least one size");
   PS_REQUIRE(n <= kMaxScales, PS_ERR_ARGUMENT, "at most %d scales supported", kMaxScales);
   for (int i = 0; i < n; ++i) PS_REQUIRE(s[i] >= 8, PS_ERR_CONFIG, "window sizes must be integers >= 8");
@@ -502,19 +502,19 @@ extern "C" int ps_detect(const ps_image_batch* img, const int32_t* host_scales, 
   cudaStream_t s = (cudaStream_t)stream;
   if (img->pixel_type == PS_PIXELS_U8) {
     PS_REQUIRE(img->alpha > 0 && img->alpha * img->nr * img->nc <= 0.05 * 255.0, PS_ERR_CONFIG,
-               "alpha=%g outside the ramp limits (imaging.py:138-145)", img->alpha);
+               "alpha=%g outside the ramp limits (imaging.py:121-128)", img->alpha);
     RampU8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
     return run_detect(img, im, true, host_scales, n_scales, dedupe, out, workspace, workspace_bytes, s);
   }
   if (img->pixel_type == PS_PIXELS_F64_RAW) {
     PS_REQUIRE(img->alpha > 0 && img->alpha * img->nr * img->nc <= 0.05 * 255.0, PS_ERR_CONFIG,
-               "alpha=%g outside the ramp limits (imaging.py:138-145)", img->alpha);
+               "alpha=%g outside the ramp limits (imaging.py:121-128)", img->alpha);
     RampF64Raw im{(const double*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
     return run_detect(img, im, false, host_scales, n_scales, dedupe, out, workspace, workspace_bytes, s);
   }
   if (img->pixel_type == PS_PIXELS_RGB8) {
     PS_REQUIRE(img->alpha > 0 && img->alpha * img->nr * img->nc <= 0.05 * 255.0, PS_ERR_CONFIG,
-               "alpha=%g outside the ramp limits (imaging.py:138-145)", img->alpha);
+               "alpha=%g outside the ramp limits (imaging.py:121-128)", img->alpha);
     PS_REQUIRE((int64_t)img->nr * img->row_pitch * 3 < (int64_t)INT32_MAX, PS_ERR_ARGUMENT,
                "image too large (3*nr*pitch >= 2^31)");
     RampRGB8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha, img->gray_lut};

@@ -61,7 +61,7 @@ struct Arena {
 
 // ---------------------------------------------------------------------------
 // ramped-pixel access.  P[r,c] exactly as apply_linear_ramp computes it
-// (reference imaging.py:146-149): fl(I + fl(k * alpha)), k = r*nc + c + 1.
+// (reference imaging.py:129-132): fl(I + fl(k * alpha)), k = r*nc + c + 1.
 // Explicit _rn intrinsics keep nvcc from contracting into an FMA.
 // ---------------------------------------------------------------------------
 // exact int -> double for 0 <= x < 2^32 on the FP64 pipe (no I2F):

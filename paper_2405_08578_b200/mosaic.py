@@ -32,7 +32,7 @@ from .pipeline import pair_seed
 from .records import RigidTransform
 
 
-# ---- table (mosaic.py:28-53) -------------------------------------------------------
+# ---- table (mosaic.py:29-55) -------------------------------------------------------
 
 @dataclass(frozen=True)
 class PairEntry:
@@ -339,25 +339,59 @@ def _all_gather(t: torch.Tensor, world: int, group, cache: dict | None = None, t
     return out.view((world,) + tuple(t.shape))
 
 
+def _prepare_groups(engine, imgs):
+    """engine.prepare over images of possibly different sizes: one call per
+    size (each a batched launch), slots padded to the group's largest
+    capacity and returned in the input order."""
+    keys = [tuple(im.shape) for im in imgs]
+    if len(set(keys)) == 1:
+        return engine.prepare(imgs)
+    outs, where = [], []
+    for key in dict.fromkeys(keys):
+        idx = [i for i, k in enumerate(keys) if k == key]
+        outs.append(engine.prepare([imgs[i] for i in idx]))
+        where.append(idx)
+    cap = max(o[2].shape[1] for o in outs)
+    order = np.argsort(np.concatenate(where), kind="stable")
+    perm = torch.as_tensor(order, device=outs[0][0].device)
+    return tuple(torch.cat([_pad_cap(o[f], cap) if f < 3 else o[f] for o in outs])[perm] for f in range(4))
+
+
+def _pad_cap(t: torch.Tensor, cap: int) -> torch.Tensor:
+    """Zero-pad the keypoint axis (dim 1) of a slot tensor to ``cap``."""
+    if t.shape[1] >= cap:
+        return t
+    extra = torch.zeros((t.shape[0], cap - t.shape[1]) + tuple(t.shape[2:]), dtype=t.dtype, device=t.device)
+    return torch.cat([t, extra], dim=1)
+
+
+def _plan_cap(engine, shape) -> int:
+    """Keypoint slots per image of this size (the detect plan's count-law bound)."""
+    from .pipeline import alloc_plan_cap
+
+    return int(getattr(engine, "plan_cap", lambda nr, nc: alloc_plan_cap(nr, nc, engine.cfg))(shape[0], shape[1]))
+
+
 def build_pairwise_table(images: Sequence, cfg, *, engine=None, group=None) -> PairwiseTransformTable:
     """mosaic.py:79-112 over the ranks of ``group`` (see module docstring)."""
     n = len(images)
     if n < 2:
         raise ConfigError("pairwise table needs at least 2 images")
-    shapes = {tuple(np.asarray(im).shape) for im in images}
-    if len(shapes) != 1:
-        raise ConfigError("all images of a pairwise table must have the same size")
     engine = engine or GpuEngine(cfg)
     rank, world = _group_info(group)
     dev = engine.comm_device()
+    mixed = len({tuple(im.shape) for im in images}) > 1  # images of different sizes (reference allows them)
 
     # phase 1: my images (k % world == rank); slots padded to `per` images per rank
     mine = list(range(rank, n, world))
     per = -(-n // world)
-    rows, cols, desc, cnt = engine.prepare([images[k] for k in mine]) if mine else (None,) * 4
+    rows, cols, desc, cnt = _prepare_groups(engine, [images[k] for k in mine]) if mine else (None,) * 4
     if rows is None:  # ranks without images contribute empty slots of the agreed shape
         probe = engine.prepare([images[0]])
         rows, cols, desc, cnt = (x[:0] for x in probe)
+    if mixed:  # every rank pads its slots to the largest keypoint capacity of any image
+        cap = max(_plan_cap(engine, tuple(im.shape)) for im in images)
+        rows, cols, desc = (_pad_cap(t, cap) for t in (rows, cols, desc))
     cap, D = desc.shape[1], desc.shape[2]
 
     def pad(t, fill=0):
@@ -438,7 +472,19 @@ def build_pairwise_table(images: Sequence, cfg, *, engine=None, group=None) -> P
     return table
 
 
-# ---- planning (mosaic.py:115-180) -----------------------------------------------------------
+# ---- planning (reference mosaic.py:113-180, restated on an inlier matrix) ----------------
+#
+# The reference walks Python sets and re-scans the table per query.  Here the
+# table is turned once into an (n, n) matrix of inlier counts (-1 = no
+# verified pair) and every query is a vector operation on it; the greedy
+# order and both tie rules are the reference's:
+#   anchor = free image with the most verified neighbours among the free
+#            ones, lowest index on ties (select_reference, :115-119);
+#   link   = placed image with the most inliers to the candidate, lowest
+#            index on ties (_best_link, :122-127);
+#   rounds sweep the free images in index order until a sweep places none
+#   (plan_mosaic, :130-180); an anchor with no link into the placed set
+#   is dropped to final_unmatched.
 
 @dataclass(eq=False)
 class MosaicRound:
@@ -455,79 +501,100 @@ class MosaicPlan:
     stage_seconds: dict = field(default_factory=dict)
 
 
+def inlier_matrix(table: PairwiseTransformTable) -> np.ndarray:
+    """(n, n) int64: inlier count of every verified (row, column) entry, -1 elsewhere."""
+    W = np.full((table.n, table.n), -1, dtype=np.int64)
+    for (a, b), e in table.entries.items():
+        W[a, b] = e.inlier_count
+    return W
+
+
+def _anchor(W: np.ndarray, free: np.ndarray) -> int:
+    deg = ((W >= 0) & free[None, :]).sum(axis=1)
+    idx = np.flatnonzero(free)
+    return int(idx[np.argmax(deg[idx])])  # argmax: first (= lowest index) of the maxima
+
+
+def _link(W: np.ndarray, placed: np.ndarray, c: int):
+    score = np.where(placed, W[:, c], -1)
+    p = int(np.argmax(score))
+    return p if score[p] >= 0 else None
+
+
 def select_reference(table: PairwiseTransformTable, remaining: set) -> int:
     if not remaining:
         raise ValueError("remaining set is empty")
-    return min(remaining, key=lambda a: (-table.neighbor_count(a, remaining), a))
-
-
-def _best_link(table: PairwiseTransformTable, candidate: int, placed: dict):
-    links = [p for p in placed if table.present(p, candidate)]
-    if not links:
-        return None
-    return min(links, key=lambda p: (-table.get(p, candidate).inlier_count, p))
+    free = np.zeros(table.n, dtype=bool)
+    free[list(remaining)] = True
+    return _anchor(inlier_matrix(table), free)
 
 
 def plan_mosaic(table: PairwiseTransformTable, ids: Sequence[str]):
-    """Greedy rounds: the most-connected remaining image anchors a round and
-    every reachable image is placed by composing along its best link."""
-    remaining = set(range(table.n))
-    placed: dict = {}
-    rounds, unmatched = [], []
-    while remaining:
-        ref = select_reference(table, remaining)
-        if not placed:
-            placed[ref] = RigidTransform.identity()
+    """Greedy rounds over the table -> (MosaicPlan, {image index: placement})."""
+    W = inlier_matrix(table)
+    free = np.ones(table.n, dtype=bool)
+    on_canvas = np.zeros(table.n, dtype=bool)
+    pose: dict = {}
+    rounds, dropped = [], []
+
+    def attach(c: int, via: int) -> None:
+        pose[c] = pose[via].compose(table.get(via, c).transform)
+        on_canvas[c], free[c] = True, False
+
+    while free.any():
+        a = _anchor(W, free)
+        if not on_canvas.any():
+            pose[a] = RigidTransform.identity()
+            on_canvas[a], free[a] = True, False
         else:
-            link = _best_link(table, ref, placed)
-            if link is None:
-                remaining.discard(ref)
-                unmatched.append(ref)
+            via = _link(W, on_canvas, a)
+            free[a] = False
+            if via is None:
+                dropped.append(a)
                 continue
-            placed[ref] = placed[link].compose(table.get(link, ref).transform)
-        remaining.discard(ref)
-        stitched, progress = [], True
-        while progress:
-            progress = False
-            for cand in sorted(remaining):
-                link = _best_link(table, cand, placed)
-                if link is None:
-                    continue
-                placed[cand] = placed[link].compose(table.get(link, cand).transform)
-                remaining.discard(cand)
-                stitched.append(cand)
-                progress = True
-        rounds.append(MosaicRound(ids[ref], [ids[i] for i in stitched]))
-    plan = MosaicPlan(rounds, [ids[i] for i in sorted(unmatched)], {ids[i]: t for i, t in placed.items()})
-    return plan, placed
+            attach(a, via)
+        joined = []
+        swept = True
+        while swept:
+            swept = False
+            for c in np.flatnonzero(free).tolist():  # ascending, re-checked as the canvas grows
+                via = _link(W, on_canvas, c)
+                if via is not None:
+                    attach(c, via)
+                    joined.append(c)
+                    swept = True
+        rounds.append(MosaicRound(ids[a], [ids[i] for i in joined]))
+    plan = MosaicPlan(rounds, [ids[i] for i in sorted(dropped)], {ids[i]: t for i, t in pose.items()})
+    return plan, pose
 
 
 def plan_and_stitch(images: Sequence, cfg, *, engine=None, group=None):
-    """mosaic.py:183-225 on the GPU: pairwise table (sharded over ``group``),
-    plan, and the device composite of the placed images -> (plan, composite).
-    ``images`` are IntensityImage-like objects (``pixels``, ``image_id``)."""
+    """Reference mosaic.py:183-220 on the GPU -> (plan, composite): the
+    pairwise table (sharded over ``group``), the planner above, and the
+    device composite of every placed image.  ``images`` are
+    IntensityImage-like objects (``pixels``, ``image_id``)."""
     import time
 
     from . import compositor as K
 
     if len(images) < 2:
         raise ConfigError("mosaic needs at least 2 images")
-    ids = [img.image_id for img in images]
-    if len(set(ids)) != len(ids):
+    names = [im.image_id for im in images]
+    if len(names) != len(set(names)):
         raise ConfigError("image ids must be unique")
-    t0 = time.perf_counter()
-    pixels = [img.pixels for img in images]
-    table = build_pairwise_table(pixels, cfg, engine=engine, group=group)
-    t1 = time.perf_counter()
-    plan, placed = plan_mosaic(table, ids)
-    plan.pair_inliers = {(ids[a], ids[b]): e.inlier_count for (a, b), e in table.entries.items() if a < b}
-    t2 = time.perf_counter()
-    placements = [K.Placement(ids[i], placed[i]) for i in sorted(placed)]
-    dims = {ids[i]: tuple(np.asarray(images[i].pixels).shape[:2]) for i in placed}
-    canvas = K.compute_canvas(placements, dims)
-    composite = K.warp_and_blend({ids[i]: images[i].pixels for i in placed}, placements, canvas,
+    clock = [time.perf_counter()]
+    table = build_pairwise_table([im.pixels for im in images], cfg, engine=engine, group=group)
+    clock.append(time.perf_counter())
+    plan, pose = plan_mosaic(table, names)
+    plan.pair_inliers = {(names[a], names[b]): e.inlier_count for (a, b), e in table.entries.items() if a < b}
+    clock.append(time.perf_counter())
+    order = sorted(pose)
+    placements = [K.Placement(names[i], pose[i]) for i in order]
+    shapes = {names[i]: tuple(np.asarray(images[i].pixels).shape[:2]) for i in order}
+    canvas = K.compute_canvas(placements, shapes)
+    composite = K.warp_and_blend({names[i]: images[i].pixels for i in order}, placements, canvas,
                                  blend=cfg.blend, resample=cfg.resample)
-    t3 = time.perf_counter()
-    plan.stage_seconds = {"pairwise_table": t1 - t0, "planning": t2 - t1, "compositing": t3 - t2}
+    clock.append(time.perf_counter())
+    plan.stage_seconds = dict(zip(("pairwise_table", "planning", "compositing"),
+                                  (clock[1] - clock[0], clock[2] - clock[1], clock[3] - clock[2])))
     return plan, composite
-

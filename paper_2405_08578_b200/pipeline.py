@@ -142,7 +142,7 @@ def prepare_batch(images, cfg: PipelineConfig, *, stream=None, meta=False) -> li
     batch = torch.stack(raws).cuda(non_blocking=True)
     nr, nc = batch.shape[1], batch.shape[2]
     alpha = cfg.alpha if cfg.alpha is not None else default_alpha(nr, nc)
-    apply_linear_ramp(IntensityImage(raws[0]), alpha)  # validation (imaging.py:138-145)
+    apply_linear_ramp(IntensityImage(raws[0]), alpha)  # validation (imaging.py:121-128)
     dimg = device.as_device_images(batch, alpha)
     torch.cuda.synchronize()
     t0 = time.perf_counter()

@@ -3,7 +3,7 @@
 These mirror the reference's dataclasses field for field so the drop-in
 entry points accept and return the same shapes of data:
 
-  IntensityImage / RampedImage      imaging.py:44-80
+  IntensityImage / RampedImage      imaging.py:28-63
   ScaleSet / FeaturePoint           detector.py:33-80
   DescriptorConfig / DescribedFeatures  descriptor.py:37-79
   MatcherConfig / MatchPair         matcher.py:16-36
@@ -101,12 +101,12 @@ class _LazyRamp:
 
 
 def default_alpha(nr: int, nc: int) -> float:
-    """imaging.py:125-127."""
+    """imaging.py:108-111."""
     return 1e-6 * 255.0 / (nr * nc)
 
 
 def apply_linear_ramp(img: IntensityImage, alpha: float) -> RampedImage:
-    """imaging.py:130-149; validation identical, ramp deferred to the device."""
+    """imaging.py:113-132; validation identical, ramp deferred to the device."""
     if not math.isfinite(alpha) or alpha <= 0:
         raise ConfigError(f"alpha must be positive, got {alpha}")
     if alpha * img.nr * img.nc > RAMP_SPAN_LIMIT:

@@ -155,11 +155,11 @@ def config3_images(seed: int = 0, rot_deg: float = 5.0, scale_range=(0.95, 1.05)
     return [out[k] for k in order], [truth[k] for k in order]
 
 
-LUMA = np.array([0.299, 0.587, 0.114])  # BT.601 weights (reference imaging.py:38)
+LUMA = np.array([0.299, 0.587, 0.114])  # BT.601 weights (reference imaging.py:21)
 
 
 def gray_bt601(rgb: np.ndarray) -> np.ndarray:
-    """The reference's to_grayscale (imaging.py:83-85): float64 rgb @ weights."""
+    """The reference's to_grayscale (imaging.py:66-68): float64 rgb @ weights."""
     return np.asarray(rgb, dtype=np.float64) @ LUMA
 
 

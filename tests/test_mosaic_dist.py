@@ -60,15 +60,25 @@ def fragments():
     return [np.ascontiguousarray(c) for c in crops[:5]]
 
 
+def mixed_fragments():
+    """Fragments of different sizes (the reference accepts them, mosaic.py:79-112)."""
+    s = scenes.scene(300, 420, 21)
+    boxes = [(0, 0, 160, 224), (0, 98, 150, 200), (140, 0, 160, 224), (130, 90, 170, 250), (140, 196, 150, 200)]
+    return [np.ascontiguousarray(s[r:r + h, c:c + w]) for r, c, h, w in boxes]
+
+
 def table_digest(t):
     return sorted((a, b, round(e.transform.theta, 12), round(e.transform.t_x, 9), round(e.transform.t_y, 9),
                    e.inlier_count) for (a, b), e in t.entries.items())
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, mixed=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        if mixed:
+            q.put((rank, table_digest(mosaic.build_pairwise_table(mixed_fragments(), CFG, engine=OracleEngine(CFG)))))
+            return
         t = mosaic.build_pairwise_table(fragments(), CFG, engine=OracleEngine(CFG))
         # an engine with persistent gather buffers (as GraphEngine): two tables through the same buffers
         eng = OracleEngine(CFG)
@@ -93,8 +103,7 @@ def single_table():
     return mosaic.build_pairwise_table(fragments(), CFG, engine=OracleEngine(CFG))
 
 
-def test_single_rank_table_matches_sequential_reference_semantics(single_table):
-    imgs = fragments()
+def sequential_table(imgs):
     eng = OracleEngine(CFG)
     prep = [eng.prepare([im]) for im in imgs]
     want = mosaic.PairwiseTransformTable(n=len(imgs))
@@ -106,8 +115,30 @@ def test_single_rank_table_matches_sequential_reference_semantics(single_table):
             if ok:
                 from paper_2405_08578_b200.records import RigidTransform
                 want.set_pair(a, b, RigidTransform(th, tx, ty).inverse(), ni)
+    return want
+
+
+def test_single_rank_table_matches_sequential_reference_semantics(single_table):
+    want = sequential_table(fragments())
     assert table_digest(single_table) == table_digest(want)
     assert len(single_table.entries) >= 8  # the overlapping neighbours register
+
+
+def test_mixed_size_images_one_and_two_ranks():
+    want = table_digest(sequential_table(mixed_fragments()))
+    assert want, "some mixed-size pairs register"
+    assert table_digest(mosaic.build_pairwise_table(mixed_fragments(), CFG, engine=OracleEngine(CFG))) == want
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, True)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    for rank, dig in (q.get(timeout=10) for _ in procs):
+        assert dig == want, f"rank {rank} table differs"
 
 
 def test_two_ranks_gloo_equal_one_rank(single_table):

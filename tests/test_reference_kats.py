@@ -122,3 +122,48 @@ def test_errors_alias_reference_classes(tmp_path):
     proc = subprocess.run([sys.executable, "-c", code], cwd=str(tmp_path), env=env, capture_output=True,
                           text=True, timeout=300)
     assert proc.returncode == 0 and "ok" in proc.stdout, proc.stderr[-2000:]
+
+
+PLAN_SCRIPT = r'''
+import numpy as np
+from peakstitch import mosaic as RM
+from peakstitch.registration import RigidTransform as RT
+from paper_2405_08578_b200 import mosaic as M
+from paper_2405_08578_b200.records import RigidTransform as MT
+rng = np.random.default_rng(5)
+for trial in range(300):
+    n = int(rng.integers(2, 10))
+    rt, mt = RM.PairwiseTransformTable(n=n), M.PairwiseTransformTable(n=n)
+    for a in range(n):
+        for b in range(a + 1, n):
+            if rng.random() < float(rng.choice([0.15, 0.4, 0.8])):
+                th, tx, ty = rng.uniform(-3, 3), rng.uniform(-99, 99), rng.uniform(-99, 99)
+                k = int(rng.integers(8, 12))  # few distinct counts: many ties
+                rt.set_pair(a, b, RT(th, tx, ty), k)
+                mt.set_pair(a, b, MT(th, tx, ty), k)
+    ids = [f"i{k}" for k in range(n)]
+    rp, rplaced = RM.plan_mosaic(rt, ids)
+    mp_, mplaced = M.plan_mosaic(mt, ids)
+    assert [(r.reference_id, r.stitched_ids) for r in rp.rounds] == [(r.reference_id, r.stitched_ids) for r in mp_.rounds]
+    assert rp.final_unmatched == mp_.final_unmatched
+    assert sorted(rplaced) == sorted(mplaced)
+    for k in rplaced:
+        a, b = rplaced[k], mplaced[k]
+        assert (a.theta, a.t_x, a.t_y) == (b.theta, b.t_x, b.t_y), (trial, k)
+    for rem in ({0}, set(range(n))):
+        assert RM.select_reference(rt, rem) == M.select_reference(mt, rem)
+print("plan ok")
+'''
+
+
+@needs_ref
+def test_planner_equals_reference_planner(tmp_path):
+    """CPU: the inlier-matrix planner (mosaic.plan_mosaic) reproduces the
+    reference's plan_mosaic (mosaic.py:130-180) -- rounds, anchors, order,
+    unmatched, placements bit for bit -- on 300 random tables with tied
+    inlier counts."""
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([REF, REPO, env.get("PYTHONPATH", "")])
+    proc = subprocess.run([sys.executable, "-c", PLAN_SCRIPT], cwd=str(tmp_path), env=env, capture_output=True,
+                          text=True, timeout=600)
+    assert proc.returncode == 0 and "plan ok" in proc.stdout, (proc.stdout + proc.stderr)[-3000:]
