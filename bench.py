@@ -422,7 +422,9 @@ def bench_c5_pairs(args, world, rank, dev, n_pairs=256, steps=2, with_cpu=False)
     from paper_2405_08578_b200.pipeline import PipelineConfig
 
     cfg = PipelineConfig(window_min=16, window_max=64)
-    mine = [p for p in range(n_pairs) if p % world == rank]
+    from paper_2405_08578_b200 import shard
+
+    mine = shard.round_robin(n_pairs, rank, world)  # pairs sharded, no data-path collective
     grey = []
     import multiprocessing as mp
 
@@ -887,7 +889,9 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     # weak scaling: every rank runs the full C2 batch of its own seeded images
     # (seeds rank*64 .. rank*64+63; rank 0's batch is BASELINE configs[1]'s)
-    mine = [rank * args.images + k for k in range(args.images)]
+    from paper_2405_08578_b200 import shard
+
+    mine = shard.image_slots(rank, world, args.images)
     n = len(mine)
     host = np.empty((n, NR, NC), dtype=np.uint8)
     import multiprocessing as mp

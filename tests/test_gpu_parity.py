@@ -178,6 +178,19 @@ def test_descriptor_saturated_clusters_bit_identical_and_deterministic():
     assert torch.equal(a, b)
     uniq = torch.unique(a[0], dim=0).shape[0]
     assert uniq < a.shape[1]  # flat regions produce identical (saturated) rows
+    # rows bit-identical in the oracle are bit-identical on the GPU
+    d64 = device.describe(t, kp, cfg, out64=True, out32=False)[0].cpu().numpy()
+    P = O.ramp(img.astype(np.float64), O.default_alpha(*img.shape))
+    h = kp.image(0)
+    idx = np.random.default_rng(3).choice(len(h["row"]), 1500, replace=False)
+    groups = {}
+    for k in idx:
+        ref = O.describe_one(P, int(h["row"][k]), int(h["col"][k]), 16, 0.0625, 4, 64, True)
+        groups.setdefault(ref.tobytes(), []).append(int(k))
+    multi = [g for g in groups.values() if len(g) > 1]
+    assert multi
+    for g in multi:
+        assert all(np.array_equal(d64[g[0]], d64[k]) for k in g[1:]), g
 
 
 def test_descriptor_properties():
