@@ -246,6 +246,147 @@ __global__ void __launch_bounds__(256) detect_u8_w8(RampU8 img, int64_t img_stri
   }
 }
 
+// ---- vectorised strip kernel: any window side (integer-key mode) ----------
+// One CTA per (image, window row); thread t owns the 16-pixel column chunk
+// [16t, 16t + 16) over the window row's rows (one 16-byte load per row for
+// u8, three for RGB8).  Per pixel column it keeps the max and min of the key
+// (v << 16 | r), r = row within the window: the largest v with the HIGHEST
+// row and the smallest v with the LOWEST row -- the integer-key rule of
+// detector.py:114-119 restricted to one column.  The column keys go to
+// shared memory and one thread per window folds its columns left to right
+// (max: >= so the highest column wins a tie, min: < so the lowest does),
+// which completes the rule: highest / lowest flat index among equal values.
+// Reads every image byte once (HBM-bound).
+template <class Img>
+struct StripKeys;
+
+template <>
+struct StripKeys<RampU8> {
+  using K = uint32_t;
+  static constexpr int kLoads = 1;
+  __device__ __forceinline__ static void row(const RampU8& im, int rr, int chunk, uint32_t rkey, K (&mx)[16],
+                                             K (&mn)[16]) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(im.p + (int64_t)rr * im.pitch) + chunk);
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      // [r lo, r hi, v, 0]: rkey's bytes 0, 1 and its zero byte 2 around pixel byte j % 4
+      const uint32_t key = __byte_perm(w[j >> 2], rkey, 0x6004u | ((uint32_t)(j & 3) << 8) | 0x50u);
+      mx[j] = max(mx[j], key);
+      mn[j] = min(mn[j], key);
+    }
+  }
+};
+
+template <>
+struct StripKeys<RampRGB8> {
+  using K = uint64_t;
+  static constexpr int kLoads = 3;
+  __device__ __forceinline__ static void row(const RampRGB8& im, int rr, int chunk, uint32_t rkey, K (&mx)[16],
+                                             K (&mn)[16]) {
+    const uint4* src = reinterpret_cast<const uint4*>(im.p + 3 * (int64_t)rr * im.pitch) + 3 * chunk;
+    const uint4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2);
+    const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int o = 3 * j;  // byte offset of pixel j's R
+      const uint32_t R = (w[o >> 2] >> (8 * (o & 3))) & 0xffu;
+      const uint32_t G = (w[(o + 1) >> 2] >> (8 * ((o + 1) & 3))) & 0xffu;
+      const uint32_t B = (w[(o + 2) >> 2] >> (8 * ((o + 2) & 3))) & 0xffu;
+      const K key = ((K)(299u * R + 587u * G + 114u * B) << 16) | rkey;
+      mx[j] = max(mx[j], key);
+      mn[j] = min(mn[j], key);
+    }
+  }
+};
+
+template <class Img>
+__global__ void __launch_bounds__(256) detect_strip(Img img, int64_t img_stride, int B, int L, int wr_n, int wc,
+                                                    int nwin, int32_t* __restrict__ tmax,
+                                                    int32_t* __restrict__ tmin, KpOut out, int32_t scale_tag) {
+  using K = typename StripKeys<Img>::K;
+  extern __shared__ unsigned char strip_smem[];
+  const int nr = img.nr, nc = img.nc;
+  const int chunks = (nc + 15) >> 4;
+  K* cmax = reinterpret_cast<K*>(strip_smem);
+  K* cmin = cmax + 16 * chunks;
+  for (int64_t task = blockIdx.x; task < (int64_t)B * wr_n; task += gridDim.x) {
+    const int b = (int)(task / wr_n), wr = (int)(task % wr_n);
+    Img im = img;
+    im.p = img.p + (int64_t)b * img_stride * decltype(img)::kElem;
+    const int r0 = wr * L, h = min(L, nr - r0);
+    __syncthreads();  // the previous task's folds are done with the column keys
+    for (int t = threadIdx.x; t < chunks; t += blockDim.x) {
+      K mx[16], mn[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) { mx[j] = 0; mn[j] = ~(K)0; }
+      for (int r = 0; r < h; ++r) StripKeys<Img>::row(im, r0 + r, t, (uint32_t)r, mx, mn);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        cmax[16 * t + j] = mx[j];
+        cmin[16 * t + j] = mn[j];
+      }
+    }
+    __syncthreads();
+    for (int wcol = threadIdx.x; wcol < wc; wcol += blockDim.x) {
+      const int c0 = wcol * L, c1 = min(c0 + L, nc);
+      K bx = cmax[c0], bn = cmin[c0];
+      int cx = c0, cn = c0;
+      for (int c = c0 + 1; c < c1; ++c) {
+        const K kx = cmax[c], kn = cmin[c];
+        if (kx >= bx) { bx = kx; cx = c; }
+        if (kn < bn) { bn = kn; cn = c; }
+      }
+      const int32_t kmax = (r0 + (int)(bx & 0xffffu)) * nc + cx;
+      const int32_t kmin = (r0 + (int)(bn & 0xffffu)) * nc + cn;
+      const int w = wr * wc + wcol;
+      if (tmax) {
+        tmax[(int64_t)b * nwin + w] = kmax;
+        tmin[(int64_t)b * nwin + w] = kmin;
+      }
+      if (out.row) {  // direct emission: slot 2w (max), 2w+1 (min)
+        const int64_t sl = (int64_t)b * out.cap + 2 * (int64_t)w;
+        const int32_t ks[2] = {kmax, kmin};
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int rr = ks[q] / nc, cc = ks[q] % nc;
+          out.row[sl + q] = rr;
+          out.col[sl + q] = cc;
+          out.value[sl + q] = im.at(rr, cc);
+          if (out.scale) out.scale[sl + q] = scale_tag;
+          if (out.pol) out.pol[sl + q] = (int8_t)q;
+          if (out.window) out.window[sl + q] = w;
+        }
+      }
+    }
+  }
+}
+
+template <class Img>
+int launch_strip(const Img& img, const ps_image_batch* ib, int B, int L, int wc, int nwin, const KpOut& ko,
+                 int32_t* tmax, int32_t* tmin, cudaStream_t st) {
+  using K = typename StripKeys<Img>::K;
+  const int wr_n = (img.nr + L - 1) / L, chunks = (img.nc + 15) / 16;
+  const size_t smem = 2 * (size_t)16 * chunks * sizeof(K);
+  const int threads = std::min(256, std::max(32, (chunks + 31) / 32 * 32));
+  cudaFuncSetAttribute(detect_strip<Img>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int64_t tasks = (int64_t)B * wr_n;
+  const int grid = (int)std::min<int64_t>(tasks, 148 * 16);
+  detect_strip<Img><<<grid, threads, smem, st>>>(img, ib->image_stride, B, L, wr_n, wc, nwin, tmax, tmin, ko, L);
+  PS_LAUNCHED("detect_strip");
+  return PS_OK;
+}
+
+// strip kernel preconditions: 16-byte aligned rows and images, rows of at
+// most 2^16 (row index in the key), column keys within the shared memory
+bool strip_ok(const ps_image_batch* ib, int L, int key_bytes) {
+  const int64_t bpp = ib->pixel_type == PS_PIXELS_RGB8 ? 3 : 1;
+  const bool aligned = ((uintptr_t)ib->data) % 16 == 0 && (ib->row_pitch * bpp) % 16 == 0 &&
+                       (ib->image_stride * bpp) % 16 == 0;
+  const size_t smem = 2 * (size_t)16 * ((ib->nc + 15) / 16) * key_bytes;
+  return aligned && L < 65536 && smem <= 200 * 1024;
+}
+
 // ---- general emission (several scales and/or dedupe) ------------------------
 struct Tables {
   int32_t* tmax[kMaxScales];
@@ -385,9 +526,11 @@ int launch_key(const Img&, const ps_image_batch*, int, int, int, int, bool, cons
   return PS_ERR_ARGUMENT;
 }
 
-// RGB8 with a valid ramp: integer luma key, generic warp-per-window kernel.
+// RGB8 with a valid ramp: integer luma key; the vectorised strip kernel when
+// the rows are 16-byte aligned, else the generic warp-per-window kernel.
 int launch_key(const RampRGB8& img, const ps_image_batch* ib, int B, int L, int wc, int nwin, bool,
                const KpOut& ko, int32_t* tmax, int32_t* tmin, cudaStream_t st) {
+  if (strip_ok(ib, L, 8)) return launch_strip(img, ib, B, L, wc, nwin, ko, tmax, tmin, st);
   window_extrema_warp<0><<<grid_for((int64_t)B * nwin, 8), 256, 0, st>>>(img, ib->image_stride, B, L, wc, nwin,
                                                                            tmax, tmin, ko, L);
   PS_LAUNCHED("window_extrema_warp<rgb key>");
@@ -403,6 +546,8 @@ int launch_key(const RampU8& img, const ps_image_batch* ib, int B, int L, int wc
     detect_u8_w8<<<(unsigned)((th + 255) / 256), 256, 0, st>>>(img, ib->image_stride, B, wr_n, wc_n, ppr, ko, tmax,
                                                                 tmin);
     PS_LAUNCHED("detect_u8_w8");
+  } else if (strip_ok(ib, L, 4)) {
+    return launch_strip(img, ib, B, L, wc, nwin, ko, tmax, tmin, st);
   } else {
     window_extrema_warp<0><<<grid_for((int64_t)B * nwin, 8), 256, 0, st>>>(img, ib->image_stride, B, L, wc, nwin,
                                                                              tmax, tmin, ko, L);

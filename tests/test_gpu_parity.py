@@ -895,3 +895,33 @@ def test_descriptor_out_of_image_features_clamped_like_reference():
     for k, f in enumerate(feats):
         ref = O.describe_one(P, f.row, f.col, f.scale, 0.0625, 4, 64)
         assert np.max(np.abs(got[k] - ref)) <= P2_TOL * max(np.linalg.norm(ref), 1e-300), f
+
+
+@pytest.mark.parametrize("nr,nc,scales", [(97, 131, (16, 24)), (200, 333, (36,)), (150, 255, (8, 12, 40)),
+                                          (64, 64, (17,)), (300, 257, (32, 64, 128)), (130, 140, (8, 16, 32))])
+def test_strip_detector_padded_pitch_tie_heavy(nr, nc, scales):
+    """The vectorised strip kernel (any window side, 16-byte aligned rows):
+    tie-heavy u8 and RGB rasters in a padded-pitch layout (odd widths, shrunk
+    trailing windows, non-nested and nested scale sets) against the oracle."""
+    rng = np.random.default_rng(nr * nc)
+    pitch = (nc + 15) // 16 * 16 + 16
+    px = (rng.integers(0, 3, size=(2, nr, nc)) * 100).astype(np.uint8)
+    buf = torch.zeros((2, nr, pitch), dtype=torch.uint8, device="cuda")
+    buf[:, :, :nc] = torch.from_numpy(px).cuda()
+    alpha = O.default_alpha(nr, nc)
+    kp = device.detect(device.DeviceImages(buf[:, :, :nc], "u8", alpha), scales)
+    rgb = rng.integers(0, 2, size=(2, nr, nc, 3)).astype(np.uint8) * np.uint8(120)
+    rbuf = torch.zeros((2, nr, pitch, 3), dtype=torch.uint8, device="cuda")
+    rbuf[:, :, :nc] = torch.from_numpy(rgb).cuda()
+    from paper_2405_08578_b200.ingest import gray_source
+
+    kr = device.detect(device.DeviceImages(rbuf[:, :, :nc], "rgb8", alpha, gray_source(rbuf.device)), scales)
+    for b in range(2):
+        want = O.detect(O.ramp(px[b].astype(np.float64), alpha), scales)
+        h = kp.image(b)
+        h["pol"] = h.pop("polarity")
+        assert_kp_equal(h, want, f"u8 {b}")
+        want = O.detect(O.ramp(scenes.gray_bt601(rgb[b]), alpha), scales)
+        h = kr.image(b)
+        h["pol"] = h.pop("polarity")
+        assert_kp_equal(h, want, f"rgb {b}")
