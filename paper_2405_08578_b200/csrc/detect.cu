@@ -17,6 +17,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "ps_common.cuh"
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(256) detect_u8_w8(RampU8 img, int64_t img_stri
 // One CTA per (image, window row); thread t owns the 16-pixel column chunk
 // [16t, 16t + 16) over the window row's rows (one 16-byte load per row for
 // u8, three for RGB8).  Per pixel column it keeps the max and min of the key
-// (v << 16 | r), r = row within the window: the largest v with the HIGHEST
+// (v << 8 | r), r = row within the window: the largest v with the HIGHEST
 // row and the smallest v with the LOWEST row -- the integer-key rule of
 // detector.py:114-119 restricted to one column.  The column keys go to
 // shared memory and one thread per window folds its columns left to right
@@ -262,83 +263,155 @@ struct StripKeys;
 
 template <>
 struct StripKeys<RampU8> {
+  // accumulators: 16-bit keys (v << 8 | r), two per register (columns 2i, 2i+1),
+  // reduced with the packed u16 max / min
   using K = uint32_t;
-  static constexpr int kLoads = 1;
-  __device__ __forceinline__ static void row(const RampU8& im, int rr, int chunk, uint32_t rkey, K (&mx)[16],
-                                             K (&mn)[16]) {
-    const uint4 q = __ldg(reinterpret_cast<const uint4*>(im.p + (int64_t)rr * im.pitch) + chunk);
+  using Raw = uint4;
+  static constexpr int kBatch = 8;  // rows whose loads are in flight together
+  static constexpr int kBatch16 = 2;  // the same for detect_strip16 (row pairs: fold2)
+  static constexpr int kMinBlocks16 = 3;  // its resident 256-thread CTAs per SM
+  static constexpr int kMaxThreads = 256;
+  static constexpr int kAcc = 8;    // registers per accumulator set
+  static constexpr int kMaxRows = 256;  // the row index must fit its 8 bits
+  __device__ __forceinline__ static Raw load(const RampU8& im, int rr, int chunk) {
+    return __ldg(reinterpret_cast<const uint4*>(im.p + (int64_t)rr * im.pitch) + chunk);
+  }
+  __device__ __forceinline__ static void init(uint32_t (&mx)[kAcc], uint32_t (&mn)[kAcc]) {
+#pragma unroll
+    for (int j = 0; j < kAcc; ++j) { mx[j] = 0u; mn[j] = 0xffffffffu; }
+  }
+  __device__ __forceinline__ static void fold(const Raw& q, uint32_t r, uint32_t (&mx)[kAcc], uint32_t (&mn)[kAcc]) {
     const uint32_t w[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      // [r lo, r hi, v, 0]: rkey's bytes 0, 1 and its zero byte 2 around pixel byte j % 4
-      const uint32_t key = __byte_perm(w[j >> 2], rkey, 0x6004u | ((uint32_t)(j & 3) << 8) | 0x50u);
-      mx[j] = max(mx[j], key);
-      mn[j] = min(mn[j], key);
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t k01 = __byte_perm(w[i], r, 0x1404u);  // [r, v0, r, v1]
+      const uint32_t k23 = __byte_perm(w[i], r, 0x3424u);  // [r, v2, r, v3]
+      mx[2 * i] = __vmaxu2(mx[2 * i], k01);
+      mn[2 * i] = __vminu2(mn[2 * i], k01);
+      mx[2 * i + 1] = __vmaxu2(mx[2 * i + 1], k23);
+      mn[2 * i + 1] = __vminu2(mn[2 * i + 1], k23);
     }
+  }
+  // two rows at once: 3-input packed max / min
+  __device__ __forceinline__ static void fold2(const Raw& q0, const Raw& q1, uint32_t r, uint32_t (&mx)[kAcc],
+                                               uint32_t (&mn)[kAcc]) {
+    const uint32_t w0[4] = {q0.x, q0.y, q0.z, q0.w}, w1[4] = {q1.x, q1.y, q1.z, q1.w};
+    const uint32_t r1 = r + 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t a01 = __byte_perm(w0[i], r, 0x1404u), a23 = __byte_perm(w0[i], r, 0x3424u);
+      const uint32_t b01 = __byte_perm(w1[i], r1, 0x1404u), b23 = __byte_perm(w1[i], r1, 0x3424u);
+      mx[2 * i] = __vimax3_u16x2(mx[2 * i], a01, b01);
+      mn[2 * i] = __vimin3_u16x2(mn[2 * i], a01, b01);
+      mx[2 * i + 1] = __vimax3_u16x2(mx[2 * i + 1], a23, b23);
+      mn[2 * i + 1] = __vimin3_u16x2(mn[2 * i + 1], a23, b23);
+    }
+  }
+  __device__ __forceinline__ static K key(const uint32_t (&acc)[kAcc], int j) {  // column j: (v << 8 | r)
+    return (acc[j >> 1] >> (16 * (j & 1))) & 0xffffu;
   }
 };
 
 template <>
 struct StripKeys<RampRGB8> {
-  using K = uint64_t;
-  static constexpr int kLoads = 3;
-  __device__ __forceinline__ static void row(const RampRGB8& im, int rr, int chunk, uint32_t rkey, K (&mx)[16],
-                                             K (&mn)[16]) {
+  // accumulators: 32-bit keys (k << 8 | r), k = 299R + 587G + 114B < 2^18
+  using K = uint32_t;
+  struct Raw {
+    uint4 a, b, c;
+  };
+  static constexpr int kBatch = 4;
+  static constexpr int kBatch16 = 2;
+  static constexpr int kMinBlocks16 = 2;
+  static constexpr int kMaxThreads = 256;
+  static constexpr int kAcc = 16;
+  static constexpr int kMaxRows = 256;  // the row index must fit its 8 bits
+  __device__ __forceinline__ static void init(K (&mx)[kAcc], K (&mn)[kAcc]) {
+#pragma unroll
+    for (int j = 0; j < kAcc; ++j) { mx[j] = 0u; mn[j] = 0xffffffffu; }
+  }
+  __device__ __forceinline__ static K key(const K (&acc)[kAcc], int j) { return acc[j]; }  // (v << 8 | r)
+  __device__ __forceinline__ static Raw load(const RampRGB8& im, int rr, int chunk) {
     const uint4* src = reinterpret_cast<const uint4*>(im.p + 3 * (int64_t)rr * im.pitch) + 3 * chunk;
-    const uint4 a = __ldg(src), b = __ldg(src + 1), c = __ldg(src + 2);
-    const uint32_t w[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+    return Raw{__ldg(src), __ldg(src + 1), __ldg(src + 2)};
+  }
+  __device__ __forceinline__ static void fold(const Raw& q, uint32_t r, K (&mx)[kAcc], K (&mn)[kAcc]) {
+    const uint32_t w[13] = {q.a.x, q.a.y, q.a.z, q.a.w, q.b.x, q.b.y, q.b.z, q.b.w, q.c.x, q.c.y, q.c.z, q.c.w, 0u};
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const int o = 3 * j;  // byte offset of pixel j's R
-      const uint32_t R = (w[o >> 2] >> (8 * (o & 3))) & 0xffu;
-      const uint32_t G = (w[(o + 1) >> 2] >> (8 * ((o + 1) & 3))) & 0xffu;
-      const uint32_t B = (w[(o + 2) >> 2] >> (8 * ((o + 2) & 3))) & 0xffu;
-      const K key = ((K)(299u * R + 587u * G + 114u * B) << 16) | rkey;
+      // [R, G, B, x] of pixel j from the two words it spans
+      const uint32_t px = __byte_perm(w[o >> 2], w[(o >> 2) + 1], (uint32_t)(o & 3) * 0x111u + 0x210u);
+      // 299R + 587G + 114B = 256 (R + 2G) + (43R + 75G + 114B): two byte dot products
+      const uint32_t hi = __dp4a(px, 0x00000201u, 0u);
+      const uint32_t lo = __dp4a(px, 0x00724b2bu, 0u);
+      const K key = (hi << 16) + (lo << 8) + r;  // (k << 8 | r)
       mx[j] = max(mx[j], key);
       mn[j] = min(mn[j], key);
     }
   }
 };
 
+
+// A task is (image, window row, segment of SW windows, at most 256 column
+// chunks); thread t owns the segment's column chunk t over all the window
+// row's rows.  Loads are software pipelined: the next kBatch rows are
+// requested before the current ones are folded.
 template <class Img>
-__global__ void __launch_bounds__(256) detect_strip(Img img, int64_t img_stride, int B, int L, int wr_n, int wc,
-                                                    int nwin, int32_t* __restrict__ tmax,
-                                                    int32_t* __restrict__ tmin, KpOut out, int32_t scale_tag) {
-  using K = typename StripKeys<Img>::K;
+__global__ void __launch_bounds__(StripKeys<Img>::kMaxThreads) detect_strip(
+    Img img, int64_t img_stride, int B, int L, int wr_n, int wc, int nwin, int SW, int nseg,
+    int32_t* __restrict__ tmax, int32_t* __restrict__ tmin, KpOut out, int32_t scale_tag) {
+  using SK = StripKeys<Img>;
+  using K = typename SK::K;
+  using A = typename std::conditional<std::is_same<Img, RampU8>::value, uint32_t, K>::type;
+  constexpr int NB = SK::kBatch;
   extern __shared__ unsigned char strip_smem[];
   const int nr = img.nr, nc = img.nc;
-  const int chunks = (nc + 15) >> 4;
   K* cmax = reinterpret_cast<K*>(strip_smem);
-  K* cmin = cmax + 16 * chunks;
-  for (int64_t task = blockIdx.x; task < (int64_t)B * wr_n; task += gridDim.x) {
-    const int b = (int)(task / wr_n), wr = (int)(task % wr_n);
+  K* cmin = cmax + (size_t)SW * L;
+  for (int64_t task = blockIdx.x; task < (int64_t)B * wr_n * nseg; task += gridDim.x) {
+    const int seg = (int)(task % nseg);
+    const int64_t bw = task / nseg;
+    const int b = (int)(bw / wr_n), wr = (int)(bw % wr_n);
     Img im = img;
     im.p = img.p + (int64_t)b * img_stride * decltype(img)::kElem;
     const int r0 = wr * L, h = min(L, nr - r0);
+    const int cs = seg * SW * L, ce = min(cs + SW * L, nc);  // cs is a multiple of 16 (SW is)
+    const int chunks = (ce - cs + 15) >> 4, chunk0 = cs >> 4;
     __syncthreads();  // the previous task's folds are done with the column keys
     for (int t = threadIdx.x; t < chunks; t += blockDim.x) {
-      K mx[16], mn[16];
+      A mx[SK::kAcc], mn[SK::kAcc];
+      SK::init(mx, mn);
+      typename SK::Raw cur[NB], nxt[NB];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) { mx[j] = 0; mn[j] = ~(K)0; }
-      for (int r = 0; r < h; ++r) StripKeys<Img>::row(im, r0 + r, t, (uint32_t)r, mx, mn);
+      for (int i = 0; i < NB; ++i) cur[i] = SK::load(im, r0 + min(i, h - 1), chunk0 + t);
+      for (int r = 0; r < h; r += NB) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) nxt[i] = SK::load(im, r0 + min(r + NB + i, h - 1), chunk0 + t);  // clamped
+#pragma unroll
+        for (int i = 0; i < NB; ++i)
+          if (r + i < h) SK::fold(cur[i], (uint32_t)(r + i), mx, mn);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) cur[i] = nxt[i];
+      }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        cmax[16 * t + j] = mx[j];
-        cmin[16 * t + j] = mn[j];
+        cmax[16 * t + j] = SK::key(mx, j);
+        cmin[16 * t + j] = SK::key(mn, j);
       }
     }
     __syncthreads();
-    for (int wcol = threadIdx.x; wcol < wc; wcol += blockDim.x) {
+    const int w0 = seg * SW, w1 = min(w0 + SW, wc);
+    for (int wcol = w0 + (int)threadIdx.x; wcol < w1; wcol += blockDim.x) {
       const int c0 = wcol * L, c1 = min(c0 + L, nc);
-      K bx = cmax[c0], bn = cmin[c0];
+      K bx = cmax[c0 - cs], bn = cmin[c0 - cs];
       int cx = c0, cn = c0;
       for (int c = c0 + 1; c < c1; ++c) {
-        const K kx = cmax[c], kn = cmin[c];
+        const K kx = cmax[c - cs], kn = cmin[c - cs];
         if (kx >= bx) { bx = kx; cx = c; }
         if (kn < bn) { bn = kn; cn = c; }
       }
-      const int32_t kmax = (r0 + (int)(bx & 0xffffu)) * nc + cx;
-      const int32_t kmin = (r0 + (int)(bn & 0xffffu)) * nc + cn;
+      const int32_t kmax = (r0 + (int)(bx & 0xffu)) * nc + cx;
+      const int32_t kmin = (r0 + (int)(bn & 0xffu)) * nc + cn;
       const int w = wr * wc + wcol;
       if (tmax) {
         tmax[(int64_t)b * nwin + w] = kmax;
@@ -362,29 +435,168 @@ __global__ void __launch_bounds__(256) detect_strip(Img img, int64_t img_stride,
   }
 }
 
+// Window sides that are multiples of 16 (every scale of C1, C3 and C5): a
+// window is G = L / 16 whole 16-pixel chunks and its rows are split into R
+// groups, so G * R lanes (a power of two <= 32) own one window and each lane
+// folds one chunk over L / R rows (8 when L <= 64: all loads in flight at
+// once).  Lane = (row group, window of the warp, chunk), chunk fastest, so a
+// row group's lanes read contiguous columns.  Each lane reduces its 16
+// columns to one (v, r, c) key per polarity and the window's lanes combine
+// with xor shuffles -- no shared memory, no block barrier.  Max: largest
+// (v, r, c), i.e. the highest flat index among equal values; min: smallest
+// (v, r, c), the lowest.
+template <class Img>
+__global__ void __launch_bounds__(256, StripKeys<Img>::kMinBlocks16) detect_strip16(
+    Img img, int64_t img_stride, int B, int L, int G, int R, int wr_n, int wc, int nwin, int32_t* __restrict__ tmax,
+    int32_t* __restrict__ tmin, KpOut out, int32_t scale_tag) {
+  using SK = StripKeys<Img>;
+  using A = typename std::conditional<std::is_same<Img, RampU8>::value, uint32_t, typename SK::K>::type;
+  constexpr int NB = SK::kBatch16;
+  const int nr = img.nr, nc = img.nc;
+  const int lane = threadIdx.x & 31;
+  const int W = 32 / (G * R);                 // windows per warp
+  const int wblocks = (wc + W - 1) / W;       // warps per window row
+  const int c = lane % G, wl = (lane / G) % W, rg = lane / (G * W);
+  const int rpt = L / R;                      // rows per lane
+  const int64_t nwarps = (int64_t)B * wr_n * wblocks;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gw < nwarps; gw += wstride) {
+    const int wb = (int)(gw % wblocks);
+    const int64_t bw = gw / wblocks;
+    const int b = (int)(bw / wr_n), wr = (int)(bw % wr_n);
+    const int wcol = wb * W + wl;
+    const int chunk = wcol * G + c;
+    Img im = img;
+    im.p = img.p + (int64_t)b * img_stride * decltype(img)::kElem;
+    const int r0 = wr * L, h = min(L, nr - r0);
+    const int ra = rg * rpt, rb = min(ra + rpt, h);
+    const bool has = wcol < wc && 16 * chunk < nc && ra < rb;
+    A mx[SK::kAcc], mn[SK::kAcc];
+    SK::init(mx, mn);
+    if (has) {
+      typename SK::Raw cur[NB], nxt[NB];
+#pragma unroll
+      for (int i = 0; i < NB; ++i) cur[i] = SK::load(im, r0 + min(ra + i, rb - 1), chunk);
+      for (int r = ra; r < rb; r += NB) {
+        if (r + NB < rb) {
+#pragma unroll
+          for (int i = 0; i < NB; ++i) nxt[i] = SK::load(im, r0 + min(r + NB + i, rb - 1), chunk);  // clamped
+        }
+        if constexpr (std::is_same<Img, RampU8>::value) {
+          if (r + NB <= rb) {
+#pragma unroll
+            for (int i = 0; i < NB; i += 2) SK::fold2(cur[i], cur[i + 1], (uint32_t)(r + i), mx, mn);
+          } else {
+#pragma unroll
+            for (int i = 0; i < NB; ++i)
+              if (r + i < rb) SK::fold(cur[i], (uint32_t)(r + i), mx, mn);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < NB; ++i)
+            if (r + i < rb) SK::fold(cur[i], (uint32_t)(r + i), mx, mn);
+        }
+#pragma unroll
+        for (int i = 0; i < NB; ++i) cur[i] = nxt[i];
+      }
+    }
+    const int cw = 16 * c;  // column offset of the chunk within its window
+    unsigned long long bx = 0ull, bn = ~0ull;
+    if (has) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (16 * chunk + j >= nc) continue;
+        const unsigned long long col = (unsigned long long)(cw + j);
+        const unsigned long long fx = ((unsigned long long)SK::key(mx, j) << 8) | col;  // (v, r, c)
+        const unsigned long long fn = ((unsigned long long)SK::key(mn, j) << 8) | col;
+        bx = fx > bx ? fx : bx;
+        bn = fn < bn ? fn : bn;
+      }
+    }
+    for (int o = 1; o < G; o <<= 1) {  // chunks of the window
+      const unsigned long long ox = __shfl_xor_sync(0xffffffffu, bx, o);
+      const unsigned long long on = __shfl_xor_sync(0xffffffffu, bn, o);
+      bx = ox > bx ? ox : bx;
+      bn = on < bn ? on : bn;
+    }
+    for (int o = G * W; o < 32; o <<= 1) {  // row groups of the window
+      const unsigned long long ox = __shfl_xor_sync(0xffffffffu, bx, o);
+      const unsigned long long on = __shfl_xor_sync(0xffffffffu, bn, o);
+      bx = ox > bx ? ox : bx;
+      bn = on < bn ? on : bn;
+    }
+    if (wcol < wc && c == 0 && rg == 0) {
+      const int c0 = wcol * L;
+      const int32_t kmax = (r0 + (int)((bx >> 8) & 0xffull)) * nc + c0 + (int)(bx & 0xffull);
+      const int32_t kmin = (r0 + (int)((bn >> 8) & 0xffull)) * nc + c0 + (int)(bn & 0xffull);
+      const int w = wr * wc + wcol;
+      if (tmax) {
+        tmax[(int64_t)b * nwin + w] = kmax;
+        tmin[(int64_t)b * nwin + w] = kmin;
+      }
+      if (out.row) {  // direct emission: slot 2w (max), 2w+1 (min)
+        const int64_t sl = (int64_t)b * out.cap + 2 * (int64_t)w;
+        const int32_t ks[2] = {kmax, kmin};
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int rr = ks[q] / nc, cc = ks[q] % nc;
+          out.row[sl + q] = rr;
+          out.col[sl + q] = cc;
+          out.value[sl + q] = im.at(rr, cc);
+          if (out.scale) out.scale[sl + q] = scale_tag;
+          if (out.pol) out.pol[sl + q] = (int8_t)q;
+          if (out.window) out.window[sl + q] = w;
+        }
+      }
+    }
+  }
+}
+
+// windows per task: at most 256 chunks of 16 columns, a multiple of 16 windows
+// (16-byte aligned chunk starts); a window row narrower than that is one task
+int strip_windows(int L, int wc) {
+  const int sw = std::max(16, (4096 / L) / 16 * 16);
+  return std::min(sw, (wc + 15) / 16 * 16);
+}
+
 template <class Img>
 int launch_strip(const Img& img, const ps_image_batch* ib, int B, int L, int wc, int nwin, const KpOut& ko,
                  int32_t* tmax, int32_t* tmin, cudaStream_t st) {
   using K = typename StripKeys<Img>::K;
-  const int wr_n = (img.nr + L - 1) / L, chunks = (img.nc + 15) / 16;
-  const size_t smem = 2 * (size_t)16 * chunks * sizeof(K);
-  const int threads = std::min(256, std::max(32, (chunks + 31) / 32 * 32));
+  if (L % 16 == 0 && L <= 256) {  // whole-chunk windows: the shuffle kernel
+    const int wr_n = (img.nr + L - 1) / L;
+    const int G = L / 16, R = std::max(1, std::min(L / 32, 32 / G));  // G * R lanes per window, <= 32 rows each
+    const int W = 32 / (G * R);
+    const int64_t warps = (int64_t)B * wr_n * ((wc + W - 1) / W);
+    const int grid = (int)std::min<int64_t>((warps + 7) / 8, 148 * 24);
+    detect_strip16<Img><<<grid, 256, 0, st>>>(img, ib->image_stride, B, L, G, R, wr_n, wc, nwin, tmax, tmin, ko,
+                                              L);
+    PS_LAUNCHED("detect_strip16");
+    return PS_OK;
+  }
+  const int wr_n = (img.nr + L - 1) / L;
+  const int SW = strip_windows(L, wc), nseg = (wc + SW - 1) / SW;
+  const size_t smem = 2 * (size_t)SW * L * sizeof(K);
+  const int chunks = std::min((SW * L + 15) / 16, (img.nc + 15) / 16);
+  const int threads = std::min(StripKeys<Img>::kMaxThreads, (chunks + 31) / 32 * 32);
   cudaFuncSetAttribute(detect_strip<Img>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int64_t tasks = (int64_t)B * wr_n;
-  const int grid = (int)std::min<int64_t>(tasks, 148 * 16);
-  detect_strip<Img><<<grid, threads, smem, st>>>(img, ib->image_stride, B, L, wr_n, wc, nwin, tmax, tmin, ko, L);
+  const int64_t tasks = (int64_t)B * wr_n * nseg;
+  const int grid = (int)std::min<int64_t>(tasks, 148 * 32);
+  detect_strip<Img><<<grid, threads, smem, st>>>(img, ib->image_stride, B, L, wr_n, wc, nwin, SW, nseg, tmax, tmin,
+                                                 ko, L);
   PS_LAUNCHED("detect_strip");
   return PS_OK;
 }
 
 // strip kernel preconditions: 16-byte aligned rows and images, rows of at
 // most 2^16 (row index in the key), column keys within the shared memory
-bool strip_ok(const ps_image_batch* ib, int L, int key_bytes) {
+bool strip_ok(const ps_image_batch* ib, int L, int key_bytes, int max_rows) {
   const int64_t bpp = ib->pixel_type == PS_PIXELS_RGB8 ? 3 : 1;
   const bool aligned = ((uintptr_t)ib->data) % 16 == 0 && (ib->row_pitch * bpp) % 16 == 0 &&
                        (ib->image_stride * bpp) % 16 == 0;
-  const size_t smem = 2 * (size_t)16 * ((ib->nc + 15) / 16) * key_bytes;
-  return aligned && L < 65536 && smem <= 200 * 1024;
+  const int wc = (ib->nc + L - 1) / L;
+  const size_t smem = 2 * (size_t)strip_windows(L, wc) * L * key_bytes;
+  return aligned && L <= max_rows && smem <= 200 * 1024;
 }
 
 // ---- general emission (several scales and/or dedupe) ------------------------
@@ -530,7 +742,7 @@ int launch_key(const Img&, const ps_image_batch*, int, int, int, int, bool, cons
 // the rows are 16-byte aligned, else the generic warp-per-window kernel.
 int launch_key(const RampRGB8& img, const ps_image_batch* ib, int B, int L, int wc, int nwin, bool,
                const KpOut& ko, int32_t* tmax, int32_t* tmin, cudaStream_t st) {
-  if (strip_ok(ib, L, 8)) return launch_strip(img, ib, B, L, wc, nwin, ko, tmax, tmin, st);
+  if (strip_ok(ib, L, 4, StripKeys<RampRGB8>::kMaxRows)) return launch_strip(img, ib, B, L, wc, nwin, ko, tmax, tmin, st);
   window_extrema_warp<0><<<grid_for((int64_t)B * nwin, 8), 256, 0, st>>>(img, ib->image_stride, B, L, wc, nwin,
                                                                            tmax, tmin, ko, L);
   PS_LAUNCHED("window_extrema_warp<rgb key>");
@@ -546,7 +758,7 @@ int launch_key(const RampU8& img, const ps_image_batch* ib, int B, int L, int wc
     detect_u8_w8<<<(unsigned)((th + 255) / 256), 256, 0, st>>>(img, ib->image_stride, B, wr_n, wc_n, ppr, ko, tmax,
                                                                 tmin);
     PS_LAUNCHED("detect_u8_w8");
-  } else if (strip_ok(ib, L, 4)) {
+  } else if (strip_ok(ib, L, 4, StripKeys<RampU8>::kMaxRows)) {
     return launch_strip(img, ib, B, L, wc, nwin, ko, tmax, tmin, st);
   } else {
     window_extrema_warp<0><<<grid_for((int64_t)B * nwin, 8), 256, 0, st>>>(img, ib->image_stride, B, L, wc, nwin,
