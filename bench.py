@@ -985,8 +985,10 @@ def run_ours(args):
             "unit": "GB/s", "frac": round(ach_des / peak, 4), "traffic": traffic,
             "peak_source": peak_kind, "kernel_ms": round(des_ms, 4),
             "algorithmic_bytes_per_launch": bytes_desc,
-            "note": "describe is issue-bound (float64 geometry and magnitudes, float32 angle screens, shared "
-                    "atomics), not HBM-bound; bytes = 1 B/px + 16 B/kp in + 512 B/kp out",
+            "note": "describe is bound by the L1 / shared-memory pipe (74 % of its wavefront peak: staged "
+                    "float64 boxes, bilinear gathers, histogram atomics) and instruction issue (66 %), not by HBM or "
+                    "the FP64 pipe (fp64_pipe below); bytes = 1 B/px + 16 B/kp in + 512 B/kp out "
+                    "(profiles/r02_ncu_details_describe_pair.csv)",
             "ncu": ncu_full}
     kernels = {"detect_u8_w8": {"ms": round(det_ms, 4), "GB/s": round(ach_det, 1),
                                 "frac_hbm": round(ach_det / peak, 4), "bytes_per_launch": bytes_detect},
@@ -1053,7 +1055,9 @@ def run_ours(args):
             fj = json.load(f)
         if int(fj.get("images", -1)) == n:
             ach = fj["fp64_flops_per_launch"] / (des_ms / 1e3) / 1e12
+            ops = fj["fp64_thread_ops_per_launch"] / (des_ms / 1e3) / 1e12  # DADD / DMUL / DFMA each one pipe op
             roof["fp64_pipe"].update({"achieved_tflops": round(ach, 2), "frac": round(ach / fp64["tflops"], 4),
+                                      "pipe_ops_frac": round(ops / (fp64["tflops"] / 2), 4),
                                       "fp64_flops_per_launch": fj["fp64_flops_per_launch"],
                                       "source": fj.get("source")})
 
