@@ -159,12 +159,21 @@ PS_API int ps_describe(const ps_image_batch* img, const ps_keypoints* kp, int32_
                 const int32_t* host_scale_set, int32_t n_scale_set, double beta0, int32_t d,
                 int32_t l_max, int32_t orientation_normalize, float* out_desc32,
                 double* out_desc64, void* stream);
-/* ps_describe with an explicit kernel policy (tests / A-B measurements; the
- * descriptors agree to float64 rounding under every policy):
- * PS_DESCRIBE_AUTO as ps_describe; PS_DESCRIBE_GENERAL the general float64
- * kernel for every keypoint; PS_DESCRIBE_SINGLE the one-keypoint-per-warp
- * fast kernel instead of the two-keypoints-per-warp one (w = 8). */
-enum ps_describe_policy { PS_DESCRIBE_AUTO = 0, PS_DESCRIBE_GENERAL = 1, PS_DESCRIBE_SINGLE = 2 };
+/* ps_describe with an explicit kernel policy (tests / A-B measurements):
+ * PS_DESCRIBE_AUTO as ps_describe: when only out_desc32 is requested, w = 8
+ * keypoints (d = 4) of 8-bit rasters run the float32 throughput kernel
+ * (descriptors ~1e-7 relative from the reference's float64 ones, every
+ * orientation-bin decision certified or taken in float64), everything else
+ * the float64 kernels (~1e-14); PS_DESCRIBE_PRECISE the float64 kernels for
+ * every keypoint; PS_DESCRIBE_GENERAL the general float64 kernel for every
+ * keypoint; PS_DESCRIBE_SINGLE the one-keypoint-per-warp float64 fast kernel
+ * instead of the two-keypoints-per-warp one (w = 8). */
+enum ps_describe_policy {
+  PS_DESCRIBE_AUTO = 0,
+  PS_DESCRIBE_GENERAL = 1,
+  PS_DESCRIBE_SINGLE = 2,
+  PS_DESCRIBE_PRECISE = 3
+};
 PS_API int ps_describe_ex(const ps_image_batch* img, const ps_keypoints* kp, int32_t default_scale,
                 const int32_t* host_scale_set, int32_t n_scale_set, double beta0, int32_t d,
                 int32_t l_max, int32_t orientation_normalize, float* out_desc32,

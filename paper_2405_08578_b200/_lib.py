@@ -20,7 +20,7 @@ PS_PIXELS_U8, PS_PIXELS_F64, PS_PIXELS_F64_RAW, PS_PIXELS_RGB8 = 0, 1, 2, 3
 ABI_VERSION = 4
 PS_MATCH_NEAREST, PS_MATCH_THRESHOLD_ALL, PS_MATCH_RATIO = 0, 1, 2
 PS_MATCH_FORCE_EXACT, PS_MATCH_FORCE_TC = 0x100, 0x200  # per-call path selection (OR-ed into the strategy)
-PS_DESCRIBE_AUTO, PS_DESCRIBE_GENERAL, PS_DESCRIBE_SINGLE = 0, 1, 2
+PS_DESCRIBE_AUTO, PS_DESCRIBE_GENERAL, PS_DESCRIBE_SINGLE, PS_DESCRIBE_PRECISE = 0, 1, 2, 3
 
 
 class ImageBatch(C.Structure):

@@ -203,7 +203,7 @@ def detect(images, scales, *, alpha=None, dedupe=True, ramped=False, meta=True, 
 
 
 DESCRIBE_POLICIES = {"auto": _lib.PS_DESCRIBE_AUTO, "general": _lib.PS_DESCRIBE_GENERAL,
-                     "single": _lib.PS_DESCRIBE_SINGLE}
+                     "single": _lib.PS_DESCRIBE_SINGLE, "precise": _lib.PS_DESCRIBE_PRECISE}
 
 
 def describe(images, kp: Keypoints, cfg, *, alpha=None, ramped=False, scale_set=None, out64=False,
@@ -232,15 +232,16 @@ def describe(images, kp: Keypoints, cfg, *, alpha=None, ramped=False, scale_set=
     return d64 if out64 else d32
 
 
-def describe_into(images, kp: Keypoints, cfg, out32: torch.Tensor, *, scale_set=None, stream=None) -> None:
+def describe_into(images, kp: Keypoints, cfg, out32: torch.Tensor, *, scale_set=None, stream=None,
+                  policy: str = "auto") -> None:
     """As ``describe`` into a preallocated float32 [B, cap, D] buffer (no allocation)."""
     im = images if isinstance(images, DeviceImages) else as_device_images(images)
     sset = [int(s) for s in (scale_set or kp.scale_set or (kp.default_scale,))]
     ib, kc = im.c_struct(), kp.c_struct()
-    _lib.check(_lib.lib().ps_describe(C.byref(ib), C.byref(kc), int(kp.default_scale), _lib.int32_array(sset),
-                                      len(sset), float(cfg.beta0), int(cfg.d), int(cfg.l_max),
-                                      int(bool(cfg.orientation_normalize)), _ptr(out32), None,
-                                      C.c_void_p(_stream_ptr(stream))), "describe")
+    _lib.check(_lib.lib().ps_describe_ex(C.byref(ib), C.byref(kc), int(kp.default_scale), _lib.int32_array(sset),
+                                         len(sset), float(cfg.beta0), int(cfg.d), int(cfg.l_max),
+                                         int(bool(cfg.orientation_normalize)), _ptr(out32), None,
+                                         DESCRIBE_POLICIES[policy], C.c_void_p(_stream_ptr(stream))), "describe")
 
 
 # ---------------------------------------------------------------------------
