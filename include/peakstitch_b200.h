@@ -174,6 +174,12 @@ enum ps_describe_policy {
   PS_DESCRIBE_SINGLE = 2,
   PS_DESCRIBE_PRECISE = 3
 };
+/* OR-ed into `policy`: the caller vouches that keypoint slots 2w / 2w+1 hold
+ * the max / min of window w of the default scale's row-major window grid --
+ * what ps_detect writes when dedupe leaves one evaluated scale (a nested
+ * scale set).  A performance hint only: keypoints that are not where it says
+ * are still described correctly, by the float64 kernel. */
+#define PS_DESCRIBE_WINDOW_SLOTS 0x100
 PS_API int ps_describe_ex(const ps_image_batch* img, const ps_keypoints* kp, int32_t default_scale,
                 const int32_t* host_scale_set, int32_t n_scale_set, double beta0, int32_t d,
                 int32_t l_max, int32_t orientation_normalize, float* out_desc32,

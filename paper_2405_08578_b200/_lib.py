@@ -21,6 +21,7 @@ ABI_VERSION = 4
 PS_MATCH_NEAREST, PS_MATCH_THRESHOLD_ALL, PS_MATCH_RATIO = 0, 1, 2
 PS_MATCH_FORCE_EXACT, PS_MATCH_FORCE_TC = 0x100, 0x200  # per-call path selection (OR-ed into the strategy)
 PS_DESCRIBE_AUTO, PS_DESCRIBE_GENERAL, PS_DESCRIBE_SINGLE, PS_DESCRIBE_PRECISE = 0, 1, 2, 3
+PS_DESCRIBE_WINDOW_SLOTS = 0x100  # include/peakstitch_b200.h: slots follow the default scale's window grid
 
 
 class ImageBatch(C.Structure):

@@ -1084,11 +1084,45 @@ __global__ void __launch_bounds__(kPairWarps * 32, 3) describe_pair_kernel(Img i
                                                                            float* __restrict__ out32,
                                                                            double* __restrict__ out64,
                                                                            int64_t* __restrict__ work,
-                                                                           unsigned long long* __restrict__ n_work) {
+                                                                           unsigned long long* __restrict__ n_work,
+                                                                           const int64_t* __restrict__ in_work,
+                                                                           const unsigned long long* __restrict__ in_n) {
   extern __shared__ double dsm[];
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, hsel = lane >> 4, hl = lane & 15;
   double* stage = dsm + (2 * wid + hsel) * FastStage::kTotal;
   unsigned* hw = reinterpret_cast<unsigned*>(dsm + 2 * kPairWarps * FastStage::kTotal) + (2 * wid + hsel) * kFastHist;
+  if (in_work) {  // the slots a previous kernel queued (float32 kernel: border keypoints, other sides)
+    const int64_t nin = (int64_t)*in_n;
+    for (int64_t pi = (int64_t)blockIdx.x * kPairWarps + wid; 2 * pi < nin; pi += (int64_t)gridDim.x * kPairWarps) {
+      const bool live = 2 * pi + hsel < nin;
+      const int64_t g = live ? in_work[2 * pi + hsel] : 0;
+      const int b = (int)(g / cap);
+      int row = live ? kp_row[g] : 8, col = live ? kp_col[g] : 8;
+      bool fast = live && img.nr >= FastStage::kBox && img.nc >= FastStage::kBox && row >= 0 && row < img.nr &&
+                  col >= 0 && col < img.nc;
+      if (fast) {
+        if (kp_scale) {
+          const int scale = kp_scale[g];
+          bool f = false;
+          for (int k = 0; k < prm.n_w8; ++k) f |= prm.w8_scale[k] == scale;
+          fast = f;
+        } else {
+          fast = prm.default_w8;
+        }
+      }
+      if (!__any_sync(0xffffffffu, fast)) {
+        if (live && hl == 0) work[atomicAdd(n_work, 1ull)] = g;
+        continue;
+      }
+      Img im = img;
+      im.p = img.p + (int64_t)(fast ? b : 0) * img_stride * decltype(img)::kElem;
+      if (!fast) { row = 8; col = 8; }
+      const bool ok = describe_pair_w8<ORIENT>(im, row, col, fast, prm, hw, stage,
+                                               out32 ? out32 + g * 128 : nullptr, out64 ? out64 + g * 128 : nullptr);
+      if (live && !ok && hl == 0) work[atomicAdd(n_work, 1ull)] = g;
+    }
+    return;
+  }
   const int64_t total = (int64_t)B * cap;
   const int64_t npairs = (total + 1) / 2;
   const bool box_ok = img.nr >= FastStage::kBox && img.nc >= FastStage::kBox;
@@ -1140,7 +1174,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, 3) describe_pair_kernel(Img i
 template <class Img>
 int launch_fast(const Img& im, const ps_image_batch* img, const ps_keypoints* kp, int32_t default_scale,
                 const DescParams& prm, float* out_desc32, double* out_desc64, int64_t total, size_t shmem,
-                int policy, cudaStream_t s) {
+                int policy, bool window_slots, cudaStream_t s) {
   if (policy == PS_DESCRIBE_GENERAL) {  // the general kernel for every keypoint
     int64_t blocks = (total + kWarps - 1) / kWarps;
     if (blocks > 148 * 8) blocks = 148 * 8;
@@ -1175,8 +1209,31 @@ int launch_fast(const Img& im, const ps_image_batch* img, const ps_keypoints* kp
   const bool f32 = policy == PS_DESCRIBE_AUTO && out_desc64 == nullptr && out_desc32 != nullptr && prm.d == 4 &&
                    prm.n_w8 > 0;
   if (f32) {
-    int st2 = launch_describe_f32(im, img, kp, prm, out_desc32, work, n_work, s);
+    // float32 kernel -> its queue (border keypoints, other sides) through the
+    // float64 pair kernel -> what that queues through the general kernel
+    int st2 = launch_describe_f32(im, img, kp, default_scale, prm, out_desc32, window_slots, work, n_work, s);
     if (st2) return st2;
+    int64_t* work2 = nullptr;
+    cudaMallocAsync(&work2, (size_t)total * sizeof(int64_t) + 16, s);
+    st2 = check_cuda("cudaMallocAsync(describe work list 2)");
+    if (st2) return st2;
+    unsigned long long* n_work2 = reinterpret_cast<unsigned long long*>(work2 + total);
+    cudaMemsetAsync(n_work2, 0, sizeof(unsigned long long), s);
+    const size_t pshmem =
+        (size_t)2 * kPairWarps * (FastStage::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
+    auto kern = prm.orient ? describe_pair_kernel<true, Img> : describe_pair_kernel<false, Img>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pshmem);
+    kern<<<148 * 3, kPairWarps * 32, pshmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col, kp->scale,
+                                                  kp->count, kp->cap, prm, out_desc32, out_desc64, work2, n_work2,
+                                                  work, n_work);
+    PS_LAUNCHED("describe_pair_kernel(queued)");
+    describe_kernel<Img><<<148 * 2, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,
+                                                             kp->scale, default_scale, kp->count, kp->cap, prm,
+                                                             out_desc32, out_desc64, work2, n_work2);
+    PS_LAUNCHED("describe_kernel(queued)");
+    cudaFreeAsync(work2, s);
+    cudaFreeAsync(work, s);
+    return check_cuda("cudaFreeAsync");
   } else if (prm.n_w8 == 0 && prm.n_w16 > 0) {  // w = 16 scales only (e.g. the default 32..128 windows)
     const size_t fshmem = (size_t)kFastWarps * (FastBox<16>::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
     cudaFuncSetAttribute(describe_fast_u8<16, Img>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fshmem);
@@ -1195,7 +1252,7 @@ int launch_fast(const Img& im, const ps_image_batch* img, const ps_keypoints* kp
     if (pblocks > 148 * PS_PAIR_BLOCKS_PER_SM) pblocks = 148 * PS_PAIR_BLOCKS_PER_SM;
     kern<<<(unsigned)pblocks, kPairWarps * 32, pshmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,
                                                              kp->scale, kp->count, kp->cap, prm, out_desc32,
-                                                             out_desc64, work, n_work);
+                                                             out_desc64, work, n_work, nullptr, nullptr);
     PS_LAUNCHED("describe_pair_kernel");
   } else {
     const size_t fshmem = (size_t)kFastWarps * (FastStage::kTotal * sizeof(double) + kFastHist * sizeof(unsigned));
@@ -1228,6 +1285,8 @@ extern "C" int ps_describe_ex(const ps_image_batch* img, const ps_keypoints* kp,
                               int32_t policy, void* stream) {
   PS_REQUIRE(img && kp && img->data && kp->row && kp->col && host_scale_set, PS_ERR_ARGUMENT,
              "null argument to ps_describe");
+  const bool window_slots = (policy & PS_DESCRIBE_WINDOW_SLOTS) != 0;
+  policy &= ~PS_DESCRIBE_WINDOW_SLOTS;
   PS_REQUIRE(policy == PS_DESCRIBE_AUTO || policy == PS_DESCRIBE_GENERAL || policy == PS_DESCRIBE_SINGLE ||
                  policy == PS_DESCRIBE_PRECISE,
              PS_ERR_ARGUMENT, "unknown describe policy %d", policy);
@@ -1317,11 +1376,13 @@ extern "C" int ps_describe_ex(const ps_image_batch* img, const ps_keypoints* kp,
   cudaFuncSetAttribute(describe_kernel<RampF64Raw>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
   if (img->pixel_type == PS_PIXELS_U8) {
     RampU8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
-    return launch_fast(im, img, kp, default_scale, prm, out_desc32, out_desc64, total, shmem, policy, s);
+    return launch_fast(im, img, kp, default_scale, prm, out_desc32, out_desc64, total, shmem, policy, window_slots,
+                       s);
   } else if (img->pixel_type == PS_PIXELS_RGB8) {
     RampRGB8 im{(const uint8_t*)img->data, img->row_pitch, img->nr, img->nc, img->alpha, img->gray_lut};
     cudaFuncSetAttribute(describe_kernel<RampRGB8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem);
-    return launch_fast(im, img, kp, default_scale, prm, out_desc32, out_desc64, total, shmem, policy, s);
+    return launch_fast(im, img, kp, default_scale, prm, out_desc32, out_desc64, total, shmem, policy, window_slots,
+                       s);
   } else if (img->pixel_type == PS_PIXELS_F64_RAW) {
     RampF64Raw im{(const double*)img->data, img->row_pitch, img->nr, img->nc, img->alpha};
     describe_kernel<<<(unsigned)blocks, kWarps * 32, shmem, s>>>(im, img->image_stride, img->batch, kp->row, kp->col,

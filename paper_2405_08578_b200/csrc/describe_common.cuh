@@ -134,11 +134,13 @@ __device__ __forceinline__ int exact_bin(double a, double b, double c0, double s
 }
 
 // Float32 throughput path (describe_f32.cu): every w = 8, d = 4 keypoint at
-// least 6 pixels inside an 8-bit (grey or RGB) image; everything else -- and
-// keypoints whose dominant orientation has no clear float32 lead -- is
-// appended to `work` for the float64 general kernel.  Writes float32 rows only.
+// least 6 pixels inside an 8-bit (grey or RGB) image; everything else is
+// appended to `work` for the float64 general kernel.  Writes float32 rows
+// only.  window_slots: the caller vouches for the window layout of the
+// default scale (PS_DESCRIBE_WINDOW_SLOTS); with L = 8 the tile kernel runs.
 template <class Img>
-int launch_describe_f32(const Img& im, const ps_image_batch* img, const ps_keypoints* kp, const DescParams& prm,
-                        float* out_desc32, int64_t* work, unsigned long long* n_work, cudaStream_t s);
+int launch_describe_f32(const Img& im, const ps_image_batch* img, const ps_keypoints* kp, int32_t default_scale,
+                        const DescParams& prm, float* out_desc32, bool window_slots, int64_t* work,
+                        unsigned long long* n_work, cudaStream_t s);
 
 }  // namespace ps

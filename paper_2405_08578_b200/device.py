@@ -139,6 +139,9 @@ class Keypoints:
     window: torch.Tensor | None = None
     default_scale: int = 0
     scale_set: tuple = ()
+    # window side L when slot 2w / 2w+1 is the max / min of window w of L's
+    # row-major grid (ps_detect with dedupe and one evaluated scale), else 0
+    window_slots: int = 0
 
     @property
     def cap(self) -> int:
@@ -167,6 +170,20 @@ class Keypoints:
         return out
 
 
+def _window_slots(sizes, dedupe) -> int:
+    """L_min when ps_detect evaluates only L_min (with dedupe, a scale that is
+    a multiple of a smaller one contributes only duplicates, csrc/detect.cu):
+    its output is then window w's max / min in slots 2w / 2w+1."""
+    s = sorted(sizes)
+    evaluated = [x for i, x in enumerate(s) if not any(x % y == 0 for y in s[:i])]
+    return s[0] if dedupe and evaluated == [s[0]] else 0
+
+
+def _describe_policy(policy: str, kp: "Keypoints") -> int:
+    flag = _lib.PS_DESCRIBE_WINDOW_SLOTS if (kp.window_slots and kp.window_slots == kp.default_scale) else 0
+    return DESCRIBE_POLICIES[policy] | flag
+
+
 def detect(images, scales, *, alpha=None, dedupe=True, ramped=False, meta=True, stream=None) -> Keypoints:
     """Multiscale window extrema of every image (detector.py:154-172).
 
@@ -193,6 +210,7 @@ def detect(images, scales, *, alpha=None, dedupe=True, ramped=False, meta=True, 
         window=torch.empty((B, K), dtype=torch.int32, device=dev) if meta else None,
         default_scale=sizes[0],
         scale_set=tuple(sizes),
+        window_slots=_window_slots(sizes, dedupe),
     )
     ws = _workspace(wsb.value, dev)
     ib, kc = im.c_struct(), kp.c_struct()
@@ -225,7 +243,7 @@ def describe(images, kp: Keypoints, cfg, *, alpha=None, ramped=False, scale_set=
     ib, kc = im.c_struct(), kp.c_struct()
     _lib.check(L.ps_describe_ex(C.byref(ib), C.byref(kc), int(kp.default_scale), _lib.int32_array(sset), len(sset),
                                 float(cfg.beta0), int(cfg.d), int(cfg.l_max), int(bool(cfg.orientation_normalize)),
-                                _ptr(d32), _ptr(d64), DESCRIBE_POLICIES[policy], C.c_void_p(_stream_ptr(stream))),
+                                _ptr(d32), _ptr(d64), _describe_policy(policy, kp), C.c_void_p(_stream_ptr(stream))),
                "describe")
     if out64 and out32:
         return d32, d64
@@ -241,7 +259,7 @@ def describe_into(images, kp: Keypoints, cfg, out32: torch.Tensor, *, scale_set=
     _lib.check(_lib.lib().ps_describe_ex(C.byref(ib), C.byref(kc), int(kp.default_scale), _lib.int32_array(sset),
                                          len(sset), float(cfg.beta0), int(cfg.d), int(cfg.l_max),
                                          int(bool(cfg.orientation_normalize)), _ptr(out32), None,
-                                         DESCRIBE_POLICIES[policy], C.c_void_p(_stream_ptr(stream))), "describe")
+                                         _describe_policy(policy, kp), C.c_void_p(_stream_ptr(stream))), "describe")
 
 
 # ---------------------------------------------------------------------------

@@ -209,3 +209,47 @@ def test_f32_kernel_batch_slots_and_counts():
         single = device.describe(t[b], kb, cfg, alpha=alpha)[0]
         n = int(kp.count[b])
         assert torch.equal(out[b, :n], single[:n]), b
+
+
+@pytest.mark.parametrize("nr,nc,batch", [(1600, 2688, 2), (203, 333, 3), (64, 72, 1), (37, 600, 2)])
+def test_f32_tile_kernel_equals_per_keypoint_kernel(nr, nc, batch):
+    """The L = 8 window-layout tile kernel (PS_DESCRIBE_WINDOW_SLOTS) and the
+    per-keypoint kernel compute the same float32 arithmetic: bit-identical rows,
+    partial tiles at the right / bottom edges included."""
+    import dataclasses
+
+    imgs = np.stack([scenes.scene(nr, nc, 20 + s) for s in range(batch)])
+    t = torch.from_numpy(imgs).cuda()
+    alpha = O.default_alpha(nr, nc)
+    cfg = R.DescriptorConfig(0.0625, 4, 128, True)
+    scales = tuple(s for s in (8, 16, 32, 64, 128) if s <= min(nr, nc))
+    kp = device.detect(t, scales, alpha=alpha, meta=False)
+    assert kp.window_slots == 8
+    tile = device.describe(t, kp, cfg, alpha=alpha)
+    box = device.describe(t, dataclasses.replace(kp, window_slots=0), cfg, alpha=alpha)
+    assert torch.equal(tile, box)
+    f64 = device.describe(t, kp, cfg, alpha=alpha, out64=True, out32=False)
+    for b in range(batch):
+        n = int(kp.count[b])
+        assert float(rel_err(tile[b, :n], f64[b, :n]).max()) <= F32_VS_F64
+
+
+def test_f32_tile_kernel_wrong_layout_still_correct():
+    """The window-layout flag is a hint: keypoints that are not in their window
+    (here: slots shuffled) are described by the float64 kernel, still right."""
+    import dataclasses
+
+    img = scenes.scene(400, 640, 9)
+    t = torch.from_numpy(img).cuda()
+    alpha = O.default_alpha(400, 640)
+    cfg = R.DescriptorConfig(0.0625, 4, 128, True)
+    kp = device.detect(t, (8, 16), alpha=alpha, meta=False)
+    n = int(kp.count[0])
+    perm = torch.randperm(n, generator=torch.Generator().manual_seed(0)).cuda()
+    shuffled = dataclasses.replace(kp, row=kp.row[:, :n][:, perm].contiguous(), col=kp.col[:, :n][:, perm].contiguous())
+    assert shuffled.window_slots == 8
+    got = device.describe(t, shuffled, cfg, alpha=alpha)
+    want = device.describe(t, dataclasses.replace(shuffled, window_slots=0), cfg, alpha=alpha)
+    f64 = device.describe(t, shuffled, cfg, alpha=alpha, out64=True, out32=False)
+    assert float(rel_err(got[0, :n], f64[0, :n]).max()) <= F32_VS_F64
+    assert float(rel_err(want[0, :n], f64[0, :n]).max()) <= F32_VS_F64
