@@ -79,6 +79,7 @@ constexpr float kBand = 2e-14f;      // the reference's own float64 rounding of 
 struct F32Params {
   float cA, cB;                  // ramp part of a / b: 2 nc alpha, 2 alpha
   float ks;                      // key -> grey scale: 1 (8-bit grey), 0.001 (RGB luma key 299 R + 587 G + 114 B)
+  int tab36;                     // 8-bit grey with a small ramp: axis-sample 36-bins from g_bin36 (exact)
   float ct[36], st[36];          // cos(-theta0_k), sin(-theta0_k) (descriptor.py:180)
   float ce36[37], se36[37];      // cos / sin of the 36-bin edges m 2 pi / 36 (descriptor.py:144)
   float ce8[36][9], se8[36][9];  // cos / sin of theta0_k + m pi / 4: 8-bin edges as absolute angles (:215, 244)
@@ -97,8 +98,27 @@ __device__ unsigned long long g_dbg_cnt[8];  // fb8 samples, fb8 special lines, 
 #define DBG_COUNT(i) ((void)0)
 #endif
 
+// 36-bin of an axis sample of an 8-bit grey raster within the quadrant:
+// g_bin36[|da| * 256 + |db|] = floor(atan2(|db|, |da|) / 10 degrees), da, db
+// the integer differences of a = da + 2 nc alpha, b = db + 2 alpha
+// (descriptor.py:135-138, 144).  The bin is exact, not a screen: no integer
+// pair with |da|, |db| <= 255 comes within 1.27e-3 (in gradient units) of a
+// non-axis 10-degree edge line (tests/test_host_logic.py checks all 2^16),
+// while the ramp moves a gradient by |(2 nc alpha, 2 alpha)| < 1e-3
+// (tab36's host condition) and the reference's rounding by ~1e-13; on the
+// axes the positive ramp decides (da = 0 < db: just below 90 degrees, bin 8;
+// db = 0: just above 0, bin 0).  Quadrants by the signs of a, b mirror it.
+__device__ uint8_t g_bin36[256 * 256];
+
 __global__ void init_geom8_kernel(DescParams prm) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int e = t; e < 256 * 256; e += gridDim.x * blockDim.x) {
+    const int da = e >> 8, db = e & 255;
+    int bin = 0;
+    if (da == 0 && db > 0) bin = 8;
+    else if (db > 0) bin = (int)floor(atan2((double)db, (double)da) * (36.0 / (2.0 * M_PI)));
+    g_bin36[e] = (uint8_t)bin;
+  }
   if (t >= 36 * 64) return;
   const int k = t >> 6, j = (t >> 4) & 3, l = t & 15;
   const int iv = 2 * (l >> 2) + (j >> 1), iu = 2 * (l & 3) + (j & 1);
@@ -470,12 +490,23 @@ __device__ __forceinline__ void describe_kp(const Img& im, const float2* Fc, con
     // ---- dominant orientation: 36-bin histogram of the axis region (descriptor.py:142-146)
     float mg[4];
     unsigned bins = 0u, unc = 0u;
+    constexpr bool kU8 = std::is_same<Img, RampU8>::value;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const float2 f = Fc[axis_off(j)];
       const float a = fmaf(f.x, ks, cA), bb = fmaf(f.y, ks, cB);
-      const float x = wrap_two_pi_f(atan2_f32(bb, a)) * 5.729577951308232f;
       int bin;
+      if (kU8 && fp.tab36) {
+        // exact table bin: |da|, |db| from the float bits (|d| + 2^23), quadrant from the signs of a, b
+        const unsigned ia = __float_as_uint(fabsf(f.x) + 8388608.0f), ib = __float_as_uint(fabsf(f.y) + 8388608.0f);
+        const int t = __ldg(g_bin36 + __byte_perm(ib, ia, 0x2240));  // |da| << 8 | |db|
+        const bool na = a < 0.0f, nb = bb < 0.0f;
+        bin = nb ? (na ? 18 + t : 35 - t) : (na ? 17 - t : t);
+        bins |= (unsigned)bin << (8 * j);
+        mg[j] = sqrt_approx(fmaf(a, a, bb * bb));
+        continue;
+      }
+      const float x = wrap_two_pi_f(atan2_f32(bb, a)) * 5.729577951308232f;
       if (!cert_bin(x, 36, bin)) {
         // at the axis edges 0, 90, 180, 270 degrees one component's sign decides
         // exactly (sd = b cos e - a sin e with cos, sin in {0, +-1})
@@ -577,42 +608,34 @@ __device__ __forceinline__ void describe_kp(const Img& im, const float2* Fc, con
 #pragma unroll
   for (int j = 0; j < 4; ++j) h8[32 * ((obs >> (8 * j)) & 255u)] += mg2[j];
   // ---- L2 normalise, clamp at 0.2, renormalise (descriptor.py:250-255); lane = bins 8 hl .. 8 hl + 7
-  float v[8];
+  float2 p[4];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) v[k] = h8[32 * k];
-  float sa = v[0] * v[0], sb = v[1] * v[1];
+  for (int k = 0; k < 4; ++k) p[k] = make_float2(h8[64 * k], h8[64 * k + 32]);
+  float2 q2 = __fmul2_rn(p[0], p[0]);
 #pragma unroll
-  for (int t = 2; t < 8; t += 2) {
-    sa = fmaf(v[t], v[t], sa);
-    sb = fmaf(v[t + 1], v[t + 1], sb);
-  }
-  float ss = sa + sb;
+  for (int k = 1; k < 4; ++k) q2 = __ffma2_rn(p[k], p[k], q2);
+  float ss = q2.x + q2.y;
 #pragma unroll
   for (int o = 8; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  if (ss > 0.0f) {
-    const float r1 = rsqrtf(ss);
-    float s2a = 0.0f, s2b = 0.0f;
+  const float r1 = ss > 0.0f ? rsqrtf(ss) : 0.0f;  // a flat (all-zero) histogram stays zero
 #pragma unroll
-    for (int t = 0; t < 8; t += 2) {
-      v[t] = fminf(v[t] * r1, 0.2f);
-      v[t + 1] = fminf(v[t + 1] * r1, 0.2f);
-      s2a = fmaf(v[t], v[t], s2a);
-      s2b = fmaf(v[t + 1], v[t + 1], s2b);
-    }
-    float s2 = s2a + s2b;
-#pragma unroll
-    for (int o = 8; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-    const float r2 = rsqrtf(s2);
-#pragma unroll
-    for (int t = 0; t < 8; ++t) v[t] *= r2;
-  } else {
-#pragma unroll
-    for (int t = 0; t < 8; ++t) v[t] = 0.0f;
+  for (int k = 0; k < 4; ++k) {
+    p[k] = __fmul2_rn(p[k], make_float2(r1, r1));
+    p[k] = make_float2(fminf(p[k].x, 0.2f), fminf(p[k].y, 0.2f));
   }
+  q2 = __fmul2_rn(p[0], p[0]);
+#pragma unroll
+  for (int k = 1; k < 4; ++k) q2 = __ffma2_rn(p[k], p[k], q2);
+  float s2 = q2.x + q2.y;
+#pragma unroll
+  for (int o = 8; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  const float r2 = ss > 0.0f ? rsqrtf(s2) : 0.0f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) p[k] = __fmul2_rn(p[k], make_float2(r2, r2));
   if (ok) {
     float4* d = reinterpret_cast<float4*>(out32 + g * 128) + 2 * hl;
-    d[0] = make_float4(v[0], v[1], v[2], v[3]);
-    d[1] = make_float4(v[4], v[5], v[6], v[7]);
+    d[0] = make_float4(p[0].x, p[0].y, p[1].x, p[1].y);
+    d[1] = make_float4(p[2].x, p[2].y, p[3].x, p[3].y);
   }
   if (live && !ok && hl == 0) work[atomicAdd(n_work, 1ull)] = g;  // border keypoints, other region sides
 }
@@ -703,6 +726,40 @@ __global__ void __launch_bounds__(kF32Warps * 32, PS_F32_MINB)
   }
 }
 
+constexpr int kChunksPerThread = (kTPR * (kTPC / 8) + kF32Warps * 32 - 1) / (kF32Warps * 32);
+// The 8-byte pixel chunks of tile task `task` this thread stages: chunk q =
+// row q / (kTPC / 8) (image row R0 - 6 + r), 8 columns from C0 - 8 + 8 k;
+// pixels outside the image read as 0 (no interior keypoint's fields use them).
+__device__ __forceinline__ void load_tile_chunks(const RampU8& img, int64_t img_stride, int nr, int nc, int pitch,
+                                                 int64_t task, int tiles, int tcn, int tid,
+                                                 uint2 (&pre)[kChunksPerThread]) {
+  const int b = (int)(task / tiles), t = (int)(task - (int64_t)b * tiles);
+  const int tr = t / tcn, tc = t - tr * tcn;
+  const int R0 = tr * kTR * 8, C0 = tc * kTC * 8;
+  const uint8_t* ip = img.p + (int64_t)b * img_stride;
+#pragma unroll
+  for (int u = 0; u < kChunksPerThread; ++u) {
+    const int q = tid + u * kF32Warps * 32;
+    const int r = q / (kTPC / 8), k = q - r * (kTPC / 8);
+    const int gr = R0 - 6 + r, gc = C0 - 8 + 8 * k;
+    uint2 w = make_uint2(0u, 0u);
+    if (q < kTPR * (kTPC / 8) && gr >= 0 && gr < nr) {
+      if (gc >= 0 && gc + 8 <= nc) {
+        w = __ldg(reinterpret_cast<const uint2*>(ip + gr * pitch + gc));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (gc + i >= 0 && gc + i < nc) {
+            const unsigned by = __ldg(ip + gr * pitch + gc + i);
+            if (i < 4) w.x |= by << (8 * i);
+            else w.y |= by << (8 * (i - 4));
+          }
+      }
+    }
+    pre[u] = w;
+  }
+}
+
 // The window layout of L = 8 (ps_detect of a nested scale set with dedupe:
 // slots 2w, 2w+1 = max, min of window w, row-major): a block stages the
 // fields of a tile of kTR x kTC windows with coalesced 8-byte loads, then
@@ -730,31 +787,28 @@ __global__ void __launch_bounds__(kF32Warps * 32, PS_F32_MINB)
   const int trn = (nwr + kTR - 1) / kTR, tcn = (ncw + kTC - 1) / kTC;
   const int tiles = trn * tcn;
   const int64_t ntask = (int64_t)B * tiles;
+  uint2 pre[kChunksPerThread];
+  if (blockIdx.x < ntask) load_tile_chunks(img, img_stride, nr, nc, pitch, blockIdx.x, tiles, tcn, tid, pre);
   for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
     const int b = (int)(task / tiles), t = (int)(task - (int64_t)b * tiles);
     const int tr = t / tcn, tc = t - tr * tcn;
     const int R0 = tr * kTR * 8, C0 = tc * kTC * 8;
     const uint8_t* ip = img.p + (int64_t)b * img_stride;
-    // ---- pixels -> float keys (exact), 8-byte chunks; outside the image: 0 (no interior keypoint reads them)
-    for (int q = tid; q < kTPR * (kTPC / 8); q += kF32Warps * 32) {
-      const int r = q / (kTPC / 8), k = q - r * (kTPC / 8);
-      const int gr = R0 - 6 + r, gc = C0 - 8 + 8 * k;
-      float v[8];
-      if (gr >= 0 && gr < nr && gc >= 0 && gc + 8 <= nc) {
-        const uint2 w = __ldg(reinterpret_cast<const uint2*>(ip + gr * pitch + gc));
+    // ---- pixels -> float keys (exact): this task's chunks were loaded during the previous task's rounds
+#pragma unroll
+    for (int u = 0; u < kChunksPerThread; ++u) {
+      const int q = tid + u * kF32Warps * 32;
+      if (q < kTPR * (kTPC / 8)) {
+        float v[8];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          v[i] = __uint_as_float(__byte_perm(w.x, 0x4Bu, 0x4550u + i)) - 8388608.0f;
-          v[4 + i] = __uint_as_float(__byte_perm(w.y, 0x4Bu, 0x4550u + i)) - 8388608.0f;
+          v[i] = __uint_as_float(__byte_perm(pre[u].x, 0x4Bu, 0x4550u + i)) - 8388608.0f;
+          v[4 + i] = __uint_as_float(__byte_perm(pre[u].y, 0x4Bu, 0x4550u + i)) - 8388608.0f;
         }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          v[i] = (gr >= 0 && gr < nr && gc + i >= 0 && gc + i < nc) ? u_to_f(__ldg(ip + gr * pitch + gc + i)) : 0.0f;
+        float4* d = reinterpret_cast<float4*>(px + q * 8);
+        d[0] = make_float4(v[0], v[1], v[2], v[3]);
+        d[1] = make_float4(v[4], v[5], v[6], v[7]);
       }
-      float4* d = reinterpret_cast<float4*>(px + r * kTPC + 8 * k);
-      d[0] = make_float4(v[0], v[1], v[2], v[3]);
-      d[1] = make_float4(v[4], v[5], v[6], v[7]);
     }
     __syncthreads();
     // ---- fields: a(fr, fc) = px[fr+2][fc+3] - px[fr][fc+3], b = px[fr+1][fc+4] - px[fr+1][fc+2]
@@ -773,6 +827,8 @@ __global__ void __launch_bounds__(kF32Warps * 32, PS_F32_MINB)
       }
     }
     __syncthreads();
+    // the next task's pixel chunks: their global latency overlaps this task's keypoints
+    if (task + gridDim.x < ntask) load_tile_chunks(img, img_stride, nr, nc, pitch, task + gridDim.x, tiles, tcn, tid, pre);
     // ---- the tile's 64 keypoints, 16 per round; the two halves of a warp take window w's max and min
 #pragma unroll
     for (int k = 0; k < 8; ++k) h8[32 * k] = 0.0f;
@@ -820,7 +876,7 @@ int ensure_geom8(const DescParams& prm, cudaStream_t s) {
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
   if (g_geom_ready.load() & bit) return PS_OK;
-  init_geom8_kernel<<<(36 * 64 + 255) / 256, 256, 0, s>>>(prm);
+  init_geom8_kernel<<<64, 256, 0, s>>>(prm);
   PS_LAUNCHED("init_geom8_kernel");
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(s, &cs);
@@ -833,6 +889,7 @@ void fill_f32_params(F32Params& fp, const ps_image_batch* img, const DescParams&
   fp.cA = (float)(2.0 * (double)img->nc * img->alpha);
   fp.cB = (float)(2.0 * img->alpha);
   fp.ks = img->pixel_type == PS_PIXELS_RGB8 ? 0.001f : 1.0f;
+  fp.tab36 = img->pixel_type == PS_PIXELS_U8 && std::hypot(2.0 * (double)img->nc * img->alpha, 2.0 * img->alpha) < 1e-3;
   for (int k = 0; k < 36; ++k) {
     fp.ct[k] = (float)prm.cos_t[k];
     fp.st[k] = (float)prm.sin_t[k];

@@ -200,3 +200,38 @@ def test_plan_and_stitch_argument_errors():
     with pytest.raises(ConfigError):
         plan_and_stitch([R.IntensityImage(rng.uniform(0, 255, (64, 64)), "same"),
                          R.IntensityImage(rng.uniform(0, 255, (64, 64)), "same")], cfg)
+
+
+def test_axis_sample_36bin_table_is_exact_for_8bit_gradients():
+    """csrc/describe_f32.cu g_bin36: for an 8-bit grey raster the axis-sample
+    gradient is (da + 2 nc alpha, db + 2 alpha) with integer |da|, |db| <= 255.
+    No such integer vector off the axes lies within 1.2e-3 (perpendicular
+    distance, gradient units) of a 10-degree bin edge line, so a ramp term
+    below 1e-3 cannot move it across one: the reference's bin is the table's.
+    On the axes the positive ramp decides (da = 0 < db -> bin 8, db = 0 -> 0)."""
+    import math
+
+    import numpy as np
+
+    p, q = np.meshgrid(np.arange(256, dtype=np.float64), np.arange(256, dtype=np.float64), indexing="ij")
+    off = (p > 0) & (q > 0)
+    edges = np.arange(10) * (2 * math.pi / 36)
+    # perpendicular distance of (p, q) to the line at angle e: |q cos e - p sin e|
+    dist = np.min(np.abs(q[..., None] * np.cos(edges) - p[..., None] * np.sin(edges)), axis=-1)
+    assert dist[off].min() > 1.2e-3
+    # table formula vs the reference's float64 arithmetic with a ramp, in all four quadrants
+    rng = np.random.default_rng(0)
+    tab = np.where((p == 0) & (q > 0), 8, np.floor(np.arctan2(q, p) * (36 / (2 * math.pi)))).astype(int)
+    tab[(p == 0) & (q == 0)] = 0
+    # (2 nc alpha, 2 alpha): C2, C4, a 13-column image at the 1e-3 limit (flat: atan(1 / nc) < 10 degrees)
+    for nc, alpha in [(2688, 5.93e-11), (8192, 3.8e-12), (13, 3.8e-5)]:
+        ca, cb = 2 * nc * alpha, 2 * alpha
+        da = rng.integers(-255, 256, 20000).astype(np.float64)
+        db = rng.integers(-255, 256, 20000).astype(np.float64)
+        da[:2000] = 0
+        db[2000:4000] = 0
+        a, b = da + ca, db + cb
+        want = np.minimum((np.mod(np.arctan2(b, a), 2 * math.pi) * (36 / (2 * math.pi))).astype(int), 35)
+        t = tab[np.abs(da).astype(int), np.abs(db).astype(int)]
+        got = np.where(b < 0, np.where(a < 0, 18 + t, 35 - t), np.where(a < 0, 17 - t, t))
+        assert np.array_equal(got, want), (ca, cb)
