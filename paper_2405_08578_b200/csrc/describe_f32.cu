@@ -530,27 +530,18 @@ __device__ __forceinline__ void describe_kp(const Img& im, const float2* Fc, con
     // q = rint(mag 2^(22 - e)) <= 2^23 for the half's largest magnitude < 2^(e + 1)
     const unsigned eb = half_max(__float_as_uint(fmaxf(fmaxf(mg[0], mg[1]), fmaxf(mg[2], mg[3]))), hsel) >> 23;
     const float s36 = eb == 0u ? 1.0f : __uint_as_float((unsigned)min(max(276 - (int)eb, 1), 254) << 23);
-    // A lane's samples usually share a bin (neighbours in one subregion): merge
-    // them first (fewer same-address atomics in smooth regions).
-    unsigned q[4], bj[4];
+    // A lane's four samples (one subregion) usually share a bin in smooth
+    // regions: then one atomic, else four.
+    unsigned q[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      q[j] = __float_as_uint(fmaf(mg[j], s36, 8388608.0f)) - 0x4B000000u;
-      bj[j] = (bins >> (8 * j)) & 255u;
+    for (int j = 0; j < 4; ++j) q[j] = __float_as_uint(fmaf(mg[j], s36, 8388608.0f)) - 0x4B000000u;
+    const unsigned b0 = bins & 255u;
+    if (bins == b0 * 0x01010101u) {
+      atomicAdd(h36 + b0, (q[0] + q[1]) + (q[2] + q[3]));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) atomicAdd(h36 + ((bins >> (8 * j)) & 255u), q[j]);
     }
-#pragma unroll
-    for (int j = 1; j < 4; ++j) {
-#pragma unroll
-      for (int i = 0; i < j; ++i) {
-        if (q[j] && bj[j] == bj[i]) {
-          q[i] += q[j];
-          q[j] = 0u;
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (q[j]) atomicAdd(h36 + bj[j], q[j]);
     __syncwarp();
     // argmax with a clear lead (the sums are < 1e-5 relative from the
     // reference's; keys: the sum with its low 6 bits replaced by 63 - bin)
@@ -585,7 +576,7 @@ __device__ __forceinline__ void describe_kp(const Img& im, const float2* Fc, con
   // ---- descriptor samples (rotated grid, descriptor.py:164-216; or the axis region, :241-242)
   float mg2[4];
   unsigned obs = 0u, unc2 = 0u;
-#pragma unroll
+#pragma unroll 2
   for (int j = 0; j < 4; ++j) {
     float2 err;
     const float2 gv = blend_sample<ORIENT, FS>(Fc, geom, hk, j, hl, axis_off(j), ks, cA, cB, err);
@@ -788,13 +779,13 @@ __global__ void __launch_bounds__(kF32Warps * 32, PS_F32_MINB)
   const int tiles = trn * tcn;
   const int64_t ntask = (int64_t)B * tiles;
   uint2 pre[kChunksPerThread];
-  if (blockIdx.x < ntask) load_tile_chunks(img, img_stride, nr, nc, pitch, blockIdx.x, tiles, tcn, tid, pre);
   for (int64_t task = blockIdx.x; task < ntask; task += gridDim.x) {
     const int b = (int)(task / tiles), t = (int)(task - (int64_t)b * tiles);
     const int tr = t / tcn, tc = t - tr * tcn;
     const int R0 = tr * kTR * 8, C0 = tc * kTC * 8;
     const uint8_t* ip = img.p + (int64_t)b * img_stride;
-    // ---- pixels -> float keys (exact): this task's chunks were loaded during the previous task's rounds
+    // ---- pixels -> float keys (exact)
+    load_tile_chunks(img, img_stride, nr, nc, pitch, task, tiles, tcn, tid, pre);
 #pragma unroll
     for (int u = 0; u < kChunksPerThread; ++u) {
       const int q = tid + u * kF32Warps * 32;
@@ -828,7 +819,7 @@ __global__ void __launch_bounds__(kF32Warps * 32, PS_F32_MINB)
     }
     __syncthreads();
     // the next task's pixel chunks: their global latency overlaps this task's keypoints
-    if (task + gridDim.x < ntask) load_tile_chunks(img, img_stride, nr, nc, pitch, task + gridDim.x, tiles, tcn, tid, pre);
+
     // ---- the tile's 64 keypoints, 16 per round; the two halves of a warp take window w's max and min
 #pragma unroll
     for (int k = 0; k < 8; ++k) h8[32 * k] = 0.0f;
@@ -836,8 +827,8 @@ __global__ void __launch_bounds__(kF32Warps * 32, PS_F32_MINB)
     __syncwarp();
 #pragma unroll 1
     for (int rd = 0; rd < kTR * kTC / kF32Warps; ++rd) {
-      const int wl = rd * kF32Warps + wid;
-      const int wr = tr * kTR + (wl / kTC), wc = tc * kTC + (wl % kTC);
+      static_assert(kTC == kF32Warps, "round rd: warp wid takes window (tile row rd, tile column wid)");
+      const int wr = tr * kTR + rd, wc = tc * kTC + wid;
       const int slot = 2 * (wr * ncw + wc) + hsel;
       const bool live = wr < nwr && wc < ncw && (!counts || slot < counts[b]);
       const int64_t g = (int64_t)b * cap + slot;
