@@ -9,14 +9,17 @@ detect + describe of the whole 64-image batch; metric Mpixel/s.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 * ``value``: device-resident inputs, CUDA events around exactly K steps,
-  barrier + synchronize on both sides, max over ranks.  Images are sharded
-  over ranks (strong scaling: 64 images in total, no collective on the data
+  barrier + synchronize on both sides, max over ranks.  Weak scaling: every
+  rank describes its own seeded 64-image batch (no collective on the data
   path).  The 275 MB input batch is larger than the 126 MB L2, so no flush.
 * ``e2e``: the same metric through the public host API
   (``pipeline.BatchPreparer``): pinned host images in, host keypoints and
   float32 descriptors out, H2D/D2H inside the timed region.
 * ``roofline``: the dominant kernel (describe) against measured HBM
-  bandwidth, plus the detect kernel, from CUDA events inside the timed run.
+  bandwidth (the contract's bound) and against instruction issue (what
+  bounds it: warp instructions per launch from the committed ncu capture over
+  the live time), plus the detect kernel, from CUDA events inside the timed
+  run; ``kernels.describe_precise_f64`` times the float64 kernels.
 * ``cpu_baseline``: the oracle port (oracle/lpsift_oracle.py, numpy, the
   reference's algorithm) on this host's cores, bounded sample, rank 0, N=1.
 * ``--impl reference``: times that CPU port as the reference arm.
@@ -991,25 +994,30 @@ def run_ours(args):
     if os.path.exists(tp):
         with open(tp) as f:
             tj = json.load(f)
-        tr = tj.get("describe_kernel")
+        tr = tj.get("describe")
         if tr and int(tr.get("images", -1)) == n:
             traffic = tr["dram_bytes_per_launch"]
             ncu_full = tr.get("ncu_full")
     ach_des = bytes_desc / (des_ms / 1e3) / 1e9
     ach_det = bytes_detect / (det_ms / 1e3) / 1e9
-    roof = {"bound": "hbm", "kernel": "describe_kernel", "achieved": round(ach_des, 1), "peak": peak,
+    roof = {"bound": "hbm", "kernel": "describe_f32_tile_kernel", "achieved": round(ach_des, 1), "peak": peak,
             "unit": "GB/s", "frac": round(ach_des / peak, 4), "traffic": traffic,
             "peak_source": peak_kind, "kernel_ms": round(des_ms, 4),
             "algorithmic_bytes_per_launch": bytes_desc,
-            "note": "describe is bound by the L1 / shared-memory pipe (74 % of its wavefront peak: staged "
-                    "float64 boxes, bilinear gathers, histogram atomics) and instruction issue (66 %), not by HBM or "
-                    "the FP64 pipe (fp64_pipe below); bytes = 1 B/px + 16 B/kp in + 512 B/kp out "
-                    "(profiles/r02_ncu_details_describe_pair.csv)",
+            "note": "describe (float32 tile kernel + the float64 kernels for the border keypoints it queues) is "
+                    "instruction-issue bound (issue below), not HBM-bound: bytes = 1 B/px + 16 B/kp in + "
+                    "512 B/kp out; DRAM traffic from ncu equals the algorithmic bytes",
             "ncu": ncu_full}
+    if ncu_full and ncu_full.get("warp_instructions"):
+        # instruction roofline: warp instructions per launch (ncu, same launch) over this run's time,
+        # against 4 issue slots per SM per clock at the sampled SM clock
+        clk_hz = None  # filled after the clock sampler has run (below)
+        roof["issue"] = {"warp_instructions_per_launch": ncu_full["warp_instructions"],
+                         "source": ncu_full.get("source")}
     kernels = {"detect_u8_w8": {"ms": round(det_ms, 4), "GB/s": round(ach_det, 1),
                                 "frac_hbm": round(ach_det / peak, 4), "bytes_per_launch": bytes_detect},
-               "describe_kernel": {"ms": round(des_ms, 4), "GB/s": round(ach_des, 1),
-                                   "keypoints_per_s": round(n_kp / (des_ms / 1e3), 1)}}
+               "describe": {"ms": round(des_ms, 4), "GB/s": round(ach_des, 1),
+                            "keypoints_per_s": round(n_kp / (des_ms / 1e3), 1)}}
 
     # detect alone, back to back (its inputs, 275 MB, exceed L2): the kernel's own roofline fraction,
     # without the write-back of the previous describe's dirty descriptor lines that it absorbs in the step
@@ -1063,19 +1071,29 @@ def run_ours(args):
     with_cpu = rank == 0 and world == 1 and not args.no_cpu
     if with_cpu:
         cpu = cpu_baseline(steps=1, warmup=0)
+    # the float64 kernels (PS_DESCRIBE_PRECISE; the path of float64-output calls such as the
+    # reference-facing describe_features): same batch, CUDA events, with the FP64-pipe peak probe
+    pe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    device.describe_into(dimg, kp, cfg, desc, scale_set=kp.scale_set, policy="precise")
+    pe[0].record(stream)
+    for _ in range(3):
+        device.describe_into(dimg, kp, cfg, desc, scale_set=kp.scale_set, policy="precise")
+    pe[1].record(stream)
+    torch.cuda.synchronize()
     fp64 = fp64_probe(dev)
-    roof["fp64_pipe"] = {"peak_tflops_measured": fp64["tflops"], "probe": fp64["how"]}
-    tj = os.path.join(REPO, "profiles", "describe_fp64.json")
-    if os.path.exists(tj):  # FP64 FLOPs per launch from an ncu capture of the same launch (committed)
-        with open(tj) as f:
-            fj = json.load(f)
-        if int(fj.get("images", -1)) == n:
-            ach = fj["fp64_flops_per_launch"] / (des_ms / 1e3) / 1e12
-            ops = fj["fp64_thread_ops_per_launch"] / (des_ms / 1e3) / 1e12  # DADD / DMUL / DFMA each one pipe op
-            roof["fp64_pipe"].update({"achieved_tflops": round(ach, 2), "frac": round(ach / fp64["tflops"], 4),
-                                      "pipe_ops_frac": round(ops / (fp64["tflops"] / 2), 4),
-                                      "fp64_flops_per_launch": fj["fp64_flops_per_launch"],
-                                      "source": fj.get("source")})
+    kernels["describe_precise_f64"] = {
+        "ms": round(pe[0].elapsed_time(pe[1]) / 3, 4), "fp64_peak_tflops_measured": fp64["tflops"],
+        "probe": fp64["how"],
+        "note": "float64 kernels (describe_pair_kernel + describe_kernel), ~1e-14 from the reference; "
+                "the headline float32 kernel is ~1e-7 (P2 bar 1e-4)"}
+
+    if "issue" in roof:
+        mhz = (clocks or {}).get("sm_mhz") or 1965.0
+        peak_issue = 148 * 4 * mhz * 1e6  # warp instructions per second, all SMs
+        ach = roof["issue"]["warp_instructions_per_launch"] / (des_ms / 1e3)
+        roof["issue"].update({"achieved_per_s": round(ach, 1), "peak_per_s": round(peak_issue, 1),
+                              "frac": round(ach / peak_issue, 4), "sm_mhz": mhz,
+                              "note": "4 warp-instruction issue slots per SM per clock (148 SMs)"})
 
     latency = None
     if not args.no_stitch:
