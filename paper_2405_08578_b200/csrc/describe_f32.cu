@@ -772,6 +772,9 @@ __global__ void __launch_bounds__(kF32Warps * 32, PS_F32_MINB)
   float* h8 = hw + lane;
   unsigned* h36 = reinterpret_cast<unsigned*>(hw + kH8W + hsel * kH36);
   unsigned* scr = reinterpret_cast<unsigned*>(hw + hsel * (kH8W / 2));
+  int* kpr = reinterpret_cast<int*>(sm + kTileF);  // the tile's keypoints: row, column, slot / flags
+  int* kpc = kpr + 2 * kTR * kTC;
+  int* kpf = kpc + 2 * kTR * kTC;
   const float4* __restrict__ geom = g_geom8[1];
   const int nr = img.nr, nc = img.nc, pitch = (int)img.pitch;
   const int nwr = (nr + 7) >> 3, ncw = (nc + 7) >> 3;
@@ -784,6 +787,21 @@ __global__ void __launch_bounds__(kF32Warps * 32, PS_F32_MINB)
     const int tr = t / tcn, tc = t - tr * tcn;
     const int R0 = tr * kTR * 8, C0 = tc * kTC * 8;
     const uint8_t* ip = img.p + (int64_t)b * img_stride;
+    const int64_t gb = (int64_t)b * cap;
+    // ---- the tile's 64 keypoints, once: keypoint k (round k / 16, warp k / 2 % 8, half k % 2) is
+    //      window (tr * kTR + k / 16, tc * kTC + k / 2 % 8)'s max (k even) / min; slot << 2 | live << 1 | fast
+    if (tid < 2 * kTR * kTC) {
+      const int wr = tr * kTR + (tid >> 4), wc = tc * kTC + ((tid >> 1) & 7);
+      const int slot = 2 * (wr * ncw + wc) + (tid & 1);
+      const bool live = wr < nwr && wc < ncw && (!counts || slot < counts[b]);
+      const int row = live ? kp_row[gb + slot] : 0, col = live ? kp_col[gb + slot] : 0;
+      const bool fast = live && row >= wr * 8 && row < wr * 8 + 8 && col >= wc * 8 && col < wc * 8 + 8 &&
+                        row >= 6 && row <= nr - 7 && col >= 6 && col <= nc - 7 && prm.default_w8;
+      if (live && !fast) work[atomicAdd(n_work, 1ull)] = gb + slot;  // border keypoints, other layouts
+      kpr[tid] = row;
+      kpc[tid] = col;
+      kpf[tid] = slot << 2 | (live ? 2 : 0) | (fast ? 1 : 0);
+    }
     // ---- pixels -> float keys (exact)
     load_tile_chunks(img, img_stride, nr, nc, pitch, task, tiles, tcn, tid, pre);
 #pragma unroll
@@ -826,27 +844,24 @@ __global__ void __launch_bounds__(kF32Warps * 32, PS_F32_MINB)
     if (hl < kH36 / 4) reinterpret_cast<uint4*>(h36)[hl] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
 #pragma unroll 1
-    for (int rd = 0; rd < kTR * kTC / kF32Warps; ++rd) {
+    for (int rd = 0; rd < kTR; ++rd) {
       static_assert(kTC == kF32Warps, "round rd: warp wid takes window (tile row rd, tile column wid)");
-      const int wr = tr * kTR + rd, wc = tc * kTC + wid;
-      const int slot = 2 * (wr * ncw + wc) + hsel;
-      const bool live = wr < nwr && wc < ncw && (!counts || slot < counts[b]);
-      const int64_t g = (int64_t)b * cap + slot;
-      int row = live ? kp_row[g] : 0, col = live ? kp_col[g] : 0;
-      const bool in_win = row >= wr * 8 && row < wr * 8 + 8 && col >= wc * 8 && col < wc * 8 + 8;
-      bool fast = live && in_win && row >= 6 && row <= nr - 7 && col >= 6 && col <= nc - 7 && prm.default_w8;
-      if (!__any_sync(0xffffffffu, fast)) {
-        if (live && hl == 0) work[atomicAdd(n_work, 1ull)] = g;
-        continue;
+      const int k = rd * 16 + 2 * wid + hsel;
+      const int f = kpf[k];
+      const bool fast = f & 1;
+      if (!__any_sync(0xffffffffu, fast)) continue;
+      int row = kpr[k], col = kpc[k];
+      // a half without a fast keypoint shadows its partner's (same window): in the image and the tile
+      const int prow = __shfl_xor_sync(0xffffffffu, row, 16), pcol = __shfl_xor_sync(0xffffffffu, col, 16);
+      if (!fast) {
+        row = prow;
+        col = pcol;
       }
-      if (!fast) {  // dummy keypoint inside the tile: the half-warp stays in step, nothing is written
-        row = max(R0 + 6, 6);
-        col = max(C0 + 6, 6);
-      }
+      const int64_t g = gb + (f >> 2);
       RampU8 im = img;
       im.p = ip;
       const float2* Fc = F + (row - (R0 - 5)) * kTFS + (col - (C0 - 5));
-      describe_kp<ORIENT, kTFS>(im, Fc, geom, row, col, fast, live, g, h8, h36, scr, hl, hsel, fp, prm, out32,
+      describe_kp<ORIENT, kTFS>(im, Fc, geom, row, col, fast, fast, g, h8, h36, scr, hl, hsel, fp, prm, out32,
                                 work, n_work);
       __syncwarp();
 #pragma unroll
@@ -923,7 +938,7 @@ int launch_describe_f32(const Img& im, const ps_image_batch* img, const ps_keypo
                     (img->batch == 1 || img->image_stride % 8 == 0);
   if constexpr (std::is_same<Img, RampU8>::value) {
     if (tile) {
-      const size_t shm = (size_t)kTileF * sizeof(float);
+      const size_t shm = (size_t)kTileF * sizeof(float) + 3 * 2 * kTR * kTC * sizeof(int);
       auto kern = prm.orient ? describe_f32_tile_kernel<true> : describe_f32_tile_kernel<false>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
       const int nwr = (img->nr + 7) / 8, ncw = (img->nc + 7) / 8;
