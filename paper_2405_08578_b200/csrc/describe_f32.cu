@@ -775,6 +775,7 @@ __global__ void __launch_bounds__(kF32Warps * 32, PS_F32_MINB)
   int* kpr = reinterpret_cast<int*>(sm + kTileF);  // the tile's keypoints: row, column, slot / flags
   int* kpc = kpr + 2 * kTR * kTC;
   int* kpf = kpc + 2 * kTR * kTC;
+  int* kctr = kpf + 2 * kTR * kTC;  // next window of the tile to describe
   const float4* __restrict__ geom = g_geom8[1];
   const int nr = img.nr, nc = img.nc, pitch = (int)img.pitch;
   const int nwr = (nr + 7) >> 3, ncw = (nc + 7) >> 3;
@@ -790,6 +791,7 @@ __global__ void __launch_bounds__(kF32Warps * 32, PS_F32_MINB)
     const int64_t gb = (int64_t)b * cap;
     // ---- the tile's 64 keypoints, once: keypoint k (round k / 16, warp k / 2 % 8, half k % 2) is
     //      window (tr * kTR + k / 16, tc * kTC + k / 2 % 8)'s max (k even) / min; slot << 2 | live << 1 | fast
+    if (tid == 0) *kctr = 0;
     if (tid < 2 * kTR * kTC) {
       const int wr = tr * kTR + (tid >> 4), wc = tc * kTC + ((tid >> 1) & 7);
       const int slot = 2 * (wr * ncw + wc) + (tid & 1);
@@ -843,10 +845,15 @@ __global__ void __launch_bounds__(kF32Warps * 32, PS_F32_MINB)
     for (int k = 0; k < 8; ++k) h8[32 * k] = 0.0f;
     if (hl < kH36 / 4) reinterpret_cast<uint4*>(h36)[hl] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
+    // windows are claimed dynamically (a warp whose keypoints take a rare path
+    // does not hold the block's next barrier while the others idle)
 #pragma unroll 1
-    for (int rd = 0; rd < kTR; ++rd) {
-      static_assert(kTC == kF32Warps, "round rd: warp wid takes window (tile row rd, tile column wid)");
-      const int k = rd * 16 + 2 * wid + hsel;
+    for (;;) {
+      int wl = 0;
+      if (lane == 0) wl = atomicAdd(kctr, 1);
+      wl = __shfl_sync(0xffffffffu, wl, 0);
+      if (wl >= kTR * kTC) break;
+      const int k = 2 * wl + hsel;
       const int f = kpf[k];
       const bool fast = f & 1;
       if (!__any_sync(0xffffffffu, fast)) continue;
@@ -938,7 +945,7 @@ int launch_describe_f32(const Img& im, const ps_image_batch* img, const ps_keypo
                     (img->batch == 1 || img->image_stride % 8 == 0);
   if constexpr (std::is_same<Img, RampU8>::value) {
     if (tile) {
-      const size_t shm = (size_t)kTileF * sizeof(float) + 3 * 2 * kTR * kTC * sizeof(int);
+      const size_t shm = (size_t)kTileF * sizeof(float) + (3 * 2 * kTR * kTC + 4) * sizeof(int);
       auto kern = prm.orient ? describe_f32_tile_kernel<true> : describe_f32_tile_kernel<false>;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
       const int nwr = (img->nr + 7) / 8, ncw = (img->nc + 7) / 8;
