@@ -97,6 +97,19 @@ constexpr size_t smem_bytes() {
 // max that propagates NaN (its bits order above +inf as unsigned)
 __device__ __forceinline__ float nan_max(float a, float b) { return (b != b || b > a) ? b : a; }
 
+// This lane's four elements (lane * 4 .. + 3) of a 128-wide row, one vector load.
+template <class T>
+__device__ __forceinline__ void load4(const T* __restrict__ row, int lane, double (&x)[4]) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(row) + lane);
+    x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+  } else {
+    const double2 v0 = __ldg(reinterpret_cast<const double2*>(row) + 2 * lane);
+    const double2 v1 = __ldg(reinterpret_cast<const double2*>(row) + 2 * lane + 1);
+    x[0] = v0.x; x[1] = v0.y; x[2] = v1.x; x[3] = v1.y;
+  }
+}
+
 template <class T>
 __global__ void prep_tiles(const T* __restrict__ src, const int32_t* __restrict__ idx,
                            const int32_t* __restrict__ count_p, int64_t count_const, int64_t n_pad, int R,
@@ -111,9 +124,8 @@ __global__ void prep_tiles(const T* __restrict__ src, const int32_t* __restrict_
        u += (int64_t)gridDim.x * (blockDim.x >> 5)) {
     const bool live = u < count;
     const int64_t s = live ? (idx ? (int64_t)idx[u] : u) : 0;
-    double x[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) x[e] = live ? (double)src[s * KD + lane * 4 + e] : 0.0;
+    double x[4] = {0.0, 0.0, 0.0, 0.0};
+    if (live) load4(src + s * KD, lane, x);
     __half h[4];
     double sx = 0.0, sr = 0.0, sh = 0.0;
 #pragma unroll
@@ -529,12 +541,25 @@ __global__ void certify_exact(const float* __restrict__ topv, const int32_t* __r
     int tj[TOPK];
 #pragma unroll
     for (int q = 0; q < TOPK; ++q) { tv[q] = INFINITY; tj[q] = -1; }
-    for (int l = 0; l < n_lists; ++l)  // the 4 smallest of the per-split lists are the global top-4
+    for (int l = 0; l < n_lists; ++l) {  // the 4 smallest of the per-split lists are the global top-4
+      float lv[TOPK];
+      int lj[TOPK];
+      if constexpr (TOPK == 4) {
+        const float4 v4 = __ldg(reinterpret_cast<const float4*>(topv + ((int64_t)l * nx_pad + uu) * TOPK));
+        const int4 j4 = __ldg(reinterpret_cast<const int4*>(topj + ((int64_t)l * nx_pad + uu) * TOPK));
+        lv[0] = v4.x; lv[1] = v4.y; lv[2] = v4.z; lv[3] = v4.w;
+        lj[0] = j4.x; lj[1] = j4.y; lj[2] = j4.z; lj[3] = j4.w;
+      } else {
 #pragma unroll
-      for (int q = 0; q < TOPK; ++q) {
-        const float v = topv[((int64_t)l * nx_pad + uu) * TOPK + q];
-        if (v < tv[TOPK - 1]) topk_insert(v, topj[((int64_t)l * nx_pad + uu) * TOPK + q], tv, tj);
+        for (int q = 0; q < TOPK; ++q) {
+          lv[q] = topv[((int64_t)l * nx_pad + uu) * TOPK + q];
+          lj[q] = topj[((int64_t)l * nx_pad + uu) * TOPK + q];
+        }
       }
+#pragma unroll
+      for (int q = 0; q < TOPK; ++q)
+        if (lv[q] < tv[TOPK - 1]) topk_insert(lv[q], lj[q], tv, tj);
+    }
     const double lim = (double)tv[0] + 2.0 * E;
     const bool over = (double)tv[TOPK - 1] <= lim;  // candidates may extend past the top-4
     if (live && over && t == 0) {
@@ -693,10 +718,13 @@ __global__ void hash_insert(const T* __restrict__ X, int64_t n, unsigned long lo
        i += (int64_t)gridDim.x * (blockDim.x >> 5)) {
     unsigned long long h = 0;
     bool same_as_prev = i > 0;  // a run of identical rows: only its first row competes for the minimum
+    double xv[4], pv[4];
+    load4(X + i * KD, lane, xv);
+    if (i > 0) load4(X + (i - 1) * KD, lane, pv);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const T v = X[i * KD + lane * 4 + e];
-      if (i > 0) same_as_prev &= v == X[(i - 1) * KD + lane * 4 + e];
+      const T v = (T)xv[e];
+      if (i > 0) same_as_prev &= xv[e] == pv[e];
       unsigned long long bits;
       if (sizeof(T) == 8) bits = (unsigned long long)__double_as_longlong((double)v);
       else bits = (unsigned long long)__float_as_uint((float)v);
@@ -737,8 +765,11 @@ __global__ void mark_reps_table(const T* __restrict__ X, int64_t n, const int32_
     const int l = tidx[slot_of[i]];
     bool same = true;
     if (l != (int)i) {
+      double a[4], c[4];
+      load4(X + i * KD, lane, a);
+      load4(X + (int64_t)l * KD, lane, c);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) same &= X[i * KD + lane * 4 + e] == X[(int64_t)l * KD + lane * 4 + e];
+      for (int e = 0; e < 4; ++e) same &= a[e] == c[e];
       same = __all_sync(0xffffffffu, same);
     }
     if (lane == 0) {
@@ -986,14 +1017,21 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   // column within their certified limit on the tensor cores, then decide exactly
   gather_rows<<<grid_for(nx_max, 256), 256, 0, st>>>(w.overflow, w.n_overflow, x_idx, w.xsrc);
   PS_LAUNCHED("gather_rows");
-  prep_tiles<T><<<grid_for(xrows, 8), 256, 0, st>>>(X, w.xsrc, w.n_overflow, 0, xrows, BMH, w.xt, w.xinfo, nullptr, 0, BM);
-  PS_LAUNCHED("prep_tiles(overflow)");
+  // operand tiles of the overflow rows: the enumeration reads at most the
+  // first kEnumBlocksAsync row blocks without a host count (async), all of
+  // them with one (sync; rows beyond take the exact scan either way)
+  const int64_t n_over = sync ? read_count(w.n_overflow, st) : -1;
+  const int64_t over_rows = sync ? rup(n_over, BM) : std::min<int64_t>(xrows, (int64_t)kEnumBlocksAsync * BM);
+  if (over_rows > 0) {
+    prep_tiles<T><<<grid_for(over_rows, 8), 256, 0, st>>>(X, w.xsrc, w.n_overflow, 0, over_rows, BMH, w.xt, w.xinfo,
+                                                          nullptr, 0, BM);
+    PS_LAUNCHED("prep_tiles(overflow)");
+  }
   cudaMemsetAsync(w.n_pairs, 0, sizeof(unsigned long long), st);
   cudaMemsetAsync(w.best_bits, 0xff, nx_max * sizeof(unsigned long long), st);
   cudaMemsetAsync(w.best_j, 0x7f, nx_max * sizeof(int32_t), st);
   int enum_rows = INT32_MAX;
   if (sync) {
-    const int64_t n_over = read_count(w.n_overflow, st);
     g_stats[3] += n_over;
     if (n_over > 0) {
       g_stats[5] += (int64_t)tc_grid(n_over, ny).x * ((ny + BN - 1) / BN) * flops_tile;
