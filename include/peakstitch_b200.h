@@ -210,6 +210,27 @@ PS_API int ps_match_async(const void* desc1, int64_t n1, const void* desc2, int6
                    int32_t* out_ref2, double* out_delta, int64_t* out_count, int64_t cap,
                    void* workspace, size_t workspace_bytes, void* stream);
 
+/* Many nearest_neighbor matches in one launch sequence: pair q matches
+ * descriptor set pair_a[q] against set pair_b[q] (the pairwise-table loop,
+ * mosaic.py:79-112, calling match_features, matcher.py:57-95, per pair).
+ * set_desc: host array of n_sets device pointers to [set_rows[s], 128]
+ * row-major float32 (desc_is_f64 = 0) or float64 rows; pair_a / pair_b: host
+ * int32 arrays of n_pairs set indices.  Each set's duplicate grouping and
+ * tensor-core operand tiles are built once however many pairs it enters, and
+ * every stage runs as one launch for all pairs.  Pair q's matches, sorted by
+ * (delta, ref1, ref2), go to row q of out_ref1 / out_ref2 / out_delta (device
+ * [n_pairs, out_stride], out_stride >= min(set_rows[a], set_rows[b]) for every
+ * pair) and its count to out_count[q] (device int64).  No host
+ * synchronisation (capturable); results equal ps_match's pair by pair.
+ * Limits: dim = 128, n_sets <= 512, n_pairs <= 256. */
+PS_API int ps_match_batch_plan(int32_t n_sets, const int64_t* set_rows, int32_t n_pairs, int32_t dim,
+                               size_t* workspace_bytes_out);
+PS_API int ps_match_batch_async(int32_t n_sets, const void* const* set_desc, const int64_t* set_rows,
+                                int32_t n_pairs, const int32_t* pair_a, const int32_t* pair_b, int32_t dim,
+                                int32_t desc_is_f64, double delta_s, int32_t* out_ref1, int32_t* out_ref2,
+                                double* out_delta, int64_t out_stride, int64_t* out_count, void* workspace,
+                                size_t workspace_bytes, void* stream);
+
 /* One direction of nearest_neighbor matching: out_index[i] / out_dist[i] =
  * the exact first argmin over the rows of Y of the reference distance to row
  * i of X (matcher.py:74 with _distance_matrix :48-54).  The building block of

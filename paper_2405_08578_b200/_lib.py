@@ -72,6 +72,12 @@ SIGNATURES = {
                                  C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                  C.c_void_p, C.c_size_t, C.c_void_p]),
     "ps_pair_points": (C.c_int, [C.c_void_p] * 9 + [C.c_int64, C.c_void_p]),
+    "ps_match_batch_plan": (C.c_int, [C.c_int32, C.POINTER(C.c_int64), C.c_int32, C.c_int32,
+                                      C.POINTER(C.c_size_t)]),
+    "ps_match_batch_async": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_int32,
+                                       C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int32, C.c_int32,
+                                       C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                       C.c_void_p, C.c_size_t, C.c_void_p]),
     "ps_match_stats": (C.c_int, [C.POINTER(C.c_int64), C.c_int32]),
     "ps_nearest_plan": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]),
     "ps_nearest": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32,

@@ -111,7 +111,7 @@ __device__ __forceinline__ void load4(const T* __restrict__ row, int lane, doubl
 }
 
 template <class T>
-__global__ void prep_tiles(const T* __restrict__ src, const int32_t* __restrict__ idx,
+__device__ __forceinline__ void prep_tiles_body(const T* __restrict__ src, const int32_t* __restrict__ idx,
                            const int32_t* __restrict__ count_p, int64_t count_const, int64_t n_pad, int R,
                            uint8_t* __restrict__ tiles, double* __restrict__ info, unsigned* __restrict__ maxes,
                            int is_y, int align) {
@@ -200,6 +200,14 @@ __global__ void prep_tiles(const T* __restrict__ src, const int32_t* __restrict_
     if (m != 0.0f) atomicMax(maxes + threadIdx.x, __float_as_uint(m));
   }
 }
+template <class T>
+__global__ void prep_tiles(const T* __restrict__ src, const int32_t* __restrict__ idx,
+                           const int32_t* __restrict__ count_p, int64_t count_const, int64_t n_pad, int R,
+                           uint8_t* __restrict__ tiles, double* __restrict__ info, unsigned* __restrict__ maxes,
+                           int is_y, int align) {
+  prep_tiles_body<T>(src, idx, count_p, count_const, n_pad, R, tiles, info, maxes, is_y, align);
+}
+
 
 // ---- the tcgen05 row-minimum kernel --------------------------------------------------
 __device__ __forceinline__ void topk_insert(float v, int j, float (&tv)[TOPK], int (&tj)[TOPK]) {
@@ -220,7 +228,7 @@ __device__ __forceinline__ void topk_insert(float v, int j, float (&tv)[TOPK], i
 // share of the Y tiles; MODE 0 writes one top-4 list per (split, part) --
 // list index sp * kParts + part of row g at topv[(list * nx_pad + g) * TOPK].
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Yt,
+__device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Yt,
                                                           const int32_t* __restrict__ cnt_x,
                                                           const int32_t* __restrict__ cnt_y, float* __restrict__ topv,
                                                           int32_t* __restrict__ topj, const float* __restrict__ lim,
@@ -469,6 +477,16 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restrict__ Xt, const uint8_t* __restrict__ Yt,
+                                                          const int32_t* __restrict__ cnt_x,
+                                                          const int32_t* __restrict__ cnt_y, float* __restrict__ topv,
+                                                          int32_t* __restrict__ topj, const float* __restrict__ lim,
+                                                          unsigned long long* __restrict__ pairs,
+                                                          unsigned long long* __restrict__ n_pairs, int64_t cap) {
+  nn_topk_tc_body<MODE>(Xt, Yt, cnt_x, cnt_y, topv, topj, lim, pairs, n_pairs, cap);
+}
+
 
 // ---- certification + exact float64 recheck ------------------------------------------
 // Reference distance between float-typed rows a and b (numpy pairwise order).
@@ -511,7 +529,7 @@ __device__ __forceinline__ double exact_dist8(const T* __restrict__ a, const T* 
 // indices (ties break on original indices).  Writes nn[x_orig[u]] and d[...];
 // rows whose candidates may not fit the top-4 are appended to `overflow`.
 template <class T>
-__global__ void certify_exact(const float* __restrict__ topv, const int32_t* __restrict__ topj,
+__device__ __forceinline__ void certify_exact_body(const float* __restrict__ topv, const int32_t* __restrict__ topj,
                               const int32_t* __restrict__ cnt_x, const int32_t* __restrict__ x_orig,
                               const int32_t* __restrict__ y_orig, const double* __restrict__ xinfo,
                               const unsigned* __restrict__ ymax, const T* __restrict__ X, const T* __restrict__ Y,
@@ -610,19 +628,35 @@ __global__ void certify_exact(const float* __restrict__ topv, const int32_t* __r
     }
   }
 }
+template <class T>
+__global__ void certify_exact(const float* __restrict__ topv, const int32_t* __restrict__ topj,
+                              const int32_t* __restrict__ cnt_x, const int32_t* __restrict__ x_orig,
+                              const int32_t* __restrict__ y_orig, const double* __restrict__ xinfo,
+                              const unsigned* __restrict__ ymax, const T* __restrict__ X, const T* __restrict__ Y,
+                              int32_t* __restrict__ nn, double* __restrict__ dist, int32_t* __restrict__ overflow,
+                              int32_t* __restrict__ n_overflow, float* __restrict__ overflow_lim, int n_lists,
+                              int64_t nx_pad) {
+  certify_exact_body<T>(topv, topj, cnt_x, x_orig, y_orig, xinfo, ymax, X, Y, nn, dist, overflow, n_overflow, overflow_lim, n_lists, nx_pad);
+}
+
 
 // overflow row q -> source row of X (composition of the two index lists)
-__global__ void gather_rows(const int32_t* __restrict__ overflow, const int32_t* __restrict__ n_overflow,
+__device__ __forceinline__ void gather_rows_body(const int32_t* __restrict__ overflow, const int32_t* __restrict__ n_overflow,
                             const int32_t* __restrict__ x_idx, int32_t* __restrict__ out) {
   const int n = *n_overflow;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x)
     out[q] = x_idx ? x_idx[overflow[q]] : overflow[q];
 }
+__global__ void gather_rows(const int32_t* __restrict__ overflow, const int32_t* __restrict__ n_overflow,
+                            const int32_t* __restrict__ x_idx, int32_t* __restrict__ out) {
+  gather_rows_body(overflow, n_overflow, x_idx, out);
+}
+
 
 // exact distance of every enumerated (overflow row, column) pair; per row the
 // minimum distance bits, then the lowest original column at that distance
 template <class T>
-__global__ void pair_dist_min(const unsigned long long* __restrict__ pairs,
+__device__ __forceinline__ void pair_dist_min_body(const unsigned long long* __restrict__ pairs,
                               const unsigned long long* __restrict__ n_pairs, int64_t cap,
                               const int32_t* __restrict__ xsrc, const int32_t* __restrict__ y_idx,
                               const T* __restrict__ X, const T* __restrict__ Y, double* __restrict__ pd,
@@ -645,9 +679,18 @@ __global__ void pair_dist_min(const unsigned long long* __restrict__ pairs,
     }
   }
 }
+template <class T>
+__global__ void pair_dist_min(const unsigned long long* __restrict__ pairs,
+                              const unsigned long long* __restrict__ n_pairs, int64_t cap,
+                              const int32_t* __restrict__ xsrc, const int32_t* __restrict__ y_idx,
+                              const T* __restrict__ X, const T* __restrict__ Y, double* __restrict__ pd,
+                              unsigned long long* __restrict__ best_bits) {
+  pair_dist_min_body<T>(pairs, n_pairs, cap, xsrc, y_idx, X, Y, pd, best_bits);
+}
+
 
 template <class T>
-__global__ void pair_argmin(const unsigned long long* __restrict__ pairs, const unsigned long long* __restrict__ n_pairs,
+__device__ __forceinline__ void pair_argmin_body(const unsigned long long* __restrict__ pairs, const unsigned long long* __restrict__ n_pairs,
                             int64_t cap, const int32_t* __restrict__ y_idx, const double* __restrict__ pd,
                             const unsigned long long* __restrict__ best_bits, int* __restrict__ best_j) {
   const int64_t n = min((int64_t)*n_pairs, cap);
@@ -656,8 +699,15 @@ __global__ void pair_argmin(const unsigned long long* __restrict__ pairs, const 
     if ((unsigned long long)__double_as_longlong(pd[k]) == best_bits[q]) atomicMin(best_j + q, y_idx ? y_idx[jt] : jt);
   }
 }
+template <class T>
+__global__ void pair_argmin(const unsigned long long* __restrict__ pairs, const unsigned long long* __restrict__ n_pairs,
+                            int64_t cap, const int32_t* __restrict__ y_idx, const double* __restrict__ pd,
+                            const unsigned long long* __restrict__ best_bits, int* __restrict__ best_j) {
+  pair_argmin_body<T>(pairs, n_pairs, cap, y_idx, pd, best_bits, best_j);
+}
 
-__global__ void pair_write(const int32_t* __restrict__ n_overflow, const int32_t* __restrict__ xsrc,
+
+__device__ __forceinline__ void pair_write_body(const int32_t* __restrict__ n_overflow, const int32_t* __restrict__ xsrc,
                            const unsigned long long* __restrict__ best_bits, const int* __restrict__ best_j,
                            int32_t* __restrict__ nn, double* __restrict__ dist, int enum_rows) {
   const int n = min(*n_overflow, enum_rows);  // rows beyond were not enumerated (exact_rows decides them)
@@ -666,10 +716,16 @@ __global__ void pair_write(const int32_t* __restrict__ n_overflow, const int32_t
     dist[xsrc[q]] = __longlong_as_double((long long)best_bits[q]);
   }
 }
+__global__ void pair_write(const int32_t* __restrict__ n_overflow, const int32_t* __restrict__ xsrc,
+                           const unsigned long long* __restrict__ best_bits, const int* __restrict__ best_j,
+                           int32_t* __restrict__ nn, double* __restrict__ dist, int enum_rows) {
+  pair_write_body(n_overflow, xsrc, best_bits, best_j, nn, dist, enum_rows);
+}
+
 
 // exact full scans (only if the enumerated pairs overflowed their buffer)
 template <class T>
-__global__ void exact_rows(const int32_t* __restrict__ rows, const int32_t* __restrict__ n_rows,
+__device__ __forceinline__ void exact_rows_body(const int32_t* __restrict__ rows, const int32_t* __restrict__ n_rows,
                            const int32_t* __restrict__ x_orig, const T* __restrict__ X, const T* __restrict__ Y,
                            int64_t ny, int32_t* __restrict__ nn, double* __restrict__ dist,
                            const unsigned long long* __restrict__ n_pairs, int64_t cap, int enum_rows) {
@@ -706,12 +762,20 @@ __global__ void exact_rows(const int32_t* __restrict__ rows, const int32_t* __re
     __syncthreads();
   }
 }
+template <class T>
+__global__ void exact_rows(const int32_t* __restrict__ rows, const int32_t* __restrict__ n_rows,
+                           const int32_t* __restrict__ x_orig, const T* __restrict__ X, const T* __restrict__ Y,
+                           int64_t ny, int32_t* __restrict__ nn, double* __restrict__ dist,
+                           const unsigned long long* __restrict__ n_pairs, int64_t cap, int enum_rows) {
+  exact_rows_body<T>(rows, n_rows, x_orig, X, Y, ny, nn, dist, n_pairs, cap, enum_rows);
+}
+
 
 // ---- duplicate rows --------------------------------------------------------------------
 // Open-addressing table of row hashes (tsize a power of two, keys 0 = empty):
 // per hash the lowest row index.  slot_of[i] receives row i's slot.
 template <class T>
-__global__ void hash_insert(const T* __restrict__ X, int64_t n, unsigned long long* __restrict__ tkey,
+__device__ __forceinline__ void hash_insert_body(const T* __restrict__ X, int64_t n, unsigned long long* __restrict__ tkey,
                             int32_t* __restrict__ tidx, int64_t tsize, int32_t* __restrict__ slot_of) {
   const int lane = threadIdx.x & 31;
   for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
@@ -752,11 +816,17 @@ __global__ void hash_insert(const T* __restrict__ X, int64_t n, unsigned long lo
     }
   }
 }
+template <class T>
+__global__ void hash_insert(const T* __restrict__ X, int64_t n, unsigned long long* __restrict__ tkey,
+                            int32_t* __restrict__ tidx, int64_t tsize, int32_t* __restrict__ slot_of) {
+  hash_insert_body<T>(X, n, tkey, tidx, tsize, slot_of);
+}
+
 
 // rep[i] = the lowest row with row i's hash when bitwise equal to row i, else
 // i itself (a hash collision only splits a group); flag[i] = (rep == i).
 template <class T>
-__global__ void mark_reps_table(const T* __restrict__ X, int64_t n, const int32_t* __restrict__ tidx,
+__device__ __forceinline__ void mark_reps_table_body(const T* __restrict__ X, int64_t n, const int32_t* __restrict__ tidx,
                                 const int32_t* __restrict__ slot_of, int32_t* __restrict__ rep,
                                 int32_t* __restrict__ flag) {
   const int lane = threadIdx.x & 31;
@@ -779,6 +849,13 @@ __global__ void mark_reps_table(const T* __restrict__ X, int64_t n, const int32_
     }
   }
 }
+template <class T>
+__global__ void mark_reps_table(const T* __restrict__ X, int64_t n, const int32_t* __restrict__ tidx,
+                                const int32_t* __restrict__ slot_of, int32_t* __restrict__ rep,
+                                int32_t* __restrict__ flag) {
+  mark_reps_table_body<T>(X, n, tidx, slot_of, rep, flag);
+}
+
 
 __global__ void copy_from_rep(const int32_t* __restrict__ rep, int64_t n, int32_t* __restrict__ nn,
                               double* __restrict__ dist) {
@@ -797,7 +874,7 @@ __global__ void iota32(int32_t* v, int64_t n) {
 }
 
 // columns worth checking: nn12 of rows with d < delta_s
-__global__ void mark_columns(const int32_t* __restrict__ a_uniq, const int32_t* __restrict__ n_auniq,
+__device__ __forceinline__ void mark_columns_body(const int32_t* __restrict__ a_uniq, const int32_t* __restrict__ n_auniq,
                              const int32_t* __restrict__ nn12, const double* __restrict__ d12, double delta_s,
                              int32_t* __restrict__ colflag) {
   const int n = *n_auniq;
@@ -806,9 +883,15 @@ __global__ void mark_columns(const int32_t* __restrict__ a_uniq, const int32_t* 
     if (d12[i] < delta_s) colflag[nn12[i]] = 1;
   }
 }
+__global__ void mark_columns(const int32_t* __restrict__ a_uniq, const int32_t* __restrict__ n_auniq,
+                             const int32_t* __restrict__ nn12, const double* __restrict__ d12, double delta_s,
+                             int32_t* __restrict__ colflag) {
+  mark_columns_body(a_uniq, n_auniq, nn12, d12, delta_s, colflag);
+}
+
 
 // acceptance over original rows (matcher.py:74-79); only representatives can be mutual
-__global__ void accept_pairs(const int32_t* __restrict__ a_rep, int64_t n1, const int32_t* __restrict__ nn12,
+__device__ __forceinline__ void accept_pairs_body(const int32_t* __restrict__ a_rep, int64_t n1, const int32_t* __restrict__ nn12,
                              const double* __restrict__ d12, const int32_t* __restrict__ nn21, double delta_s,
                              unsigned long long* __restrict__ keys_pair, unsigned long long* __restrict__ keys_delta,
                              unsigned long long* __restrict__ counter) {
@@ -822,6 +905,13 @@ __global__ void accept_pairs(const int32_t* __restrict__ a_rep, int64_t n1, cons
     }
   }
 }
+__global__ void accept_pairs(const int32_t* __restrict__ a_rep, int64_t n1, const int32_t* __restrict__ nn12,
+                             const double* __restrict__ d12, const int32_t* __restrict__ nn21, double delta_s,
+                             unsigned long long* __restrict__ keys_pair, unsigned long long* __restrict__ keys_delta,
+                             unsigned long long* __restrict__ counter) {
+  accept_pairs_body(a_rep, n1, nn12, d12, nn21, delta_s, keys_pair, keys_delta, counter);
+}
+
 
 // ---- host orchestration ------------------------------------------------------------
 struct Side {  // a descriptor matrix with its duplicate-row structure
@@ -1064,6 +1154,482 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   return PS_OK;
 }
 
+// ---- many pairs, one launch sequence ---------------------------------------------------
+// ps_match_batch_async: P (set a, set b) nearest_neighbor matches over S
+// descriptor sets as ONE sequence of ~35 launches (blockIdx.y / .z = pair, or
+// set for the per-set stages) instead of ~45 per pair.  Each set is hashed,
+// grouped and turned into operand tiles once however many pairs it enters (in
+// a 3 x 3 stitch every image is in 8 pairs): its X-form tiles serve the pairs'
+// row passes, its Y-form tiles both passes.  Per pair the stages are those of
+// nearest_pass in asynchronous mode, through the same kernel bodies, so every
+// pair's result equals ps_match_async's (the mosaic loop the batch replaces:
+// reference mosaic.py:79-112 calling match_features, matcher.py:57-95).
+constexpr int kBatchMaxSets = 512;
+constexpr int kBatchMaxPairs = 256;
+
+template <class T>
+struct BatchIn {  // kernel parameter (__grid_constant__): the sets and the pair list
+  const T* desc[kBatchMaxSets];
+  int32_t rows[kBatchMaxSets];
+  uint8_t role[kBatchMaxSets];  // bit 0: set a of some pair (X-form tiles), bit 1: set b of some pair
+  int16_t pa[kBatchMaxPairs], pb[kBatchMaxPairs];
+};
+
+struct BatchWs {  // uniform slots: set s / pair q at base + s (q) * stride
+  int64_t n, xrows, yrows, tsize, nchunk, lists, pair_cap, over_rows;
+  int32_t *slot_of, *rep, *flag, *uniq, *n_uniq, *sel_cnt;  // per set (sel_cnt: per set or pair)
+  unsigned long long* tkey;
+  int32_t* tidx;
+  uint8_t *xt, *yt;
+  double *xinfo, *yinfo;
+  unsigned* ymax;
+  float* topv;  // per pair from here
+  int32_t* topj;
+  int32_t *nn12, *nn21, *colflag, *cols, *n_cols, *overflow, *n_overflow, *xsrc, *best_j;
+  double *d12, *d21, *xinfo2, *xinfoo, *pd;
+  uint8_t *xt2, *xto;
+  float* lim;
+  unsigned long long *best_bits, *pairs, *n_pairs, *kp, *kd, *counter;
+};
+
+constexpr int kSelChunk = 2048;  // flags per selection CTA (256 threads x 8)
+
+BatchWs carve_batch(void* base, int64_t S, int64_t P, int64_t n, size_t* used) {
+  Arena ar{(char*)base, 0, 0};
+  BatchWs w{};
+  const int64_t N = std::max<int64_t>(n, 1);
+  w.n = N;
+  w.xrows = rup(N, BM);
+  w.yrows = rup(N, BN);
+  w.tsize = 64;
+  while (w.tsize < 2 * N) w.tsize <<= 1;
+  w.nchunk = (N + kSelChunk - 1) / kSelChunk;
+  w.lists = kParts * kMaxSplit;
+  w.pair_cap = std::max<int64_t>(1 << 16, 4 * N);
+  w.over_rows = std::min<int64_t>(w.xrows, (int64_t)kEnumBlocksAsync * BM);
+  w.slot_of = ar.take<int32_t>(S * N);
+  w.rep = ar.take<int32_t>(S * N);
+  w.flag = ar.take<int32_t>(S * N);
+  w.uniq = ar.take<int32_t>(S * N);
+  w.n_uniq = ar.take<int32_t>(S);
+  w.sel_cnt = ar.take<int32_t>(std::max(S, P) * w.nchunk);
+  w.tkey = ar.take<unsigned long long>(S * w.tsize);
+  w.tidx = ar.take<int32_t>(S * w.tsize);
+  w.xt = ar.take<uint8_t>(S * w.xrows * ROW_BYTES);
+  w.xinfo = ar.take<double>(S * 3 * w.xrows);
+  w.yt = ar.take<uint8_t>(S * w.yrows * ROW_BYTES);
+  w.yinfo = ar.take<double>(S * 3 * w.yrows);
+  w.ymax = ar.take<unsigned>(S * 4);
+  w.topv = ar.take<float>(P * w.lists * w.xrows * TOPK);
+  w.topj = ar.take<int32_t>(P * w.lists * w.xrows * TOPK);
+  w.nn12 = ar.take<int32_t>(P * N);
+  w.nn21 = ar.take<int32_t>(P * N);
+  w.colflag = ar.take<int32_t>(P * N);
+  w.cols = ar.take<int32_t>(P * N);
+  w.n_cols = ar.take<int32_t>(P);
+  w.overflow = ar.take<int32_t>(P * N);
+  w.n_overflow = ar.take<int32_t>(2 * P);
+  w.xsrc = ar.take<int32_t>(P * N);
+  w.best_j = ar.take<int32_t>(P * N);
+  w.d12 = ar.take<double>(P * N);
+  w.d21 = ar.take<double>(P * N);
+  w.xt2 = ar.take<uint8_t>(P * w.xrows * ROW_BYTES);
+  w.xinfo2 = ar.take<double>(P * 3 * w.xrows);
+  w.xto = ar.take<uint8_t>(P * w.over_rows * ROW_BYTES);
+  w.xinfoo = ar.take<double>(P * 3 * w.over_rows);
+  w.lim = ar.take<float>(P * w.xrows);
+  w.best_bits = ar.take<unsigned long long>(P * N);
+  w.pairs = ar.take<unsigned long long>(P * w.pair_cap);
+  w.pd = ar.take<double>(P * w.pair_cap);
+  w.n_pairs = ar.take<unsigned long long>(2 * P);
+  w.kp = ar.take<unsigned long long>(P * N);
+  w.kd = ar.take<unsigned long long>(P * N);
+  w.counter = ar.take<unsigned long long>(P);
+  *used = ar.used + 256;
+  return w;
+}
+
+template <class T>
+struct PassView {  // pair q in pass 0 (distinct rows of a vs b) or 1 (matchable columns of b vs a)
+  const T *X, *Y;
+  const int32_t *x_idx, *n_x, *y_idx, *n_y;
+  const uint8_t *xt, *yt;
+  const double* xinfo;
+  const unsigned* ymax;
+  int32_t* nn;
+  double* dist;
+  int64_t ny;
+};
+
+template <class T>
+__device__ __forceinline__ PassView<T> pass_view(const BatchIn<T>& in, const BatchWs& w, int q, int pass) {
+  const int sa = in.pa[q], sb = in.pb[q];
+  const int64_t xs = pass ? sb : sa, ys = pass ? sa : sb, qq = q;
+  PassView<T> v;
+  v.X = in.desc[xs];
+  v.Y = in.desc[ys];
+  v.x_idx = pass ? w.cols + qq * w.n : w.uniq + xs * w.n;
+  v.n_x = pass ? w.n_cols + qq : w.n_uniq + xs;
+  v.y_idx = w.uniq + ys * w.n;
+  v.n_y = w.n_uniq + ys;
+  v.xt = pass ? w.xt2 + qq * w.xrows * ROW_BYTES : w.xt + xs * w.xrows * ROW_BYTES;
+  v.xinfo = pass ? w.xinfo2 + qq * 3 * w.xrows : w.xinfo + xs * 3 * w.xrows;
+  v.yt = w.yt + ys * w.yrows * ROW_BYTES;
+  v.ymax = w.ymax + 4 * ys;
+  v.nn = (pass ? w.nn21 : w.nn12) + qq * w.n;
+  v.dist = (pass ? w.d21 : w.d12) + qq * w.n;
+  v.ny = in.rows[ys];
+  return v;
+}
+
+// per-set stages (blockIdx.y = set; sets in no pair are skipped)
+template <class T>
+__global__ void b_hash(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
+  const int64_t s = blockIdx.y;
+  if (!in.role[s]) return;
+  hash_insert_body<T>(in.desc[s], in.rows[s], w.tkey + s * w.tsize, w.tidx + s * w.tsize, w.tsize,
+                      w.slot_of + s * w.n);
+}
+
+template <class T>
+__global__ void b_reps(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
+  const int64_t s = blockIdx.y;
+  if (!in.role[s]) return;
+  mark_reps_table_body<T>(in.desc[s], in.rows[s], w.tidx + s * w.tsize, w.slot_of + s * w.n, w.rep + s * w.n,
+                          w.flag + s * w.n);
+}
+
+template <class T>
+__global__ void b_prep_sets(const __grid_constant__ BatchIn<T> in, const BatchWs w, int is_y) {
+  const int64_t s = blockIdx.y;
+  if (is_y ? !in.role[s] : !(in.role[s] & 1)) return;  // uniform per block
+  if (is_y)
+    prep_tiles_body<T>(in.desc[s], w.uniq + s * w.n, w.n_uniq + s, 0, w.yrows, BN, w.yt + s * w.yrows * ROW_BYTES,
+                       w.yinfo + s * 3 * w.yrows, w.ymax + 4 * s, 1, BN);
+  else
+    prep_tiles_body<T>(in.desc[s], w.uniq + s * w.n, w.n_uniq + s, 0, w.xrows, BMH, w.xt + s * w.xrows * ROW_BYTES,
+                       w.xinfo + s * 3 * w.xrows, nullptr, 0, BM);
+}
+
+// Order-preserving selection of the flagged indices of every segment in two
+// launches: segment g = the flags of set g (SEG 0: its representatives) or of
+// pair g's columns (SEG 1), length rows[g] / rows[pb[g]].
+template <class T, int SEG>
+__device__ __forceinline__ int64_t seg_len(const BatchIn<T>& in, int g) {
+  return SEG == 0 ? (in.role[g] ? in.rows[g] : 0) : in.rows[in.pb[g]];
+}
+
+__device__ __forceinline__ int block_sum256(int v, int* sh) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int t = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) t += sh[k];
+  __syncthreads();
+  return t;
+}
+
+template <class T, int SEG>
+__global__ void __launch_bounds__(256) b_sel_count(const __grid_constant__ BatchIn<T> in,
+                                                   const int32_t* __restrict__ flag, int64_t stride,
+                                                   int32_t* __restrict__ cnt, int64_t nchunk) {
+  __shared__ int sh[8];
+  const int g = blockIdx.y;
+  const int64_t len = seg_len<T, SEG>(in, g), c0 = (int64_t)blockIdx.x * kSelChunk;
+  if (c0 >= len) return;
+  const int32_t* f = flag + (int64_t)g * stride;
+  const int64_t c1 = min(len, c0 + kSelChunk);
+  int k = 0;
+  for (int64_t i = c0 + threadIdx.x; i < c1; i += 256) k += f[i] != 0;
+  k = block_sum256(k, sh);
+  if (threadIdx.x == 0) cnt[(int64_t)g * nchunk + blockIdx.x] = k;
+}
+
+template <class T, int SEG>
+__global__ void __launch_bounds__(256) b_sel_scatter(const __grid_constant__ BatchIn<T> in,
+                                                     const int32_t* __restrict__ flag, int64_t stride,
+                                                     const int32_t* __restrict__ cnt, int64_t nchunk,
+                                                     int32_t* __restrict__ out, int32_t* __restrict__ n_out) {
+  __shared__ int sh[8], wsum[8];
+  const int g = blockIdx.y;
+  const int64_t len = seg_len<T, SEG>(in, g), c0 = (int64_t)blockIdx.x * kSelChunk;
+  if (c0 >= len) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) n_out[g] = 0;
+    return;
+  }
+  int b = 0;  // flagged entries of the segment's earlier chunks
+  for (int c = threadIdx.x; c < (int)blockIdx.x; c += 256) b += cnt[(int64_t)g * nchunk + c];
+  int base = block_sum256(b, sh);
+  const int32_t* f = flag + (int64_t)g * stride;
+  int32_t* o = out + (int64_t)g * stride;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t c1 = min(len, c0 + kSelChunk);
+  for (int64_t i0 = c0; i0 < c1; i0 += 256) {  // block-uniform trip count
+    const int64_t i = i0 + threadIdx.x;
+    const bool p = i < c1 && f[i] != 0;
+    const unsigned m = __ballot_sync(0xffffffffu, p);
+    if (lane == 0) wsum[wid] = __popc(m);
+    __syncthreads();
+    int pre = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int x = wsum[k];
+      pre += k < wid ? x : 0;
+      tot += x;
+    }
+    if (p) o[base + pre + __popc(m & ((1u << lane) - 1u))] = (int32_t)i;
+    base += tot;
+    __syncthreads();
+  }
+  if (c1 == len && threadIdx.x == 0) n_out[g] = base;
+}
+
+// per-pair stages (blockIdx.y = pair; the tensor-core kernel: blockIdx.z)
+__global__ void b_init(int P, const BatchWs w) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= P) return;
+  w.n_overflow[2 * q] = w.n_overflow[2 * q + 1] = 0;
+  w.n_pairs[2 * q] = w.n_pairs[2 * q + 1] = 0ull;
+  w.counter[q] = 0ull;
+}
+
+template <int MODE, class T>
+__global__ void __launch_bounds__(kThreads, 1) b_topk(const __grid_constant__ BatchIn<T> in, const BatchWs w,
+                                                      int pass) {
+  const int64_t q = blockIdx.z;
+  const PassView<T> v = pass_view(in, w, (int)q, pass);
+  if (MODE == 0)
+    nn_topk_tc_body<0>(v.xt, v.yt, v.n_x, v.n_y, w.topv + q * w.lists * w.xrows * TOPK,
+                       w.topj + q * w.lists * w.xrows * TOPK, nullptr, nullptr, nullptr, 0);
+  else
+    nn_topk_tc_body<1>(w.xto + q * w.over_rows * ROW_BYTES, v.yt, w.n_overflow + 2 * q + pass, v.n_y, nullptr,
+                       nullptr, w.lim + q * w.xrows, w.pairs + q * w.pair_cap, w.n_pairs + 2 * q + pass,
+                       w.pair_cap);
+}
+
+template <class T>
+__global__ void b_certify(const __grid_constant__ BatchIn<T> in, const BatchWs w, int pass, int n_lists,
+                          int64_t nx_pad) {
+  const int64_t q = blockIdx.y;
+  const PassView<T> v = pass_view(in, w, (int)q, pass);
+  certify_exact_body<T>(w.topv + q * w.lists * w.xrows * TOPK, w.topj + q * w.lists * w.xrows * TOPK, v.n_x, v.x_idx,
+                        v.y_idx, v.xinfo, v.ymax, v.X, v.Y, v.nn, v.dist, w.overflow + q * w.n,
+                        w.n_overflow + 2 * q + pass, w.lim + q * w.xrows, n_lists, nx_pad);
+}
+
+// overflow rows -> source rows, and their enumeration minima reset
+template <class T>
+__global__ void b_gather(const __grid_constant__ BatchIn<T> in, const BatchWs w, int pass) {
+  const int64_t q = blockIdx.y;
+  const PassView<T> v = pass_view(in, w, (int)q, pass);
+  const int32_t* ov = w.overflow + q * w.n;
+  const int n = w.n_overflow[2 * q + pass];
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    w.xsrc[q * w.n + k] = v.x_idx[ov[k]];
+    w.best_bits[q * w.n + k] = ~0ull;
+    w.best_j[q * w.n + k] = 0x7f7f7f7f;
+  }
+}
+
+template <class T>
+__global__ void b_prep_rows(const __grid_constant__ BatchIn<T> in, const BatchWs w, int pass, int over) {
+  const int64_t q = blockIdx.y;
+  if (over) {  // the overflow rows' X tiles (pair-private)
+    const PassView<T> v = pass_view(in, w, (int)q, pass);
+    prep_tiles_body<T>(v.X, w.xsrc + q * w.n, w.n_overflow + 2 * q + pass, 0, w.over_rows, BMH,
+                       w.xto + q * w.over_rows * ROW_BYTES, w.xinfoo + q * 3 * w.over_rows, nullptr, 0, BM);
+  } else {  // pass 1's X tiles: the pair's matchable columns of b
+    prep_tiles_body<T>(in.desc[in.pb[q]], w.cols + q * w.n, w.n_cols + q, 0, w.xrows, BMH,
+                       w.xt2 + q * w.xrows * ROW_BYTES, w.xinfo2 + q * 3 * w.xrows, nullptr, 0, BM);
+  }
+}
+
+template <class T>
+__global__ void b_pair_dist_min(const __grid_constant__ BatchIn<T> in, const BatchWs w, int pass) {
+  const int64_t q = blockIdx.y;
+  const PassView<T> v = pass_view(in, w, (int)q, pass);
+  pair_dist_min_body<T>(w.pairs + q * w.pair_cap, w.n_pairs + 2 * q + pass, w.pair_cap, w.xsrc + q * w.n, v.y_idx,
+                        v.X, v.Y, w.pd + q * w.pair_cap, w.best_bits + q * w.n);
+}
+
+template <class T>
+__global__ void b_pair_argmin(const __grid_constant__ BatchIn<T> in, const BatchWs w, int pass) {
+  const int64_t q = blockIdx.y;
+  const PassView<T> v = pass_view(in, w, (int)q, pass);
+  pair_argmin_body<T>(w.pairs + q * w.pair_cap, w.n_pairs + 2 * q + pass, w.pair_cap, v.y_idx, w.pd + q * w.pair_cap,
+                      w.best_bits + q * w.n, w.best_j + q * w.n);
+}
+
+template <class T>
+__global__ void b_pair_write(const __grid_constant__ BatchIn<T> in, const BatchWs w, int pass, int enum_rows) {
+  const int64_t q = blockIdx.y;
+  const PassView<T> v = pass_view(in, w, (int)q, pass);
+  pair_write_body(w.n_overflow + 2 * q + pass, w.xsrc + q * w.n, w.best_bits + q * w.n, w.best_j + q * w.n, v.nn,
+                  v.dist, enum_rows);
+}
+
+template <class T>
+__global__ void b_exact_rows(const __grid_constant__ BatchIn<T> in, const BatchWs w, int pass, int enum_rows) {
+  const int64_t q = blockIdx.y;
+  const PassView<T> v = pass_view(in, w, (int)q, pass);
+  exact_rows_body<T>(w.overflow + q * w.n, w.n_overflow + 2 * q + pass, v.x_idx, v.X, v.Y, v.ny, v.nn, v.dist,
+                     w.n_pairs + 2 * q + pass, w.pair_cap, enum_rows);
+}
+
+template <class T>
+__global__ void b_mark_columns(const __grid_constant__ BatchIn<T> in, const BatchWs w, double delta_s) {
+  const int64_t q = blockIdx.y, sa = in.pa[q];
+  mark_columns_body(w.uniq + sa * w.n, w.n_uniq + sa, w.nn12 + q * w.n, w.d12 + q * w.n, delta_s,
+                    w.colflag + q * w.n);
+}
+
+template <class T>
+__global__ void b_accept(const __grid_constant__ BatchIn<T> in, const BatchWs w, double delta_s) {
+  const int64_t q = blockIdx.y, sa = in.pa[q];
+  accept_pairs_body(w.rep + sa * w.n, in.rows[sa], w.nn12 + q * w.n, w.d12 + q * w.n, w.nn21 + q * w.n, delta_s,
+                    w.kp + q * w.n, w.kd + q * w.n, w.counter + q);
+}
+
+// Accepted pairs sorted by (delta, ref1, ref2) by ranking (pair keys are
+// unique, so ranks are a permutation) and written straight to the outputs
+// (a pair's accepted count is at most min(n1, n2) <= the output stride).
+constexpr int kBRankTile = 1024;
+constexpr int kBRankLanes = 8;
+__global__ void __launch_bounds__(256) b_rank_out(const BatchWs w, int64_t stride, int32_t* __restrict__ ref1,
+                                                  int32_t* __restrict__ ref2, double* __restrict__ delta,
+                                                  int64_t* __restrict__ out_count) {
+  __shared__ unsigned long long td[kBRankTile], tp[kBRankTile];
+  constexpr int kPerBlock = 256 / kBRankLanes;
+  const int64_t q = blockIdx.y;
+  const unsigned long long c = w.counter[q];
+  if (blockIdx.x == 0 && threadIdx.x == 0) out_count[q] = (int64_t)c;
+  const int n = (int)min((unsigned long long)stride, c);
+  if ((int)(blockIdx.x * kPerBlock) >= n) return;  // uniform per block
+  const unsigned long long* kd = w.kd + q * w.n;
+  const unsigned long long* kp = w.kp + q * w.n;
+  const int g = threadIdx.x & (kBRankLanes - 1);
+  const int e = blockIdx.x * kPerBlock + threadIdx.x / kBRankLanes;
+  const unsigned long long d = e < n ? kd[e] : 0ull, p = e < n ? kp[e] : 0ull;
+  int rank = 0;
+  for (int t0 = 0; t0 < n; t0 += kBRankTile) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < kBRankTile; k += blockDim.x) {
+      const int f = t0 + k;
+      td[k] = f < n ? kd[f] : ~0ull;
+      tp[k] = f < n ? kp[f] : ~0ull;
+    }
+    __syncthreads();
+    const int m = min(kBRankTile, n - t0);
+#pragma unroll 4
+    for (int k = g; k < m; k += kBRankLanes) rank += (td[k] < d) | ((td[k] == d) & (tp[k] < p));
+  }
+#pragma unroll
+  for (int o = 1; o < kBRankLanes; o <<= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+  if (e < n && g == 0) {
+    ref1[q * stride + rank] = (int32_t)(p >> 32);
+    ref2[q * stride + rank] = (int32_t)(p & 0xffffffffu);
+    delta[q * stride + rank] = __longlong_as_double((long long)d);
+  }
+}
+
+// column splits of a batched tensor-core launch (rb row blocks per pair)
+int batch_split(int64_t P, int64_t rb, int64_t tiles) {
+  if (P * rb >= kThroughputRowBlocks) return 1;
+  int best = 1;
+  int64_t best_cost = INT64_MAX;
+  for (int s = 1; s <= std::min<int64_t>(kMaxSplit, tiles); ++s) {
+    const int64_t waves = (P * rb * s + kSMs - 1) / kSMs;
+    const int64_t cost = waves * ((tiles + s - 1) / s + 4 * XH);
+    if (cost < best_cost) { best_cost = cost; best = s; }
+  }
+  return best;
+}
+
+template <class T>
+int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1, int32_t* ref2, double* delta,
+               int64_t stride, int64_t* out_count, void* ws, size_t ws_bytes, cudaStream_t st) {
+  int64_t n = 1;
+  for (int s = 0; s < S; ++s)
+    if (in.role[s]) n = std::max<int64_t>(n, in.rows[s]);
+  size_t need = 0;
+  carve_batch(nullptr, S, P, n, &need);
+  PS_REQUIRE(ws && ws_bytes >= need, PS_ERR_ARGUMENT, "batched match workspace %zu < %zu", ws_bytes, need);
+  const BatchWs w = carve_batch(ws, S, P, n, &need);
+  const int64_t N = w.n;
+  cudaMemsetAsync(w.tkey, 0, (size_t)S * w.tsize * sizeof(unsigned long long), st);
+  cudaMemsetAsync(w.tidx, 0x7f, (size_t)S * w.tsize * sizeof(int32_t), st);
+  cudaMemsetAsync(w.ymax, 0, (size_t)S * 4 * sizeof(unsigned), st);
+  cudaMemsetAsync(w.colflag, 0, (size_t)P * N * sizeof(int32_t), st);
+  b_init<<<(P + 255) / 256, 256, 0, st>>>(P, w);
+  PS_LAUNCHED("b_init");
+  // per set: duplicate grouping, representatives, operand tiles
+  const dim3 gs(grid_for(N, 8), S);
+  b_hash<T><<<gs, 256, 0, st>>>(in, w);
+  PS_LAUNCHED("b_hash");
+  b_reps<T><<<gs, 256, 0, st>>>(in, w);
+  PS_LAUNCHED("b_reps");
+  b_sel_count<T, 0><<<dim3(w.nchunk, S), 256, 0, st>>>(in, w.flag, N, w.sel_cnt, w.nchunk);
+  PS_LAUNCHED("b_sel_count");
+  b_sel_scatter<T, 0><<<dim3(w.nchunk, S), 256, 0, st>>>(in, w.flag, N, w.sel_cnt, w.nchunk, w.uniq, w.n_uniq);
+  PS_LAUNCHED("b_sel_scatter");
+  b_prep_sets<T><<<dim3(grid_for(w.xrows, 8), S), 256, 0, st>>>(in, w, 0);
+  PS_LAUNCHED("b_prep_sets(X)");
+  b_prep_sets<T><<<dim3(grid_for(w.yrows, 8), S), 256, 0, st>>>(in, w, 1);
+  PS_LAUNCHED("b_prep_sets(Y)");
+  cudaFuncSetAttribute(b_topk<0, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<0>());
+  cudaFuncSetAttribute(b_topk<1, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<1>());
+  for (int pass = 0; pass < 2; ++pass) {
+    int64_t nx = 1, ny = 1;  // row bounds over the pairs
+    for (int q = 0; q < P; ++q) {
+      nx = std::max<int64_t>(nx, in.rows[pass ? in.pb[q] : in.pa[q]]);
+      ny = std::max<int64_t>(ny, in.rows[pass ? in.pa[q] : in.pb[q]]);
+    }
+    if (pass == 1) {  // the matchable columns of b, and their X tiles
+      b_mark_columns<T><<<dim3(grid_for(N, 256), P), 256, 0, st>>>(in, w, delta_s);
+      PS_LAUNCHED("b_mark_columns");
+      b_sel_count<T, 1><<<dim3(w.nchunk, P), 256, 0, st>>>(in, w.colflag, N, w.sel_cnt, w.nchunk);
+      PS_LAUNCHED("b_sel_count");
+      b_sel_scatter<T, 1><<<dim3(w.nchunk, P), 256, 0, st>>>(in, w.colflag, N, w.sel_cnt, w.nchunk, w.cols,
+                                                             w.n_cols);
+      PS_LAUNCHED("b_sel_scatter");
+      b_prep_rows<T><<<dim3(grid_for(rup(nx, BM), 8), P), 256, 0, st>>>(in, w, pass, 0);
+      PS_LAUNCHED("b_prep_rows(columns)");
+    }
+    const int64_t rb = (nx + BM - 1) / BM, tiles = (ny + BN - 1) / BN;
+    const int split = batch_split(P, rb, tiles);
+    b_topk<0, T><<<dim3(rb, split, P), kThreads, smem_bytes<0>(), st>>>(in, w, pass);
+    PS_LAUNCHED("b_topk<top4>");
+    b_certify<T><<<dim3(grid_for(nx, 32), P), 256, 0, st>>>(in, w, pass, kParts * split, rb * BM);
+    PS_LAUNCHED("b_certify");
+    b_gather<T><<<dim3(grid_for(nx, 256), P), 256, 0, st>>>(in, w, pass);
+    PS_LAUNCHED("b_gather");
+    // near-tie rows: the first enum_rows of each pair enumerated on the
+    // tensor cores, the rest (and overflowing enumerations) scanned exactly
+    const int eb = (int)std::min<int64_t>(kEnumBlocksAsync, rb);
+    const int enum_rows = eb * BM;
+    b_prep_rows<T><<<dim3(grid_for(enum_rows, 8), P), 256, 0, st>>>(in, w, pass, 1);
+    PS_LAUNCHED("b_prep_rows(overflow)");
+    const int split_e = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)kMaxSplit, tiles, 4 * kSMs / (P * eb)}));
+    b_topk<1, T><<<dim3(eb, split_e, P), kThreads, smem_bytes<1>(), st>>>(in, w, pass);
+    PS_LAUNCHED("b_topk<enumerate>");
+    b_pair_dist_min<T><<<dim3(std::max(4, 148 * 16 / P), P), 256, 0, st>>>(in, w, pass);
+    PS_LAUNCHED("b_pair_dist_min");
+    b_pair_argmin<T><<<dim3(std::max(2, 148 * 8 / P), P), 256, 0, st>>>(in, w, pass);
+    PS_LAUNCHED("b_pair_argmin");
+    b_pair_write<T><<<dim3(grid_for(enum_rows, 256), P), 256, 0, st>>>(in, w, pass, enum_rows);
+    PS_LAUNCHED("b_pair_write");
+    b_exact_rows<T><<<dim3(std::max(2, 148 * 4 / P), P), 256, 0, st>>>(in, w, pass, enum_rows);
+    PS_LAUNCHED("b_exact_rows");
+  }
+  b_accept<T><<<dim3(grid_for(N, 256), P), 256, 0, st>>>(in, w, delta_s);
+  PS_LAUNCHED("b_accept");
+  b_rank_out<<<dim3((stride + 31) / 32, P), 256, 0, st>>>(w, stride, ref1, ref2, delta, out_count);
+  PS_LAUNCHED("b_rank_out");
+  return PS_OK;
+}
+
 }  // namespace tc
 }  // namespace ps
 
@@ -1189,3 +1755,82 @@ template int ps_tc_nearest_impl<float>(const float*, int64_t, const float*, int6
                                        unsigned long long*, unsigned long long*, void*, size_t, cudaStream_t, bool);
 template int ps_tc_nearest_impl<double>(const double*, int64_t, const double*, int64_t, double, unsigned long long*,
                                         unsigned long long*, unsigned long long*, void*, size_t, cudaStream_t, bool);
+
+// ---- batched pairs: C entry points -------------------------------------------------------
+namespace {
+int batch_check(int32_t n_sets, const int64_t* set_rows, int32_t n_pairs, int32_t dim) {
+  PS_REQUIRE(dim == ps::tc::KD, PS_ERR_ARGUMENT, "batched match needs %d-d descriptors, got %d", ps::tc::KD, dim);
+  PS_REQUIRE(n_sets >= 1 && n_sets <= ps::tc::kBatchMaxSets, PS_ERR_ARGUMENT, "n_sets %d outside [1, %d]", n_sets,
+             ps::tc::kBatchMaxSets);
+  PS_REQUIRE(n_pairs >= 0 && n_pairs <= ps::tc::kBatchMaxPairs, PS_ERR_ARGUMENT, "n_pairs %d outside [0, %d]",
+             n_pairs, ps::tc::kBatchMaxPairs);
+  PS_REQUIRE(set_rows, PS_ERR_ARGUMENT, "null set_rows");
+  for (int s = 0; s < n_sets; ++s)
+    PS_REQUIRE(set_rows[s] >= 0 && set_rows[s] < INT32_MAX, PS_ERR_ARGUMENT, "bad row count %lld of set %d",
+               (long long)set_rows[s], s);
+  return PS_OK;
+}
+int64_t batch_rows_bound(int32_t n_sets, const int64_t* set_rows) {
+  int64_t n = 1;
+  for (int s = 0; s < n_sets; ++s) n = std::max<int64_t>(n, set_rows[s]);
+  return n;
+}
+template <class T>
+int batch_run(int32_t n_sets, const void* const* set_desc, const int64_t* set_rows, int32_t n_pairs,
+              const int32_t* pair_a, const int32_t* pair_b, double delta_s, int32_t* out_ref1, int32_t* out_ref2,
+              double* out_delta, int64_t out_stride, int64_t* out_count, void* ws, size_t ws_bytes,
+              cudaStream_t st) {
+  static thread_local ps::tc::BatchIn<T> in;  // ~7 KB: not on the stack
+  memset(&in, 0, sizeof(in));
+  for (int s = 0; s < n_sets; ++s) {
+    in.desc[s] = static_cast<const T*>(set_desc[s]);
+    in.rows[s] = (int32_t)set_rows[s];
+  }
+  for (int q = 0; q < n_pairs; ++q) {
+    in.pa[q] = (int16_t)pair_a[q];
+    in.pb[q] = (int16_t)pair_b[q];
+    in.role[pair_a[q]] |= 1;
+    in.role[pair_b[q]] |= 2;
+  }
+  return ps::tc::batch_impl<T>(in, n_sets, n_pairs, delta_s, out_ref1, out_ref2, out_delta, out_stride, out_count,
+                               ws, ws_bytes, st);
+}
+}  // namespace
+
+extern "C" int ps_match_batch_plan(int32_t n_sets, const int64_t* set_rows, int32_t n_pairs, int32_t dim,
+                                   size_t* workspace_bytes_out) {
+  const int rc = batch_check(n_sets, set_rows, n_pairs, dim);
+  if (rc) return rc;
+  size_t need = 0;
+  ps::tc::carve_batch(nullptr, n_sets, std::max(n_pairs, 1), batch_rows_bound(n_sets, set_rows), &need);
+  if (workspace_bytes_out) *workspace_bytes_out = need;
+  return PS_OK;
+}
+
+extern "C" int ps_match_batch_async(int32_t n_sets, const void* const* set_desc, const int64_t* set_rows,
+                                    int32_t n_pairs, const int32_t* pair_a, const int32_t* pair_b, int32_t dim,
+                                    int32_t desc_is_f64, double delta_s, int32_t* out_ref1, int32_t* out_ref2,
+                                    double* out_delta, int64_t out_stride, int64_t* out_count, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+  int rc = batch_check(n_sets, set_rows, n_pairs, dim);
+  if (rc) return rc;
+  PS_REQUIRE(delta_s > 0, PS_ERR_CONFIG, "delta_s must be positive, got %g", delta_s);
+  if (n_pairs == 0) return PS_OK;
+  PS_REQUIRE(set_desc && pair_a && pair_b && out_ref1 && out_ref2 && out_delta && out_count, PS_ERR_ARGUMENT,
+             "null argument to ps_match_batch_async");
+  for (int q = 0; q < n_pairs; ++q) {
+    const int a = pair_a[q], b = pair_b[q];
+    PS_REQUIRE(a >= 0 && a < n_sets && b >= 0 && b < n_sets, PS_ERR_ARGUMENT, "pair %d: set index out of range", q);
+    PS_REQUIRE(out_stride >= std::min(set_rows[a], set_rows[b]), PS_ERR_ARGUMENT,
+               "out_stride %lld < min(rows) of pair %d", (long long)out_stride, q);
+    PS_REQUIRE((set_desc[a] || set_rows[a] == 0) && (set_desc[b] || set_rows[b] == 0), PS_ERR_ARGUMENT,
+               "pair %d: null descriptor set", q);
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  rc = desc_is_f64 ? batch_run<double>(n_sets, set_desc, set_rows, n_pairs, pair_a, pair_b, delta_s, out_ref1,
+                                       out_ref2, out_delta, out_stride, out_count, workspace, workspace_bytes, st)
+                   : batch_run<float>(n_sets, set_desc, set_rows, n_pairs, pair_a, pair_b, delta_s, out_ref1,
+                                      out_ref2, out_delta, out_stride, out_count, workspace, workspace_bytes, st);
+  if (rc) return rc;
+  return ps::check_cuda("ps_match_batch_async");
+}

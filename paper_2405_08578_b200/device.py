@@ -401,6 +401,57 @@ def match_many(pairs, delta_s: float = 0.35, *, streams=None):
     return [(r1[:k], r2[:k], dl[:k]) for (r1, r2, dl), k in zip(outs, m)]
 
 
+BATCH_MAX_SETS, BATCH_MAX_PAIRS = 512, 256  # ps_match_batch_async limits per call
+
+
+def match_batch_async(sets, pairs, delta_s: float = 0.35, *, out_count=None, stream=None):
+    """nearest_neighbor matching of many pairs over shared descriptor sets as
+    one launch sequence (ps_match_batch_async): each set's duplicate grouping
+    and tensor-core operand tiles are built once however many pairs use it,
+    and every stage is one launch for all pairs.  No host synchronisation
+    (capturable).  ``sets`` = [desc [n_s, 128] device tensors], ``pairs`` =
+    [(a, b), ...] set indices.  Returns (ref1 int32 [P, S], ref2 int32 [P, S],
+    delta float64 [P, S], count int64 [P]) with S = max over pairs of
+    min(n_a, n_b); row q holds pair q's matches in [0, count[q]), sorted by
+    (delta, ref1, ref2) -- the same as ``match`` pair by pair."""
+    if delta_s <= 0:
+        raise ConfigError(f"delta_s must be positive, got {delta_s}")
+    P = len(pairs)
+    if not sets:
+        raise ValueError("match_batch_async needs at least one descriptor set")
+    dt = torch.float64 if any(s.dtype == torch.float64 for s in sets) else torch.float32
+    ds = [s.to(dt).contiguous() for s in sets]
+    for d in ds:
+        _require_cuda(d, "descriptor set")
+        if d.dim() != 2 or int(d.shape[1]) != 128:
+            raise ValueError(f"match_batch_async needs [n, 128] descriptor sets, got {tuple(d.shape)}")
+    dev = ds[0].device
+    rows = [int(d.shape[0]) for d in ds]
+    stride = max([min(rows[a], rows[b]) for a, b in pairs] + [1])
+    cnt = out_count if out_count is not None else torch.zeros(P, dtype=torch.int64, device=dev)
+    r1 = torch.empty((P, stride), dtype=torch.int32, device=dev)
+    r2 = torch.empty((P, stride), dtype=torch.int32, device=dev)
+    dl = torch.empty((P, stride), dtype=torch.float64, device=dev)
+    L = _lib.lib()
+    for q0 in range(0, P, BATCH_MAX_PAIRS):
+        chunk = list(pairs[q0:q0 + BATCH_MAX_PAIRS])
+        used = sorted({s for pr in chunk for s in pr})  # <= 2 x BATCH_MAX_PAIRS = BATCH_MAX_SETS
+        local = {s: i for i, s in enumerate(used)}
+        S = len(used)
+        ptrs = (C.c_void_p * S)(*[ds[s].data_ptr() for s in used])
+        rows_c = (C.c_int64 * S)(*[rows[s] for s in used])
+        pa = (C.c_int32 * len(chunk))(*[local[a] for a, _ in chunk])
+        pb = (C.c_int32 * len(chunk))(*[local[b] for _, b in chunk])
+        wsb = C.c_size_t()
+        _lib.check(L.ps_match_batch_plan(S, rows_c, len(chunk), 128, C.byref(wsb)), "match_batch")
+        ws = _workspace(wsb.value, dev)
+        _lib.check(L.ps_match_batch_async(S, ptrs, rows_c, len(chunk), pa, pb, 128, int(dt == torch.float64),
+                                          float(delta_s), _ptr(r1[q0:]), _ptr(r2[q0:]), _ptr(dl[q0:]), stride,
+                                          _ptr(cnt[q0:]), _ptr(ws), wsb.value, C.c_void_p(_stream_ptr(stream))),
+                   "match_batch")
+    return r1, r2, dl, cnt
+
+
 def pair_points(r1, r2, kp1_row, kp1_col, kp2_row, kp2_col, stream=None):
     """(x, y) = (col, row) float64 coordinates of matched pairs (registration.py:143-146)."""
     n = int(r1.shape[0])

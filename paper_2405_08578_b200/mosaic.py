@@ -66,6 +66,8 @@ class PairwiseTransformTable:
 class GpuEngine:
     """Hot path on the local GPU through the C-ABI (device.py)."""
 
+    batch_match = True  # register_many: every pair's match in one ps_match_batch_async launch sequence
+
     def __init__(self, cfg, pair_workers: int = 1, batched: bool = True, n_streams: int = 4):
         self.cfg = cfg
         self.device = torch.device("cuda", torch.cuda.current_device())
@@ -116,9 +118,28 @@ class GpuEngine:
         mc = cfg.matcher_config()
         streams = self._streams()
         counts = torch.zeros(len(items), dtype=torch.int64, device=self.device)
-        outs = device.match_many_async([(it[2][: it[3]], it[6][: it[7]]) for it in items], mc.delta_s, counts,
-                                       streams=streams)
         caps = [min(int(it[3]), int(it[7])) for it in items]
+        if self.batch_match and all(it[2].dim() == 2 and int(it[2].shape[1]) == 128 for it in items):
+            # one launch sequence for every pair; an image's descriptor set
+            # (same rows at the same address) is grouped and tiled once
+            sets, index, pairs = [], {}, []
+            for it in items:
+                ends = []
+                for d, n in ((it[2], int(it[3])), (it[6], int(it[7]))):
+                    key = (d.data_ptr(), n, str(d.dtype))
+                    if key not in index:
+                        index[key] = len(sets)
+                        sets.append(d[:n])
+                    ends.append(index[key])
+                pairs.append(tuple(ends))
+            r1, r2, dl, _ = device.match_batch_async(sets, pairs, mc.delta_s, out_count=counts)
+            outs = [(r1[q, :c], r2[q, :c], dl[q, :c]) for q, c in enumerate(caps)]
+            for s in streams or ():
+                for t in (r1, r2, counts):
+                    t.record_stream(s)
+        else:
+            outs = device.match_many_async([(it[2][: it[3]], it[6][: it[7]]) for it in items], mc.delta_s, counts,
+                                           streams=streams)
         width = 8 + (max(caps + [8]) + 7) // 8
         block = torch.zeros((len(items), width), dtype=torch.float64, device=self.device)
         live = [False] * len(items)

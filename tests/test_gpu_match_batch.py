@@ -1,0 +1,148 @@
+"""Batched pair matching (ps_match_batch_async) against the per-pair matcher.
+
+``device.match`` is pinned to the oracle / reference fixtures elsewhere
+(test_gpu_parity.py P3, test_gpu_pairs.py, test_gpu_c4.py); the batch runs
+the same kernel bodies per pair, so every pair's (ref1, ref2, delta) list and
+count must be bit-identical to ``device.match`` on the same two sets --
+including sets shared by several pairs, a set matched with itself, duplicate
+rows, empty sets and float64 descriptors.  The C3 table (9 images, 36 pairs,
+every image in 8 pairs) is checked through the engine the bench times.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2405_08578_b200 import device, scenes  # noqa: E402
+from paper_2405_08578_b200.pipeline import PipelineConfig  # noqa: E402
+
+
+def _unit_rows(rng, n, dup_every=0, dtype=torch.float32):
+    x = rng.standard_normal((n, 128))
+    x = np.abs(x) * (rng.random((n, 128)) < 0.4)  # sparse, non-negative like SIFT rows
+    x /= np.maximum(np.linalg.norm(x, axis=1, keepdims=True), 1e-12)
+    if dup_every:
+        x[::dup_every] = x[0]  # a cluster of bit-identical rows (saturated regions)
+    return torch.from_numpy(x).to(dtype).cuda()
+
+
+def _perturbed(rng, base, sigma, n_extra):
+    x = base.double().cpu().numpy()
+    y = x[rng.permutation(x.shape[0])] + sigma * rng.standard_normal(x.shape)
+    y = np.vstack([y, np.abs(rng.standard_normal((n_extra, 128)))])
+    y = np.abs(y)
+    y /= np.maximum(np.linalg.norm(y, axis=1, keepdims=True), 1e-12)
+    return torch.from_numpy(y).to(base.dtype).cuda()
+
+
+def _check(sets, pairs, delta_s=0.35):
+    r1, r2, dl, cnt = device.match_batch_async(sets, pairs, delta_s)
+    torch.cuda.synchronize()
+    cnt = cnt.cpu().numpy()
+    for q, (a, b) in enumerate(pairs):
+        e1, e2, ed = device.match(sets[a], sets[b], delta_s, path="tensor") if min(
+            sets[a].shape[0], sets[b].shape[0]) else (torch.zeros(0), torch.zeros(0), torch.zeros(0))
+        m = int(e1.shape[0])
+        assert int(cnt[q]) == m, (q, a, b, int(cnt[q]), m)
+        assert torch.equal(r1[q, :m].cpu(), e1.cpu().to(torch.int32)), (q, a, b)
+        assert torch.equal(r2[q, :m].cpu(), e2.cpu().to(torch.int32)), (q, a, b)
+        assert torch.equal(dl[q, :m].cpu(), ed.cpu().to(torch.float64)), (q, a, b)
+    return cnt
+
+
+def test_batch_equals_per_pair_shared_sets():
+    rng = np.random.default_rng(11)
+    base = _unit_rows(rng, 3000, dup_every=97)
+    sets = [base, _perturbed(rng, base, 0.01, 500), _perturbed(rng, base, 0.03, 0),
+            _unit_rows(rng, 1200), _perturbed(rng, base[:700], 0.005, 60)]
+    pairs = [(0, 1), (0, 2), (1, 2), (2, 0), (3, 0), (0, 3), (4, 1), (1, 4), (2, 2), (3, 4)]
+    cnt = _check(sets, pairs)
+    assert cnt[0] > 1000 and cnt[8] > 0  # real matches, including the self pair
+
+
+def test_batch_sizes_and_edge_cases():
+    rng = np.random.default_rng(5)
+    a = _unit_rows(rng, 1)
+    b = _unit_rows(rng, 300)
+    c = _unit_rows(rng, 129)  # one past a row block
+    d = _unit_rows(rng, 256 * 3 + 1, dup_every=2)  # half the rows identical
+    e = torch.zeros((0, 128), dtype=torch.float32, device="cuda")
+    sets = [a, b, c, d, e]
+    pairs = [(0, 1), (1, 0), (1, 2), (2, 3), (3, 2), (3, 3), (0, 0), (4, 1), (1, 4)]
+    cnt = _check(sets, pairs, delta_s=10.0)  # every mutual pair accepted
+    assert cnt[7] == 0 and cnt[8] == 0 and cnt[6] == 1
+
+
+def test_batch_float64_sets():
+    rng = np.random.default_rng(8)
+    base = _unit_rows(rng, 1500, dtype=torch.float64)
+    sets = [base, _perturbed(rng, base, 0.02, 100), _perturbed(rng, base, 0.02, 0)]
+    _check(sets, [(0, 1), (1, 2), (2, 0)])
+
+
+def test_batch_many_pairs_chunked():
+    """More pairs than one call takes (BATCH_MAX_PAIRS): chunked launches."""
+    rng = np.random.default_rng(3)
+    sets = [_unit_rows(rng, 200 + 7 * k) for k in range(24)]
+    pairs = [(i, j) for i in range(24) for j in range(24) if i != j][: device.BATCH_MAX_PAIRS + 40]
+    r1, r2, dl, cnt = device.match_batch_async(sets, pairs, 1.5)
+    torch.cuda.synchronize()
+    for q in (0, 17, device.BATCH_MAX_PAIRS - 1, device.BATCH_MAX_PAIRS, len(pairs) - 1):
+        a, b = pairs[q]
+        e1, e2, ed = device.match(sets[a], sets[b], 1.5, path="tensor")
+        m = int(e1.shape[0])
+        assert int(cnt[q]) == m
+        assert torch.equal(r1[q, :m], e1.to(torch.int32)) and torch.equal(r2[q, :m], e2.to(torch.int32))
+        assert torch.equal(dl[q, :m], ed)
+
+
+def test_batch_c3_table_equals_per_pair():
+    """C3 (9 x 2688x1600 crops, 36 pairs): the batch on the images'
+    descriptor sets equals device.match pair by pair, and the engine's
+    table (batched) equals the per-pair-launch engine's."""
+    from paper_2405_08578_b200 import mosaic
+
+    imgs, _ = scenes.config3_images()
+    cfg = PipelineConfig()
+    eng = mosaic.GpuEngine(cfg)
+    rows, cols, desc, count = eng.prepare(imgs)
+    n = count.cpu().tolist()
+    sets = [desc[k, : n[k]] for k in range(len(imgs))]
+    pairs = [(a, b) for a in range(len(imgs)) for b in range(a + 1, len(imgs))]
+    cnt = _check(sets, pairs)
+    assert cnt.sum() > 0
+    control, _ = scenes.config3_images(0, rot_deg=0.0, scale_range=(1.0, 1.0), noise=0.0)
+    for images, min_registered in ((imgs, 0), (control, 15)):
+        t_batch = mosaic.build_pairwise_table(images, cfg, engine=eng)
+        eng2 = mosaic.GpuEngine(cfg)
+        eng2.batch_match = False
+        t_pair = mosaic.build_pairwise_table(images, cfg, engine=eng2)
+        assert t_batch.entries.keys() == t_pair.entries.keys()
+        assert len(t_batch.entries) >= 2 * min_registered
+        for k, v in t_batch.entries.items():
+            w = t_pair.entries[k]
+            assert v.inlier_count == w.inlier_count and v.transform == w.transform
+
+
+def test_batch_graph_replay_c5_pairs():
+    """C5-style disjoint pairs (RGB, homography warp) through the graph
+    engine: replays equal the eager batched phase and the per-pair path."""
+    from paper_2405_08578_b200 import mosaic
+
+    cfg = PipelineConfig(window_min=16, window_max=64)
+    pairs = [scenes.config5_pair(k) for k in range(6)]
+    batch = torch.from_numpy(np.stack([im for a, b, _ in pairs for im in (a, b)])).cuda()
+    g = device.as_device_images(batch, rgb=True)
+    eng = mosaic.GraphEngine(cfg)
+    rows, cols, desc, count = eng.prepare_device(g)
+    n = count.cpu().tolist()
+    items = [(rows[2 * k], cols[2 * k], desc[2 * k], n[2 * k], rows[2 * k + 1], cols[2 * k + 1], desc[2 * k + 1],
+              n[2 * k + 1], 1000 + k) for k in range(len(pairs))]
+    first = eng.register_many(items)  # eager + capture
+    again = eng.register_many(items)  # replay
+    ref = [eng.register(*it) for it in items]
+    assert first == again == ref
