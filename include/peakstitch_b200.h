@@ -254,6 +254,37 @@ PS_API int ps_pair_points(const int32_t* ref1, const int32_t* ref2, const int64_
                    const int32_t* col2, double* src_xy, double* dst_xy, int64_t cap,
                    void* stream);
 
+/* ---- batched registration: registration.py:143-203 per pair ------------- */
+/* One matched pair of a batch: its two images' keypoint coordinates (device
+ * int32), its capacity n_cap = min(n1, n2) (>= min_inliers, <= ref_stride),
+ * and the PCG64 state of default_rng(seed) (numpy bit_generator.state:
+ * state, inc, has_uint32, uinteger) that the reference's RANSAC draws from
+ * (registration.py:164).  live = 0 skips the pair (its block is untouched). */
+typedef struct {
+  const int32_t *row1, *col1, *row2, *col2;
+  int64_t n_cap;
+  uint64_t state_hi, state_lo, inc_hi, inc_lo;
+  int32_t has_uint32;
+  uint32_t uinteger;
+  int32_t live;
+} ps_register_pair;
+/* The point gather (ps_pair_points) and RANSAC (ps_ransac_samples_async +
+ * ps_ransac_rigid_async) of up to 256 matched pairs as one launch per stage:
+ * pair q's matches are row q of ref1 / ref2 (device int32 [n_pairs,
+ * ref_stride], e.g. ps_match_batch_async's outputs) with count[q] (device
+ * int64).  Pair q's result goes to out_block + q * block_stride (doubles):
+ * [0, 3) model (theta, t_x, t_y), [3] rms, [4, 8) int64 status / consensus /
+ * inliers / best iteration, and from byte 64 the uint8 inlier mask
+ * (block_stride >= 8 + ceil(ref_stride / 8)).  Results equal the per-pair
+ * calls'; no host synchronisation. */
+PS_API int ps_register_batch_plan(int32_t n_pairs, int64_t n_cap, int32_t iterations,
+                                  size_t* workspace_bytes_out);
+PS_API int ps_register_batch_async(int32_t n_pairs, const ps_register_pair* pairs, const int32_t* ref1,
+                                   const int32_t* ref2, int64_t ref_stride, const int64_t* count,
+                                   int32_t iterations, double inlier_tol, int32_t min_inliers,
+                                   double* out_block, int64_t block_stride, void* workspace,
+                                   size_t workspace_bytes, void* stream);
+
 /* ---- RANSAC: registration.py:107-203 ------------------------------------ */
 /* samples: device int32 [iterations, 2], the reference's index stream
  * (registration.py:164, 170-173), generated on the host from the seed.

@@ -43,6 +43,13 @@ class PlacementC(C.Structure):
                 ("t_x", C.c_double), ("t_y", C.c_double)]
 
 
+class RegisterPairC(C.Structure):
+    _fields_ = [("row1", C.c_void_p), ("col1", C.c_void_p), ("row2", C.c_void_p), ("col2", C.c_void_p),
+                ("n_cap", C.c_int64), ("state_hi", C.c_uint64), ("state_lo", C.c_uint64),
+                ("inc_hi", C.c_uint64), ("inc_lo", C.c_uint64), ("has_uint32", C.c_int32),
+                ("uinteger", C.c_uint32), ("live", C.c_int32)]
+
+
 PS_BLEND_FEATHER, PS_BLEND_OVERWRITE = 0, 1
 PS_RESAMPLE_BILINEAR, PS_RESAMPLE_NEAREST = 0, 1
 
@@ -72,6 +79,10 @@ SIGNATURES = {
                                  C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                  C.c_void_p, C.c_size_t, C.c_void_p]),
     "ps_pair_points": (C.c_int, [C.c_void_p] * 9 + [C.c_int64, C.c_void_p]),
+    "ps_register_batch_plan": (C.c_int, [C.c_int32, C.c_int64, C.c_int32, C.POINTER(C.c_size_t)]),
+    "ps_register_batch_async": (C.c_int, [C.c_int32, C.POINTER(RegisterPairC), C.c_void_p, C.c_void_p, C.c_int64,
+                                          C.c_void_p, C.c_int32, C.c_double, C.c_int32, C.c_void_p, C.c_int64,
+                                          C.c_void_p, C.c_size_t, C.c_void_p]),
     "ps_match_batch_plan": (C.c_int, [C.c_int32, C.POINTER(C.c_int64), C.c_int32, C.c_int32,
                                       C.POINTER(C.c_size_t)]),
     "ps_match_batch_async": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_int32,

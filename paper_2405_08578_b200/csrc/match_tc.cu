@@ -1562,10 +1562,16 @@ int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1
   cudaMemsetAsync(w.tidx, 0x7f, (size_t)S * w.tsize * sizeof(int32_t), st);
   cudaMemsetAsync(w.ymax, 0, (size_t)S * 4 * sizeof(unsigned), st);
   cudaMemsetAsync(w.colflag, 0, (size_t)P * N * sizeof(int32_t), st);
+  // grids: blocks per set / pair capped so the whole launch is a few waves
+  // (the bodies loop grid-stride; one tiny block per 8 rows of every set
+  // made block scheduling the cost at C5's 512 sets)
+  auto per = [](int64_t natural, int64_t groups) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(natural, (148 * 16 + groups - 1) / groups));
+  };
   b_init<<<(P + 255) / 256, 256, 0, st>>>(P, w);
   PS_LAUNCHED("b_init");
   // per set: duplicate grouping, representatives, operand tiles
-  const dim3 gs(grid_for(N, 8), S);
+  const dim3 gs(per(grid_for(N, 8), S), S);
   b_hash<T><<<gs, 256, 0, st>>>(in, w);
   PS_LAUNCHED("b_hash");
   b_reps<T><<<gs, 256, 0, st>>>(in, w);
@@ -1574,9 +1580,9 @@ int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1
   PS_LAUNCHED("b_sel_count");
   b_sel_scatter<T, 0><<<dim3(w.nchunk, S), 256, 0, st>>>(in, w.flag, N, w.sel_cnt, w.nchunk, w.uniq, w.n_uniq);
   PS_LAUNCHED("b_sel_scatter");
-  b_prep_sets<T><<<dim3(grid_for(w.xrows, 8), S), 256, 0, st>>>(in, w, 0);
+  b_prep_sets<T><<<dim3(per(grid_for(w.xrows, 8), S), S), 256, 0, st>>>(in, w, 0);
   PS_LAUNCHED("b_prep_sets(X)");
-  b_prep_sets<T><<<dim3(grid_for(w.yrows, 8), S), 256, 0, st>>>(in, w, 1);
+  b_prep_sets<T><<<dim3(per(grid_for(w.yrows, 8), S), S), 256, 0, st>>>(in, w, 1);
   PS_LAUNCHED("b_prep_sets(Y)");
   cudaFuncSetAttribute(b_topk<0, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<0>());
   cudaFuncSetAttribute(b_topk<1, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<1>());
@@ -1587,29 +1593,29 @@ int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1
       ny = std::max<int64_t>(ny, in.rows[pass ? in.pa[q] : in.pb[q]]);
     }
     if (pass == 1) {  // the matchable columns of b, and their X tiles
-      b_mark_columns<T><<<dim3(grid_for(N, 256), P), 256, 0, st>>>(in, w, delta_s);
+      b_mark_columns<T><<<dim3(per(grid_for(N, 256), P), P), 256, 0, st>>>(in, w, delta_s);
       PS_LAUNCHED("b_mark_columns");
       b_sel_count<T, 1><<<dim3(w.nchunk, P), 256, 0, st>>>(in, w.colflag, N, w.sel_cnt, w.nchunk);
       PS_LAUNCHED("b_sel_count");
       b_sel_scatter<T, 1><<<dim3(w.nchunk, P), 256, 0, st>>>(in, w.colflag, N, w.sel_cnt, w.nchunk, w.cols,
                                                              w.n_cols);
       PS_LAUNCHED("b_sel_scatter");
-      b_prep_rows<T><<<dim3(grid_for(rup(nx, BM), 8), P), 256, 0, st>>>(in, w, pass, 0);
+      b_prep_rows<T><<<dim3(per(grid_for(rup(nx, BM), 8), P), P), 256, 0, st>>>(in, w, pass, 0);
       PS_LAUNCHED("b_prep_rows(columns)");
     }
     const int64_t rb = (nx + BM - 1) / BM, tiles = (ny + BN - 1) / BN;
     const int split = batch_split(P, rb, tiles);
     b_topk<0, T><<<dim3(rb, split, P), kThreads, smem_bytes<0>(), st>>>(in, w, pass);
     PS_LAUNCHED("b_topk<top4>");
-    b_certify<T><<<dim3(grid_for(nx, 32), P), 256, 0, st>>>(in, w, pass, kParts * split, rb * BM);
+    b_certify<T><<<dim3(per(grid_for(nx, 32), P), P), 256, 0, st>>>(in, w, pass, kParts * split, rb * BM);
     PS_LAUNCHED("b_certify");
-    b_gather<T><<<dim3(grid_for(nx, 256), P), 256, 0, st>>>(in, w, pass);
+    b_gather<T><<<dim3(per(grid_for(nx, 256), P), P), 256, 0, st>>>(in, w, pass);
     PS_LAUNCHED("b_gather");
     // near-tie rows: the first enum_rows of each pair enumerated on the
     // tensor cores, the rest (and overflowing enumerations) scanned exactly
     const int eb = (int)std::min<int64_t>(kEnumBlocksAsync, rb);
     const int enum_rows = eb * BM;
-    b_prep_rows<T><<<dim3(grid_for(enum_rows, 8), P), 256, 0, st>>>(in, w, pass, 1);
+    b_prep_rows<T><<<dim3(per(grid_for(enum_rows, 8), P), P), 256, 0, st>>>(in, w, pass, 1);
     PS_LAUNCHED("b_prep_rows(overflow)");
     const int split_e = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)kMaxSplit, tiles, 4 * kSMs / (P * eb)}));
     b_topk<1, T><<<dim3(eb, split_e, P), kThreads, smem_bytes<1>(), st>>>(in, w, pass);
@@ -1623,7 +1629,7 @@ int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1
     b_exact_rows<T><<<dim3(std::max(2, 148 * 4 / P), P), 256, 0, st>>>(in, w, pass, enum_rows);
     PS_LAUNCHED("b_exact_rows");
   }
-  b_accept<T><<<dim3(grid_for(N, 256), P), 256, 0, st>>>(in, w, delta_s);
+  b_accept<T><<<dim3(per(grid_for(N, 256), P), P), 256, 0, st>>>(in, w, delta_s);
   PS_LAUNCHED("b_accept");
   b_rank_out<<<dim3((stride + 31) / 32, P), 256, 0, st>>>(w, stride, ref1, ref2, delta, out_count);
   PS_LAUNCHED("b_rank_out");

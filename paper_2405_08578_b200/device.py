@@ -630,6 +630,38 @@ def ransac_async_dev(src: torch.Tensor, dst: torch.Tensor, n_dev: torch.Tensor, 
                                        wsb.value, sp), "ransac")
 
 
+def register_batch_async(jobs, ref1: torch.Tensor, ref2: torch.Tensor, count: torch.Tensor, iterations: int,
+                         inlier_tol: float, min_inliers: int, out: torch.Tensor, stream=None) -> None:
+    """Point gather + RANSAC of many matched pairs as one launch per stage
+    (ps_register_batch_async; results equal pair_points_dev +
+    ransac_async_dev pair by pair).  ``jobs`` = [(row1, col1, row2, col2,
+    n_cap, seed) or None (skipped), ...] for the rows of ``ref1`` / ``ref2``
+    (int32 [P, S]) and ``count`` (int64 [P]); pair q's ``ransac_async``
+    result block goes to ``out[q]`` (float64 [P, >= 8 + ceil(S / 8)])."""
+    if iterations < 1 or inlier_tol <= 0 or min_inliers < 2:
+        raise ConfigError("invalid RANSAC parameters")
+    P, S = int(ref1.shape[0]), int(ref1.shape[1])
+    L = _lib.lib()
+    m64 = (1 << 64) - 1
+    for q0 in range(0, P, BATCH_MAX_PAIRS):
+        q1 = min(P, q0 + BATCH_MAX_PAIRS)
+        arr = (_lib.RegisterPairC * (q1 - q0))()
+        for k, job in enumerate(jobs[q0:q1]):
+            if job is None:
+                continue
+            r1, c1, r2, c2, n_cap, seed = job
+            st, inc, has_u32, u32 = _pcg_state(int(seed))
+            arr[k] = _lib.RegisterPairC(r1.data_ptr(), c1.data_ptr(), r2.data_ptr(), c2.data_ptr(), int(n_cap),
+                                        st >> 64, st & m64, inc >> 64, inc & m64, has_u32, u32, 1)
+        wsb = C.c_size_t()
+        _lib.check(L.ps_register_batch_plan(q1 - q0, S, int(iterations), C.byref(wsb)), "register_batch")
+        ws = _workspace(wsb.value, ref1.device)
+        _lib.check(L.ps_register_batch_async(q1 - q0, arr, _ptr(ref1[q0:]), _ptr(ref2[q0:]), S, _ptr(count[q0:]),
+                                             int(iterations), float(inlier_tol), int(min_inliers), _ptr(out[q0:]),
+                                             int(out.stride(0)), _ptr(ws), wsb.value,
+                                             C.c_void_p(_stream_ptr(stream))), "register_batch")
+
+
 def ransac_result(h: torch.Tensor, n: int) -> RansacOutcome:
     """Decode a host copy of a ``ransac_async`` result block."""
     model_h, rms_h = h[0:3].numpy(), float(h[3])

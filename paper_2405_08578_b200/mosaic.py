@@ -119,9 +119,16 @@ class GpuEngine:
         streams = self._streams()
         counts = torch.zeros(len(items), dtype=torch.int64, device=self.device)
         caps = [min(int(it[3]), int(it[7])) for it in items]
-        if self.batch_match and all(it[2].dim() == 2 and int(it[2].shape[1]) == 128 for it in items):
-            # one launch sequence for every pair; an image's descriptor set
-            # (same rows at the same address) is grouped and tiled once
+        width = 8 + (max(caps + [8]) + 7) // 8
+        block = torch.zeros((len(items), width), dtype=torch.float64, device=self.device)
+        rcs = [cfg.ransac_config(it[8]) for it in items]
+        live = [caps[q] >= rcs[q].min_inliers for q in range(len(items))]  # registration.py:158-162
+        same = len({(rc.iterations, rc.inlier_tol, rc.min_inliers) for rc in rcs}) == 1
+        if self.batch_match and same and all(it[2].dim() == 2 and int(it[2].shape[1]) == 128 for it in items):
+            # the whole phase as two launch sequences on the current stream:
+            # every pair's match (an image's descriptor set -- same rows at the
+            # same address -- grouped and tiled once), then every pair's point
+            # gather + RANSAC
             sets, index, pairs = [], {}, []
             for it in items:
                 ends = []
@@ -132,27 +139,23 @@ class GpuEngine:
                         sets.append(d[:n])
                     ends.append(index[key])
                 pairs.append(tuple(ends))
-            r1, r2, dl, _ = device.match_batch_async(sets, pairs, mc.delta_s, out_count=counts)
-            outs = [(r1[q, :c], r2[q, :c], dl[q, :c]) for q, c in enumerate(caps)]
-            for s in streams or ():
-                for t in (r1, r2, counts):
-                    t.record_stream(s)
-        else:
-            outs = device.match_many_async([(it[2][: it[3]], it[6][: it[7]]) for it in items], mc.delta_s, counts,
-                                           streams=streams)
-        width = 8 + (max(caps + [8]) + 7) // 8
-        block = torch.zeros((len(items), width), dtype=torch.float64, device=self.device)
-        live = [False] * len(items)
+            r1, r2, _, _ = device.match_batch_async(sets, pairs, mc.delta_s, out_count=counts)
+            jobs = [(it[0], it[1], it[4], it[5], caps[q], rcs[q].seed) if live[q] else None
+                    for q, it in enumerate(items)]
+            rc = rcs[0]
+            device.register_batch_async(jobs, r1, r2, counts, rc.iterations, rc.inlier_tol, rc.min_inliers, block)
+            return block, live
+        outs = device.match_many_async([(it[2][: it[3]], it[6][: it[7]]) for it in items], mc.delta_s, counts,
+                                       streams=streams)
         cur = torch.cuda.current_stream(self.device)
         if streams:
             ready = cur.record_event()
             for s in streams:
                 s.wait_event(ready)
         for q, (it, (r1, r2, _)) in enumerate(zip(items, outs)):
-            rc = cfg.ransac_config(it[8])
-            if caps[q] < rc.min_inliers:  # cannot reach min_inliers whatever the count (registration.py:158-162)
+            rc = rcs[q]
+            if not live[q]:
                 continue
-            live[q] = True
             s = streams[q % len(streams)] if streams else None
             with torch.cuda.stream(s) if s is not None else _nullcontext():
                 src, dst = device.pair_points_dev(r1, r2, counts[q:q + 1], it[0], it[1], it[4], it[5])

@@ -146,3 +146,45 @@ def test_batch_graph_replay_c5_pairs():
     again = eng.register_many(items)  # replay
     ref = [eng.register(*it) for it in items]
     assert first == again == ref
+
+
+def test_register_batch_equals_per_pair_ransac():
+    """ps_register_batch_async vs pair_points_dev + ransac_async_dev per pair:
+    rigid pairs with outliers, a pair whose count is below min_inliers, a
+    skipped pair; identical result blocks (model, rms, status words, mask)."""
+    rng = np.random.default_rng(21)
+    P, S, iters, tol, min_in = 5, 600, 500, 3.0, 4
+    kp = []  # per pair: (row1, col1, row2, col2) int32 device arrays
+    r1 = torch.zeros((P, S), dtype=torch.int32)
+    r2 = torch.zeros((P, S), dtype=torch.int32)
+    counts = torch.tensor([S, 400, 3, 250, S], dtype=torch.int64)
+    for q in range(P):
+        n1, n2 = 900, 800
+        rows1, cols1 = rng.integers(0, 1600, n1), rng.integers(0, 2688, n1)
+        th, tx, ty = rng.uniform(-0.1, 0.1), rng.uniform(-300, 300), rng.uniform(-200, 200)
+        # image-2 keypoints: a rigid map of image-1 keypoints (rounded) plus clutter
+        idx = rng.permutation(n1)[:n2]
+        x2 = np.cos(th) * cols1[idx] - np.sin(th) * rows1[idx] + tx
+        y2 = np.sin(th) * cols1[idx] + np.cos(th) * rows1[idx] + ty
+        out = rng.random(n2) < 0.3
+        x2 = np.where(out, rng.integers(0, 2688, n2), np.rint(x2))
+        y2 = np.where(out, rng.integers(0, 1600, n2), np.rint(y2))
+        kp.append(tuple(torch.from_numpy(np.asarray(a, dtype=np.int32)).cuda() for a in (rows1, cols1, y2, x2)))
+        m = int(counts[q])
+        sel = rng.permutation(n2)[:m]
+        r1[q, :m] = torch.from_numpy(idx[sel].astype(np.int32))
+        r2[q, :m] = torch.from_numpy(sel.astype(np.int32))
+    r1, r2, counts = r1.cuda(), r2.cuda(), counts.cuda()
+    width = 8 + (S + 7) // 8
+    got = torch.zeros((P, width), dtype=torch.float64, device="cuda")
+    jobs = [(kp[q][0], kp[q][1], kp[q][2], kp[q][3], S, 100 + q) if q != 4 else None for q in range(P)]
+    device.register_batch_async(jobs, r1, r2, counts, iters, tol, min_in, got)
+    want = torch.zeros((P, width), dtype=torch.float64, device="cuda")
+    for q in range(4):
+        src, dst = device.pair_points_dev(r1[q], r2[q], counts[q:q + 1], *kp[q])
+        device.ransac_async_dev(src, dst, counts[q:q + 1], S, iters, tol, min_in, 100 + q, want[q])
+    torch.cuda.synchronize()
+    assert torch.equal(got.view(torch.uint8), want.view(torch.uint8))
+    info = got[:, 4:8].contiguous().view(torch.int64).cpu().numpy()
+    assert info[0, 0] == 0 and info[2, 0] != 0 and info[0, 2] > 300  # registered / too few pairs
+    assert not got[4].any()  # skipped pair untouched

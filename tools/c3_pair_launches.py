@@ -19,7 +19,8 @@ torch.cuda.synchronize()
 (pg,) = eng._pair_graphs.values()
 (ent,) = eng._prep_graphs.values()
 torch.cuda.profiler.start()
-ent["graph"].replay()
+for g in ent["graphs"]:
+    g.replay()
 pg[0].replay()
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
