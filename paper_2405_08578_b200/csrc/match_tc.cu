@@ -1218,7 +1218,6 @@ BatchWs carve_batch(void* base, int64_t S, int64_t P, int64_t n, size_t* used) {
   w.xt = ar.take<uint8_t>(S * w.xrows * ROW_BYTES);
   w.xinfo = ar.take<double>(S * 3 * w.xrows);
   w.yt = ar.take<uint8_t>(S * w.yrows * ROW_BYTES);
-  w.yinfo = ar.take<double>(S * 3 * w.yrows);
   w.ymax = ar.take<unsigned>(S * 4);
   w.topv = ar.take<float>(P * w.lists * w.xrows * TOPK);
   w.topj = ar.take<int32_t>(P * w.lists * w.xrows * TOPK);
@@ -1282,13 +1281,106 @@ __device__ __forceinline__ PassView<T> pass_view(const BatchIn<T>& in, const Bat
   return v;
 }
 
-// per-set stages (blockIdx.y = set; sets in no pair are skipped)
+// per-set stages (blockIdx.y = set; sets in no pair are skipped).  A
+// half-warp owns a row (lane hl: elements 8 hl .. 8 hl + 7, two 16-byte
+// loads), so a warp keeps two rows' loads and reductions in flight.
+template <class T>
+__device__ __forceinline__ void load8(const T* __restrict__ row, int hl, double (&x)[8]) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 v0 = __ldg(reinterpret_cast<const float4*>(row) + 2 * hl);
+    const float4 v1 = __ldg(reinterpret_cast<const float4*>(row) + 2 * hl + 1);
+    x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
+    x[4] = v1.x; x[5] = v1.y; x[6] = v1.z; x[7] = v1.w;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(row) + 4 * hl + k);
+      x[2 * k] = v.x;
+      x[2 * k + 1] = v.y;
+    }
+  }
+}
+
+// hash_insert with a half-warp per row (same hash: a sum over the elements).
+// Each half-warp walks a contiguous run of rows two at a time, so "identical
+// to the previous row" is tested on the hash keys it already holds: a row
+// whose key equals its predecessor's skips the minimum update (the run's
+// first row, the smallest index with that key in the run, competes; equal
+// keys share a slot, so every slot still receives the smallest index of
+// its key) -- one row load per row instead of two.
+template <class T>
+__device__ __forceinline__ unsigned long long row_hash(const double (&xv)[8], int hl, unsigned hmask) {
+  unsigned long long h = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const T v = (T)xv[e];
+    unsigned long long bits;
+    if (sizeof(T) == 8) bits = (unsigned long long)__double_as_longlong((double)v);
+    else bits = (unsigned long long)__float_as_uint((float)v);
+    unsigned long long z = bits + 0x9E3779B97F4A7C15ull * (unsigned long long)(hl * 8 + e + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    h += z ^ (z >> 31);
+  }
+#pragma unroll
+  for (int o = 8; o; o >>= 1) h += __shfl_xor_sync(hmask, h, o);
+  return h | 1ull;  // 0 marks an empty slot
+}
+
+__device__ __forceinline__ void hash_put(unsigned long long key, bool compete, int64_t i,
+                                         unsigned long long* __restrict__ tkey, int32_t* __restrict__ tidx,
+                                         int64_t tsize, int32_t* __restrict__ slot_of) {
+  int64_t slot = (int64_t)((key >> 20) & (unsigned long long)(tsize - 1));
+  for (;;) {  // plain read first: duplicate rows find their slot without an atomic
+    unsigned long long prev = *(volatile unsigned long long*)(tkey + slot);
+    if (prev == 0ull) prev = atomicCAS(tkey + slot, 0ull, key);
+    if (prev == 0ull || prev == key) break;
+    slot = (slot + 1) & (tsize - 1);
+  }
+  if (compete && *(volatile int32_t*)(tidx + slot) > (int32_t)i) atomicMin(tidx + slot, (int32_t)i);
+  slot_of[i] = (int32_t)slot;
+}
+
 template <class T>
 __global__ void b_hash(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
   const int64_t s = blockIdx.y;
   if (!in.role[s]) return;
-  hash_insert_body<T>(in.desc[s], in.rows[s], w.tkey + s * w.tsize, w.tidx + s * w.tsize, w.tsize,
-                      w.slot_of + s * w.n);
+  const T* X = in.desc[s];
+  const int64_t n = in.rows[s], tsize = w.tsize;
+  unsigned long long* tkey = w.tkey + s * tsize;
+  int32_t* tidx = w.tidx + s * tsize;
+  int32_t* slot_of = w.slot_of + s * w.n;
+  const int hl = threadIdx.x & 15;
+  const unsigned hmask = (threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu;
+  const int64_t halves = (int64_t)gridDim.x * (blockDim.x >> 4);
+  const int64_t hw = (int64_t)blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4);
+  const int64_t run = (n + halves - 1) / halves;
+  const int64_t i0 = hw * run, i1 = min(n, i0 + run);
+  if (i0 >= i1) return;  // uniform per half-warp
+  unsigned long long prev = 0ull;  // key of row i0 - 1 (none: 0 never equals a key)
+  if (i0 > 0) {
+    double xv[8];
+    load8(X + (i0 - 1) * KD, hl, xv);
+    prev = row_hash<T>(xv, hl, hmask);
+  }
+  // 16 rows' keys per round (lane k keeps row base + k's), then the 16 table
+  // inserts run in parallel, one per lane
+  const int hbase = threadIdx.x & 16;
+  for (int64_t base = i0; base < i1; base += 16) {
+    const int m = (int)min((int64_t)16, i1 - base);
+    unsigned long long mine = 0ull;
+#pragma unroll 4
+    for (int k = 0; k < m; ++k) {
+      double xv[8];
+      load8(X + (base + k) * KD, hl, xv);
+      const unsigned long long key = row_hash<T>(xv, hl, hmask);
+      if (hl == k) mine = key;
+    }
+    unsigned long long before = __shfl_sync(hmask, mine, hbase + ((hl + 15) & 15));
+    if (hl == 0) before = prev;
+    if (hl < m) hash_put(mine, mine != before, base + hl, tkey, tidx, tsize, slot_of);
+    prev = __shfl_sync(hmask, mine, hbase + m - 1);
+  }
 }
 
 template <class T>
@@ -1299,16 +1391,120 @@ __global__ void b_reps(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
                           w.flag + s * w.n);
 }
 
+__device__ __forceinline__ int64_t rup_dev(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// Both operand forms of a set's distinct rows from one read (prep_tiles'
+// arithmetic): the Y-form tiles (every set in a pair), the X-form tiles (sets
+// that are some pair's set a), the row norms (xinfo) and the Y maxima.
 template <class T>
-__global__ void b_prep_sets(const __grid_constant__ BatchIn<T> in, const BatchWs w, int is_y) {
+__global__ void b_prep_sets(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
   const int64_t s = blockIdx.y;
-  if (is_y ? !in.role[s] : !(in.role[s] & 1)) return;  // uniform per block
-  if (is_y)
-    prep_tiles_body<T>(in.desc[s], w.uniq + s * w.n, w.n_uniq + s, 0, w.yrows, BN, w.yt + s * w.yrows * ROW_BYTES,
-                       w.yinfo + s * 3 * w.yrows, w.ymax + 4 * s, 1, BN);
-  else
-    prep_tiles_body<T>(in.desc[s], w.uniq + s * w.n, w.n_uniq + s, 0, w.xrows, BMH, w.xt + s * w.xrows * ROW_BYTES,
-                       w.xinfo + s * 3 * w.xrows, nullptr, 0, BM);
+  const int role = in.role[s];
+  if (!role) return;  // uniform per block
+  const bool want_x = role & 1;
+  const T* src = in.desc[s];
+  const int32_t* idx = w.uniq + s * w.n;
+  const int64_t count = w.n_uniq[s];
+  uint8_t* xt = w.xt + s * w.xrows * ROW_BYTES;
+  uint8_t* yt = w.yt + s * w.yrows * ROW_BYTES;
+  double* info = w.xinfo + s * 3 * w.xrows;
+  const int64_t n_used_y = min(w.yrows, rup_dev(count, BN)), n_used_x = min(w.xrows, rup_dev(count, BM));
+  const int hl = threadIdx.x & 15;
+  const unsigned hmask = (threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu;
+  float mx0 = 0.0f, mx1 = 0.0f, mx2 = 0.0f;
+  for (int64_t u = (int64_t)blockIdx.x * (blockDim.x >> 4) + (threadIdx.x >> 4); u < n_used_y;
+       u += (int64_t)gridDim.x * (blockDim.x >> 4)) {
+    const bool live = u < count;
+    double x[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    if (live) load8(src + (int64_t)idx[u] * KD, hl, x);
+    __half h[8];
+    double sx = 0.0, sr = 0.0, sh = 0.0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      h[e] = __double2half(x[e]);
+      const double hv = (double)__half2float(h[e]);
+      const double rv = x[e] - hv;
+      sx += x[e] * x[e];
+      sr += rv * rv;
+      sh += hv * hv;
+    }
+#pragma unroll
+    for (int o = 8; o; o >>= 1) {
+      sx += __shfl_xor_sync(hmask, sx, o);
+      sr += __shfl_xor_sync(hmask, sr, o);
+      sh += __shfl_xor_sync(hmask, sh, o);
+    }
+    uint4 px, py;  // 8 fp16: x_h (X form) and -2 x_h (Y form, exact)
+    {
+      __half2 p[4], q[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        p[k] = __halves2half2(h[2 * k], h[2 * k + 1]);
+        q[k] = __hmul2(p[k], __float2half2_rn(-2.0f));
+      }
+      px = make_uint4(*reinterpret_cast<uint32_t*>(&p[0]), *reinterpret_cast<uint32_t*>(&p[1]),
+                      *reinterpret_cast<uint32_t*>(&p[2]), *reinterpret_cast<uint32_t*>(&p[3]));
+      py = make_uint4(*reinterpret_cast<uint32_t*>(&q[0]), *reinterpret_cast<uint32_t*>(&q[1]),
+                      *reinterpret_cast<uint32_t*>(&q[2]), *reinterpret_cast<uint32_t*>(&q[3]));
+    }
+    {  // Y form
+      const int64_t tile = u / BN;
+      const int r = (int)(u % BN);
+      uint8_t* base = yt + tile * (int64_t)BN * ROW_BYTES;
+      *reinterpret_cast<uint4*>(base + sw128_offset(BN, r, hl * 8)) = py;
+      if (hl < 2) {
+        uint4 q = make_uint4(0u, 0u, 0u, 0u);
+        if (hl == 0) {
+          __half a0, a1, a2;
+          if (!live) {
+            a0 = __float2half(INFINITY);
+            a1 = a2 = __float2half(0.0f);
+          } else {
+            a0 = __double2half(sx);
+            const double r1 = __hisinf(a0) ? 0.0 : sx - (double)__half2float(a0);
+            a1 = __double2half(r1);
+            a2 = __double2half(r1 - (double)__half2float(a1));
+          }
+          const __half2 q0 = __halves2half2(a0, a1), q1 = __halves2half2(a2, __float2half(0.0f));
+          q.x = *reinterpret_cast<const uint32_t*>(&q0);
+          q.y = *reinterpret_cast<const uint32_t*>(&q1);
+        }
+        *reinterpret_cast<uint4*>(base + BN * KD * 2 + (r >> 3) * 256 + hl * 128 + (r & 7) * 16) = q;
+      }
+    }
+    if (want_x && u < n_used_x) {  // X form
+      const int64_t tile = u / BMH;
+      const int r = (int)(u % BMH);
+      uint8_t* base = xt + tile * (int64_t)BMH * ROW_BYTES;
+      *reinterpret_cast<uint4*>(base + sw128_offset(BMH, r, hl * 8)) = px;
+      if (hl < 2) {
+        uint4 q = make_uint4(0u, 0u, 0u, 0u);
+        if (hl == 0) {
+          const __half2 one = __float2half2_rn(1.0f), q1 = __halves2half2(__float2half(1.0f), __float2half(0.0f));
+          q.x = *reinterpret_cast<const uint32_t*>(&one);
+          q.y = *reinterpret_cast<const uint32_t*>(&q1);
+        }
+        *reinterpret_cast<uint4*>(base + BMH * KD * 2 + (r >> 3) * 256 + hl * 128 + (r & 7) * 16) = q;
+      }
+    }
+    if (hl == 0 && live) {
+      info[3 * u + 0] = sqrt(sx);
+      info[3 * u + 1] = sqrt(sr);
+      info[3 * u + 2] = sqrt(sh);
+      mx0 = nan_max(mx0, (float)(sqrt(sx) * (1.0 + 1e-6)));
+      mx1 = nan_max(mx1, (float)(sqrt(sr) * (1.0 + 1e-6)));
+      mx2 = nan_max(mx2, (float)(sqrt(sh) * (1.0 + 1e-6)));
+    }
+  }
+  __shared__ float smx[3][64];
+  const int hw = threadIdx.x >> 4, nh = blockDim.x >> 4;
+  if (hl == 0) { smx[0][hw] = mx0; smx[1][hw] = mx1; smx[2][hw] = mx2; }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    float m = 0.0f;
+    for (int k = 0; k < nh; ++k) m = nan_max(m, smx[threadIdx.x][k]);
+    if (m != 0.0f) atomicMax(w.ymax + 4 * s + threadIdx.x, __float_as_uint(m));
+  }
 }
 
 // Order-preserving selection of the flagged indices of every segment in two
@@ -1572,7 +1768,7 @@ int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1
   PS_LAUNCHED("b_init");
   // per set: duplicate grouping, representatives, operand tiles
   const dim3 gs(per(grid_for(N, 8), S), S);
-  b_hash<T><<<gs, 256, 0, st>>>(in, w);
+  b_hash<T><<<dim3(per(grid_for(N, 16), S), S), 256, 0, st>>>(in, w);
   PS_LAUNCHED("b_hash");
   b_reps<T><<<gs, 256, 0, st>>>(in, w);
   PS_LAUNCHED("b_reps");
@@ -1580,10 +1776,8 @@ int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1
   PS_LAUNCHED("b_sel_count");
   b_sel_scatter<T, 0><<<dim3(w.nchunk, S), 256, 0, st>>>(in, w.flag, N, w.sel_cnt, w.nchunk, w.uniq, w.n_uniq);
   PS_LAUNCHED("b_sel_scatter");
-  b_prep_sets<T><<<dim3(per(grid_for(w.xrows, 8), S), S), 256, 0, st>>>(in, w, 0);
-  PS_LAUNCHED("b_prep_sets(X)");
-  b_prep_sets<T><<<dim3(per(grid_for(w.yrows, 8), S), S), 256, 0, st>>>(in, w, 1);
-  PS_LAUNCHED("b_prep_sets(Y)");
+  b_prep_sets<T><<<dim3(per(grid_for(w.yrows, 16), S), S), 256, 0, st>>>(in, w);
+  PS_LAUNCHED("b_prep_sets");
   cudaFuncSetAttribute(b_topk<0, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<0>());
   cudaFuncSetAttribute(b_topk<1, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<1>());
   for (int pass = 0; pass < 2; ++pass) {

@@ -71,8 +71,12 @@ def test_batch_sizes_and_edge_cases():
     c = _unit_rows(rng, 129)  # one past a row block
     d = _unit_rows(rng, 256 * 3 + 1, dup_every=2)  # half the rows identical
     e = torch.zeros((0, 128), dtype=torch.float32, device="cuda")
-    sets = [a, b, c, d, e]
-    pairs = [(0, 1), (1, 0), (1, 2), (2, 3), (3, 2), (3, 3), (0, 0), (4, 1), (1, 4)]
+    f = _unit_rows(rng, 3000)
+    for k in range(0, 3000, 37):  # runs of consecutive identical rows (flat regions), some chunk-straddling
+        f[k:k + 1 + k % 23] = f[k]
+    f[1500:1900] = f[1499]
+    sets = [a, b, c, d, e, f]
+    pairs = [(0, 1), (1, 0), (1, 2), (2, 3), (3, 2), (3, 3), (0, 0), (4, 1), (1, 4), (5, 3), (3, 5), (5, 5)]
     cnt = _check(sets, pairs, delta_s=10.0)  # every mutual pair accepted
     assert cnt[7] == 0 and cnt[8] == 0 and cnt[6] == 1
 
