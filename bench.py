@@ -75,6 +75,46 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
+def tensor_peak():
+    pj = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(pj):
+        with open(pj) as f:
+            return float(json.load(f)["bf16_tflops"]), "measured"
+    return 1641.9, "fallback"
+
+
+def pair_phase_evidence(geng, pair_rows, count_launches, reps=10):
+    """Device time of a GraphEngine's pair-phase graph (every pair's match ->
+    point gather -> RANSAC; CUDA events over back-to-back replays), the
+    library kernels one such phase launches (counted on an eager run:
+    ``count_launches()``), and the phase's tensor roofline: algorithmic
+    2 * 128 * n_a * n_b FLOPs of the pairs' distance matrices (what the
+    reference's _distance_matrix computes per pair) over the phase time.  The
+    tensor-core kernel b_topk (two passes) is 60-65 % of the serialised phase
+    (profiles/r02c_launches_c5_pairs.txt); the rest is certification,
+    grouping / tiling and RANSAC."""
+    import torch
+
+    g = next(iter(geng._pair_graphs.values()))[0]
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    flops = 2.0 * 128 * sum(float(a) * float(b) for a, b in pair_rows)
+    peak, src = tensor_peak()
+    ach = flops / (ms / 1e3) / 1e12
+    return {"pair_phase_ms": round(ms, 4), "pair_phase_launches": int(count_launches()),
+            "roofline": {"bound": "tensor", "kernel": "pair phase (b_topk tcgen05 passes + certification + RANSAC)",
+                         "achieved": round(ach, 2), "peak": peak, "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+                         "peak_source": src, "algorithmic_flops": flops,
+                         "note": "algorithmic 2*128*n_a*n_b per pair over the pair-phase graph replay (CUDA events)"}}
+
+
 # ---------------------------------------------------------------------------
 # CPU baseline: the oracle port, bounded sample
 # ---------------------------------------------------------------------------
@@ -262,11 +302,27 @@ def bench_c3_stitch(args, world, rank, dev, steps=3, with_cpu=False):
         torch.cuda.synchronize()
         t_alt.append(time.perf_counter() - t0)
     recaptured = (len(geng._prep_graphs), len(geng._pair_graphs)) != n_graphs
+    from paper_2405_08578_b200 import _lib
+
+    def c3_launches():  # library kernels of one eager pair phase (the graph replays the same sequence)
+        eng = mosaic.GpuEngine(cfg)
+        rows, cols, desc, cnt = eng.prepare(images[:9])
+        h = cnt.cpu().tolist()
+        items = [(rows[a], cols[a], desc[a], h[a], rows[b], cols[b], desc[b], h[b], 0)
+                 for a in range(9) for b in range(a + 1, 9)]
+        torch.cuda.synchronize()
+        l0 = _lib.kernel_launches()
+        eng._pairs_dev(items)
+        torch.cuda.synchronize()
+        return _lib.kernel_launches() - l0
+
+    cnt9 = geng.prepare(images)[3].cpu().tolist()
+    phase = pair_phase_evidence(geng, [(cnt9[a], cnt9[b]) for a in range(9) for b in range(a + 1, 9)], c3_launches)
     assert table.entries.keys() == table1.entries.keys() == table2.entries.keys()
     n_pairs = len(table.entries) // 2
     # control (untimed): the same generator with the perturbations off registers the overlapping pairs --
     # the timed set registers none because LP-SIFT's window peaks do not survive its rotation / noise
-    # (tools/c3_variants.py; the CPU oracle agrees pair by pair)
+    # (the live reference agrees pair by pair: tests/test_gpu_pairs.py, goldens from tests/golden/make_golden.py)
     ctl_images, _ = scenes.config3_images(0, rot_deg=0.0, scale_range=(1.0, 1.0), noise=0.0)
     ctl = mosaic.build_pairwise_table(ctl_images, cfg)
     _, ctl_placed = mosaic.plan_mosaic(ctl, ids)
@@ -290,10 +346,13 @@ def bench_c3_stitch(args, world, rank, dev, steps=3, with_cpu=False):
             "batched_eager_value": round(t_b, 4), "per_pair_calls_value": round(t_pp, 4),
             "alternating_frames_value": round(statistics.median(t_alt[1:]), 4), "alternating_frames_recaptured": recaptured,
             "batching": "value: mosaic.GraphEngine -- the 9 images (pinned host memory) uploaded every step, "
-                        "detect+describe and the whole pair phase (36 x match -> point gather -> RANSAC, the "
-                        "match counts feeding RANSAC on the device) replayed as two CUDA graphs over 4 streams, "
-                        "one result read; batched_eager_value: the same chain launched eagerly (one host sync for "
-                        "all pairs); per_pair_calls_value: one synchronous pair at a time",
+                        "detect+describe replayed as CUDA graphs (3-image chunks, uploads overlapped), the whole "
+                        "pair phase (36 pairs: ps_match_batch_async -- every image's descriptor set grouped and "
+                        "tiled once, one launch per stage for all pairs -- then ps_register_batch_async, the match "
+                        "counts feeding RANSAC on the device) replayed as one graph, one result read; "
+                        "batched_eager_value: the same chain launched eagerly; per_pair_calls_value: one "
+                        "synchronous pair at a time",
+            **phase,
             "n_gpus": world, "registered_pairs": n_pairs, "placed": len(placed),
             "rounds": len(plan.rounds), "unmatched": plan.final_unmatched,
             "control_translation_only_noise0": {"registered_pairs": len(ctl.entries) // 2, "placed": len(ctl_placed)},
@@ -540,6 +599,24 @@ def bench_c5_pairs(args, world, rank, dev, n_pairs=256, steps=2, with_cpu=False)
     dtb, stats = timed(run_batched)
     dt, statsg = timed(run_graph)
     dte, statse = timed(run_graph_e2e)
+    from paper_2405_08578_b200 import _lib
+
+    def c5_launches():  # library kernels of one eager pair phase (the graph replays the same sequence)
+        eng = mosaic.GpuEngine(cfg)
+        rows, cols, desc, cnt = eng._prepare_dev(allimg)
+        h = cnt.cpu().tolist()
+        items = [(rows[2 * q], cols[2 * q], desc[2 * q], h[2 * q], rows[2 * q + 1], cols[2 * q + 1],
+                  desc[2 * q + 1], h[2 * q + 1], cfg.seed) for q in range(len(grey))]
+        torch.cuda.synchronize()
+        l0 = _lib.kernel_launches()
+        eng._pairs_dev(items)
+        torch.cuda.synchronize()
+        return _lib.kernel_launches() - l0
+
+    phase = {}
+    if grey:
+        cn = geng.prepare_device(allimg)[3].cpu().tolist()
+        phase = pair_phase_evidence(geng, [(cn[2 * q], cn[2 * q + 1]) for q in range(len(grey))], c5_launches)
     assert [s[1] for s in statse] == [s[1] for s in statsg]
     assert [s[0] for s in stats[:n_sub]] == [s[0] for s in stats1]
     assert [s[1] for s in stats[:n_sub]] == [s[1] for s in stats1] and [s[1] for s in statsg] == [s[1] for s in stats]
@@ -551,10 +628,13 @@ def bench_c5_pairs(args, world, rank, dev, n_pairs=256, steps=2, with_cpu=False)
             "registered": int(sum(s[1] for s in stats)),
             "timing": "host wall clock, CUDA-synchronized, max over ranks; RGB inputs resident on the GPU",
             "batching": "value: mosaic.GraphEngine -- all local images detected + described in one replayed "
-                        "CUDA graph, one count read, then every pair's match -> point gather -> RANSAC chain "
-                        "(device-side counts) replayed as one graph over 8 streams, one result read; "
-                        "batched_eager_value: the same batches launched eagerly with one count and one result "
-                        "read-back; per_pair_calls_value: one synchronous pair at a time (first 16 pairs of each rank)",
+                        "CUDA graph, one count read, then the pair phase replayed as one graph: "
+                        "ps_match_batch_async (every pair's match, one launch per stage) and "
+                        "ps_register_batch_async (every pair's point gather + RANSAC on the device-side counts), "
+                        "one result read; batched_eager_value: detect/describe in one call, per-pair matcher and "
+                        "RANSAC launches over 4 streams with one count and one result read-back; "
+                        "per_pair_calls_value: one synchronous pair at a time (first 16 pairs of each rank)",
+            **phase,
             "ingest": "RGB8 pixel type: luma-key detection, host-built 2^24 grey table (ingest.py)",
             "e2e": {"value": round(n_pairs / dte, 3), "unit": "pairs/s",
                     "h2d_bytes_per_step": int(host_rgb.numel()) * world if grey else 0,
@@ -1129,7 +1209,7 @@ def run_ours(args):
         out = {
             "metric": "Mpixel/s LP-SIFT detect+describe", "value": round(value, 2), "unit": "Mpixel/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/f32",
             "data": "synthetic (seeded noise+shapes generator, paper_2405_08578_b200/scenes.py)",
             "config": {"workload": WORKLOAD, "images": args.images, "image_hw": [NR, NC], "scales": list(SCALES),
                        "keypoints_per_image": K, "descriptor": "float32 128-d", "l2": "inputs larger than L2",
