@@ -230,6 +230,7 @@ def bench_c4_matching(args, world=1, rank=0, dev=None, with_cpu=True, steps=5):
                         "note": ("executed fp16 tcgen05 FLOPs (issued MMA tiles) over the whole match call; the "
                                  "duplicate-row grouping removes most of the nominal 2*n1*n2*128")},
            "algorithmic_tflops_equivalent": round(flops / (ms / 1e3) / 1e12, 2),
+           "tmem_roofline": tmem_roofline(stats.get("mma_flops", 0), ms, dev),
            "tc_stats": stats,
            "exactness": "bit-exact vs float64 reference arithmetic (tests/test_gpu_parity.py P3)",
            "n_gpus": world, "parallelism": ("single GPU" if world == 1 else
@@ -873,7 +874,57 @@ def bench_c4_dense(args, rank, dev, steps=5):
                          "note": "algorithmic 2*n1*n2*128 over the whole call (both passes, the exact float64 "
                                  "certification and the ordering included); executed counts the fp16 MMA tiles "
                                  "issued (K = 144 incl. the |y|^2 augmentation)"},
+            "tmem_roofline": tmem_roofline(stats.get("mma_flops", 0), ms, dev),
             "timing": "CUDA events over %d back-to-back calls (each has one host count read)" % steps}
+
+
+_TMEM_PEAK = {}
+
+
+def tmem_probe(dev):
+    """Tensor-memory read bandwidth of this GPU (ps_probe_tmem_read, CUDA events)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2405_08578_b200 import _lib
+
+    if "gbs" in _TMEM_PEAK:
+        return _TMEM_PEAK
+    L = _lib.lib()
+    sink = torch.zeros(148, dtype=torch.int32, device=dev)
+    nb = C.c_double()
+    st = torch.cuda.current_stream()
+    for _ in range(2):
+        _lib.check(L.ps_probe_tmem_read(20000, 148, C.c_void_p(sink.data_ptr()), C.byref(nb),
+                                        C.c_void_p(st.cuda_stream)), "probe")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(5):
+        _lib.check(L.ps_probe_tmem_read(20000, 148, C.c_void_p(sink.data_ptr()), C.byref(nb),
+                                        C.c_void_p(st.cuda_stream)), "probe")
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    _TMEM_PEAK.update({"gbs": round(nb.value / (ms / 1e3) / 1e9, 1), "ms": round(ms, 3),
+                       "how": "ps_probe_tmem_read: 148 CTAs x 16 warps, two 64-column tcgen05.ld (32x32b.x64) per "
+                              "wait x 20000, all 512 TMEM columns allocated per SM, CUDA events"})
+    return _TMEM_PEAK
+
+
+def tmem_roofline(mma_flops, ms, dev):
+    """Tensor-memory read traffic of the tensor-core matcher against the
+    box's TMEM read bandwidth (ps_probe_tmem_read): the epilogue reads every
+    fp32 accumulator once (128 KB per 128 x 256 tile; tiles = executed MMA
+    FLOPs / (2 * 128 * 256 * 144)).  The fraction is small: the TMEM read
+    is NOT what bounds the kernel (K3 explains what does)."""
+    if not mma_flops:
+        return None
+    pk = tmem_probe(dev)
+    tiles = mma_flops / (2.0 * 128 * 256 * 144)
+    gbs = tiles * 128 * 256 * 4 / (ms / 1e3) / 1e9
+    return {"bound": "tmem-read (not binding)", "achieved": round(gbs, 1), "peak": pk["gbs"], "unit": "GB/s",
+            "frac": round(gbs / pk["gbs"], 4), "tiles": int(tiles), "probe": pk}
 
 
 def _bf16_peak():

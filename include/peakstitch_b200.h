@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 4
+#define PS_ABI_VERSION 5
 
 #if defined(__GNUC__)
 #define PS_API __attribute__((visibility("default")))
@@ -136,6 +136,12 @@ PS_API int ps_device_sync(void* stream);     /* cudaStreamSynchronize + error ch
  * the denominator of the describe kernel's compute roofline.
  * sink: device double[blocks] (never written in practice). */
 PS_API int ps_probe_fp64_fma(int64_t iters, int32_t blocks, double* sink, double* out_flops, void* stream);
+/* Roofline probe (bench.py): `blocks` CTAs (one per SM) each allocate all 512
+ * TMEM columns and 16 warps read them with 64-column tcgen05.ld, two per
+ * wait, `iters` times; *out_bytes = the bytes read.  Timed with events it is
+ * the tensor-memory read bandwidth that bounds the tensor-core matcher's
+ * epilogue (every fp32 distance accumulator is read once). */
+PS_API int ps_probe_tmem_read(int64_t iters, int32_t blocks, uint32_t* sink, double* out_bytes, void* stream);
 
 /* ---- detect: detector.py:154-172 --------------------------------------- */
 /* Validates the scale set (ScaleSet rules, detector.py:33-68) against the

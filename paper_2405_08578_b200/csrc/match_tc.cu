@@ -2034,3 +2034,45 @@ extern "C" int ps_match_batch_async(int32_t n_sets, const void* const* set_desc,
   if (rc) return rc;
   return ps::check_cuda("ps_match_batch_async");
 }
+
+// ---- roofline probe: tensor-memory read bandwidth -----------------------------------------
+// The nearest-neighbour epilogue must read every fp32 accumulator from TMEM
+// (128 KB per 128 x 256 tile) while the MMA of a tile (K = 144) takes 9 x 128
+// cycles: the TMEM read rate, not the MMA rate, bounds nn_topk_tc / b_topk.
+// One CTA per SM allocates all 512 columns; kWarps warps (4 per lane
+// quarter) each issue two 64-column tcgen05.ld per wait, `iters` times.
+namespace {
+constexpr int kProbeWarps = 16;
+__global__ void __launch_bounds__(kProbeWarps * 32, 1) tmem_read_probe(int64_t iters, uint32_t* sink) {
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) ps::tc::tmem_alloc(&slot, 512);
+  ps::tc::tc_fence_before();
+  __syncthreads();
+  ps::tc::tc_fence_after();
+  const uint32_t tmem = slot;
+  const int quarter = warp & 3, part = warp >> 2;  // 4 parts x 128 columns
+  const uint32_t base = tmem + ((uint32_t)(quarter * 32) << 16) + part * 128;
+  uint32_t acc = 0;
+  for (int64_t it = 0; it < iters; ++it) {
+    uint32_t a[64], b[64];
+    ps::tc::tmem_ld_cols(base, a);
+    ps::tc::tmem_ld_cols(base + 64, b);
+    ps::tc::tmem_ld_wait();
+#pragma unroll
+    for (int k = 0; k < 64; k += 8) acc ^= a[k] + b[k + 1];
+  }
+  if (acc == 0x9E3779B9u) sink[blockIdx.x] = acc;  // keeps the loads; practically never true
+  ps::tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) ps::tc::tmem_dealloc(tmem, 512);
+}
+}  // namespace
+
+extern "C" int ps_probe_tmem_read(int64_t iters, int32_t blocks, uint32_t* sink, double* out_bytes, void* stream) {
+  PS_REQUIRE(iters > 0 && blocks > 0 && sink && out_bytes, PS_ERR_ARGUMENT, "bad probe arguments");
+  tmem_read_probe<<<blocks, kProbeWarps * 32, 0, (cudaStream_t)stream>>>(iters, sink);
+  PS_LAUNCHED("tmem_read_probe");
+  *out_bytes = (double)blocks * kProbeWarps * (double)iters * 2.0 * 64 * 32 * 4;
+  return ps::check_cuda("tmem_read_probe");
+}
