@@ -350,7 +350,9 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
             const uint64_t bd = sdesc_k_sw128(b0 + (k >> 2) * (BN * 128) + koff);
             mma_f16(acc, ad, bd, idesc, k > 0 ? 1u : 0u);
           }
+#ifndef PS_TC_DIAG_NOAUG  // diagnostic builds only: without the |y|^2 augmentation step (wrong results)
           mma_f16(acc, sdesc_k_none(ah + BMH * KD * 2), sdesc_k_none(b0 + BN * KD * 2), idesc, 1u);
+#endif
         }
         mma_commit(b_empty + s);
         mma_commit(acc_full + ab);
@@ -374,6 +376,14 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
       tc_fence_after();
       const int tg = t_begin + (t + t_rot < n_tiles ? t + t_rot : t + t_rot - n_tiles);  // global tile index
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (ab * XH + h) * BN + part * kCols;
+#ifdef PS_TC_DIAG_NOEPI  // diagnostic builds only: the accumulator handshake without reading it (wrong results)
+      if (MODE == 0) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty + ab);
+        continue;
+      }
+#endif
       // Pruning bound shared by the row's kParts threads: every published 4th
       // best has four real values at or below it, so the row's final top-4
       // lies strictly below the smallest of them (ties at the bound cannot be
