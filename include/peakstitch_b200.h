@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 5
+#define PS_ABI_VERSION 6
 
 #if defined(__GNUC__)
 #define PS_API __attribute__((visibility("default")))
@@ -221,7 +221,12 @@ PS_API int ps_match_async(const void* desc1, int64_t n1, const void* desc2, int6
  * mosaic.py:79-112, calling match_features, matcher.py:57-95, per pair).
  * set_desc: host array of n_sets device pointers to [set_rows[s], 128]
  * row-major float32 (desc_is_f64 = 0) or float64 rows; pair_a / pair_b: host
- * int32 arrays of n_pairs set indices.  Each set's duplicate grouping and
+ * int32 arrays of n_pairs set indices.  set_count: NULL, or a host array of
+ * n_sets device int32 pointers (each NULL or the set's live row count,
+ * clamped to [0, set_rows[s]]): set_rows is then the set's capacity (grids,
+ * workspace, out_stride) and the kernels read the count on the device, so a
+ * captured graph stays valid when the counts change between replays (a
+ * camera rig's frames).  Each set's duplicate grouping and
  * tensor-core operand tiles are built once however many pairs it enters, and
  * every stage runs as one launch for all pairs.  Pair q's matches, sorted by
  * (delta, ref1, ref2), go to row q of out_ref1 / out_ref2 / out_delta (device
@@ -232,7 +237,7 @@ PS_API int ps_match_async(const void* desc1, int64_t n1, const void* desc2, int6
 PS_API int ps_match_batch_plan(int32_t n_sets, const int64_t* set_rows, int32_t n_pairs, int32_t dim,
                                size_t* workspace_bytes_out);
 PS_API int ps_match_batch_async(int32_t n_sets, const void* const* set_desc, const int64_t* set_rows,
-                                int32_t n_pairs, const int32_t* pair_a, const int32_t* pair_b, int32_t dim,
+                                const int32_t* const* set_count, int32_t n_pairs, const int32_t* pair_a, const int32_t* pair_b, int32_t dim,
                                 int32_t desc_is_f64, double delta_s, int32_t* out_ref1, int32_t* out_ref2,
                                 double* out_delta, int64_t out_stride, int64_t* out_count, void* workspace,
                                 size_t workspace_bytes, void* stream);

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpeakstit
 PS_OK, PS_ERR_CONFIG, PS_ERR_VALUE, PS_ERR_DEGENERATE, PS_ERR_REGISTRATION = 0, 1, 2, 3, 4
 PS_ERR_CUDA, PS_ERR_ARGUMENT, PS_ERR_CAPACITY = 5, 6, 7
 PS_PIXELS_U8, PS_PIXELS_F64, PS_PIXELS_F64_RAW, PS_PIXELS_RGB8 = 0, 1, 2, 3
-ABI_VERSION = 5
+ABI_VERSION = 6
 PS_MATCH_NEAREST, PS_MATCH_THRESHOLD_ALL, PS_MATCH_RATIO = 0, 1, 2
 PS_MATCH_FORCE_EXACT, PS_MATCH_FORCE_TC = 0x100, 0x200  # per-call path selection (OR-ed into the strategy)
 PS_DESCRIBE_AUTO, PS_DESCRIBE_GENERAL, PS_DESCRIBE_SINGLE, PS_DESCRIBE_PRECISE = 0, 1, 2, 3
@@ -86,7 +86,8 @@ SIGNATURES = {
                                           C.c_void_p, C.c_size_t, C.c_void_p]),
     "ps_match_batch_plan": (C.c_int, [C.c_int32, C.POINTER(C.c_int64), C.c_int32, C.c_int32,
                                       C.POINTER(C.c_size_t)]),
-    "ps_match_batch_async": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64), C.c_int32,
+    "ps_match_batch_async": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_void_p), C.c_int32,
                                        C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int32, C.c_int32,
                                        C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                        C.c_void_p, C.c_size_t, C.c_void_p]),

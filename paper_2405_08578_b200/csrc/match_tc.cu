@@ -1180,7 +1180,8 @@ constexpr int kBatchMaxPairs = 256;
 template <class T>
 struct BatchIn {  // kernel parameter (__grid_constant__): the sets and the pair list
   const T* desc[kBatchMaxSets];
-  int32_t rows[kBatchMaxSets];
+  int32_t rows[kBatchMaxSets];  // capacity (grids, workspace)
+  const int32_t* cnt[kBatchMaxSets];  // optional device row count (<= rows): the kernels use min(rows, *cnt)
   uint8_t role[kBatchMaxSets];  // bit 0: set a of some pair (X-form tiles), bit 1: set b of some pair
   int16_t pa[kBatchMaxPairs], pb[kBatchMaxPairs];
 };
@@ -1258,6 +1259,14 @@ BatchWs carve_batch(void* base, int64_t S, int64_t P, int64_t n, size_t* used) {
   return w;
 }
 
+// rows of set s the kernels work on: its device count when given (a graph
+// replayed on new frames sees the new counts), else the host row count
+template <class T>
+__device__ __forceinline__ int64_t set_n(const BatchIn<T>& in, int64_t s) {
+  const int64_t cap = in.rows[s];
+  return in.cnt[s] ? max((int64_t)0, min(cap, (int64_t)__ldg(in.cnt[s]))) : cap;
+}
+
 template <class T>
 struct PassView {  // pair q in pass 0 (distinct rows of a vs b) or 1 (matchable columns of b vs a)
   const T *X, *Y;
@@ -1287,7 +1296,7 @@ __device__ __forceinline__ PassView<T> pass_view(const BatchIn<T>& in, const Bat
   v.ymax = w.ymax + 4 * ys;
   v.nn = (pass ? w.nn21 : w.nn12) + qq * w.n;
   v.dist = (pass ? w.d21 : w.d12) + qq * w.n;
-  v.ny = in.rows[ys];
+  v.ny = set_n(in, ys);
   return v;
 }
 
@@ -1356,7 +1365,7 @@ __global__ void b_hash(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
   const int64_t s = blockIdx.y;
   if (!in.role[s]) return;
   const T* X = in.desc[s];
-  const int64_t n = in.rows[s], tsize = w.tsize;
+  const int64_t n = set_n(in, s), tsize = w.tsize;
   unsigned long long* tkey = w.tkey + s * tsize;
   int32_t* tidx = w.tidx + s * tsize;
   int32_t* slot_of = w.slot_of + s * w.n;
@@ -1397,7 +1406,7 @@ template <class T>
 __global__ void b_reps(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
   const int64_t s = blockIdx.y;
   if (!in.role[s]) return;
-  mark_reps_table_body<T>(in.desc[s], in.rows[s], w.tidx + s * w.tsize, w.slot_of + s * w.n, w.rep + s * w.n,
+  mark_reps_table_body<T>(in.desc[s], set_n(in, s), w.tidx + s * w.tsize, w.slot_of + s * w.n, w.rep + s * w.n,
                           w.flag + s * w.n);
 }
 
@@ -1522,7 +1531,7 @@ __global__ void b_prep_sets(const __grid_constant__ BatchIn<T> in, const BatchWs
 // pair g's columns (SEG 1), length rows[g] / rows[pb[g]].
 template <class T, int SEG>
 __device__ __forceinline__ int64_t seg_len(const BatchIn<T>& in, int g) {
-  return SEG == 0 ? (in.role[g] ? in.rows[g] : 0) : in.rows[in.pb[g]];
+  return SEG == 0 ? (in.role[g] ? set_n(in, g) : 0) : set_n(in, in.pb[g]);
 }
 
 __device__ __forceinline__ int block_sum256(int v, int* sh) {
@@ -1694,7 +1703,7 @@ __global__ void b_mark_columns(const __grid_constant__ BatchIn<T> in, const Batc
 template <class T>
 __global__ void b_accept(const __grid_constant__ BatchIn<T> in, const BatchWs w, double delta_s) {
   const int64_t q = blockIdx.y, sa = in.pa[q];
-  accept_pairs_body(w.rep + sa * w.n, in.rows[sa], w.nn12 + q * w.n, w.d12 + q * w.n, w.nn21 + q * w.n, delta_s,
+  accept_pairs_body(w.rep + sa * w.n, set_n(in, sa), w.nn12 + q * w.n, w.d12 + q * w.n, w.nn21 + q * w.n, delta_s,
                     w.kp + q * w.n, w.kd + q * w.n, w.counter + q);
 }
 
@@ -1986,15 +1995,17 @@ int64_t batch_rows_bound(int32_t n_sets, const int64_t* set_rows) {
   return n;
 }
 template <class T>
-int batch_run(int32_t n_sets, const void* const* set_desc, const int64_t* set_rows, int32_t n_pairs,
+int batch_run(int32_t n_sets, const void* const* set_desc, const int64_t* set_rows,
+              const int32_t* const* set_count, int32_t n_pairs,
               const int32_t* pair_a, const int32_t* pair_b, double delta_s, int32_t* out_ref1, int32_t* out_ref2,
               double* out_delta, int64_t out_stride, int64_t* out_count, void* ws, size_t ws_bytes,
               cudaStream_t st) {
-  static thread_local ps::tc::BatchIn<T> in;  // ~7 KB: not on the stack
+  static thread_local ps::tc::BatchIn<T> in;  // ~11 KB: not on the stack
   memset(&in, 0, sizeof(in));
   for (int s = 0; s < n_sets; ++s) {
     in.desc[s] = static_cast<const T*>(set_desc[s]);
     in.rows[s] = (int32_t)set_rows[s];
+    in.cnt[s] = set_count ? set_count[s] : nullptr;
   }
   for (int q = 0; q < n_pairs; ++q) {
     in.pa[q] = (int16_t)pair_a[q];
@@ -2018,7 +2029,7 @@ extern "C" int ps_match_batch_plan(int32_t n_sets, const int64_t* set_rows, int3
 }
 
 extern "C" int ps_match_batch_async(int32_t n_sets, const void* const* set_desc, const int64_t* set_rows,
-                                    int32_t n_pairs, const int32_t* pair_a, const int32_t* pair_b, int32_t dim,
+                                    const int32_t* const* set_count, int32_t n_pairs, const int32_t* pair_a, const int32_t* pair_b, int32_t dim,
                                     int32_t desc_is_f64, double delta_s, int32_t* out_ref1, int32_t* out_ref2,
                                     double* out_delta, int64_t out_stride, int64_t* out_count, void* workspace,
                                     size_t workspace_bytes, void* stream) {
@@ -2037,9 +2048,9 @@ extern "C" int ps_match_batch_async(int32_t n_sets, const void* const* set_desc,
                "pair %d: null descriptor set", q);
   }
   cudaStream_t st = (cudaStream_t)stream;
-  rc = desc_is_f64 ? batch_run<double>(n_sets, set_desc, set_rows, n_pairs, pair_a, pair_b, delta_s, out_ref1,
+  rc = desc_is_f64 ? batch_run<double>(n_sets, set_desc, set_rows, set_count, n_pairs, pair_a, pair_b, delta_s, out_ref1,
                                        out_ref2, out_delta, out_stride, out_count, workspace, workspace_bytes, st)
-                   : batch_run<float>(n_sets, set_desc, set_rows, n_pairs, pair_a, pair_b, delta_s, out_ref1,
+                   : batch_run<float>(n_sets, set_desc, set_rows, set_count, n_pairs, pair_a, pair_b, delta_s, out_ref1,
                                       out_ref2, out_delta, out_stride, out_count, workspace, workspace_bytes, st);
   if (rc) return rc;
   return ps::check_cuda("ps_match_batch_async");

@@ -404,7 +404,7 @@ def match_many(pairs, delta_s: float = 0.35, *, streams=None):
 BATCH_MAX_SETS, BATCH_MAX_PAIRS = 512, 256  # ps_match_batch_async limits per call
 
 
-def match_batch_async(sets, pairs, delta_s: float = 0.35, *, out_count=None, stream=None):
+def match_batch_async(sets, pairs, delta_s: float = 0.35, *, out_count=None, stream=None, set_counts=None):
     """nearest_neighbor matching of many pairs over shared descriptor sets as
     one launch sequence (ps_match_batch_async): each set's duplicate grouping
     and tensor-core operand tiles are built once however many pairs use it,
@@ -413,7 +413,12 @@ def match_batch_async(sets, pairs, delta_s: float = 0.35, *, out_count=None, str
     [(a, b), ...] set indices.  Returns (ref1 int32 [P, S], ref2 int32 [P, S],
     delta float64 [P, S], count int64 [P]) with S = max over pairs of
     min(n_a, n_b); row q holds pair q's matches in [0, count[q]), sorted by
-    (delta, ref1, ref2) -- the same as ``match`` pair by pair."""
+    (delta, ref1, ref2) -- the same as ``match`` pair by pair.
+
+    ``set_counts`` (optional): one device int32 tensor (1 element) or None
+    per set, the set's live row count; the set tensor is then its capacity and
+    the kernels read the count on the device, so a graph captured over this
+    call stays valid when the counts change between replays."""
     if delta_s <= 0:
         raise ConfigError(f"delta_s must be positive, got {delta_s}")
     P = len(pairs)
@@ -439,13 +444,21 @@ def match_batch_async(sets, pairs, delta_s: float = 0.35, *, out_count=None, str
         local = {s: i for i, s in enumerate(used)}
         S = len(used)
         ptrs = (C.c_void_p * S)(*[ds[s].data_ptr() for s in used])
+        cnts = None
+        if set_counts is not None:
+            for s in used:
+                c = set_counts[s]
+                if c is not None and (c.dtype != torch.int32 or c.device != dev or c.numel() < 1):
+                    raise ValueError("set_counts entries must be device int32 tensors on the sets' device")
+            cnts = (C.c_void_p * S)(*[set_counts[s].data_ptr() if set_counts[s] is not None else None
+                                      for s in used])
         rows_c = (C.c_int64 * S)(*[rows[s] for s in used])
         pa = (C.c_int32 * len(chunk))(*[local[a] for a, _ in chunk])
         pb = (C.c_int32 * len(chunk))(*[local[b] for _, b in chunk])
         wsb = C.c_size_t()
         _lib.check(L.ps_match_batch_plan(S, rows_c, len(chunk), 128, C.byref(wsb)), "match_batch")
         ws = _workspace(wsb.value, dev)
-        _lib.check(L.ps_match_batch_async(S, ptrs, rows_c, len(chunk), pa, pb, 128, int(dt == torch.float64),
+        _lib.check(L.ps_match_batch_async(S, ptrs, rows_c, cnts, len(chunk), pa, pb, 128, int(dt == torch.float64),
                                           float(delta_s), _ptr(r1[q0:]), _ptr(r2[q0:]), _ptr(dl[q0:]), stride,
                                           _ptr(cnt[q0:]), _ptr(ws), wsb.value, C.c_void_p(_stream_ptr(stream))),
                    "match_batch")

@@ -99,7 +99,10 @@ class GpuEngine:
 
     def register_many(self, items):
         """Every pair of ``items`` = [(ra, ca, da, na, rb, cb, db, nb, seed), ...]
-        with ONE host synchronisation: all matches, point gathers and RANSAC
+        (optionally + (count_a, count_b): device int32 keypoint counts; the
+        batched matcher then reads the counts on the device and sizes
+        everything by the slots' capacity, so a captured pair graph survives
+        frames whose counts differ) with ONE host synchronisation: all matches, point gathers and RANSAC
         runs are enqueued back to back (device.match_many_async, the match
         counts stay on the device and feed ransac_async_dev; pairs spread over
         ``self.streams``), then the result words of every pair are read at once."""
@@ -118,7 +121,11 @@ class GpuEngine:
         mc = cfg.matcher_config()
         streams = self._streams()
         counts = torch.zeros(len(items), dtype=torch.int64, device=self.device)
-        caps = [min(int(it[3]), int(it[7])) for it in items]
+        dev_cnt = all(len(it) > 9 for it in items) and self.batch_match
+        if dev_cnt:  # capacity-sized: the device counts decide (registration.py:158-162 on the device)
+            caps = [min(int(it[2].shape[0]), int(it[6].shape[0])) for it in items]
+        else:
+            caps = [min(int(it[3]), int(it[7])) for it in items]
         width = 8 + (max(caps + [8]) + 7) // 8
         block = torch.zeros((len(items), width), dtype=torch.float64, device=self.device)
         rcs = [cfg.ransac_config(it[8]) for it in items]
@@ -129,17 +136,23 @@ class GpuEngine:
             # every pair's match (an image's descriptor set -- same rows at the
             # same address -- grouped and tiled once), then every pair's point
             # gather + RANSAC
-            sets, index, pairs = [], {}, []
+            sets, index, pairs, set_counts = [], {}, [], []
             for it in items:
                 ends = []
-                for d, n in ((it[2], int(it[3])), (it[6], int(it[7]))):
-                    key = (d.data_ptr(), n, str(d.dtype))
+                sides = ((it[2], int(it[3]), it[9] if dev_cnt else None),
+                         (it[6], int(it[7]), it[10] if dev_cnt else None))
+                for d, n, c in sides:
+                    if c is not None:
+                        n = int(d.shape[0])
+                    key = (d.data_ptr(), n, str(d.dtype), c.data_ptr() if c is not None else 0)
                     if key not in index:
                         index[key] = len(sets)
                         sets.append(d[:n])
+                        set_counts.append(c)
                     ends.append(index[key])
                 pairs.append(tuple(ends))
-            r1, r2, _, _ = device.match_batch_async(sets, pairs, mc.delta_s, out_count=counts)
+            r1, r2, _, _ = device.match_batch_async(sets, pairs, mc.delta_s, out_count=counts,
+                                                    set_counts=set_counts if dev_cnt else None)
             jobs = [(it[0], it[1], it[4], it[5], caps[q], rcs[q].seed) if live[q] else None
                     for q, it in enumerate(items)]
             rc = rcs[0]
@@ -309,8 +322,13 @@ class GraphEngine(GpuEngine):
     def register_many(self, items):
         if self.cfg.matcher_config().strategy != "nearest_neighbor":
             return [self.register(*it) for it in items]
-        key = tuple((it[0].data_ptr(), it[1].data_ptr(), it[2].data_ptr(), int(it[3]), it[4].data_ptr(),
-                     it[5].data_ptr(), it[6].data_ptr(), int(it[7]), int(it[8])) for it in items)
+        if all(len(it) > 9 for it in items):  # device counts: keyed on capacities, not on this frame's counts
+            key = tuple((it[0].data_ptr(), it[1].data_ptr(), it[2].data_ptr(), int(it[2].shape[0]),
+                         it[9].data_ptr(), it[4].data_ptr(), it[5].data_ptr(), it[6].data_ptr(),
+                         int(it[6].shape[0]), it[10].data_ptr(), int(it[8])) for it in items)
+        else:
+            key = tuple((it[0].data_ptr(), it[1].data_ptr(), it[2].data_ptr(), int(it[3]), it[4].data_ptr(),
+                         it[5].data_ptr(), it[6].data_ptr(), int(it[7]), int(it[8])) for it in items)
         ent = self._pair_graphs.get(key)
         if ent is None:
             block, live = self._pairs_dev(items)  # eager warm-up; its results are this call's
@@ -456,8 +474,19 @@ def build_pairwise_table(images: Sequence, cfg, *, engine=None, group=None) -> P
 
     workers = getattr(engine, "pair_workers", 1)
     if getattr(engine, "batched", False) and hasattr(engine, "register_many"):
-        outs = engine.register_many([img(jobs[q][0]) + img(jobs[q][1]) + (pair_seed(cfg.seed, *jobs[q]),)
-                                     for q in mine_q])
+        # the device keypoint counts ride along (int32 slots): the batched
+        # matcher reads them on the device, so replayed pair graphs do not
+        # depend on this call's counts
+        dev_cnt = g_cnt.dtype == torch.int32 and getattr(engine, "batch_match", False)
+
+        def cnt(k):
+            return (g_cnt[k % world, k // world].reshape(1),) if dev_cnt else ()
+
+        items = []
+        for q in mine_q:
+            a, b = jobs[q]
+            items.append(img(a) + img(b) + (pair_seed(cfg.seed, a, b),) + (cnt(a) + cnt(b) if dev_cnt else ()))
+        outs = engine.register_many(items)
     elif workers > 1 and len(mine_q) > 1:
         import threading
         from concurrent.futures import ThreadPoolExecutor

@@ -22,7 +22,7 @@ def declared_symbols():
 
 
 def test_library_loads_and_reports_version():
-    assert _lib.lib().ps_abi_version() == _lib.ABI_VERSION == 5
+    assert _lib.lib().ps_abi_version() == _lib.ABI_VERSION == 6
 
 
 def test_every_declared_symbol_is_exported():

@@ -152,6 +152,39 @@ def test_batch_graph_replay_c5_pairs():
     assert first == again == ref
 
 
+def test_batch_graph_replay_with_device_counts_that_change():
+    """Items carrying device keypoint counts (build_pairwise_table's form):
+    the pair graph is keyed on slot capacities, so frames whose counts differ
+    replay the SAME graph (no re-capture) and still equal the per-pair path
+    on the truncated sets -- including a pair whose count falls below
+    min_inliers (RegistrationError decided on the device)."""
+    from paper_2405_08578_b200 import mosaic
+
+    cfg = PipelineConfig(window_min=16, window_max=64)
+    pairs = [scenes.config5_pair(k) for k in range(4)]
+    batch = torch.from_numpy(np.stack([im for a, b, _ in pairs for im in (a, b)])).cuda()
+    g = device.as_device_images(batch, rgb=True)
+    eng = mosaic.GraphEngine(cfg)
+    rows, cols, desc, count = eng.prepare_device(g)
+    full = count.cpu().tolist()
+    live = torch.zeros(len(full), dtype=torch.int32, device=count.device)  # the counts the graph reads
+    items = [(rows[2 * k], cols[2 * k], desc[2 * k], full[2 * k], rows[2 * k + 1], cols[2 * k + 1],
+              desc[2 * k + 1], full[2 * k + 1], 2000 + k, live[2 * k:2 * k + 1], live[2 * k + 1:2 * k + 2])
+             for k in range(len(pairs))]
+    rng = np.random.default_rng(4)
+    for frame in range(3):
+        n = [int(c) if frame == 0 else int(rng.integers(c // 3, c + 1)) for c in full]
+        if frame == 2:
+            n[0] = 5  # below min_inliers: no registration
+        live.copy_(torch.tensor(n, dtype=torch.int32))
+        got = eng.register_many(items)
+        assert len(eng._pair_graphs) == 1  # captured once, replayed for every frame
+        want = [eng.register(*it[:3], n[2 * k], *it[4:7], n[2 * k + 1], it[8]) for k, it in enumerate(items)]
+        assert got == want, frame
+        if frame == 2:
+            assert got[0][0] is False
+
+
 def test_register_batch_equals_per_pair_ransac():
     """ps_register_batch_async vs pair_points_dev + ransac_async_dev per pair:
     rigid pairs with outliers, a pair whose count is below min_inliers, a

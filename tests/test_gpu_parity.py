@@ -8,7 +8,9 @@ Bars:
      is expected <= 1e-12 away; the bar is the contract's);
   P3 matches on identical descriptors: (ref1, ref2) and delta bit-exact;
   P4 RANSAC: inlier list, consensus and success exact; transform within
-     1e-3 px at the image corners.
+     1e-3 px at the image corners;
+  P5 end to end: every match-set difference classified as a near-tie under the
+     measured descriptor perturbation (tests/match_diff.py), none unexplained.
 """
 
 import json
@@ -27,6 +29,7 @@ from paper_2405_08578_b200 import device, records as R, scenes  # noqa: E402
 from paper_2405_08578_b200 import matcher as Mt  # noqa: E402
 from paper_2405_08578_b200 import registration as Rg  # noqa: E402
 from paper_2405_08578_b200.errors import DegenerateSampleError, RegistrationError  # noqa: E402
+from match_diff import classify, ref_match_with_gaps  # noqa: E402
 
 P2_TOL = 1e-4
 KP = ("row", "col", "scale", "pol", "window", "value")
@@ -335,9 +338,16 @@ def test_end_to_end_small_pair(golden):
         preps.append(p)
     pairs, res, _, _ = register_prepared(preps[0], preps[1], cfg)
     assert res is not None
-    # P5: match set differences only among near-ties; inliers/transform
+    # P5: every match-set difference is a near-tie of the reference's distance
+    # matrix under the measured descriptor perturbation (tests/match_diff.py)
     want_pairs = set(zip(g["m__ref1"].tolist(), g["m__ref2"].tolist()))
     got_pairs = {(p.ref1, p.ref2) for p in pairs}
+    Ar, Br = (g[f"{t}__desc"].astype(np.float32).astype(np.float64) for t in "ab")  # the golden matched fp32 rows
+    (w1, w2, _), stats = ref_match_with_gaps(Ar, Br, cfg.delta_s)
+    assert set(zip(w1.tolist(), w2.tolist())) == want_pairs  # the classifier's matrix is the reference's
+    cls = classify(Ar, Br, *(p.descriptors.double().cpu().numpy() for p in preps), want_pairs, got_pairs,
+                   cfg.delta_s, stats)
+    assert cls["others"] == [], cls
     assert len(want_pairs ^ got_pairs) <= 0.02 * len(want_pairs)
     assert corner_error((res.transform.theta, res.transform.t_x, res.transform.t_y), g["r__model"], 384, 400) <= 1e-3
 
@@ -455,8 +465,9 @@ def test_nearest_tc_unnormalised_magnitudes(scale):
 
 
 def test_end_to_end_c1_against_oracle_chain():
-    """P5 at C1 size: keypoints exact, descriptors <= 1e-4, match-set
-    difference limited to near-ties (<= 5 %), identical RANSAC transform."""
+    """P5 at C1 size: keypoints exact, descriptors <= 1e-4, every match-set
+    difference classified as a near-tie ("others" = 0, tests/match_diff.py),
+    identical RANSAC transform."""
     a, b = scenes.config1_pair(0)
     cfg = R.DescriptorConfig(0.0625, 4, 64, True)
     ref, gpu = [], []
@@ -472,9 +483,15 @@ def test_end_to_end_c1_against_oracle_chain():
         g = gpu[-1][1].double().cpu().numpy()
         rel = np.max(np.abs(g - ref[-1][1]), axis=1) / np.maximum(np.linalg.norm(ref[-1][1], axis=1), 1e-300)
         assert rel.max() <= P2_TOL
-    w1, w2, _ = O.match(*(r[1].astype(np.float32).astype(np.float64) for r in ref))
+    Ar, Br = (r[1].astype(np.float32).astype(np.float64) for r in ref)
+    (w1, w2, _), stats = ref_match_with_gaps(Ar, Br, 0.35)
     r1, r2, _ = device.match(gpu[0][1], gpu[1][1])
     want, got = set(zip(w1.tolist(), w2.tolist())), set(zip(r1.cpu().numpy().tolist(), r2.cpu().numpy().tolist()))
+    # P5: classify every difference; none may be unexplained
+    cls = classify(Ar, Br, *(gg[1].double().cpu().numpy() for gg in gpu), want, got, 0.35, stats)
+    print(f"P5 C1: {len(want)} reference matches, {cls['diff']} differ: row ties {cls['row_tie']}, "
+          f"column ties {cls['col_tie']}, threshold {cls['threshold']}, others {len(cls['others'])}")
+    assert cls["others"] == [], cls["others"][:5]
     assert len(got ^ want) <= 0.05 * len(want)
     ref_r = O.ransac(*O.pair_points(w1, w2, ref[0][0], ref[1][0]), 1000, 3.0, 8, 0)
     src, dst = device.pair_points(r1, r2, gpu[0][0].row[0], gpu[0][0].col[0], gpu[1][0].row[0], gpu[1][0].col[0])

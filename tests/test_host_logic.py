@@ -235,3 +235,31 @@ def test_axis_sample_36bin_table_is_exact_for_8bit_gradients():
         t = tab[np.abs(da).astype(int), np.abs(db).astype(int)]
         got = np.where(b < 0, np.where(a < 0, 18 + t, 35 - t), np.where(a < 0, 17 - t, t))
         assert np.array_equal(got, want), (ca, cb)
+
+
+def test_p5_classifier_explains_perturbation_flips_and_flags_others():
+    """tests/match_diff.py (the P5 classifier): its one-pass match equals the
+    oracle's, every flip caused by a bounded descriptor perturbation is a
+    near-tie, and a pair no tie explains lands in ``others``."""
+    from match_diff import classify, ref_match_with_gaps
+
+    rng = np.random.default_rng(5)
+    A = rng.random((300, 128))
+    A /= np.linalg.norm(A, axis=1, keepdims=True)
+    # rows 0..49 have two candidates at nearly equal distance: flips happen
+    B = np.concatenate([A[:200] + rng.normal(0, 0.01, (200, 128)), A[:50] + rng.normal(0, 0.01, (50, 128)),
+                        rng.random((100, 128))])
+    B[250] = B[251]  # an exact column tie
+    B /= np.linalg.norm(B, axis=1, keepdims=True)
+    (w1, w2, wd), stats = ref_match_with_gaps(A, B, 0.35)
+    o1, o2, od = O.match(A, B, 0.35)
+    assert np.array_equal(w1, o1) and np.array_equal(w2, o2) and np.array_equal(wd, od)
+    Ag = (A + rng.normal(0, 3e-3, A.shape)).astype(np.float32)
+    Bg = (B + rng.normal(0, 3e-3, B.shape)).astype(np.float32)
+    g1, g2, _ = O.match(Ag.astype(np.float64), Bg.astype(np.float64), 0.35)
+    want, got = set(zip(w1.tolist(), w2.tolist())), set(zip(g1.tolist(), g2.tolist()))
+    res = classify(A, B, Ag, Bg, want, got, 0.35, stats)
+    assert res["diff"] == len(want ^ got) >= 5 and res["others"] == []
+    # a far-from-tie pair inserted by hand is not explained
+    bad = classify(A, B, A, B, want, got | {(0, 299)}, 0.35, stats)
+    assert (0, 299) in {(i, j) for i, j, _ in bad["others"]}
