@@ -209,6 +209,21 @@ __global__ void prep_tiles(const T* __restrict__ src, const int32_t* __restrict_
 }
 
 
+// The certified error bound of a row's v values (see certify_exact_body):
+// |v - (d^2 - |x|^2)| <= E for every column.  rx = |x - x_h|, hx = |x_h|;
+// ymax = float bits of max |y|, max |y - y_h|, max |y_h| over the columns.
+// Out of the fp16 range (|y|^2 split to inf, or elements): no certificate (inf).
+__device__ __forceinline__ double cert_bound(double rx, double hx, const unsigned* __restrict__ ymax) {
+  const double Nmax = __uint_as_float(ymax[0]), Rmax = __uint_as_float(ymax[1]), Hmax = __uint_as_float(ymax[2]);
+  // v = fp32-accumulated sum of 144 fp16 products: x_h . (-2 y_h) plus the
+  // three-term split of |y|^2 (split error <= 2^-33 |y|^2 + fp16 underflow)
+  const double gamma = 144.0 * 2.384185791015625e-07;  // 144 * 2^-22 (fp32 accumulation)
+  double E = 1.01 * (2.0 * (rx * Nmax + hx * Rmax) + gamma * (2.0 * hx * Hmax + Nmax * Nmax) +
+                     1e-9 * Nmax * Nmax + 1.2e-7);
+  if (!(E < 1e30) || !(Nmax * Nmax < 6.0e4)) E = INFINITY;
+  return E;
+}
+
 // ---- the tcgen05 row-minimum kernel --------------------------------------------------
 __device__ __forceinline__ void topk_insert(float v, int j, float (&tv)[TOPK], int (&tj)[TOPK]) {
   // sorted ascending; caller guarantees v < tv[TOPK-1]
@@ -233,7 +248,10 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
                                                           const int32_t* __restrict__ cnt_y, float* __restrict__ topv,
                                                           int32_t* __restrict__ topj, const float* __restrict__ lim,
                                                           unsigned long long* __restrict__ pairs,
-                                                          unsigned long long* __restrict__ n_pairs, int64_t cap) {
+                                                          unsigned long long* __restrict__ n_pairs, int64_t cap,
+                                                          const double* __restrict__ xinfo = nullptr,
+                                                          const unsigned* __restrict__ ymax = nullptr,
+                                                          double cand_d2 = -1.0) {
   constexpr int STAGES = MODE == 0 ? STAGES_TOP : STAGES_ENUM;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int nx = *cnt_x, ny = *cnt_y;
@@ -370,6 +388,18 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
     const int64_t grow = (int64_t)rb * BM + row;
     // dead rows (beyond the count; their X rows may be stale) get a NaN limit: no v compares <= NaN
     const float my_lim = (MODE == 1 && grow < nx) ? lim[grow] : __int_as_float(0x7fc00000);
+    // MODE 0 with cand_d2 >= 0: every (row, column) whose true squared distance can be below cand_d2
+    // (v <= cand_d2 - |x|^2 + E_row, the certification bound) is appended to `pairs` -- the column
+    // candidates that decide the mutual test without a second pass (see cand_dist_min)
+    float cthr = -INFINITY;
+    bool cand_full = false;
+    if (MODE == 0 && cand_d2 >= 0.0 && grow < nx) {
+      const double nxv = xinfo[3 * grow], E = cert_bound(xinfo[3 * grow + 1], xinfo[3 * grow + 2], ymax);
+      double c = cand_d2 - nxv * nxv + E + 1e-6 + 1e-9 * cand_d2;
+      if (c == c && c < 1e30) cthr = __double2float_ru(c);
+      else atomicAdd(n_pairs, (unsigned long long)cap + 1ull);  // no certificate (NaN / out of range): the
+                                                                // count past cap selects the two-pass path
+    }
     for (int t = 0; t < n_tiles; ++t) {
       const int ab = t % NACC;
       mbar_wait(acc_full + ab, (t / NACC) & 1);
@@ -414,11 +444,23 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
           const float v3 = __uint_as_float(r[4 * q + 3]);
           const float m4 = fminf(fminf(v0, v1), fminf(v2, v3));
           if (MODE == 0) {
-            if (m4 < fminf(tv[TOPK - 1], tsh)) {  // rare after the first tiles
+            if (m4 < fmaxf(fminf(tv[TOPK - 1], tsh), cthr)) {  // rare after the first tiles
               if (v0 < fminf(tv[TOPK - 1], tsh)) topk_insert(v0, jb + 4 * q + 0, tv, tj);
               if (v1 < fminf(tv[TOPK - 1], tsh)) topk_insert(v1, jb + 4 * q + 1, tv, tj);
               if (v2 < fminf(tv[TOPK - 1], tsh)) topk_insert(v2, jb + 4 * q + 2, tv, tj);
               if (v3 < fminf(tv[TOPK - 1], tsh)) topk_insert(v3, jb + 4 * q + 3, tv, tj);
+              if (m4 <= cthr && !cand_full) {  // column candidates (padding columns hold +inf: excluded by ny)
+                const float vv[4] = {v0, v1, v2, v3};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int jc = jb + 4 * q + e;
+                  if (vv[e] <= cthr && jc < ny && !cand_full) {
+                    const unsigned long long slot = atomicAdd(n_pairs, 1ull);
+                    if ((int64_t)slot < cap) pairs[slot] = ((unsigned long long)grow << 32) | (unsigned long long)jc;
+                    else cand_full = true;  // the count past cap tells the host / the later kernels
+                  }
+                }
+              }
             }
           } else if (__any_sync(0xffffffffu, m4 <= my_lim)) {
             // an inf limit (void certificate) enumerates every real column (padding columns hold +inf).
@@ -493,8 +535,10 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
                                                           const int32_t* __restrict__ cnt_y, float* __restrict__ topv,
                                                           int32_t* __restrict__ topj, const float* __restrict__ lim,
                                                           unsigned long long* __restrict__ pairs,
-                                                          unsigned long long* __restrict__ n_pairs, int64_t cap) {
-  nn_topk_tc_body<MODE>(Xt, Yt, cnt_x, cnt_y, topv, topj, lim, pairs, n_pairs, cap);
+                                                          unsigned long long* __restrict__ n_pairs, int64_t cap,
+                                                          const double* __restrict__ xinfo, const unsigned* __restrict__ ymax,
+                                                          double cand_d2) {
+  nn_topk_tc_body<MODE>(Xt, Yt, cnt_x, cnt_y, topv, topj, lim, pairs, n_pairs, cap, xinfo, ymax, cand_d2);
 }
 
 
@@ -547,7 +591,6 @@ __device__ __forceinline__ void certify_exact_body(const float* __restrict__ top
                               int32_t* __restrict__ n_overflow, float* __restrict__ overflow_lim, int n_lists,
                               int64_t nx_pad) {
   const int nx = *cnt_x;
-  const double Nmax = __uint_as_float(ymax[0]), Rmax = __uint_as_float(ymax[1]), Hmax = __uint_as_float(ymax[2]);
   const int t = threadIdx.x & 7;
   const int per_block = blockDim.x >> 3;
   for (int ub = blockIdx.x * per_block; ub < nx; ub += gridDim.x * per_block) {  // 8 lanes per row
@@ -555,16 +598,10 @@ __device__ __forceinline__ void certify_exact_body(const float* __restrict__ top
     const bool live = u < nx;
     const int uu = live ? u : 0;
     const int xi = x_orig ? x_orig[uu] : uu;
-    const double rx = xinfo[3 * uu + 1], hx = xinfo[3 * uu + 2];
-    // |v - (d^2 - |x|^2)| <= 2(|x - x_h||y| + |x_h||y - y_h|) + 2 g |x_h||y_h| + rounding of v
-    // v = fp32-accumulated sum of 144 fp16 products: x_h . (-2 y_h) plus the
-    // three-term split of |y|^2 (split error <= 2^-33 |y|^2 + fp16 underflow)
-    const double gamma = 144.0 * 2.384185791015625e-07;  // 144 * 2^-22 (fp32 accumulation)
-    double E = 1.01 * (2.0 * (rx * Nmax + hx * Rmax) + gamma * (2.0 * hx * Hmax + Nmax * Nmax) +
-                       1e-9 * Nmax * Nmax + 1.2e-7);
-    // out of the fp16 range (|y|^2 split to inf, or elements): no certificate --
-    // every column is enumerated and the rows fall back to the exact scan
-    if (!(E < 1e30) || !(Nmax * Nmax < 6.0e4)) E = INFINITY;
+    // |v - (d^2 - |x|^2)| <= 2(|x - x_h||y| + |x_h||y - y_h|) + 2 g |x_h||y_h| + rounding of v;
+    // out of the fp16 range there is no certificate: every column is enumerated
+    // and the rows fall back to the exact scan
+    const double E = cert_bound(xinfo[3 * uu + 1], xinfo[3 * uu + 2], ymax);
     float tv[TOPK];
     int tj[TOPK];
 #pragma unroll
@@ -886,7 +923,10 @@ __global__ void iota32(int32_t* v, int64_t n) {
 // columns worth checking: nn12 of rows with d < delta_s
 __device__ __forceinline__ void mark_columns_body(const int32_t* __restrict__ a_uniq, const int32_t* __restrict__ n_auniq,
                              const int32_t* __restrict__ nn12, const double* __restrict__ d12, double delta_s,
-                             int32_t* __restrict__ colflag) {
+                             int32_t* __restrict__ colflag, const unsigned long long* __restrict__ n_cand = nullptr,
+                             int64_t cand_cap = 0) {
+  // the column candidates of pass 1 already decided nn21: no column needs pass 2
+  if (n_cand && (int64_t)*n_cand <= cand_cap) return;
   const int n = *n_auniq;
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
     const int i = a_uniq[u];
@@ -895,8 +935,9 @@ __device__ __forceinline__ void mark_columns_body(const int32_t* __restrict__ a_
 }
 __global__ void mark_columns(const int32_t* __restrict__ a_uniq, const int32_t* __restrict__ n_auniq,
                              const int32_t* __restrict__ nn12, const double* __restrict__ d12, double delta_s,
-                             int32_t* __restrict__ colflag) {
-  mark_columns_body(a_uniq, n_auniq, nn12, d12, delta_s, colflag);
+                             int32_t* __restrict__ colflag, const unsigned long long* __restrict__ n_cand,
+                             int64_t cand_cap) {
+  mark_columns_body(a_uniq, n_auniq, nn12, d12, delta_s, colflag, n_cand, cand_cap);
 }
 
 
@@ -923,6 +964,69 @@ __global__ void accept_pairs(const int32_t* __restrict__ a_rep, int64_t n1, cons
 }
 
 
+// ---- column candidates: the mutual test without a second pass ---------------------------
+// Pass 1 lists every (row u, tile column jt) whose squared distance can be
+// below delta_s^2 (nn_topk_tc_body, cand_d2).  A pair (i, j = nn12[i]) is
+// accepted only if d(i, j) < delta_s and i is the first argmin of column j
+// over the distinct rows of A; that argmin then has a distance below delta_s
+// too, so it is in the list: the exact float64 minimum over the listed rows
+// of a column (lowest original row index among equal distances) equals
+// pass 2's nn21 for every column acceptance looks at.  A list that outgrew
+// its capacity (*n_cand > cap) leaves everything to pass 2.
+template <class T>
+__device__ __forceinline__ void cand_dist_min_body(const unsigned long long* __restrict__ cand,
+                                                   const unsigned long long* __restrict__ n_cand, int64_t cap,
+                                                   const int32_t* __restrict__ x_idx,
+                                                   const int32_t* __restrict__ y_idx, const T* __restrict__ X,
+                                                   const T* __restrict__ Y, double* __restrict__ pd,
+                                                   unsigned long long* __restrict__ cbits) {
+  const int64_t n = (int64_t)*n_cand;
+  if (n > cap) return;
+  const int t = threadIdx.x & 7;
+  const int64_t per_block = blockDim.x >> 3;
+  for (int64_t kb = (int64_t)blockIdx.x * per_block; kb < n; kb += (int64_t)gridDim.x * per_block) {
+    const int64_t k = kb + (threadIdx.x >> 3);
+    const bool live = k < n;
+    const unsigned long long pr = live ? cand[k] : 0ull;
+    const int u = (int)(pr >> 32), jt = (int)(pr & 0xffffffffu);
+    const int xi = live ? (x_idx ? x_idx[u] : u) : 0, yj = live ? (y_idx ? y_idx[jt] : jt) : 0;
+    const double d = exact_dist8(X + (int64_t)xi * KD, Y + (int64_t)yj * KD, t);
+    if (live && t == 0) {
+      pd[k] = d;
+      atomicMin(cbits + yj, (unsigned long long)__double_as_longlong(d));
+    }
+  }
+}
+template <class T>
+__device__ __forceinline__ void cand_argmin_body(const unsigned long long* __restrict__ cand,
+                                                 const unsigned long long* __restrict__ n_cand, int64_t cap,
+                                                 const int32_t* __restrict__ x_idx, const int32_t* __restrict__ y_idx,
+                                                 const double* __restrict__ pd,
+                                                 const unsigned long long* __restrict__ cbits,
+                                                 int32_t* __restrict__ nn21) {
+  const int64_t n = (int64_t)*n_cand;
+  if (n > cap) return;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int u = (int)(cand[k] >> 32), jt = (int)(cand[k] & 0xffffffffu);
+    const int yj = y_idx ? y_idx[jt] : jt;
+    if ((unsigned long long)__double_as_longlong(pd[k]) == cbits[yj]) atomicMin(nn21 + yj, x_idx ? x_idx[u] : u);
+  }
+}
+template <class T>
+__global__ void cand_dist_min(const unsigned long long* __restrict__ cand, const unsigned long long* __restrict__ n_cand,
+                              int64_t cap, const int32_t* __restrict__ x_idx, const int32_t* __restrict__ y_idx,
+                              const T* __restrict__ X, const T* __restrict__ Y, double* __restrict__ pd,
+                              unsigned long long* __restrict__ cbits) {
+  cand_dist_min_body<T>(cand, n_cand, cap, x_idx, y_idx, X, Y, pd, cbits);
+}
+template <class T>
+__global__ void cand_argmin(const unsigned long long* __restrict__ cand, const unsigned long long* __restrict__ n_cand,
+                            int64_t cap, const int32_t* __restrict__ x_idx, const int32_t* __restrict__ y_idx,
+                            const double* __restrict__ pd, const unsigned long long* __restrict__ cbits,
+                            int32_t* __restrict__ nn21) {
+  cand_argmin_body<T>(cand, n_cand, cap, x_idx, y_idx, pd, cbits, nn21);
+}
+
 // ---- host orchestration ------------------------------------------------------------
 struct Side {  // a descriptor matrix with its duplicate-row structure
   int32_t *iota, *slot_of, *rep, *flag, *uniq, *n_uniq;
@@ -944,6 +1048,9 @@ struct TcWs {
   float* lim;
   unsigned long long *pairs, *n_pairs, *best_bits;
   int64_t pair_cap;
+  unsigned long long *cand, *n_cand, *cbits;  // pass 1's column candidates (cand_dist_min)
+  double* cpd;
+  int64_t cand_cap;
 };
 
 inline int64_t rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
@@ -1049,6 +1156,11 @@ TcWs carve_tc(void* base, int64_t n1, int64_t n2, size_t* used) {
   w.colflag = ar.take<int32_t>(n2);
   w.cols = ar.take<int32_t>(n2);
   w.n_cols = ar.take<int32_t>(1);
+  w.cand_cap = std::max<int64_t>(1 << 18, 8 * nmax);
+  w.cand = ar.take<unsigned long long>(w.cand_cap);
+  w.cpd = ar.take<double>(w.cand_cap);
+  w.n_cand = ar.take<unsigned long long>(1);
+  w.cbits = ar.take<unsigned long long>(n2);
   *used = ar.used + 256;
   return w;
 }
@@ -1081,7 +1193,8 @@ int dedupe(const T* X, int64_t n, Side& s, const TcWs& w, cudaStream_t st) {
 template <class T>
 int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t* n_x, const T* Y, int64_t ny_all,
                  const int32_t* y_idx, const int32_t* n_y, int32_t* nn, double* dist, const TcWs& w,
-                 cudaStream_t st, int64_t* nx_io = nullptr, int64_t* ny_io = nullptr, bool sync = true) {
+                 cudaStream_t st, int64_t* nx_io = nullptr, int64_t* ny_io = nullptr, bool sync = true,
+                 double cand_d2 = -1.0) {  // >= 0: the top-4 pass also lists the column candidates (w.cand)
   const int64_t xrows = rup(nx_max, BM), yrows = rup(ny_all, BN);
   cudaMemsetAsync(w.ymax, 0, 4 * sizeof(unsigned), st);
   cudaMemsetAsync(w.n_overflow, 0, sizeof(int32_t), st);
@@ -1106,8 +1219,9 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   const dim3 g0 = tc_grid(nx, ny, !sync);
   const int64_t flops_tile = 2ll * BM * BN * KD;
   if (sync) g_stats[5] += (int64_t)g0.x * ((ny + BN - 1) / BN) * flops_tile;
-  nn_topk_tc<0><<<g0, kThreads, smem_bytes<0>(), st>>>(w.xt, w.yt, n_x, n_y, w.topv, w.topj, nullptr, nullptr,
-                                                      nullptr, 0);
+  nn_topk_tc<0><<<g0, kThreads, smem_bytes<0>(), st>>>(w.xt, w.yt, n_x, n_y, w.topv, w.topj, nullptr,
+                                                      cand_d2 >= 0 ? w.cand : nullptr, w.n_cand, w.cand_cap, w.xinfo,
+                                                      w.ymax, cand_d2);
   PS_LAUNCHED("nn_topk_tc<top4>");
   certify_exact<T><<<grid_for(nx, 32), 256, 0, st>>>(w.topv, w.topj, n_x, x_idx, y_idx, w.xinfo, w.ymax, X, Y, nn,
                                                       dist, w.overflow, w.n_overflow, w.lim, kParts * (int)g0.y,
@@ -1137,7 +1251,7 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
       g_stats[5] += (int64_t)tc_grid(n_over, ny).x * ((ny + BN - 1) / BN) * flops_tile;
       nn_topk_tc<1><<<tc_grid(n_over, ny), kThreads, smem_bytes<1>(), st>>>(w.xt, w.yt, w.n_overflow, n_y, nullptr,
                                                                             nullptr, w.lim, w.pairs, w.n_pairs,
-                                                                            w.pair_cap);
+                                                                            w.pair_cap, nullptr, nullptr, -1.0);
       PS_LAUNCHED("nn_topk_tc<enumerate>");
     }
   } else {
@@ -1148,7 +1262,7 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
     const dim3 ge((unsigned)std::min<int64_t>(kEnumBlocksAsync, (nx + BM - 1) / BM), (unsigned)std::min(kMaxSplit, tiles));
     enum_rows = (int)ge.x * BM;  // overflow rows beyond these take the exact scan
     nn_topk_tc<1><<<ge, kThreads, smem_bytes<1>(), st>>>(w.xt, w.yt, w.n_overflow, n_y, nullptr, nullptr, w.lim,
-                                                         w.pairs, w.n_pairs, w.pair_cap);
+                                                         w.pairs, w.n_pairs, w.pair_cap, nullptr, nullptr, -1.0);
     PS_LAUNCHED("nn_topk_tc<enumerate>");
   }
   pair_dist_min<T><<<148 * 16, 256, 0, st>>>(w.pairs, w.n_pairs, w.pair_cap, w.xsrc, y_idx, X, Y, w.pd, w.best_bits);
@@ -1201,6 +1315,9 @@ struct BatchWs {  // uniform slots: set s / pair q at base + s (q) * stride
   uint8_t *xt2, *xto;
   float* lim;
   unsigned long long *best_bits, *pairs, *n_pairs, *kp, *kd, *counter;
+  unsigned long long *cand, *n_cand, *cbits;  // pass 0's column candidates per pair (cand_dist_min)
+  double* cpd;
+  int64_t cand_cap;
 };
 
 constexpr int kSelChunk = 2048;  // flags per selection CTA (256 threads x 8)
@@ -1255,6 +1372,11 @@ BatchWs carve_batch(void* base, int64_t S, int64_t P, int64_t n, size_t* used) {
   w.kp = ar.take<unsigned long long>(P * N);
   w.kd = ar.take<unsigned long long>(P * N);
   w.counter = ar.take<unsigned long long>(P);
+  w.cand_cap = std::max<int64_t>(1 << 14, 4 * N);
+  w.cand = ar.take<unsigned long long>(P * w.cand_cap);
+  w.cpd = ar.take<double>(P * w.cand_cap);
+  w.n_cand = ar.take<unsigned long long>(P);
+  w.cbits = ar.take<unsigned long long>(P * N);
   *used = ar.used + 256;
   return w;
 }
@@ -1608,16 +1730,18 @@ __global__ void b_init(int P, const BatchWs w) {
   w.n_overflow[2 * q] = w.n_overflow[2 * q + 1] = 0;
   w.n_pairs[2 * q] = w.n_pairs[2 * q + 1] = 0ull;
   w.counter[q] = 0ull;
+  w.n_cand[q] = 0ull;
 }
 
 template <int MODE, class T>
 __global__ void __launch_bounds__(kThreads, 1) b_topk(const __grid_constant__ BatchIn<T> in, const BatchWs w,
-                                                      int pass) {
+                                                      int pass, double cand_d2) {
   const int64_t q = blockIdx.z;
   const PassView<T> v = pass_view(in, w, (int)q, pass);
   if (MODE == 0)
     nn_topk_tc_body<0>(v.xt, v.yt, v.n_x, v.n_y, w.topv + q * w.lists * w.xrows * TOPK,
-                       w.topj + q * w.lists * w.xrows * TOPK, nullptr, nullptr, nullptr, 0);
+                       w.topj + q * w.lists * w.xrows * TOPK, nullptr, w.cand + q * w.cand_cap, w.n_cand + q,
+                       w.cand_cap, v.xinfo, v.ymax, pass == 0 ? cand_d2 : -1.0);
   else
     nn_topk_tc_body<1>(w.xto + q * w.over_rows * ROW_BYTES, v.yt, w.n_overflow + 2 * q + pass, v.n_y, nullptr,
                        nullptr, w.lim + q * w.xrows, w.pairs + q * w.pair_cap, w.n_pairs + 2 * q + pass,
@@ -1697,7 +1821,21 @@ template <class T>
 __global__ void b_mark_columns(const __grid_constant__ BatchIn<T> in, const BatchWs w, double delta_s) {
   const int64_t q = blockIdx.y, sa = in.pa[q];
   mark_columns_body(w.uniq + sa * w.n, w.n_uniq + sa, w.nn12 + q * w.n, w.d12 + q * w.n, delta_s,
-                    w.colflag + q * w.n);
+                    w.colflag + q * w.n, w.n_cand + q, w.cand_cap);
+}
+
+// pass 0's column candidates -> nn21 (the pair needs no pass 1 then)
+template <class T>
+__global__ void b_cand_dist_min(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
+  const int64_t q = blockIdx.y, sa = in.pa[q], sb = in.pb[q];
+  cand_dist_min_body<T>(w.cand + q * w.cand_cap, w.n_cand + q, w.cand_cap, w.uniq + sa * w.n, w.uniq + sb * w.n,
+                        in.desc[sa], in.desc[sb], w.cpd + q * w.cand_cap, w.cbits + q * w.n);
+}
+template <class T>
+__global__ void b_cand_argmin(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
+  const int64_t q = blockIdx.y, sa = in.pa[q], sb = in.pb[q];
+  cand_argmin_body<T>(w.cand + q * w.cand_cap, w.n_cand + q, w.cand_cap, w.uniq + sa * w.n, w.uniq + sb * w.n,
+                      w.cpd + q * w.cand_cap, w.cbits + q * w.n, w.nn21 + q * w.n);
 }
 
 template <class T>
@@ -1777,6 +1915,8 @@ int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1
   cudaMemsetAsync(w.tidx, 0x7f, (size_t)S * w.tsize * sizeof(int32_t), st);
   cudaMemsetAsync(w.ymax, 0, (size_t)S * 4 * sizeof(unsigned), st);
   cudaMemsetAsync(w.colflag, 0, (size_t)P * N * sizeof(int32_t), st);
+  cudaMemsetAsync(w.cbits, 0xff, (size_t)P * N * sizeof(unsigned long long), st);
+  cudaMemsetAsync(w.nn21, 0x7f, (size_t)P * N * sizeof(int32_t), st);
   // grids: blocks per set / pair capped so the whole launch is a few waves
   // (the bodies loop grid-stride; one tiny block per 8 rows of every set
   // made block scheduling the cost at C5's 512 sets)
@@ -1805,7 +1945,14 @@ int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1
       nx = std::max<int64_t>(nx, in.rows[pass ? in.pb[q] : in.pa[q]]);
       ny = std::max<int64_t>(ny, in.rows[pass ? in.pa[q] : in.pb[q]]);
     }
-    if (pass == 1) {  // the matchable columns of b, and their X tiles
+    if (pass == 1) {
+      // pass 0's column candidates decide nn21 of a pair whose list fitted; only the other pairs mark
+      // columns, so the stages below find no work for the former
+      b_cand_dist_min<T><<<dim3(std::max(2, 148 * 8 / P), P), 256, 0, st>>>(in, w);
+      PS_LAUNCHED("b_cand_dist_min");
+      b_cand_argmin<T><<<dim3(std::max(2, 148 * 4 / P), P), 256, 0, st>>>(in, w);
+      PS_LAUNCHED("b_cand_argmin");
+      // the matchable columns of b, and their X tiles
       b_mark_columns<T><<<dim3(per(grid_for(N, 256), P), P), 256, 0, st>>>(in, w, delta_s);
       PS_LAUNCHED("b_mark_columns");
       b_sel_count<T, 1><<<dim3(w.nchunk, P), 256, 0, st>>>(in, w.colflag, N, w.sel_cnt, w.nchunk);
@@ -1818,7 +1965,7 @@ int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1
     }
     const int64_t rb = (nx + BM - 1) / BM, tiles = (ny + BN - 1) / BN;
     const int split = batch_split(P, rb, tiles);
-    b_topk<0, T><<<dim3(rb, split, P), kThreads, smem_bytes<0>(), st>>>(in, w, pass);
+    b_topk<0, T><<<dim3(rb, split, P), kThreads, smem_bytes<0>(), st>>>(in, w, pass, delta_s * delta_s);
     PS_LAUNCHED("b_topk<top4>");
     b_certify<T><<<dim3(per(grid_for(nx, 32), P), P), 256, 0, st>>>(in, w, pass, kParts * split, rb * BM);
     PS_LAUNCHED("b_certify");
@@ -1831,7 +1978,7 @@ int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1
     b_prep_rows<T><<<dim3(per(grid_for(enum_rows, 8), P), P), 256, 0, st>>>(in, w, pass, 1);
     PS_LAUNCHED("b_prep_rows(overflow)");
     const int split_e = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)kMaxSplit, tiles, 4 * kSMs / (P * eb)}));
-    b_topk<1, T><<<dim3(eb, split_e, P), kThreads, smem_bytes<1>(), st>>>(in, w, pass);
+    b_topk<1, T><<<dim3(eb, split_e, P), kThreads, smem_bytes<1>(), st>>>(in, w, pass, -1.0);
     PS_LAUNCHED("b_topk<enumerate>");
     b_pair_dist_min<T><<<dim3(std::max(4, 148 * 16 / P), P), 256, 0, st>>>(in, w, pass);
     PS_LAUNCHED("b_pair_dist_min");
@@ -1891,10 +2038,27 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   mark();
   // pass 1: rows of A (representatives) against the distinct rows of B
   int64_t ua = -1, ub = -1;
-  rc = nearest_pass(A, n1, w.a.uniq, w.a.n_uniq, B, n2, w.b.uniq, w.b.n_uniq, w.nn12, w.d12, w, st, &ua, &ub, sync);
+  cudaMemsetAsync(w.n_cand, 0, sizeof(unsigned long long), st);
+  rc = nearest_pass(A, n1, w.a.uniq, w.a.n_uniq, B, n2, w.b.uniq, w.b.n_uniq, w.nn12, w.d12, w, st, &ua, &ub, sync,
+                    delta_s * delta_s);
   if (rc) return rc;
   g_stats[0] = ua;
   g_stats[1] = ub;
+  // the column candidates pass 1 listed decide nn21 (exact float64, first row index among equal distances)
+  cudaMemsetAsync(w.cbits, 0xff, n2 * sizeof(unsigned long long), st);
+  cudaMemsetAsync(w.nn21, 0x7f, n2 * sizeof(int32_t), st);
+  cand_dist_min<T><<<148 * 8, 256, 0, st>>>(w.cand, w.n_cand, w.cand_cap, w.a.uniq, w.b.uniq, A, B, w.cpd, w.cbits);
+  PS_LAUNCHED("cand_dist_min");
+  cand_argmin<T><<<148 * 4, 256, 0, st>>>(w.cand, w.n_cand, w.cand_cap, w.a.uniq, w.b.uniq, w.cpd, w.cbits, w.nn21);
+  PS_LAUNCHED("cand_argmin");
+  bool two_pass = true;  // unknown on the host in asynchronous mode: pass 2 is launched and finds no column
+  if (sync) {
+    unsigned long long nc = 0;
+    cudaMemcpyAsync(&nc, w.n_cand, sizeof(nc), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    two_pass = (int64_t)nc > w.cand_cap;
+    g_stats[6] = (int64_t)nc;
+  }
   mark();
   const int of1 = prof ? count_of(w.n_overflow) : 0;
   unsigned long long np1 = 0;
@@ -1902,9 +2066,12 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
     cudaMemcpyAsync(&np1, w.n_pairs, 8, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
   }
-  // pass 2: the columns that can be matched against the distinct rows of A
+  // pass 2 (only when the candidate list outgrew its buffer, or the certificate is void): the columns
+  // that can be matched against the distinct rows of A
+  if (two_pass) {
   cudaMemsetAsync(w.colflag, 0, n2 * sizeof(int32_t), st);
-  mark_columns<<<grid_for(n1, 256), 256, 0, st>>>(w.a.uniq, w.a.n_uniq, w.nn12, w.d12, delta_s, w.colflag);
+  mark_columns<<<grid_for(n1, 256), 256, 0, st>>>(w.a.uniq, w.a.n_uniq, w.nn12, w.d12, delta_s, w.colflag, w.n_cand,
+                                                  w.cand_cap);
   PS_LAUNCHED("mark_columns");
   iota32<<<grid_for(n2, 256), 256, 0, st>>>(w.b.iota, n2);
   PS_LAUNCHED("iota32");
@@ -1915,8 +2082,9 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   int64_t ncols = -1;
   rc = nearest_pass(B, n2, w.cols, w.n_cols, A, n1, w.a.uniq, w.a.n_uniq, w.nn21, w.d21, w, st, &ncols, &ua, sync);
   if (rc) return rc;
-  mark();
   g_stats[2] = ncols;
+  }  // two_pass
+  mark();
   accept_pairs<<<grid_for(n1, 256), 256, 0, st>>>(w.a.rep, n1, w.nn12, w.d12, w.nn21, delta_s, keys_pair, keys_delta,
                                                   counter);
   PS_LAUNCHED("accept_pairs");
