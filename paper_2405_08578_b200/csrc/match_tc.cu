@@ -224,6 +224,38 @@ __device__ __forceinline__ double cert_bound(double rx, double hx, const unsigne
   return E;
 }
 
+// Column candidates: the mutual test without a second pass.  A pair
+// (i, j = nn12[i]) is accepted only if d(i, j) < delta_s and i is the first
+// argmin of column j over the distinct rows of A; that argmin's distance is
+// then below delta_s too.  So pass 1 keeps, per row, every column whose
+// squared distance can be below delta_s^2 (v <= delta_s^2 - |x|^2 + E, the
+// certification bound) inside its certified candidate set -- the row's limit
+// in the candidate limit becomes max(v_min + 2E, that threshold) -- and every exact
+// float64 distance below delta_s it computes (certify_exact, pair_dist_min)
+// competes for its column: cbits[j] = smallest distance bits, then nn21[j] =
+// lowest original row at that distance (cand_argmin, pair_argmin).  For every
+// column acceptance looks at, that equals pass 2's result.  It is incomplete
+// -- and pass 2 then runs as before (needs_pass2) -- when a row's top-4 may
+// not hold all its columns below the threshold (*incomplete; the row is not
+// made an overflow row for it: on clustered descriptors that would be most
+// rows), or when rows were decided by the exact scan (exact_rows: overflow
+// rows beyond the enumerated ones, or an enumeration that outgrew its buffer).
+// cbits == nullptr disables it all (pass 2 itself, rows-only calls).
+struct ColCand {
+  double delta_s;
+  int32_t* incomplete;        // set when some row may have unlisted columns below the threshold
+  unsigned long long* cbits;  // per original column
+  int32_t* nn21;              // per original column
+  unsigned long long* list;   // (original row << 32 | original column) of certify_exact's candidates
+  double* pd;                 // their distances
+  unsigned long long* n_list;
+};
+__device__ __forceinline__ bool needs_pass2(const int32_t* __restrict__ n_overflow, int enum_rows,
+                                            const unsigned long long* __restrict__ n_pairs, int64_t cap,
+                                            const int32_t* __restrict__ incomplete) {
+  return *incomplete != 0 || *n_overflow > enum_rows || (int64_t)*n_pairs > cap;
+}
+
 // ---- the tcgen05 row-minimum kernel --------------------------------------------------
 __device__ __forceinline__ void topk_insert(float v, int j, float (&tv)[TOPK], int (&tj)[TOPK]) {
   // sorted ascending; caller guarantees v < tv[TOPK-1]
@@ -248,10 +280,7 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
                                                           const int32_t* __restrict__ cnt_y, float* __restrict__ topv,
                                                           int32_t* __restrict__ topj, const float* __restrict__ lim,
                                                           unsigned long long* __restrict__ pairs,
-                                                          unsigned long long* __restrict__ n_pairs, int64_t cap,
-                                                          const double* __restrict__ xinfo = nullptr,
-                                                          const unsigned* __restrict__ ymax = nullptr,
-                                                          double cand_d2 = -1.0) {
+                                                          unsigned long long* __restrict__ n_pairs, int64_t cap) {
   constexpr int STAGES = MODE == 0 ? STAGES_TOP : STAGES_ENUM;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int nx = *cnt_x, ny = *cnt_y;
@@ -388,18 +417,6 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
     const int64_t grow = (int64_t)rb * BM + row;
     // dead rows (beyond the count; their X rows may be stale) get a NaN limit: no v compares <= NaN
     const float my_lim = (MODE == 1 && grow < nx) ? lim[grow] : __int_as_float(0x7fc00000);
-    // MODE 0 with cand_d2 >= 0: every (row, column) whose true squared distance can be below cand_d2
-    // (v <= cand_d2 - |x|^2 + E_row, the certification bound) is appended to `pairs` -- the column
-    // candidates that decide the mutual test without a second pass (see cand_dist_min)
-    float cthr = -INFINITY;
-    bool cand_full = false;
-    if (MODE == 0 && cand_d2 >= 0.0 && grow < nx) {
-      const double nxv = xinfo[3 * grow], E = cert_bound(xinfo[3 * grow + 1], xinfo[3 * grow + 2], ymax);
-      double c = cand_d2 - nxv * nxv + E + 1e-6 + 1e-9 * cand_d2;
-      if (c == c && c < 1e30) cthr = __double2float_ru(c);
-      else atomicAdd(n_pairs, (unsigned long long)cap + 1ull);  // no certificate (NaN / out of range): the
-                                                                // count past cap selects the two-pass path
-    }
     for (int t = 0; t < n_tiles; ++t) {
       const int ab = t % NACC;
       mbar_wait(acc_full + ab, (t / NACC) & 1);
@@ -444,23 +461,11 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
           const float v3 = __uint_as_float(r[4 * q + 3]);
           const float m4 = fminf(fminf(v0, v1), fminf(v2, v3));
           if (MODE == 0) {
-            if (m4 < fmaxf(fminf(tv[TOPK - 1], tsh), cthr)) {  // rare after the first tiles
+            if (m4 < fminf(tv[TOPK - 1], tsh)) {  // rare after the first tiles
               if (v0 < fminf(tv[TOPK - 1], tsh)) topk_insert(v0, jb + 4 * q + 0, tv, tj);
               if (v1 < fminf(tv[TOPK - 1], tsh)) topk_insert(v1, jb + 4 * q + 1, tv, tj);
               if (v2 < fminf(tv[TOPK - 1], tsh)) topk_insert(v2, jb + 4 * q + 2, tv, tj);
               if (v3 < fminf(tv[TOPK - 1], tsh)) topk_insert(v3, jb + 4 * q + 3, tv, tj);
-              if (m4 <= cthr && !cand_full) {  // column candidates (padding columns hold +inf: excluded by ny)
-                const float vv[4] = {v0, v1, v2, v3};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const int jc = jb + 4 * q + e;
-                  if (vv[e] <= cthr && jc < ny && !cand_full) {
-                    const unsigned long long slot = atomicAdd(n_pairs, 1ull);
-                    if ((int64_t)slot < cap) pairs[slot] = ((unsigned long long)grow << 32) | (unsigned long long)jc;
-                    else cand_full = true;  // the count past cap tells the host / the later kernels
-                  }
-                }
-              }
             }
           } else if (__any_sync(0xffffffffu, m4 <= my_lim)) {
             // an inf limit (void certificate) enumerates every real column (padding columns hold +inf).
@@ -535,10 +540,8 @@ __global__ void __launch_bounds__(kThreads, 1) nn_topk_tc(const uint8_t* __restr
                                                           const int32_t* __restrict__ cnt_y, float* __restrict__ topv,
                                                           int32_t* __restrict__ topj, const float* __restrict__ lim,
                                                           unsigned long long* __restrict__ pairs,
-                                                          unsigned long long* __restrict__ n_pairs, int64_t cap,
-                                                          const double* __restrict__ xinfo, const unsigned* __restrict__ ymax,
-                                                          double cand_d2) {
-  nn_topk_tc_body<MODE>(Xt, Yt, cnt_x, cnt_y, topv, topj, lim, pairs, n_pairs, cap, xinfo, ymax, cand_d2);
+                                                          unsigned long long* __restrict__ n_pairs, int64_t cap) {
+  nn_topk_tc_body<MODE>(Xt, Yt, cnt_x, cnt_y, topv, topj, lim, pairs, n_pairs, cap);
 }
 
 
@@ -589,7 +592,7 @@ __device__ __forceinline__ void certify_exact_body(const float* __restrict__ top
                               const unsigned* __restrict__ ymax, const T* __restrict__ X, const T* __restrict__ Y,
                               int32_t* __restrict__ nn, double* __restrict__ dist, int32_t* __restrict__ overflow,
                               int32_t* __restrict__ n_overflow, float* __restrict__ overflow_lim, int n_lists,
-                              int64_t nx_pad) {
+                              int64_t nx_pad, const ColCand cc) {
   const int nx = *cnt_x;
   const int t = threadIdx.x & 7;
   const int per_block = blockDim.x >> 3;
@@ -626,12 +629,19 @@ __device__ __forceinline__ void certify_exact_body(const float* __restrict__ top
         if (lv[q] < tv[TOPK - 1]) topk_insert(lv[q], lj[q], tv, tj);
     }
     const double lim = (double)tv[0] + 2.0 * E;
+    double clim = lim;  // candidate limit: also every column that can be closer than delta_s (ColCand)
+    if (cc.cbits) {
+      const double nxv = xinfo[3 * uu];
+      const double c = cc.delta_s * cc.delta_s * (1.0 + 1e-9) - nxv * nxv + E + 1e-6;
+      clim = (c == c) ? fmax(lim, c) : INFINITY;
+    }
     const bool over = (double)tv[TOPK - 1] <= lim;  // candidates may extend past the top-4
     if (live && over && t == 0) {
       const int slot = atomicAdd(n_overflow, 1);
       overflow[slot] = u;
-      overflow_lim[slot] = __double2float_ru(lim);
+      overflow_lim[slot] = __double2float_ru(clim);  // the enumeration lists the row's column candidates too
     }
+    if (cc.cbits && live && !over && t == 0 && (double)tv[TOPK - 1] <= clim) *cc.incomplete = 1;
     double bd = INFINITY;
     int bj = INT32_MAX;
     // the (up to TOPK) candidate distances are computed together: TOPK
@@ -642,7 +652,7 @@ __device__ __forceinline__ void certify_exact_body(const float* __restrict__ top
     bool any = false;
 #pragma unroll
     for (int q = 0; q < TOPK; ++q) {
-      cand[q] = live && !over && tj[q] >= 0 && (double)tv[q] <= lim;
+      cand[q] = live && !over && tj[q] >= 0 && (double)tv[q] <= clim;
       yj[q] = cand[q] ? (y_orig ? y_orig[tj[q]] : tj[q]) : 0;
       any |= cand[q];
     }
@@ -667,6 +677,12 @@ __device__ __forceinline__ void certify_exact_body(const float* __restrict__ top
         const double p4 = __dadd_rn(p2, __shfl_down_sync(0xffffffffu, p2, 4));
         const double dd = __dsqrt_rn(p4);
         if (cand[q] && (dd < bd || (dd == bd && yj[q] < bj))) { bd = dd; bj = yj[q]; }
+        if (cc.cbits && cand[q] && t == 0 && dd < cc.delta_s) {  // competes for its column
+          const unsigned long long slot = atomicAdd(cc.n_list, 1ull);  // <= TOPK per row: the list cannot overflow
+          cc.list[slot] = ((unsigned long long)(unsigned)xi << 32) | (unsigned long long)(unsigned)yj[q];
+          cc.pd[slot] = dd;
+          atomicMin(cc.cbits + yj[q], (unsigned long long)__double_as_longlong(dd));
+        }
       }
     }
     if (live && !over && t == 0) {
@@ -682,8 +698,9 @@ __global__ void certify_exact(const float* __restrict__ topv, const int32_t* __r
                               const unsigned* __restrict__ ymax, const T* __restrict__ X, const T* __restrict__ Y,
                               int32_t* __restrict__ nn, double* __restrict__ dist, int32_t* __restrict__ overflow,
                               int32_t* __restrict__ n_overflow, float* __restrict__ overflow_lim, int n_lists,
-                              int64_t nx_pad) {
-  certify_exact_body<T>(topv, topj, cnt_x, x_orig, y_orig, xinfo, ymax, X, Y, nn, dist, overflow, n_overflow, overflow_lim, n_lists, nx_pad);
+                              int64_t nx_pad, const ColCand cc) {
+  certify_exact_body<T>(topv, topj, cnt_x, x_orig, y_orig, xinfo, ymax, X, Y, nn, dist, overflow, n_overflow,
+                        overflow_lim, n_lists, nx_pad, cc);
 }
 
 
@@ -707,7 +724,7 @@ __device__ __forceinline__ void pair_dist_min_body(const unsigned long long* __r
                               const unsigned long long* __restrict__ n_pairs, int64_t cap,
                               const int32_t* __restrict__ xsrc, const int32_t* __restrict__ y_idx,
                               const T* __restrict__ X, const T* __restrict__ Y, double* __restrict__ pd,
-                              unsigned long long* __restrict__ best_bits) {
+                              unsigned long long* __restrict__ best_bits, const ColCand cc) {
   const int64_t n = min((int64_t)*n_pairs, cap);
   const int t = threadIdx.x & 7;
   const int64_t per_block = blockDim.x >> 3;
@@ -723,6 +740,7 @@ __device__ __forceinline__ void pair_dist_min_body(const unsigned long long* __r
     if (live && t == 0) {
       pd[k] = d;
       atomicMin(best_bits + q, (unsigned long long)__double_as_longlong(d));
+      if (cc.cbits && d < cc.delta_s) atomicMin(cc.cbits + yj, (unsigned long long)__double_as_longlong(d));
     }
   }
 }
@@ -731,26 +749,31 @@ __global__ void pair_dist_min(const unsigned long long* __restrict__ pairs,
                               const unsigned long long* __restrict__ n_pairs, int64_t cap,
                               const int32_t* __restrict__ xsrc, const int32_t* __restrict__ y_idx,
                               const T* __restrict__ X, const T* __restrict__ Y, double* __restrict__ pd,
-                              unsigned long long* __restrict__ best_bits) {
-  pair_dist_min_body<T>(pairs, n_pairs, cap, xsrc, y_idx, X, Y, pd, best_bits);
+                              unsigned long long* __restrict__ best_bits, const ColCand cc) {
+  pair_dist_min_body<T>(pairs, n_pairs, cap, xsrc, y_idx, X, Y, pd, best_bits, cc);
 }
 
 
 template <class T>
 __device__ __forceinline__ void pair_argmin_body(const unsigned long long* __restrict__ pairs, const unsigned long long* __restrict__ n_pairs,
                             int64_t cap, const int32_t* __restrict__ y_idx, const double* __restrict__ pd,
-                            const unsigned long long* __restrict__ best_bits, int* __restrict__ best_j) {
+                            const unsigned long long* __restrict__ best_bits, int* __restrict__ best_j,
+                            const int32_t* __restrict__ xsrc, const ColCand cc) {
   const int64_t n = min((int64_t)*n_pairs, cap);
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     const int q = (int)(pairs[k] >> 32), jt = (int)(pairs[k] & 0xffffffffu);
-    if ((unsigned long long)__double_as_longlong(pd[k]) == best_bits[q]) atomicMin(best_j + q, y_idx ? y_idx[jt] : jt);
+    const int yj = y_idx ? y_idx[jt] : jt;
+    const unsigned long long db = (unsigned long long)__double_as_longlong(pd[k]);
+    if (db == best_bits[q]) atomicMin(best_j + q, yj);
+    if (cc.cbits && db == cc.cbits[yj]) atomicMin(cc.nn21 + yj, xsrc[q]);  // the column's first row at its minimum
   }
 }
 template <class T>
 __global__ void pair_argmin(const unsigned long long* __restrict__ pairs, const unsigned long long* __restrict__ n_pairs,
                             int64_t cap, const int32_t* __restrict__ y_idx, const double* __restrict__ pd,
-                            const unsigned long long* __restrict__ best_bits, int* __restrict__ best_j) {
-  pair_argmin_body<T>(pairs, n_pairs, cap, y_idx, pd, best_bits, best_j);
+                            const unsigned long long* __restrict__ best_bits, int* __restrict__ best_j,
+                            const int32_t* __restrict__ xsrc, const ColCand cc) {
+  pair_argmin_body<T>(pairs, n_pairs, cap, y_idx, pd, best_bits, best_j, xsrc, cc);
 }
 
 
@@ -923,10 +946,11 @@ __global__ void iota32(int32_t* v, int64_t n) {
 // columns worth checking: nn12 of rows with d < delta_s
 __device__ __forceinline__ void mark_columns_body(const int32_t* __restrict__ a_uniq, const int32_t* __restrict__ n_auniq,
                              const int32_t* __restrict__ nn12, const double* __restrict__ d12, double delta_s,
-                             int32_t* __restrict__ colflag, const unsigned long long* __restrict__ n_cand = nullptr,
-                             int64_t cand_cap = 0) {
-  // the column candidates of pass 1 already decided nn21: no column needs pass 2
-  if (n_cand && (int64_t)*n_cand <= cand_cap) return;
+                             int32_t* __restrict__ colflag, const int32_t* __restrict__ n_overflow, int enum_rows,
+                             const unsigned long long* __restrict__ n_pairs, int64_t pair_cap,
+                             const int32_t* __restrict__ incomplete) {
+  // pass 1's column candidates already decided nn21 (ColCand): no column needs pass 2
+  if (incomplete && !needs_pass2(n_overflow, enum_rows, n_pairs, pair_cap, incomplete)) return;
   const int n = *n_auniq;
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
     const int i = a_uniq[u];
@@ -935,9 +959,11 @@ __device__ __forceinline__ void mark_columns_body(const int32_t* __restrict__ a_
 }
 __global__ void mark_columns(const int32_t* __restrict__ a_uniq, const int32_t* __restrict__ n_auniq,
                              const int32_t* __restrict__ nn12, const double* __restrict__ d12, double delta_s,
-                             int32_t* __restrict__ colflag, const unsigned long long* __restrict__ n_cand,
-                             int64_t cand_cap) {
-  mark_columns_body(a_uniq, n_auniq, nn12, d12, delta_s, colflag, n_cand, cand_cap);
+                             int32_t* __restrict__ colflag, const int32_t* __restrict__ n_overflow, int enum_rows,
+                             const unsigned long long* __restrict__ n_pairs, int64_t pair_cap,
+                             const int32_t* __restrict__ incomplete) {
+  mark_columns_body(a_uniq, n_auniq, nn12, d12, delta_s, colflag, n_overflow, enum_rows, n_pairs, pair_cap,
+                    incomplete);
 }
 
 
@@ -964,68 +990,16 @@ __global__ void accept_pairs(const int32_t* __restrict__ a_rep, int64_t n1, cons
 }
 
 
-// ---- column candidates: the mutual test without a second pass ---------------------------
-// Pass 1 lists every (row u, tile column jt) whose squared distance can be
-// below delta_s^2 (nn_topk_tc_body, cand_d2).  A pair (i, j = nn12[i]) is
-// accepted only if d(i, j) < delta_s and i is the first argmin of column j
-// over the distinct rows of A; that argmin then has a distance below delta_s
-// too, so it is in the list: the exact float64 minimum over the listed rows
-// of a column (lowest original row index among equal distances) equals
-// pass 2's nn21 for every column acceptance looks at.  A list that outgrew
-// its capacity (*n_cand > cap) leaves everything to pass 2.
-template <class T>
-__device__ __forceinline__ void cand_dist_min_body(const unsigned long long* __restrict__ cand,
-                                                   const unsigned long long* __restrict__ n_cand, int64_t cap,
-                                                   const int32_t* __restrict__ x_idx,
-                                                   const int32_t* __restrict__ y_idx, const T* __restrict__ X,
-                                                   const T* __restrict__ Y, double* __restrict__ pd,
-                                                   unsigned long long* __restrict__ cbits) {
-  const int64_t n = (int64_t)*n_cand;
-  if (n > cap) return;
-  const int t = threadIdx.x & 7;
-  const int64_t per_block = blockDim.x >> 3;
-  for (int64_t kb = (int64_t)blockIdx.x * per_block; kb < n; kb += (int64_t)gridDim.x * per_block) {
-    const int64_t k = kb + (threadIdx.x >> 3);
-    const bool live = k < n;
-    const unsigned long long pr = live ? cand[k] : 0ull;
-    const int u = (int)(pr >> 32), jt = (int)(pr & 0xffffffffu);
-    const int xi = live ? (x_idx ? x_idx[u] : u) : 0, yj = live ? (y_idx ? y_idx[jt] : jt) : 0;
-    const double d = exact_dist8(X + (int64_t)xi * KD, Y + (int64_t)yj * KD, t);
-    if (live && t == 0) {
-      pd[k] = d;
-      atomicMin(cbits + yj, (unsigned long long)__double_as_longlong(d));
-    }
-  }
-}
-template <class T>
-__device__ __forceinline__ void cand_argmin_body(const unsigned long long* __restrict__ cand,
-                                                 const unsigned long long* __restrict__ n_cand, int64_t cap,
-                                                 const int32_t* __restrict__ x_idx, const int32_t* __restrict__ y_idx,
-                                                 const double* __restrict__ pd,
-                                                 const unsigned long long* __restrict__ cbits,
-                                                 int32_t* __restrict__ nn21) {
-  const int64_t n = (int64_t)*n_cand;
-  if (n > cap) return;
+// ---- column candidates (ColCand): certify_exact's list -> nn21 ---------------------------
+__device__ __forceinline__ void cand_argmin_body(const ColCand cc) {
+  if (!cc.cbits) return;
+  const int64_t n = (int64_t)*cc.n_list;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-    const int u = (int)(cand[k] >> 32), jt = (int)(cand[k] & 0xffffffffu);
-    const int yj = y_idx ? y_idx[jt] : jt;
-    if ((unsigned long long)__double_as_longlong(pd[k]) == cbits[yj]) atomicMin(nn21 + yj, x_idx ? x_idx[u] : u);
+    const int xi = (int)(cc.list[k] >> 32), yj = (int)(cc.list[k] & 0xffffffffu);
+    if ((unsigned long long)__double_as_longlong(cc.pd[k]) == cc.cbits[yj]) atomicMin(cc.nn21 + yj, xi);
   }
 }
-template <class T>
-__global__ void cand_dist_min(const unsigned long long* __restrict__ cand, const unsigned long long* __restrict__ n_cand,
-                              int64_t cap, const int32_t* __restrict__ x_idx, const int32_t* __restrict__ y_idx,
-                              const T* __restrict__ X, const T* __restrict__ Y, double* __restrict__ pd,
-                              unsigned long long* __restrict__ cbits) {
-  cand_dist_min_body<T>(cand, n_cand, cap, x_idx, y_idx, X, Y, pd, cbits);
-}
-template <class T>
-__global__ void cand_argmin(const unsigned long long* __restrict__ cand, const unsigned long long* __restrict__ n_cand,
-                            int64_t cap, const int32_t* __restrict__ x_idx, const int32_t* __restrict__ y_idx,
-                            const double* __restrict__ pd, const unsigned long long* __restrict__ cbits,
-                            int32_t* __restrict__ nn21) {
-  cand_argmin_body<T>(cand, n_cand, cap, x_idx, y_idx, pd, cbits, nn21);
-}
+__global__ void cand_argmin(const ColCand cc) { cand_argmin_body(cc); }
 
 // ---- host orchestration ------------------------------------------------------------
 struct Side {  // a descriptor matrix with its duplicate-row structure
@@ -1048,8 +1022,9 @@ struct TcWs {
   float* lim;
   unsigned long long *pairs, *n_pairs, *best_bits;
   int64_t pair_cap;
-  unsigned long long *cand, *n_cand, *cbits;  // pass 1's column candidates (cand_dist_min)
+  unsigned long long *cand, *n_cand, *cbits;  // pass 1's column candidates (ColCand)
   double* cpd;
+  int32_t* cand_incomplete;
   int64_t cand_cap;
 };
 
@@ -1160,6 +1135,7 @@ TcWs carve_tc(void* base, int64_t n1, int64_t n2, size_t* used) {
   w.cand = ar.take<unsigned long long>(w.cand_cap);
   w.cpd = ar.take<double>(w.cand_cap);
   w.n_cand = ar.take<unsigned long long>(1);
+  w.cand_incomplete = ar.take<int32_t>(1);
   w.cbits = ar.take<unsigned long long>(n2);
   *used = ar.used + 256;
   return w;
@@ -1194,7 +1170,7 @@ template <class T>
 int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t* n_x, const T* Y, int64_t ny_all,
                  const int32_t* y_idx, const int32_t* n_y, int32_t* nn, double* dist, const TcWs& w,
                  cudaStream_t st, int64_t* nx_io = nullptr, int64_t* ny_io = nullptr, bool sync = true,
-                 double cand_d2 = -1.0) {  // >= 0: the top-4 pass also lists the column candidates (w.cand)
+                 ColCand cc = ColCand{}, int* enum_rows_out = nullptr) {  // cc.cbits: the pass also decides the columns
   const int64_t xrows = rup(nx_max, BM), yrows = rup(ny_all, BN);
   cudaMemsetAsync(w.ymax, 0, 4 * sizeof(unsigned), st);
   cudaMemsetAsync(w.n_overflow, 0, sizeof(int32_t), st);
@@ -1219,13 +1195,12 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   const dim3 g0 = tc_grid(nx, ny, !sync);
   const int64_t flops_tile = 2ll * BM * BN * KD;
   if (sync) g_stats[5] += (int64_t)g0.x * ((ny + BN - 1) / BN) * flops_tile;
-  nn_topk_tc<0><<<g0, kThreads, smem_bytes<0>(), st>>>(w.xt, w.yt, n_x, n_y, w.topv, w.topj, nullptr,
-                                                      cand_d2 >= 0 ? w.cand : nullptr, w.n_cand, w.cand_cap, w.xinfo,
-                                                      w.ymax, cand_d2);
+  nn_topk_tc<0><<<g0, kThreads, smem_bytes<0>(), st>>>(w.xt, w.yt, n_x, n_y, w.topv, w.topj, nullptr, nullptr,
+                                                      nullptr, 0);
   PS_LAUNCHED("nn_topk_tc<top4>");
   certify_exact<T><<<grid_for(nx, 32), 256, 0, st>>>(w.topv, w.topj, n_x, x_idx, y_idx, w.xinfo, w.ymax, X, Y, nn,
                                                       dist, w.overflow, w.n_overflow, w.lim, kParts * (int)g0.y,
-                                                      (int64_t)g0.x * BM);
+                                                      (int64_t)g0.x * BM, cc);
   PS_LAUNCHED("certify_exact");
   // rows with more near-tied candidates than the top-4: enumerate every
   // column within their certified limit on the tensor cores, then decide exactly
@@ -1251,7 +1226,7 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
       g_stats[5] += (int64_t)tc_grid(n_over, ny).x * ((ny + BN - 1) / BN) * flops_tile;
       nn_topk_tc<1><<<tc_grid(n_over, ny), kThreads, smem_bytes<1>(), st>>>(w.xt, w.yt, w.n_overflow, n_y, nullptr,
                                                                             nullptr, w.lim, w.pairs, w.n_pairs,
-                                                                            w.pair_cap, nullptr, nullptr, -1.0);
+                                                                            w.pair_cap);
       PS_LAUNCHED("nn_topk_tc<enumerate>");
     }
   } else {
@@ -1262,13 +1237,20 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
     const dim3 ge((unsigned)std::min<int64_t>(kEnumBlocksAsync, (nx + BM - 1) / BM), (unsigned)std::min(kMaxSplit, tiles));
     enum_rows = (int)ge.x * BM;  // overflow rows beyond these take the exact scan
     nn_topk_tc<1><<<ge, kThreads, smem_bytes<1>(), st>>>(w.xt, w.yt, w.n_overflow, n_y, nullptr, nullptr, w.lim,
-                                                         w.pairs, w.n_pairs, w.pair_cap, nullptr, nullptr, -1.0);
+                                                         w.pairs, w.n_pairs, w.pair_cap);
     PS_LAUNCHED("nn_topk_tc<enumerate>");
   }
-  pair_dist_min<T><<<148 * 16, 256, 0, st>>>(w.pairs, w.n_pairs, w.pair_cap, w.xsrc, y_idx, X, Y, w.pd, w.best_bits);
+  if (enum_rows_out) *enum_rows_out = enum_rows;
+  pair_dist_min<T><<<148 * 16, 256, 0, st>>>(w.pairs, w.n_pairs, w.pair_cap, w.xsrc, y_idx, X, Y, w.pd, w.best_bits,
+                                             cc);
   PS_LAUNCHED("pair_dist_min");
-  pair_argmin<T><<<148 * 8, 256, 0, st>>>(w.pairs, w.n_pairs, w.pair_cap, y_idx, w.pd, w.best_bits, w.best_j);
+  pair_argmin<T><<<148 * 8, 256, 0, st>>>(w.pairs, w.n_pairs, w.pair_cap, y_idx, w.pd, w.best_bits, w.best_j,
+                                          w.xsrc, cc);
   PS_LAUNCHED("pair_argmin");
+  if (cc.cbits) {
+    cand_argmin<<<148 * 4, 256, 0, st>>>(cc);
+    PS_LAUNCHED("cand_argmin");
+  }
   pair_write<<<grid_for(nx_max, 256), 256, 0, st>>>(w.n_overflow, w.xsrc, w.best_bits, w.best_j, nn, dist,
                                                      enum_rows);
   PS_LAUNCHED("pair_write");
@@ -1315,8 +1297,9 @@ struct BatchWs {  // uniform slots: set s / pair q at base + s (q) * stride
   uint8_t *xt2, *xto;
   float* lim;
   unsigned long long *best_bits, *pairs, *n_pairs, *kp, *kd, *counter;
-  unsigned long long *cand, *n_cand, *cbits;  // pass 0's column candidates per pair (cand_dist_min)
+  unsigned long long *cand, *n_cand, *cbits;  // pass 0's column candidates per pair (ColCand)
   double* cpd;
+  int32_t* cand_incomplete;
   int64_t cand_cap;
 };
 
@@ -1376,6 +1359,7 @@ BatchWs carve_batch(void* base, int64_t S, int64_t P, int64_t n, size_t* used) {
   w.cand = ar.take<unsigned long long>(P * w.cand_cap);
   w.cpd = ar.take<double>(P * w.cand_cap);
   w.n_cand = ar.take<unsigned long long>(P);
+  w.cand_incomplete = ar.take<int32_t>(P);
   w.cbits = ar.take<unsigned long long>(P * N);
   *used = ar.used + 256;
   return w;
@@ -1723,6 +1707,13 @@ __global__ void __launch_bounds__(256) b_sel_scatter(const __grid_constant__ Bat
   if (c1 == len && threadIdx.x == 0) n_out[g] = base;
 }
 
+// pair q's column candidates (pass 0 only)
+__device__ __forceinline__ ColCand col_cand(const BatchWs& w, int64_t q, int pass, double delta_s) {
+  if (pass) return ColCand{};
+  return ColCand{delta_s, w.cand_incomplete + q, w.cbits + q * w.n, w.nn21 + q * w.n, w.cand + q * w.cand_cap, w.cpd + q * w.cand_cap,
+                 w.n_cand + q};
+}
+
 // per-pair stages (blockIdx.y = pair; the tensor-core kernel: blockIdx.z)
 __global__ void b_init(int P, const BatchWs w) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1731,17 +1722,17 @@ __global__ void b_init(int P, const BatchWs w) {
   w.n_pairs[2 * q] = w.n_pairs[2 * q + 1] = 0ull;
   w.counter[q] = 0ull;
   w.n_cand[q] = 0ull;
+  w.cand_incomplete[q] = 0;
 }
 
 template <int MODE, class T>
 __global__ void __launch_bounds__(kThreads, 1) b_topk(const __grid_constant__ BatchIn<T> in, const BatchWs w,
-                                                      int pass, double cand_d2) {
+                                                      int pass) {
   const int64_t q = blockIdx.z;
   const PassView<T> v = pass_view(in, w, (int)q, pass);
   if (MODE == 0)
     nn_topk_tc_body<0>(v.xt, v.yt, v.n_x, v.n_y, w.topv + q * w.lists * w.xrows * TOPK,
-                       w.topj + q * w.lists * w.xrows * TOPK, nullptr, w.cand + q * w.cand_cap, w.n_cand + q,
-                       w.cand_cap, v.xinfo, v.ymax, pass == 0 ? cand_d2 : -1.0);
+                       w.topj + q * w.lists * w.xrows * TOPK, nullptr, nullptr, nullptr, 0);
   else
     nn_topk_tc_body<1>(w.xto + q * w.over_rows * ROW_BYTES, v.yt, w.n_overflow + 2 * q + pass, v.n_y, nullptr,
                        nullptr, w.lim + q * w.xrows, w.pairs + q * w.pair_cap, w.n_pairs + 2 * q + pass,
@@ -1750,12 +1741,13 @@ __global__ void __launch_bounds__(kThreads, 1) b_topk(const __grid_constant__ Ba
 
 template <class T>
 __global__ void b_certify(const __grid_constant__ BatchIn<T> in, const BatchWs w, int pass, int n_lists,
-                          int64_t nx_pad) {
+                          int64_t nx_pad, double delta_s) {
   const int64_t q = blockIdx.y;
   const PassView<T> v = pass_view(in, w, (int)q, pass);
   certify_exact_body<T>(w.topv + q * w.lists * w.xrows * TOPK, w.topj + q * w.lists * w.xrows * TOPK, v.n_x, v.x_idx,
                         v.y_idx, v.xinfo, v.ymax, v.X, v.Y, v.nn, v.dist, w.overflow + q * w.n,
-                        w.n_overflow + 2 * q + pass, w.lim + q * w.xrows, n_lists, nx_pad);
+                        w.n_overflow + 2 * q + pass, w.lim + q * w.xrows, n_lists, nx_pad,
+                        col_cand(w, q, pass, delta_s));
 }
 
 // overflow rows -> source rows, and their enumeration minima reset
@@ -1786,19 +1778,20 @@ __global__ void b_prep_rows(const __grid_constant__ BatchIn<T> in, const BatchWs
 }
 
 template <class T>
-__global__ void b_pair_dist_min(const __grid_constant__ BatchIn<T> in, const BatchWs w, int pass) {
+__global__ void b_pair_dist_min(const __grid_constant__ BatchIn<T> in, const BatchWs w, int pass, double delta_s) {
   const int64_t q = blockIdx.y;
   const PassView<T> v = pass_view(in, w, (int)q, pass);
   pair_dist_min_body<T>(w.pairs + q * w.pair_cap, w.n_pairs + 2 * q + pass, w.pair_cap, w.xsrc + q * w.n, v.y_idx,
-                        v.X, v.Y, w.pd + q * w.pair_cap, w.best_bits + q * w.n);
+                        v.X, v.Y, w.pd + q * w.pair_cap, w.best_bits + q * w.n, col_cand(w, q, pass, delta_s));
 }
 
 template <class T>
-__global__ void b_pair_argmin(const __grid_constant__ BatchIn<T> in, const BatchWs w, int pass) {
+__global__ void b_pair_argmin(const __grid_constant__ BatchIn<T> in, const BatchWs w, int pass, double delta_s) {
   const int64_t q = blockIdx.y;
   const PassView<T> v = pass_view(in, w, (int)q, pass);
   pair_argmin_body<T>(w.pairs + q * w.pair_cap, w.n_pairs + 2 * q + pass, w.pair_cap, v.y_idx, w.pd + q * w.pair_cap,
-                      w.best_bits + q * w.n, w.best_j + q * w.n);
+                      w.best_bits + q * w.n, w.best_j + q * w.n, w.xsrc + q * w.n, col_cand(w, q, pass, delta_s));
+  cand_argmin_body(col_cand(w, q, pass, delta_s));  // certify's list: the column minima are final here
 }
 
 template <class T>
@@ -1818,24 +1811,11 @@ __global__ void b_exact_rows(const __grid_constant__ BatchIn<T> in, const BatchW
 }
 
 template <class T>
-__global__ void b_mark_columns(const __grid_constant__ BatchIn<T> in, const BatchWs w, double delta_s) {
+__global__ void b_mark_columns(const __grid_constant__ BatchIn<T> in, const BatchWs w, double delta_s, int enum_rows) {
   const int64_t q = blockIdx.y, sa = in.pa[q];
   mark_columns_body(w.uniq + sa * w.n, w.n_uniq + sa, w.nn12 + q * w.n, w.d12 + q * w.n, delta_s,
-                    w.colflag + q * w.n, w.n_cand + q, w.cand_cap);
-}
-
-// pass 0's column candidates -> nn21 (the pair needs no pass 1 then)
-template <class T>
-__global__ void b_cand_dist_min(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
-  const int64_t q = blockIdx.y, sa = in.pa[q], sb = in.pb[q];
-  cand_dist_min_body<T>(w.cand + q * w.cand_cap, w.n_cand + q, w.cand_cap, w.uniq + sa * w.n, w.uniq + sb * w.n,
-                        in.desc[sa], in.desc[sb], w.cpd + q * w.cand_cap, w.cbits + q * w.n);
-}
-template <class T>
-__global__ void b_cand_argmin(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
-  const int64_t q = blockIdx.y, sa = in.pa[q], sb = in.pb[q];
-  cand_argmin_body<T>(w.cand + q * w.cand_cap, w.n_cand + q, w.cand_cap, w.uniq + sa * w.n, w.uniq + sb * w.n,
-                      w.cpd + q * w.cand_cap, w.cbits + q * w.n, w.nn21 + q * w.n);
+                    w.colflag + q * w.n, w.n_overflow + 2 * q, enum_rows, w.n_pairs + 2 * q, w.pair_cap,
+                    w.cand_incomplete + q);
 }
 
 template <class T>
@@ -1939,6 +1919,7 @@ int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1
   PS_LAUNCHED("b_prep_sets");
   cudaFuncSetAttribute(b_topk<0, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<0>());
   cudaFuncSetAttribute(b_topk<1, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes<1>());
+  int enum_rows0 = 0;
   for (int pass = 0; pass < 2; ++pass) {
     int64_t nx = 1, ny = 1;  // row bounds over the pairs
     for (int q = 0; q < P; ++q) {
@@ -1946,14 +1927,9 @@ int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1
       ny = std::max<int64_t>(ny, in.rows[pass ? in.pa[q] : in.pb[q]]);
     }
     if (pass == 1) {
-      // pass 0's column candidates decide nn21 of a pair whose list fitted; only the other pairs mark
-      // columns, so the stages below find no work for the former
-      b_cand_dist_min<T><<<dim3(std::max(2, 148 * 8 / P), P), 256, 0, st>>>(in, w);
-      PS_LAUNCHED("b_cand_dist_min");
-      b_cand_argmin<T><<<dim3(std::max(2, 148 * 4 / P), P), 256, 0, st>>>(in, w);
-      PS_LAUNCHED("b_cand_argmin");
-      // the matchable columns of b, and their X tiles
-      b_mark_columns<T><<<dim3(per(grid_for(N, 256), P), P), 256, 0, st>>>(in, w, delta_s);
+      // pass 0 decided nn21 of every pair none of whose rows took the exact scan (ColCand): only the
+      // other pairs mark columns, so the stages below find no work for the former
+      b_mark_columns<T><<<dim3(per(grid_for(N, 256), P), P), 256, 0, st>>>(in, w, delta_s, enum_rows0);
       PS_LAUNCHED("b_mark_columns");
       b_sel_count<T, 1><<<dim3(w.nchunk, P), 256, 0, st>>>(in, w.colflag, N, w.sel_cnt, w.nchunk);
       PS_LAUNCHED("b_sel_count");
@@ -1965,9 +1941,9 @@ int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1
     }
     const int64_t rb = (nx + BM - 1) / BM, tiles = (ny + BN - 1) / BN;
     const int split = batch_split(P, rb, tiles);
-    b_topk<0, T><<<dim3(rb, split, P), kThreads, smem_bytes<0>(), st>>>(in, w, pass, delta_s * delta_s);
+    b_topk<0, T><<<dim3(rb, split, P), kThreads, smem_bytes<0>(), st>>>(in, w, pass);
     PS_LAUNCHED("b_topk<top4>");
-    b_certify<T><<<dim3(per(grid_for(nx, 32), P), P), 256, 0, st>>>(in, w, pass, kParts * split, rb * BM);
+    b_certify<T><<<dim3(per(grid_for(nx, 32), P), P), 256, 0, st>>>(in, w, pass, kParts * split, rb * BM, delta_s);
     PS_LAUNCHED("b_certify");
     b_gather<T><<<dim3(per(grid_for(nx, 256), P), P), 256, 0, st>>>(in, w, pass);
     PS_LAUNCHED("b_gather");
@@ -1975,14 +1951,15 @@ int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1
     // tensor cores, the rest (and overflowing enumerations) scanned exactly
     const int eb = (int)std::min<int64_t>(kEnumBlocksAsync, rb);
     const int enum_rows = eb * BM;
+    if (pass == 0) enum_rows0 = enum_rows;
     b_prep_rows<T><<<dim3(per(grid_for(enum_rows, 8), P), P), 256, 0, st>>>(in, w, pass, 1);
     PS_LAUNCHED("b_prep_rows(overflow)");
     const int split_e = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)kMaxSplit, tiles, 4 * kSMs / (P * eb)}));
-    b_topk<1, T><<<dim3(eb, split_e, P), kThreads, smem_bytes<1>(), st>>>(in, w, pass, -1.0);
+    b_topk<1, T><<<dim3(eb, split_e, P), kThreads, smem_bytes<1>(), st>>>(in, w, pass);
     PS_LAUNCHED("b_topk<enumerate>");
-    b_pair_dist_min<T><<<dim3(std::max(4, 148 * 16 / P), P), 256, 0, st>>>(in, w, pass);
+    b_pair_dist_min<T><<<dim3(std::max(4, 148 * 16 / P), P), 256, 0, st>>>(in, w, pass, delta_s);
     PS_LAUNCHED("b_pair_dist_min");
-    b_pair_argmin<T><<<dim3(std::max(2, 148 * 8 / P), P), 256, 0, st>>>(in, w, pass);
+    b_pair_argmin<T><<<dim3(std::max(2, 148 * 8 / P), P), 256, 0, st>>>(in, w, pass, delta_s);
     PS_LAUNCHED("b_pair_argmin");
     b_pair_write<T><<<dim3(grid_for(enum_rows, 256), P), 256, 0, st>>>(in, w, pass, enum_rows);
     PS_LAUNCHED("b_pair_write");
@@ -2038,26 +2015,33 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   mark();
   // pass 1: rows of A (representatives) against the distinct rows of B
   int64_t ua = -1, ub = -1;
+  // pass 1 also decides the columns (ColCand): nn21 from the exact distances below delta_s it computes
   cudaMemsetAsync(w.n_cand, 0, sizeof(unsigned long long), st);
-  rc = nearest_pass(A, n1, w.a.uniq, w.a.n_uniq, B, n2, w.b.uniq, w.b.n_uniq, w.nn12, w.d12, w, st, &ua, &ub, sync,
-                    delta_s * delta_s);
+  cudaMemsetAsync(w.cbits, 0xff, n2 * sizeof(unsigned long long), st);
+  cudaMemsetAsync(w.nn21, 0x7f, n2 * sizeof(int32_t), st);
+  cudaMemsetAsync(w.cand_incomplete, 0, sizeof(int32_t), st);
+  ColCand cc{delta_s, w.cand_incomplete, w.cbits, w.nn21, w.cand, w.cpd, w.n_cand};
+#ifdef PS_TC_DIAG_NOCAND  // diagnostic builds only: always two passes
+  cc = ColCand{};
+#endif
+  int enum_rows = INT32_MAX;
+  rc = nearest_pass(A, n1, w.a.uniq, w.a.n_uniq, B, n2, w.b.uniq, w.b.n_uniq, w.nn12, w.d12, w, st, &ua, &ub, sync, cc,
+                    &enum_rows);
   if (rc) return rc;
   g_stats[0] = ua;
   g_stats[1] = ub;
-  // the column candidates pass 1 listed decide nn21 (exact float64, first row index among equal distances)
-  cudaMemsetAsync(w.cbits, 0xff, n2 * sizeof(unsigned long long), st);
-  cudaMemsetAsync(w.nn21, 0x7f, n2 * sizeof(int32_t), st);
-  cand_dist_min<T><<<148 * 8, 256, 0, st>>>(w.cand, w.n_cand, w.cand_cap, w.a.uniq, w.b.uniq, A, B, w.cpd, w.cbits);
-  PS_LAUNCHED("cand_dist_min");
-  cand_argmin<T><<<148 * 4, 256, 0, st>>>(w.cand, w.n_cand, w.cand_cap, w.a.uniq, w.b.uniq, w.cpd, w.cbits, w.nn21);
-  PS_LAUNCHED("cand_argmin");
-  bool two_pass = true;  // unknown on the host in asynchronous mode: pass 2 is launched and finds no column
-  if (sync) {
-    unsigned long long nc = 0;
-    cudaMemcpyAsync(&nc, w.n_cand, sizeof(nc), cudaMemcpyDeviceToHost, st);
+  // pass 2 is needed only if rows were left to the exact scan (they list no columns).  Synchronous
+  // mode enumerates every overflow row, so only an enumeration that outgrew its buffer counts; in
+  // asynchronous mode the host cannot know: pass 2 is launched and finds no column (mark_columns)
+  bool two_pass = true;
+  if (sync && cc.cbits) {
+    unsigned long long np = 0;
+    int32_t inc = 0;
+    cudaMemcpyAsync(&np, w.n_pairs, sizeof(np), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(&inc, w.cand_incomplete, sizeof(inc), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    two_pass = (int64_t)nc > w.cand_cap;
-    g_stats[6] = (int64_t)nc;
+    two_pass = inc != 0 || (int64_t)np > w.pair_cap;
+    g_stats[6] = two_pass ? 2 : 1;  // passes run
   }
   mark();
   const int of1 = prof ? count_of(w.n_overflow) : 0;
@@ -2070,8 +2054,9 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   // that can be matched against the distinct rows of A
   if (two_pass) {
   cudaMemsetAsync(w.colflag, 0, n2 * sizeof(int32_t), st);
-  mark_columns<<<grid_for(n1, 256), 256, 0, st>>>(w.a.uniq, w.a.n_uniq, w.nn12, w.d12, delta_s, w.colflag, w.n_cand,
-                                                  w.cand_cap);
+  mark_columns<<<grid_for(n1, 256), 256, 0, st>>>(w.a.uniq, w.a.n_uniq, w.nn12, w.d12, delta_s, w.colflag,
+                                                  w.n_overflow, enum_rows, w.n_pairs, w.pair_cap,
+                                                  cc.cbits ? w.cand_incomplete : nullptr);
   PS_LAUNCHED("mark_columns");
   iota32<<<grid_for(n2, 256), 256, 0, st>>>(w.b.iota, n2);
   PS_LAUNCHED("iota32");

@@ -763,5 +763,5 @@ def match_stats() -> dict:
     arr = (C.c_int64 * 8)()
     _lib.lib().ps_match_stats(arr, 8)
     keys = ("distinct_rows_a", "distinct_rows_b", "candidate_columns", "enumerated_rows", "enumerated_pairs",
-            "mma_flops")
+            "mma_flops", "passes")
     return {k: int(arr[i]) for i, k in enumerate(keys)}
