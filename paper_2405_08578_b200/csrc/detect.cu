@@ -435,6 +435,123 @@ __global__ void __launch_bounds__(StripKeys<Img>::kMaxThreads) detect_strip(
   }
 }
 
+// Any window side up to kStripWMaxL, without block barriers: a task is
+// (image, window row, run of W windows) and belongs to ONE warp -- lane l owns
+// the 16-pixel chunk chunk0 + l of the run's columns (W * L + misalignment
+// <= 32 chunks) over the window row's rows, the column keys go to the warp's
+// own shared-memory slice, and after a __syncwarp the run's windows are folded
+// by one lane each exactly as in detect_strip.  Warps are independent, so the
+// loads of one overlap the folds of the others (detect_strip's CTAs idle at
+// two barriers per task, and a window row split into 256-chunk segments
+// leaves a ragged last segment); the chunks shared by neighbouring runs (at
+// most one per side) are read twice, from L2.
+constexpr int kStripWMaxL = 160;
+constexpr int kStripWCols = 512;  // column keys per warp and polarity
+template <class Img>
+struct StripW;
+template <>
+struct StripW<RampU8> {
+  static constexpr int kBatch = 8, kMinBlocks = 4;
+};
+template <>
+struct StripW<RampRGB8> {
+  static constexpr int kBatch = 2, kMinBlocks = 3;
+};
+inline int stripw_windows(int L) { return (kStripWCols - 30) / L; }  // 15 + W L + 15 <= 512
+
+template <class Img>
+__global__ void __launch_bounds__(256, StripW<Img>::kMinBlocks) detect_stripw(
+    Img img, int64_t img_stride, int B, int L, int wr_n, int wc, int nwin, int W, int nrun,
+    int32_t* __restrict__ tmax, int32_t* __restrict__ tmin, KpOut out, int32_t scale_tag) {
+  using SK = StripKeys<Img>;
+  using K = typename SK::K;
+  using A = typename std::conditional<std::is_same<Img, RampU8>::value, uint32_t, K>::type;
+  constexpr int NB = StripW<Img>::kBatch;
+  __shared__ K keys[8][2][kStripWCols];
+  const int nr = img.nr, nc = img.nc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  K* cmax = keys[warp][0];
+  K* cmin = keys[warp][1];
+  const int64_t ntask = (int64_t)B * wr_n * nrun, wstride = (int64_t)gridDim.x * 8;
+  for (int64_t task = (int64_t)blockIdx.x * 8 + warp; task < ntask; task += wstride) {
+    const int run = (int)(task % nrun);
+    const int64_t bw = task / nrun;
+    const int b = (int)(bw / wr_n), wr = (int)(bw % wr_n);
+    Img im = img;
+    im.p = img.p + (int64_t)b * img_stride * decltype(img)::kElem;
+    const int r0 = wr * L, h = min(L, nr - r0);
+    const int w0 = run * W, w1 = min(w0 + W, wc);
+    const int cb = w0 * L, ce = min(w1 * L, nc);
+    const int chunk0 = cb >> 4, nch = ((ce + 15) >> 4) - chunk0;  // <= 32
+    A mx[SK::kAcc], mn[SK::kAcc];
+    SK::init(mx, mn);
+    if (lane < nch) {
+      typename SK::Raw cur[NB];
+      for (int r = 0; r < h; r += NB) {
+        // one batch of rows in flight per warp (no second buffer): the registers saved double the
+        // resident warps, which is what keeps enough bytes in flight per SM
+#pragma unroll
+        for (int i = 0; i < NB; ++i) cur[i] = SK::load(im, r0 + min(r + i, h - 1), chunk0 + lane);  // clamped
+        if constexpr (std::is_same<Img, RampU8>::value) {
+          if (r + NB <= h) {
+#pragma unroll
+            for (int i = 0; i < NB; i += 2) SK::fold2(cur[i], cur[i + 1], (uint32_t)(r + i), mx, mn);
+          } else {
+#pragma unroll
+            for (int i = 0; i < NB; ++i)
+              if (r + i < h) SK::fold(cur[i], (uint32_t)(r + i), mx, mn);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < NB; ++i)
+            if (r + i < h) SK::fold(cur[i], (uint32_t)(r + i), mx, mn);
+        }
+      }
+    }
+    __syncwarp();  // the previous task's window folds are done with the keys
+    if (lane < nch) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        cmax[16 * lane + j] = SK::key(mx, j);
+        cmin[16 * lane + j] = SK::key(mn, j);
+      }
+    }
+    __syncwarp();
+    const int cs = chunk0 << 4;
+    for (int wcol = w0 + lane; wcol < w1; wcol += 32) {
+      const int c0 = wcol * L, c1 = min(c0 + L, nc);
+      K bx = cmax[c0 - cs], bn = cmin[c0 - cs];
+      int cx = c0, cn = c0;
+      for (int c = c0 + 1; c < c1; ++c) {
+        const K kx = cmax[c - cs], kn = cmin[c - cs];
+        if (kx >= bx) { bx = kx; cx = c; }
+        if (kn < bn) { bn = kn; cn = c; }
+      }
+      const int32_t kmax = (r0 + (int)(bx & 0xffu)) * nc + cx;
+      const int32_t kmin = (r0 + (int)(bn & 0xffu)) * nc + cn;
+      const int w = wr * wc + wcol;
+      if (tmax) {
+        tmax[(int64_t)b * nwin + w] = kmax;
+        tmin[(int64_t)b * nwin + w] = kmin;
+      }
+      if (out.row) {  // direct emission: slot 2w (max), 2w+1 (min)
+        const int64_t sl = (int64_t)b * out.cap + 2 * (int64_t)w;
+        const int32_t ks[2] = {kmax, kmin};
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int rr = ks[q] / nc, cc = ks[q] % nc;
+          out.row[sl + q] = rr;
+          out.col[sl + q] = cc;
+          out.value[sl + q] = im.at(rr, cc);
+          if (out.scale) out.scale[sl + q] = scale_tag;
+          if (out.pol) out.pol[sl + q] = (int8_t)q;
+          if (out.window) out.window[sl + q] = w;
+        }
+      }
+    }
+  }
+}
+
 // Window sides that are multiples of 16 (every scale of C1, C3 and C5): a
 // window is G = L / 16 whole 16-pixel chunks and its rows are split into R
 // groups, so G * R lanes (a power of two <= 32) own one window and each lane
@@ -563,7 +680,7 @@ template <class Img>
 int launch_strip(const Img& img, const ps_image_batch* ib, int B, int L, int wc, int nwin, const KpOut& ko,
                  int32_t* tmax, int32_t* tmin, cudaStream_t st) {
   using K = typename StripKeys<Img>::K;
-  if (L % 16 == 0 && L <= 256) {  // whole-chunk windows: the shuffle kernel
+  if (L % 16 == 0 && L <= 256 && (L & (L - 1)) == 0) {  // whole-chunk windows (G a power of two): the shuffle kernel
     const int wr_n = (img.nr + L - 1) / L;
     const int G = L / 16, R = std::max(1, std::min(L / 32, 32 / G));  // G * R lanes per window, <= 32 rows each
     const int W = 32 / (G * R);
@@ -575,6 +692,15 @@ int launch_strip(const Img& img, const ps_image_batch* ib, int B, int L, int wc,
     return PS_OK;
   }
   const int wr_n = (img.nr + L - 1) / L;
+  if (L <= kStripWMaxL) {  // warp-owned runs of windows: no block barriers
+    const int nrun = (wc + stripw_windows(L) - 1) / stripw_windows(L);
+    const int W = (wc + nrun - 1) / nrun;  // balanced runs
+    const int64_t tasks = (int64_t)B * wr_n * nrun;
+    const int grid = (int)std::min<int64_t>((tasks + 7) / 8, 148 * StripW<Img>::kMinBlocks * 4);
+    detect_stripw<Img><<<grid, 256, 0, st>>>(img, ib->image_stride, B, L, wr_n, wc, nwin, W, nrun, tmax, tmin, ko, L);
+    PS_LAUNCHED("detect_stripw");
+    return PS_OK;
+  }
   const int SW = strip_windows(L, wc), nseg = (wc + SW - 1) / SW;
   const size_t smem = 2 * (size_t)SW * L * sizeof(K);
   const int chunks = std::min((SW * L + 15) / 16, (img.nc + 15) / 16);

@@ -491,7 +491,14 @@ int match_impl(const void* desc1, int64_t n1, const void* desc2, int64_t n2, int
   pad_unused<<<grid_blocks(n, 256), 256, 0, st>>>(w.kp, w.kd, w.counter, n);
   PS_LAUNCHED("pad_unused");
   size_t tb = w.tmp_bytes;
-  cub::DeviceRadixSort::SortPairs(w.tmp, tb, w.kp, w.kp2, w.kd, w.kd2, n, 0, 64, st);
+  // pair keys are (row << 32 | column): only the bits that can differ are sorted.  The rows of
+  // nearest_neighbor / ratio_test matches are unique, so their row bits alone order the pairs
+  // (padding keys are placed last by the delta sort whatever this one does with them)
+  int row_bits = 1;
+  while (row_bits < 32 && (1ll << row_bits) < n1) ++row_bits;
+  const int base = strategy & 0xff;
+  const int bit0 = (base == PS_MATCH_NEAREST || base == PS_MATCH_RATIO) ? 32 : 0;
+  cub::DeviceRadixSort::SortPairs(w.tmp, tb, w.kp, w.kp2, w.kd, w.kd2, n, bit0, 32 + row_bits, st);
   PS_LAUNCHED("cub_sort(pair)");
   tb = w.tmp_bytes;
   cub::DeviceRadixSort::SortPairs(w.tmp, tb, w.kd2, w.kd, w.kp2, w.kp, n, 0, 64, st);

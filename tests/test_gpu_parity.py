@@ -915,7 +915,10 @@ def test_descriptor_out_of_image_features_clamped_like_reference():
 
 
 @pytest.mark.parametrize("nr,nc,scales", [(97, 131, (16, 24)), (200, 333, (36,)), (150, 255, (8, 12, 40)),
-                                          (64, 64, (17,)), (300, 257, (32, 64, 128)), (130, 140, (8, 16, 32))])
+                                          (64, 64, (17,)), (300, 257, (32, 64, 128)), (130, 140, (8, 16, 32)),
+                                          (250, 300, (48,)), (300, 1200, (48, 80)), (150, 2000, (36,)),
+                                          (100, 1700, (20,)), (330, 900, (96, 100)), (400, 700, (160, 176)),
+                                          (75, 5000, (36, 37))])
 def test_strip_detector_padded_pitch_tie_heavy(nr, nc, scales):
     """The vectorised strip kernel (any window side, 16-byte aligned rows):
     tie-heavy u8 and RGB rasters in a padded-pitch layout (odd widths, shrunk
