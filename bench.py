@@ -823,14 +823,55 @@ def bench_c1_latency(args, rank, dev, with_cpu, steps=10):
     return out
 
 
+def bench_detect_shapes(dev, peak):
+    """K1 on the shapes of C3 (u8, L 32..128), C4 (u8, L = 36) and C5 (RGB8, L 16..64): one
+    detect call replayed as a CUDA graph (no host launch gaps), CUDA events over 20 replays."""
+    import torch
+
+    from paper_2405_08578_b200 import device
+
+    out = {}
+    cases = [("C3 9x1600x2688 u8 L32..128", (9, 1600, 2688), (32, 64, 128), False),
+             ("C4 2x8192x8192 u8 L36", (2, 8192, 8192), (36,), False),
+             ("C5 64x1080x1920 rgb8 L16..64", (64, 1080, 1920), (16, 32, 64), True)]
+    for name, (B, nr, nc), scales, rgb in cases:
+        g = torch.Generator(device=dev).manual_seed(1)
+        t = torch.randint(0, 256, (B, nr, nc, 3) if rgb else (B, nr, nc), dtype=torch.uint8, device=dev, generator=g)
+        im = device.as_device_images(t, rgb=rgb)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                kp = device.detect(im, scales, meta=False, stream=s)
+            s.synchronize()
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr, stream=s):
+                kp = device.detect(im, scales, meta=False, stream=s)
+            gr.replay()
+            s.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(20):
+                gr.replay()
+            e1.record(s)
+            s.synchronize()
+        ms = e0.elapsed_time(e1) / 20
+        nbytes = t.numel() + int(kp.count.sum()) * 16
+        out[name] = {"us": round(ms * 1e3, 1), "GB/s": round(nbytes / ms / 1e6, 1),
+                     "frac_hbm": round(nbytes / ms / 1e6 / peak, 4), "bytes_per_launch": nbytes}
+        del t, im, kp, gr
+    return out
+
+
 # ---------------------------------------------------------------------------
 # Dense tensor-core matching at C4 scale (SURVEY §8(d) K3 >= 50 % of peak)
 # ---------------------------------------------------------------------------
 
 def bench_c4_dense(args, rank, dev, steps=5):
     """103,968^2 distinct unit descriptors (half of B near-copies of A rows,
-    so pass 2 runs too): the MNN match on the tensor cores, algorithmic
-    2*n1*n2*128 FLOPs / time vs the measured bf16 dense peak."""
+    so half the columns are matchable): the MNN match on the tensor cores,
+    algorithmic 2*n1*n2*128 FLOPs / time vs the measured bf16 dense peak.
+    ``passes`` reports whether the column pass ran (2) or pass 1's exact
+    distances below delta_s decided the columns (1; csrc/match_tc.cu ColCand)."""
     import torch
 
     from paper_2405_08578_b200 import device
@@ -866,13 +907,14 @@ def bench_c4_dense(args, rank, dev, steps=5):
     peak = _bf16_peak()
     return {"metric": "dense MNN pair-matches/s (103,968^2 distinct unit 128-d fp32 descriptors, tcgen05)",
             "value": round(n * n / (ms / 1e3), 1), "unit": "pair-matches/s", "ms_per_pair": round(ms, 3),
-            "matches": int(r[0].shape[0]), "exact_equal": same,
+            "matches": int(r[0].shape[0]), "exact_equal": same, "passes": stats.get("passes", 0),
             "roofline": {"bound": "tensor", "achieved": round(flops / (ms / 1e3) / 1e12, 1), "peak": peak,
                          "unit": "TFLOP/s", "frac": round(flops / (ms / 1e3) / 1e12 / peak, 4),
                          "algorithmic_flops": flops,
                          "executed_mma_flops": stats.get("mma_flops", 0),
-                         "note": "algorithmic 2*n1*n2*128 over the whole call (both passes, the exact float64 "
-                                 "certification and the ordering included); executed counts the fp16 MMA tiles "
+                         "note": "algorithmic 2*n1*n2*128 over the whole call (duplicate grouping, operand "
+                                 "tiles, the tensor-core pass(es), the exact float64 certification, the column "
+                                 "argmin and the ordering included); executed counts the fp16 MMA tiles "
                                  "issued (K = 144 incl. the |y|^2 augmentation)"},
             "tmem_roofline": tmem_roofline(stats.get("mma_flops", 0), ms, dev),
             "timing": "CUDA events over %d back-to-back calls (each has one host count read)" % steps}
@@ -1170,6 +1212,11 @@ def run_ours(args):
     kernels["detect_u8_w8"]["isolated"] = {"ms": round(det_iso_ms, 4), "GB/s": round(ach_iso, 1),
                                            "frac_hbm": round(ach_iso / peak, 4),
                                            "timing": f"CUDA events over {n_iso} back-to-back launches"}
+
+    # the other configs' detector shapes, in isolation (random 8-bit rasters: the detector's work does
+    # not depend on the content): bytes = 1 (3 for RGB) per pixel read + 16 per kept keypoint written
+    if rank == 0 and not getattr(args, "no_match", False):
+        kernels["detect_other_shapes"] = bench_detect_shapes(dev, peak)
 
     # ---- e2e through the public host API ----
     e2e = None
