@@ -268,8 +268,8 @@ struct StripKeys<RampU8> {
   using K = uint32_t;
   using Raw = uint4;
   static constexpr int kBatch = 8;  // rows whose loads are in flight together
-  static constexpr int kBatch16 = 2;  // the same for detect_strip16 (row pairs: fold2)
-  static constexpr int kMinBlocks16 = 3;  // its resident 256-thread CTAs per SM
+  static constexpr int kBatch16 = 8;  // the same for detect_strip16 (row pairs: fold2; single-buffered)
+  static constexpr int kMinBlocks16 = 4;  // its resident 256-thread CTAs per SM
   static constexpr int kMaxThreads = 256;
   static constexpr int kAcc = 8;    // registers per accumulator set
   static constexpr int kMaxRows = 256;  // the row index must fit its 8 bits
@@ -320,8 +320,8 @@ struct StripKeys<RampRGB8> {
     uint4 a, b, c;
   };
   static constexpr int kBatch = 4;
-  static constexpr int kBatch16 = 2;
-  static constexpr int kMinBlocks16 = 2;
+  static constexpr int kBatch16 = 4;  // detect_strip16: rows in flight per lane (single-buffered)
+  static constexpr int kMinBlocks16 = 3;
   static constexpr int kMaxThreads = 256;
   static constexpr int kAcc = 16;
   static constexpr int kMaxRows = 256;  // the row index must fit its 8 bits
@@ -333,6 +333,26 @@ struct StripKeys<RampRGB8> {
   __device__ __forceinline__ static Raw load(const RampRGB8& im, int rr, int chunk) {
     const uint4* src = reinterpret_cast<const uint4*>(im.p + 3 * (int64_t)rr * im.pitch) + 3 * chunk;
     return Raw{__ldg(src), __ldg(src + 1), __ldg(src + 2)};
+  }
+  // detect_strip16: a lane reduces its whole chunk to ONE key per polarity, (k << 12 | r << 4 | j)
+  // (k < 2^18, r < 2^8, j = column within the chunk): 2 accumulator registers instead of 32, which
+  // is what lets a third CTA reside per SM.  PARTIAL: only the first `nvalid` columns exist.
+  template <bool PARTIAL>
+  __device__ __forceinline__ static void fold_one(const Raw& q, uint32_t r, int nvalid, K& mx, K& mn) {
+    const uint32_t w[13] = {q.a.x, q.a.y, q.a.z, q.a.w, q.b.x, q.b.y, q.b.z, q.b.w, q.c.x, q.c.y, q.c.z, q.c.w, 0u};
+    const uint32_t r4 = r << 4;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int o = 3 * j;
+      const uint32_t px = __byte_perm(w[o >> 2], w[(o >> 2) + 1], (uint32_t)(o & 3) * 0x111u + 0x210u);
+      const uint32_t hi = __dp4a(px, 0x00000201u, 0u);
+      const uint32_t lo = __dp4a(px, 0x00724b2bu, 0u);
+      const K key = (hi << 20) + (lo << 12) + (r4 + (uint32_t)j);
+      if (!PARTIAL || j < nvalid) {
+        mx = max(mx, key);
+        mn = min(mn, key);
+      }
+    }
   }
   __device__ __forceinline__ static void fold(const Raw& q, uint32_t r, K (&mx)[kAcc], K (&mn)[kAcc]) {
     const uint32_t w[13] = {q.a.x, q.a.y, q.a.z, q.a.w, q.b.x, q.b.y, q.b.z, q.b.w, q.c.x, q.c.y, q.c.z, q.c.w, 0u};
@@ -588,18 +608,18 @@ __global__ void __launch_bounds__(256, StripKeys<Img>::kMinBlocks16) detect_stri
     const int r0 = wr * L, h = min(L, nr - r0);
     const int ra = rg * rpt, rb = min(ra + rpt, h);
     const bool has = wcol < wc && 16 * chunk < nc && ra < rb;
-    A mx[SK::kAcc], mn[SK::kAcc];
-    SK::init(mx, mn);
-    if (has) {
-      typename SK::Raw cur[NB], nxt[NB];
+    const int cw = 16 * c;  // column offset of the chunk within its window
+    unsigned long long bx = 0ull, bn = ~0ull;
+    // one batch of rows in flight per lane and no second buffer: the registers saved let another
+    // CTA reside per SM, which keeps more bytes in flight than two batches would
+    if constexpr (std::is_same<Img, RampU8>::value) {
+      A mx[SK::kAcc], mn[SK::kAcc];
+      SK::init(mx, mn);
+      if (has) {
+        typename SK::Raw cur[NB];
+        for (int r = ra; r < rb; r += NB) {
 #pragma unroll
-      for (int i = 0; i < NB; ++i) cur[i] = SK::load(im, r0 + min(ra + i, rb - 1), chunk);
-      for (int r = ra; r < rb; r += NB) {
-        if (r + NB < rb) {
-#pragma unroll
-          for (int i = 0; i < NB; ++i) nxt[i] = SK::load(im, r0 + min(r + NB + i, rb - 1), chunk);  // clamped
-        }
-        if constexpr (std::is_same<Img, RampU8>::value) {
+          for (int i = 0; i < NB; ++i) cur[i] = SK::load(im, r0 + min(r + i, rb - 1), chunk);  // clamped
           if (r + NB <= rb) {
 #pragma unroll
             for (int i = 0; i < NB; i += 2) SK::fold2(cur[i], cur[i + 1], (uint32_t)(r + i), mx, mn);
@@ -608,26 +628,37 @@ __global__ void __launch_bounds__(256, StripKeys<Img>::kMinBlocks16) detect_stri
             for (int i = 0; i < NB; ++i)
               if (r + i < rb) SK::fold(cur[i], (uint32_t)(r + i), mx, mn);
           }
-        } else {
-#pragma unroll
-          for (int i = 0; i < NB; ++i)
-            if (r + i < rb) SK::fold(cur[i], (uint32_t)(r + i), mx, mn);
         }
 #pragma unroll
-        for (int i = 0; i < NB; ++i) cur[i] = nxt[i];
+        for (int j = 0; j < 16; ++j) {
+          if (16 * chunk + j >= nc) continue;
+          const unsigned long long col = (unsigned long long)(cw + j);
+          const unsigned long long fx = ((unsigned long long)SK::key(mx, j) << 8) | col;  // (v, r, c)
+          const unsigned long long fn = ((unsigned long long)SK::key(mn, j) << 8) | col;
+          bx = fx > bx ? fx : bx;
+          bn = fn < bn ? fn : bn;
+        }
       }
-    }
-    const int cw = 16 * c;  // column offset of the chunk within its window
-    unsigned long long bx = 0ull, bn = ~0ull;
-    if (has) {
+    } else {  // RGB8: the chunk's single (k, r, j) key per polarity
+      typename SK::K kx = 0u, kn = 0xffffffffu;
+      if (has) {
+        const int nvalid = min(16, nc - 16 * chunk);
+        typename SK::Raw cur[NB];
+        for (int r = ra; r < rb; r += NB) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if (16 * chunk + j >= nc) continue;
-        const unsigned long long col = (unsigned long long)(cw + j);
-        const unsigned long long fx = ((unsigned long long)SK::key(mx, j) << 8) | col;  // (v, r, c)
-        const unsigned long long fn = ((unsigned long long)SK::key(mn, j) << 8) | col;
-        bx = fx > bx ? fx : bx;
-        bn = fn < bn ? fn : bn;
+          for (int i = 0; i < NB; ++i) cur[i] = SK::load(im, r0 + min(r + i, rb - 1), chunk);  // clamped
+          if (nvalid == 16) {
+#pragma unroll
+            for (int i = 0; i < NB; ++i)
+              if (r + i < rb) SK::template fold_one<false>(cur[i], (uint32_t)(r + i), 16, kx, kn);
+          } else {
+#pragma unroll
+            for (int i = 0; i < NB; ++i)
+              if (r + i < rb) SK::template fold_one<true>(cur[i], (uint32_t)(r + i), nvalid, kx, kn);
+          }
+        }
+        bx = ((unsigned long long)(kx >> 4) << 8) | (unsigned long long)(cw + (int)(kx & 15u));  // (v, r, c)
+        bn = ((unsigned long long)(kn >> 4) << 8) | (unsigned long long)(cw + (int)(kn & 15u));
       }
     }
     for (int o = 1; o < G; o <<= 1) {  // chunks of the window
