@@ -269,7 +269,8 @@ struct StripKeys<RampU8> {
   using Raw = uint4;
   static constexpr int kBatch = 8;  // rows whose loads are in flight together
   static constexpr int kBatch16 = 8;  // the same for detect_strip16 (row pairs: fold2; single-buffered)
-  static constexpr int kMinBlocks16 = 4;  // its resident 256-thread CTAs per SM
+  static constexpr int kStage16 = 8;  // rows staged through shared memory besides (8 + 8 = C1 / C5's 16-row windows)
+  static constexpr int kMinBlocks16 = 3;  // its resident 256-thread CTAs per SM
   static constexpr int kMaxThreads = 256;
   static constexpr int kAcc = 8;    // registers per accumulator set
   static constexpr int kMaxRows = 256;  // the row index must fit its 8 bits
@@ -469,14 +470,32 @@ constexpr int kStripWMaxL = 160;
 constexpr int kStripWCols = 512;  // column keys per warp and polarity
 template <class Img>
 struct StripW;
+// u8: a lane keeps kBatch rows in flight in registers AND kStage rows in flight into its own
+// shared-memory slots (cp.async, 16 bytes per row): bytes in flight are what bounds the kernel, and
+// registers alone hold too few of them (8 rows x 1024 threads = 131 KB per SM -> 0.46 of HBM).
 template <>
 struct StripW<RampU8> {
-  static constexpr int kBatch = 8, kMinBlocks = 4;
+#ifndef PS_STRIPW_STAGE
+#define PS_STRIPW_STAGE 10  // 8 + 10 rows: two rounds cover C4's 36-row windows exactly (A/B 8..18: 16.7 us vs 18.7)
+#endif
+  static constexpr int kBatch = 8, kStage = PS_STRIPW_STAGE, kMinBlocks = 3;
+  using KS = uint16_t;  // stored column key (v << 8 | r)
 };
 template <>
 struct StripW<RampRGB8> {
-  static constexpr int kBatch = 2, kMinBlocks = 3;
+  static constexpr int kBatch = 2, kStage = 0, kMinBlocks = 3;
+  using KS = uint32_t;
 };
+template <class Img>
+constexpr size_t stripw_smem() {
+  // per warp: the staging slots, reused for the run's column keys once its rows are folded
+  return 8 * std::max<size_t>(2 * kStripWCols * sizeof(typename StripW<Img>::KS), (size_t)StripW<Img>::kStage * 512);
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst_smem, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 inline int stripw_windows(int L) { return (kStripWCols - 30) / L; }  // 15 + W L + 15 <= 512
 
 template <class Img>
@@ -486,12 +505,16 @@ __global__ void __launch_bounds__(256, StripW<Img>::kMinBlocks) detect_stripw(
   using SK = StripKeys<Img>;
   using K = typename SK::K;
   using A = typename std::conditional<std::is_same<Img, RampU8>::value, uint32_t, K>::type;
-  constexpr int NB = StripW<Img>::kBatch;
-  __shared__ K keys[8][2][kStripWCols];
+  using KS = typename StripW<Img>::KS;
+  constexpr int NB = StripW<Img>::kBatch, NS = StripW<Img>::kStage;
+  extern __shared__ __align__(16) unsigned char stripw_raw[];
   const int nr = img.nr, nc = img.nc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  K* cmax = keys[warp][0];
-  K* cmin = keys[warp][1];
+  unsigned char* warp_area = stripw_raw + (size_t)warp * (stripw_smem<Img>() / 8);
+  KS* cmax = reinterpret_cast<KS*>(warp_area);  // the column keys alias the staging slots
+  KS* cmin = cmax + kStripWCols;
+  // this lane's staging slots: row i of a staged batch at stage + 512 i (conflict-free 16-byte reads)
+  unsigned char* stage = warp_area + lane * 16;
   const int64_t ntask = (int64_t)B * wr_n * nrun, wstride = (int64_t)gridDim.x * 8;
   for (int64_t task = (int64_t)blockIdx.x * 8 + warp; task < ntask; task += wstride) {
     const int run = (int)(task % nrun);
@@ -505,7 +528,52 @@ __global__ void __launch_bounds__(256, StripW<Img>::kMinBlocks) detect_stripw(
     const int chunk0 = cb >> 4, nch = ((ce + 15) >> 4) - chunk0;  // <= 32
     A mx[SK::kAcc], mn[SK::kAcc];
     SK::init(mx, mn);
-    if (lane < nch) {
+    __syncwarp();  // the previous run's window folds are done with the keys (they alias the staging slots)
+    if constexpr (NS > 0) {
+      if (lane < nch) {
+        // rows [r, r + NB) travel through registers, rows [r + NB, r + NB + NS) through the lane's
+        // staging slots, alternately: both kinds are in flight while the other is folded
+        const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
+        const unsigned char* colp = reinterpret_cast<const unsigned char*>(im.p) + 16 * (int64_t)(chunk0 + lane);
+        auto stage_rows = [&](int ra) {  // rows ra .. ra + NS - 1 (those below h) -> the slots
+#pragma unroll
+          for (int i = 0; i < NS; ++i)
+            if (ra + i < h) cp_async16(stage_s + 512u * i, colp + (int64_t)(r0 + ra + i) * im.pitch);
+          cp_async_commit();
+        };
+        typename SK::Raw cur[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) cur[i] = SK::load(im, r0 + min(i, h - 1), chunk0 + lane);  // clamped
+        stage_rows(NB);
+        for (int r = 0; r < h; r += NB + NS) {
+          if (r + NB <= h) {
+#pragma unroll
+            for (int i = 0; i < NB; i += 2) SK::fold2(cur[i], cur[i + 1], (uint32_t)(r + i), mx, mn);
+          } else {
+#pragma unroll
+            for (int i = 0; i < NB; ++i)
+              if (r + i < h) SK::fold(cur[i], (uint32_t)(r + i), mx, mn);
+          }
+          if (r + NB + NS < h) {
+#pragma unroll
+            for (int i = 0; i < NB; ++i) cur[i] = SK::load(im, r0 + min(r + NB + NS + i, h - 1), chunk0 + lane);
+          }
+          cp_async_wait_all();
+          const int rs = r + NB;
+          if (rs + NS <= h) {
+#pragma unroll
+            for (int i = 0; i < NS; i += 2)
+              SK::fold2(*reinterpret_cast<const uint4*>(stage + 512 * i),
+                        *reinterpret_cast<const uint4*>(stage + 512 * (i + 1)), (uint32_t)(rs + i), mx, mn);
+          } else {
+#pragma unroll
+            for (int i = 0; i < NS; ++i)
+              if (rs + i < h) SK::fold(*reinterpret_cast<const uint4*>(stage + 512 * i), (uint32_t)(rs + i), mx, mn);
+          }
+          if (r + 2 * NB + NS < h) stage_rows(r + 2 * NB + NS);  // after the slots' last reads were consumed
+        }
+      }
+    } else if (lane < nch) {
       typename SK::Raw cur[NB];
       for (int r = 0; r < h; r += NB) {
         // one batch of rows in flight per warp (no second buffer): the registers saved double the
@@ -528,12 +596,12 @@ __global__ void __launch_bounds__(256, StripW<Img>::kMinBlocks) detect_stripw(
         }
       }
     }
-    __syncwarp();  // the previous task's window folds are done with the keys
+    __syncwarp();  // every lane has folded its staged rows
     if (lane < nch) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        cmax[16 * lane + j] = SK::key(mx, j);
-        cmin[16 * lane + j] = SK::key(mn, j);
+        cmax[16 * lane + j] = (KS)SK::key(mx, j);
+        cmin[16 * lane + j] = (KS)SK::key(mn, j);
       }
     }
     __syncwarp();
@@ -615,11 +683,25 @@ __global__ void __launch_bounds__(256, StripKeys<Img>::kMinBlocks16) detect_stri
     if constexpr (std::is_same<Img, RampU8>::value) {
       A mx[SK::kAcc], mn[SK::kAcc];
       SK::init(mx, mn);
+      // as detect_stripw: NB rows in flight in registers and NS more into the lane's own staging
+      // slots (cp.async), alternately
+      constexpr int NS = SK::kStage16;
+      __shared__ __align__(16) unsigned char stage16[8][NS * 512];
       if (has) {
-        typename SK::Raw cur[NB];
-        for (int r = ra; r < rb; r += NB) {
+        unsigned char* stage = stage16[threadIdx.x >> 5] + lane * 16;
+        const uint32_t stage_s = (uint32_t)__cvta_generic_to_shared(stage);
+        const unsigned char* colp = reinterpret_cast<const unsigned char*>(im.p) + 16 * (int64_t)chunk;
+        auto stage_rows = [&](int r) {  // rows r .. r + NS - 1 (those below rb) -> the slots
 #pragma unroll
-          for (int i = 0; i < NB; ++i) cur[i] = SK::load(im, r0 + min(r + i, rb - 1), chunk);  // clamped
+          for (int i = 0; i < NS; ++i)
+            if (r + i < rb) cp_async16(stage_s + 512u * i, colp + (int64_t)(r0 + r + i) * im.pitch);
+          cp_async_commit();
+        };
+        typename SK::Raw cur[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) cur[i] = SK::load(im, r0 + min(ra + i, rb - 1), chunk);  // clamped
+        stage_rows(ra + NB);
+        for (int r = ra; r < rb; r += NB + NS) {
           if (r + NB <= rb) {
 #pragma unroll
             for (int i = 0; i < NB; i += 2) SK::fold2(cur[i], cur[i + 1], (uint32_t)(r + i), mx, mn);
@@ -628,6 +710,23 @@ __global__ void __launch_bounds__(256, StripKeys<Img>::kMinBlocks16) detect_stri
             for (int i = 0; i < NB; ++i)
               if (r + i < rb) SK::fold(cur[i], (uint32_t)(r + i), mx, mn);
           }
+          if (r + NB + NS < rb) {
+#pragma unroll
+            for (int i = 0; i < NB; ++i) cur[i] = SK::load(im, r0 + min(r + NB + NS + i, rb - 1), chunk);
+          }
+          cp_async_wait_all();
+          const int rs = r + NB;
+          if (rs + NS <= rb) {
+#pragma unroll
+            for (int i = 0; i < NS; i += 2)
+              SK::fold2(*reinterpret_cast<const uint4*>(stage + 512 * i),
+                        *reinterpret_cast<const uint4*>(stage + 512 * (i + 1)), (uint32_t)(rs + i), mx, mn);
+          } else {
+#pragma unroll
+            for (int i = 0; i < NS; ++i)
+              if (rs + i < rb) SK::fold(*reinterpret_cast<const uint4*>(stage + 512 * i), (uint32_t)(rs + i), mx, mn);
+          }
+          if (r + 2 * NB + NS < rb) stage_rows(r + 2 * NB + NS);  // after the slots' last reads were consumed
         }
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -713,7 +812,7 @@ int launch_strip(const Img& img, const ps_image_batch* ib, int B, int L, int wc,
   using K = typename StripKeys<Img>::K;
   if (L % 16 == 0 && L <= 256 && (L & (L - 1)) == 0) {  // whole-chunk windows (G a power of two): the shuffle kernel
     const int wr_n = (img.nr + L - 1) / L;
-    const int G = L / 16, R = std::max(1, std::min(L / 32, 32 / G));  // G * R lanes per window, <= 32 rows each
+    const int G = L / 16, R = std::max(1, std::min(L / 16, 32 / G));  // G * R lanes per window, 16 rows each up to L = 64
     const int W = 32 / (G * R);
     const int64_t warps = (int64_t)B * wr_n * ((wc + W - 1) / W);
     const int grid = (int)std::min<int64_t>((warps + 7) / 8, 148 * 24);
@@ -728,7 +827,9 @@ int launch_strip(const Img& img, const ps_image_batch* ib, int B, int L, int wc,
     const int W = (wc + nrun - 1) / nrun;  // balanced runs
     const int64_t tasks = (int64_t)B * wr_n * nrun;
     const int grid = (int)std::min<int64_t>((tasks + 7) / 8, 148 * StripW<Img>::kMinBlocks * 4);
-    detect_stripw<Img><<<grid, 256, 0, st>>>(img, ib->image_stride, B, L, wr_n, wc, nwin, W, nrun, tmax, tmin, ko, L);
+    cudaFuncSetAttribute(detect_stripw<Img>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stripw_smem<Img>());
+    detect_stripw<Img><<<grid, 256, stripw_smem<Img>(), st>>>(img, ib->image_stride, B, L, wr_n, wc, nwin, W, nrun,
+                                                              tmax, tmin, ko, L);
     PS_LAUNCHED("detect_stripw");
     return PS_OK;
   }
