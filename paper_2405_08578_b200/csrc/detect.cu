@@ -478,18 +478,24 @@ struct StripW<RampU8> {
 #ifndef PS_STRIPW_STAGE
 #define PS_STRIPW_STAGE 10  // 8 + 10 rows: two rounds cover C4's 36-row windows exactly (A/B 8..18: 16.7 us vs 18.7)
 #endif
-  static constexpr int kBatch = 8, kStage = PS_STRIPW_STAGE, kMinBlocks = 3;
+#ifndef PS_STRIPW_WARPS
+#define PS_STRIPW_WARPS 8
+#endif
+#ifndef PS_STRIPW_BLOCKS
+#define PS_STRIPW_BLOCKS 3
+#endif
+  static constexpr int kBatch = 8, kStage = PS_STRIPW_STAGE, kMinBlocks = PS_STRIPW_BLOCKS, kWarps = PS_STRIPW_WARPS;
   using KS = uint16_t;  // stored column key (v << 8 | r)
 };
 template <>
 struct StripW<RampRGB8> {
-  static constexpr int kBatch = 2, kStage = 0, kMinBlocks = 3;
+  static constexpr int kBatch = 2, kStage = 0, kMinBlocks = 3, kWarps = 8;
   using KS = uint32_t;
 };
 template <class Img>
 constexpr size_t stripw_smem() {
   // per warp: the staging slots, reused for the run's column keys once its rows are folded
-  return 8 * std::max<size_t>(2 * kStripWCols * sizeof(typename StripW<Img>::KS), (size_t)StripW<Img>::kStage * 512);
+  return StripW<Img>::kWarps * std::max<size_t>(2 * kStripWCols * sizeof(typename StripW<Img>::KS), (size_t)StripW<Img>::kStage * 512);
 }
 __device__ __forceinline__ void cp_async16(uint32_t dst_smem, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src) : "memory");
@@ -499,7 +505,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 inline int stripw_windows(int L) { return (kStripWCols - 30) / L; }  // 15 + W L + 15 <= 512
 
 template <class Img>
-__global__ void __launch_bounds__(256, StripW<Img>::kMinBlocks) detect_stripw(
+__global__ void __launch_bounds__(32 * StripW<Img>::kWarps, StripW<Img>::kMinBlocks) detect_stripw(
     Img img, int64_t img_stride, int B, int L, int wr_n, int wc, int nwin, int W, int nrun,
     int32_t* __restrict__ tmax, int32_t* __restrict__ tmin, KpOut out, int32_t scale_tag) {
   using SK = StripKeys<Img>;
@@ -510,13 +516,14 @@ __global__ void __launch_bounds__(256, StripW<Img>::kMinBlocks) detect_stripw(
   extern __shared__ __align__(16) unsigned char stripw_raw[];
   const int nr = img.nr, nc = img.nc;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned char* warp_area = stripw_raw + (size_t)warp * (stripw_smem<Img>() / 8);
+  constexpr int WPB = StripW<Img>::kWarps;
+  unsigned char* warp_area = stripw_raw + (size_t)warp * (stripw_smem<Img>() / WPB);
   KS* cmax = reinterpret_cast<KS*>(warp_area);  // the column keys alias the staging slots
   KS* cmin = cmax + kStripWCols;
   // this lane's staging slots: row i of a staged batch at stage + 512 i (conflict-free 16-byte reads)
   unsigned char* stage = warp_area + lane * 16;
-  const int64_t ntask = (int64_t)B * wr_n * nrun, wstride = (int64_t)gridDim.x * 8;
-  for (int64_t task = (int64_t)blockIdx.x * 8 + warp; task < ntask; task += wstride) {
+  const int64_t ntask = (int64_t)B * wr_n * nrun, wstride = (int64_t)gridDim.x * WPB;
+  for (int64_t task = (int64_t)blockIdx.x * WPB + warp; task < ntask; task += wstride) {
     const int run = (int)(task % nrun);
     const int64_t bw = task / nrun;
     const int b = (int)(bw / wr_n), wr = (int)(bw % wr_n);
@@ -826,9 +833,10 @@ int launch_strip(const Img& img, const ps_image_batch* ib, int B, int L, int wc,
     const int nrun = (wc + stripw_windows(L) - 1) / stripw_windows(L);
     const int W = (wc + nrun - 1) / nrun;  // balanced runs
     const int64_t tasks = (int64_t)B * wr_n * nrun;
-    const int grid = (int)std::min<int64_t>((tasks + 7) / 8, 148 * StripW<Img>::kMinBlocks * 4);
+    constexpr int WPB = StripW<Img>::kWarps;
+    const int grid = (int)std::min<int64_t>((tasks + WPB - 1) / WPB, 148 * StripW<Img>::kMinBlocks * 4);
     cudaFuncSetAttribute(detect_stripw<Img>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stripw_smem<Img>());
-    detect_stripw<Img><<<grid, 256, stripw_smem<Img>(), st>>>(img, ib->image_stride, B, L, wr_n, wc, nwin, W, nrun,
+    detect_stripw<Img><<<grid, 32 * WPB, stripw_smem<Img>(), st>>>(img, ib->image_stride, B, L, wr_n, wc, nwin, W, nrun,
                                                               tmax, tmin, ko, L);
     PS_LAUNCHED("detect_stripw");
     return PS_OK;
