@@ -452,6 +452,17 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
         uint32_t r[kChunk];
         tmem_ld_cols(tbase + c0, r);
         tmem_ld_wait();
+#ifndef PS_TC_LATE_RELEASE
+        // the accumulator's values are in registers now: release it BEFORE the compare work, so the
+        // MMA of tile t + 2 can be issued while this tile is still being scanned (released after the
+        // scan, the issue of t + 2 started ~700 cycles after MMA t ended and could not finish before
+        // MMA t + 1 did: the tensor pipe idled every tile)
+        if (c0 + kChunk >= kCols) {
+          tc_fence_before();
+          __syncwarp();  // every lane's TMEM reads are complete (tcgen05.wait::ld) before lane 0 releases
+          if (lane == 0) mbar_arrive(acc_empty + ab);
+        }
+#endif
         const int jb = tg * BN + part * kCols + c0;
 #pragma unroll
         for (int q = 0; q < kChunk / 4; ++q) {
@@ -507,9 +518,11 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
       } else {
         *(volatile float*)(sthr + part * BM + row) = tv[TOPK - 1];
       }
+#ifdef PS_TC_LATE_RELEASE  // diagnostic builds only: the accumulator released after the scan
       tc_fence_before();
       __syncwarp();  // every lane's TMEM reads are complete (tcgen05.wait::ld) before lane 0 releases
       if (lane == 0) mbar_arrive(acc_empty + ab);
+#endif
     }
     if (MODE == 1) {
       unsigned long long* hb = hitbuf + ew * HITBUF;
