@@ -18,7 +18,7 @@
 template <class T>
 int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double delta_s, unsigned long long* keys_pair,
                        unsigned long long* keys_delta, unsigned long long* counter, void* ws, size_t ws_bytes,
-                       cudaStream_t st, bool sync);
+                       cudaStream_t st, bool sync, int64_t* count_out);
 size_t ps_tc_nearest_ws(int64_t n1, int64_t n2);
 template <class T>
 int ps_tc_rows_impl(const T* X, int64_t nx, const T* Y, int64_t ny, int32_t* nn, double* dist, void* ws,
@@ -453,11 +453,12 @@ int match_impl(const void* desc1, int64_t n1, const void* desc2, int64_t n2, int
   MatchWs w = carve(workspace, n1, n2, cand, &used, extra);
   cudaMemsetAsync(w.counter, 0, sizeof(unsigned long long), st);
   int rc;
+  int64_t tc_count = -1;  // the tensor-core path's accepted count when it has read it already
   if (tc) {
     rc = desc_is_f64 ? ps_tc_nearest_impl((const double*)desc1, n1, (const double*)desc2, n2, delta_s, w.kp, w.kd,
-                                          w.counter, w.extra, w.extra_bytes, st, sync)
+                                          w.counter, w.extra, w.extra_bytes, st, sync, &tc_count)
                      : ps_tc_nearest_impl((const float*)desc1, n1, (const float*)desc2, n2, delta_s, w.kp, w.kd,
-                                          w.counter, w.extra, w.extra_bytes, st, sync);
+                                          w.counter, w.extra, w.extra_bytes, st, sync, &tc_count);
   } else {
     rc = desc_is_f64
              ? launch_match((const double*)desc1, n1, (const double*)desc2, n2, dim, delta_s, strategy, w, cand, st)
@@ -473,10 +474,12 @@ int match_impl(const void* desc1, int64_t n1, const void* desc2, int64_t n2, int
   // so does the tensor-core path in asynchronous mode.
   int n = (int)(cand > 0 ? cand : 1);
   if (tc && sync) {
-    unsigned long long c = 0;
-    cudaMemcpyAsync(&c, w.counter, sizeof(c), cudaMemcpyDeviceToHost, st);
-    const cudaError_t e = cudaStreamSynchronize(st);
-    PS_REQUIRE(e == cudaSuccess, PS_ERR_CUDA, "match count: %s", cudaGetErrorString(e));
+    unsigned long long c = (unsigned long long)std::max<int64_t>(tc_count, 0);
+    if (tc_count < 0) {
+      cudaMemcpyAsync(&c, w.counter, sizeof(c), cudaMemcpyDeviceToHost, st);
+      const cudaError_t e = cudaStreamSynchronize(st);
+      PS_REQUIRE(e == cudaSuccess, PS_ERR_CUDA, "match count: %s", cudaGetErrorString(e));
+    }
     n = (int)std::max<unsigned long long>(1ull, std::min<unsigned long long>(c, (unsigned long long)n));
   }
   if (n <= kSmallSort) {

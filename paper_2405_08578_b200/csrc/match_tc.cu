@@ -642,19 +642,24 @@ __device__ __forceinline__ void certify_exact_body(const float* __restrict__ top
         if (lv[q] < tv[TOPK - 1]) topk_insert(lv[q], lj[q], tv, tj);
     }
     const double lim = (double)tv[0] + 2.0 * E;
-    double clim = lim;  // candidate limit: also every column that can be closer than delta_s (ColCand)
+    double cth = -INFINITY;  // column threshold: v of every column that can be closer than delta_s (ColCand)
     if (cc.cbits) {
       const double nxv = xinfo[3 * uu];
       const double c = cc.delta_s * cc.delta_s * (1.0 + 1e-9) - nxv * nxv + E + 1e-6;
-      clim = (c == c) ? fmax(lim, c) : INFINITY;
+      cth = (c == c) ? c : INFINITY;
     }
+    const double clim = fmax(lim, cth);  // candidate limit
     const bool over = (double)tv[TOPK - 1] <= lim;  // candidates may extend past the top-4
+    // a row whose 4th best is within the column threshold may have any number of columns below it:
+    // the list is declared incomplete instead of enumerating them (clustered descriptors: most rows)
+    const bool many = cc.cbits && (double)tv[TOPK - 1] <= cth;
     if (live && over && t == 0) {
       const int slot = atomicAdd(n_overflow, 1);
       overflow[slot] = u;
-      overflow_lim[slot] = __double2float_ru(clim);  // the enumeration lists the row's column candidates too
+      // otherwise the enumeration lists the row's (at most three) column candidates too
+      overflow_lim[slot] = __double2float_ru(many ? lim : clim);
     }
-    if (cc.cbits && live && !over && t == 0 && (double)tv[TOPK - 1] <= clim) *cc.incomplete = 1;
+    if (live && many && t == 0) *cc.incomplete = 1;
     double bd = INFINITY;
     int bj = INT32_MAX;
     // the (up to TOPK) candidate distances are computed together: TOPK
@@ -1183,7 +1188,8 @@ template <class T>
 int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t* n_x, const T* Y, int64_t ny_all,
                  const int32_t* y_idx, const int32_t* n_y, int32_t* nn, double* dist, const TcWs& w,
                  cudaStream_t st, int64_t* nx_io = nullptr, int64_t* ny_io = nullptr, bool sync = true,
-                 ColCand cc = ColCand{}, int* enum_rows_out = nullptr) {  // cc.cbits: the pass also decides the columns
+                 ColCand cc = ColCand{}, int* enum_rows_out = nullptr,  // cc.cbits: the pass also decides the columns
+                 int32_t* incomplete_out = nullptr) {  // sync: *cc.incomplete, read with the overflow count
   const int64_t xrows = rup(nx_max, BM), yrows = rup(ny_all, BN);
   cudaMemsetAsync(w.ymax, 0, 4 * sizeof(unsigned), st);
   cudaMemsetAsync(w.n_overflow, 0, sizeof(int32_t), st);
@@ -1222,7 +1228,14 @@ int nearest_pass(const T* X, int64_t nx_max, const int32_t* x_idx, const int32_t
   // operand tiles of the overflow rows: the enumeration reads at most the
   // first kEnumBlocksAsync row blocks without a host count (async), all of
   // them with one (sync; rows beyond take the exact scan either way)
-  const int64_t n_over = sync ? read_count(w.n_overflow, st) : -1;
+  int64_t n_over = -1;
+  if (sync && cc.cbits && incomplete_out) {  // one synchronisation for both
+    int64_t inc = 0;
+    read_counts(w.n_overflow, cc.incomplete, &n_over, &inc, st);
+    *incomplete_out = (int32_t)inc;
+  } else if (sync) {
+    n_over = read_count(w.n_overflow, st);
+  }
   const int64_t over_rows = sync ? rup(n_over, BM) : std::min<int64_t>(xrows, (int64_t)kEnumBlocksAsync * BM);
   if (over_rows > 0) {
     prep_tiles<T><<<grid_for(over_rows, 8), 256, 0, st>>>(X, w.xsrc, w.n_overflow, 0, over_rows, BMH, w.xt, w.xinfo,
@@ -1994,7 +2007,7 @@ int batch_impl(const BatchIn<T>& in, int S, int P, double delta_s, int32_t* ref1
 template <class T>
 int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double delta_s, unsigned long long* keys_pair,
                        unsigned long long* keys_delta, unsigned long long* counter, void* ws, size_t ws_bytes,
-                       cudaStream_t st, bool sync) {
+                       cudaStream_t st, bool sync, int64_t* count_out) {  // sync: *count_out = accepted pairs (or left alone)
   using namespace ps::tc;
   size_t need = 0;
   carve_tc(nullptr, n1, n2, &need);
@@ -2038,24 +2051,18 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   cc = ColCand{};
 #endif
   int enum_rows = INT32_MAX;
+  int32_t incomplete = 0;
   rc = nearest_pass(A, n1, w.a.uniq, w.a.n_uniq, B, n2, w.b.uniq, w.b.n_uniq, w.nn12, w.d12, w, st, &ua, &ub, sync, cc,
-                    &enum_rows);
+                    &enum_rows, &incomplete);
   if (rc) return rc;
   g_stats[0] = ua;
   g_stats[1] = ub;
-  // pass 2 is needed only if rows were left to the exact scan (they list no columns).  Synchronous
-  // mode enumerates every overflow row, so only an enumeration that outgrew its buffer counts; in
-  // asynchronous mode the host cannot know: pass 2 is launched and finds no column (mark_columns)
-  bool two_pass = true;
-  if (sync && cc.cbits) {
-    unsigned long long np = 0;
-    int32_t inc = 0;
-    cudaMemcpyAsync(&np, w.n_pairs, sizeof(np), cudaMemcpyDeviceToHost, st);
-    cudaMemcpyAsync(&inc, w.cand_incomplete, sizeof(inc), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    two_pass = inc != 0 || (int64_t)np > w.pair_cap;
-    g_stats[6] = two_pass ? 2 : 1;  // passes run
-  }
+  // The column pass is needed only if pass 1's column candidates are incomplete.  Synchronous mode
+  // knows the flag (read with the overflow count) and enumerates every overflow row, so what is left
+  // is an enumeration that outgrew its buffer -- checked below with the accepted count, in the one
+  // synchronisation the caller needs anyway.  Asynchronous mode cannot know: the column pass is
+  // launched and finds no column (mark_columns).
+  bool two_pass = !(sync && cc.cbits) || incomplete != 0;
   mark();
   const int of1 = prof ? count_of(w.n_overflow) : 0;
   unsigned long long np1 = 0;
@@ -2086,6 +2093,38 @@ int ps_tc_nearest_impl(const T* A, int64_t n1, const T* B, int64_t n2, double de
   accept_pairs<<<grid_for(n1, 256), 256, 0, st>>>(w.a.rep, n1, w.nn12, w.d12, w.nn21, delta_s, keys_pair, keys_delta,
                                                   counter);
   PS_LAUNCHED("accept_pairs");
+  if (sync) {
+    g_stats[6] = two_pass ? 2 : 1;  // passes run
+    unsigned long long c = 0, np = 0;
+    cudaMemcpyAsync(&c, counter, sizeof(c), cudaMemcpyDeviceToHost, st);
+    if (!two_pass) cudaMemcpyAsync(&np, w.n_pairs, sizeof(np), cudaMemcpyDeviceToHost, st);
+    const cudaError_t e = cudaStreamSynchronize(st);
+    PS_REQUIRE(e == cudaSuccess, PS_ERR_CUDA, "match count: %s", cudaGetErrorString(e));
+    if (!two_pass && (int64_t)np > w.pair_cap) {
+      // pass 1's enumeration outgrew its buffer (its rows took the exact scan and listed no
+      // columns): the column pass after all, and the acceptance again
+      g_stats[6] = 2;
+      cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st);
+      cudaMemsetAsync(w.colflag, 0, n2 * sizeof(int32_t), st);
+      mark_columns<<<grid_for(n1, 256), 256, 0, st>>>(w.a.uniq, w.a.n_uniq, w.nn12, w.d12, delta_s, w.colflag,
+                                                      nullptr, 0, nullptr, 0, nullptr);
+      PS_LAUNCHED("mark_columns");
+      iota32<<<grid_for(n2, 256), 256, 0, st>>>(w.b.iota, n2);
+      PS_LAUNCHED("iota32");
+      size_t tb2 = w.cub_bytes;
+      cub::DeviceSelect::Flagged(w.cub_tmp, tb2, w.b.iota, w.colflag, w.cols, w.n_cols, (int)n2, st);
+      PS_LAUNCHED("cub_select(columns)");
+      int64_t ncols2 = -1;
+      rc = nearest_pass(B, n2, w.cols, w.n_cols, A, n1, w.a.uniq, w.a.n_uniq, w.nn21, w.d21, w, st, &ncols2, &ua, true);
+      if (rc) return rc;
+      g_stats[2] = ncols2;
+      accept_pairs<<<grid_for(n1, 256), 256, 0, st>>>(w.a.rep, n1, w.nn12, w.d12, w.nn21, delta_s, keys_pair,
+                                                      keys_delta, counter);
+      PS_LAUNCHED("accept_pairs");
+    } else if (count_out) {
+      *count_out = (int64_t)c;
+    }
+  }
   if (prof) {
     cudaStreamSynchronize(st);
     float t[8] = {0};
@@ -2137,9 +2176,9 @@ size_t ps_tc_nearest_ws(int64_t n1, int64_t n2) {
 }
 
 template int ps_tc_nearest_impl<float>(const float*, int64_t, const float*, int64_t, double, unsigned long long*,
-                                       unsigned long long*, unsigned long long*, void*, size_t, cudaStream_t, bool);
+                                       unsigned long long*, unsigned long long*, void*, size_t, cudaStream_t, bool, int64_t*);
 template int ps_tc_nearest_impl<double>(const double*, int64_t, const double*, int64_t, double, unsigned long long*,
-                                        unsigned long long*, unsigned long long*, void*, size_t, cudaStream_t, bool);
+                                        unsigned long long*, unsigned long long*, void*, size_t, cudaStream_t, bool, int64_t*);
 
 // ---- batched pairs: C entry points -------------------------------------------------------
 namespace {
