@@ -380,6 +380,20 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
     if (lane == 0) {  // ---- MMA issuer
       const uint32_t idesc = idesc_f16_f32(BMH, BN);
       const uint32_t a0 = smem_u32(sA);
+#ifndef PS_TC_NO_PREDESC  // operand descriptors built once (-DPS_TC_NO_PREDESC: rebuilt per MMA, 2.4 % slower) (the start-address field of a Y stage is added per tile)
+      uint64_t adp[XH][KD / 16 + 1], bdp[KD / 16 + 1];
+#pragma unroll
+      for (int h = 0; h < XH; ++h) {
+#pragma unroll
+        for (int k = 0; k < KD / 16; ++k)
+          adp[h][k] = sdesc_k_sw128(a0 + h * A_BYTES + (k >> 2) * (BMH * 128) + (uint32_t)((k & 3) * 32));
+        adp[h][KD / 16] = sdesc_k_none(a0 + h * A_BYTES + BMH * KD * 2);
+      }
+      const uint32_t bb = smem_u32(sB);
+#pragma unroll
+      for (int k = 0; k < KD / 16; ++k) bdp[k] = sdesc_k_sw128(bb + (k >> 2) * (BN * 128) + (uint32_t)((k & 3) * 32));
+      bdp[KD / 16] = sdesc_k_none(bb + BN * KD * 2);
+#endif
       mbar_wait(a_full, 0);
       for (int t = 0; t < n_tiles; ++t) {
         const int s = t % STAGES, ab = t % NACC;
@@ -387,6 +401,16 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
         mbar_wait(b_full + s, (t / STAGES) & 1);
         tc_fence_after();
         const uint32_t b0 = smem_u32(sB + s * B_BYTES);
+#ifndef PS_TC_NO_PREDESC
+        const uint64_t soff = (uint64_t)((uint32_t)s * (B_BYTES >> 4));  // stage offset in the 16-byte address field
+#pragma unroll
+        for (int h = 0; h < XH; ++h) {
+          const uint32_t acc = tmem + (uint32_t)((ab * XH + h) * BN);
+#pragma unroll
+          for (int k = 0; k <= KD / 16; ++k) mma_f16(acc, adp[h][k], bdp[k] + soff, idesc, k > 0 ? 1u : 0u);
+        }
+        (void)b0;
+#else
 #pragma unroll
         for (int h = 0; h < XH; ++h) {  // accumulator (ab, h): TMEM columns (ab * XH + h) * BN
           const uint32_t ah = a0 + h * A_BYTES, acc = tmem + (uint32_t)((ab * XH + h) * BN);
@@ -401,6 +425,7 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
           mma_f16(acc, sdesc_k_none(ah + BMH * KD * 2), sdesc_k_none(b0 + BN * KD * 2), idesc, 1u);
 #endif
         }
+#endif  // PS_TC_NO_PREDESC
         mma_commit(b_empty + s);
         mma_commit(acc_full + ab);
       }
@@ -447,6 +472,56 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
       unsigned long long* hb = hitbuf + ew * HITBUF;
       int fill = MODE == 1 ? hitcnt[ew] : 0;
       constexpr int kChunk = kCols < 64 ? kCols : 64;  // TMEM columns per load (x64 or x32)
+#ifdef PS_TC_SCAN_2PHASE
+      if constexpr (MODE == 0) {
+        // A/B build only (-DPS_TC_SCAN_2PHASE): two-phase scan -- (1) a branch-free pass over the
+        // chunk's 16 groups that only records which groups beat the bound, (2) a warp-uniform loop
+        // over the union of the lanes' hit groups that re-reads those four columns from TMEM
+        // (dynamic address: no register indexing) and inserts; the accumulator is released after (2).
+        // The scan, not the TMEM read, is what the epilogue costs (LOADONLY / NOEPI diagnostics: 1.86
+        // vs 2.50 ms per dense pass), but this compact form (the scan loop shrinks from ~1,500 to
+        // ~300 instructions) measures 2.53 ms against the inlined form's 2.50: neither code size nor
+        // the insertions are the cost -- the ~90 compare instructions per warp and tile are.
+#pragma unroll 1
+        for (int c0 = 0; c0 < kCols; c0 += kChunk) {
+          uint32_t hit = 0;
+          {
+            uint32_t r[kChunk];
+            tmem_ld_cols(tbase + c0, r);
+            tmem_ld_wait();
+            const float thr0 = fminf(tv[TOPK - 1], tsh);  // the bound only falls: later groups may be flagged needlessly
+#pragma unroll
+            for (int q = 0; q < kChunk / 4; ++q) {
+              const float m4 = fminf(fminf(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1])),
+                                     fminf(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
+              hit |= m4 < thr0 ? 1u << q : 0u;
+            }
+          }
+          uint32_t wm = __reduce_or_sync(0xffffffffu, hit);
+          const int jb = tg * BN + part * kCols + c0;
+#pragma unroll 1
+          while (wm) {
+            const int g = __ffs(wm) - 1;
+            wm &= wm - 1u;
+            uint32_t x[4];
+            tmem_ld4(tbase + c0 + 4 * g, x);
+            tmem_ld_wait();
+            if ((hit >> g) & 1u) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float v = __uint_as_float(x[e]);
+                if (v < fminf(tv[TOPK - 1], tsh)) topk_insert(v, jb + 4 * g + e, tv, tj);
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();  // every lane's TMEM reads are complete (tcgen05.wait::ld) before lane 0 releases
+        if (lane == 0) mbar_arrive(acc_empty + ab);
+        *(volatile float*)(sthr + part * BM + row) = tv[TOPK - 1];
+        continue;
+      }
+#endif
 #pragma unroll 1
       for (int c0 = 0; c0 < kCols; c0 += kChunk) {
         uint32_t r[kChunk];
@@ -464,6 +539,15 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
         }
 #endif
         const int jb = tg * BN + part * kCols + c0;
+#ifdef PS_TC_DIAG_LOADONLY  // diagnostic builds only: the TMEM read without the scan (wrong results)
+        if (MODE == 0) {
+          uint32_t x = 0;
+#pragma unroll
+          for (int q = 0; q < kChunk; q += 16) x ^= r[q];
+          if (x == 0x9E3779B9u) tv[0] = 0.0f;
+          continue;
+        }
+#endif
 #pragma unroll
         for (int q = 0; q < kChunk / 4; ++q) {
           const float v0 = __uint_as_float(r[4 * q + 0]);
@@ -472,7 +556,7 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
           const float v3 = __uint_as_float(r[4 * q + 3]);
           const float m4 = fminf(fminf(v0, v1), fminf(v2, v3));
           if (MODE == 0) {
-            if (m4 < fminf(tv[TOPK - 1], tsh)) {  // rare after the first tiles
+            if (m4 < fminf(tv[TOPK - 1], tsh)) {
               if (v0 < fminf(tv[TOPK - 1], tsh)) topk_insert(v0, jb + 4 * q + 0, tv, tj);
               if (v1 < fminf(tv[TOPK - 1], tsh)) topk_insert(v1, jb + 4 * q + 1, tv, tj);
               if (v2 < fminf(tv[TOPK - 1], tsh)) topk_insert(v2, jb + 4 * q + 2, tv, tj);
