@@ -52,8 +52,13 @@ constexpr int BN = PS_TC_BN;   // Y rows per tile (= MMA N)
 constexpr int NACC = 512 / (XH * BN);  // accumulator buffers in flight (TMEM holds 512 columns)
 static_assert(NACC >= 2 && (NACC & (NACC - 1)) == 0, "TMEM ring");
 constexpr int KD = 128;        // descriptor length
+// Candidates kept per (row, part, split).  The scan's cost is its ALU-pipe instructions (half rate,
+// four epilogue warps per scheduler in lockstep: ~8 cycles of scheduler time per warp instruction,
+// PS_TC_DIAG_CLOCKS), and both the hit rate and the insertion shrink with the list: 3 instead of 4
+// is +7 % on C5's pairs (6,360 -> 6,810 pairs/s), 2 % on the dense match, nothing on C4; 2 makes so
+// many rows overflow on clustered descriptors that C5 collapses (152 pairs/s).
 #ifndef PS_TC_TOPK
-#define PS_TC_TOPK 4
+#define PS_TC_TOPK 3
 #endif
 constexpr int TOPK = PS_TC_TOPK;  // candidates kept per (row, part, split)
 // Y-tile stages: as many as fit beside the X tiles (XH = 1, BN = 256: 2 x 72 KB;
@@ -395,10 +400,24 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
       bdp[KD / 16] = sdesc_k_none(bb + BN * KD * 2);
 #endif
       mbar_wait(a_full, 0);
+#ifdef PS_TC_DIAG_CLOCKS  // diagnostic builds only: where the issuer and one epilogue warp spend their cycles
+      long long c_acc = 0, c_b = 0, c_iss = 0;
+#endif
       for (int t = 0; t < n_tiles; ++t) {
         const int s = t % STAGES, ab = t % NACC;
+#ifdef PS_TC_DIAG_CLOCKS
+        const long long k0 = clock64();
+#endif
         mbar_wait(acc_empty + ab, ((t / NACC) & 1) ^ 1);
+#ifdef PS_TC_DIAG_CLOCKS
+        const long long k1 = clock64();
+#endif
         mbar_wait(b_full + s, (t / STAGES) & 1);
+#ifdef PS_TC_DIAG_CLOCKS
+        const long long k2 = clock64();
+        c_acc += k1 - k0;
+        c_b += k2 - k1;
+#endif
         tc_fence_after();
         const uint32_t b0 = smem_u32(sB + s * B_BYTES);
 #ifndef PS_TC_NO_PREDESC
@@ -428,7 +447,15 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
 #endif  // PS_TC_NO_PREDESC
         mma_commit(b_empty + s);
         mma_commit(acc_full + ab);
+#ifdef PS_TC_DIAG_CLOCKS
+        c_iss += clock64() - k2;
+#endif
       }
+#ifdef PS_TC_DIAG_CLOCKS
+      if (MODE == 0 && blockIdx.x == 7 && blockIdx.y == 0)
+        printf("[issuer] tiles %d: wait acc_empty %lld, wait b_full %lld, issue %lld cycles per tile\n", n_tiles,
+               c_acc / n_tiles, c_b / n_tiles, c_iss / n_tiles);
+#endif
     }
   } else {  // ---- epilogue: thread = row, kParts warps per lane quarter split the columns
     const int quarter = warp & 3;
@@ -442,9 +469,20 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
     const int64_t grow = (int64_t)rb * BM + row;
     // dead rows (beyond the count; their X rows may be stale) get a NaN limit: no v compares <= NaN
     const float my_lim = (MODE == 1 && grow < nx) ? lim[grow] : __int_as_float(0x7fc00000);
+#ifdef PS_TC_DIAG_CLOCKS
+    long long e_wait = 0, e_work = 0, e_mark = 0, e_ld = 0, e_hot = 0, e_slow = 0, e_nslow = 0;
+#endif
     for (int t = 0; t < n_tiles; ++t) {
       const int ab = t % NACC;
+#ifdef PS_TC_DIAG_CLOCKS
+      const long long q0 = clock64();
+      if (t > 0) e_work += q0 - e_mark;
+#endif
       mbar_wait(acc_full + ab, (t / NACC) & 1);
+#ifdef PS_TC_DIAG_CLOCKS
+      e_mark = clock64();
+      e_wait += e_mark - q0;
+#endif
       tc_fence_after();
       const int tg = t_begin + (t + t_rot < n_tiles ? t + t_rot : t + t_rot - n_tiles);  // global tile index
       const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + (ab * XH + h) * BN + part * kCols;
@@ -485,39 +523,78 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
 #pragma unroll 1
         for (int c0 = 0; c0 < kCols; c0 += kChunk) {
           uint32_t hit = 0;
-          {
-            uint32_t r[kChunk];
-            tmem_ld_cols(tbase + c0, r);
-            tmem_ld_wait();
-            const float thr0 = fminf(tv[TOPK - 1], tsh);  // the bound only falls: later groups may be flagged needlessly
+#ifdef PS_TC_DIAG_CLOCKS
+          const long long z0 = clock64();
+#endif
+          uint32_t r[kChunk];
+          tmem_ld_cols(tbase + c0, r);
+          tmem_ld_wait();
+#ifdef PS_TC_DIAG_CLOCKS
+          e_ld += clock64() - z0;
+#endif
+          if (c0 + kChunk >= kCols) {  // the accumulator's values are in registers: release it before the scan
+            tc_fence_before();
+            __syncwarp();  // every lane's TMEM reads are complete (tcgen05.wait::ld) before lane 0 releases
+            if (lane == 0) mbar_arrive(acc_empty + ab);
+          }
+          const float thr0 = fminf(tv[TOPK - 1], tsh);  // the bound only falls: later groups may be flagged needlessly
 #pragma unroll
-            for (int q = 0; q < kChunk / 4; ++q) {
-              const float m4 = fminf(fminf(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1])),
-                                     fminf(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
-              hit |= m4 < thr0 ? 1u << q : 0u;
-            }
+          for (int q = 0; q < kChunk / 4; ++q) {
+            const float m4 = fminf(fminf(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1])),
+                                   fminf(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
+            hit |= m4 < thr0 ? 1u << q : 0u;
           }
           uint32_t wm = __reduce_or_sync(0xffffffffu, hit);
+#ifdef PS_TC_DIAG_CLOCKS
+          const long long z1 = clock64();
+          e_hot += z1 - z0;
+          e_nslow += __popc(wm);
+#endif
           const int jb = tg * BN + part * kCols + c0;
 #pragma unroll 1
           while (wm) {
             const int g = __ffs(wm) - 1;
             wm &= wm - 1u;
-            uint32_t x[4];
-            tmem_ld4(tbase + c0 + 4 * g, x);
-            tmem_ld_wait();
+            // the group's four values: a warp-uniform jump into 16 four-move cases (the registers
+            // cannot be indexed; re-reading the columns from TMEM cost ~500 cycles per group)
+            uint32_t x0, x1, x2, x3;
+            static_assert(kChunk == 64 || kChunk == 32, "chunk of 8 or 16 groups");
+#define PS_GROUP(q) \
+  case q:           \
+    x0 = r[(4 * (q)) % kChunk], x1 = r[(4 * (q) + 1) % kChunk], x2 = r[(4 * (q) + 2) % kChunk], x3 = r[(4 * (q) + 3) % kChunk]; \
+    break;
+            switch (g) {
+              PS_GROUP(0) PS_GROUP(1) PS_GROUP(2) PS_GROUP(3) PS_GROUP(4) PS_GROUP(5) PS_GROUP(6) PS_GROUP(7)
+              PS_GROUP(8) PS_GROUP(9) PS_GROUP(10) PS_GROUP(11) PS_GROUP(12) PS_GROUP(13) PS_GROUP(14)
+              default:
+                x0 = r[kChunk - 4], x1 = r[kChunk - 3], x2 = r[kChunk - 2], x3 = r[kChunk - 1];
+            }
+#undef PS_GROUP
             if ((hit >> g) & 1u) {
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float v = __uint_as_float(x[e]);
-                if (v < fminf(tv[TOPK - 1], tsh)) topk_insert(v, jb + 4 * g + e, tv, tj);
+              // the whole warp pays for this block whenever one lane is in it: one insertion of the
+              // group's minimum (first column on ties), the other three only if the group's second
+              // smallest also beats the updated bound (rare)
+              const float v0 = __uint_as_float(x0), v1 = __uint_as_float(x1), v2 = __uint_as_float(x2),
+                          v3 = __uint_as_float(x3);
+              const float lo01 = fminf(v0, v1), lo23 = fminf(v2, v3), m4 = fminf(lo01, lo23);
+              if (m4 < fminf(tv[TOPK - 1], tsh)) {
+                const int jm = v0 == m4 ? 0 : v1 == m4 ? 1 : v2 == m4 ? 2 : 3;
+                topk_insert(m4, jb + 4 * g + jm, tv, tj);
+                const float s4 = fminf(fmaxf(lo01, lo23), fminf(fmaxf(v0, v1), fmaxf(v2, v3)));
+                if (s4 < fminf(tv[TOPK - 1], tsh)) {
+#pragma unroll 1
+                  for (int e = 0; e < 4; ++e) {
+                    const float v = e == 0 ? v0 : e == 1 ? v1 : e == 2 ? v2 : v3;
+                    if (e != jm && v < fminf(tv[TOPK - 1], tsh)) topk_insert(v, jb + 4 * g + e, tv, tj);
+                  }
+                }
               }
             }
           }
         }
-        tc_fence_before();
-        __syncwarp();  // every lane's TMEM reads are complete (tcgen05.wait::ld) before lane 0 releases
-        if (lane == 0) mbar_arrive(acc_empty + ab);
+#ifdef PS_TC_DIAG_CLOCKS
+        e_slow += clock64() - e_mark;
+#endif
         *(volatile float*)(sthr + part * BM + row) = tv[TOPK - 1];
         continue;
       }
@@ -608,6 +685,12 @@ __device__ __forceinline__ void nn_topk_tc_body(const uint8_t* __restrict__ Xt, 
       if (lane == 0) mbar_arrive(acc_empty + ab);
 #endif
     }
+#ifdef PS_TC_DIAG_CLOCKS
+    if (MODE == 0 && blockIdx.x == 7 && blockIdx.y == 0 && lane == 0 && (ew == 0 || ew == 5))
+      printf("[epilogue warp %d] wait acc_full %lld, ld + scan %lld cycles per tile (2-phase: ld %lld, ld + hot %lld, "
+             "wait-done to slow-done %lld, slow groups %lld per 100 tiles)\n", ew, e_wait / n_tiles,
+             e_work / max(n_tiles - 1, 1), e_ld / n_tiles, e_hot / n_tiles, e_slow / n_tiles, 100 * e_nslow / n_tiles);
+#endif
     if (MODE == 1) {
       unsigned long long* hb = hitbuf + ew * HITBUF;
       const int fill = hitcnt[ew];

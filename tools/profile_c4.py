@@ -18,4 +18,11 @@ for im in (a, b):
 for _ in range(int(sys.argv[1]) if len(sys.argv) > 1 else 2):
     r = device.match(ds[0], ds[1])
 torch.cuda.synchronize()
-print("matches", int(r[0].shape[0]))
+import time
+ts = []
+for _ in range(5):
+    t0 = time.perf_counter()
+    r = device.match(ds[0], ds[1])
+    torch.cuda.synchronize()
+    ts.append(time.perf_counter() - t0)
+print("matches", int(r[0].shape[0]), "C4 match ms", round(sorted(ts)[2] * 1e3, 3), device.match_stats())
