@@ -1626,20 +1626,29 @@ __device__ __forceinline__ void load8(const T* __restrict__ row, int hl, double 
 // first row, the smallest index with that key in the run, competes; equal
 // keys share a slot, so every slot still receives the smallest index of
 // its key) -- one row load per row instead of two.
+// The row key from the row's raw 32-bit words (no float <-> double conversions, one 32 x 32 -> 64
+// multiply-add per word and one avalanche per lane; with three 64-bit multiplies per element
+// b_hash was ALU-bound at 1.6 TB/s).  Any key function is exact here -- a collision only splits a
+// group (mark_reps compares the rows) -- so only its cost and spread matter.
 template <class T>
-__device__ __forceinline__ unsigned long long row_hash(const double (&xv)[8], int hl, unsigned hmask) {
+__device__ __forceinline__ unsigned long long row_hash_words(const T* __restrict__ row, int hl, unsigned hmask) {
+  constexpr int W = (int)sizeof(T) * 2;  // 32-bit words of this lane's 8 elements
+  const uint4* p = reinterpret_cast<const uint4*>(row) + hl * (W / 4);
   unsigned long long h = 0;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const T v = (T)xv[e];
-    unsigned long long bits;
-    if (sizeof(T) == 8) bits = (unsigned long long)__double_as_longlong((double)v);
-    else bits = (unsigned long long)__float_as_uint((float)v);
-    unsigned long long z = bits + 0x9E3779B97F4A7C15ull * (unsigned long long)(hl * 8 + e + 1);
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    h += z ^ (z >> 31);
+  for (int q = 0; q < W / 4; ++q) {
+    const uint4 w = __ldg(p + q);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t c = (0x9E3779B1u * (uint32_t)(hl * W + 4 * q + e + 1)) | 1u;  // per-position odd multiplier
+      const uint32_t x = ws[e] ^ __funnelshift_l(ws[e], ws[e], 15);
+      h += (unsigned long long)x * c + (unsigned long long)(x >> 7);
+    }
   }
+  h = (h ^ (h >> 30)) * 0xBF58476D1CE4E5B9ull;
+  h = (h ^ (h >> 27)) * 0x94D049BB133111EBull;
+  h ^= h >> 31;
 #pragma unroll
   for (int o = 8; o; o >>= 1) h += __shfl_xor_sync(hmask, h, o);
   return h | 1ull;  // 0 marks an empty slot
@@ -1676,11 +1685,7 @@ __global__ void b_hash(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
   const int64_t i0 = hw * run, i1 = min(n, i0 + run);
   if (i0 >= i1) return;  // uniform per half-warp
   unsigned long long prev = 0ull;  // key of row i0 - 1 (none: 0 never equals a key)
-  if (i0 > 0) {
-    double xv[8];
-    load8(X + (i0 - 1) * KD, hl, xv);
-    prev = row_hash<T>(xv, hl, hmask);
-  }
+  if (i0 > 0) prev = row_hash_words<T>(X + (i0 - 1) * KD, hl, hmask);
   // 16 rows' keys per round (lane k keeps row base + k's), then the 16 table
   // inserts run in parallel, one per lane
   const int hbase = threadIdx.x & 16;
@@ -1689,9 +1694,7 @@ __global__ void b_hash(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
     unsigned long long mine = 0ull;
 #pragma unroll 4
     for (int k = 0; k < m; ++k) {
-      double xv[8];
-      load8(X + (base + k) * KD, hl, xv);
-      const unsigned long long key = row_hash<T>(xv, hl, hmask);
+      const unsigned long long key = row_hash_words<T>(X + (base + k) * KD, hl, hmask);
       if (hl == k) mine = key;
     }
     unsigned long long before = __shfl_sync(hmask, mine, hbase + ((hl + 15) & 15));
