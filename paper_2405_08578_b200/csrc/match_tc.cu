@@ -1029,54 +1029,7 @@ __global__ void exact_rows(const int32_t* __restrict__ rows, const int32_t* __re
 // ---- duplicate rows --------------------------------------------------------------------
 // Open-addressing table of row hashes (tsize a power of two, keys 0 = empty):
 // per hash the lowest row index.  slot_of[i] receives row i's slot.
-template <class T>
-__device__ __forceinline__ void hash_insert_body(const T* __restrict__ X, int64_t n, unsigned long long* __restrict__ tkey,
-                            int32_t* __restrict__ tidx, int64_t tsize, int32_t* __restrict__ slot_of) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
-       i += (int64_t)gridDim.x * (blockDim.x >> 5)) {
-    unsigned long long h = 0;
-    bool same_as_prev = i > 0;  // a run of identical rows: only its first row competes for the minimum
-    double xv[4], pv[4];
-    load4(X + i * KD, lane, xv);
-    if (i > 0) load4(X + (i - 1) * KD, lane, pv);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const T v = (T)xv[e];
-      if (i > 0) same_as_prev &= xv[e] == pv[e];
-      unsigned long long bits;
-      if (sizeof(T) == 8) bits = (unsigned long long)__double_as_longlong((double)v);
-      else bits = (unsigned long long)__float_as_uint((float)v);
-      unsigned long long z = bits + 0x9E3779B97F4A7C15ull * (unsigned long long)(lane * 4 + e + 1);
-      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-      h += z ^ (z >> 31);
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
-    same_as_prev = __all_sync(0xffffffffu, same_as_prev);
-    if (lane == 0) {
-      const unsigned long long key = h | 1ull;
-      int64_t slot = (int64_t)((h >> 20) & (unsigned long long)(tsize - 1));
-      for (;;) {  // plain read first: duplicate rows find their slot without an atomic
-        unsigned long long prev = *(volatile unsigned long long*)(tkey + slot);
-        if (prev == 0ull) prev = atomicCAS(tkey + slot, 0ull, key);
-        if (prev == 0ull || prev == key) break;
-        slot = (slot + 1) & (tsize - 1);
-      }
-      // the run's first row (smaller index, same key) does it: thousands of
-      // identical flat-region rows would otherwise serialise on one address
-      if (!same_as_prev && *(volatile int32_t*)(tidx + slot) > (int32_t)i) atomicMin(tidx + slot, (int32_t)i);
-      slot_of[i] = (int32_t)slot;
-    }
-  }
-}
-template <class T>
-__global__ void hash_insert(const T* __restrict__ X, int64_t n, unsigned long long* __restrict__ tkey,
-                            int32_t* __restrict__ tidx, int64_t tsize, int32_t* __restrict__ slot_of) {
-  hash_insert_body<T>(X, n, tkey, tidx, tsize, slot_of);
-}
-
+// (hash_rows / b_hash below: a half-warp per row.)
 
 // rep[i] = the lowest row with row i's hash when bitwise equal to row i, else
 // i itself (a hash collision only splits a group); flag[i] = (rep == i).
@@ -1333,11 +1286,15 @@ int grid_for(int64_t work, int per) {
 }
 
 template <class T>
+__global__ void hash_rows(const T* __restrict__ X, int64_t n, unsigned long long* __restrict__ tkey,
+                          int32_t* __restrict__ tidx, int64_t tsize, int32_t* __restrict__ slot_of);  // below
+
+template <class T>
 int dedupe(const T* X, int64_t n, Side& s, const TcWs& w, cudaStream_t st) {
   cudaMemsetAsync(s.tkey, 0, s.tsize * sizeof(unsigned long long), st);
   cudaMemsetAsync(s.tidx, 0x7f, s.tsize * sizeof(int32_t), st);
-  hash_insert<T><<<grid_for(n, 8), 256, 0, st>>>(X, n, s.tkey, s.tidx, s.tsize, s.slot_of);
-  PS_LAUNCHED("hash_insert");
+  hash_rows<T><<<grid_for(n, 16), 256, 0, st>>>(X, n, s.tkey, s.tidx, s.tsize, s.slot_of);  // a half-warp per row
+  PS_LAUNCHED("hash_rows");
   mark_reps_table<T><<<grid_for(n, 8), 256, 0, st>>>(X, n, s.tidx, s.slot_of, s.rep, s.flag);
   PS_LAUNCHED("mark_reps_table");
   iota32<<<grid_for(n, 256), 256, 0, st>>>(s.iota, n);
@@ -1619,7 +1576,7 @@ __device__ __forceinline__ void load8(const T* __restrict__ row, int hl, double 
   }
 }
 
-// hash_insert with a half-warp per row (same hash: a sum over the elements).
+// The table inserts with a half-warp per row (the key: a sum over the row's words).
 // Each half-warp walks a contiguous run of rows two at a time, so "identical
 // to the previous row" is tested on the hash keys it already holds: a row
 // whose key equals its predecessor's skips the minimum update (the run's
@@ -1668,15 +1625,11 @@ __device__ __forceinline__ void hash_put(unsigned long long key, bool compete, i
   slot_of[i] = (int32_t)slot;
 }
 
+// Row keys into the open-addressing table, a half-warp per row (the grid's x dimension walks the rows)
 template <class T>
-__global__ void b_hash(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
-  const int64_t s = blockIdx.y;
-  if (!in.role[s]) return;
-  const T* X = in.desc[s];
-  const int64_t n = set_n(in, s), tsize = w.tsize;
-  unsigned long long* tkey = w.tkey + s * tsize;
-  int32_t* tidx = w.tidx + s * tsize;
-  int32_t* slot_of = w.slot_of + s * w.n;
+__device__ __forceinline__ void hash_rows_body(const T* __restrict__ X, int64_t n, unsigned long long* __restrict__ tkey,
+                                               int32_t* __restrict__ tidx, int64_t tsize,
+                                               int32_t* __restrict__ slot_of) {
   const int hl = threadIdx.x & 15;
   const unsigned hmask = (threadIdx.x & 16) ? 0xffff0000u : 0x0000ffffu;
   const int64_t halves = (int64_t)gridDim.x * (blockDim.x >> 4);
@@ -1702,6 +1655,20 @@ __global__ void b_hash(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
     if (hl < m) hash_put(mine, mine != before, base + hl, tkey, tidx, tsize, slot_of);
     prev = __shfl_sync(hmask, mine, hbase + m - 1);
   }
+}
+
+
+template <class T>
+__global__ void b_hash(const __grid_constant__ BatchIn<T> in, const BatchWs w) {
+  const int64_t s = blockIdx.y;
+  if (!in.role[s]) return;
+  hash_rows_body<T>(in.desc[s], set_n(in, s), w.tkey + s * w.tsize, w.tidx + s * w.tsize, w.tsize,
+                    w.slot_of + s * w.n);
+}
+template <class T>
+__global__ void hash_rows(const T* __restrict__ X, int64_t n, unsigned long long* __restrict__ tkey,
+                          int32_t* __restrict__ tidx, int64_t tsize, int32_t* __restrict__ slot_of) {
+  hash_rows_body<T>(X, n, tkey, tidx, tsize, slot_of);
 }
 
 template <class T>
