@@ -302,7 +302,9 @@ PS_API int ps_register_batch_async(int32_t n_pairs, const ps_register_pair* pair
  * out_model: device double[3] = (theta, t_x, t_y) of the refit, theta in
  * (-pi, pi].  out_mask: device uint8[n] final inlier mask.
  * out_info: device int64[4] = (status, consensus_size, n_inliers, best_iter)
- * with status PS_OK or PS_ERR_REGISTRATION.  out_rms: device double[1]. */
+ * with status PS_OK or PS_ERR_REGISTRATION; best_iter is -1 when the maximal
+ * consensus is below min_inliers (the call fails whatever the rms order, so
+ * no winner is selected: registration.py:187-190).  out_rms: device double[1]. */
 PS_API int ps_ransac_plan(int64_t n, int32_t iterations, size_t* workspace_bytes_out);
 PS_API int ps_ransac_rigid(const double* src_xy, const double* dst_xy, int64_t n,
                     const int32_t* samples, int32_t iterations, double inlier_tol,
