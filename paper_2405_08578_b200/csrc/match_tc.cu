@@ -810,7 +810,9 @@ __device__ __forceinline__ void certify_exact_body(const float* __restrict__ top
     }
     const double lim = (double)tv[0] + 2.0 * E;
     double cth = -INFINITY;  // column threshold: v of every column that can be closer than delta_s (ColCand)
-    if (cc.cbits) {
+    // once some row has declared the list incomplete the column pass will run, so later rows need not
+    // widen their candidate sets (a benign race: the list is simply not used then)
+    if (cc.cbits && *(volatile int32_t*)cc.incomplete == 0) {
       const double nxv = xinfo[3 * uu];
       const double c = cc.delta_s * cc.delta_s * (1.0 + 1e-9) - nxv * nxv + E + 1e-6;
       cth = (c == c) ? c : INFINITY;
