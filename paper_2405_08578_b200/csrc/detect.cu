@@ -45,6 +45,16 @@ struct KpOut {
   int64_t cap;
 };
 
+// The ramped value of pixel (r, c) whose 8-bit sample v the caller already holds in its key: the
+// same two operations as RampU8::at without the dependent pixel load (RGB8 needs the grey: at()).
+template <class Img>
+__device__ __forceinline__ double value_from_key(const Img& im, unsigned, int r, int c) { return im.at(r, c); }
+template <>
+__device__ __forceinline__ double value_from_key<RampU8>(const RampU8& im, unsigned v, int r, int c) {
+  const double k = u32_to_f64((unsigned)(r * im.nc + c + 1));
+  return __dadd_rn(u32_to_f64(v), __dmul_rn(k, im.alpha));
+}
+
 // ---- comparison helpers -----------------------------------------------------
 
 struct BestF64 {
@@ -632,12 +642,13 @@ __global__ void __launch_bounds__(32 * StripW<Img>::kWarps, StripW<Img>::kMinBlo
       if (out.row) {  // direct emission: slot 2w (max), 2w+1 (min)
         const int64_t sl = (int64_t)b * out.cap + 2 * (int64_t)w;
         const int32_t ks[2] = {kmax, kmin};
+        const unsigned vs[2] = {(unsigned)(bx >> 8), (unsigned)(bn >> 8)};
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int rr = ks[q] / nc, cc = ks[q] % nc;
           out.row[sl + q] = rr;
           out.col[sl + q] = cc;
-          out.value[sl + q] = im.at(rr, cc);
+          out.value[sl + q] = value_from_key(im, vs[q], rr, cc);
           if (out.scale) out.scale[sl + q] = scale_tag;
           if (out.pol) out.pol[sl + q] = (int8_t)q;
           if (out.window) out.window[sl + q] = w;
@@ -791,12 +802,13 @@ __global__ void __launch_bounds__(256, StripKeys<Img>::kMinBlocks16) detect_stri
       if (out.row) {  // direct emission: slot 2w (max), 2w+1 (min)
         const int64_t sl = (int64_t)b * out.cap + 2 * (int64_t)w;
         const int32_t ks[2] = {kmax, kmin};
+        const unsigned vs[2] = {(unsigned)(bx >> 16) & 0xffu, (unsigned)(bn >> 16) & 0xffu};  // u8: (v, r, c) keys
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int rr = ks[q] / nc, cc = ks[q] % nc;
           out.row[sl + q] = rr;
           out.col[sl + q] = cc;
-          out.value[sl + q] = im.at(rr, cc);
+          out.value[sl + q] = value_from_key(im, vs[q], rr, cc);
           if (out.scale) out.scale[sl + q] = scale_tag;
           if (out.pol) out.pol[sl + q] = (int8_t)q;
           if (out.window) out.window[sl + q] = w;
