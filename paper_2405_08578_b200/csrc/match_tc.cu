@@ -11,15 +11,23 @@
 //     (M=128, N=256, K=16) per tile into a double-buffered TMEM accumulator;
 //     four epilogue warps read it with tcgen05.ld (thread = row) and keep
 //     v = |y|^2 - 2 x.y with a fused running minimum; only when a tile holds a
-//     value below the row's current 4th best is it rescanned into a top-4 list.
+//     value below the row's current k-th best is it rescanned into a top-k list
+//     (k = PS_TC_TOPK = 3).
 //     The distance matrix never leaves TMEM.
 //  3. Certification: |v - (d^2 - |x|^2)| <= E_i, a rigorous bound from the
 //     fp16 rounding residual norms and fp32 accumulation, so the true first
 //     argmin is among the candidates with v <= v_min + 2 E_i; those are
 //     recomputed with the reference's exact float64 arithmetic.  Rows whose
-//     candidate set may exceed the top-4 are rescanned exactly in float64.
-//  4. Pass 2 repeats 2-3 for the columns that can be matched (nn12 of rows
-//     with d < delta_s) against all rows, giving the column argmin nn21.
+//     candidate set may exceed the list are enumerated on the tensor cores
+//     (MODE 1) and decided exactly in float64.
+//  4. The column argmin nn21: pass 1 keeps, per row, every column that can be
+//     closer than delta_s inside its certified candidate set, and the exact
+//     distances below delta_s it computes compete for their columns (ColCand
+//     below) -- for every column acceptance reads, that is the column argmin.
+//     Only when that list is incomplete (a row with more such columns than its
+//     list holds, rows left to the exact scan, a void certificate) pass 2
+//     repeats 2-3 for the columns that can be matched (nn12 of rows with
+//     d < delta_s) against all rows.
 #include <cub/cub.cuh>
 
 #include <algorithm>
